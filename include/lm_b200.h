@@ -1,0 +1,222 @@
+/* lm_b200.h -- C ABI of the B200-native local-mapping hot path (CreateNewMapPoints +
+ * SearchAndFuse of arXiv 2511.02036, reference package `localmap`).
+ *
+ * A context owns one CUDA device, one stream and a set of device-resident maps
+ * ("sessions"). Each map is a structure-of-arrays store of keyframes (poses, pinhole
+ * intrinsics, keypoints, 256-bit descriptors, per-keyframe cell grids), map points
+ * (positions, representative descriptors, observation lists, per-level counters) and a
+ * dense covisibility matrix. All buffers are allocated once at map creation.
+ *
+ * Conventions: plain C types, explicit sizes, no exceptions. Every function returns an
+ * lm_status; on failure lm_last_error(ctx) holds a message. Map point ids and keyframe
+ * ids are int64 like the reference's Python ints. Descriptors are 32 bytes per keypoint.
+ *
+ * Reference entry points each call replaces (paths under pkg/src/localmap/):
+ *   lm_kf_stage + lm_kf_insert   MapModel.insert_keyframe mapmodel.py:185-199 and
+ *                                DeviceStore.upload_keyframe devicestore.py:68-78
+ *   lm_create_map_points         create_map_points triangulation.py:195-300
+ *   lm_search                    search_for_triangulation triangulation.py:80-114
+ *   lm_run_fusion                run_fusion fusion.py:307-347
+ *   lm_fusion_targets            collect_fusion_targets fusion.py:38-54
+ *   lm_fuse_pass                 fuse_pass fusion.py:132-175
+ *   lm_apply_fusion              apply_fusion fusion.py:249-292
+ *   lm_cull_recent               cull_recent_map_points culling.py:28-59
+ *   lm_step / lm_step_batch      one pipeline iteration pipeline.py:152-195 (insert, recent
+ *                                cull, triangulation, fusion; LBA and keyframe culling are
+ *                                out of scope)
+ *   lm_mp_new / lm_obs_add / lm_obs_erase / lm_mp_kill / lm_mp_replace
+ *                                MapModel ops mapmodel.py:201-267
+ *   lm_covisible_neighbors       MapModel.covisible_neighbors mapmodel.py:269-273
+ *   lm_ledger                    TransferLedger.as_dict devicestore.py:32-48
+ */
+#ifndef LM_B200_H
+#define LM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum lm_status {
+  LM_OK = 0,
+  LM_ERR_INVALID_ARGUMENT = -1, /* InvalidArgumentError */
+  LM_ERR_INVALID_STATE = -2,    /* InvalidStateError */
+  LM_ERR_SLOT_CONFLICT = -3,    /* SlotConflictError */
+  LM_ERR_CAPACITY = -4,         /* StoreCapacityError */
+  LM_ERR_CUDA = -5,             /* CUDA runtime failure */
+  LM_ERR_DEGENERATE = -6        /* DegenerateGeometryError */
+} lm_status;
+
+typedef struct lm_ctx lm_ctx;
+
+typedef struct lm_map_caps {
+  int32_t max_keyframes;        /* keyframe slots (covisibility is dense max_keyframes^2 int32) */
+  int32_t max_keypoints;        /* keypoint pool over all keyframes */
+  int32_t max_keypoints_per_kf; /* upper bound of one keyframe's keypoint count */
+  int32_t max_points;           /* map point id space */
+  int32_t obs_pool_entries;     /* observation pool (8 bytes per entry) */
+  int32_t num_levels;           /* pyramid levels, <= 16 */
+  double scale_factor;          /* pyramid scale factor (> 1) */
+  int32_t min_covis_weight;     /* MapConfig.min_covis_weight */
+  int32_t min_obs_keep;         /* MapConfig.min_obs_keep */
+  /* StoreConfig ledger sizes */
+  int32_t keypoint_record_bytes, descriptor_bytes, map_point_record_bytes, store_capacity;
+} lm_map_caps;
+
+typedef struct lm_match_cfg { /* MatchConfig config.py:22-30 */
+  int32_t match_max_distance;
+  double chi2_epi;
+  int32_t level_window;
+} lm_match_cfg;
+
+typedef struct lm_gate_cfg { /* GateConfig config.py:13-19 */
+  double cos_parallax_max, chi2_mono, scale_ratio_slack;
+} lm_gate_cfg;
+
+typedef struct lm_fuse_cfg { /* FuseConfig config.py:33-44 */
+  int32_t match_max_distance;
+  double fuse_radius, min_view_cos, dist_band_slack;
+  int32_t level_window, n1, n2;
+} lm_fuse_cfg;
+
+typedef struct lm_cull_cfg { /* CullConfig config.py:63-72 (recent-point fields) */
+  double found_ratio_min;
+  int32_t probation_kfs, min_obs_graduate;
+} lm_cull_cfg;
+
+typedef struct lm_step_params {
+  int32_t neighbor_count;
+  int32_t do_cull, do_create, do_fuse; /* stage switches (1 = run) */
+  int32_t processed_index;             /* pipeline._processed before this keyframe */
+  lm_match_cfg match;
+  lm_gate_cfg gate;
+  lm_fuse_cfg fuse;
+  lm_cull_cfg cull;
+} lm_step_params;
+
+#define LM_MAX_NEIGHBORS 64
+#define LM_MAX_TARGETS 320
+
+typedef struct lm_step_stats { /* CreationStats triangulation.py:49-60 + run_fusion counts */
+  int32_t created, conflicts, degenerate;
+  int32_t gate_parallax, gate_depth, gate_reprojection, gate_scale;
+  int32_t n_degenerate_neighbors;
+  int64_t degenerate_neighbors[LM_MAX_NEIGHBORS];
+  int32_t n_neighbors;
+  int64_t neighbors[LM_MAX_NEIGHBORS];
+  int32_t n_targets;
+  int32_t merged, observations_added, stale;
+  int32_t culled;
+  int64_t first_new_id; /* created ids are first_new_id .. first_new_id+created-1 */
+  int32_t error;        /* nonzero: a device arena overflowed (lm_status code) */
+  int32_t pad;
+} lm_step_stats;
+
+typedef struct lm_candidate { /* MatchCandidate triangulation.py:41-46 */
+  int64_t neighbor_kf_id;
+  int32_t kp_index_current, kp_index_neighbor, distance, pad;
+} lm_candidate;
+
+#define LM_ACT_ADD 1
+#define LM_ACT_MERGE 2
+typedef struct lm_fuse_action { /* FuseAction fusion.py:29-35; existing_mp_id = -1 for None */
+  int64_t target_kf_id, mp_id_projected;
+  int32_t kp_index_hit, kind;
+  int64_t existing_mp_id;
+} lm_fuse_action;
+
+typedef struct lm_ledger_t { /* TransferLedger devicestore.py:25-48 */
+  int64_t persistent_bytes_up, naive_bytes_up;
+  int64_t small_bytes_triangulation, small_bytes_fusion, small_transfer_events, evictions;
+} lm_ledger_t;
+
+typedef struct lm_map_sizes {
+  int32_t n_kf_slots;  /* keyframe slots used (staged, live or dead) */
+  int32_t n_points;    /* map point ids issued (next id) */
+  int32_t n_keypoints; /* keypoint pool entries used */
+  int32_t obs_used;    /* observation pool entries used */
+  int32_t recent_n;    /* points under probation */
+} lm_map_sizes;
+
+/* ---- context / maps ---- */
+int lm_version(void);
+int lm_ctx_create(int32_t device, lm_ctx** out);
+int lm_ctx_destroy(lm_ctx* ctx);
+const char* lm_last_error(lm_ctx* ctx);
+int lm_map_create(lm_ctx* ctx, const lm_map_caps* caps, int32_t* map_out);
+int lm_map_reset(lm_ctx* ctx, int32_t map); /* back to an empty map, arenas kept */
+int lm_map_sizes_get(lm_ctx* ctx, int32_t map, lm_map_sizes* out);
+int lm_synchronize(lm_ctx* ctx);
+
+/* ---- keyframes ---- */
+/* Copy a keyframe into the map's pool without inserting it (not visible to any stage).
+ * quat = (x,y,z,w) canonical unit quaternion, trans = world->camera translation,
+ * cam = fx, fy, cx, cy, width, height. level: int64 per keypoint. bindings may be NULL
+ * (all unbound); otherwise ids of live map points to register at insert. */
+int lm_kf_stage(lm_ctx* ctx, int32_t map, int64_t kf_id, const double quat[4], const double trans[3],
+                const double cam[6], int32_t n, const double* u, const double* v, const int64_t* level,
+                const uint8_t* desc, const int64_t* bindings);
+/* Insert a staged keyframe into the map (insert_keyframe + upload_keyframe). */
+int lm_kf_insert(lm_ctx* ctx, int32_t map, int64_t kf_id);
+int lm_kf_kill(lm_ctx* ctx, int32_t map, int64_t kf_id); /* MapModel.kill_keyframe */
+
+/* ---- the hot path ---- */
+int lm_step(lm_ctx* ctx, int32_t map, int64_t kf_id, const lm_step_params* p, lm_step_stats* out);
+/* Enqueue one step for each (map, keyframe) pair in one batched launch sequence. If out is
+ * NULL the call does not synchronise (stats stay on the device until lm_step_stats_fetch). */
+int lm_step_batch(lm_ctx* ctx, int32_t n, const int32_t* maps, const int64_t* kf_ids, const lm_step_params* p,
+                  lm_step_stats* out);
+int lm_step_stats_fetch(lm_ctx* ctx, int32_t n, const int32_t* maps, lm_step_stats* out);
+int lm_create_map_points(lm_ctx* ctx, int32_t map, int64_t kf_id, int32_t neighbor_count,
+                         const lm_match_cfg* mc, const lm_gate_cfg* gc, lm_step_stats* out);
+int lm_run_fusion(lm_ctx* ctx, int32_t map, int64_t kf_id, const lm_fuse_cfg* fc, lm_step_stats* out);
+int lm_cull_recent(lm_ctx* ctx, int32_t map, int32_t processed_index, const lm_cull_cfg* cc, int32_t* culled);
+int lm_search(lm_ctx* ctx, int32_t map, int64_t cur_kf, int64_t nbr_kf, const lm_match_cfg* mc,
+              const uint8_t* unbound_cur, const uint8_t* unbound_nbr, lm_candidate* out, int32_t cap,
+              int32_t* n_out);
+int lm_fusion_targets(lm_ctx* ctx, int32_t map, int64_t kf_id, int32_t n1, int32_t n2, int64_t* out,
+                      int32_t cap, int32_t* n_out);
+int lm_fuse_pass(lm_ctx* ctx, int32_t map, const int64_t* point_ids, int32_t n, int64_t target_kf,
+                 const lm_fuse_cfg* fc, lm_fuse_action* acts, int32_t act_cap, int32_t* n_act,
+                 int64_t* visible, int32_t* n_vis);
+int lm_apply_fusion(lm_ctx* ctx, int32_t map, const lm_fuse_action* acts, int32_t n, int32_t counts[3]);
+
+/* ---- map bookkeeping (single-op kernels; the same device code the stages use) ---- */
+int lm_mp_new(lm_ctx* ctx, int32_t map, const double pos[3], const uint8_t desc[32], int64_t first_kf,
+              int64_t* id_out);
+int lm_obs_add(lm_ctx* ctx, int32_t map, int64_t mp, int64_t kf, int32_t kp);
+int lm_obs_erase(lm_ctx* ctx, int32_t map, int64_t mp, int64_t kf);
+int lm_mp_kill(lm_ctx* ctx, int32_t map, int64_t mp);
+int lm_mp_replace(lm_ctx* ctx, int32_t map, int64_t loser, int64_t winner, int32_t* migrated);
+int lm_mp_set_counts(lm_ctx* ctx, int32_t map, int64_t mp, int32_t found, int32_t visible);
+int lm_covisible_neighbors(lm_ctx* ctx, int32_t map, int64_t kf, int32_t n, int64_t* out, int32_t cap,
+                           int32_t* n_out);
+int lm_ledger(lm_ctx* ctx, int32_t map, lm_ledger_t* out);
+
+/* ---- state export (parity, snapshots) ---- */
+/* keyframe table: per slot kf_id, state (1 staged, 2 live, 3 dead), kp_off, kp_n */
+int lm_export_keyframes(lm_ctx* ctx, int32_t map, int64_t* kf_id, int32_t* state, int32_t* kp_off,
+                        int32_t* kp_n, int32_t cap, int32_t* n_out);
+int lm_export_bindings(lm_ctx* ctx, int32_t map, int32_t* bind, int32_t cap); /* whole keypoint pool */
+/* points 0..n-1: pos[3n], rep[32n], alive[n], found[n], visible[n], nobs[n], counts[n*L];
+ * observations flattened in id order (each point's list sorted by kf id): obs_kf[], obs_kp[]. */
+int lm_export_points(lm_ctx* ctx, int32_t map, int32_t n, double* pos, uint8_t* rep, uint8_t* alive,
+                     int32_t* found, int32_t* visible, int32_t* nobs, int32_t* counts, int64_t* obs_kf,
+                     int32_t* obs_kp, int32_t obs_cap);
+int lm_export_covis(lm_ctx* ctx, int32_t map, int32_t* w, int32_t cap); /* dense slot x slot */
+int lm_recent_export(lm_ctx* ctx, int32_t map, int64_t* ids, int32_t* born, int32_t cap, int32_t* n_out);
+int lm_recent_import(lm_ctx* ctx, int32_t map, const int64_t* ids, const int32_t* born, int32_t n);
+
+/* ---- host-side math, exported for CPU parity tests (no GPU needed) ---- */
+int lm_host_fundamental(const double qa[4], const double ta[3], const double qb[4], const double tb[3],
+                        const double cam_a[4], const double cam_b[4], double F[9]);
+int lm_host_projection(const double quat[4], const double trans[3], const double cam[4], double R[9],
+                       double C[3], double P[12]);
+int lm_host_triangulate(const double Pa[12], const double Pb[12], const double Ca[3], const double Cb[3],
+                        const double pix[4], double X[3]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LM_B200_H */

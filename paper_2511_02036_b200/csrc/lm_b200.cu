@@ -1,0 +1,1303 @@
+// lm_b200.cu -- C ABI of the B200 local-mapping hot path (see include/lm_b200.h).
+//
+// Host responsibilities only: arena allocation, keyframe staging (one pinned->device copy
+// and one scatter/grid kernel per keyframe), slot bookkeeping, kernel launches on the
+// context's stream, and exports. No hot-path arithmetic runs on the host: the per-keyframe
+// pose tables (R, C, P = K[R|t]) are computed here once at staging with the same
+// __host__ __device__ code the kernels use (lm_math.cuh).
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "lm_kernels.cuh"
+
+using namespace lm;
+
+namespace {
+
+constexpr int kRing = 64;       // step-argument ring entries
+constexpr int kMaxBatch = 128;  // maps per batched step
+constexpr int kStageRing = 4;   // keyframe staging buffers
+
+struct StageHdr {
+  int slot, n, kp_off, nx, ny;
+  double cs;
+  long long kf_id;
+  double q[4], R[9], t[3], C[3], P[12], cam[6];
+};
+
+struct HostMap {
+  DevMap d{};
+  lm_map_caps caps{};
+  std::unordered_map<long long, int> slot_of;
+  std::vector<int> state;  // host mirror of kf_state
+  std::vector<int> kp_n, kp_off;
+  std::vector<long long> ids;
+  int n_slots = 0, kp_head = 0, resident = 0;
+  std::vector<void*> allocs;
+  lm_step_stats* d_stats = nullptr;
+  lm_step_stats* d_totals = nullptr;
+  int* d_result = nullptr;  // single-op results
+};
+
+}  // namespace
+
+struct lm_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<HostMap*> maps;
+  DevMap* d_maps = nullptr;
+  int d_maps_cap = 0;
+  StepArgs* h_args = nullptr;  // pinned [kRing * kMaxBatch]
+  StepArgs* d_args = nullptr;
+  cudaEvent_t args_ev[kRing];
+  bool args_used[kRing];
+  int ring_pos = 0;
+  unsigned char* h_stage[kStageRing];
+  unsigned char* d_stage[kStageRing];
+  size_t stage_bytes = 0;
+  cudaEvent_t stage_ev[kStageRing];
+  bool stage_used[kStageRing];
+  int stage_pos = 0;
+  lm_step_stats* h_stats = nullptr;  // pinned [kMaxBatch]
+  std::string err;
+};
+
+static int fail(lm_ctx* ctx, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  return code;
+}
+
+#define CU(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess) return fail(ctx, LM_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define CHECK_LAUNCH() CU(cudaGetLastError())
+
+template <class T>
+static int arena(lm_ctx* ctx, HostMap* m, T** p, size_t count) {
+  void* q = nullptr;
+  CU(cudaMalloc(&q, count * sizeof(T) + 16));
+  CU(cudaMemsetAsync(q, 0, count * sizeof(T) + 16, ctx->stream));
+  m->allocs.push_back(q);
+  *p = (T*)q;
+  return LM_OK;
+}
+
+static int check_map(lm_ctx* ctx, int32_t map, HostMap** out) {
+  if (!ctx) return LM_ERR_INVALID_ARGUMENT;
+  if (map < 0 || map >= (int)ctx->maps.size() || !ctx->maps[map])
+    return fail(ctx, LM_ERR_INVALID_ARGUMENT, "unknown map %d", map);
+  *out = ctx->maps[map];
+  return LM_OK;
+}
+
+static int slot_of(lm_ctx* ctx, HostMap* m, long long kf_id, int* slot, bool need_live) {
+  auto it = m->slot_of.find(kf_id);
+  if (it == m->slot_of.end()) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "unknown keyframe %lld", kf_id);
+  *slot = it->second;
+  if (need_live && m->state[*slot] != KF_LIVE)
+    return fail(ctx, LM_ERR_INVALID_STATE, "keyframe %lld is not live", kf_id);
+  return LM_OK;
+}
+
+static int upload_maps(lm_ctx* ctx) {
+  const int n = (int)ctx->maps.size();
+  if (n > ctx->d_maps_cap) {
+    if (ctx->d_maps) CU(cudaFree(ctx->d_maps));
+    ctx->d_maps_cap = n < 16 ? 16 : 2 * n;
+    CU(cudaMalloc(&ctx->d_maps, sizeof(DevMap) * ctx->d_maps_cap));
+  }
+  std::vector<DevMap> h(n);
+  for (int i = 0; i < n; ++i) h[i] = ctx->maps[i]->d;
+  CU(cudaMemcpyAsync(ctx->d_maps, h.data(), sizeof(DevMap) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return LM_OK;
+}
+
+// scatter a staged keyframe into the arenas and build its cell grid
+__global__ void __launch_bounds__(1024) k_stage(DevMap M, const unsigned char* buf) {
+  const StageHdr* h = (const StageHdr*)buf;
+  const int n = h->n, off = h->kp_off, slot = h->slot;
+  const double* u = (const double*)(buf + sizeof(StageHdr));
+  const double* v = u + n;
+  const uint4* desc = (const uint4*)(v + n);
+  const int* bind = (const int*)(desc + 2 * n);
+  const unsigned char* lev = (const unsigned char*)(bind + n);
+  __shared__ int cnt[GRID_CELLS];
+  __shared__ int sh[32];
+  if (threadIdx.x == 0) {
+    M.kf_id[slot] = h->kf_id;
+    M.kp_off[slot] = off;
+    M.kp_n[slot] = n;
+    for (int k = 0; k < 4; ++k) M.q[4 * slot + k] = h->q[k];
+    for (int k = 0; k < 9; ++k) M.R[9 * slot + k] = h->R[k];
+    for (int k = 0; k < 3; ++k) M.t[3 * slot + k] = h->t[k];
+    for (int k = 0; k < 3; ++k) M.C[3 * slot + k] = h->C[k];
+    for (int k = 0; k < 12; ++k) M.P[12 * slot + k] = h->P[k];
+    for (int k = 0; k < 6; ++k) M.cam[6 * slot + k] = h->cam[k];
+    M.g_cs[slot] = h->cs;
+    M.g_nx[slot] = h->nx;
+    M.g_ny[slot] = h->ny;
+    M.kf_state[slot] = KF_STAGED;
+  }
+  const int nx = h->nx, ny = h->ny, nc = nx * ny;
+  const double cs = h->cs;
+  for (int c = threadIdx.x; c < nc; c += 1024) cnt[c] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += 1024) {
+    M.ku[off + i] = u[i];
+    M.kv[off + i] = v[i];
+    M.kdesc[2 * (off + i)] = desc[2 * i];
+    M.kdesc[2 * (off + i) + 1] = desc[2 * i + 1];
+    M.kbind[off + i] = bind[i];
+    M.klev[off + i] = lev[i];
+    const double fx = floor(u[i] / cs), fy = floor(v[i] / cs);
+    int cx = fx == fx ? (fx < 0 ? 0 : (fx > nx - 1 ? nx - 1 : (int)fx)) : 0;
+    int cy = fy == fy ? (fy < 0 ? 0 : (fy > ny - 1 ? ny - 1 : (int)fy)) : 0;
+    atomicAdd(&cnt[cy * nx + cx], 1);
+  }
+  __syncthreads();
+  // exclusive scan of cell counts (chunked block scan)
+  int* cst = M.cell_start + (size_t)slot * (GRID_CELLS + 1);
+  int run = 0;
+  for (int b0 = 0; b0 < nc; b0 += 1024) {
+    const int c = b0 + threadIdx.x;
+    const int x = c < nc ? cnt[c] : 0;
+    int tot;
+    const int at = block_excl_scan<1024>(x, sh, tot);
+    if (c < nc) {
+      cst[c] = run + at;
+      cnt[c] = run + at;  // cursor
+    }
+    run += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) cst[nc] = run;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += 1024) {
+    const double fx = floor(u[i] / cs), fy = floor(v[i] / cs);
+    int cx = fx == fx ? (fx < 0 ? 0 : (fx > nx - 1 ? nx - 1 : (int)fx)) : 0;
+    int cy = fy == fy ? (fy < 0 ? 0 : (fy > ny - 1 ? ny - 1 : (int)fy)) : 0;
+    const int at = atomicAdd(&cnt[cy * nx + cx], 1);
+    M.cell_items[off + at] = off + i;
+  }
+}
+
+// ------------------------------------------------------------------- single-op map kernel
+enum MapOp { OP_NEW = 1, OP_OBS_ADD, OP_OBS_ERASE, OP_KILL, OP_REPLACE, OP_SET_COUNTS, OP_KF_KILL, OP_NEIGHBORS,
+             OP_REFRESH, OP_APPLY, OP_TARGETS, OP_FUSE_PASS, OP_CULL };
+
+struct OpArgs {
+  int op;
+  int a, b, c;        // ids / slots / kp
+  int n;              // count
+  double pos[3];
+  unsigned char desc[32];
+  long long first_kf;
+  int found, visible;
+  lm_fuse_cfg fc;
+  lm_cull_cfg cc;
+  int processed;
+  int n_slots;
+};
+
+__global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, int* res) {
+  const DevMap& M = maps[map];
+  extern __shared__ int dyn[];
+  __shared__ int sh[32];
+  __shared__ int out_nb[1024];
+  const int tid = threadIdx.x;
+  switch (A.op) {
+    case OP_NEW: {
+      if (tid) return;
+      const int id = M.scal[SC_NEXT_ID];
+      if (id >= M.mp_cap) {
+        res[0] = LM_ERR_CAPACITY;
+        return;
+      }
+      M.scal[SC_NEXT_ID] = id + 1;
+      for (int k = 0; k < 3; ++k) M.pos[3 * id + k] = A.pos[k];
+      uint4 r[2];
+      memcpy(r, A.desc, 32);
+      M.rep[2 * id] = r[0];
+      M.rep[2 * id + 1] = r[1];
+      M.alive[id] = 1;
+      M.found[id] = 1;
+      M.visible[id] = 1;
+      M.first_kf[id] = A.first_kf;
+      M.nobs[id] = 0;
+      M.ocap[id] = 0;
+      M.ooff[id] = 0;
+      res[0] = LM_OK;
+      res[1] = id;
+      return;
+    }
+    case OP_OBS_ADD: {
+      if (tid) return;
+      const int mp = A.a, slot = A.b, kp = A.c;
+      if (mp < 0 || mp >= M.scal[SC_NEXT_ID]) { res[0] = LM_ERR_INVALID_ARGUMENT; return; }
+      if (!M.alive[mp]) { res[0] = LM_ERR_INVALID_STATE; return; }
+      if (kp < 0 || kp >= M.kp_n[slot]) { res[0] = LM_ERR_INVALID_ARGUMENT; return; }
+      if (M.kbind[M.kp_off[slot] + kp] >= 0) { res[0] = LM_ERR_SLOT_CONFLICT; res[1] = M.kbind[M.kp_off[slot] + kp]; return; }
+      if (obs_find(M, mp, slot) >= 0) { res[0] = LM_ERR_SLOT_CONFLICT; res[1] = -2; return; }
+      link(M, mp, slot, kp);
+      mark_dirty(M, mp);
+      res[0] = M.scal[SC_ERR] ? M.scal[SC_ERR] : LM_OK;
+      return;
+    }
+    case OP_OBS_ERASE: {
+      if (tid) return;
+      const int mp = A.a, slot = A.b;
+      if (mp < 0 || mp >= M.scal[SC_NEXT_ID]) { res[0] = LM_ERR_INVALID_ARGUMENT; return; }
+      if (!M.alive[mp]) { res[0] = LM_ERR_INVALID_STATE; return; }
+      const int k = obs_find(M, mp, slot);
+      if (k < 0) { res[0] = LM_ERR_INVALID_ARGUMENT; return; }
+      unlink_at(M, mp, k);
+      if (M.nobs[mp] < M.min_obs_keep) kill_point(M, mp);
+      else mark_dirty(M, mp);
+      res[0] = LM_OK;
+      return;
+    }
+    case OP_KILL: {
+      if (tid) return;
+      const int mp = A.a;
+      if (mp < 0 || mp >= M.scal[SC_NEXT_ID]) { res[0] = LM_ERR_INVALID_ARGUMENT; return; }
+      if (!M.alive[mp]) { res[0] = LM_ERR_INVALID_STATE; return; }
+      kill_point(M, mp);
+      res[0] = LM_OK;
+      return;
+    }
+    case OP_REPLACE: {
+      if (tid) return;
+      const int lo = A.a, wi = A.b;
+      if (lo == wi || lo < 0 || wi < 0 || lo >= M.scal[SC_NEXT_ID] || wi >= M.scal[SC_NEXT_ID]) {
+        res[0] = LM_ERR_INVALID_ARGUMENT;
+        return;
+      }
+      if (!M.alive[lo] || !M.alive[wi]) { res[0] = LM_ERR_INVALID_STATE; return; }
+      if (M.nobs[lo] > M.nobs[wi]) { res[0] = LM_ERR_INVALID_ARGUMENT; return; }
+      res[1] = replace_point(M, lo, wi);
+      res[0] = LM_OK;
+      return;
+    }
+    case OP_SET_COUNTS: {
+      if (tid) return;
+      M.found[A.a] = A.found;
+      M.visible[A.a] = A.visible;
+      res[0] = LM_OK;
+      return;
+    }
+    case OP_KF_KILL: {  // kill_keyframe mapmodel.py:275-283
+      if (tid) return;
+      const int slot = A.a;
+      const int off = M.kp_off[slot], n = M.kp_n[slot];
+      // sorted unique bound ids; erase each observation of this keyframe
+      for (;;) {
+        int lo = 0x7fffffff;
+        for (int i = 0; i < n; ++i) {
+          const int mp = M.kbind[off + i];
+          if (mp >= 0 && mp < lo) lo = mp;
+        }
+        if (lo == 0x7fffffff) break;
+        const int k = obs_find(M, lo, slot);
+        if (M.alive[lo] && k >= 0) {
+          unlink_at(M, lo, k);
+          if (M.nobs[lo] < M.min_obs_keep) kill_point(M, lo);
+          else mark_dirty(M, lo);
+        } else {
+          for (int i = 0; i < n; ++i)
+            if (M.kbind[off + i] == lo) M.kbind[off + i] = -1;
+        }
+      }
+      M.kf_state[slot] = KF_DEAD;
+      for (int s = 0; s < M.kf_cap; ++s) {
+        M.covis[(size_t)slot * M.kf_cap + s] = 0;
+        M.covis[(size_t)s * M.kf_cap + slot] = 0;
+      }
+      res[0] = LM_OK;
+      return;
+    }
+    case OP_NEIGHBORS: {
+      int* sh_slot = dyn;
+      int* sh_w = dyn + M.kf_cap;
+      const int got = ranked_neighbors<1024>(M, A.a, A.n, sh_slot, sh_w, out_nb, sh, A.n_slots);
+      for (int k = tid; k < got; k += 1024) res[2 + k] = out_nb[k];
+      if (tid == 0) {
+        res[0] = LM_OK;
+        res[1] = got;
+      }
+      return;
+    }
+    case OP_REFRESH: {
+      refresh_dirty<1024>(M);
+      if (tid == 0) res[0] = M.scal[SC_ERR];
+      return;
+    }
+    case OP_APPLY: {
+      if (tid) return;
+      int c[3] = {0, 0, 0};
+      apply_actions(M, M.s.acts, A.n, c);
+      res[0] = M.scal[SC_ERR];
+      res[1] = c[0];
+      res[2] = c[1];
+      res[3] = c[2];
+      return;
+    }
+    case OP_TARGETS: {
+      int* sh_slot = dyn;
+      int* sh_w = dyn + M.kf_cap;
+      const int T = fusion_targets<1024>(M, A.a, A.fc.n1, A.fc.n2, A.n_slots, sh_slot, sh_w, sh);
+      if (tid == 0) {
+        res[0] = LM_OK;
+        res[1] = T;
+      }
+      return;
+    }
+    case OP_FUSE_PASS: {
+      refresh_dirty<1024>(M);
+      int nvis = 0;
+      const int na = gather_pass<1024>(M, A.fc, A.n, A.a, false, sh, &nvis);
+      if (tid == 0) {
+        res[0] = M.scal[SC_ERR];
+        res[1] = na;
+        res[2] = nvis;
+      }
+      return;
+    }
+    default:
+      if (tid == 0) res[0] = LM_ERR_INVALID_ARGUMENT;
+  }
+}
+
+static int run_op(lm_ctx* ctx, HostMap* m, int map, OpArgs& a, int* res_host, int nres) {
+  a.n_slots = m->n_slots;
+  const size_t dyn = 2 * sizeof(int) * m->d.kf_cap;
+  k_op<<<1, 1024, dyn, ctx->stream>>>(ctx->d_maps, map, a, m->d_result);
+  CHECK_LAUNCH();
+  CU(cudaMemcpyAsync(res_host, m->d_result, sizeof(int) * nres, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return LM_OK;
+}
+
+static int op_status(lm_ctx* ctx, int code, const char* what) {
+  switch (code) {
+    case LM_OK: return LM_OK;
+    case LM_ERR_INVALID_ARGUMENT: return fail(ctx, code, "%s: invalid argument", what);
+    case LM_ERR_INVALID_STATE: return fail(ctx, code, "%s: entity is dead", what);
+    case LM_ERR_SLOT_CONFLICT: return fail(ctx, code, "%s: slot already bound", what);
+    case LM_ERR_CAPACITY: return fail(ctx, code, "%s: device arena capacity exceeded", what);
+    default: return fail(ctx, code, "%s: error %d", what, code);
+  }
+}
+
+// ------------------------------------------------------------------- ABI
+extern "C" {
+
+int lm_version(void) { return 1; }
+
+int lm_ctx_create(int32_t device, lm_ctx** out) {
+  if (!out) return LM_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  lm_ctx* ctx = new lm_ctx();
+  ctx->device = device;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || device < 0 || device >= ndev) {
+    *out = ctx;
+    return fail(ctx, LM_ERR_CUDA, "no CUDA device %d (%s)", device, cudaGetErrorString(e));
+  }
+  CU(cudaSetDevice(device));
+  CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  CU(cudaMallocHost(&ctx->h_args, sizeof(StepArgs) * kRing * kMaxBatch));
+  CU(cudaMalloc(&ctx->d_args, sizeof(StepArgs) * kRing * kMaxBatch));
+  CU(cudaMallocHost(&ctx->h_stats, sizeof(lm_step_stats) * kMaxBatch));
+  for (int i = 0; i < kRing; ++i) {
+    CU(cudaEventCreateWithFlags(&ctx->args_ev[i], cudaEventDisableTiming));
+    ctx->args_used[i] = false;
+  }
+  for (int i = 0; i < kStageRing; ++i) {
+    CU(cudaEventCreateWithFlags(&ctx->stage_ev[i], cudaEventDisableTiming));
+    ctx->stage_used[i] = false;
+    ctx->h_stage[i] = nullptr;
+    ctx->d_stage[i] = nullptr;
+  }
+  CU(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+  CU(cudaFuncSetAttribute(k_fuse, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+  CU(cudaFuncSetAttribute(k_op, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+  *out = ctx;
+  return LM_OK;
+}
+
+int lm_ctx_destroy(lm_ctx* ctx) {
+  if (!ctx) return LM_OK;
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (HostMap* m : ctx->maps) {
+    if (!m) continue;
+    for (void* p : m->allocs) cudaFree(p);
+    delete m;
+  }
+  if (ctx->d_maps) cudaFree(ctx->d_maps);
+  if (ctx->h_args) cudaFreeHost(ctx->h_args);
+  if (ctx->d_args) cudaFree(ctx->d_args);
+  if (ctx->h_stats) cudaFreeHost(ctx->h_stats);
+  for (int i = 0; i < kStageRing; ++i) {
+    if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
+    if (ctx->d_stage[i]) cudaFree(ctx->d_stage[i]);
+  }
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return LM_OK;
+}
+
+const char* lm_last_error(lm_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int lm_synchronize(lm_ctx* ctx) {
+  if (!ctx) return LM_ERR_INVALID_ARGUMENT;
+  CU(cudaStreamSynchronize(ctx->stream));
+  return LM_OK;
+}
+
+static double host_pow(double b, int e) { return pow(b, (double)e); }
+
+int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
+  if (!ctx || !c || !map_out) return LM_ERR_INVALID_ARGUMENT;
+  if (c->num_levels < 1 || c->num_levels > LMAX || !(c->scale_factor > 1.0) || c->max_keyframes < 2 ||
+      c->max_keypoints_per_kf < 1 || c->max_keypoints < c->max_keypoints_per_kf || c->max_points < 1 ||
+      c->obs_pool_entries < 8)
+    return fail(ctx, LM_ERR_INVALID_ARGUMENT, "invalid map capacities");
+  CU(cudaSetDevice(ctx->device));
+  HostMap* m = new HostMap();
+  m->caps = *c;
+  DevMap& d = m->d;
+  d.kf_cap = c->max_keyframes;
+  d.kp_cap = c->max_keypoints;
+  d.kpkf_max = c->max_keypoints_per_kf;
+  d.mp_cap = c->max_points;
+  d.obs_cap = c->obs_pool_entries;
+  d.L = c->num_levels;
+  d.min_w = c->min_covis_weight < 1 ? 1 : c->min_covis_weight;
+  d.min_obs_keep = c->min_obs_keep;
+  d.recent_cap = c->max_points;
+  d.kp_rec_bytes = c->keypoint_record_bytes;
+  d.desc_bytes = c->descriptor_bytes;
+  d.mp_rec_bytes = c->map_point_record_bytes;
+  d.sf = c->scale_factor;
+  d.log_sf = log(c->scale_factor);
+  for (int l = 0; l < LMAX; ++l) {
+    d.S[l] = host_pow(c->scale_factor, l);
+    d.S2[l] = host_pow(c->scale_factor, 2 * l);
+  }
+  const size_t K = d.kf_cap, KP = d.kp_cap, MP = d.mp_cap, NK = (size_t)NMAX * d.kpkf_max;
+  int rc = LM_OK;
+#define A(ptr, n) \
+  if ((rc = arena(ctx, m, &(ptr), (n))) != LM_OK) return rc
+  A(d.kf_id, K); A(d.kf_state, K); A(d.kp_off, K); A(d.kp_n, K);
+  A(d.q, 4 * K); A(d.R, 9 * K); A(d.t, 3 * K); A(d.C, 3 * K); A(d.P, 12 * K); A(d.cam, 6 * K);
+  A(d.g_cs, K); A(d.g_nx, K); A(d.g_ny, K);
+  A(d.cell_start, K * (GRID_CELLS + 1)); A(d.cell_items, KP);
+  A(d.ku, KP); A(d.kv, KP); A(d.klev, KP); A(d.kdesc, 2 * KP); A(d.kbind, KP);
+  A(d.pos, 3 * MP); A(d.rep, 2 * MP); A(d.alive, MP); A(d.found, MP); A(d.visible, MP); A(d.first_kf, MP);
+  A(d.nobs, MP); A(d.ocap, MP); A(d.ooff, MP); A(d.obs, (size_t)d.obs_cap); A(d.counts, MP * d.L);
+  A(d.dirty, MP); A(d.dirty_list, MP);
+  A(d.covis, K * K);
+  A(d.recent_id, MP); A(d.recent_born, MP);
+  A(d.scal, SC_N); A(d.ledger, LG_N);
+  Scratch& s = d.s;
+  A(s.nbr, NMAX); A(s.deg, NMAX); A(s.F, 9 * NMAX);
+  A(s.cur_sorted, d.kpkf_max); A(s.cur_bucket, LMAX + 1);
+  A(s.tiles, 3 * (d.kpkf_max / MATCH_TILE + LMAX + 1)); A(s.n_tiles, 1);
+  A(s.nb_n, NMAX); A(s.nb_bucket, NMAX * (LMAX + 1)); A(s.nb_j, NK); A(s.nb_desc, 2 * NK);
+  A(s.nb_u, NK); A(s.nb_v, NK); A(s.nb_thr, NK); A(s.pick, NK); A(s.bestj, NK);
+  A(s.cand_n, NMAX); A(s.cand_i, NK); A(s.cand_j, NK); A(s.cand_d, NK); A(s.cand_st, NK); A(s.cand_X, 3 * NK);
+  A(s.win_rank, d.kpkf_max); A(s.mask_cur, d.kpkf_max); A(s.mask_nbr, d.kpkf_max);
+  A(s.targets, TMAX); A(s.n_targets, 1); A(s.rank_buf, (size_t)TMAX * (2 * K + 1));
+  s.pts_cap = d.kpkf_max;
+  A(s.pts, s.pts_cap); A(s.geo, s.pts_cap);
+  s.act_cap = TMAX * d.kpkf_max;
+  A(s.acts, (size_t)s.act_cap); A(s.act_flag, (size_t)s.act_cap); A(s.vis_flag, (size_t)s.act_cap);
+  A(m->d_stats, 1); A(m->d_totals, 1); A(m->d_result, 4 + 1024 + TMAX);
+#undef A
+  s.stats = m->d_stats;
+  m->state.assign(K, KF_FREE);
+  m->kp_n.assign(K, 0);
+  m->kp_off.assign(K, 0);
+  m->ids.assign(K, 0);
+  ctx->maps.push_back(m);
+  *map_out = (int32_t)ctx->maps.size() - 1;
+  return upload_maps(ctx);
+}
+
+int lm_map_reset(lm_ctx* ctx, int32_t map) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  DevMap& d = m->d;
+  const size_t K = d.kf_cap, MP = d.mp_cap;
+  CU(cudaMemsetAsync(d.kf_state, 0, sizeof(int) * K, ctx->stream));
+  CU(cudaMemsetAsync(d.covis, 0, sizeof(int) * K * K, ctx->stream));
+  CU(cudaMemsetAsync(d.alive, 0, MP, ctx->stream));
+  CU(cudaMemsetAsync(d.nobs, 0, sizeof(int) * MP, ctx->stream));
+  CU(cudaMemsetAsync(d.ocap, 0, sizeof(int) * MP, ctx->stream));
+  CU(cudaMemsetAsync(d.counts, 0, sizeof(int) * MP * d.L, ctx->stream));
+  CU(cudaMemsetAsync(d.dirty, 0, sizeof(int) * MP, ctx->stream));
+  CU(cudaMemsetAsync(d.scal, 0, sizeof(int) * SC_N, ctx->stream));
+  CU(cudaMemsetAsync(d.ledger, 0, sizeof(unsigned long long) * LG_N, ctx->stream));
+  CU(cudaMemsetAsync(m->d_totals, 0, sizeof(lm_step_stats), ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  m->slot_of.clear();
+  std::fill(m->state.begin(), m->state.end(), KF_FREE);
+  m->n_slots = m->kp_head = m->resident = 0;
+  return LM_OK;
+}
+
+int lm_map_sizes_get(lm_ctx* ctx, int32_t map, lm_map_sizes* out) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  int sc[SC_N];
+  CU(cudaMemcpyAsync(sc, m->d.scal, sizeof sc, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  out->n_kf_slots = m->n_slots;
+  out->n_points = sc[SC_NEXT_ID];
+  out->n_keypoints = m->kp_head;
+  out->obs_used = sc[SC_OBS_HEAD];
+  out->recent_n = sc[SC_RECENT_N];
+  return LM_OK;
+}
+
+int lm_kf_stage(lm_ctx* ctx, int32_t map, int64_t kf_id, const double quat[4], const double trans[3],
+                const double cam[6], int32_t n, const double* u, const double* v, const int64_t* level,
+                const uint8_t* desc, const int64_t* bindings) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  DevMap& d = m->d;
+  if (m->slot_of.count(kf_id)) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "duplicate keyframe id %lld", (long long)kf_id);
+  if (n < 0 || n > d.kpkf_max)
+    return fail(ctx, LM_ERR_CAPACITY, "keyframe has %d keypoints, map limit %d", n, d.kpkf_max);
+  if (m->n_slots >= d.kf_cap) return fail(ctx, LM_ERR_CAPACITY, "keyframe slots exhausted (%d)", d.kf_cap);
+  if (m->kp_head + n > d.kp_cap) return fail(ctx, LM_ERR_CAPACITY, "keypoint pool exhausted (%d)", d.kp_cap);
+  if (!(cam[0] > 0 && cam[1] > 0 && cam[4] > 0 && cam[5] > 0))
+    return fail(ctx, LM_ERR_INVALID_ARGUMENT, "bad intrinsics");
+  for (int i = 0; i < n; ++i)
+    if (level[i] < 0 || level[i] >= d.L) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "keypoint level outside pyramid");
+  // staging buffer (ring)
+  const size_t need = sizeof(StageHdr) + (size_t)n * (8 + 8 + 32 + 4 + 1) + 64;
+  const int b = ctx->stage_pos++ % kStageRing;
+  if (ctx->stage_used[b]) CU(cudaEventSynchronize(ctx->stage_ev[b]));
+  if (ctx->stage_bytes < need) {
+    const size_t sz = need < ((size_t)d.kpkf_max * 53 + sizeof(StageHdr) + 64) ? ((size_t)d.kpkf_max * 53 + sizeof(StageHdr) + 64) : need;
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < kStageRing; ++i) {
+      if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
+      if (ctx->d_stage[i]) cudaFree(ctx->d_stage[i]);
+      CU(cudaMallocHost(&ctx->h_stage[i], sz));
+      CU(cudaMalloc(&ctx->d_stage[i], sz));
+      ctx->stage_used[i] = false;
+    }
+    ctx->stage_bytes = sz;
+  }
+  unsigned char* hb = ctx->h_stage[b];
+  StageHdr* h = (StageHdr*)hb;
+  const int slot = m->n_slots;
+  h->slot = slot;
+  h->n = n;
+  h->kp_off = m->kp_head;
+  h->kf_id = kf_id;
+  for (int k = 0; k < 4; ++k) h->q[k] = quat[k];
+  for (int k = 0; k < 3; ++k) h->t[k] = trans[k];
+  for (int k = 0; k < 6; ++k) h->cam[k] = cam[k];
+  quat_to_rot(h->q, h->R);
+  camera_center(h->R, h->t, h->C);
+  proj_matrix(cam[0], cam[1], cam[2], cam[3], h->R, h->t, h->P);
+  const double big = cam[4] > cam[5] ? cam[4] : cam[5];
+  double cs = 16.0;
+  while (ceil(cam[4] / cs) * ceil(cam[5] / cs) > GRID_CELLS) cs *= 2.0;
+  (void)big;
+  h->cs = cs;
+  h->nx = (int)ceil(cam[4] / cs);
+  h->ny = (int)ceil(cam[5] / cs);
+  double* pu = (double*)(hb + sizeof(StageHdr));
+  double* pv = pu + n;
+  unsigned char* pd = (unsigned char*)(pv + n);
+  int* pb = (int*)(pd + 32 * (size_t)n);
+  unsigned char* pl = (unsigned char*)(pb + n);
+  memcpy(pu, u, sizeof(double) * n);
+  memcpy(pv, v, sizeof(double) * n);
+  memcpy(pd, desc, 32 * (size_t)n);
+  for (int i = 0; i < n; ++i) {
+    pb[i] = bindings ? (int)bindings[i] : -1;
+    pl[i] = (unsigned char)level[i];
+  }
+  CU(cudaMemcpyAsync(ctx->d_stage[b], hb, need, cudaMemcpyHostToDevice, ctx->stream));
+  k_stage<<<1, 1024, 0, ctx->stream>>>(d, ctx->d_stage[b]);
+  CHECK_LAUNCH();
+  CU(cudaEventRecord(ctx->stage_ev[b], ctx->stream));
+  ctx->stage_used[b] = true;
+  m->slot_of[kf_id] = slot;
+  m->state[slot] = KF_STAGED;
+  m->kp_n[slot] = n;
+  m->kp_off[slot] = m->kp_head;
+  m->ids[slot] = kf_id;
+  m->n_slots++;
+  m->kp_head += n;
+  return LM_OK;
+}
+
+// ------------------------------------------------------------------- steps
+__global__ void k_begin(DevMap* maps, const StepArgs* args) {
+  const DevMap& M = maps[args[blockIdx.x].map];
+  int* p = (int*)M.s.stats;
+  for (int k = threadIdx.x; k < (int)(sizeof(lm_step_stats) / 4); k += blockDim.x) p[k] = 0;
+}
+
+__global__ void k_end(DevMap* maps, const StepArgs* args) {
+  const DevMap& M = maps[args[blockIdx.x].map];
+  if (threadIdx.x == 0) M.s.stats->error = M.scal[SC_ERR];
+}
+
+static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args) {
+  if (n < 1 || n > kMaxBatch) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "batch of %d maps", n);
+  const int e = ctx->ring_pos++ % kRing;
+  if (ctx->args_used[e]) CU(cudaEventSynchronize(ctx->args_ev[e]));
+  StepArgs* h = ctx->h_args + (size_t)e * kMaxBatch;
+  StepArgs* dv = ctx->d_args + (size_t)e * kMaxBatch;
+  int tiles = 1, slots = 1, kfcap = 2;
+  for (int k = 0; k < n; ++k) {
+    HostMap* m = ctx->maps[maps[k]];
+    h[k] = args[k];
+    h[k].map = maps[k];
+    const int t = m->d.kpkf_max / MATCH_TILE + m->d.L + 1;
+    tiles = t > tiles ? t : tiles;
+    slots = m->n_slots > slots ? m->n_slots : slots;
+    kfcap = m->d.kf_cap > kfcap ? m->d.kf_cap : kfcap;
+  }
+  DevMap* dmaps = ctx->d_maps;
+  CU(cudaMemcpyAsync(dv, h, sizeof(StepArgs) * n, cudaMemcpyHostToDevice, ctx->stream));
+  const size_t dyn = 2 * sizeof(int) * kfcap;
+  k_begin<<<n, 128, 0, ctx->stream>>>(dmaps, dv);
+  k_insert<<<n, 1, 0, ctx->stream>>>(dmaps, dv);
+  k_cull<<<n, 1024, 0, ctx->stream>>>(dmaps, dv);
+  k_select<<<n, 256, dyn, ctx->stream>>>(dmaps, dv, slots);
+  k_prep<<<dim3(1 + NMAX, n), 256, 0, ctx->stream>>>(dmaps, dv);
+  k_match<<<dim3(tiles, NMAX, n), MATCH_TILE, 0, ctx->stream>>>(dmaps, dv);
+  k_tri<<<dim3(NMAX, n), 256, 0, ctx->stream>>>(dmaps, dv);
+  k_commit<<<n, 1024, 0, ctx->stream>>>(dmaps, dv);
+  k_fuse<<<n, 1024, dyn, ctx->stream>>>(dmaps, dv, slots);
+  k_end<<<n, 32, 0, ctx->stream>>>(dmaps, dv);
+  CHECK_LAUNCH();
+  CU(cudaEventRecord(ctx->args_ev[e], ctx->stream));
+  ctx->args_used[e] = true;
+  return LM_OK;
+}
+
+static int fill_args(lm_ctx* ctx, HostMap* m, int64_t kf_id, const lm_step_params* p, StepArgs& a, bool insert) {
+  int slot;
+  int rc = slot_of(ctx, m, kf_id, &slot, false);
+  if (rc) return rc;
+  memset(&a, 0, sizeof a);
+  a.cur = slot;
+  a.do_insert = 0;
+  if (m->state[slot] == KF_STAGED) {
+    if (!insert) return fail(ctx, LM_ERR_INVALID_STATE, "keyframe %lld is staged, not inserted", (long long)kf_id);
+    if (m->resident >= m->caps.store_capacity && m->caps.store_capacity > 0)
+      return fail(ctx, LM_ERR_CAPACITY, "store capacity %d exceeded; size the pre-allocation", m->caps.store_capacity);
+    a.do_insert = 1;
+  } else if (m->state[slot] != KF_LIVE) {
+    return fail(ctx, LM_ERR_INVALID_STATE, "keyframe %lld is dead", (long long)kf_id);
+  }
+  if (p) {
+    a.n_nbr_req = p->neighbor_count;
+    a.do_cull = p->do_cull;
+    a.do_create = p->do_create;
+    a.do_fuse = p->do_fuse;
+    a.processed = p->processed_index;
+    a.mc = p->match;
+    a.gc = p->gate;
+    a.fc = p->fuse;
+    a.cc = p->cull;
+  }
+  if (a.n_nbr_req > NMAX) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "neighbor_count > %d", NMAX);
+  if (a.do_fuse && a.fc.n1 + a.fc.n1 * a.fc.n2 > TMAX)
+    return fail(ctx, LM_ERR_INVALID_ARGUMENT, "n1 + n1*n2 > %d", TMAX);
+  return LM_OK;
+}
+
+static void after_insert(HostMap* m, const StepArgs& a) {
+  if (a.do_insert) {
+    m->state[a.cur] = KF_LIVE;
+    m->resident++;
+  }
+}
+
+static int run_batch(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args, lm_step_stats* out) {
+  int rc = launch_steps(ctx, n, maps, args);
+  if (rc) return rc;
+  CHECK_LAUNCH();
+  for (int k = 0; k < n; ++k) after_insert(ctx->maps[maps[k]], args[k]);
+  if (!out) return LM_OK;
+  for (int k = 0; k < n; ++k)
+    CU(cudaMemcpyAsync(ctx->h_stats + k, ctx->maps[maps[k]]->d_stats, sizeof(lm_step_stats), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  memcpy(out, ctx->h_stats, sizeof(lm_step_stats) * n);
+  for (int k = 0; k < n; ++k)
+    if (out[k].error) return fail(ctx, out[k].error, "device arena overflow or invalid pre-bound slot in map %d", maps[k]);
+  return LM_OK;
+}
+
+int lm_step(lm_ctx* ctx, int32_t map, int64_t kf_id, const lm_step_params* p, lm_step_stats* out) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  StepArgs a;
+  rc = fill_args(ctx, m, kf_id, p, a, true);
+  if (rc) return rc;
+  return run_batch(ctx, 1, &map, &a, out);
+}
+
+int lm_step_batch(lm_ctx* ctx, int32_t n, const int32_t* maps, const int64_t* kf_ids, const lm_step_params* p,
+                  lm_step_stats* out) {
+  if (!ctx || n < 1 || n > kMaxBatch) return LM_ERR_INVALID_ARGUMENT;
+  std::vector<StepArgs> args(n);
+  for (int k = 0; k < n; ++k) {
+    HostMap* m;
+    int rc = check_map(ctx, maps[k], &m);
+    if (rc) return rc;
+    rc = fill_args(ctx, m, kf_ids[k], p, args[k], true);
+    if (rc) return rc;
+  }
+  return run_batch(ctx, n, maps, args.data(), out);
+}
+
+int lm_step_stats_fetch(lm_ctx* ctx, int32_t n, const int32_t* maps, lm_step_stats* out) {
+  for (int k = 0; k < n; ++k) {
+    HostMap* m;
+    int rc = check_map(ctx, maps[k], &m);
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(out + k, m->d_stats, sizeof(lm_step_stats), cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CU(cudaStreamSynchronize(ctx->stream));
+  return LM_OK;
+}
+
+static int single_stage(lm_ctx* ctx, int32_t map, int64_t kf_id, lm_step_params& p, lm_step_stats* out) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  int slot;
+  rc = slot_of(ctx, m, kf_id, &slot, true);
+  if (rc) return rc;
+  lm_step_stats tmp;
+  return lm_step(ctx, map, kf_id, &p, out ? out : &tmp);
+}
+
+int lm_kf_insert(lm_ctx* ctx, int32_t map, int64_t kf_id) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  int slot;
+  rc = slot_of(ctx, m, kf_id, &slot, false);
+  if (rc) return rc;
+  if (m->state[slot] != KF_STAGED) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "duplicate keyframe id %lld", (long long)kf_id);
+  lm_step_params p;
+  memset(&p, 0, sizeof p);
+  lm_step_stats st;
+  return lm_step(ctx, map, kf_id, &p, &st);
+}
+
+int lm_create_map_points(lm_ctx* ctx, int32_t map, int64_t kf_id, int32_t neighbor_count, const lm_match_cfg* mc,
+                         const lm_gate_cfg* gc, lm_step_stats* out) {
+  if (!mc || !gc) return LM_ERR_INVALID_ARGUMENT;
+  lm_step_params p;
+  memset(&p, 0, sizeof p);
+  p.neighbor_count = neighbor_count;
+  p.do_create = neighbor_count > 0;
+  p.match = *mc;
+  p.gate = *gc;
+  return single_stage(ctx, map, kf_id, p, out);
+}
+
+int lm_run_fusion(lm_ctx* ctx, int32_t map, int64_t kf_id, const lm_fuse_cfg* fc, lm_step_stats* out) {
+  if (!fc) return LM_ERR_INVALID_ARGUMENT;
+  lm_step_params p;
+  memset(&p, 0, sizeof p);
+  p.do_fuse = 1;
+  p.fuse = *fc;
+  return single_stage(ctx, map, kf_id, p, out);
+}
+
+int lm_cull_recent(lm_ctx* ctx, int32_t map, int32_t processed_index, const lm_cull_cfg* cc, int32_t* culled) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  // any live keyframe works as the step anchor; the cull stage does not read it
+  int anchor = -1;
+  for (int s = 0; s < m->n_slots; ++s)
+    if (m->state[s] == KF_LIVE) {
+      anchor = s;
+      break;
+    }
+  if (anchor < 0) {
+    if (culled) *culled = 0;
+    return LM_OK;
+  }
+  lm_step_params p;
+  memset(&p, 0, sizeof p);
+  p.do_cull = 1;
+  p.processed_index = processed_index;
+  p.cull = *cc;
+  lm_step_stats st;
+  rc = lm_step(ctx, map, m->ids[anchor], &p, &st);
+  if (culled) *culled = st.culled;
+  return rc;
+}
+
+int lm_search(lm_ctx* ctx, int32_t map, int64_t cur_kf, int64_t nbr_kf, const lm_match_cfg* mc,
+              const uint8_t* unbound_cur, const uint8_t* unbound_nbr, lm_candidate* out, int32_t cap, int32_t* n_out) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  int cs, ns;
+  if ((rc = slot_of(ctx, m, cur_kf, &cs, false)) || (rc = slot_of(ctx, m, nbr_kf, &ns, false))) return rc;
+  if (m->state[cs] == KF_FREE || m->state[ns] == KF_FREE) return fail(ctx, LM_ERR_INVALID_STATE, "keyframe not staged");
+  StepArgs a;
+  memset(&a, 0, sizeof a);
+  a.cur = cs;
+  a.do_create = 1;
+  a.explicit_nbr = 1;
+  a.nbr0 = ns;
+  a.search_only = 1;
+  a.mc = *mc;
+  a.n_nbr_req = 1;
+  if (unbound_cur) {
+    CU(cudaMemcpyAsync(m->d.s.mask_cur, unbound_cur, m->kp_n[cs], cudaMemcpyHostToDevice, ctx->stream));
+    a.use_mask_cur = 1;
+  }
+  if (unbound_nbr) {
+    CU(cudaMemcpyAsync(m->d.s.mask_nbr, unbound_nbr, m->kp_n[ns], cudaMemcpyHostToDevice, ctx->stream));
+    a.use_mask_nbr = 1;
+  }
+  rc = launch_steps(ctx, 1, &map, &a);
+  if (rc) return rc;
+  int cnt = 0;
+  CU(cudaMemcpyAsync(&cnt, m->d.s.cand_n, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  *n_out = cnt;
+  if (cnt > cap) return fail(ctx, LM_ERR_CAPACITY, "candidate buffer too small (%d > %d)", cnt, cap);
+  std::vector<int> ci(cnt), cj(cnt), cd(cnt);
+  if (cnt) {
+    CU(cudaMemcpyAsync(ci.data(), m->d.s.cand_i, sizeof(int) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(cj.data(), m->d.s.cand_j, sizeof(int) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(cd.data(), m->d.s.cand_d, sizeof(int) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
+  for (int k = 0; k < cnt; ++k) {
+    out[k].neighbor_kf_id = nbr_kf;
+    out[k].kp_index_current = ci[k];
+    out[k].kp_index_neighbor = cj[k];
+    out[k].distance = cd[k];
+    out[k].pad = 0;
+  }
+  return LM_OK;
+}
+
+int lm_fusion_targets(lm_ctx* ctx, int32_t map, int64_t kf_id, int32_t n1, int32_t n2, int64_t* out, int32_t cap,
+                      int32_t* n_out) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  int slot;
+  if ((rc = slot_of(ctx, m, kf_id, &slot, true))) return rc;
+  if (n1 + n1 * n2 > TMAX) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "n1 + n1*n2 > %d", TMAX);
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_TARGETS;
+  a.a = slot;
+  a.fc.n1 = n1;
+  a.fc.n2 = n2;
+  int res[2];
+  if ((rc = run_op(ctx, m, map, a, res, 2))) return rc;
+  const int T = res[1];
+  *n_out = T;
+  if (T > cap) return fail(ctx, LM_ERR_CAPACITY, "target buffer too small");
+  std::vector<int> t(T);
+  if (T) CU(cudaMemcpy(t.data(), m->d.s.targets, sizeof(int) * T, cudaMemcpyDeviceToHost));
+  for (int k = 0; k < T; ++k) out[k] = m->ids[t[k]];
+  return LM_OK;
+}
+
+int lm_fuse_pass(lm_ctx* ctx, int32_t map, const int64_t* point_ids, int32_t n, int64_t target_kf,
+                 const lm_fuse_cfg* fc, lm_fuse_action* acts, int32_t act_cap, int32_t* n_act, int64_t* visible,
+                 int32_t* n_vis) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  int slot;
+  if ((rc = slot_of(ctx, m, target_kf, &slot, true))) return rc;
+  if (n > m->d.s.pts_cap) return fail(ctx, LM_ERR_CAPACITY, "too many points for one pass (%d)", n);
+  *n_act = 0;
+  *n_vis = 0;
+  if (n == 0) return LM_OK;
+  std::vector<int> ids(n);
+  for (int k = 0; k < n; ++k) ids[k] = (int)point_ids[k];
+  CU(cudaMemcpyAsync(m->d.s.pts, ids.data(), sizeof(int) * n, cudaMemcpyHostToDevice, ctx->stream));
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_FUSE_PASS;
+  a.a = slot;
+  a.n = n;
+  a.fc = *fc;
+  int res[3];
+  if ((rc = run_op(ctx, m, map, a, res, 3))) return rc;
+  if (res[0]) return op_status(ctx, res[0], "fuse_pass");
+  const int na = res[1];
+  if (na > act_cap) return fail(ctx, LM_ERR_CAPACITY, "action buffer too small");
+  std::vector<ActRec> ar(na);
+  std::vector<int> vf(n);
+  if (na) CU(cudaMemcpy(ar.data(), m->d.s.acts, sizeof(ActRec) * na, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(vf.data(), m->d.s.vis_flag, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  for (int k = 0; k < na; ++k) {
+    acts[k].target_kf_id = m->ids[ar[k].slot];
+    acts[k].mp_id_projected = ar[k].pid;
+    acts[k].kp_index_hit = ar[k].j;
+    acts[k].kind = ar[k].kind;
+    acts[k].existing_mp_id = ar[k].other;
+  }
+  int nv = 0;
+  for (int k = 0; k < n; ++k)
+    if (vf[k]) visible[nv++] = point_ids[k];
+  *n_act = na;
+  *n_vis = nv;
+  return LM_OK;
+}
+
+int lm_apply_fusion(lm_ctx* ctx, int32_t map, const lm_fuse_action* acts, int32_t n, int32_t counts[3]) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  counts[0] = counts[1] = counts[2] = 0;
+  if (n == 0) return LM_OK;
+  if (n > m->d.s.act_cap) return fail(ctx, LM_ERR_CAPACITY, "too many actions");
+  std::vector<ActRec> ar(n);
+  for (int k = 0; k < n; ++k) {
+    auto it = m->slot_of.find(acts[k].target_kf_id);
+    ar[k].slot = it == m->slot_of.end() ? -1 : it->second;
+    ar[k].pid = (int)acts[k].mp_id_projected;
+    ar[k].j = acts[k].kp_index_hit;
+    ar[k].other = (int)acts[k].existing_mp_id;
+    ar[k].kind = acts[k].kind;
+    if (ar[k].slot < 0 || ar[k].pid < 0) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "action refers to unknown entity");
+  }
+  CU(cudaMemcpyAsync(m->d.s.acts, ar.data(), sizeof(ActRec) * n, cudaMemcpyHostToDevice, ctx->stream));
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_APPLY;
+  a.n = n;
+  int res[4];
+  if ((rc = run_op(ctx, m, map, a, res, 4))) return rc;
+  if (res[0]) return op_status(ctx, res[0], "apply_fusion");
+  counts[0] = res[1];
+  counts[1] = res[2];
+  counts[2] = res[3];
+  return LM_OK;
+}
+
+int lm_mp_new(lm_ctx* ctx, int32_t map, const double pos[3], const uint8_t desc[32], int64_t first_kf,
+              int64_t* id_out) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_NEW;
+  for (int k = 0; k < 3; ++k) a.pos[k] = pos[k];
+  memcpy(a.desc, desc, 32);
+  a.first_kf = first_kf;
+  int res[2];
+  if ((rc = run_op(ctx, m, map, a, res, 2))) return rc;
+  if (res[0]) return op_status(ctx, res[0], "new_map_point");
+  *id_out = res[1];
+  return LM_OK;
+}
+
+int lm_obs_add(lm_ctx* ctx, int32_t map, int64_t mp, int64_t kf, int32_t kp) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  int slot;
+  if ((rc = slot_of(ctx, m, kf, &slot, true))) return rc;
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_OBS_ADD;
+  a.a = (int)mp;
+  a.b = slot;
+  a.c = kp;
+  int res[2];
+  if ((rc = run_op(ctx, m, map, a, res, 2))) return rc;
+  return op_status(ctx, res[0], "add_observation");
+}
+
+int lm_obs_erase(lm_ctx* ctx, int32_t map, int64_t mp, int64_t kf) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  int slot;
+  if ((rc = slot_of(ctx, m, kf, &slot, false))) return rc;
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_OBS_ERASE;
+  a.a = (int)mp;
+  a.b = slot;
+  int res[1];
+  if ((rc = run_op(ctx, m, map, a, res, 1))) return rc;
+  return op_status(ctx, res[0], "erase_observation");
+}
+
+int lm_mp_kill(lm_ctx* ctx, int32_t map, int64_t mp) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_KILL;
+  a.a = (int)mp;
+  int res[1];
+  if ((rc = run_op(ctx, m, map, a, res, 1))) return rc;
+  return op_status(ctx, res[0], "kill_map_point");
+}
+
+int lm_mp_replace(lm_ctx* ctx, int32_t map, int64_t loser, int64_t winner, int32_t* migrated) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_REPLACE;
+  a.a = (int)loser;
+  a.b = (int)winner;
+  int res[2];
+  if ((rc = run_op(ctx, m, map, a, res, 2))) return rc;
+  if (res[0]) return op_status(ctx, res[0], "replace_map_point");
+  if (migrated) *migrated = res[1];
+  return LM_OK;
+}
+
+int lm_mp_set_counts(lm_ctx* ctx, int32_t map, int64_t mp, int32_t found, int32_t visible) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_SET_COUNTS;
+  a.a = (int)mp;
+  a.found = found;
+  a.visible = visible;
+  int res[1];
+  return run_op(ctx, m, map, a, res, 1);
+}
+
+int lm_kf_kill(lm_ctx* ctx, int32_t map, int64_t kf_id) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  int slot;
+  if ((rc = slot_of(ctx, m, kf_id, &slot, true))) return rc;
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_KF_KILL;
+  a.a = slot;
+  int res[1];
+  if ((rc = run_op(ctx, m, map, a, res, 1))) return rc;
+  m->state[slot] = KF_DEAD;
+  return op_status(ctx, res[0], "kill_keyframe");
+}
+
+int lm_covisible_neighbors(lm_ctx* ctx, int32_t map, int64_t kf, int32_t n, int64_t* out, int32_t cap,
+                           int32_t* n_out) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  int slot;
+  if ((rc = slot_of(ctx, m, kf, &slot, true))) return rc;
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_NEIGHBORS;
+  a.a = slot;
+  a.n = n < 0 ? 1024 : (n > 1024 ? 1024 : n);
+  std::vector<int> res(2 + 1024);
+  if ((rc = run_op(ctx, m, map, a, res.data(), 2 + 1024))) return rc;
+  const int got = res[1];
+  *n_out = got;
+  if (got > cap) return fail(ctx, LM_ERR_CAPACITY, "neighbor buffer too small");
+  for (int k = 0; k < got; ++k) out[k] = m->ids[res[2 + k]];
+  return LM_OK;
+}
+
+int lm_ledger(lm_ctx* ctx, int32_t map, lm_ledger_t* out) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  unsigned long long lg[LG_N];
+  CU(cudaMemcpyAsync(lg, m->d.ledger, sizeof lg, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  out->persistent_bytes_up = (int64_t)lg[LG_PERSIST];
+  out->naive_bytes_up = (int64_t)lg[LG_NAIVE];
+  out->small_bytes_triangulation = (int64_t)lg[LG_SMALL_TRI];
+  out->small_bytes_fusion = (int64_t)lg[LG_SMALL_FUSE];
+  out->small_transfer_events = (int64_t)lg[LG_SMALL_EVENTS];
+  out->evictions = (int64_t)lg[LG_EVICT];
+  return LM_OK;
+}
+
+static int refresh(lm_ctx* ctx, HostMap* m, int map) {
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_REFRESH;
+  int res[1];
+  int rc = run_op(ctx, m, map, a, res, 1);
+  if (rc) return rc;
+  return res[0] ? op_status(ctx, res[0], "refresh") : LM_OK;
+}
+
+int lm_export_keyframes(lm_ctx* ctx, int32_t map, int64_t* kf_id, int32_t* state, int32_t* kp_off, int32_t* kp_n,
+                        int32_t cap, int32_t* n_out) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  const int n = m->n_slots;
+  *n_out = n;
+  if (n > cap) return fail(ctx, LM_ERR_CAPACITY, "keyframe buffer too small");
+  for (int s = 0; s < n; ++s) {
+    kf_id[s] = m->ids[s];
+    state[s] = m->state[s];
+    kp_off[s] = m->kp_off[s];
+    kp_n[s] = m->kp_n[s];
+  }
+  return LM_OK;
+}
+
+int lm_export_bindings(lm_ctx* ctx, int32_t map, int32_t* bind, int32_t cap) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  if (cap < m->kp_head) return fail(ctx, LM_ERR_CAPACITY, "binding buffer too small");
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (m->kp_head) CU(cudaMemcpy(bind, m->d.kbind, sizeof(int) * m->kp_head, cudaMemcpyDeviceToHost));
+  return LM_OK;
+}
+
+int lm_export_points(lm_ctx* ctx, int32_t map, int32_t n, double* pos, uint8_t* rep, uint8_t* alive, int32_t* found,
+                     int32_t* visible, int32_t* nobs, int32_t* counts, int64_t* obs_kf, int32_t* obs_kp,
+                     int32_t obs_cap) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  if ((rc = refresh(ctx, m, map))) return rc;
+  if (n <= 0) return LM_OK;
+  const DevMap& d = m->d;
+  CU(cudaMemcpy(pos, d.pos, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(rep, d.rep, 32 * (size_t)n, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(alive, d.alive, n, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(found, d.found, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(visible, d.visible, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(nobs, d.nobs, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(counts, d.counts, sizeof(int) * n * d.L, cudaMemcpyDeviceToHost));
+  std::vector<int> off(n);
+  CU(cudaMemcpy(off.data(), d.ooff, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  int used = 0;
+  CU(cudaMemcpy(&used, d.scal + SC_OBS_HEAD, sizeof(int), cudaMemcpyDeviceToHost));
+  std::vector<int2> pool(used > 0 ? used : 1);
+  if (used) CU(cudaMemcpy(pool.data(), d.obs, sizeof(int2) * used, cudaMemcpyDeviceToHost));
+  long long tot = 0;
+  for (int i = 0; i < n; ++i) tot += nobs[i];
+  if (tot > obs_cap) return fail(ctx, LM_ERR_CAPACITY, "observation buffer too small (%lld)", tot);
+  int w = 0;
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < nobs[i]; ++k) {
+      const int2 e = pool[off[i] + k];
+      obs_kf[w] = m->ids[e.x];
+      obs_kp[w] = e.y;
+      ++w;
+    }
+  return LM_OK;
+}
+
+int lm_export_covis(lm_ctx* ctx, int32_t map, int32_t* w, int32_t cap) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  const size_t K = m->d.kf_cap;
+  if ((size_t)cap < K * K) return fail(ctx, LM_ERR_CAPACITY, "covis buffer too small");
+  CU(cudaStreamSynchronize(ctx->stream));
+  CU(cudaMemcpy(w, m->d.covis, sizeof(int) * K * K, cudaMemcpyDeviceToHost));
+  return LM_OK;
+}
+
+int lm_recent_export(lm_ctx* ctx, int32_t map, int64_t* ids, int32_t* born, int32_t cap, int32_t* n_out) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  int n = 0;
+  CU(cudaStreamSynchronize(ctx->stream));
+  CU(cudaMemcpy(&n, m->d.scal + SC_RECENT_N, sizeof(int), cudaMemcpyDeviceToHost));
+  *n_out = n;
+  if (n > cap) return fail(ctx, LM_ERR_CAPACITY, "recent buffer too small");
+  std::vector<int> id(n);
+  if (n) {
+    CU(cudaMemcpy(id.data(), m->d.recent_id, sizeof(int) * n, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(born, m->d.recent_born, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  }
+  for (int k = 0; k < n; ++k) ids[k] = id[k];
+  return LM_OK;
+}
+
+int lm_recent_import(lm_ctx* ctx, int32_t map, const int64_t* ids, const int32_t* born, int32_t n) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  if (n > m->d.recent_cap) return fail(ctx, LM_ERR_CAPACITY, "recent list too long");
+  std::vector<int> id(n);
+  for (int k = 0; k < n; ++k) id[k] = (int)ids[k];
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (n) {
+    CU(cudaMemcpy(m->d.recent_id, id.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(m->d.recent_born, born, sizeof(int) * n, cudaMemcpyHostToDevice));
+  }
+  CU(cudaMemcpy(m->d.scal + SC_RECENT_N, &n, sizeof(int), cudaMemcpyHostToDevice));
+  return LM_OK;
+}
+
+// ------------------------------------------------------------------- host math (CPU tests)
+int lm_host_fundamental(const double qa[4], const double ta[3], const double qb[4], const double tb[3],
+                        const double cam_a[4], const double cam_b[4], double F[9]) {
+  return fundamental(qa, ta, qb, tb, cam_a, cam_b, F) ? LM_OK : LM_ERR_DEGENERATE;
+}
+
+int lm_host_projection(const double quat[4], const double trans[3], const double cam[4], double R[9], double C[3],
+                       double P[12]) {
+  quat_to_rot(quat, R);
+  camera_center(R, trans, C);
+  proj_matrix(cam[0], cam[1], cam[2], cam[3], R, trans, P);
+  return LM_OK;
+}
+
+int lm_host_triangulate(const double Pa[12], const double Pb[12], const double Ca[3], const double Cb[3],
+                        const double pix[4], double X[3]) {
+  return triangulate(Pa, Pb, Ca, Cb, pix[0], pix[1], pix[2], pix[3], X) ? LM_OK : LM_ERR_DEGENERATE;
+}
+
+}  // extern "C"

@@ -1,0 +1,981 @@
+// lm_kernels.cuh -- the per-keyframe kernels of the hot path (sm_100a).
+//
+// One step for a batch of maps (blockIdx.{y,z} or blockIdx.x selects the map):
+//   k_insert   insert a staged keyframe (state, ledger, pre-bound slots)
+//   k_cull     recent map-point culling (culling.py:28-59), one CTA per map
+//   k_select   covisible neighbours + recency padding + F per pair (triangulation.py:219-232)
+//   k_prep     level-bucketed unbound keypoint lists per (current | neighbour)
+//   k_match    popcount Hamming x epipolar search, tile of current keypoints x one neighbour
+//              (triangulation.py:117-136), then one-to-one via 64-bit atomicMin (63-77)
+//   k_tri      candidate compaction in current-index order + fused DLT + creation gates
+//   k_commit   winner = lowest neighbour rank whose candidate passes; ids by block scan in
+//              (rank, i) order; point / binding / counter / covisibility writes (257-299)
+//   k_fuse     SearchAndFuse (fusion.py:307-347): targets, forward gather-all/apply-all,
+//              reverse gather/apply per target; one CTA per map
+#pragma once
+#include "lm_map.cuh"
+#include "lm_math.cuh"
+
+namespace lm {
+
+struct StepArgs {
+  int map;            // index into the context's map table
+  int cur;            // current keyframe slot
+  int n_nbr_req;      // neighbor_count
+  int do_insert, do_cull, do_create, do_fuse;
+  int processed;      // pipeline._processed
+  int explicit_nbr;   // lm_search: neighbour list given (nbr0), masks optional
+  int nbr0;
+  int use_mask_cur, use_mask_nbr;
+  int search_only;    // lm_search: stop after candidate compaction
+  lm_match_cfg mc;
+  lm_gate_cfg gc;
+  lm_fuse_cfg fc;
+  lm_cull_cfg cc;
+};
+
+// ---------------------------------------------------------------------------------- helpers
+
+template <int BLOCK>
+__device__ __forceinline__ int block_excl_scan(int v, int* sh, int& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int s = lane < BLOCK / 32 ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < BLOCK / 32) sh[lane] = s;
+  }
+  __syncthreads();
+  const int base = wid ? sh[wid - 1] : 0;
+  total = sh[BLOCK / 32 - 1];
+  __syncthreads();
+  return base + x - v;
+}
+
+template <int BLOCK>
+__device__ __forceinline__ int block_sum(int v, int* sh) {
+  int t;
+  block_excl_scan<BLOCK>(v, sh, t);
+  return t;
+}
+
+__device__ __forceinline__ long long payload_bytes(const DevMap& M, int slot) {
+  return (long long)M.kp_n[slot] * (M.kp_rec_bytes + M.desc_bytes);
+}
+
+// covisible_neighbors(k, n) (mapmodel.py:269-273 + CovisibilityGraph.neighbors 100-105):
+// live slots with weight >= min_w, ordered by (-weight, kf_id). Block-cooperative:
+// compacts the row into sh_slot/sh_w, ranks each entry by counting better entries and
+// scatters to out[rank]; returns min(count, n) (n < 0: all).
+template <int BLOCK>
+__device__ int ranked_neighbors(const DevMap& M, int k, int n, int* sh_slot, int* sh_w, int* out, int* sh_scan,
+                                int n_slots) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  const int* row = M.covis + (size_t)k * M.kf_cap;
+  for (int s = threadIdx.x; s < n_slots; s += BLOCK) {
+    const int w = row[s];
+    if (w >= M.min_w && w > 0 && s != k && M.kf_state[s] == KF_LIVE) {
+      const int at = atomicAdd(&cnt, 1);
+      sh_slot[at] = s;
+      sh_w[at] = w;
+    }
+  }
+  __syncthreads();
+  const int c = cnt;
+  const int lim = n < 0 ? c : (n < c ? n : c);
+  for (int e = threadIdx.x; e < c; e += BLOCK) {
+    const int we = sh_w[e];
+    const long long ie = M.kf_id[sh_slot[e]];
+    int r = 0;
+    for (int f = 0; f < c; ++f) {
+      const int wf = sh_w[f];
+      r += (wf > we) || (wf == we && M.kf_id[sh_slot[f]] < ie);
+    }
+    if (r < lim) out[r] = sh_slot[e];
+  }
+  __syncthreads();
+  return lim;
+}
+
+// ---------------------------------------------------------------------------------- insert
+
+__global__ void k_insert(DevMap* maps, const StepArgs* args) {
+  const StepArgs& A = args[blockIdx.x];
+  const DevMap& M = maps[A.map];
+  if (!A.do_insert) return;
+  const int slot = A.cur;
+  if (threadIdx.x == 0) {
+    M.kf_state[slot] = KF_LIVE;
+    M.ledger[LG_PERSIST] += (unsigned long long)payload_bytes(M, slot);
+    // pre-bound slots register their observations (insert_keyframe mapmodel.py:185-199)
+    const int off = M.kp_off[slot], n = M.kp_n[slot];
+    for (int i = 0; i < n; ++i) {
+      const int mp = M.kbind[off + i];
+      if (mp < 0) continue;
+      M.kbind[off + i] = -1;
+      if (mp >= M.scal[SC_NEXT_ID] || !M.alive[mp] || obs_find(M, mp, slot) >= 0) {
+        set_err(M, LM_ERR_INVALID_ARGUMENT);
+        continue;
+      }
+      link(M, mp, slot, i);
+      mark_dirty(M, mp);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------- cull
+
+__global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* args) {
+  const StepArgs& A = args[blockIdx.x];
+  const DevMap& M = maps[A.map];
+  if (!A.do_cull) return;
+  __shared__ int sh[32];
+  const int n = M.scal[SC_RECENT_N];
+  int kept = 0, culled = 0;
+  for (int base = 0; base < n; base += 1024) {
+    const int e = base + threadIdx.x;
+    int keep = 0, id = -1, born = 0;
+    if (e < n) {
+      id = M.recent_id[e];
+      born = M.recent_born[e];
+      if (M.alive[id]) {
+        const double ratio = (double)M.found[id] / (double)(M.visible[id] > 1 ? M.visible[id] : 1);
+        if (ratio < A.cc.found_ratio_min) {
+          kill_point(M, id);
+          ++culled;
+        } else if (A.processed - born >= A.cc.probation_kfs) {
+          if (M.nobs[id] < A.cc.min_obs_graduate) {
+            kill_point(M, id);
+            ++culled;
+          }
+        } else {
+          keep = 1;
+        }
+      }
+    }
+    int tot;
+    const int at = block_excl_scan<1024>(keep, sh, tot);
+    if (keep) {  // stable in-place compaction: write index <= read index
+      M.recent_id[kept + at] = id;
+      M.recent_born[kept + at] = born;
+    }
+    kept += tot;
+    __syncthreads();
+  }
+  const int tc = block_sum<1024>(culled, sh);
+  if (threadIdx.x == 0) {
+    M.scal[SC_RECENT_N] = kept;
+    M.s.stats->culled = tc;
+  }
+}
+
+// ---------------------------------------------------------------------------------- select
+
+__global__ void __launch_bounds__(256) k_select(DevMap* maps, const StepArgs* args, int n_slots_max) {
+  const StepArgs& A = args[blockIdx.x];
+  const DevMap& M = maps[A.map];
+  if (!A.do_create) return;
+  extern __shared__ int dyn[];
+  int* sh_slot = dyn;
+  int* sh_w = dyn + M.kf_cap;
+  __shared__ int out[NMAX];
+  __shared__ int sh_scan[32];
+  __shared__ int n_out;
+  const int cur = A.cur;
+  int want = A.n_nbr_req < NMAX ? A.n_nbr_req : NMAX;
+  if (A.explicit_nbr) {
+    if (threadIdx.x == 0) {
+      out[0] = A.nbr0;
+      n_out = 1;
+    }
+    __syncthreads();
+  } else {
+    const int got = ranked_neighbors<256>(M, cur, want, sh_slot, sh_w, out, sh_scan, n_slots_max);
+    if (threadIdx.x == 0) n_out = got;
+    __syncthreads();
+    if (n_out < want) {
+      // recency padding: live keyframes other than cur, newest kf id first, not yet listed
+      __shared__ int cnt;
+      if (threadIdx.x == 0) cnt = 0;
+      __syncthreads();
+      for (int s = threadIdx.x; s < n_slots_max; s += 256) {
+        if (s == cur || M.kf_state[s] != KF_LIVE) continue;
+        bool listed = false;
+        for (int k = 0; k < n_out; ++k) listed |= out[k] == s;
+        if (!listed) sh_slot[atomicAdd(&cnt, 1)] = s;
+      }
+      __syncthreads();
+      const int c = cnt, need = want - n_out;
+      for (int e = threadIdx.x; e < c; e += 256) {
+        const long long ie = M.kf_id[sh_slot[e]];
+        int r = 0;
+        for (int f = 0; f < c; ++f) r += M.kf_id[sh_slot[f]] > ie;
+        if (r < need) out[n_out + r] = sh_slot[e];
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) n_out = n_out + (c < need ? c : need);
+      __syncthreads();
+    }
+  }
+  const int nn = n_out;
+  lm_step_stats* st = M.s.stats;
+  if (threadIdx.x < nn) {
+    const int s = out[threadIdx.x];
+    M.s.nbr[threadIdx.x] = s;
+    double F[9];
+    const double ca[4] = {M.cam[6 * cur], M.cam[6 * cur + 1], M.cam[6 * cur + 2], M.cam[6 * cur + 3]};
+    const double cb[4] = {M.cam[6 * s], M.cam[6 * s + 1], M.cam[6 * s + 2], M.cam[6 * s + 3]};
+    const bool ok = fundamental(M.q + 4 * cur, M.t + 3 * cur, M.q + 4 * s, M.t + 3 * s, ca, cb, F);
+    M.s.deg[threadIdx.x] = ok ? 0 : 1;
+    for (int k = 0; k < 9; ++k) M.s.F[9 * threadIdx.x + k] = F[k];
+    st->neighbors[threadIdx.x] = M.kf_id[s];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st->n_neighbors = nn;
+    int nd = 0;
+    unsigned long long naive = 0;
+    for (int r = 0; r < nn; ++r) {
+      naive += (unsigned long long)payload_bytes(M, out[r]);
+      if (M.s.deg[r]) st->degenerate_neighbors[nd++] = M.kf_id[out[r]];
+    }
+    st->n_degenerate_neighbors = nd;
+    if (!A.explicit_nbr) M.ledger[LG_NAIVE] += naive;
+  }
+}
+
+// ---------------------------------------------------------------------------------- prep
+
+__device__ __forceinline__ bool is_unbound(const DevMap& M, const StepArgs& A, int g, int local, bool cur_side) {
+  if (cur_side ? A.use_mask_cur : A.use_mask_nbr) return (cur_side ? M.s.mask_cur : M.s.mask_nbr)[local] != 0;
+  return M.kbind[g] < 0;
+}
+
+__global__ void __launch_bounds__(256) k_prep(DevMap* maps, const StepArgs* args) {
+  const StepArgs& A = args[blockIdx.y];
+  const DevMap& M = maps[A.map];
+  if (!A.do_create) return;
+  const int nn = M.s.stats->n_neighbors;
+  const int list = blockIdx.x;  // 0 = current, r+1 = neighbour r
+  if (list > nn) return;
+  __shared__ int lcount[LMAX], lstart[LMAX + 1], lcur[LMAX];
+  const int L = M.L;
+  const int slot = list == 0 ? A.cur : M.s.nbr[list - 1];
+  const int r = list - 1;
+  const int off = M.kp_off[slot], n = M.kp_n[slot];
+  const int ncur = M.kp_n[A.cur];
+  if (list > 0 && M.s.deg[r]) {
+    if (threadIdx.x == 0) {
+      M.s.nb_n[r] = 0;
+      M.s.cand_n[r] = 0;
+    }
+    return;
+  }
+  if (threadIdx.x < LMAX) lcount[threadIdx.x] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += 256)
+    if (is_unbound(M, A, off + i, i, list == 0)) atomicAdd(&lcount[M.klev[off + i]], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int l = 0; l < L; ++l) {
+      lstart[l] = acc;
+      lcur[l] = acc;
+      acc += lcount[l];
+    }
+    lstart[L] = acc;
+  }
+  __syncthreads();
+  if (list == 0) {
+    for (int i = threadIdx.x; i < n; i += 256) {
+      M.s.win_rank[i] = 0x7fffffff;
+      if (is_unbound(M, A, off + i, i, true)) {
+        const int at = atomicAdd(&lcur[M.klev[off + i]], 1);
+        M.s.cur_sorted[at] = i;
+      }
+    }
+    if (threadIdx.x <= L) M.s.cur_bucket[threadIdx.x] = lstart[threadIdx.x];
+    if (threadIdx.x == 0) {  // tiles never straddle a level
+      int nt = 0;
+      for (int l = 0; l < L; ++l)
+        for (int s = lstart[l]; s < lstart[l + 1]; s += MATCH_TILE) {
+          const int c = lstart[l + 1] - s;
+          M.s.tiles[3 * nt] = l;
+          M.s.tiles[3 * nt + 1] = s;
+          M.s.tiles[3 * nt + 2] = c < MATCH_TILE ? c : MATCH_TILE;
+          ++nt;
+        }
+      *M.s.n_tiles = nt;
+    }
+  } else {
+    const size_t base = (size_t)r * M.kpkf_max;
+    for (int i = threadIdx.x; i < n; i += 256) {
+      M.s.bestj[base + i] = ~0ull;
+      if (is_unbound(M, A, off + i, i, false)) {
+        const int lv = M.klev[off + i];
+        const int at = atomicAdd(&lcur[lv], 1);
+        M.s.nb_j[base + at] = i;
+        M.s.nb_desc[2 * (base + at)] = M.kdesc[2 * (off + i)];
+        M.s.nb_desc[2 * (base + at) + 1] = M.kdesc[2 * (off + i) + 1];
+        M.s.nb_u[base + at] = M.ku[off + i];
+        M.s.nb_v[base + at] = M.kv[off + i];
+        M.s.nb_thr[base + at] = A.mc.chi2_epi * M.S2[lv];
+      }
+    }
+    for (int i = threadIdx.x; i < ncur; i += 256) M.s.pick[base + i] = ~0ull;
+    if (threadIdx.x <= L) M.s.nb_bucket[r * (LMAX + 1) + threadIdx.x] = lstart[threadIdx.x];
+    if (threadIdx.x == 0) M.s.nb_n[r] = lstart[L];
+  }
+}
+
+// ---------------------------------------------------------------------------------- match
+
+// grid (tiles, NMAX, maps), block MATCH_TILE. Each thread owns one unbound current
+// keypoint of the tile's level and scans the neighbour's unbound keypoints of levels
+// [l-w, l+w], staged MATCH_JT at a time in shared memory (warp-broadcast reads). Hamming
+// first (8 x POPC), the fp64 epipolar test only on the rare dist <= max survivors; the
+// running minimum is the lexicographic (dist, j) key of the reference's first-argmin.
+__global__ void __launch_bounds__(MATCH_TILE) k_match(DevMap* maps, const StepArgs* args) {
+  const StepArgs& A = args[blockIdx.z];
+  const DevMap& M = maps[A.map];
+  if (!A.do_create) return;
+  const int r = blockIdx.y;
+  if (r >= M.s.stats->n_neighbors || M.s.deg[r]) return;
+  const int tile = blockIdx.x;
+  if (tile >= *M.s.n_tiles) return;
+  __shared__ uint4 sd[2 * MATCH_JT];
+  const int lv = M.s.tiles[3 * tile], start = M.s.tiles[3 * tile + 1], cnt = M.s.tiles[3 * tile + 2];
+  const int w = A.mc.level_window;
+  const int l0 = lv - w < 0 ? 0 : lv - w;
+  const int l1 = lv + w > M.L - 1 ? M.L - 1 : lv + w;
+  const int* bk = M.s.nb_bucket + r * (LMAX + 1);
+  const int jb = bk[l0], je = bk[l1 + 1];
+  const size_t base = (size_t)r * M.kpkf_max;
+  const int cur = A.cur;
+  const int off = M.kp_off[cur];
+  const bool active = threadIdx.x < cnt;
+  int i = 0;
+  uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0;
+  double l[3] = {0, 0, 0}, den = 0;
+  if (active) {
+    i = M.s.cur_sorted[start + threadIdx.x];
+    a0 = M.kdesc[2 * (off + i)];
+    a1 = M.kdesc[2 * (off + i) + 1];
+    epi_line(M.s.F + 9 * r, M.ku[off + i], M.kv[off + i], l);
+    den = l[0] * l[0] + l[1] * l[1];
+  }
+  const int maxd = A.mc.match_max_distance;
+  unsigned long long best = ~0ull;
+  for (int t0 = jb; t0 < je; t0 += MATCH_JT) {
+    const int tn = je - t0 < MATCH_JT ? je - t0 : MATCH_JT;
+    __syncthreads();
+    for (int k = threadIdx.x; k < 2 * tn; k += MATCH_TILE) sd[k] = M.s.nb_desc[2 * (base + t0) + k];
+    __syncthreads();
+    if (active) {
+      for (int k = 0; k < tn; ++k) {
+        const int dist = hamming(a0, a1, sd[2 * k], sd[2 * k + 1]);
+        if (dist <= maxd) {
+          const size_t e = base + t0 + k;
+          if (epi_d2(l, den, M.s.nb_u[e], M.s.nb_v[e]) <= M.s.nb_thr[e]) {
+            const unsigned long long key = ((unsigned long long)dist << 32) | (unsigned)M.s.nb_j[e];
+            best = key < best ? key : best;
+          }
+        }
+      }
+    }
+  }
+  if (active && best != ~0ull) {
+    M.s.pick[base + i] = best;
+    const unsigned j = (unsigned)(best & 0xffffffffu);
+    atomicMin(&M.s.bestj[base + j], (best & 0xffffffff00000000ull) | (unsigned)i);
+  }
+}
+
+// ---------------------------------------------------------------------------------- tri
+
+__global__ void __launch_bounds__(256) k_tri(DevMap* maps, const StepArgs* args) {
+  const StepArgs& A = args[blockIdx.y];
+  const DevMap& M = maps[A.map];
+  if (!A.do_create) return;
+  const int r = blockIdx.x;
+  if (r >= M.s.stats->n_neighbors) return;
+  if (M.s.deg[r]) return;  // cand_n[r] = 0 set by k_prep
+  __shared__ int sh[32];
+  const int cur = A.cur;
+  const int ncur = M.kp_n[cur];
+  const size_t base = (size_t)r * M.kpkf_max;
+  int count = 0;
+  for (int b0 = 0; b0 < ncur; b0 += 256) {
+    const int i = b0 + threadIdx.x;
+    int flag = 0;
+    unsigned long long pk = ~0ull;
+    if (i < ncur) {
+      pk = M.s.pick[base + i];
+      if (pk != ~0ull) {
+        const unsigned j = (unsigned)(pk & 0xffffffffu);
+        flag = M.s.bestj[base + j] == ((pk & 0xffffffff00000000ull) | (unsigned)i);
+      }
+    }
+    int tot;
+    const int at = block_excl_scan<256>(flag, sh, tot);
+    if (flag) {
+      M.s.cand_i[base + count + at] = i;
+      M.s.cand_j[base + count + at] = (int)(pk & 0xffffffffu);
+      M.s.cand_d[base + count + at] = (int)(pk >> 32);
+    }
+    count += tot;
+  }
+  if (threadIdx.x == 0) M.s.cand_n[r] = count;
+  if (A.search_only) return;
+  const int nb = M.s.nbr[r];
+  const int offa = M.kp_off[cur], offb = M.kp_off[nb];
+  for (int k = threadIdx.x; k < count; k += 256) {
+    const int i = M.s.cand_i[base + k], j = M.s.cand_j[base + k];
+    const int ga = offa + i, gb = offb + j;
+    double X[3] = {0, 0, 0};
+    int st;
+    if (!triangulate(M.P + 12 * cur, M.P + 12 * nb, M.C + 3 * cur, M.C + 3 * nb, M.ku[ga], M.kv[ga], M.ku[gb],
+                     M.kv[gb], X)) {
+      st = CS_DEGEN;
+    } else {
+      const int la = M.klev[ga], lb = M.klev[gb];
+      ViewGeo va{M.R + 9 * cur, M.t + 3 * cur, M.C + 3 * cur, M.cam[6 * cur], M.cam[6 * cur + 1],
+                 M.cam[6 * cur + 2], M.cam[6 * cur + 3], M.ku[ga], M.kv[ga], M.S2[la], M.S[la], M.sf};
+      ViewGeo vb{M.R + 9 * nb, M.t + 3 * nb, M.C + 3 * nb, M.cam[6 * nb], M.cam[6 * nb + 1],
+                 M.cam[6 * nb + 2], M.cam[6 * nb + 3], M.ku[gb], M.kv[gb], M.S2[lb], M.S[lb], M.sf};
+      st = creation_gates(va, vb, X, A.gc.cos_parallax_max, A.gc.chi2_mono, A.gc.scale_ratio_slack);
+    }
+    M.s.cand_st[base + k] = st;
+    M.s.cand_X[3 * (base + k)] = X[0];
+    M.s.cand_X[3 * (base + k) + 1] = X[1];
+    M.s.cand_X[3 * (base + k) + 2] = X[2];
+    if (st == CS_PASS) atomicMin(&M.s.win_rank[i], r);
+  }
+}
+
+// ---------------------------------------------------------------------------------- commit
+
+__global__ void __launch_bounds__(1024) k_commit(DevMap* maps, const StepArgs* args) {
+  const StepArgs& A = args[blockIdx.x];
+  const DevMap& M = maps[A.map];
+  if (!A.do_create || A.search_only) return;
+  __shared__ int sh[32];
+  __shared__ int coff[NMAX + 1];
+  __shared__ int per_r[NMAX];
+  __shared__ int okcap;
+  const int nn = M.s.stats->n_neighbors;
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int r = 0; r < nn; ++r) {
+      coff[r] = acc;
+      acc += M.s.cand_n[r];
+    }
+    coff[nn] = acc;
+  }
+  if (threadIdx.x < NMAX) per_r[threadIdx.x] = 0;
+  __syncthreads();
+  const int total = coff[nn];
+  const int cur = A.cur;
+  // outcome of candidate g: 0 created, 1 conflict, 2+ failure status
+  auto outcome = [&](int g, int& r, int& k) -> int {
+    r = 0;
+    while (coff[r + 1] <= g) ++r;
+    k = g - coff[r];
+    const size_t e = (size_t)r * M.kpkf_max + k;
+    const int i = M.s.cand_i[e];
+    if (M.s.win_rank[i] < r) return 1;
+    const int st = M.s.cand_st[e];
+    return st == CS_PASS ? 0 : 1 + st;
+  };
+  // pass 1: totals and capacity
+  int c_created = 0, c_conf = 0, c_deg = 0, c_g[5] = {0, 0, 0, 0, 0};
+  for (int g = threadIdx.x; g < total; g += 1024) {
+    int r, k;
+    const int oc = outcome(g, r, k);
+    if (oc == 0) ++c_created;
+    else if (oc == 1) ++c_conf;
+    else if (oc == 1 + CS_DEGEN) ++c_deg;
+    else ++c_g[oc - 1];
+  }
+  const int created = block_sum<1024>(c_created, sh);
+  const int conflicts = block_sum<1024>(c_conf, sh);
+  const int degen = block_sum<1024>(c_deg, sh);
+  int gates[4];
+  for (int q = 0; q < 4; ++q) gates[q] = block_sum<1024>(c_g[q + 1], sh);
+  const int id0 = M.scal[SC_NEXT_ID];
+  const int obs0 = M.scal[SC_OBS_HEAD];
+  const int rec0 = M.scal[SC_RECENT_N];
+  if (threadIdx.x == 0) {
+    okcap = 1;
+    if ((long long)id0 + created > M.mp_cap || (long long)obs0 + 4LL * created > M.obs_cap ||
+        rec0 + created > M.recent_cap) {
+      okcap = 0;
+      set_err(M, LM_ERR_CAPACITY);
+    }
+  }
+  __syncthreads();
+  if (okcap) {
+    int run = 0;
+    for (int b0 = 0; b0 < total; b0 += 1024) {
+      const int g = b0 + threadIdx.x;
+      int r = 0, k = 0, oc = -1;
+      if (g < total) oc = outcome(g, r, k);
+      int tot;
+      const int at = block_excl_scan<1024>(oc == 0, sh, tot);
+      if (oc == 0) {
+        const int rank = run + at;
+        const int id = id0 + rank;
+        const size_t e = (size_t)r * M.kpkf_max + k;
+        const int i = M.s.cand_i[e], j = M.s.cand_j[e];
+        const int nb = M.s.nbr[r];
+        const int ga = M.kp_off[cur] + i, gb = M.kp_off[nb] + j;
+        M.pos[3 * id] = M.s.cand_X[3 * e];
+        M.pos[3 * id + 1] = M.s.cand_X[3 * e + 1];
+        M.pos[3 * id + 2] = M.s.cand_X[3 * e + 2];
+        const bool cur_first = M.kf_id[cur] < M.kf_id[nb];
+        const int grep = cur_first ? ga : gb;
+        M.rep[2 * id] = M.kdesc[2 * grep];
+        M.rep[2 * id + 1] = M.kdesc[2 * grep + 1];
+        M.alive[id] = 1;
+        M.found[id] = 1;
+        M.visible[id] = 1;
+        M.first_kf[id] = M.kf_id[cur];
+        const int oo = obs0 + 4 * rank;
+        M.ooff[id] = oo;
+        M.ocap[id] = 4;
+        M.nobs[id] = 2;
+        M.obs[oo] = cur_first ? make_int2(cur, i) : make_int2(nb, j);
+        M.obs[oo + 1] = cur_first ? make_int2(nb, j) : make_int2(cur, i);
+        M.dirty[id] = 0;
+        M.counts[(size_t)id * M.L + M.klev[ga]] += 1;
+        M.counts[(size_t)id * M.L + M.klev[gb]] += 1;
+        M.kbind[ga] = id;
+        M.kbind[gb] = id;
+        atomicAdd(&per_r[r], 1);
+        M.recent_id[rec0 + rank] = id;
+        M.recent_born[rec0 + rank] = A.processed;
+      }
+      run += tot;
+    }
+  }
+  __syncthreads();
+  if (okcap && threadIdx.x < nn && per_r[threadIdx.x]) covis_add(M, cur, M.s.nbr[threadIdx.x], per_r[threadIdx.x]);
+  if (threadIdx.x == 0) {
+    lm_step_stats* st = M.s.stats;
+    st->created = okcap ? created : 0;
+    st->conflicts = conflicts;
+    st->degenerate = degen;
+    st->gate_parallax = gates[0];
+    st->gate_depth = gates[1];
+    st->gate_reprojection = gates[2];
+    st->gate_scale = gates[3];
+    st->first_new_id = id0;
+    if (okcap) {
+      M.scal[SC_NEXT_ID] = id0 + created;
+      M.scal[SC_OBS_HEAD] = obs0 + 4 * created;
+      M.scal[SC_RECENT_N] = rec0 + created;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------- fusion
+
+// point geometry (fusion.py:57-94)
+__device__ void point_geometry(const DevMap& M, int mp, double slack, PGeo& g) {
+  g.ok = 0;
+  if (mp < 0 || !M.alive[mp] || M.nobs[mp] == 0) return;
+  const double x = M.pos[3 * mp], y = M.pos[3 * mp + 1], z = M.pos[3 * mp + 2];
+  const int2* o = M.obs + M.ooff[mp];
+  const int n = M.nobs[mp];
+  double lo = INFINITY, hi = -INFINITY, ax = 0, ay = 0, az = 0;
+  for (int k = 0; k < n; ++k) {
+    const int s = o[k].x;
+    const double rx = x - M.C[3 * s], ry = y - M.C[3 * s + 1], rz = z - M.C[3 * s + 2];
+    const double dd = sqrt(rx * rx + ry * ry + rz * rz);
+    if (dd <= 0) continue;
+    const double d0 = dd / M.S[M.klev[M.kp_off[s] + o[k].y]];
+    lo = d0 < lo ? d0 : lo;
+    hi = d0 > hi ? d0 : hi;
+    ax = ax + rx / dd;
+    ay = ay + ry / dd;
+    az = az + rz / dd;
+  }
+  if (!isfinite(lo)) return;
+  const double nrm = sqrt(ax * ax + ay * ay + az * az);
+  if (nrm > 0) {
+    g.vx = ax / nrm;
+    g.vy = ay / nrm;
+    g.vz = az / nrm;
+  } else {
+    g.vx = ax;
+    g.vy = ay;
+    g.vz = az;
+  }
+  g.x = x;
+  g.y = y;
+  g.z = z;
+  g.d0 = lo;
+  g.blo = lo / slack;
+  g.bhi = hi * M.S[M.L - 1] * slack;
+  g.r0 = M.rep[2 * mp];
+  g.r1 = M.rep[2 * mp + 1];
+  g.ok = 1;
+}
+
+// project + gates + grid window search + action build for one (point, target) pair
+// (fusion.py:97-129, 178-196, 161-174). Returns 1 if visible; *act filled when an action.
+__device__ int gather_one(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g, int pid, int ts, ActRec* act,
+                          int* has_act) {
+  *has_act = 0;
+  if (!g.ok) return 0;
+  const double* R = M.R + 9 * ts;
+  const double* t = M.t + 3 * ts;
+  const double* C = M.C + 3 * ts;
+  const double* cam = M.cam + 6 * ts;
+  const double qx = R[0] * g.x + R[1] * g.y + R[2] * g.z;
+  const double qy = R[3] * g.x + R[4] * g.y + R[5] * g.z;
+  const double qz = R[6] * g.x + R[7] * g.y + R[8] * g.z;
+  const double zc = qz + t[2];
+  const double u = cam[0] * ((qx + t[0]) / zc) + cam[2];
+  const double v = cam[1] * ((qy + t[1]) / zc) + cam[3];
+  const bool inview = zc > 0 && u >= 0 && u < cam[4] && v >= 0 && v < cam[5];
+  const double dx = g.x - C[0], dy = g.y - C[1], dz = g.z - C[2];
+  const double d = sqrt(dx * dx + dy * dy + dz * dz);
+  const double cosv = (dx * g.vx + dy * g.vy + dz * g.vz) / d;
+  double lraw = log(d / g.d0) / M.log_sf;
+  if (!isfinite(lraw)) lraw = 0.0;
+  double lr = rint(lraw);
+  lr = lr < 0 ? 0 : (lr > M.L - 1 ? M.L - 1 : lr);
+  const int lp = (int)lr;
+  const double rad = fc.fuse_radius * M.S[lp];
+  if (!(zc > 0 && inview && d >= g.blo && d <= g.bhi && cosv >= fc.min_view_cos)) return 0;
+  // conservative cell window, exact test inside
+  const double cs = M.g_cs[ts];
+  const int nx = M.g_nx[ts], ny = M.g_ny[ts];
+  int x0 = (int)floor((u - rad - 1.0) / cs), x1 = (int)floor((u + rad + 1.0) / cs);
+  int y0 = (int)floor((v - rad - 1.0) / cs), y1 = (int)floor((v + rad + 1.0) / cs);
+  x0 = x0 < 0 ? 0 : x0;
+  y0 = y0 < 0 ? 0 : y0;
+  x1 = x1 > nx - 1 ? nx - 1 : x1;
+  y1 = y1 > ny - 1 ? ny - 1 : y1;
+  const int* cst = M.cell_start + (size_t)ts * (GRID_CELLS + 1);
+  const int off = M.kp_off[ts];
+  const double r2 = rad * rad;
+  unsigned long long best = ~0ull;
+  for (int cy = y0; cy <= y1; ++cy) {
+    for (int cx = x0; cx <= x1; ++cx) {
+      const int cell = cy * nx + cx;
+      for (int it = cst[cell]; it < cst[cell + 1]; ++it) {
+        const int gk = M.cell_items[off + it];
+        const double du = M.ku[gk] - u, dv = M.kv[gk] - v;
+        const int dl = (int)M.klev[gk] - lp;
+        if (du * du + dv * dv <= r2 && (dl < 0 ? -dl : dl) <= fc.level_window) {
+          const int dist = hamming(M.kdesc[2 * gk], M.kdesc[2 * gk + 1], g.r0, g.r1);
+          if (dist <= fc.match_max_distance) {
+            const unsigned long long key = ((unsigned long long)dist << 32) | (unsigned)(gk - off);
+            best = key < best ? key : best;
+          }
+        }
+      }
+    }
+  }
+  if (best != ~0ull) {
+    const int j = (int)(best & 0xffffffffu);
+    const int owner = M.kbind[off + j];
+    if (owner < 0) {
+      if (obs_find(M, pid, ts) < 0) {
+        *act = ActRec{ts, pid, j, -1, LM_ACT_ADD};
+        *has_act = 1;
+      }
+    } else if (owner != pid && M.alive[owner]) {
+      *act = ActRec{ts, pid, j, owner, LM_ACT_MERGE};
+      *has_act = 1;
+    }
+  }
+  return 1;
+}
+
+// apply_fusion (fusion.py:249-292), sequential in list order
+__device__ void apply_actions(const DevMap& M, const ActRec* acts, int n, int cnt[3]) {
+  for (int a = 0; a < n; ++a) {
+    const ActRec x = acts[a];
+    if (x.pid < 0 || !M.alive[x.pid] || M.kf_state[x.slot] != KF_LIVE) {
+      ++cnt[2];
+      continue;
+    }
+    const int g = M.kp_off[x.slot] + x.j;
+    if (x.kind == LM_ACT_MERGE) {
+      if (x.other < 0 || !M.alive[x.other] || x.other == x.pid || M.kbind[g] != x.other) {
+        ++cnt[2];
+        continue;
+      }
+      merge_pair(M, x.pid, x.other);
+      ++cnt[0];
+      continue;
+    }
+    const int now = M.kbind[g];
+    if (now >= 0) {
+      if (!M.alive[now] || now == x.pid) {
+        ++cnt[2];
+        continue;
+      }
+      merge_pair(M, x.pid, now);
+      ++cnt[0];
+      continue;
+    }
+    if (obs_find(M, x.pid, x.slot) >= 0) {
+      ++cnt[2];
+      continue;
+    }
+    link(M, x.pid, x.slot, x.j);
+    mark_dirty(M, x.pid);
+    M.found[x.pid] += 1;
+    ++cnt[1];
+  }
+}
+
+// recompute every dirty representative descriptor (warp per point)
+template <int BLOCK>
+__device__ void refresh_dirty(const DevMap& M) {
+  __syncthreads();
+  const int n = M.scal[SC_DIRTY_N];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k = wid; k < n; k += BLOCK / 32) {
+    const int mp = M.dirty_list[k];
+    if (M.alive[mp]) refresh_rep_warp(M, mp, lane);
+    __syncwarp();
+    if (lane == 0) M.dirty[mp] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) M.scal[SC_DIRTY_N] = 0;
+  __syncthreads();
+}
+
+// bound live points of keyframe slot (mapmodel.py:291-300), in keypoint order, into M.s.pts
+template <int BLOCK>
+__device__ int bound_points(const DevMap& M, int slot, int* sh) {
+  const int off = M.kp_off[slot], n = M.kp_n[slot];
+  int count = 0;
+  for (int b0 = 0; b0 < n; b0 += BLOCK) {
+    const int i = b0 + threadIdx.x;
+    int mp = -1, f = 0;
+    if (i < n) {
+      mp = M.kbind[off + i];
+      f = mp >= 0 && M.alive[mp];
+    }
+    int tot;
+    const int at = block_excl_scan<BLOCK>(f, sh, tot);
+    if (f) M.s.pts[count + at] = mp;
+    count += tot;
+  }
+  __syncthreads();
+  return count;
+}
+
+// collect_fusion_targets (fusion.py:38-54)
+template <int BLOCK>
+__device__ int fusion_targets(const DevMap& M, int cur, int n1, int n2, int n_slots, int* sh_slot, int* sh_w,
+                              int* sh_scan) {
+  __shared__ int first[TMAX];
+  __shared__ int n_first, n_t;
+  const int nf = ranked_neighbors<BLOCK>(M, cur, n1 < TMAX ? n1 : TMAX, sh_slot, sh_w, first, sh_scan, n_slots);
+  if (threadIdx.x == 0) n_first = nf;
+  __syncthreads();
+  // rank every first-order row in parallel: warp w handles rows w, w+32, ...
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int f = wid; f < n_first; f += BLOCK / 32) {
+    int* buf = M.s.rank_buf + (size_t)f * (2 * M.kf_cap + 1);  // [count][slots...][ranked...]
+    const int row_slot = first[f];
+    const int* row = M.covis + (size_t)row_slot * M.kf_cap;
+    int c = 0;
+    for (int s0 = 0; s0 < n_slots; s0 += 32) {
+      const int s = s0 + lane;
+      const bool take = s < n_slots && s != row_slot && row[s] >= M.min_w && row[s] > 0 && M.kf_state[s] == KF_LIVE;
+      const unsigned bal = __ballot_sync(0xffffffffu, take);
+      if (take) buf[1 + c + __popc(bal & ((1u << lane) - 1))] = s;
+      c += __popc(bal);
+    }
+    __syncwarp();
+    for (int e = lane; e < c; e += 32) {
+      const int se = buf[1 + e];
+      const int we = row[se];
+      const long long ie = M.kf_id[se];
+      int rk = 0;
+      for (int q = 0; q < c; ++q) {
+        const int sq = buf[1 + q];
+        const int wq = row[sq];
+        rk += (wq > we) || (wq == we && M.kf_id[sq] < ie);
+      }
+      buf[1 + M.kf_cap + rk] = se;
+    }
+    if (lane == 0) buf[0] = c;
+    __syncwarp();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int nt = 0;
+    for (int f = 0; f < n_first; ++f) M.s.targets[nt++] = first[f];
+    for (int f = 0; f < n_first; ++f) {
+      const int* buf = M.s.rank_buf + (size_t)f * (2 * M.kf_cap + 1);
+      const int c = buf[0];
+      int added = 0;
+      for (int q = 0; q < c && added < n2 && nt < TMAX; ++q) {
+        const int s = buf[1 + M.kf_cap + q];
+        if (s == cur) continue;
+        bool seen = false;
+        for (int u = 0; u < nt && !seen; ++u) seen = M.s.targets[u] == s;
+        if (!seen) {
+          M.s.targets[nt++] = s;
+          ++added;
+        }
+      }
+    }
+    n_t = nt;
+    *M.s.n_targets = nt;
+  }
+  __syncthreads();
+  return n_t;
+}
+
+// one reverse-style pass: points M.s.pts[0..P) into target ts, gather + (optionally) visible
+// increments + compaction into M.s.acts; returns action count
+template <int BLOCK>
+__device__ int gather_pass(const DevMap& M, const lm_fuse_cfg& fc, int P, int ts, bool bump_visible, int* sh,
+                           int* vis_out) {
+  for (int p = threadIdx.x; p < P; p += BLOCK) point_geometry(M, M.s.pts[p], fc.dist_band_slack, M.s.geo[p]);
+  __syncthreads();
+  int count = 0, nvis = 0;
+  for (int b0 = 0; b0 < P; b0 += BLOCK) {
+    const int p = b0 + threadIdx.x;
+    ActRec a;
+    int has = 0, vis = 0;
+    if (p < P) {
+      const int pid = M.s.pts[p];
+      vis = gather_one(M, fc, M.s.geo[p], pid, ts, &a, &has);
+      if (vis && bump_visible && M.alive[pid]) atomicAdd(&M.visible[pid], 1);
+      if (vis_out) M.s.vis_flag[p] = vis;
+    }
+    int tot;
+    const int at = block_excl_scan<BLOCK>(has, sh, tot);
+    if (has) M.s.acts[count + at] = a;
+    count += tot;
+    nvis += vis;
+  }
+  if (vis_out) *vis_out = block_sum<BLOCK>(nvis, sh);
+  __syncthreads();
+  return count;
+}
+
+// full run_fusion for one map per CTA
+__global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* args, int n_slots_max) {
+  const StepArgs& A = args[blockIdx.x];
+  const DevMap& M = maps[A.map];
+  if (!A.do_fuse) return;
+  extern __shared__ int dyn[];
+  int* sh_slot = dyn;
+  int* sh_w = dyn + M.kf_cap;
+  __shared__ int sh[32];
+  __shared__ int cnt[3];
+  const lm_fuse_cfg& fc = A.fc;
+  const int cur = A.cur;
+  if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
+  refresh_dirty<1024>(M);
+  const int T = fusion_targets<1024>(M, cur, fc.n1, fc.n2, n_slots_max, sh_slot, sh_w, sh);
+  lm_step_stats* st = M.s.stats;
+  if (T == 0) {
+    if (threadIdx.x == 0) {
+      st->n_targets = 0;
+      st->merged = st->observations_added = st->stale = 0;
+    }
+    return;
+  }
+  const int mpb = M.mp_rec_bytes;
+  // forward: gather all targets against the unchanged map, then one ordered apply
+  const int P = bound_points<1024>(M, cur, sh);
+  if (threadIdx.x == 0) {
+    unsigned long long naive = 0;
+    for (int k = 0; k < T; ++k) naive += (unsigned long long)payload_bytes(M, M.s.targets[k]);
+    M.ledger[LG_NAIVE] += naive + (unsigned long long)P * mpb;
+    M.ledger[LG_PERSIST] += (unsigned long long)P * mpb;
+    M.ledger[LG_SMALL_FUSE] += (unsigned long long)P * mpb;
+    M.ledger[LG_SMALL_EVENTS] += 1;
+  }
+  for (int p = threadIdx.x; p < P; p += 1024) point_geometry(M, M.s.pts[p], fc.dist_band_slack, M.s.geo[p]);
+  __syncthreads();
+  const int TP = T * P;
+  for (int it = threadIdx.x; it < TP; it += 1024) {
+    const int t = it / P, p = it - t * P;
+    ActRec a;
+    int has = 0;
+    const int pid = M.s.pts[p];
+    const int vis = gather_one(M, fc, M.s.geo[p], pid, M.s.targets[t], &a, &has);
+    if (vis) atomicAdd(&M.visible[pid], 1);
+    M.s.act_flag[it] = has;
+    if (has) M.s.acts[M.s.act_cap - TP + it] = a;  // park in the tail, compact below
+  }
+  __syncthreads();
+  int nact = 0;
+  for (int b0 = 0; b0 < TP; b0 += 1024) {
+    const int it = b0 + threadIdx.x;
+    const int f = it < TP ? M.s.act_flag[it] : 0;
+    ActRec a;
+    if (f) a = M.s.acts[M.s.act_cap - TP + it];
+    int tot;
+    const int at = block_excl_scan<1024>(f, sh, tot);
+    __syncthreads();
+    if (f) M.s.acts[nact + at] = a;
+    nact += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int c[3] = {0, 0, 0};
+    apply_actions(M, M.s.acts, nact, c);
+    cnt[0] += c[0];
+    cnt[1] += c[1];
+    cnt[2] += c[2];
+  }
+  __syncthreads();
+  // reverse: per target, its bound points into the current keyframe, gather then apply
+  for (int t = 0; t < T; ++t) {
+    refresh_dirty<1024>(M);
+    const int ts = M.s.targets[t];
+    const int Pt = bound_points<1024>(M, ts, sh);
+    if (threadIdx.x == 0) {
+      M.ledger[LG_NAIVE] += (unsigned long long)Pt * mpb;
+      M.ledger[LG_PERSIST] += (unsigned long long)Pt * mpb;
+      M.ledger[LG_SMALL_FUSE] += (unsigned long long)Pt * mpb;
+      M.ledger[LG_SMALL_EVENTS] += 1;
+    }
+    const int na = gather_pass<1024>(M, fc, Pt, cur, true, sh, nullptr);
+    if (threadIdx.x == 0) {
+      int c[3] = {0, 0, 0};
+      apply_actions(M, M.s.acts, na, c);
+      cnt[0] += c[0];
+      cnt[1] += c[1];
+      cnt[2] += c[2];
+    }
+    __syncthreads();
+  }
+  refresh_dirty<1024>(M);
+  if (threadIdx.x == 0) {
+    st->n_targets = T;
+    st->merged = cnt[0];
+    st->observations_added = cnt[1];
+    st->stale = cnt[2];
+  }
+}
+
+}  // namespace lm

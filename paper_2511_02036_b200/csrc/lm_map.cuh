@@ -1,0 +1,350 @@
+// lm_map.cuh -- device-resident map store and its mutation primitives.
+//
+// Layout (all arenas allocated once per map, SoA, indexed by keyframe slot / global
+// keypoint index / map point id):
+//   keyframes  kf_id, state, kp_off, kp_n, q[4], R[9], t[3], C[3], P[12], cam[6], cell grid
+//   keypoints  u, v (f64), level (u8), desc (2 x uint4), binding (i32, -1 = unbound)
+//   points     pos[3] (f64), rep (2 x uint4), alive, found, visible, first_kf,
+//              observation list (slot, kp) in an 8-byte pool, sorted by keyframe id,
+//              per-level counters counts[id*L + level]
+//   covis      dense int32 [kf_cap x kf_cap], symmetric
+//
+// The primitives restate MapModel's bookkeeping (pkg/src/localmap/mapmodel.py):
+//   link        _record_obs 150-155        unlink_at   _unrecord_obs 157-163
+//   kill_point  kill_map_point 233-237     replace     replace_map_point 245-267
+//   merge_pair  fusion._merge 295-304      refresh     _refresh_rep_descriptor 165-181
+// Covisibility updates are atomicAdd (commutative, order-free); everything else is
+// single-writer per entity. The representative descriptor is refreshed lazily: the
+// reference recomputes it after every observation change, but it is a pure function of
+// the observation list and is only read by the fusion gather and by export, so
+// mutations mark the point dirty and `refresh_dirty` recomputes it before those reads.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lm_b200.h"
+
+namespace lm {
+
+constexpr int NMAX = LM_MAX_NEIGHBORS;  // neighbours per triangulation step
+constexpr int TMAX = LM_MAX_TARGETS;    // fusion targets per keyframe
+constexpr int LMAX = 16;                // pyramid levels
+constexpr int GRID_CELLS = 4096;        // cells per keyframe grid
+constexpr int REFRESH_MAXN = 512;       // observations handled by the rep-refresh fast path
+constexpr int MATCH_TILE = 128;         // current keypoints per match CTA
+constexpr int MATCH_JT = 256;           // neighbour descriptors staged per smem tile
+
+enum KfState { KF_FREE = 0, KF_STAGED = 1, KF_LIVE = 2, KF_DEAD = 3 };
+enum Scal { SC_NEXT_ID = 0, SC_OBS_HEAD, SC_RECENT_N, SC_ERR, SC_DIRTY_N, SC_N = 8 };
+enum LedgerIdx { LG_PERSIST = 0, LG_NAIVE, LG_SMALL_TRI, LG_SMALL_FUSE, LG_SMALL_EVENTS, LG_EVICT, LG_N = 8 };
+enum CandStatus { CS_PASS = 0, CS_PARALLAX = 1, CS_DEPTH = 2, CS_REPROJ = 3, CS_SCALE = 4, CS_DEGEN = 5 };
+
+struct ActRec {  // gathered fusion action (device form)
+  int slot;      // target keyframe slot
+  int pid;       // projected point
+  int j;         // keypoint hit
+  int other;     // existing point (MERGE) or -1
+  int kind;      // LM_ACT_ADD / LM_ACT_MERGE
+};
+
+struct PGeo {  // _point_geometry row (fusion.py:57-94)
+  double x, y, z, blo, bhi, d0, vx, vy, vz;
+  uint4 r0, r1;
+  int ok;
+};
+
+// per-step scratch of one map
+struct Scratch {
+  // triangulation
+  int n_nbr;
+  int* nbr;              // [NMAX] slots
+  int* deg;              // [NMAX]
+  double* F;             // [NMAX*9]
+  int* cur_sorted;       // [kpkf_max]
+  int* cur_bucket;       // [LMAX+1]
+  int* tiles;            // [(kpkf_max/MATCH_TILE + LMAX) * 3] level,start,count
+  int* n_tiles;          // [1]
+  int* nb_n;             // [NMAX]
+  int* nb_bucket;        // [NMAX*(LMAX+1)]
+  int* nb_j;             // [NMAX*kpkf_max]
+  uint4* nb_desc;        // [NMAX*kpkf_max*2]
+  double* nb_u;          // [NMAX*kpkf_max]
+  double* nb_v;
+  double* nb_thr;
+  unsigned long long* pick;   // [NMAX*kpkf_max] (dist<<32 | j)
+  unsigned long long* bestj;  // [NMAX*kpkf_max] (dist<<32 | i)
+  int* cand_n;           // [NMAX]
+  int* cand_i;           // [NMAX*kpkf_max]
+  int* cand_j;
+  int* cand_d;
+  int* cand_st;
+  double* cand_X;        // [NMAX*kpkf_max*3]
+  int* win_rank;         // [kpkf_max]
+  unsigned char* mask_cur;  // optional explicit unbound masks (lm_search)
+  unsigned char* mask_nbr;
+  // fusion
+  int* targets;          // [TMAX]
+  int* n_targets;        // [1]
+  int* rank_buf;         // [TMAX * kf_cap] second-order walk scratch
+  int* pts;              // [max(kpkf_max, pts_cap)] point list of the current pass
+  PGeo* geo;             // [pts_cap]
+  ActRec* acts;          // [TMAX*kpkf_max]
+  int* act_flag;         // [TMAX*kpkf_max]
+  int* vis_flag;         // [TMAX*kpkf_max]
+  int pts_cap;
+  int act_cap;
+  lm_step_stats* stats;  // [1]
+};
+
+struct DevMap {
+  int kf_cap, kp_cap, kpkf_max, mp_cap, obs_cap, L, min_w, min_obs_keep, recent_cap;
+  int kp_rec_bytes, desc_bytes, mp_rec_bytes;
+  double sf, log_sf;
+  double S[LMAX], S2[LMAX];
+  // keyframes
+  long long* kf_id;
+  int* kf_state;
+  int* kp_off;
+  int* kp_n;
+  double* q;
+  double* R;
+  double* t;
+  double* C;
+  double* P;
+  double* cam;
+  double* g_cs;
+  int* g_nx;
+  int* g_ny;
+  int* cell_start;  // [kf_cap*(GRID_CELLS+1)]
+  int* cell_items;  // [kp_cap] global keypoint index
+  // keypoints
+  double* ku;
+  double* kv;
+  unsigned char* klev;
+  uint4* kdesc;
+  int* kbind;
+  // points
+  double* pos;
+  uint4* rep;
+  unsigned char* alive;
+  int* found;
+  int* visible;
+  long long* first_kf;
+  int* nobs;
+  int* ocap;
+  int* ooff;
+  int2* obs;
+  int* counts;
+  int* dirty;
+  int* dirty_list;
+  // covisibility
+  int* covis;
+  // probation list (culling.RecentPoint)
+  int* recent_id;
+  int* recent_born;
+  // scalars
+  int* scal;
+  unsigned long long* ledger;
+  Scratch s;
+};
+
+__device__ __forceinline__ void set_err(const DevMap& M, int code) { atomicCAS(&M.scal[SC_ERR], 0, code); }
+
+__device__ __forceinline__ int hamming(uint4 a0, uint4 a1, uint4 b0, uint4 b1) {
+  return __popc(a0.x ^ b0.x) + __popc(a0.y ^ b0.y) + __popc(a0.z ^ b0.z) + __popc(a0.w ^ b0.w) +
+         __popc(a1.x ^ b1.x) + __popc(a1.y ^ b1.y) + __popc(a1.z ^ b1.z) + __popc(a1.w ^ b1.w);
+}
+
+__device__ __forceinline__ void covis_add(const DevMap& M, int a, int b, int d) {
+  if (a == b) return;
+  atomicAdd(&M.covis[(size_t)a * M.kf_cap + b], d);
+  atomicAdd(&M.covis[(size_t)b * M.kf_cap + a], d);
+}
+
+__device__ __forceinline__ int obs_find(const DevMap& M, int mp, int slot) {
+  const int2* o = M.obs + M.ooff[mp];
+  const int n = M.nobs[mp];
+  for (int k = 0; k < n; ++k)
+    if (o[k].x == slot) return k;
+  return -1;
+}
+
+// insert (slot, kp) keeping the list ordered by keyframe id; grows by doubling
+__device__ bool obs_insert(const DevMap& M, int mp, int slot, int kp) {
+  const int n = M.nobs[mp];
+  if (n == M.ocap[mp]) {
+    const int nc = M.ocap[mp] < 4 ? 4 : 2 * M.ocap[mp];
+    const int off = atomicAdd(&M.scal[SC_OBS_HEAD], nc);
+    if (off + nc > M.obs_cap) {
+      set_err(M, LM_ERR_CAPACITY);
+      return false;
+    }
+    const int2* src = M.obs + M.ooff[mp];
+    for (int k = 0; k < n; ++k) M.obs[off + k] = src[k];
+    M.ooff[mp] = off;
+    M.ocap[mp] = nc;
+  }
+  int2* o = M.obs + M.ooff[mp];
+  const long long kid = M.kf_id[slot];
+  int k = n;
+  while (k > 0 && M.kf_id[o[k - 1].x] > kid) {
+    o[k] = o[k - 1];
+    --k;
+  }
+  o[k] = make_int2(slot, kp);
+  M.nobs[mp] = n + 1;
+  return true;
+}
+
+__device__ __forceinline__ void mark_dirty(const DevMap& M, int mp) {
+  if (atomicExch(&M.dirty[mp], 1) == 0) {
+    const int at = atomicAdd(&M.scal[SC_DIRTY_N], 1);
+    M.dirty_list[at] = mp;
+  }
+}
+
+// _record_obs: covis +1 with every current observer, bind the slot, count the level
+__device__ void link(const DevMap& M, int mp, int slot, int kp) {
+  const int2* o = M.obs + M.ooff[mp];
+  const int n = M.nobs[mp];
+  for (int k = 0; k < n; ++k) covis_add(M, slot, o[k].x, +1);
+  if (!obs_insert(M, mp, slot, kp)) return;
+  const int g = M.kp_off[slot] + kp;
+  M.kbind[g] = mp;
+  M.counts[(size_t)mp * M.L + M.klev[g]] += 1;
+}
+
+// _unrecord_obs of list entry k: unbind, uncount, covis -1 with every remaining observer
+__device__ void unlink_at(const DevMap& M, int mp, int k) {
+  int2* o = M.obs + M.ooff[mp];
+  const int2 e = o[k];
+  const int n = M.nobs[mp] - 1;
+  for (int m = k; m < n; ++m) o[m] = o[m + 1];
+  M.nobs[mp] = n;
+  const int g = M.kp_off[e.x] + e.y;
+  M.kbind[g] = -1;
+  M.counts[(size_t)mp * M.L + M.klev[g]] -= 1;
+  for (int m = 0; m < n; ++m) covis_add(M, e.x, o[m].x, -1);
+}
+
+__device__ void kill_point(const DevMap& M, int mp) {
+  while (M.nobs[mp] > 0) unlink_at(M, mp, 0);
+  M.alive[mp] = 0;
+}
+
+// replace_map_point(loser, winner); returns migrated observation count
+__device__ int replace_point(const DevMap& M, int loser, int winner) {
+  int migrated = 0;
+  while (M.nobs[loser] > 0) {
+    const int2 e = M.obs[M.ooff[loser]];
+    unlink_at(M, loser, 0);
+    if (obs_find(M, winner, e.x) >= 0) continue;  // winner sees this keyframe: slot stays unbound
+    link(M, winner, e.x, e.y);
+    ++migrated;
+  }
+  M.found[winner] += M.found[loser];
+  M.visible[winner] += M.visible[loser];
+  M.alive[loser] = 0;
+  mark_dirty(M, winner);
+  return migrated;
+}
+
+// fusion._merge: more observations wins, ties lose the higher id; winner found += 1
+__device__ void merge_pair(const DevMap& M, int a, int b) {
+  const int na = M.nobs[a], nb = M.nobs[b];
+  int loser, winner;
+  if (na == nb) {
+    loser = a > b ? a : b;
+    winner = a > b ? b : a;
+  } else if (na < nb) {
+    loser = a;
+    winner = b;
+  } else {
+    loser = b;
+    winner = a;
+  }
+  replace_point(M, loser, winner);
+  M.found[winner] += 1;
+}
+
+// k-th smallest of d[0..n) (quickselect, d is scratch)
+__device__ int kth_smallest(unsigned short* d, int n, int k) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const unsigned short pivot = d[(lo + hi) >> 1];
+    int i = lo, j = hi;
+    while (i <= j) {
+      while (d[i] < pivot) ++i;
+      while (d[j] > pivot) --j;
+      if (i <= j) {
+        const unsigned short tmp = d[i];
+        d[i] = d[j];
+        d[j] = tmp;
+        ++i;
+        --j;
+      }
+    }
+    if (k <= j)
+      hi = j;
+    else if (k >= i)
+      lo = i;
+    else
+      return d[k];
+  }
+  return d[k];
+}
+
+// _refresh_rep_descriptor, one warp per point: the observing descriptor whose median
+// Hamming distance to the others is smallest (first in (kf id) order wins). The median of
+// the n-1 integer distances is compared as the sum of the two middle order statistics,
+// which orders exactly like the reference's float nanmedian.
+__device__ void refresh_rep_warp(const DevMap& M, int mp, int lane) {
+  const int n = M.nobs[mp];
+  if (n == 0) return;
+  const int2* o = M.obs + M.ooff[mp];
+  if (n <= 2) {  // one observation, or two (equal medians -> the first)
+    if (lane == 0) {
+      const int g = M.kp_off[o[0].x] + o[0].y;
+      M.rep[2 * mp] = M.kdesc[2 * g];
+      M.rep[2 * mp + 1] = M.kdesc[2 * g + 1];
+    }
+    return;
+  }
+  if (n > REFRESH_MAXN) {
+    if (lane == 0) set_err(M, LM_ERR_CAPACITY);
+    return;
+  }
+  unsigned short d[REFRESH_MAXN];
+  const int m = n - 1, k0 = (m - 1) >> 1, k1 = m >> 1;
+  unsigned best = 0xffffffffu;  // (med2 << 16) | row
+  for (int a = lane; a < n; a += 32) {
+    const int ga = M.kp_off[o[a].x] + o[a].y;
+    const uint4 a0 = M.kdesc[2 * ga], a1 = M.kdesc[2 * ga + 1];
+    int c = 0;
+    for (int b = 0; b < n; ++b) {
+      if (b == a) continue;
+      const int gb = M.kp_off[o[b].x] + o[b].y;
+      d[c++] = (unsigned short)hamming(a0, a1, M.kdesc[2 * gb], M.kdesc[2 * gb + 1]);
+    }
+    const int v0 = kth_smallest(d, m, k0);
+    int v1 = v0;
+    if (k1 != k0) {  // next order statistic: min of the upper partition
+      v1 = 0x7fffffff;
+      for (int b = k0 + 1; b < m; ++b) v1 = d[b] < v1 ? d[b] : v1;
+    }
+    const unsigned key = ((unsigned)(v0 + v1) << 16) | (unsigned)a;
+    best = key < best ? key : best;
+  }
+  for (int off = 16; off; off >>= 1) {
+    const unsigned other = __shfl_xor_sync(0xffffffffu, best, off);
+    best = other < best ? other : best;
+  }
+  if (lane == 0) {
+    const int a = best & 0xffff;
+    const int g = M.kp_off[o[a].x] + o[a].y;
+    M.rep[2 * mp] = M.kdesc[2 * g];
+    M.rep[2 * mp + 1] = M.kdesc[2 * g + 1];
+  }
+}
+
+}  // namespace lm

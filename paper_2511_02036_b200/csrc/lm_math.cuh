@@ -1,0 +1,269 @@
+// lm_math.cuh -- fp64 geometry of the hot path, compiled for both host and sm_100a.
+//
+// Every expression is evaluated in the reference's IEEE order (NumPy evaluates
+// elementwise, left to right, one rounding per op). Device code is built with
+// --fmad=false and host code with -ffp-contract=off, so `a*b + c` is two roundings
+// everywhere; fma() is used only where the reference itself fuses: NumPy's 3x3 matmuls
+// go through OpenBLAS dgemm, whose small-matrix kernel accumulates
+// c = fma(a2,b2, fma(a1,b1, a0*b0)) (verified bit-exact in tests/test_host_math.py).
+//
+// Known non-bitwise points (all "borderline-flip" class, counted by the parity tests):
+//   * scalar `x ** 2` in the reference is libm pow(x, 2); here x*x (IEEE exact rounding).
+//   * the DLT null vector: LAPACK dgesdd there, one-sided Jacobi here (1e-4 rel contract).
+//   * np.log in the fusion level prediction vs CUDA log (both <= 1 ulp).
+// Reference provenance (pkg/src/localmap/geometry.py): quat->R 65-76, center 99-103,
+// transform 91-97, fundamental 287-304, epipolar 307-322, triangulate 258-284,
+// parallax 341-353, gates 407-459, projection 237-246.
+#pragma once
+#include <math.h>
+#include <stdint.h>
+
+#ifdef __CUDACC__
+#define LM_HD __host__ __device__ __forceinline__
+#else
+#define LM_HD inline
+#endif
+
+namespace lm {
+
+constexpr double kBaselineEps = 1e-9;
+constexpr double kHomogEps = 1e-12;
+
+// rotation matrix (row-major) of a unit quaternion (x, y, z, w)
+LM_HD void quat_to_rot(const double q[4], double R[9]) {
+  const double x = q[0], y = q[1], z = q[2], w = q[3];
+  const double xx = x * x, yy = y * y, zz = z * z;
+  const double xy = x * y, xz = x * z, yz = y * z;
+  const double wx = w * x, wy = w * y, wz = w * z;
+  R[0] = 1.0 - 2.0 * (yy + zz); R[1] = 2.0 * (xy - wz);       R[2] = 2.0 * (xz + wy);
+  R[3] = 2.0 * (xy + wz);       R[4] = 1.0 - 2.0 * (xx + zz); R[5] = 2.0 * (yz - wx);
+  R[6] = 2.0 * (xz - wy);       R[7] = 2.0 * (yz + wx);       R[8] = 1.0 - 2.0 * (xx + yy);
+}
+
+// out = R p, each row a left-to-right dot product
+LM_HD void rot_apply(const double R[9], double x, double y, double z, double out[3]) {
+  out[0] = R[0] * x + R[1] * y + R[2] * z;
+  out[1] = R[3] * x + R[4] * y + R[5] * z;
+  out[2] = R[6] * x + R[7] * y + R[8] * z;
+}
+
+// out = R^T p
+LM_HD void rot_apply_t(const double R[9], double x, double y, double z, double out[3]) {
+  out[0] = R[0] * x + R[3] * y + R[6] * z;
+  out[1] = R[1] * x + R[4] * y + R[7] * z;
+  out[2] = R[2] * x + R[5] * y + R[8] * z;
+}
+
+// SE3Pose.__post_init__ normalisation: q / |q|, canonical hemisphere w >= 0
+LM_HD void quat_canon(double q[4]) {
+  const double n = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  q[0] = q[0] / n; q[1] = q[1] / n; q[2] = q[2] / n; q[3] = q[3] / n;
+  if (q[3] < 0) { q[0] = -q[0]; q[1] = -q[1]; q[2] = -q[2]; q[3] = -q[3]; }
+}
+
+LM_HD void camera_center(const double R[9], const double t[3], double C[3]) {
+  double c[3];
+  rot_apply_t(R, t[0], t[1], t[2], c);
+  C[0] = -c[0]; C[1] = -c[1]; C[2] = -c[2];
+}
+
+// C = A B for 3x3 row-major, OpenBLAS small-kernel accumulation order
+LM_HD void mat3_mul(const double* A, const double* B, double* C) {
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      C[i * 3 + j] = fma(A[i * 3 + 2], B[6 + j], fma(A[i * 3 + 1], B[3 + j], A[i * 3] * B[j]));
+}
+
+// inverse of K = [[fx,0,cx],[0,fy,cy],[0,0,1]] as numpy.linalg.inv (LAPACK gesv) returns it:
+// diagonal reciprocals, off-diagonal -c * (1/f)
+LM_HD void kinv(double fx, double fy, double cx, double cy, double Ki[9]) {
+  const double rx = 1.0 / fx, ry = 1.0 / fy;
+  Ki[0] = rx;  Ki[1] = 0.0; Ki[2] = -cx * rx;
+  Ki[3] = 0.0; Ki[4] = ry;  Ki[5] = -cy * ry;
+  Ki[6] = 0.0; Ki[7] = 0.0; Ki[8] = 1.0;
+}
+
+// P = K [R | t] (3x4 row-major), same dgemm accumulation as mat3_mul
+LM_HD void proj_matrix(double fx, double fy, double cx, double cy, const double R[9], const double t[3],
+                       double P[12]) {
+  const double K[9] = {fx, 0.0, cx, 0.0, fy, cy, 0.0, 0.0, 1.0};
+  double M[12];
+  for (int i = 0; i < 3; ++i) {
+    M[i * 4 + 0] = R[i * 3 + 0]; M[i * 4 + 1] = R[i * 3 + 1]; M[i * 4 + 2] = R[i * 3 + 2];
+    M[i * 4 + 3] = t[i];
+  }
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 4; ++j)
+      P[i * 4 + j] = fma(K[i * 3 + 2], M[8 + j], fma(K[i * 3 + 1], M[4 + j], K[i * 3] * M[j]));
+}
+
+// F mapping pixels of view a to epipolar lines of view b (geometry.py:287-304).
+// Returns false for a zero baseline (|t_rel| < 1e-9), the reference's DegenerateGeometryError.
+LM_HD bool fundamental(const double qa[4], const double ta[3], const double qb[4], const double tb[3],
+                       const double cam_a[4], const double cam_b[4], double F[9]) {
+  double Ra[9], Rb[9];
+  quat_to_rot(qa, Ra);
+  quat_to_rot(qb, Rb);
+  // a.inverse()
+  double ai[3];
+  rot_apply_t(Ra, ta[0], ta[1], ta[2], ai);
+  double qi[4] = {-qa[0], -qa[1], -qa[2], qa[3]};
+  quat_canon(qi);
+  const double ti[3] = {-ai[0], -ai[1], -ai[2]};
+  // b.compose(a_inv)
+  const double bx = qb[0], by = qb[1], bz = qb[2], bw = qb[3];
+  const double ix = qi[0], iy = qi[1], iz = qi[2], iw = qi[3];
+  double qr[4] = {bw * ix + bx * iw + by * iz - bz * iy, bw * iy - bx * iz + by * iw + bz * ix,
+                  bw * iz + bx * iy - by * ix + bz * iw, bw * iw - bx * ix - by * iy - bz * iz};
+  quat_canon(qr);
+  double rt[3];
+  rot_apply(Rb, ti[0], ti[1], ti[2], rt);
+  const double t[3] = {rt[0] + tb[0], rt[1] + tb[1], rt[2] + tb[2]};
+  if (sqrt(t[0] * t[0] + t[1] * t[1] + t[2] * t[2]) < kBaselineEps) return false;
+  const double S[9] = {0.0, -t[2], t[1], t[2], 0.0, -t[0], -t[1], t[0], 0.0};
+  double Rr[9], E[9], KbT[9], Ka[9], Kb[9], X[9];
+  quat_to_rot(qr, Rr);
+  mat3_mul(S, Rr, E);
+  kinv(cam_b[0], cam_b[1], cam_b[2], cam_b[3], Kb);
+  kinv(cam_a[0], cam_a[1], cam_a[2], cam_a[3], Ka);
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) KbT[i * 3 + j] = Kb[j * 3 + i];
+  mat3_mul(KbT, E, X);
+  mat3_mul(X, Ka, F);
+  return true;
+}
+
+// epipolar line of pixel (u, v): l = F [u v 1]^T
+LM_HD void epi_line(const double F[9], double u, double v, double l[3]) {
+  l[0] = F[0] * u + F[1] * v + F[2];
+  l[1] = F[3] * u + F[4] * v + F[5];
+  l[2] = F[6] * u + F[7] * v + F[8];
+}
+
+// squared pixel distance of (u, v) to line l, den = l0^2 + l1^2 precomputed; inf if den <= 0
+LM_HD double epi_d2(const double l[3], double den, double u, double v) {
+  double num = l[0] * u + l[1] * v + l[2];
+  num = num * num;
+  return den > 0 ? num / den : INFINITY;
+}
+
+// Smallest right singular vector of a 4x4 matrix by one-sided (Hestenes) Jacobi.
+// A is row-major and is overwritten. Returns the unit null vector in v.
+LM_HD void null_vector4(double A[16], double v[4]) {
+  double V[16] = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1};
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    bool rotated = false;
+    for (int p = 0; p < 3; ++p) {
+      for (int q = p + 1; q < 4; ++q) {
+        double alpha = 0, beta = 0, gamma = 0;
+        for (int k = 0; k < 4; ++k) {
+          const double ap = A[k * 4 + p], aq = A[k * 4 + q];
+          alpha += ap * ap;
+          beta += aq * aq;
+          gamma += ap * aq;
+        }
+        if (gamma == 0.0 || fabs(gamma) <= 1e-17 * sqrt(alpha * beta)) continue;
+        rotated = true;
+        const double zeta = (beta - alpha) / (2.0 * gamma);
+        const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + tt * tt);
+        const double s = c * tt;
+        for (int k = 0; k < 4; ++k) {
+          const double ap = A[k * 4 + p], aq = A[k * 4 + q];
+          A[k * 4 + p] = c * ap - s * aq;
+          A[k * 4 + q] = s * ap + c * aq;
+          const double vp = V[k * 4 + p], vq = V[k * 4 + q];
+          V[k * 4 + p] = c * vp - s * vq;
+          V[k * 4 + q] = s * vp + c * vq;
+        }
+      }
+    }
+    if (!rotated) break;
+  }
+  int best = 0;
+  double bn = INFINITY;
+  for (int j = 0; j < 4; ++j) {
+    double n = 0;
+    for (int k = 0; k < 4; ++k) n += A[k * 4 + j] * A[k * 4 + j];
+    if (n < bn) { bn = n; best = j; }
+  }
+  double nv = 0;
+  for (int k = 0; k < 4; ++k) nv += V[k * 4 + best] * V[k * 4 + best];
+  nv = sqrt(nv);
+  for (int k = 0; k < 4; ++k) v[k] = V[k * 4 + best] / nv;
+}
+
+// Two-view DLT (geometry.py:258-284). Pa/Pb are K[R|t]; Ca/Cb camera centres.
+// Returns false when degenerate (baseline < 1e-9 or point at infinity).
+LM_HD bool triangulate(const double Pa[12], const double Pb[12], const double Ca[3], const double Cb[3],
+                       double ua, double va, double ub, double vb, double X[3]) {
+  const double dx = Ca[0] - Cb[0], dy = Ca[1] - Cb[1], dz = Ca[2] - Cb[2];
+  if (sqrt(dx * dx + dy * dy + dz * dz) < kBaselineEps) return false;
+  double A[16];
+  for (int j = 0; j < 4; ++j) {
+    A[0 + j] = ua * Pa[8 + j] - Pa[0 + j];
+    A[4 + j] = va * Pa[8 + j] - Pa[4 + j];
+    A[8 + j] = ub * Pb[8 + j] - Pb[0 + j];
+    A[12 + j] = vb * Pb[8 + j] - Pb[4 + j];
+  }
+  double h[4];
+  null_vector4(A, h);
+  if (fabs(h[3]) < kHomogEps) return false;
+  X[0] = h[0] / h[3];
+  X[1] = h[1] / h[3];
+  X[2] = h[2] / h[3];
+  return true;
+}
+
+enum GateCode : int { kGatePass = 0, kGateParallax = 1, kGateDepth = 2, kGateReproj = 3, kGateScale = 4,
+                      kDegenerate = 5 };
+
+struct ViewGeo {
+  const double* R;  // 9
+  const double* t;  // 3
+  const double* C;  // 3
+  double fx, fy, cx, cy;
+  double u, v;      // observed pixel
+  double sigma2;    // sf^(2*level)
+  double scale;     // sf^level
+  double sf;        // pyramid scale factor
+};
+
+// check_creation_gates (geometry.py:407-459), first failing gate wins
+LM_HD int creation_gates(const ViewGeo& a, const ViewGeo& b, const double X[3], double cos_max, double chi2_mono,
+                         double slack) {
+  const double ra0 = X[0] - a.C[0], ra1 = X[1] - a.C[1], ra2 = X[2] - a.C[2];
+  const double rb0 = X[0] - b.C[0], rb1 = X[1] - b.C[1], rb2 = X[2] - b.C[2];
+  const double na = sqrt(ra0 * ra0 + ra1 * ra1 + ra2 * ra2);
+  const double nb = sqrt(rb0 * rb0 + rb1 * rb1 + rb2 * rb2);
+  if (na < kHomogEps || nb < kHomogEps) return kGateParallax;
+  double c = (ra0 * rb0 + ra1 * rb1 + ra2 * rb2) / (na * nb);
+  c = c > 1.0 ? 1.0 : (c < -1.0 ? -1.0 : c);
+  if (!(c < cos_max)) return kGateParallax;
+  double pa[3], pb[3];
+  rot_apply(a.R, X[0], X[1], X[2], pa);
+  pa[0] = pa[0] + a.t[0]; pa[1] = pa[1] + a.t[1]; pa[2] = pa[2] + a.t[2];
+  rot_apply(b.R, X[0], X[1], X[2], pb);
+  pb[0] = pb[0] + b.t[0]; pb[1] = pb[1] + b.t[1]; pb[2] = pb[2] + b.t[2];
+  if (pa[2] <= 0 || pb[2] <= 0) return kGateDepth;
+  {
+    const double u = a.fx * (pa[0] / pa[2]) + a.cx, v = a.fy * (pa[1] / pa[2]) + a.cy;
+    const double eu = u - a.u, ev = v - a.v;
+    if (eu * eu + ev * ev > chi2_mono * a.sigma2) return kGateReproj;
+  }
+  {
+    const double u = b.fx * (pb[0] / pb[2]) + b.cx, v = b.fy * (pb[1] / pb[2]) + b.cy;
+    const double eu = u - b.u, ev = v - b.v;
+    if (eu * eu + ev * ev > chi2_mono * b.sigma2) return kGateReproj;
+  }
+  const double da = sqrt(ra0 * ra0 + ra1 * ra1 + ra2 * ra2);
+  const double db = sqrt(rb0 * rb0 + rb1 * rb1 + rb2 * rb2);
+  if (da < kHomogEps || db < kHomogEps) return kGateScale;
+  const double rd = da / db;
+  const double rs = a.scale / b.scale;
+  const double sl = slack * (a.sf > b.sf ? a.sf : b.sf);
+  if (!(rs / sl <= rd && rd <= rs * sl)) return kGateScale;
+  return kGatePass;
+}
+
+}  // namespace lm
