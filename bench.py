@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""Benchmark: keyframes/sec of triangulate+fuse (CreateNewMapPoints + SearchAndFuse) on the
+EuRoC-shaped synthetic sequence (BASELINE.json configs[1]: 752x480, 1200 features/KF,
+20 covisible neighbours, 200 keyframes), per B200, vs the CPU oracle on the host cores.
+
+One *step* = the whole 200-keyframe sequence from an empty map: per keyframe insert,
+recent map-point cull, CreateNewMapPoints, SearchAndFuse (LBA and keyframe culling are out
+of scope and force-skipped, as in the reference's throughput benches).
+
+  value  device-resident inputs (keyframes staged once, the map rewound between steps),
+         CUDA events on the library's stream around each step, L2 flushed between steps.
+  e2e    the same metric through the C-ABI with host buffers: every step stages each
+         keyframe from host memory (pinned staging + H2D inside the timed region) and
+         reads its step statistics back (D2H), wall-clock.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload c2]
+Multi-GPU (torchrun): one process per GPU, each rank runs its own independent session
+(seed offset by rank; weak scaling, no collective on the data path); the per-step time is
+the max over ranks (all_reduce MAX on a 1-element tensor).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_2511_02036_b200 import workload as W  # noqa: E402
+from paper_2511_02036_b200.config import FuseConfig, MatchConfig  # noqa: E402
+
+METRIC = "keyframes/sec (triangulate+fuse) and ms/keyframe at 1/2/4/8 B200 vs host CPU"
+UNIT = "keyframes/s"
+L2_FLUSH_BYTES = 512 << 20
+
+
+def load_workload(name: str, seed: int | None):
+    cfg = W.bench_world(name, seed)
+    return W.generate_sequence(cfg)
+
+
+def stage_params(name):
+    n, n1, n2 = W.BENCH_STAGE[name]
+    return n, MatchConfig(neighbor_count=n), FuseConfig(n1=n1, n2=n2)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary, if any."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        return d.get(kernel, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_sample(seq, name, budget_s: float):
+    """Oracle (NumPy port of the reference path) on the host: keyframes 0.. until budget."""
+    from oracle import lm_oracle as O
+
+    n, mc, fc = stage_params(name)
+    c = seq.config
+    cam = O.Cam(c.fx, c.fy, c.cx, c.cy, c.width, c.height, c.num_levels, c.scale_factor)
+    pipe = O.OraclePipeline(c.num_levels, n, fc=O.FuseCfg(n1=fc.n1, n2=fc.n2))
+    t0 = time.perf_counter()
+    done = 0
+    for rec in seq.records:
+        pipe.step(O.okf_from_record(rec, cam))
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return done, dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    seq = load_workload(args.workload, None)
+    sample_kfs = args.ref_kfs
+    from oracle import lm_oracle as O  # noqa: F401
+
+    times = []
+    for step in range(args.warmup + args.steps):
+        seq_k = seq
+        t0 = time.perf_counter()
+        done, dt = cpu_sample(seq_k, args.workload, budget_s=1e9 if sample_kfs else args.ref_budget)
+        times.append((done, dt))
+    timed = times[args.warmup:]
+    kfs = sum(d for d, _ in timed)
+    secs = sum(t for _, t in timed)
+    v = kfs / secs
+    sample = f"oracle port, keyframes 0..{timed[0][0] - 1} of {args.workload} from an empty map per step"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / len(timed),
+            "ms_per_keyframe": 1e3 * secs / kfs, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32 popc / f64 geometry", "data": "synthetic",
+            "config": config_of(args), "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+                                                       "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_of(args, seq=None):
+    n, mc, fc = stage_params(args.workload)
+    c = W.BENCH_CONFIGS[args.workload]
+    return {"workload": f"{args.workload}: EuRoC-shaped synthetic sequence" if args.workload == "c2" else args.workload,
+            "keyframes": c["keyframe_count"] if args.kfs is None else args.kfs,
+            "features_per_kf": c["features_per_kf"], "image": [c.get("width", 640), c.get("height", 480)],
+            "neighbor_count": n, "fusion_n1": fc.n1, "fusion_n2": fc.n2, "seed": c["seed"],
+            "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write)",
+            "step": "whole sequence from an empty map (insert, recent cull, triangulate, fuse per keyframe)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(W.BENCH_CONFIGS))
+    ap.add_argument("--kfs", type=int, default=None, help="limit keyframes per step (debug)")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--ref-budget", type=float, default=8.0)
+    ap.add_argument("--ref-kfs", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2511_02036_b200 import _lib
+    from paper_2511_02036_b200.session import LocalMapper, store_for
+    from paper_2511_02036_b200.mapmodel import KeyFrame
+
+    seed = W.BENCH_CONFIGS[args.workload]["seed"] + 1000 * rank
+    seq = load_workload(args.workload, seed)
+    recs = seq.records if args.kfs is None else seq.records[:args.kfs]
+    intr = seq.intrinsics()
+    n, mc, fc = stage_params(args.workload)
+    kfs = [KeyFrame(int(r.kf_id), r.pose_init, intr, r.kp_u, r.kp_v, r.kp_level, r.descriptors) for r in recs]
+    ctx = _lib.Context.get(local)
+    lib = ctx.lib
+    mapper = LocalMapper(intr, neighbor_count=n, match=mc, fuse=fc, ctx=ctx,
+                         store=store_for(len(kfs), max(k.num_keypoints for k in kfs) + 64))
+    for kf in kfs:
+        mapper.stage(kf)
+    ids = [kf.kf_id for kf in kfs]
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def one_step(profile: bool) -> float:
+        ctx.call("lm_map_rewind", mapper.map)
+        mapper.processed = 0
+        lib.lm_flush_l2(ctx.h, L2_FLUSH_BYTES)
+        ctx.call("lm_synchronize")
+        barrier()
+        ctx.call("lm_timer_start")
+        for k in ids:
+            mapper.step(k, sync=False)
+        ms = C.c_float()
+        ctx.call("lm_timer_stop", C.byref(ms))
+        return ms.value
+
+    # -------- device-resident timed region (per-stage CUDA events on the library stream)
+    for _ in range(args.warmup):
+        one_step(False)
+    lib.lm_profile_enable(ctx.h, 1)
+    lib.lm_profile_read(ctx.h, (C.c_double * 8)(), (C.c_int64 * 8)())  # drop warm-up events
+    sampler = ClockSampler(local)
+    launches0 = lib.lm_launch_count(ctx.h)
+    step_ms = []
+    totals = _lib.StepStats()
+    for _ in range(args.steps):
+        ms = one_step(True)
+        step_ms.append(max_over_ranks(ms))
+        ctx.call("lm_totals_fetch", mapper.map, C.byref(totals))
+        if totals.error:
+            raise RuntimeError(f"device error {totals.error}")
+    launches = lib.lm_launch_count(ctx.h) - launches0
+    clocks = sampler.stop()
+    prof_ms = (C.c_double * 8)()
+    prof_n = (C.c_int64 * 8)()
+    lib.lm_profile_read(ctx.h, prof_ms, prof_n)
+    lib.lm_profile_enable(ctx.h, 0)
+    stages = ["insert", "cull", "select", "prep", "match", "tri", "commit", "fuse"]
+    stage_ms = {s: prof_ms[k] / args.steps for k, s in enumerate(stages)}
+    mean_ms = sum(step_ms) / len(step_ms)
+    total_kf = len(ids) * world
+    value = total_kf / (mean_ms * 1e-3)
+
+    # -------- end-to-end through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        h2d = sum(k.num_keypoints * (8 + 8 + 32 + 4 + 1) + 208 for k in kfs)
+        d2h = C.sizeof(_lib.StepStats) * len(kfs)
+        e_ms = []
+        for it in range(args.warmup + args.steps):
+            mapper.reset()
+            barrier()
+            t0 = time.perf_counter()
+            for kf in kfs:
+                mapper.process(kf)  # stage (H2D) + step + stats readback (D2H, synchronising)
+            dt = (time.perf_counter() - t0) * 1e3
+            if it >= args.warmup:
+                e_ms.append(max_over_ranks(dt))
+        e2e = {"value": total_kf / (sum(e_ms) / len(e_ms) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": sum(e_ms) / len(e_ms),
+               "timing": "wall clock around stage+step+readback of every keyframe"}
+
+    # -------- roofline of the dominant kernel + the matching kernel's popc roofline
+    peaks = measured_peaks()
+    per_step_bytes = totals.fuse_bytes / args.steps
+    per_step_pairs = totals.match_pairs / args.steps
+    popc_peak = C.c_double()
+    ctx.call("lm_bench_popc", C.byref(popc_peak))
+    dom = max(stage_ms, key=stage_ms.get)
+    fuse_s = stage_ms["fuse"] * 1e-3
+    match_s = stage_ms["match"] * 1e-3
+    hbm_peak = peaks.get("hbm_gbs", 6457.4)
+    fuse_gbs = per_step_bytes / fuse_s / 1e9 if fuse_s > 0 else 0.0
+    roofline = {"kernel": "k_fuse", "bound": "hbm", "achieved": fuse_gbs, "peak": hbm_peak, "unit": "GB/s",
+                "frac": fuse_gbs / hbm_peak, "traffic": ncu_traffic("k_fuse"),
+                "algorithmic_bytes_per_launch": per_step_bytes / len(ids), "launch_ms": stage_ms["fuse"] / len(ids),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback",
+                "dominant_stage": dom}
+    popc_achieved = 8 * per_step_pairs / match_s if match_s > 0 else 0.0
+    roof_popc = {"kernel": "k_match", "bound": "popc", "achieved": popc_achieved / 1e12, "peak": popc_peak.value / 1e12,
+                 "unit": "Tpopc32/s", "frac": popc_achieved / popc_peak.value,
+                 "algorithmic_popc_per_launch": 8 * per_step_pairs / len(ids), "launch_ms": stage_ms["match"] / len(ids),
+                 "peak_source": "lm_bench_popc microbenchmark on this GPU (measured)"}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": mean_ms, "ms_per_keyframe": mean_ms / len(ids),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 popc / f64 geometry",
+            "data": "synthetic (workload.py restatement of the reference generator)", "config": config_of(args),
+            "parallelism": f"{world} independent sessions, one per GPU, no collective on the data path",
+            "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
+            "roofline_popc": roof_popc, "stage_ms_per_step": stage_ms,
+            "work_per_step": {"keyframes": len(ids), "match_pairs": per_step_pairs, "fuse_bytes": per_step_bytes,
+                              "created": totals.created / args.steps, "merged": totals.merged / args.steps,
+                              "observations_added": totals.observations_added / args.steps}}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        done, dt = cpu_sample(seq, args.workload, args.cpu_budget)
+        line["cpu_baseline"] = {"value": done / dt, "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": f"oracle (NumPy port) keyframes 0..{done - 1} of the same sequence, "
+                                          f"from an empty map, {dt:.1f} s"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

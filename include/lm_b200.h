@@ -110,7 +110,10 @@ typedef struct lm_step_stats { /* CreationStats triangulation.py:49-60 + run_fus
   int32_t culled;
   int64_t first_new_id; /* created ids are first_new_id .. first_new_id+created-1 */
   int32_t error;        /* nonzero: a device arena overflowed (lm_status code) */
-  int32_t pad;
+  int32_t n_candidates; /* one-to-one search candidates over all neighbours */
+  int64_t match_pairs;  /* P_elig: (unbound current, unbound level-window neighbour) pairs */
+  int64_t fuse_bytes;   /* algorithmic fusion bytes, SURVEY.md 8(d) formula */
+  int64_t fuse_passes, fuse_points, fuse_actions;
 } lm_step_stats;
 
 typedef struct lm_candidate { /* MatchCandidate triangulation.py:41-46 */
@@ -207,6 +210,23 @@ int lm_export_points(lm_ctx* ctx, int32_t map, int32_t n, double* pos, uint8_t* 
 int lm_export_covis(lm_ctx* ctx, int32_t map, int32_t* w, int32_t cap); /* dense slot x slot */
 int lm_recent_export(lm_ctx* ctx, int32_t map, int64_t* ids, int32_t* born, int32_t cap, int32_t* n_out);
 int lm_recent_import(lm_ctx* ctx, int32_t map, const int64_t* ids, const int32_t* born, int32_t n);
+
+/* ---- measurement ---- */
+/* Rewind a map to "all keyframes staged, nothing inserted": keeps the keyframe pool (no
+ * host transfer) so a sequence can be replayed with device-resident inputs. */
+int lm_map_rewind(lm_ctx* ctx, int32_t map);
+int lm_timer_start(lm_ctx* ctx);                 /* CUDA event on the context stream */
+int lm_timer_stop(lm_ctx* ctx, float* ms);       /* event + synchronize, elapsed since start */
+int lm_flush_l2(lm_ctx* ctx, int64_t bytes);     /* write a scratch buffer larger than L2 */
+int64_t lm_launch_count(lm_ctx* ctx);
+/* Running totals since map creation/reset/rewind (first_new_id holds the step count). */
+int lm_totals_fetch(lm_ctx* ctx, int32_t map, lm_step_stats* out);            /* kernels launched by this context so far */
+/* Per-stage CUDA-event timing of the step kernels (stage order: begin+insert, cull, select,
+ * prep, match, tri, commit, fuse). Enabling adds two events per stage per step. */
+int lm_profile_enable(lm_ctx* ctx, int32_t on);
+int lm_profile_read(lm_ctx* ctx, double ms[8], int64_t launches[8]); /* sums, then clears */
+/* Sustained __popc throughput of this device (popc32 results per second). */
+int lm_bench_popc(lm_ctx* ctx, double* popc_per_s);
 
 /* ---- host-side math, exported for CPU parity tests (no GPU needed) ---- */
 int lm_host_fundamental(const double qa[4], const double ta[3], const double qb[4], const double tb[3],

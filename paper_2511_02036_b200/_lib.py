@@ -68,7 +68,8 @@ class StepStats(C.Structure):
                 ("n_degenerate_neighbors", i32), ("degenerate_neighbors", i64 * MAX_NEIGHBORS),
                 ("n_neighbors", i32), ("neighbors", i64 * MAX_NEIGHBORS), ("n_targets", i32),
                 ("merged", i32), ("observations_added", i32), ("stale", i32), ("culled", i32),
-                ("first_new_id", i64), ("error", i32), ("pad", i32)]
+                ("first_new_id", i64), ("error", i32), ("n_candidates", i32), ("match_pairs", i64),
+                ("fuse_bytes", i64), ("fuse_passes", i64), ("fuse_points", i64), ("fuse_actions", i64)]
 
 
 class Candidate(C.Structure):
@@ -128,6 +129,15 @@ _SIGS = {
     "lm_export_covis": ([C.c_void_p, i32, P(i32), i32], i32),
     "lm_recent_export": ([C.c_void_p, i32, P(i64), P(i32), i32, P(i32)], i32),
     "lm_recent_import": ([C.c_void_p, i32, P(i64), P(i32), i32], i32),
+    "lm_map_rewind": ([C.c_void_p, i32], i32),
+    "lm_timer_start": ([C.c_void_p], i32),
+    "lm_timer_stop": ([C.c_void_p, P(C.c_float)], i32),
+    "lm_flush_l2": ([C.c_void_p, i64], i32),
+    "lm_launch_count": ([C.c_void_p], i64),
+    "lm_totals_fetch": ([C.c_void_p, i32, P(StepStats)], i32),
+    "lm_profile_enable": ([C.c_void_p, i32], i32),
+    "lm_profile_read": ([C.c_void_p, P(f64), P(i64)], i32),
+    "lm_bench_popc": ([C.c_void_p, P(f64)], i32),
     "lm_host_fundamental": ([P(f64), P(f64), P(f64), P(f64), P(f64), P(f64), P(f64)], i32),
     "lm_host_projection": ([P(f64), P(f64), P(f64), P(f64), P(f64), P(f64)], i32),
     "lm_host_triangulate": ([P(f64), P(f64), P(f64), P(f64), P(f64), P(f64)], i32),

@@ -53,6 +53,7 @@ struct lm_ctx {
   std::vector<HostMap*> maps;
   DevMap* d_maps = nullptr;
   int d_maps_cap = 0;
+  lm_step_stats** d_totals = nullptr;  // per map running totals (device pointers)
   StepArgs* h_args = nullptr;  // pinned [kRing * kMaxBatch]
   StepArgs* d_args = nullptr;
   cudaEvent_t args_ev[kRing];
@@ -66,6 +67,13 @@ struct lm_ctx {
   int stage_pos = 0;
   lm_step_stats* h_stats = nullptr;  // pinned [kMaxBatch]
   std::string err;
+  long long launches = 0;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  void* flush_buf = nullptr;
+  size_t flush_bytes = 0;
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_pool;   // free events
+  std::vector<std::vector<cudaEvent_t>> prof_steps;  // 9 boundary events per step
 };
 
 static int fail(lm_ctx* ctx, int code, const char* fmt, ...) {
@@ -123,6 +131,11 @@ static int upload_maps(lm_ctx* ctx) {
   std::vector<DevMap> h(n);
   for (int i = 0; i < n; ++i) h[i] = ctx->maps[i]->d;
   CU(cudaMemcpyAsync(ctx->d_maps, h.data(), sizeof(DevMap) * n, cudaMemcpyHostToDevice, ctx->stream));
+  if (ctx->d_totals) CU(cudaFree(ctx->d_totals));
+  CU(cudaMalloc(&ctx->d_totals, sizeof(lm_step_stats*) * n));
+  std::vector<lm_step_stats*> tp(n);
+  for (int i = 0; i < n; ++i) tp[i] = ctx->maps[i]->d_totals;
+  CU(cudaMemcpyAsync(ctx->d_totals, tp.data(), sizeof(lm_step_stats*) * n, cudaMemcpyHostToDevice, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   return LM_OK;
 }
@@ -387,6 +400,7 @@ static int run_op(lm_ctx* ctx, HostMap* m, int map, OpArgs& a, int* res_host, in
   const size_t dyn = 2 * sizeof(int) * m->d.kf_cap;
   k_op<<<1, 1024, dyn, ctx->stream>>>(ctx->d_maps, map, a, m->d_result);
   CHECK_LAUNCH();
+  ctx->launches += 1;
   CU(cudaMemcpyAsync(res_host, m->d_result, sizeof(int) * nres, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   return LM_OK;
@@ -645,6 +659,7 @@ int lm_kf_stage(lm_ctx* ctx, int32_t map, int64_t kf_id, const double quat[4], c
   CU(cudaMemcpyAsync(ctx->d_stage[b], hb, need, cudaMemcpyHostToDevice, ctx->stream));
   k_stage<<<1, 1024, 0, ctx->stream>>>(d, ctx->d_stage[b]);
   CHECK_LAUNCH();
+  ctx->launches += 1;
   CU(cudaEventRecord(ctx->stage_ev[b], ctx->stream));
   ctx->stage_used[b] = true;
   m->slot_of[kf_id] = slot;
@@ -664,9 +679,33 @@ __global__ void k_begin(DevMap* maps, const StepArgs* args) {
   for (int k = threadIdx.x; k < (int)(sizeof(lm_step_stats) / 4); k += blockDim.x) p[k] = 0;
 }
 
-__global__ void k_end(DevMap* maps, const StepArgs* args) {
+__global__ void k_end(DevMap* maps, const StepArgs* args, lm_step_stats** totals) {
   const DevMap& M = maps[args[blockIdx.x].map];
-  if (threadIdx.x == 0) M.s.stats->error = M.scal[SC_ERR];
+  if (threadIdx.x) return;
+  lm_step_stats* st = M.s.stats;
+  st->error = M.scal[SC_ERR];
+  lm_step_stats* t = totals[args[blockIdx.x].map];
+  t->created += st->created;
+  t->conflicts += st->conflicts;
+  t->degenerate += st->degenerate;
+  t->gate_parallax += st->gate_parallax;
+  t->gate_depth += st->gate_depth;
+  t->gate_reprojection += st->gate_reprojection;
+  t->gate_scale += st->gate_scale;
+  t->n_neighbors += st->n_neighbors;
+  t->n_targets += st->n_targets;
+  t->merged += st->merged;
+  t->observations_added += st->observations_added;
+  t->stale += st->stale;
+  t->culled += st->culled;
+  t->error = st->error;
+  t->n_candidates += st->n_candidates;
+  t->match_pairs += st->match_pairs;
+  t->fuse_bytes += st->fuse_bytes;
+  t->fuse_passes += st->fuse_passes;
+  t->fuse_points += st->fuse_points;
+  t->fuse_actions += st->fuse_actions;
+  t->first_new_id += 1;  // steps accumulated
 }
 
 static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args) {
@@ -688,16 +727,42 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   DevMap* dmaps = ctx->d_maps;
   CU(cudaMemcpyAsync(dv, h, sizeof(StepArgs) * n, cudaMemcpyHostToDevice, ctx->stream));
   const size_t dyn = 2 * sizeof(int) * kfcap;
+  std::vector<cudaEvent_t> evs;
+  auto mark = [&]() -> int {
+    if (!ctx->prof) return LM_OK;
+    cudaEvent_t ev;
+    if (ctx->prof_pool.empty()) {
+      CU(cudaEventCreate(&ev));
+    } else {
+      ev = ctx->prof_pool.back();
+      ctx->prof_pool.pop_back();
+    }
+    CU(cudaEventRecord(ev, ctx->stream));
+    evs.push_back(ev);
+    return LM_OK;
+  };
+  int rc = LM_OK;
+  if ((rc = mark())) return rc;
   k_begin<<<n, 128, 0, ctx->stream>>>(dmaps, dv);
   k_insert<<<n, 1, 0, ctx->stream>>>(dmaps, dv);
+  if ((rc = mark())) return rc;
   k_cull<<<n, 1024, 0, ctx->stream>>>(dmaps, dv);
+  if ((rc = mark())) return rc;
   k_select<<<n, 256, dyn, ctx->stream>>>(dmaps, dv, slots);
+  if ((rc = mark())) return rc;
   k_prep<<<dim3(1 + NMAX, n), 256, 0, ctx->stream>>>(dmaps, dv);
+  if ((rc = mark())) return rc;
   k_match<<<dim3(tiles, NMAX, n), MATCH_TILE, 0, ctx->stream>>>(dmaps, dv);
+  if ((rc = mark())) return rc;
   k_tri<<<dim3(NMAX, n), 256, 0, ctx->stream>>>(dmaps, dv);
+  if ((rc = mark())) return rc;
   k_commit<<<n, 1024, 0, ctx->stream>>>(dmaps, dv);
+  if ((rc = mark())) return rc;
   k_fuse<<<n, 1024, dyn, ctx->stream>>>(dmaps, dv, slots);
-  k_end<<<n, 32, 0, ctx->stream>>>(dmaps, dv);
+  k_end<<<n, 32, 0, ctx->stream>>>(dmaps, dv, ctx->d_totals);
+  if ((rc = mark())) return rc;
+  ctx->launches += 10;
+  if (ctx->prof) ctx->prof_steps.push_back(evs);
   CHECK_LAUNCH();
   CU(cudaEventRecord(ctx->args_ev[e], ctx->stream));
   ctx->args_used[e] = true;
@@ -1278,6 +1343,139 @@ int lm_recent_import(lm_ctx* ctx, int32_t map, const int64_t* ids, const int32_t
     CU(cudaMemcpy(m->d.recent_born, born, sizeof(int) * n, cudaMemcpyHostToDevice));
   }
   CU(cudaMemcpy(m->d.scal + SC_RECENT_N, &n, sizeof(int), cudaMemcpyHostToDevice));
+  return LM_OK;
+}
+
+// ------------------------------------------------------------------- measurement
+__global__ void k_rewind_state(DevMap M, int n_slots) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n_slots; s += gridDim.x * blockDim.x)
+    if (M.kf_state[s] != KF_FREE) M.kf_state[s] = KF_STAGED;
+}
+
+int lm_map_rewind(lm_ctx* ctx, int32_t map) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  DevMap& d = m->d;
+  const size_t K = d.kf_cap, MP = d.mp_cap;
+  cudaStream_t st = ctx->stream;
+  CU(cudaMemsetAsync(d.covis, 0, sizeof(int) * K * K, st));
+  CU(cudaMemsetAsync(d.alive, 0, MP, st));
+  CU(cudaMemsetAsync(d.nobs, 0, sizeof(int) * MP, st));
+  CU(cudaMemsetAsync(d.ocap, 0, sizeof(int) * MP, st));
+  CU(cudaMemsetAsync(d.counts, 0, sizeof(int) * MP * d.L, st));
+  CU(cudaMemsetAsync(d.dirty, 0, sizeof(int) * MP, st));
+  CU(cudaMemsetAsync(d.scal, 0, sizeof(int) * SC_N, st));
+  CU(cudaMemsetAsync(d.ledger, 0, sizeof(unsigned long long) * LG_N, st));
+  CU(cudaMemsetAsync(m->d_totals, 0, sizeof(lm_step_stats), st));
+  if (m->kp_head) CU(cudaMemsetAsync(d.kbind, 0xff, sizeof(int) * m->kp_head, st));
+  if (m->n_slots) {
+    k_rewind_state<<<(m->n_slots + 255) / 256, 256, 0, st>>>(d, m->n_slots);
+    CHECK_LAUNCH();
+  }
+  CU(cudaStreamSynchronize(st));
+  for (int s = 0; s < m->n_slots; ++s)
+    if (m->state[s] != KF_FREE) m->state[s] = KF_STAGED;
+  m->resident = 0;
+  return LM_OK;
+}
+
+int lm_timer_start(lm_ctx* ctx) {
+  if (!ctx->t0) {
+    CU(cudaEventCreate(&ctx->t0));
+    CU(cudaEventCreate(&ctx->t1));
+  }
+  CU(cudaEventRecord(ctx->t0, ctx->stream));
+  return LM_OK;
+}
+
+int lm_timer_stop(lm_ctx* ctx, float* ms) {
+  CU(cudaEventRecord(ctx->t1, ctx->stream));
+  CU(cudaEventSynchronize(ctx->t1));
+  CU(cudaEventElapsedTime(ms, ctx->t0, ctx->t1));
+  return LM_OK;
+}
+
+int lm_flush_l2(lm_ctx* ctx, int64_t bytes) {
+  if (bytes <= 0) return LM_OK;
+  if ((size_t)bytes > ctx->flush_bytes) {
+    if (ctx->flush_buf) CU(cudaFree(ctx->flush_buf));
+    CU(cudaMalloc(&ctx->flush_buf, (size_t)bytes));
+    ctx->flush_bytes = (size_t)bytes;
+  }
+  CU(cudaMemsetAsync(ctx->flush_buf, (int)(ctx->launches & 0xff), (size_t)bytes, ctx->stream));
+  return LM_OK;
+}
+
+int lm_totals_fetch(lm_ctx* ctx, int32_t map, lm_step_stats* out) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  CU(cudaMemcpyAsync(out, m->d_totals, sizeof(lm_step_stats), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return LM_OK;
+}
+
+int64_t lm_launch_count(lm_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int lm_profile_enable(lm_ctx* ctx, int32_t on) {
+  ctx->prof = on != 0;
+  return LM_OK;
+}
+
+int lm_profile_read(lm_ctx* ctx, double ms[8], int64_t launches[8]) {
+  CU(cudaStreamSynchronize(ctx->stream));
+  for (int k = 0; k < 8; ++k) {
+    ms[k] = 0;
+    launches[k] = 0;
+  }
+  for (auto& evs : ctx->prof_steps) {
+    for (size_t k = 0; k + 1 < evs.size() && k < 8; ++k) {
+      float t = 0;
+      CU(cudaEventElapsedTime(&t, evs[k], evs[k + 1]));
+      ms[k] += t;
+      launches[k] += 1;
+    }
+    for (cudaEvent_t ev : evs) ctx->prof_pool.push_back(ev);
+  }
+  ctx->prof_steps.clear();
+  return LM_OK;
+}
+
+__global__ void k_popc_bench(unsigned* out, int iters, unsigned key) {
+  unsigned a0 = threadIdx.x, a1 = a0 * 3 + 1, a2 = a0 * 5 + 2, a3 = a0 * 7 + 3;
+  unsigned a4 = a0 * 11 + 4, a5 = a0 * 13 + 5, a6 = a0 * 17 + 6, a7 = a0 * 19 + 7;
+  for (int i = 0; i < iters; ++i) {
+    a0 += __popc(a0 ^ key); a1 += __popc(a1 ^ key); a2 += __popc(a2 ^ key); a3 += __popc(a3 ^ key);
+    a4 += __popc(a4 ^ key); a5 += __popc(a5 ^ key); a6 += __popc(a6 ^ key); a7 += __popc(a7 ^ key);
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = a0 ^ a1 ^ a2 ^ a3 ^ a4 ^ a5 ^ a6 ^ a7;
+}
+
+int lm_bench_popc(lm_ctx* ctx, double* popc_per_s) {
+  int sms = 0;
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  unsigned* out;
+  CU(cudaMalloc(&out, sizeof(unsigned) * blocks * threads));
+  cudaEvent_t a, b;
+  CU(cudaEventCreate(&a));
+  CU(cudaEventCreate(&b));
+  k_popc_bench<<<blocks, threads, 0, ctx->stream>>>(out, iters, 0x9e3779b9u);  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    CU(cudaEventRecord(a, ctx->stream));
+    k_popc_bench<<<blocks, threads, 0, ctx->stream>>>(out, iters, 0x9e3779b9u + rep);
+    CU(cudaEventRecord(b, ctx->stream));
+    CU(cudaEventSynchronize(b));
+    float t;
+    CU(cudaEventElapsedTime(&t, a, b));
+    best = t < best ? t : best;
+  }
+  CU(cudaFree(out));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *popc_per_s = (double)blocks * threads * iters * 8 / (best * 1e-3);
   return LM_OK;
 }
 

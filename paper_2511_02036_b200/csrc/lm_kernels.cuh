@@ -364,6 +364,7 @@ __global__ void __launch_bounds__(MATCH_TILE) k_match(DevMap* maps, const StepAr
   const int* bk = M.s.nb_bucket + r * (LMAX + 1);
   const int jb = bk[l0], je = bk[l1 + 1];
   const size_t base = (size_t)r * M.kpkf_max;
+  if (threadIdx.x == 0) atomicAdd((unsigned long long*)&M.s.stats->match_pairs, (unsigned long long)cnt * (je - jb));
   const int cur = A.cur;
   const int off = M.kp_off[cur];
   const bool active = threadIdx.x < cnt;
@@ -583,6 +584,7 @@ __global__ void __launch_bounds__(1024) k_commit(DevMap* maps, const StepArgs* a
     st->gate_reprojection = gates[2];
     st->gate_scale = gates[3];
     st->first_new_id = id0;
+    st->n_candidates = total;
     if (okcap) {
       M.scal[SC_NEXT_ID] = id0 + created;
       M.scal[SC_OBS_HEAD] = obs0 + 4 * created;
@@ -879,6 +881,20 @@ __device__ int gather_pass(const DevMap& M, const lm_fuse_cfg& fc, int P, int ts
   return count;
 }
 
+// sum of observation counts of M.s.pts[0..P) (algorithmic-bytes accounting)
+template <int BLOCK>
+__device__ long long pass_obs(const DevMap& M, int P, int* sh) {
+  int c = 0;
+  for (int p = threadIdx.x; p < P; p += BLOCK) c += M.nobs[M.s.pts[p]];
+  return block_sum<BLOCK>(c, sh);
+}
+
+// per pass 56 B per point (pos 24 + rep 32), 9 B per observation, 53 B per
+// target keypoint (u,v 16 + level 1 + desc 32 + binding 4), 16 B per action
+__device__ __forceinline__ long long pass_bytes(long long pts, long long obs, long long tkp, long long acts) {
+  return 56 * pts + 9 * obs + 53 * tkp + 16 * acts;
+}
+
 // full run_fusion for one map per CTA
 __global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* args, int n_slots_max) {
   const StepArgs& A = args[blockIdx.x];
@@ -913,6 +929,9 @@ __global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* arg
     M.ledger[LG_SMALL_FUSE] += (unsigned long long)P * mpb;
     M.ledger[LG_SMALL_EVENTS] += 1;
   }
+  const long long fwd_obs = pass_obs<1024>(M, P, sh);
+  long long tkp = 0;
+  for (int k = 0; k < T; ++k) tkp += M.kp_n[M.s.targets[k]];
   for (int p = threadIdx.x; p < P; p += 1024) point_geometry(M, M.s.pts[p], fc.dist_band_slack, M.s.geo[p]);
   __syncthreads();
   const int TP = T * P;
@@ -940,6 +959,8 @@ __global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* arg
     nact += tot;
     __syncthreads();
   }
+  long long alg = pass_bytes((long long)T * P, (long long)T * fwd_obs, tkp, nact);
+  long long npts = (long long)T * P, nacts = nact;
   if (threadIdx.x == 0) {
     int c[3] = {0, 0, 0};
     apply_actions(M, M.s.acts, nact, c);
@@ -959,7 +980,11 @@ __global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* arg
       M.ledger[LG_SMALL_FUSE] += (unsigned long long)Pt * mpb;
       M.ledger[LG_SMALL_EVENTS] += 1;
     }
+    const long long ob = pass_obs<1024>(M, Pt, sh);
     const int na = gather_pass<1024>(M, fc, Pt, cur, true, sh, nullptr);
+    alg += pass_bytes(Pt, ob, M.kp_n[cur], na);
+    npts += Pt;
+    nacts += na;
     if (threadIdx.x == 0) {
       int c[3] = {0, 0, 0};
       apply_actions(M, M.s.acts, na, c);
@@ -972,6 +997,10 @@ __global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* arg
   refresh_dirty<1024>(M);
   if (threadIdx.x == 0) {
     st->n_targets = T;
+    st->fuse_bytes = alg;
+    st->fuse_passes = 2 * T;
+    st->fuse_points = npts;
+    st->fuse_actions = nacts;
     st->merged = cnt[0];
     st->observations_added = cnt[1];
     st->stale = cnt[2];
