@@ -355,18 +355,21 @@ __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, in
       return;
     }
     case OP_REFRESH: {
-      refresh_dirty<1024>(M);
+      refresh_all<1024>(M);
       if (tid == 0) res[0] = M.scal[SC_ERR];
       return;
     }
     case OP_APPLY: {
-      if (tid) return;
-      int c[3] = {0, 0, 0};
-      apply_actions(M, M.s.acts, A.n, c);
-      res[0] = M.scal[SC_ERR];
-      res[1] = c[0];
-      res[2] = c[1];
-      res[3] = c[2];
+      __shared__ int c[3];
+      if (tid < 3) c[tid] = 0;
+      __syncthreads();
+      apply_block<1024>(M, M.s.acts, A.n, c, sh);
+      if (tid == 0) {
+        res[0] = M.scal[SC_ERR];
+        res[1] = c[0];
+        res[2] = c[1];
+        res[3] = c[2];
+      }
       return;
     }
     case OP_TARGETS: {
@@ -380,7 +383,6 @@ __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, in
       return;
     }
     case OP_FUSE_PASS: {
-      refresh_dirty<1024>(M);
       int nvis = 0;
       const int na = gather_pass<1024>(M, A.fc, A.n, A.a, false, sh, &nvis);
       if (tid == 0) {
@@ -525,7 +527,7 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(d.ku, KP); A(d.kv, KP); A(d.klev, KP); A(d.kdesc, 2 * KP); A(d.kbind, KP);
   A(d.pos, 3 * MP); A(d.rep, 2 * MP); A(d.alive, MP); A(d.found, MP); A(d.visible, MP); A(d.first_kf, MP);
   A(d.nobs, MP); A(d.ocap, MP); A(d.ooff, MP); A(d.obs, (size_t)d.obs_cap); A(d.counts, MP * d.L);
-  A(d.dirty, MP); A(d.dirty_list, MP);
+  A(d.dirty, MP); A(d.dirty_list, MP); A(d.res_pt, MP); A(d.res_slot, KP);
   A(d.covis, K * K);
   A(d.recent_id, MP); A(d.recent_born, MP);
   A(d.scal, SC_N); A(d.ledger, LG_N);
@@ -542,9 +544,12 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(s.pts, s.pts_cap); A(s.geo, s.pts_cap);
   s.act_cap = TMAX * d.kpkf_max;
   A(s.acts, (size_t)s.act_cap); A(s.act_flag, (size_t)s.act_cap); A(s.vis_flag, (size_t)s.act_cap);
+  A(s.pend, (size_t)s.act_cap); A(s.ready, (size_t)s.act_cap);
   A(m->d_stats, 1); A(m->d_totals, 1); A(m->d_result, 4 + 1024 + TMAX);
 #undef A
   s.stats = m->d_stats;
+  CU(cudaMemsetAsync(d.res_pt, 0xff, sizeof(unsigned long long) * MP, ctx->stream));
+  CU(cudaMemsetAsync(d.res_slot, 0xff, sizeof(unsigned long long) * KP, ctx->stream));
   m->state.assign(K, KF_FREE);
   m->kp_n.assign(K, 0);
   m->kp_off.assign(K, 0);
@@ -570,6 +575,8 @@ int lm_map_reset(lm_ctx* ctx, int32_t map) {
   CU(cudaMemsetAsync(d.scal, 0, sizeof(int) * SC_N, ctx->stream));
   CU(cudaMemsetAsync(d.ledger, 0, sizeof(unsigned long long) * LG_N, ctx->stream));
   CU(cudaMemsetAsync(m->d_totals, 0, sizeof(lm_step_stats), ctx->stream));
+  CU(cudaMemsetAsync(d.res_pt, 0xff, sizeof(unsigned long long) * MP, ctx->stream));
+  CU(cudaMemsetAsync(d.res_slot, 0xff, sizeof(unsigned long long) * d.kp_cap, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   m->slot_of.clear();
   std::fill(m->state.begin(), m->state.end(), KF_FREE);
@@ -744,7 +751,7 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   int rc = LM_OK;
   if ((rc = mark())) return rc;
   k_begin<<<n, 128, 0, ctx->stream>>>(dmaps, dv);
-  k_insert<<<n, 1, 0, ctx->stream>>>(dmaps, dv);
+  k_insert<<<n, 256, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;
   k_cull<<<n, 1024, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;
@@ -1368,6 +1375,8 @@ int lm_map_rewind(lm_ctx* ctx, int32_t map) {
   CU(cudaMemsetAsync(d.scal, 0, sizeof(int) * SC_N, st));
   CU(cudaMemsetAsync(d.ledger, 0, sizeof(unsigned long long) * LG_N, st));
   CU(cudaMemsetAsync(m->d_totals, 0, sizeof(lm_step_stats), st));
+  CU(cudaMemsetAsync(d.res_pt, 0xff, sizeof(unsigned long long) * MP, st));
+  CU(cudaMemsetAsync(d.res_slot, 0xff, sizeof(unsigned long long) * d.kp_cap, st));
   if (m->kp_head) CU(cudaMemsetAsync(d.kbind, 0xff, sizeof(int) * m->kp_head, st));
   if (m->n_slots) {
     k_rewind_state<<<(m->n_slots + 255) / 256, 256, 0, st>>>(d, m->n_slots);

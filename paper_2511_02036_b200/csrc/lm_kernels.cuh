@@ -112,27 +112,34 @@ __device__ int ranked_neighbors(const DevMap& M, int k, int n, int* sh_slot, int
 
 // ---------------------------------------------------------------------------------- insert
 
-__global__ void k_insert(DevMap* maps, const StepArgs* args) {
+__global__ void __launch_bounds__(256) k_insert(DevMap* maps, const StepArgs* args) {
   const StepArgs& A = args[blockIdx.x];
   const DevMap& M = maps[A.map];
   if (!A.do_insert) return;
   const int slot = A.cur;
-  if (threadIdx.x == 0) {
-    M.kf_state[slot] = KF_LIVE;
-    M.ledger[LG_PERSIST] += (unsigned long long)payload_bytes(M, slot);
-    // pre-bound slots register their observations (insert_keyframe mapmodel.py:185-199)
-    const int off = M.kp_off[slot], n = M.kp_n[slot];
-    for (int i = 0; i < n; ++i) {
-      const int mp = M.kbind[off + i];
-      if (mp < 0) continue;
-      M.kbind[off + i] = -1;
-      if (mp >= M.scal[SC_NEXT_ID] || !M.alive[mp] || obs_find(M, mp, slot) >= 0) {
-        set_err(M, LM_ERR_INVALID_ARGUMENT);
-        continue;
-      }
-      link(M, mp, slot, i);
-      mark_dirty(M, mp);
+  const int off = M.kp_off[slot], n = M.kp_n[slot];
+  __shared__ int any;
+  if (threadIdx.x == 0) any = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += 256)
+    if (M.kbind[off + i] >= 0) any = 1;
+  __syncthreads();
+  if (threadIdx.x) return;
+  M.kf_state[slot] = KF_LIVE;
+  M.ledger[LG_PERSIST] += (unsigned long long)payload_bytes(M, slot);
+  if (!any) return;
+  // pre-bound slots register their observations in keypoint order (insert_keyframe
+  // mapmodel.py:185-199); rare (tests, externally seeded maps), so one thread
+  for (int i = 0; i < n; ++i) {
+    const int mp = M.kbind[off + i];
+    if (mp < 0) continue;
+    M.kbind[off + i] = -1;
+    if (mp >= M.scal[SC_NEXT_ID] || !M.alive[mp] || obs_find(M, mp, slot) >= 0) {
+      set_err(M, LM_ERR_INVALID_ARGUMENT);
+      continue;
     }
+    link(M, mp, slot, i);
+    mark_dirty(M, mp);
   }
 }
 
@@ -710,59 +717,181 @@ __device__ int gather_one(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g,
   return 1;
 }
 
-// apply_fusion (fusion.py:249-292), sequential in list order
-__device__ void apply_actions(const DevMap& M, const ActRec* acts, int n, int cnt[3]) {
-  for (int a = 0; a < n; ++a) {
-    const ActRec x = acts[a];
-    if (x.pid < 0 || !M.alive[x.pid] || M.kf_state[x.slot] != KF_LIVE) {
-      ++cnt[2];
-      continue;
+// ------------------------------------------------------------------ ordered apply
+// apply_fusion (fusion.py:249-292) with sequential semantics, executed in parallel by
+// deterministic reservations: every round, each pending action reserves every entity it
+// would read or write given the current state (its projected point, the hit slot, the
+// slot's current owner or the MERGE partner, and when a merge proceeds every slot of the
+// loser) with atomicMin of a round-tagged action index; actions holding all their keys
+// commit together (their entity sets are disjoint, and no earlier pending action touches
+// them), the rest retry. Covisibility bumps are atomic adds and commute.
+
+__device__ __forceinline__ unsigned long long res_tag(unsigned round, int a) {
+  return ((unsigned long long)(0xffffffffu - round) << 32) | (unsigned)a;
+}
+
+// visit the key set of action x under the current state; op(is_point, id) -> bool (false stops)
+template <class Op>
+__device__ bool for_keys(const DevMap& M, const ActRec& x, Op op) {
+  if (!op(true, x.pid)) return false;
+  if (!M.alive[x.pid] || M.kf_state[x.slot] != KF_LIVE) return true;  // stale
+  const int g = M.kp_off[x.slot] + x.j;
+  if (!op(false, g)) return false;
+  const int now = M.kbind[g];
+  int partner = -1;
+  if (x.kind == LM_ACT_MERGE) {
+    if (x.other >= 0 && !op(true, x.other)) return false;
+    if (now >= 0 && now != x.other && now != x.pid && !op(true, now)) return false;
+    if (x.other >= 0 && M.alive[x.other] && x.other != x.pid && now == x.other) partner = x.other;
+  } else if (now >= 0) {
+    if (now != x.pid && !op(true, now)) return false;
+    if (M.alive[now] && now != x.pid) partner = now;
+  }
+  if (partner >= 0) {
+    const int na = M.nobs[x.pid], nb = M.nobs[partner];
+    const int loser = na == nb ? (x.pid > partner ? x.pid : partner) : (na < nb ? x.pid : partner);
+    const int2* o = M.obs + M.ooff[loser];
+    const int n = M.nobs[loser];
+    for (int k = 0; k < n; ++k)
+      if (!op(false, M.kp_off[o[k].x] + o[k].y)) return false;
+  }
+  return true;
+}
+
+// one action, sequential semantics; cnt = {merged, added, stale} (shared, atomic)
+__device__ void apply_one(const DevMap& M, const ActRec& x, int* cnt) {
+  if (x.pid < 0 || !M.alive[x.pid] || M.kf_state[x.slot] != KF_LIVE) {
+    atomicAdd(&cnt[2], 1);
+    return;
+  }
+  const int g = M.kp_off[x.slot] + x.j;
+  if (x.kind == LM_ACT_MERGE) {
+    if (x.other < 0 || !M.alive[x.other] || x.other == x.pid || M.kbind[g] != x.other) {
+      atomicAdd(&cnt[2], 1);
+      return;
     }
-    const int g = M.kp_off[x.slot] + x.j;
-    if (x.kind == LM_ACT_MERGE) {
-      if (x.other < 0 || !M.alive[x.other] || x.other == x.pid || M.kbind[g] != x.other) {
-        ++cnt[2];
-        continue;
-      }
-      merge_pair(M, x.pid, x.other);
-      ++cnt[0];
-      continue;
+    merge_pair(M, x.pid, x.other);
+    atomicAdd(&cnt[0], 1);
+    return;
+  }
+  const int now = M.kbind[g];
+  if (now >= 0) {
+    if (!M.alive[now] || now == x.pid) {
+      atomicAdd(&cnt[2], 1);
+      return;
     }
-    const int now = M.kbind[g];
-    if (now >= 0) {
-      if (!M.alive[now] || now == x.pid) {
-        ++cnt[2];
-        continue;
-      }
-      merge_pair(M, x.pid, now);
-      ++cnt[0];
-      continue;
+    merge_pair(M, x.pid, now);
+    atomicAdd(&cnt[0], 1);
+    return;
+  }
+  if (obs_find(M, x.pid, x.slot) >= 0) {
+    atomicAdd(&cnt[2], 1);
+    return;
+  }
+  link(M, x.pid, x.slot, x.j);
+  mark_dirty(M, x.pid);
+  M.found[x.pid] += 1;
+  atomicAdd(&cnt[1], 1);
+}
+
+template <int BLOCK>
+__device__ void apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh) {
+  __shared__ unsigned round_sh;
+  __shared__ int npend_sh;
+  for (int a = threadIdx.x; a < n; a += BLOCK) M.s.pend[a] = a;
+  if (threadIdx.x == 0) npend_sh = n;
+  __syncthreads();
+  int guard = 0;
+  while (npend_sh > 0) {
+    const int np = npend_sh;
+    if (threadIdx.x == 0) round_sh = (unsigned)atomicAdd(&M.scal[SC_ROUND], 1) + 1u;
+    __syncthreads();
+    const unsigned rnd = round_sh;
+    for (int q = threadIdx.x; q < np; q += BLOCK) {
+      const int a = M.s.pend[q];
+      const unsigned long long tag = res_tag(rnd, a);
+      for_keys(M, acts[a], [&](bool pt, int id) {
+        atomicMin(pt ? &M.res_pt[id] : &M.res_slot[id], tag);
+        return true;
+      });
     }
-    if (obs_find(M, x.pid, x.slot) >= 0) {
-      ++cnt[2];
-      continue;
+    __syncthreads();
+    for (int q = threadIdx.x; q < np; q += BLOCK) {
+      const int a = M.s.pend[q];
+      const unsigned long long tag = res_tag(rnd, a);
+      M.s.ready[q] = for_keys(M, acts[a], [&](bool pt, int id) { return (pt ? M.res_pt[id] : M.res_slot[id]) == tag; });
     }
-    link(M, x.pid, x.slot, x.j);
-    mark_dirty(M, x.pid);
-    M.found[x.pid] += 1;
-    ++cnt[1];
+    __syncthreads();
+    for (int q = threadIdx.x; q < np; q += BLOCK)
+      if (M.s.ready[q]) apply_one(M, acts[M.s.pend[q]], cnt);
+    __syncthreads();
+    // stable compaction of the still-pending actions
+    int kept = 0;
+    for (int b0 = 0; b0 < np; b0 += BLOCK) {
+      const int q = b0 + threadIdx.x;
+      const int keep = q < np ? !M.s.ready[q] : 0;
+      const int a = keep ? M.s.pend[q] : 0;
+      int tot;
+      const int at = block_excl_scan<BLOCK>(keep, sh, tot);
+      if (keep) M.s.pend[kept + at] = a;  // write index <= read index
+      kept += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) npend_sh = kept;
+    __syncthreads();
+    if (++guard > (1 << 20)) break;
   }
 }
 
-// recompute every dirty representative descriptor (warp per point)
+// recompute the representative descriptor of every dirty point in pts[0..P) (warp per point)
 template <int BLOCK>
-__device__ void refresh_dirty(const DevMap& M) {
+__device__ void refresh_points(const DevMap& M, const int* pts, int P, int* sh) {
+  int count = 0;
+  for (int b0 = 0; b0 < P; b0 += BLOCK) {
+    const int p = b0 + threadIdx.x;
+    int mp = -1, f = 0;
+    if (p < P) {
+      mp = pts[p];
+      f = mp >= 0 && M.dirty[mp];
+    }
+    int tot;
+    const int at = block_excl_scan<BLOCK>(f, sh, tot);
+    if (f) M.dirty_list[count + at] = mp;
+    count += tot;
+  }
   __syncthreads();
-  const int n = M.scal[SC_DIRTY_N];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int k = wid; k < n; k += BLOCK / 32) {
+  for (int k = wid; k < count; k += BLOCK / 32) {
     const int mp = M.dirty_list[k];
     if (M.alive[mp]) refresh_rep_warp(M, mp, lane);
     __syncwarp();
     if (lane == 0) M.dirty[mp] = 0;
   }
   __syncthreads();
-  if (threadIdx.x == 0) M.scal[SC_DIRTY_N] = 0;
+}
+
+// every dirty point of the map (export path)
+template <int BLOCK>
+__device__ void refresh_all(const DevMap& M) {
+  __syncthreads();
+  const int n = M.scal[SC_NEXT_ID];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int b0 = 0; b0 < n; b0 += BLOCK) {
+    // warp-ballot over 32 ids at a time, refresh dirty ones cooperatively
+    for (int w0 = b0 + wid * 32; w0 < b0 + BLOCK && w0 < n; w0 += BLOCK) {
+      const int id = w0 + lane;
+      unsigned bal = __ballot_sync(0xffffffffu, id < n && M.dirty[id]);
+      while (bal) {
+        const int k = __ffs(bal) - 1;
+        bal &= bal - 1;
+        const int mp = w0 + k;
+        if (M.alive[mp]) refresh_rep_warp(M, mp, lane);
+        __syncwarp();
+        if (lane == 0) M.dirty[mp] = 0;
+        __syncwarp();
+      }
+    }
+  }
   __syncthreads();
 }
 
@@ -857,6 +986,7 @@ __device__ int fusion_targets(const DevMap& M, int cur, int n1, int n2, int n_sl
 template <int BLOCK>
 __device__ int gather_pass(const DevMap& M, const lm_fuse_cfg& fc, int P, int ts, bool bump_visible, int* sh,
                            int* vis_out) {
+  refresh_points<BLOCK>(M, M.s.pts, P, sh);
   for (int p = threadIdx.x; p < P; p += BLOCK) point_geometry(M, M.s.pts[p], fc.dist_band_slack, M.s.geo[p]);
   __syncthreads();
   int count = 0, nvis = 0;
@@ -908,7 +1038,6 @@ __global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* arg
   const lm_fuse_cfg& fc = A.fc;
   const int cur = A.cur;
   if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
-  refresh_dirty<1024>(M);
   const int T = fusion_targets<1024>(M, cur, fc.n1, fc.n2, n_slots_max, sh_slot, sh_w, sh);
   lm_step_stats* st = M.s.stats;
   if (T == 0) {
@@ -929,6 +1058,7 @@ __global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* arg
     M.ledger[LG_SMALL_FUSE] += (unsigned long long)P * mpb;
     M.ledger[LG_SMALL_EVENTS] += 1;
   }
+  refresh_points<1024>(M, M.s.pts, P, sh);
   const long long fwd_obs = pass_obs<1024>(M, P, sh);
   long long tkp = 0;
   for (int k = 0; k < T; ++k) tkp += M.kp_n[M.s.targets[k]];
@@ -961,17 +1091,9 @@ __global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* arg
   }
   long long alg = pass_bytes((long long)T * P, (long long)T * fwd_obs, tkp, nact);
   long long npts = (long long)T * P, nacts = nact;
-  if (threadIdx.x == 0) {
-    int c[3] = {0, 0, 0};
-    apply_actions(M, M.s.acts, nact, c);
-    cnt[0] += c[0];
-    cnt[1] += c[1];
-    cnt[2] += c[2];
-  }
-  __syncthreads();
+  apply_block<1024>(M, M.s.acts, nact, cnt, sh);
   // reverse: per target, its bound points into the current keyframe, gather then apply
   for (int t = 0; t < T; ++t) {
-    refresh_dirty<1024>(M);
     const int ts = M.s.targets[t];
     const int Pt = bound_points<1024>(M, ts, sh);
     if (threadIdx.x == 0) {
@@ -985,16 +1107,8 @@ __global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* arg
     alg += pass_bytes(Pt, ob, M.kp_n[cur], na);
     npts += Pt;
     nacts += na;
-    if (threadIdx.x == 0) {
-      int c[3] = {0, 0, 0};
-      apply_actions(M, M.s.acts, na, c);
-      cnt[0] += c[0];
-      cnt[1] += c[1];
-      cnt[2] += c[2];
-    }
-    __syncthreads();
+    apply_block<1024>(M, M.s.acts, na, cnt, sh);
   }
-  refresh_dirty<1024>(M);
   if (threadIdx.x == 0) {
     st->n_targets = T;
     st->fuse_bytes = alg;

@@ -35,7 +35,7 @@ constexpr int MATCH_TILE = 128;         // current keypoints per match CTA
 constexpr int MATCH_JT = 256;           // neighbour descriptors staged per smem tile
 
 enum KfState { KF_FREE = 0, KF_STAGED = 1, KF_LIVE = 2, KF_DEAD = 3 };
-enum Scal { SC_NEXT_ID = 0, SC_OBS_HEAD, SC_RECENT_N, SC_ERR, SC_DIRTY_N, SC_N = 8 };
+enum Scal { SC_NEXT_ID = 0, SC_OBS_HEAD, SC_RECENT_N, SC_ERR, SC_DIRTY_N, SC_ROUND, SC_N = 8 };
 enum LedgerIdx { LG_PERSIST = 0, LG_NAIVE, LG_SMALL_TRI, LG_SMALL_FUSE, LG_SMALL_EVENTS, LG_EVICT, LG_N = 8 };
 enum CandStatus { CS_PASS = 0, CS_PARALLAX = 1, CS_DEPTH = 2, CS_REPROJ = 3, CS_SCALE = 4, CS_DEGEN = 5 };
 
@@ -87,6 +87,8 @@ struct Scratch {
   int* n_targets;        // [1]
   int* rank_buf;         // [TMAX * kf_cap] second-order walk scratch
   int* pts;              // [max(kpkf_max, pts_cap)] point list of the current pass
+  int* pend;             // [act_cap] pending action indices (apply rounds)
+  int* ready;            // [act_cap]
   PGeo* geo;             // [pts_cap]
   ActRec* acts;          // [TMAX*kpkf_max]
   int* act_flag;         // [TMAX*kpkf_max]
@@ -137,6 +139,9 @@ struct DevMap {
   int* counts;
   int* dirty;
   int* dirty_list;
+  // deterministic-reservation tables (apply): round-tagged min action index per entity
+  unsigned long long* res_pt;    // [mp_cap]
+  unsigned long long* res_slot;  // [kp_cap]
   // covisibility
   int* covis;
   // probation list (culling.RecentPoint)
@@ -196,12 +201,8 @@ __device__ bool obs_insert(const DevMap& M, int mp, int slot, int kp) {
   return true;
 }
 
-__device__ __forceinline__ void mark_dirty(const DevMap& M, int mp) {
-  if (atomicExch(&M.dirty[mp], 1) == 0) {
-    const int at = atomicAdd(&M.scal[SC_DIRTY_N], 1);
-    M.dirty_list[at] = mp;
-  }
-}
+// the representative descriptor is stale until refresh_points / refresh_all recompute it
+__device__ __forceinline__ void mark_dirty(const DevMap& M, int mp) { M.dirty[mp] = 1; }
 
 // _record_obs: covis +1 with every current observer, bind the slot, count the level
 __device__ void link(const DevMap& M, int mp, int slot, int kp) {

@@ -149,48 +149,58 @@ LM_HD double epi_d2(const double l[3], double den, double u, double v) {
 
 // Smallest right singular vector of a 4x4 matrix by one-sided (Hestenes) Jacobi.
 // A is row-major and is overwritten. Returns the unit null vector in v.
+LM_HD void jacobi_rotate(double A[16], double V[16], int p, int q, bool& rotated) {
+  double alpha = 0, beta = 0, gamma = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double ap = A[k * 4 + p], aq = A[k * 4 + q];
+    alpha += ap * ap;
+    beta += aq * aq;
+    gamma += ap * aq;
+  }
+  // converged pair: columns orthogonal to working precision
+  if (gamma == 0.0 || fabs(gamma) <= 1e-15 * sqrt(alpha * beta)) return;
+  rotated = true;
+  const double zeta = (beta - alpha) / (2.0 * gamma);
+  const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+  const double c = 1.0 / sqrt(1.0 + tt * tt);
+  const double s = c * tt;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double ap = A[k * 4 + p], aq = A[k * 4 + q];
+    A[k * 4 + p] = c * ap - s * aq;
+    A[k * 4 + q] = s * ap + c * aq;
+    const double vp = V[k * 4 + p], vq = V[k * 4 + q];
+    V[k * 4 + p] = c * vp - s * vq;
+    V[k * 4 + q] = s * vp + c * vq;
+  }
+}
+
 LM_HD void null_vector4(double A[16], double v[4]) {
   double V[16] = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1};
-  for (int sweep = 0; sweep < 40; ++sweep) {
+  for (int sweep = 0; sweep < 30; ++sweep) {
     bool rotated = false;
-    for (int p = 0; p < 3; ++p) {
-      for (int q = p + 1; q < 4; ++q) {
-        double alpha = 0, beta = 0, gamma = 0;
-        for (int k = 0; k < 4; ++k) {
-          const double ap = A[k * 4 + p], aq = A[k * 4 + q];
-          alpha += ap * ap;
-          beta += aq * aq;
-          gamma += ap * aq;
-        }
-        if (gamma == 0.0 || fabs(gamma) <= 1e-17 * sqrt(alpha * beta)) continue;
-        rotated = true;
-        const double zeta = (beta - alpha) / (2.0 * gamma);
-        const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / sqrt(1.0 + tt * tt);
-        const double s = c * tt;
-        for (int k = 0; k < 4; ++k) {
-          const double ap = A[k * 4 + p], aq = A[k * 4 + q];
-          A[k * 4 + p] = c * ap - s * aq;
-          A[k * 4 + q] = s * ap + c * aq;
-          const double vp = V[k * 4 + p], vq = V[k * 4 + q];
-          V[k * 4 + p] = c * vp - s * vq;
-          V[k * 4 + q] = s * vp + c * vq;
-        }
-      }
-    }
+    jacobi_rotate(A, V, 0, 1, rotated);
+    jacobi_rotate(A, V, 0, 2, rotated);
+    jacobi_rotate(A, V, 0, 3, rotated);
+    jacobi_rotate(A, V, 1, 2, rotated);
+    jacobi_rotate(A, V, 1, 3, rotated);
+    jacobi_rotate(A, V, 2, 3, rotated);
     if (!rotated) break;
   }
+  double n[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) n[j] = A[j] * A[j] + A[4 + j] * A[4 + j] + A[8 + j] * A[8 + j] + A[12 + j] * A[12 + j];
   int best = 0;
-  double bn = INFINITY;
-  for (int j = 0; j < 4; ++j) {
-    double n = 0;
-    for (int k = 0; k < 4; ++k) n += A[k * 4 + j] * A[k * 4 + j];
-    if (n < bn) { bn = n; best = j; }
-  }
-  double nv = 0;
-  for (int k = 0; k < 4; ++k) nv += V[k * 4 + best] * V[k * 4 + best];
-  nv = sqrt(nv);
-  for (int k = 0; k < 4; ++k) v[k] = V[k * 4 + best] / nv;
+#pragma unroll
+  for (int j = 1; j < 4; ++j)
+    if (n[j] < n[best]) best = j;
+  double c0 = V[best], c1 = V[4 + best], c2 = V[8 + best], c3 = V[12 + best];
+  const double nv = sqrt(c0 * c0 + c1 * c1 + c2 * c2 + c3 * c3);
+  v[0] = c0 / nv;
+  v[1] = c1 / nv;
+  v[2] = c2 / nv;
+  v[3] = c3 / nv;
 }
 
 // Two-view DLT (geometry.py:258-284). Pa/Pb are K[R|t]; Ca/Cb camera centres.
