@@ -712,6 +712,8 @@ __global__ void k_end(DevMap* maps, const StepArgs* args, lm_step_stats** totals
   t->fuse_passes += st->fuse_passes;
   t->fuse_points += st->fuse_points;
   t->fuse_actions += st->fuse_actions;
+  t->apply_rounds += st->apply_rounds;
+  for (int k = 0; k < 8; ++k) t->fuse_cycles[k] += st->fuse_cycles[k];
   t->first_new_id += 1;  // steps accumulated
 }
 
@@ -721,11 +723,13 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   if (ctx->args_used[e]) CU(cudaEventSynchronize(ctx->args_ev[e]));
   StepArgs* h = ctx->h_args + (size_t)e * kMaxBatch;
   StepArgs* dv = ctx->d_args + (size_t)e * kMaxBatch;
-  int tiles = 1, slots = 1, kfcap = 2;
+  int tiles = 1, slots = 1, kfcap = 2, nbr_dim = 1;
   for (int k = 0; k < n; ++k) {
     HostMap* m = ctx->maps[maps[k]];
     h[k] = args[k];
     h[k].map = maps[k];
+    const int want = args[k].explicit_nbr ? 1 : (args[k].n_nbr_req < NMAX ? args[k].n_nbr_req : NMAX);
+    nbr_dim = want > nbr_dim ? want : nbr_dim;
     const int t = m->d.kpkf_max / MATCH_TILE + m->d.L + 1;
     tiles = t > tiles ? t : tiles;
     slots = m->n_slots > slots ? m->n_slots : slots;
@@ -757,11 +761,11 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   if ((rc = mark())) return rc;
   k_select<<<n, 256, dyn, ctx->stream>>>(dmaps, dv, slots);
   if ((rc = mark())) return rc;
-  k_prep<<<dim3(1 + NMAX, n), 256, 0, ctx->stream>>>(dmaps, dv);
+  k_prep<<<dim3(1 + nbr_dim, n), 256, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;
-  k_match<<<dim3(tiles, NMAX, n), MATCH_TILE, 0, ctx->stream>>>(dmaps, dv);
+  k_match<<<dim3(tiles, nbr_dim, n), MATCH_WARPS * 32, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;
-  k_tri<<<dim3(NMAX, n), 256, 0, ctx->stream>>>(dmaps, dv);
+  k_tri<<<dim3(nbr_dim, n), 256, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;
   k_commit<<<n, 1024, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;

@@ -350,12 +350,15 @@ __global__ void __launch_bounds__(256) k_prep(DevMap* maps, const StepArgs* args
 
 // ---------------------------------------------------------------------------------- match
 
-// grid (tiles, NMAX, maps), block MATCH_TILE. Each thread owns one unbound current
-// keypoint of the tile's level and scans the neighbour's unbound keypoints of levels
-// [l-w, l+w], staged MATCH_JT at a time in shared memory (warp-broadcast reads). Hamming
-// first (8 x POPC), the fp64 epipolar test only on the rare dist <= max survivors; the
-// running minimum is the lexicographic (dist, j) key of the reference's first-argmin.
-__global__ void __launch_bounds__(MATCH_TILE) k_match(DevMap* maps, const StepArgs* args) {
+// grid (tiles, NMAX, maps), block MATCH_WARPS x 32. A tile is 32 unbound current keypoints
+// of one pyramid level (lane = keypoint); the CTA's warps split the neighbour's unbound
+// keypoints of levels [l-w, l+w] (contiguous in the level-bucketed list) into slices.
+// Descriptors are staged in shared memory and read warp-uniformly (broadcast). Hamming
+// first: the 128-bit prefix distance already exceeds the limit for almost every
+// non-matching pair, so the second half and the fp64 epipolar test run only on survivors.
+// The running minimum is the lexicographic (dist, j) key of the reference's first-argmin;
+// warp slices combine with a shared atomicMin, neighbour one-to-one with a global one.
+__global__ void __launch_bounds__(MATCH_WARPS * 32) k_match(DevMap* maps, const StepArgs* args) {
   const StepArgs& A = args[blockIdx.z];
   const DevMap& M = maps[A.map];
   if (!A.do_create) return;
@@ -364,6 +367,8 @@ __global__ void __launch_bounds__(MATCH_TILE) k_match(DevMap* maps, const StepAr
   const int tile = blockIdx.x;
   if (tile >= *M.s.n_tiles) return;
   __shared__ uint4 sd[2 * MATCH_JT];
+  __shared__ unsigned long long best_sh[MATCH_TILE];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int lv = M.s.tiles[3 * tile], start = M.s.tiles[3 * tile + 1], cnt = M.s.tiles[3 * tile + 2];
   const int w = A.mc.level_window;
   const int l0 = lv - w < 0 ? 0 : lv - w;
@@ -372,14 +377,15 @@ __global__ void __launch_bounds__(MATCH_TILE) k_match(DevMap* maps, const StepAr
   const int jb = bk[l0], je = bk[l1 + 1];
   const size_t base = (size_t)r * M.kpkf_max;
   if (threadIdx.x == 0) atomicAdd((unsigned long long*)&M.s.stats->match_pairs, (unsigned long long)cnt * (je - jb));
+  if (threadIdx.x < MATCH_TILE) best_sh[threadIdx.x] = ~0ull;
   const int cur = A.cur;
   const int off = M.kp_off[cur];
-  const bool active = threadIdx.x < cnt;
+  const bool active = lane < cnt;
   int i = 0;
   uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0;
   double l[3] = {0, 0, 0}, den = 0;
   if (active) {
-    i = M.s.cur_sorted[start + threadIdx.x];
+    i = M.s.cur_sorted[start + lane];
     a0 = M.kdesc[2 * (off + i)];
     a1 = M.kdesc[2 * (off + i) + 1];
     epi_line(M.s.F + 9 * r, M.ku[off + i], M.kv[off + i], l);
@@ -387,28 +393,42 @@ __global__ void __launch_bounds__(MATCH_TILE) k_match(DevMap* maps, const StepAr
   }
   const int maxd = A.mc.match_max_distance;
   unsigned long long best = ~0ull;
-  for (int t0 = jb; t0 < je; t0 += MATCH_JT) {
-    const int tn = je - t0 < MATCH_JT ? je - t0 : MATCH_JT;
+  for (int c0 = jb; c0 < je; c0 += MATCH_JT) {
+    const int cn = je - c0 < MATCH_JT ? je - c0 : MATCH_JT;
     __syncthreads();
-    for (int k = threadIdx.x; k < 2 * tn; k += MATCH_TILE) sd[k] = M.s.nb_desc[2 * (base + t0) + k];
+    for (int k = threadIdx.x; k < 2 * cn; k += MATCH_WARPS * 32) sd[k] = M.s.nb_desc[2 * (base + c0) + k];
     __syncthreads();
+    // this warp's slice of the chunk
+    const int per = (cn + MATCH_WARPS - 1) / MATCH_WARPS;
+    const int k0 = wid * per, k1 = k0 + per < cn ? k0 + per : cn;
     if (active) {
-      for (int k = 0; k < tn; ++k) {
-        const int dist = hamming(a0, a1, sd[2 * k], sd[2 * k + 1]);
+#pragma unroll 2
+      for (int k = k0; k < k1; ++k) {
+        const uint4 b0 = sd[2 * k];
+        int dist = __popc(a0.x ^ b0.x) + __popc(a0.y ^ b0.y) + __popc(a0.z ^ b0.z) + __popc(a0.w ^ b0.w);
         if (dist <= maxd) {
-          const size_t e = base + t0 + k;
-          if (epi_d2(l, den, M.s.nb_u[e], M.s.nb_v[e]) <= M.s.nb_thr[e]) {
-            const unsigned long long key = ((unsigned long long)dist << 32) | (unsigned)M.s.nb_j[e];
-            best = key < best ? key : best;
+          const uint4 b1 = sd[2 * k + 1];
+          dist += __popc(a1.x ^ b1.x) + __popc(a1.y ^ b1.y) + __popc(a1.z ^ b1.z) + __popc(a1.w ^ b1.w);
+          if (dist <= maxd) {
+            const size_t e = base + c0 + k;
+            if (epi_d2(l, den, M.s.nb_u[e], M.s.nb_v[e]) <= M.s.nb_thr[e]) {
+              const unsigned long long key = ((unsigned long long)dist << 32) | (unsigned)M.s.nb_j[e];
+              best = key < best ? key : best;
+            }
           }
         }
       }
     }
   }
-  if (active && best != ~0ull) {
-    M.s.pick[base + i] = best;
-    const unsigned j = (unsigned)(best & 0xffffffffu);
-    atomicMin(&M.s.bestj[base + j], (best & 0xffffffff00000000ull) | (unsigned)i);
+  if (active && best != ~0ull) atomicMin(&best_sh[lane], best);
+  __syncthreads();
+  if (wid == 0 && active) {
+    const unsigned long long b = best_sh[lane];
+    M.s.pick[base + i] = b;
+    if (b != ~0ull) {
+      const unsigned j = (unsigned)(b & 0xffffffffu);
+      atomicMin(&M.s.bestj[base + j], (b & 0xffffffff00000000ull) | (unsigned)i);
+    }
   }
 }
 
@@ -795,7 +815,7 @@ __device__ void apply_one(const DevMap& M, const ActRec& x, int* cnt) {
 }
 
 template <int BLOCK>
-__device__ void apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh) {
+__device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh) {
   __shared__ unsigned round_sh;
   __shared__ int npend_sh;
   for (int a = threadIdx.x; a < n; a += BLOCK) M.s.pend[a] = a;
@@ -841,6 +861,7 @@ __device__ void apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt
     __syncthreads();
     if (++guard > (1 << 20)) break;
   }
+  return guard;
 }
 
 // recompute the representative descriptor of every dirty point in pts[0..P) (warp per point)
@@ -985,8 +1006,11 @@ __device__ int fusion_targets(const DevMap& M, int cur, int n1, int n2, int n_sl
 // increments + compaction into M.s.acts; returns action count
 template <int BLOCK>
 __device__ int gather_pass(const DevMap& M, const lm_fuse_cfg& fc, int P, int ts, bool bump_visible, int* sh,
-                           int* vis_out) {
+                           int* vis_out, long long* cyc = nullptr) {
+  const long long c0 = clock64();
   refresh_points<BLOCK>(M, M.s.pts, P, sh);
+  if (cyc && threadIdx.x == 0) cyc[4] += clock64() - c0;
+  const long long c1 = clock64();
   for (int p = threadIdx.x; p < P; p += BLOCK) point_geometry(M, M.s.pts[p], fc.dist_band_slack, M.s.geo[p]);
   __syncthreads();
   int count = 0, nvis = 0;
@@ -1008,6 +1032,7 @@ __device__ int gather_pass(const DevMap& M, const lm_fuse_cfg& fc, int P, int ts
   }
   if (vis_out) *vis_out = block_sum<BLOCK>(nvis, sh);
   __syncthreads();
+  if (cyc && threadIdx.x == 0) cyc[5] += clock64() - c1;
   return count;
 }
 
@@ -1037,8 +1062,14 @@ __global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* arg
   __shared__ int cnt[3];
   const lm_fuse_cfg& fc = A.fc;
   const int cur = A.cur;
+  __shared__ long long cyc[8];
+  __shared__ int rounds;
   if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
+  if (threadIdx.x < 8) cyc[threadIdx.x] = 0;
+  if (threadIdx.x == 0) rounds = 0;
+  long long t0 = clock64();
   const int T = fusion_targets<1024>(M, cur, fc.n1, fc.n2, n_slots_max, sh_slot, sh_w, sh);
+  if (threadIdx.x == 0) cyc[0] += clock64() - t0;
   lm_step_stats* st = M.s.stats;
   if (T == 0) {
     if (threadIdx.x == 0) {
@@ -1058,12 +1089,15 @@ __global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* arg
     M.ledger[LG_SMALL_FUSE] += (unsigned long long)P * mpb;
     M.ledger[LG_SMALL_EVENTS] += 1;
   }
+  t0 = clock64();
   refresh_points<1024>(M, M.s.pts, P, sh);
   const long long fwd_obs = pass_obs<1024>(M, P, sh);
   long long tkp = 0;
   for (int k = 0; k < T; ++k) tkp += M.kp_n[M.s.targets[k]];
   for (int p = threadIdx.x; p < P; p += 1024) point_geometry(M, M.s.pts[p], fc.dist_band_slack, M.s.geo[p]);
   __syncthreads();
+  if (threadIdx.x == 0) cyc[1] += clock64() - t0;
+  t0 = clock64();
   const int TP = T * P;
   for (int it = threadIdx.x; it < TP; it += 1024) {
     const int t = it / P, p = it - t * P;
@@ -1091,11 +1125,19 @@ __global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* arg
   }
   long long alg = pass_bytes((long long)T * P, (long long)T * fwd_obs, tkp, nact);
   long long npts = (long long)T * P, nacts = nact;
-  apply_block<1024>(M, M.s.acts, nact, cnt, sh);
+  if (threadIdx.x == 0) cyc[2] += clock64() - t0;
+  t0 = clock64();
+  {
+    const int rr = apply_block<1024>(M, M.s.acts, nact, cnt, sh);
+    if (threadIdx.x == 0) rounds += rr;
+  }
+  if (threadIdx.x == 0) cyc[3] += clock64() - t0;
   // reverse: per target, its bound points into the current keyframe, gather then apply
   for (int t = 0; t < T; ++t) {
     const int ts = M.s.targets[t];
+    t0 = clock64();
     const int Pt = bound_points<1024>(M, ts, sh);
+    if (threadIdx.x == 0) cyc[7] += clock64() - t0;
     if (threadIdx.x == 0) {
       M.ledger[LG_NAIVE] += (unsigned long long)Pt * mpb;
       M.ledger[LG_PERSIST] += (unsigned long long)Pt * mpb;
@@ -1103,11 +1145,16 @@ __global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* arg
       M.ledger[LG_SMALL_EVENTS] += 1;
     }
     const long long ob = pass_obs<1024>(M, Pt, sh);
-    const int na = gather_pass<1024>(M, fc, Pt, cur, true, sh, nullptr);
+    const int na = gather_pass<1024>(M, fc, Pt, cur, true, sh, nullptr, cyc);
     alg += pass_bytes(Pt, ob, M.kp_n[cur], na);
     npts += Pt;
     nacts += na;
-    apply_block<1024>(M, M.s.acts, na, cnt, sh);
+    t0 = clock64();
+    const int rr = apply_block<1024>(M, M.s.acts, na, cnt, sh);
+    if (threadIdx.x == 0) {
+      rounds += rr;
+      cyc[6] += clock64() - t0;
+    }
   }
   if (threadIdx.x == 0) {
     st->n_targets = T;
@@ -1115,6 +1162,8 @@ __global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* arg
     st->fuse_passes = 2 * T;
     st->fuse_points = npts;
     st->fuse_actions = nacts;
+    st->apply_rounds = rounds;
+    for (int k = 0; k < 8; ++k) st->fuse_cycles[k] = cyc[k];
     st->merged = cnt[0];
     st->observations_added = cnt[1];
     st->stale = cnt[2];

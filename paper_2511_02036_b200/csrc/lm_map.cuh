@@ -31,8 +31,9 @@ constexpr int TMAX = LM_MAX_TARGETS;    // fusion targets per keyframe
 constexpr int LMAX = 16;                // pyramid levels
 constexpr int GRID_CELLS = 4096;        // cells per keyframe grid
 constexpr int REFRESH_MAXN = 512;       // observations handled by the rep-refresh fast path
-constexpr int MATCH_TILE = 128;         // current keypoints per match CTA
-constexpr int MATCH_JT = 256;           // neighbour descriptors staged per smem tile
+constexpr int MATCH_TILE = 32;          // current keypoints per match CTA (one per lane)
+constexpr int MATCH_WARPS = 8;          // warps per match CTA, each scanning a slice of j
+constexpr int MATCH_JT = 1024;          // neighbour descriptors staged per smem chunk
 
 enum KfState { KF_FREE = 0, KF_STAGED = 1, KF_LIVE = 2, KF_DEAD = 3 };
 enum Scal { SC_NEXT_ID = 0, SC_OBS_HEAD, SC_RECENT_N, SC_ERR, SC_DIRTY_N, SC_ROUND, SC_N = 8 };

@@ -344,7 +344,8 @@ class TestMapModel:
         p = m2.new_map_point(np.zeros(3), base, 0)
         for k in range(5):
             m2.add_observation(p.mp_id, k, 0)
-        d = np.array([[int(np.bitwise_count(a ^ b).sum()) for b in kfs_d] for a in (kfs_d := [kf.descriptors[0] for kf in kfs])], float)
+        descs = [kf.descriptors[0] for kf in kfs]
+        d = np.array([[int(np.bitwise_count(a ^ b).sum()) for b in descs] for a in descs], float)
         np.fill_diagonal(d, np.nan)
         best = int(np.argmin(np.nanmedian(d, axis=1)))
         assert np.array_equal(m2.points[p.mp_id].rep_descriptor, kfs[best].descriptors[0])
