@@ -115,9 +115,9 @@ typedef struct lm_step_stats { /* CreationStats triangulation.py:49-60 + run_fus
   int64_t fuse_bytes;   /* algorithmic fusion bytes, SURVEY.md 8(d) formula */
   int64_t fuse_passes, fuse_points, fuse_actions;
   int64_t apply_rounds;      /* deterministic-reservation rounds over all applies */
-  int64_t fuse_cycles[8];    /* SM cycles per fusion phase: targets, fwd refresh+geometry,
+  int64_t fuse_cycles[8];    /* ns per fusion phase (%globaltimer): targets, fwd refresh+geometry,
                                 fwd gather, fwd apply, rev refresh, rev geometry+gather,
-                                rev apply, rev bound-point scan */
+                                rev apply, whole k_fuse */
 } lm_step_stats;
 
 typedef struct lm_candidate { /* MatchCandidate triangulation.py:41-46 */

@@ -36,6 +36,12 @@ struct StepArgs {
 
 // ---------------------------------------------------------------------------------- helpers
 
+__device__ __forceinline__ long long gtime() {  // ns, device-wide clock
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return (long long)t;
+}
+
 template <int BLOCK>
 __device__ __forceinline__ int block_excl_scan(int v, int* sh, int& total) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1007,10 +1013,10 @@ __device__ int fusion_targets(const DevMap& M, int cur, int n1, int n2, int n_sl
 template <int BLOCK>
 __device__ int gather_pass(const DevMap& M, const lm_fuse_cfg& fc, int P, int ts, bool bump_visible, int* sh,
                            int* vis_out, long long* cyc = nullptr) {
-  const long long c0 = clock64();
+  const long long c0 = gtime();
   refresh_points<BLOCK>(M, M.s.pts, P, sh);
-  if (cyc && threadIdx.x == 0) cyc[4] += clock64() - c0;
-  const long long c1 = clock64();
+  if (cyc && threadIdx.x == 0) cyc[4] += gtime() - c0;
+  const long long c1 = gtime();
   for (int p = threadIdx.x; p < P; p += BLOCK) point_geometry(M, M.s.pts[p], fc.dist_band_slack, M.s.geo[p]);
   __syncthreads();
   int count = 0, nvis = 0;
@@ -1032,7 +1038,7 @@ __device__ int gather_pass(const DevMap& M, const lm_fuse_cfg& fc, int P, int ts
   }
   if (vis_out) *vis_out = block_sum<BLOCK>(nvis, sh);
   __syncthreads();
-  if (cyc && threadIdx.x == 0) cyc[5] += clock64() - c1;
+  if (cyc && threadIdx.x == 0) cyc[5] += gtime() - c1;
   return count;
 }
 
@@ -1067,9 +1073,10 @@ __global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* arg
   if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
   if (threadIdx.x < 8) cyc[threadIdx.x] = 0;
   if (threadIdx.x == 0) rounds = 0;
-  long long t0 = clock64();
+  const long long t_begin = gtime();
+  long long t0 = gtime();
   const int T = fusion_targets<1024>(M, cur, fc.n1, fc.n2, n_slots_max, sh_slot, sh_w, sh);
-  if (threadIdx.x == 0) cyc[0] += clock64() - t0;
+  if (threadIdx.x == 0) cyc[0] += gtime() - t0;
   lm_step_stats* st = M.s.stats;
   if (T == 0) {
     if (threadIdx.x == 0) {
@@ -1089,15 +1096,15 @@ __global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* arg
     M.ledger[LG_SMALL_FUSE] += (unsigned long long)P * mpb;
     M.ledger[LG_SMALL_EVENTS] += 1;
   }
-  t0 = clock64();
+  t0 = gtime();
   refresh_points<1024>(M, M.s.pts, P, sh);
   const long long fwd_obs = pass_obs<1024>(M, P, sh);
   long long tkp = 0;
   for (int k = 0; k < T; ++k) tkp += M.kp_n[M.s.targets[k]];
   for (int p = threadIdx.x; p < P; p += 1024) point_geometry(M, M.s.pts[p], fc.dist_band_slack, M.s.geo[p]);
   __syncthreads();
-  if (threadIdx.x == 0) cyc[1] += clock64() - t0;
-  t0 = clock64();
+  if (threadIdx.x == 0) cyc[1] += gtime() - t0;
+  t0 = gtime();
   const int TP = T * P;
   for (int it = threadIdx.x; it < TP; it += 1024) {
     const int t = it / P, p = it - t * P;
@@ -1125,19 +1132,17 @@ __global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* arg
   }
   long long alg = pass_bytes((long long)T * P, (long long)T * fwd_obs, tkp, nact);
   long long npts = (long long)T * P, nacts = nact;
-  if (threadIdx.x == 0) cyc[2] += clock64() - t0;
-  t0 = clock64();
+  if (threadIdx.x == 0) cyc[2] += gtime() - t0;
+  t0 = gtime();
   {
     const int rr = apply_block<1024>(M, M.s.acts, nact, cnt, sh);
     if (threadIdx.x == 0) rounds += rr;
   }
-  if (threadIdx.x == 0) cyc[3] += clock64() - t0;
+  if (threadIdx.x == 0) cyc[3] += gtime() - t0;
   // reverse: per target, its bound points into the current keyframe, gather then apply
   for (int t = 0; t < T; ++t) {
     const int ts = M.s.targets[t];
-    t0 = clock64();
     const int Pt = bound_points<1024>(M, ts, sh);
-    if (threadIdx.x == 0) cyc[7] += clock64() - t0;
     if (threadIdx.x == 0) {
       M.ledger[LG_NAIVE] += (unsigned long long)Pt * mpb;
       M.ledger[LG_PERSIST] += (unsigned long long)Pt * mpb;
@@ -1149,11 +1154,11 @@ __global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* arg
     alg += pass_bytes(Pt, ob, M.kp_n[cur], na);
     npts += Pt;
     nacts += na;
-    t0 = clock64();
+    t0 = gtime();
     const int rr = apply_block<1024>(M, M.s.acts, na, cnt, sh);
     if (threadIdx.x == 0) {
       rounds += rr;
-      cyc[6] += clock64() - t0;
+      cyc[6] += gtime() - t0;
     }
   }
   if (threadIdx.x == 0) {
@@ -1163,7 +1168,8 @@ __global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* arg
     st->fuse_points = npts;
     st->fuse_actions = nacts;
     st->apply_rounds = rounds;
-    for (int k = 0; k < 8; ++k) st->fuse_cycles[k] = cyc[k];
+    for (int k = 0; k < 7; ++k) st->fuse_cycles[k] = cyc[k];
+    st->fuse_cycles[7] = gtime() - t_begin;  // whole kernel (thread 0 view)
     st->merged = cnt[0];
     st->observations_added = cnt[1];
     st->stale = cnt[2];
