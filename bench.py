@@ -50,8 +50,23 @@ def load_workload(name: str, seed: int | None):
 
 
 def stage_params(name):
-    n, n1, n2 = W.BENCH_STAGE[name]
+    n, n1, n2 = W.BENCH_STAGE["c2" if name == "c5" else name]
     return n, MatchConfig(neighbor_count=n), FuseConfig(n1=n1, n2=n2)
+
+
+def _gen(seed):
+    return W.generate_sequence(W.bench_world("c2", seed))
+
+
+def load_sessions(seeds: list[int]):
+    """C5: independent C2-shaped sequences (seeds 5000..5063), generated in parallel."""
+    from concurrent.futures import ProcessPoolExecutor
+
+    workers = max(1, min(len(seeds), (os.cpu_count() or 2) - 1))
+    if workers == 1:
+        return [_gen(s) for s in seeds]
+    with ProcessPoolExecutor(workers) as ex:
+        return list(ex.map(_gen, seeds))
 
 
 class ClockSampler:
@@ -158,7 +173,13 @@ def run_reference(args):
 
 def config_of(args, seq=None):
     n, mc, fc = stage_params(args.workload)
-    c = W.BENCH_CONFIGS[args.workload]
+    c = W.BENCH_CONFIGS["c2" if args.workload == "c5" else args.workload]
+    if args.workload == "c5":
+        return {"workload": f"c5: {args.sessions} independent EuRoC-shaped sessions (seeds 5000+), batched per GPU",
+                "sessions": args.sessions, "keyframes_per_session": c["keyframe_count"] if args.kfs is None else args.kfs,
+                "features_per_kf": c["features_per_kf"], "neighbor_count": n, "fusion_n1": fc.n1, "fusion_n2": fc.n2,
+                "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write)",
+                "step": "every session's whole sequence, one batched launch sequence per keyframe index"}
     return {"workload": f"{args.workload}: EuRoC-shaped synthetic sequence" if args.workload == "c2" else args.workload,
             "keyframes": c["keyframe_count"] if args.kfs is None else args.kfs,
             "features_per_kf": c["features_per_kf"], "image": [c.get("width", 640), c.get("height", 480)],
@@ -173,7 +194,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(W.BENCH_CONFIGS))
+    ap.add_argument("--workload", default="c2", choices=sorted(W.BENCH_CONFIGS) + ["c5"])
+    ap.add_argument("--sessions", type=int, default=64, help="c5: total sessions over all ranks")
     ap.add_argument("--kfs", type=int, default=None, help="limit keyframes per step (debug)")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=8.0)
@@ -200,6 +222,9 @@ def main():
     from paper_2511_02036_b200.session import LocalMapper, store_for
     from paper_2511_02036_b200.mapmodel import KeyFrame
 
+    if args.workload == "c5":
+        run_c5(args, rank, world, local, dist)
+        return
     seed = W.BENCH_CONFIGS[args.workload]["seed"] + 1000 * rank
     seq = load_workload(args.workload, seed)
     recs = seq.records if args.kfs is None else seq.records[:args.kfs]
@@ -244,25 +269,34 @@ def main():
     for _ in range(args.warmup):
         one_step(False)
     lib.lm_profile_enable(ctx.h, 1)
-    lib.lm_profile_read(ctx.h, (C.c_double * 8)(), (C.c_int64 * 8)())  # drop warm-up events
+    lib.lm_profile_read(ctx.h, (C.c_double * 16)(), (C.c_int64 * 16)())  # drop warm-up events
     sampler = ClockSampler(local)
     launches0 = lib.lm_launch_count(ctx.h)
     step_ms = []
+    acc = {}
     totals = _lib.StepStats()
     for _ in range(args.steps):
         ms = one_step(True)
         step_ms.append(max_over_ranks(ms))
-        ctx.call("lm_totals_fetch", mapper.map, C.byref(totals))
+        ctx.call("lm_totals_fetch", mapper.map, C.byref(totals))  # this step's totals (rewind clears)
         if totals.error:
             raise RuntimeError(f"device error {totals.error}")
+        for f, _ in _lib.StepStats._fields_:
+            v = getattr(totals, f)
+            if isinstance(v, int):
+                acc[f] = acc.get(f, 0) + v
+            elif f == "fuse_cycles":
+                acc[f] = [a + b for a, b in zip(acc.get(f, [0] * 8), list(v))]
     launches = lib.lm_launch_count(ctx.h) - launches0
     clocks = sampler.stop()
-    prof_ms = (C.c_double * 8)()
-    prof_n = (C.c_int64 * 8)()
+    prof_ms = (C.c_double * 16)()
+    prof_n = (C.c_int64 * 16)()
     lib.lm_profile_read(ctx.h, prof_ms, prof_n)
     lib.lm_profile_enable(ctx.h, 0)
-    stages = ["insert", "cull", "select", "prep", "match", "tri", "commit", "fuse"]
+    stages = ["insert", "cull", "select", "prep", "match", "tri", "commit", "fuse_targets", "fuse_geo",
+              "fuse_gather", "fuse_apply", "fuse_refresh", "fuse_rev"]
     stage_ms = {s: prof_ms[k] / args.steps for k, s in enumerate(stages)}
+    stage_ms["fuse"] = sum(stage_ms[s] for s in stages if s.startswith("fuse"))
     mean_ms = sum(step_ms) / len(step_ms)
     total_kf = len(ids) * world
     value = total_kf / (mean_ms * 1e-3)
@@ -288,8 +322,8 @@ def main():
 
     # -------- roofline of the dominant kernel + the matching kernel's popc roofline
     peaks = measured_peaks()
-    per_step_bytes = totals.fuse_bytes / args.steps
-    per_step_pairs = totals.match_pairs / args.steps
+    per_step_bytes = acc["fuse_bytes"] / args.steps
+    per_step_pairs = acc["match_pairs"] / args.steps
     popc_peak = C.c_double()
     ctx.call("lm_bench_popc", C.byref(popc_peak))
     dom = max(stage_ms, key=stage_ms.get)
@@ -297,8 +331,8 @@ def main():
     match_s = stage_ms["match"] * 1e-3
     hbm_peak = peaks.get("hbm_gbs", 6457.4)
     fuse_gbs = per_step_bytes / fuse_s / 1e9 if fuse_s > 0 else 0.0
-    roofline = {"kernel": "k_fuse", "bound": "hbm", "achieved": fuse_gbs, "peak": hbm_peak, "unit": "GB/s",
-                "frac": fuse_gbs / hbm_peak, "traffic": ncu_traffic("k_fuse"),
+    roofline = {"kernel": "k_fuse_* (SearchAndFuse stage)", "bound": "hbm", "achieved": fuse_gbs, "peak": hbm_peak, "unit": "GB/s",
+                "frac": fuse_gbs / hbm_peak, "traffic": ncu_traffic("k_fuse_rev"),
                 "algorithmic_bytes_per_launch": per_step_bytes / len(ids), "launch_ms": stage_ms["fuse"] / len(ids),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback",
                 "dominant_stage": dom}
@@ -316,13 +350,13 @@ def main():
             "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
             "roofline_popc": roof_popc, "stage_ms_per_step": stage_ms,
             "work_per_step": {"keyframes": len(ids), "match_pairs": per_step_pairs, "fuse_bytes": per_step_bytes,
-                              "created": totals.created / args.steps, "merged": totals.merged / args.steps,
-                              "observations_added": totals.observations_added / args.steps,
-                              "apply_rounds": totals.apply_rounds / args.steps},
-            "fuse_phase_ms_per_step": {n: totals.fuse_cycles[k] / args.steps / 1e6
-                                       for k, n in enumerate(["targets", "fwd_refresh_geometry", "fwd_gather",
-                                                              "fwd_apply", "rev_refresh", "rev_geometry_gather",
-                                                              "rev_apply", "k_fuse_total"])}}
+                              "created": acc["created"] / args.steps, "merged": acc["merged"] / args.steps,
+                              "observations_added": acc["observations_added"] / args.steps,
+                              "apply_rounds": acc["apply_rounds"] / args.steps},
+            "fuse_phase_ms_per_step": {n: acc["fuse_cycles"][k] / args.steps / 1e6
+                                       for k, n in enumerate(["targets", "-", "fwd_assemble", "fwd_apply",
+                                                              "rev_refresh", "rev_geometry_gather", "rev_apply", "-"])
+                                       if n != "-"}}
     if rank == 0 and world == 1 and not args.no_cpu:
         done, dt = cpu_sample(seq, args.workload, args.cpu_budget)
         line["cpu_baseline"] = {"value": done / dt, "unit": UNIT, "cores": 1, "kind": "port",
@@ -332,6 +366,75 @@ def main():
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def run_c5(args, rank, world, local, dist):
+    """Batched sessions: this rank's contiguous shard of the C5 sessions advances in
+    lock-step, one batched launch sequence (all its maps) per keyframe index."""
+    from paper_2511_02036_b200 import _lib
+    from paper_2511_02036_b200.mapmodel import KeyFrame
+    from paper_2511_02036_b200.session import LocalMapper, SessionBatch, store_for
+    from paper_2511_02036_b200.sharding import max_over_ranks, session_seeds
+
+    seeds = session_seeds(5000, args.sessions, world, rank)
+    seqs = load_sessions(seeds)
+    n, mc, fc = stage_params("c5")
+    ctx = _lib.Context.get(local)
+    lib = ctx.lib
+    mappers, kf_lists = [], []
+    for seq in seqs:
+        recs = seq.records if args.kfs is None else seq.records[:args.kfs]
+        intr = seq.intrinsics()
+        kfs = [KeyFrame(int(r.kf_id), r.pose_init, intr, r.kp_u, r.kp_v, r.kp_level, r.descriptors) for r in recs]
+        m = LocalMapper(intr, neighbor_count=n, match=mc, fuse=fc, ctx=ctx,
+                        store=store_for(len(kfs), max(k.num_keypoints for k in kfs) + 64))
+        for kf in kfs:
+            m.stage(kf)
+        mappers.append(m)
+        kf_lists.append([kf.kf_id for kf in kfs])
+    batch = SessionBatch(mappers)
+    n_kf = min(len(x) for x in kf_lists)
+    dev = f"cuda:{local}" if dist is not None else None
+
+    def one_step():
+        for m in mappers:
+            ctx.call("lm_map_rewind", m.map)
+            m.processed = 0
+        lib.lm_flush_l2(ctx.h, L2_FLUSH_BYTES)
+        ctx.call("lm_synchronize")
+        if dist is not None:
+            dist.barrier()
+        ctx.call("lm_timer_start")
+        for k in range(n_kf):
+            batch.step([ids[k] for ids in kf_lists], sync=False)
+        ms = C.c_float()
+        ctx.call("lm_timer_stop", C.byref(ms))
+        return ms.value
+
+    for _ in range(args.warmup):
+        one_step()
+    sampler = ClockSampler(local)
+    l0 = lib.lm_launch_count(ctx.h)
+    times = [max_over_ranks(one_step(), dev) for _ in range(args.steps)]
+    launches = lib.lm_launch_count(ctx.h) - l0
+    clocks = sampler.stop()
+    tot_err = 0
+    for m in mappers:
+        t = _lib.StepStats()
+        ctx.call("lm_totals_fetch", m.map, C.byref(t))
+        tot_err |= t.error
+    if tot_err:
+        raise RuntimeError(f"device error {tot_err}")
+    mean_ms = sum(times) / len(times)
+    total_kf = n_kf * args.sessions
+    line = {"metric": METRIC, "value": total_kf / (mean_ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms,
+            "ms_per_keyframe": mean_ms / n_kf, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32 popc / f64 geometry", "data": "synthetic", "config": config_of(args),
+            "parallelism": f"{args.sessions} sessions sharded contiguously over {world} GPU(s), batched launches",
+            "sessions_this_rank": len(seeds), "clocks": clocks, "gpu_launches": int(launches), "e2e": None}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

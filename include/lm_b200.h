@@ -115,9 +115,8 @@ typedef struct lm_step_stats { /* CreationStats triangulation.py:49-60 + run_fus
   int64_t fuse_bytes;   /* algorithmic fusion bytes, SURVEY.md 8(d) formula */
   int64_t fuse_passes, fuse_points, fuse_actions;
   int64_t apply_rounds;      /* deterministic-reservation rounds over all applies */
-  int64_t fuse_cycles[8];    /* ns per fusion phase (%globaltimer): targets, fwd refresh+geometry,
-                                fwd gather, fwd apply, rev refresh, rev geometry+gather,
-                                rev apply, whole k_fuse */
+  int64_t fuse_cycles[8];    /* ns per fusion phase (%globaltimer): targets, -, fwd assemble,
+                                fwd apply, rev refresh, rev geometry+gather, rev apply, - */
 } lm_step_stats;
 
 typedef struct lm_candidate { /* MatchCandidate triangulation.py:41-46 */
@@ -226,9 +225,10 @@ int64_t lm_launch_count(lm_ctx* ctx);
 /* Running totals since map creation/reset/rewind (first_new_id holds the step count). */
 int lm_totals_fetch(lm_ctx* ctx, int32_t map, lm_step_stats* out);            /* kernels launched by this context so far */
 /* Per-stage CUDA-event timing of the step kernels (stage order: begin+insert, cull, select,
- * prep, match, tri, commit, fuse). Enabling adds two events per stage per step. */
+ * prep, match, tri, commit, fuse_targets, fuse_geo, fuse_gather, fuse_apply, fuse_refresh,
+ * fuse_rev+end). Enabling adds one event per stage boundary per step. */
 int lm_profile_enable(lm_ctx* ctx, int32_t on);
-int lm_profile_read(lm_ctx* ctx, double ms[8], int64_t launches[8]); /* sums, then clears */
+int lm_profile_read(lm_ctx* ctx, double ms[16], int64_t launches[16]); /* sums, then clears */
 /* Sustained __popc throughput of this device (popc32 results per second). */
 int lm_bench_popc(lm_ctx* ctx, double* popc_per_s);
 

@@ -229,7 +229,7 @@ struct OpArgs {
 
 __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, int* res) {
   const DevMap& M = maps[map];
-  extern __shared__ int dyn[];
+  extern __shared__ __align__(16) int dyn[];
   __shared__ int sh[32];
   __shared__ int out_nb[1024];
   const int tid = threadIdx.x;
@@ -254,6 +254,8 @@ __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, in
       M.nobs[id] = 0;
       M.ocap[id] = 0;
       M.ooff[id] = 0;
+      M.gval[id] = 0;
+      M.dirty[id] = 0;
       res[0] = LM_OK;
       res[1] = id;
       return;
@@ -344,9 +346,9 @@ __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, in
       return;
     }
     case OP_NEIGHBORS: {
-      int* sh_slot = dyn;
-      int* sh_w = dyn + M.kf_cap;
-      const int got = ranked_neighbors<1024>(M, A.a, A.n, sh_slot, sh_w, out_nb, sh, A.n_slots);
+      unsigned long long* sh_key = (unsigned long long*)dyn;
+      int* sh_slot = (int*)(sh_key + M.kf_cap);
+      const int got = ranked_neighbors<1024>(M, A.a, A.n, sh_slot, sh_key, out_nb, A.n_slots);
       for (int k = tid; k < got; k += 1024) res[2 + k] = out_nb[k];
       if (tid == 0) {
         res[0] = LM_OK;
@@ -361,9 +363,11 @@ __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, in
     }
     case OP_APPLY: {
       __shared__ int c[3];
+      __shared__ PairAcc acc;
       if (tid < 3) c[tid] = 0;
-      __syncthreads();
-      apply_block<1024>(M, M.s.acts, A.n, c, sh);
+      pair_acc_init<1024>(&acc);
+      apply_block<1024>(M, M.s.acts, A.n, c, sh, &acc);
+      pair_acc_flush<1024>(M, &acc);
       if (tid == 0) {
         res[0] = M.scal[SC_ERR];
         res[1] = c[0];
@@ -373,9 +377,9 @@ __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, in
       return;
     }
     case OP_TARGETS: {
-      int* sh_slot = dyn;
-      int* sh_w = dyn + M.kf_cap;
-      const int T = fusion_targets<1024>(M, A.a, A.fc.n1, A.fc.n2, A.n_slots, sh_slot, sh_w, sh);
+      unsigned long long* sh_key = (unsigned long long*)dyn;
+      int* sh_slot = (int*)(sh_key + M.kf_cap);
+      const int T = fusion_targets<1024>(M, A.a, A.fc.n1, A.fc.n2, A.n_slots, sh_slot, sh_key);
       if (tid == 0) {
         res[0] = LM_OK;
         res[1] = T;
@@ -399,7 +403,7 @@ __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, in
 
 static int run_op(lm_ctx* ctx, HostMap* m, int map, OpArgs& a, int* res_host, int nres) {
   a.n_slots = m->n_slots;
-  const size_t dyn = 2 * sizeof(int) * m->d.kf_cap;
+  const size_t dyn = 12 * (size_t)m->d.kf_cap;
   k_op<<<1, 1024, dyn, ctx->stream>>>(ctx->d_maps, map, a, m->d_result);
   CHECK_LAUNCH();
   ctx->launches += 1;
@@ -450,9 +454,9 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
     ctx->h_stage[i] = nullptr;
     ctx->d_stage[i] = nullptr;
   }
-  CU(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-  CU(cudaFuncSetAttribute(k_fuse, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-  CU(cudaFuncSetAttribute(k_op, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+  CU(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+  CU(cudaFuncSetAttribute(k_fuse_targets, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+  CU(cudaFuncSetAttribute(k_op, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
   *out = ctx;
   return LM_OK;
 }
@@ -528,6 +532,7 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(d.pos, 3 * MP); A(d.rep, 2 * MP); A(d.alive, MP); A(d.found, MP); A(d.visible, MP); A(d.first_kf, MP);
   A(d.nobs, MP); A(d.ocap, MP); A(d.ooff, MP); A(d.obs, (size_t)d.obs_cap); A(d.counts, MP * d.L);
   A(d.dirty, MP); A(d.dirty_list, MP); A(d.res_pt, MP); A(d.res_slot, KP);
+  A(d.gacc, 3 * MP); A(d.glo, MP); A(d.ghi, MP); A(d.gval, MP);
   A(d.covis, K * K);
   A(d.recent_id, MP); A(d.recent_born, MP);
   A(d.scal, SC_N); A(d.ledger, LG_N);
@@ -539,12 +544,13 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(s.nb_u, NK); A(s.nb_v, NK); A(s.nb_thr, NK); A(s.pick, NK); A(s.bestj, NK);
   A(s.cand_n, NMAX); A(s.cand_i, NK); A(s.cand_j, NK); A(s.cand_d, NK); A(s.cand_st, NK); A(s.cand_X, 3 * NK);
   A(s.win_rank, d.kpkf_max); A(s.mask_cur, d.kpkf_max); A(s.mask_nbr, d.kpkf_max);
-  A(s.targets, TMAX); A(s.n_targets, 1); A(s.rank_buf, (size_t)TMAX * (2 * K + 1));
+  A(s.targets, TMAX); A(s.n_targets, 1); A(s.rank_buf, (size_t)TMAX * (3 * K + 1) + (size_t)TMAX * K * 2 + 2);
   s.pts_cap = d.kpkf_max;
   A(s.pts, s.pts_cap); A(s.geo, s.pts_cap);
   s.act_cap = TMAX * d.kpkf_max;
   A(s.acts, (size_t)s.act_cap); A(s.act_flag, (size_t)s.act_cap); A(s.vis_flag, (size_t)s.act_cap);
-  A(s.pend, (size_t)s.act_cap); A(s.ready, (size_t)s.act_cap);
+  A(s.pend, (size_t)s.act_cap); A(s.ready, (size_t)s.act_cap); A(s.acts2, (size_t)s.act_cap);
+  A(s.blk_cnt, (size_t)s.act_cap / 256 + 2); A(s.blk_off, (size_t)s.act_cap / 256 + 2); A(s.fctl, 8);
   A(m->d_stats, 1); A(m->d_totals, 1); A(m->d_result, 4 + 1024 + TMAX);
 #undef A
   s.stats = m->d_stats;
@@ -572,6 +578,7 @@ int lm_map_reset(lm_ctx* ctx, int32_t map) {
   CU(cudaMemsetAsync(d.ocap, 0, sizeof(int) * MP, ctx->stream));
   CU(cudaMemsetAsync(d.counts, 0, sizeof(int) * MP * d.L, ctx->stream));
   CU(cudaMemsetAsync(d.dirty, 0, sizeof(int) * MP, ctx->stream));
+  CU(cudaMemsetAsync(d.gval, 0, MP, ctx->stream));
   CU(cudaMemsetAsync(d.scal, 0, sizeof(int) * SC_N, ctx->stream));
   CU(cudaMemsetAsync(d.ledger, 0, sizeof(unsigned long long) * LG_N, ctx->stream));
   CU(cudaMemsetAsync(m->d_totals, 0, sizeof(lm_step_stats), ctx->stream));
@@ -723,13 +730,18 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   if (ctx->args_used[e]) CU(cudaEventSynchronize(ctx->args_ev[e]));
   StepArgs* h = ctx->h_args + (size_t)e * kMaxBatch;
   StepArgs* dv = ctx->d_args + (size_t)e * kMaxBatch;
-  int tiles = 1, slots = 1, kfcap = 2, nbr_dim = 1;
+  int tiles = 1, slots = 1, kfcap = 2, nbr_dim = 1, kpkf = 1, tfuse = 1;
   for (int k = 0; k < n; ++k) {
     HostMap* m = ctx->maps[maps[k]];
     h[k] = args[k];
     h[k].map = maps[k];
     const int want = args[k].explicit_nbr ? 1 : (args[k].n_nbr_req < NMAX ? args[k].n_nbr_req : NMAX);
     nbr_dim = want > nbr_dim ? want : nbr_dim;
+    kpkf = m->d.kpkf_max > kpkf ? m->d.kpkf_max : kpkf;
+    if (args[k].do_fuse) {
+      const int tf = args[k].fc.n1 + args[k].fc.n1 * args[k].fc.n2;
+      tfuse = tf > tfuse ? (tf < TMAX ? tf : TMAX) : tfuse;
+    }
     const int t = m->d.kpkf_max / MATCH_TILE + m->d.L + 1;
     tiles = t > tiles ? t : tiles;
     slots = m->n_slots > slots ? m->n_slots : slots;
@@ -737,7 +749,7 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   }
   DevMap* dmaps = ctx->d_maps;
   CU(cudaMemcpyAsync(dv, h, sizeof(StepArgs) * n, cudaMemcpyHostToDevice, ctx->stream));
-  const size_t dyn = 2 * sizeof(int) * kfcap;
+  const size_t dyn = 12 * (size_t)kfcap;
   std::vector<cudaEvent_t> evs;
   auto mark = [&]() -> int {
     if (!ctx->prof) return LM_OK;
@@ -769,10 +781,20 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   if ((rc = mark())) return rc;
   k_commit<<<n, 1024, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;
-  k_fuse<<<n, 1024, dyn, ctx->stream>>>(dmaps, dv, slots);
+  k_fuse_targets<<<n, 1024, dyn, ctx->stream>>>(dmaps, dv, slots);
+  if ((rc = mark())) return rc;
+  k_fuse_geo<<<dim3((kpkf + 7) / 8, n), 256, 0, ctx->stream>>>(dmaps, dv);
+  if ((rc = mark())) return rc;
+  k_fuse_gather<<<dim3((tfuse * kpkf + 255) / 256, n), 256, 0, ctx->stream>>>(dmaps, dv);
+  if ((rc = mark())) return rc;
+  k_fuse_apply<<<n, 1024, 0, ctx->stream>>>(dmaps, dv);
+  if ((rc = mark())) return rc;
+  k_fuse_refresh<<<dim3(148, n), 256, 0, ctx->stream>>>(dmaps, dv);
+  if ((rc = mark())) return rc;
+  k_fuse_rev<<<n, 1024, 0, ctx->stream>>>(dmaps, dv);
   k_end<<<n, 32, 0, ctx->stream>>>(dmaps, dv, ctx->d_totals);
   if ((rc = mark())) return rc;
-  ctx->launches += 10;
+  ctx->launches += 15;
   if (ctx->prof) ctx->prof_steps.push_back(evs);
   CHECK_LAUNCH();
   CU(cudaEventRecord(ctx->args_ev[e], ctx->stream));
@@ -1376,6 +1398,7 @@ int lm_map_rewind(lm_ctx* ctx, int32_t map) {
   CU(cudaMemsetAsync(d.ocap, 0, sizeof(int) * MP, st));
   CU(cudaMemsetAsync(d.counts, 0, sizeof(int) * MP * d.L, st));
   CU(cudaMemsetAsync(d.dirty, 0, sizeof(int) * MP, st));
+  CU(cudaMemsetAsync(d.gval, 0, MP, st));
   CU(cudaMemsetAsync(d.scal, 0, sizeof(int) * SC_N, st));
   CU(cudaMemsetAsync(d.ledger, 0, sizeof(unsigned long long) * LG_N, st));
   CU(cudaMemsetAsync(m->d_totals, 0, sizeof(lm_step_stats), st));
@@ -1436,14 +1459,14 @@ int lm_profile_enable(lm_ctx* ctx, int32_t on) {
   return LM_OK;
 }
 
-int lm_profile_read(lm_ctx* ctx, double ms[8], int64_t launches[8]) {
+int lm_profile_read(lm_ctx* ctx, double ms[16], int64_t launches[16]) {
   CU(cudaStreamSynchronize(ctx->stream));
-  for (int k = 0; k < 8; ++k) {
+  for (int k = 0; k < 16; ++k) {
     ms[k] = 0;
     launches[k] = 0;
   }
   for (auto& evs : ctx->prof_steps) {
-    for (size_t k = 0; k + 1 < evs.size() && k < 8; ++k) {
+    for (size_t k = 0; k + 1 < evs.size() && k < 16; ++k) {
       float t = 0;
       CU(cudaEventElapsedTime(&t, evs[k], evs[k + 1]));
       ms[k] += t;

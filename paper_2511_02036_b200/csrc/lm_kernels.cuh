@@ -80,12 +80,17 @@ __device__ __forceinline__ long long payload_bytes(const DevMap& M, int slot) {
   return (long long)M.kp_n[slot] * (M.kp_rec_bytes + M.desc_bytes);
 }
 
+// rank key of a covisibility entry: weight descending, then keyframe id ascending
+__device__ __forceinline__ unsigned long long covis_key(const DevMap& M, int slot, int w) {
+  return ((unsigned long long)(0x7fffffff - w) << 32) | (unsigned)M.kf_id[slot];
+}
+
 // covisible_neighbors(k, n) (mapmodel.py:269-273 + CovisibilityGraph.neighbors 100-105):
 // live slots with weight >= min_w, ordered by (-weight, kf_id). Block-cooperative:
-// compacts the row into sh_slot/sh_w, ranks each entry by counting better entries and
-// scatters to out[rank]; returns min(count, n) (n < 0: all).
+// compacts the row into shared (slot, key) pairs, ranks each entry by counting smaller
+// keys and scatters to out[rank]; returns min(count, n) (n < 0: all).
 template <int BLOCK>
-__device__ int ranked_neighbors(const DevMap& M, int k, int n, int* sh_slot, int* sh_w, int* out, int* sh_scan,
+__device__ int ranked_neighbors(const DevMap& M, int k, int n, int* sh_slot, unsigned long long* sh_key, int* out,
                                 int n_slots) {
   __shared__ int cnt;
   if (threadIdx.x == 0) cnt = 0;
@@ -96,20 +101,16 @@ __device__ int ranked_neighbors(const DevMap& M, int k, int n, int* sh_slot, int
     if (w >= M.min_w && w > 0 && s != k && M.kf_state[s] == KF_LIVE) {
       const int at = atomicAdd(&cnt, 1);
       sh_slot[at] = s;
-      sh_w[at] = w;
+      sh_key[at] = covis_key(M, s, w);
     }
   }
   __syncthreads();
   const int c = cnt;
   const int lim = n < 0 ? c : (n < c ? n : c);
   for (int e = threadIdx.x; e < c; e += BLOCK) {
-    const int we = sh_w[e];
-    const long long ie = M.kf_id[sh_slot[e]];
+    const unsigned long long ke = sh_key[e];
     int r = 0;
-    for (int f = 0; f < c; ++f) {
-      const int wf = sh_w[f];
-      r += (wf > we) || (wf == we && M.kf_id[sh_slot[f]] < ie);
-    }
+    for (int f = 0; f < c; ++f) r += sh_key[f] < ke;
     if (r < lim) out[r] = sh_slot[e];
   }
   __syncthreads();
@@ -156,6 +157,8 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
   const DevMap& M = maps[A.map];
   if (!A.do_cull) return;
   __shared__ int sh[32];
+  __shared__ PairAcc acc;
+  pair_acc_init<1024>(&acc);
   const int n = M.scal[SC_RECENT_N];
   int kept = 0, culled = 0;
   for (int base = 0; base < n; base += 1024) {
@@ -167,11 +170,11 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
       if (M.alive[id]) {
         const double ratio = (double)M.found[id] / (double)(M.visible[id] > 1 ? M.visible[id] : 1);
         if (ratio < A.cc.found_ratio_min) {
-          kill_point(M, id);
+          kill_point(M, id, &acc);
           ++culled;
         } else if (A.processed - born >= A.cc.probation_kfs) {
           if (M.nobs[id] < A.cc.min_obs_graduate) {
-            kill_point(M, id);
+            kill_point(M, id, &acc);
             ++culled;
           }
         } else {
@@ -189,6 +192,7 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
     __syncthreads();
   }
   const int tc = block_sum<1024>(culled, sh);
+  pair_acc_flush<1024>(M, &acc);
   if (threadIdx.x == 0) {
     M.scal[SC_RECENT_N] = kept;
     M.s.stats->culled = tc;
@@ -201,11 +205,10 @@ __global__ void __launch_bounds__(256) k_select(DevMap* maps, const StepArgs* ar
   const StepArgs& A = args[blockIdx.x];
   const DevMap& M = maps[A.map];
   if (!A.do_create) return;
-  extern __shared__ int dyn[];
-  int* sh_slot = dyn;
-  int* sh_w = dyn + M.kf_cap;
+  extern __shared__ unsigned long long dynk[];
+  unsigned long long* sh_key = dynk;
+  int* sh_slot = (int*)(dynk + M.kf_cap);
   __shared__ int out[NMAX];
-  __shared__ int sh_scan[32];
   __shared__ int n_out;
   const int cur = A.cur;
   int want = A.n_nbr_req < NMAX ? A.n_nbr_req : NMAX;
@@ -216,7 +219,7 @@ __global__ void __launch_bounds__(256) k_select(DevMap* maps, const StepArgs* ar
     }
     __syncthreads();
   } else {
-    const int got = ranked_neighbors<256>(M, cur, want, sh_slot, sh_w, out, sh_scan, n_slots_max);
+    const int got = ranked_neighbors<256>(M, cur, want, sh_slot, sh_key, out, n_slots_max);
     if (threadIdx.x == 0) n_out = got;
     __syncthreads();
     if (n_out < want) {
@@ -594,6 +597,7 @@ __global__ void __launch_bounds__(1024) k_commit(DevMap* maps, const StepArgs* a
         M.obs[oo] = cur_first ? make_int2(cur, i) : make_int2(nb, j);
         M.obs[oo + 1] = cur_first ? make_int2(nb, j) : make_int2(cur, i);
         M.dirty[id] = 0;
+        M.gval[id] = 0;
         M.counts[(size_t)id * M.L + M.klev[ga]] += 1;
         M.counts[(size_t)id * M.L + M.klev[gb]] += 1;
         M.kbind[ga] = id;
@@ -627,28 +631,24 @@ __global__ void __launch_bounds__(1024) k_commit(DevMap* maps, const StepArgs* a
 }
 
 // ---------------------------------------------------------------------------------- fusion
+//
+// SearchAndFuse (fusion.py:307-347) for one keyframe, as a chain of kernels:
+//   k_fuse_targets  1 CTA/map  collect_fusion_targets + forward point list + ledger
+//   k_fuse_geo      warp/point refresh stale rep descriptors + view geometry of the forward points
+//   k_fuse_gather   thread per (target, point): project, gate, window search, action build
+//                   (all targets against the unchanged map, as the reference's gather-all)
+//   k_fuse_apply    1 CTA/map  ordered apply of the forward batch (deterministic reservations)
+//   k_fuse_refresh  warp/point refresh every point the forward apply touched
+//   k_fuse_rev      1 CTA/map  reverse passes, gather -> apply per target (fusion.py:337-346)
 
-// point geometry (fusion.py:57-94)
+// _point_geometry row (fusion.py:57-94) from the cached accumulators
 __device__ void point_geometry(const DevMap& M, int mp, double slack, PGeo& g) {
   g.ok = 0;
   if (mp < 0 || !M.alive[mp] || M.nobs[mp] == 0) return;
-  const double x = M.pos[3 * mp], y = M.pos[3 * mp + 1], z = M.pos[3 * mp + 2];
-  const int2* o = M.obs + M.ooff[mp];
-  const int n = M.nobs[mp];
-  double lo = INFINITY, hi = -INFINITY, ax = 0, ay = 0, az = 0;
-  for (int k = 0; k < n; ++k) {
-    const int s = o[k].x;
-    const double rx = x - M.C[3 * s], ry = y - M.C[3 * s + 1], rz = z - M.C[3 * s + 2];
-    const double dd = sqrt(rx * rx + ry * ry + rz * rz);
-    if (dd <= 0) continue;
-    const double d0 = dd / M.S[M.klev[M.kp_off[s] + o[k].y]];
-    lo = d0 < lo ? d0 : lo;
-    hi = d0 > hi ? d0 : hi;
-    ax = ax + rx / dd;
-    ay = ay + ry / dd;
-    az = az + rz / dd;
-  }
+  if (!M.gval[mp]) geo_full(M, mp);
+  const double lo = M.glo[mp], hi = M.ghi[mp];
   if (!isfinite(lo)) return;
+  const double ax = M.gacc[3 * mp], ay = M.gacc[3 * mp + 1], az = M.gacc[3 * mp + 2];
   const double nrm = sqrt(ax * ax + ay * ay + az * az);
   if (nrm > 0) {
     g.vx = ax / nrm;
@@ -659,9 +659,9 @@ __device__ void point_geometry(const DevMap& M, int mp, double slack, PGeo& g) {
     g.vy = ay;
     g.vz = az;
   }
-  g.x = x;
-  g.y = y;
-  g.z = z;
+  g.x = M.pos[3 * mp];
+  g.y = M.pos[3 * mp + 1];
+  g.z = M.pos[3 * mp + 2];
   g.d0 = lo;
   g.blo = lo / slack;
   g.bhi = hi * M.S[M.L - 1] * slack;
@@ -785,7 +785,7 @@ __device__ bool for_keys(const DevMap& M, const ActRec& x, Op op) {
 }
 
 // one action, sequential semantics; cnt = {merged, added, stale} (shared, atomic)
-__device__ void apply_one(const DevMap& M, const ActRec& x, int* cnt) {
+__device__ void apply_one(const DevMap& M, const ActRec& x, int* cnt, PairAcc* acc) {
   if (x.pid < 0 || !M.alive[x.pid] || M.kf_state[x.slot] != KF_LIVE) {
     atomicAdd(&cnt[2], 1);
     return;
@@ -796,7 +796,7 @@ __device__ void apply_one(const DevMap& M, const ActRec& x, int* cnt) {
       atomicAdd(&cnt[2], 1);
       return;
     }
-    merge_pair(M, x.pid, x.other);
+    merge_pair(M, x.pid, x.other, acc);
     atomicAdd(&cnt[0], 1);
     return;
   }
@@ -806,7 +806,7 @@ __device__ void apply_one(const DevMap& M, const ActRec& x, int* cnt) {
       atomicAdd(&cnt[2], 1);
       return;
     }
-    merge_pair(M, x.pid, now);
+    merge_pair(M, x.pid, now, acc);
     atomicAdd(&cnt[0], 1);
     return;
   }
@@ -814,20 +814,20 @@ __device__ void apply_one(const DevMap& M, const ActRec& x, int* cnt) {
     atomicAdd(&cnt[2], 1);
     return;
   }
-  link(M, x.pid, x.slot, x.j);
+  link(M, x.pid, x.slot, x.j, acc);
   mark_dirty(M, x.pid);
   M.found[x.pid] += 1;
   atomicAdd(&cnt[1], 1);
 }
 
 template <int BLOCK>
-__device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh) {
+__device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh, PairAcc* acc) {
   __shared__ unsigned round_sh;
   __shared__ int npend_sh;
   for (int a = threadIdx.x; a < n; a += BLOCK) M.s.pend[a] = a;
   if (threadIdx.x == 0) npend_sh = n;
   __syncthreads();
-  int guard = 0;
+  int rounds = 0;
   while (npend_sh > 0) {
     const int np = npend_sh;
     if (threadIdx.x == 0) round_sh = (unsigned)atomicAdd(&M.scal[SC_ROUND], 1) + 1u;
@@ -849,11 +849,10 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
     }
     __syncthreads();
     for (int q = threadIdx.x; q < np; q += BLOCK)
-      if (M.s.ready[q]) apply_one(M, acts[M.s.pend[q]], cnt);
+      if (M.s.ready[q]) apply_one(M, acts[M.s.pend[q]], cnt, acc);
     __syncthreads();
-    // stable compaction of the still-pending actions
     int kept = 0;
-    for (int b0 = 0; b0 < np; b0 += BLOCK) {
+    for (int b0 = 0; b0 < np; b0 += BLOCK) {  // stable compaction of the still-pending actions
       const int q = b0 + threadIdx.x;
       const int keep = q < np ? !M.s.ready[q] : 0;
       const int a = keep ? M.s.pend[q] : 0;
@@ -865,9 +864,9 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
     }
     if (threadIdx.x == 0) npend_sh = kept;
     __syncthreads();
-    if (++guard > (1 << 20)) break;
+    if (++rounds > (1 << 20)) break;
   }
-  return guard;
+  return rounds;
 }
 
 // recompute the representative descriptor of every dirty point in pts[0..P) (warp per point)
@@ -903,22 +902,21 @@ __device__ void refresh_all(const DevMap& M) {
   __syncthreads();
   const int n = M.scal[SC_NEXT_ID];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int b0 = 0; b0 < n; b0 += BLOCK) {
-    // warp-ballot over 32 ids at a time, refresh dirty ones cooperatively
-    for (int w0 = b0 + wid * 32; w0 < b0 + BLOCK && w0 < n; w0 += BLOCK) {
-      const int id = w0 + lane;
-      unsigned bal = __ballot_sync(0xffffffffu, id < n && M.dirty[id]);
-      while (bal) {
-        const int k = __ffs(bal) - 1;
-        bal &= bal - 1;
-        const int mp = w0 + k;
-        if (M.alive[mp]) refresh_rep_warp(M, mp, lane);
-        __syncwarp();
-        if (lane == 0) M.dirty[mp] = 0;
-        __syncwarp();
-      }
+  for (int w0 = wid * 32; w0 < n; w0 += BLOCK) {
+    const int id = w0 + lane;
+    unsigned bal = __ballot_sync(0xffffffffu, id < n && M.dirty[id]);
+    while (bal) {
+      const int k = __ffs(bal) - 1;
+      bal &= bal - 1;
+      const int mp = w0 + k;
+      if (M.alive[mp]) refresh_rep_warp(M, mp, lane);
+      __syncwarp();
+      if (lane == 0) M.dirty[mp] = 0;
+      __syncwarp();
     }
   }
+  __syncthreads();
+  if (threadIdx.x == 0) M.scal[SC_DIRTY_N] = 0;
   __syncthreads();
 }
 
@@ -943,41 +941,52 @@ __device__ int bound_points(const DevMap& M, int slot, int* sh) {
   return count;
 }
 
-// collect_fusion_targets (fusion.py:38-54)
+// collect_fusion_targets (fusion.py:38-54): first-order neighbours in rank order, then per
+// first-order keyframe (in order) up to n2 not-yet-listed keyframes of its own ranking.
+// Every first-order row is ranked in parallel (warp per row, 64-bit composite keys); the
+// dependent walk is one thread over shared memory with a slot bitmap for "seen".
 template <int BLOCK>
-__device__ int fusion_targets(const DevMap& M, int cur, int n1, int n2, int n_slots, int* sh_slot, int* sh_w,
-                              int* sh_scan) {
+__device__ int fusion_targets(const DevMap& M, int cur, int n1, int n2, int n_slots, int* sh_slot,
+                              unsigned long long* sh_key) {
   __shared__ int first[TMAX];
+  __shared__ int tlist[TMAX];
   __shared__ int n_first, n_t;
-  const int nf = ranked_neighbors<BLOCK>(M, cur, n1 < TMAX ? n1 : TMAX, sh_slot, sh_w, first, sh_scan, n_slots);
+  __shared__ unsigned seen[128];  // kf_cap <= 4096 slots
+  const int nf = ranked_neighbors<BLOCK>(M, cur, n1 < TMAX ? n1 : TMAX, sh_slot, sh_key, first, n_slots);
   if (threadIdx.x == 0) n_first = nf;
+  if (threadIdx.x < 128) seen[threadIdx.x] = 0;
   __syncthreads();
-  // rank every first-order row in parallel: warp w handles rows w, w+32, ...
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const size_t stride = 3 * (size_t)M.kf_cap + 1;
   for (int f = wid; f < n_first; f += BLOCK / 32) {
-    int* buf = M.s.rank_buf + (size_t)f * (2 * M.kf_cap + 1);  // [count][slots...][ranked...]
+    // rank_buf row: [count][slot x kf_cap][ranked slot x kf_cap][key (u64) x kf_cap/2...]
+    int* buf = M.s.rank_buf + (size_t)f * stride;
+    unsigned long long* keys = (unsigned long long*)(M.s.rank_buf + (size_t)TMAX * stride) + (size_t)f * M.kf_cap;
     const int row_slot = first[f];
     const int* row = M.covis + (size_t)row_slot * M.kf_cap;
     int c = 0;
     for (int s0 = 0; s0 < n_slots; s0 += 32) {
       const int s = s0 + lane;
-      const bool take = s < n_slots && s != row_slot && row[s] >= M.min_w && row[s] > 0 && M.kf_state[s] == KF_LIVE;
+      int w = 0;
+      bool take = false;
+      if (s < n_slots) {
+        w = row[s];
+        take = s != row_slot && w >= M.min_w && w > 0 && M.kf_state[s] == KF_LIVE;
+      }
       const unsigned bal = __ballot_sync(0xffffffffu, take);
-      if (take) buf[1 + c + __popc(bal & ((1u << lane) - 1))] = s;
+      if (take) {
+        const int at = c + __popc(bal & ((1u << lane) - 1));
+        buf[1 + at] = s;
+        keys[at] = covis_key(M, s, w);
+      }
       c += __popc(bal);
     }
     __syncwarp();
     for (int e = lane; e < c; e += 32) {
-      const int se = buf[1 + e];
-      const int we = row[se];
-      const long long ie = M.kf_id[se];
+      const unsigned long long ke = keys[e];
       int rk = 0;
-      for (int q = 0; q < c; ++q) {
-        const int sq = buf[1 + q];
-        const int wq = row[sq];
-        rk += (wq > we) || (wq == we && M.kf_id[sq] < ie);
-      }
-      buf[1 + M.kf_cap + rk] = se;
+      for (int q = 0; q < c; ++q) rk += keys[q] < ke;
+      buf[1 + M.kf_cap + rk] = buf[1 + e];
     }
     if (lane == 0) buf[0] = c;
     __syncwarp();
@@ -985,18 +994,20 @@ __device__ int fusion_targets(const DevMap& M, int cur, int n1, int n2, int n_sl
   __syncthreads();
   if (threadIdx.x == 0) {
     int nt = 0;
-    for (int f = 0; f < n_first; ++f) M.s.targets[nt++] = first[f];
+    seen[cur >> 5] |= 1u << (cur & 31);
     for (int f = 0; f < n_first; ++f) {
-      const int* buf = M.s.rank_buf + (size_t)f * (2 * M.kf_cap + 1);
+      tlist[nt++] = first[f];
+      seen[first[f] >> 5] |= 1u << (first[f] & 31);
+    }
+    for (int f = 0; f < n_first; ++f) {
+      const int* buf = M.s.rank_buf + (size_t)f * stride;
       const int c = buf[0];
       int added = 0;
       for (int q = 0; q < c && added < n2 && nt < TMAX; ++q) {
         const int s = buf[1 + M.kf_cap + q];
-        if (s == cur) continue;
-        bool seen = false;
-        for (int u = 0; u < nt && !seen; ++u) seen = M.s.targets[u] == s;
-        if (!seen) {
-          M.s.targets[nt++] = s;
+        if (!(seen[s >> 5] >> (s & 31) & 1u)) {
+          seen[s >> 5] |= 1u << (s & 31);
+          tlist[nt++] = s;
           ++added;
         }
       }
@@ -1005,17 +1016,18 @@ __device__ int fusion_targets(const DevMap& M, int cur, int n1, int n2, int n_sl
     *M.s.n_targets = nt;
   }
   __syncthreads();
+  for (int k = threadIdx.x; k < n_t; k += BLOCK) M.s.targets[k] = tlist[k];
+  __syncthreads();
   return n_t;
 }
 
-// one reverse-style pass: points M.s.pts[0..P) into target ts, gather + (optionally) visible
-// increments + compaction into M.s.acts; returns action count
+// points M.s.pts[0..P) into target ts: refresh, geometry, gather, (visible), compaction
 template <int BLOCK>
 __device__ int gather_pass(const DevMap& M, const lm_fuse_cfg& fc, int P, int ts, bool bump_visible, int* sh,
-                           int* vis_out, long long* cyc = nullptr) {
+                           int* vis_out, long long* tm = nullptr) {
   const long long c0 = gtime();
   refresh_points<BLOCK>(M, M.s.pts, P, sh);
-  if (cyc && threadIdx.x == 0) cyc[4] += gtime() - c0;
+  if (tm && threadIdx.x == 0) tm[0] += gtime() - c0;
   const long long c1 = gtime();
   for (int p = threadIdx.x; p < P; p += BLOCK) point_geometry(M, M.s.pts[p], fc.dist_band_slack, M.s.geo[p]);
   __syncthreads();
@@ -1038,7 +1050,7 @@ __device__ int gather_pass(const DevMap& M, const lm_fuse_cfg& fc, int P, int ts
   }
   if (vis_out) *vis_out = block_sum<BLOCK>(nvis, sh);
   __syncthreads();
-  if (cyc && threadIdx.x == 0) cyc[5] += gtime() - c1;
+  if (tm && threadIdx.x == 0) tm[1] += gtime() - c1;
   return count;
 }
 
@@ -1056,123 +1068,207 @@ __device__ __forceinline__ long long pass_bytes(long long pts, long long obs, lo
   return 56 * pts + 9 * obs + 53 * tkp + 16 * acts;
 }
 
-// full run_fusion for one map per CTA
-__global__ void __launch_bounds__(1024) k_fuse(DevMap* maps, const StepArgs* args, int n_slots_max) {
+enum FuseCtl { FC_T = 0, FC_P = 1, FC_NACT = 2, FC_N = 8 };
+
+__global__ void __launch_bounds__(1024) k_fuse_targets(DevMap* maps, const StepArgs* args, int n_slots_max) {
   const StepArgs& A = args[blockIdx.x];
   const DevMap& M = maps[A.map];
   if (!A.do_fuse) return;
-  extern __shared__ int dyn[];
-  int* sh_slot = dyn;
-  int* sh_w = dyn + M.kf_cap;
+  extern __shared__ unsigned long long dynk[];
+  unsigned long long* sh_key = dynk;
+  int* sh_slot = (int*)(dynk + M.kf_cap);
+  __shared__ int sh[32];
+  const long long t0 = gtime();
+  const int T = fusion_targets<1024>(M, A.cur, A.fc.n1, A.fc.n2, n_slots_max, sh_slot, sh_key);
+  const int P = T ? bound_points<1024>(M, A.cur, sh) : 0;
+  if (threadIdx.x == 0) {
+    M.s.fctl[FC_T] = T;
+    M.s.fctl[FC_P] = P;
+    lm_step_stats* st = M.s.stats;
+    st->n_targets = T;
+    if (T) {
+      const unsigned long long mpb = M.mp_rec_bytes;
+      unsigned long long naive = 0;
+      long long tkp = 0;
+      for (int k = 0; k < T; ++k) {
+        naive += (unsigned long long)payload_bytes(M, M.s.targets[k]);
+        tkp += M.kp_n[M.s.targets[k]];
+      }
+      M.ledger[LG_NAIVE] += naive + P * mpb;
+      M.ledger[LG_PERSIST] += P * mpb;
+      M.ledger[LG_SMALL_FUSE] += P * mpb;
+      M.ledger[LG_SMALL_EVENTS] += 1;
+      st->fuse_points += (long long)T * P;
+      st->fuse_passes += T;
+      st->fuse_bytes += 53 * tkp;
+    }
+    st->fuse_cycles[0] += gtime() - t0;
+  }
+}
+
+// warp per forward point: refresh a stale rep descriptor, then the geometry row
+__global__ void __launch_bounds__(256) k_fuse_geo(DevMap* maps, const StepArgs* args) {
+  const StepArgs& A = args[blockIdx.y];
+  const DevMap& M = maps[A.map];
+  if (!A.do_fuse) return;
+  const int P = M.s.fctl[FC_P];
+  const int lane = threadIdx.x & 31;
+  const int p = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (p >= P) return;
+  const int mp = M.s.pts[p];
+  if (M.dirty[mp]) {
+    if (M.alive[mp]) refresh_rep_warp(M, mp, lane);
+    __syncwarp();
+    if (lane == 0) M.dirty[mp] = 0;
+  }
+  if (lane == 0) {
+    point_geometry(M, mp, A.fc.dist_band_slack, M.s.geo[p]);
+    atomicAdd((unsigned long long*)&M.s.stats->fuse_bytes,
+              (unsigned long long)(M.s.fctl[FC_T] * (56LL + 9LL * M.nobs[mp])));
+  }
+}
+
+// thread per (target, point) of the forward gather; per-CTA ordered compaction
+__global__ void __launch_bounds__(256) k_fuse_gather(DevMap* maps, const StepArgs* args) {
+  const StepArgs& A = args[blockIdx.y];
+  const DevMap& M = maps[A.map];
+  if (!A.do_fuse) return;
+  __shared__ int sh[32];
+  const int T = M.s.fctl[FC_T], P = M.s.fctl[FC_P];
+  const int TP = T * P;
+  const int b0 = blockIdx.x * 256;
+  if (b0 >= TP) return;
+  const int it = b0 + threadIdx.x;
+  ActRec a;
+  int has = 0;
+  if (it < TP) {
+    const int t = it / P, p = it - t * P;
+    const int pid = M.s.pts[p];
+    if (gather_one(M, A.fc, M.s.geo[p], pid, M.s.targets[t], &a, &has)) atomicAdd(&M.visible[pid], 1);
+  }
+  int tot;
+  const int at = block_excl_scan<256>(has, sh, tot);
+  if (has) M.s.acts2[b0 + at] = a;
+  if (threadIdx.x == 0) M.s.blk_cnt[blockIdx.x] = tot;
+}
+
+// assemble the forward batch in (target, point) order and apply it
+__global__ void __launch_bounds__(1024) k_fuse_apply(DevMap* maps, const StepArgs* args) {
+  const StepArgs& A = args[blockIdx.x];
+  const DevMap& M = maps[A.map];
+  if (!A.do_fuse) return;
+  const int T = M.s.fctl[FC_T], P = M.s.fctl[FC_P];
+  if (T == 0) return;
   __shared__ int sh[32];
   __shared__ int cnt[3];
+  __shared__ PairAcc acc;
+  const long long t0 = gtime();
+  if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
+  pair_acc_init<1024>(&acc);
+  const int nb = (T * P + 255) / 256;
+  int base = 0;
+  for (int c0 = 0; c0 < nb; c0 += 1024) {  // exclusive scan of the per-CTA counts
+    const int b = c0 + threadIdx.x;
+    const int v = b < nb ? M.s.blk_cnt[b] : 0;
+    int tot;
+    const int at = block_excl_scan<1024>(v, sh, tot);
+    if (b < nb) M.s.blk_off[b] = base + at;
+    base += tot;
+  }
+  __syncthreads();
+  const int nact = base;
+  for (int b = threadIdx.x >> 5; b < nb; b += 32) {  // warp per source CTA segment
+    const int c = M.s.blk_cnt[b], o = M.s.blk_off[b];
+    for (int k = threadIdx.x & 31; k < c; k += 32) M.s.acts[o + k] = M.s.acts2[b * 256 + k];
+  }
+  __syncthreads();
+  const long long t1 = gtime();
+  const int rr = apply_block<1024>(M, M.s.acts, nact, cnt, sh, &acc);
+  pair_acc_flush<1024>(M, &acc);
+  if (threadIdx.x == 0) {
+    lm_step_stats* st = M.s.stats;
+    st->merged += cnt[0];
+    st->observations_added += cnt[1];
+    st->stale += cnt[2];
+    st->fuse_actions += nact;
+    st->fuse_bytes += 16LL * nact;
+    st->apply_rounds += rr;
+    st->fuse_cycles[2] += t1 - t0;
+    st->fuse_cycles[3] += gtime() - t1;
+  }
+}
+
+// warp per point touched since the last refresh: representative descriptor + geometry cache
+__global__ void __launch_bounds__(256) k_fuse_refresh(DevMap* maps, const StepArgs* args) {
+  const StepArgs& A = args[blockIdx.y];
+  const DevMap& M = maps[A.map];
+  if (!A.do_fuse) return;
+  const int n = M.scal[SC_DIRTY_N];
+  const int lane = threadIdx.x & 31;
+  for (int k = blockIdx.x * 8 + (threadIdx.x >> 5); k < n; k += gridDim.x * 8) {
+    const int mp = M.dirty_list[k];
+    if (!M.dirty[mp]) continue;
+    if (M.alive[mp]) {
+      refresh_rep_warp(M, mp, lane);
+      if (lane == 0 && !M.gval[mp]) geo_full(M, mp);
+    }
+    __syncwarp();
+    if (lane == 0) M.dirty[mp] = 0;
+  }
+}
+
+// reverse passes: each target's bound points into the current keyframe, gather -> apply
+__global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs* args) {
+  const StepArgs& A = args[blockIdx.x];
+  const DevMap& M = maps[A.map];
+  if (!A.do_fuse) return;
+  const int T = M.s.fctl[FC_T];
+  if (T == 0) return;
+  __shared__ int sh[32];
+  __shared__ int cnt[3];
+  __shared__ long long tm[4];
+  __shared__ PairAcc acc;
+  if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
+  if (threadIdx.x < 4) tm[threadIdx.x] = 0;
+  if (threadIdx.x == 0) M.scal[SC_DIRTY_N] = 0;  // k_fuse_refresh consumed the list
+  pair_acc_init<1024>(&acc);
   const lm_fuse_cfg& fc = A.fc;
   const int cur = A.cur;
-  __shared__ long long cyc[8];
-  __shared__ int rounds;
-  if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
-  if (threadIdx.x < 8) cyc[threadIdx.x] = 0;
-  if (threadIdx.x == 0) rounds = 0;
-  const long long t_begin = gtime();
-  long long t0 = gtime();
-  const int T = fusion_targets<1024>(M, cur, fc.n1, fc.n2, n_slots_max, sh_slot, sh_w, sh);
-  if (threadIdx.x == 0) cyc[0] += gtime() - t0;
-  lm_step_stats* st = M.s.stats;
-  if (T == 0) {
-    if (threadIdx.x == 0) {
-      st->n_targets = 0;
-      st->merged = st->observations_added = st->stale = 0;
-    }
-    return;
-  }
-  const int mpb = M.mp_rec_bytes;
-  // forward: gather all targets against the unchanged map, then one ordered apply
-  const int P = bound_points<1024>(M, cur, sh);
-  if (threadIdx.x == 0) {
-    unsigned long long naive = 0;
-    for (int k = 0; k < T; ++k) naive += (unsigned long long)payload_bytes(M, M.s.targets[k]);
-    M.ledger[LG_NAIVE] += naive + (unsigned long long)P * mpb;
-    M.ledger[LG_PERSIST] += (unsigned long long)P * mpb;
-    M.ledger[LG_SMALL_FUSE] += (unsigned long long)P * mpb;
-    M.ledger[LG_SMALL_EVENTS] += 1;
-  }
-  t0 = gtime();
-  refresh_points<1024>(M, M.s.pts, P, sh);
-  const long long fwd_obs = pass_obs<1024>(M, P, sh);
-  long long tkp = 0;
-  for (int k = 0; k < T; ++k) tkp += M.kp_n[M.s.targets[k]];
-  for (int p = threadIdx.x; p < P; p += 1024) point_geometry(M, M.s.pts[p], fc.dist_band_slack, M.s.geo[p]);
-  __syncthreads();
-  if (threadIdx.x == 0) cyc[1] += gtime() - t0;
-  t0 = gtime();
-  const int TP = T * P;
-  for (int it = threadIdx.x; it < TP; it += 1024) {
-    const int t = it / P, p = it - t * P;
-    ActRec a;
-    int has = 0;
-    const int pid = M.s.pts[p];
-    const int vis = gather_one(M, fc, M.s.geo[p], pid, M.s.targets[t], &a, &has);
-    if (vis) atomicAdd(&M.visible[pid], 1);
-    M.s.act_flag[it] = has;
-    if (has) M.s.acts[M.s.act_cap - TP + it] = a;  // park in the tail, compact below
-  }
-  __syncthreads();
-  int nact = 0;
-  for (int b0 = 0; b0 < TP; b0 += 1024) {
-    const int it = b0 + threadIdx.x;
-    const int f = it < TP ? M.s.act_flag[it] : 0;
-    ActRec a;
-    if (f) a = M.s.acts[M.s.act_cap - TP + it];
-    int tot;
-    const int at = block_excl_scan<1024>(f, sh, tot);
-    __syncthreads();
-    if (f) M.s.acts[nact + at] = a;
-    nact += tot;
-    __syncthreads();
-  }
-  long long alg = pass_bytes((long long)T * P, (long long)T * fwd_obs, tkp, nact);
-  long long npts = (long long)T * P, nacts = nact;
-  if (threadIdx.x == 0) cyc[2] += gtime() - t0;
-  t0 = gtime();
-  {
-    const int rr = apply_block<1024>(M, M.s.acts, nact, cnt, sh);
-    if (threadIdx.x == 0) rounds += rr;
-  }
-  if (threadIdx.x == 0) cyc[3] += gtime() - t0;
-  // reverse: per target, its bound points into the current keyframe, gather then apply
+  const long long mpb = M.mp_rec_bytes;
+  long long alg = 0, npts = 0, nacts = 0;
+  int rounds = 0;
   for (int t = 0; t < T; ++t) {
     const int ts = M.s.targets[t];
     const int Pt = bound_points<1024>(M, ts, sh);
     if (threadIdx.x == 0) {
-      M.ledger[LG_NAIVE] += (unsigned long long)Pt * mpb;
-      M.ledger[LG_PERSIST] += (unsigned long long)Pt * mpb;
-      M.ledger[LG_SMALL_FUSE] += (unsigned long long)Pt * mpb;
+      M.ledger[LG_NAIVE] += Pt * mpb;
+      M.ledger[LG_PERSIST] += Pt * mpb;
+      M.ledger[LG_SMALL_FUSE] += Pt * mpb;
       M.ledger[LG_SMALL_EVENTS] += 1;
     }
     const long long ob = pass_obs<1024>(M, Pt, sh);
-    const int na = gather_pass<1024>(M, fc, Pt, cur, true, sh, nullptr, cyc);
+    const int na = gather_pass<1024>(M, fc, Pt, cur, true, sh, nullptr, tm);
     alg += pass_bytes(Pt, ob, M.kp_n[cur], na);
     npts += Pt;
     nacts += na;
-    t0 = gtime();
-    const int rr = apply_block<1024>(M, M.s.acts, na, cnt, sh);
-    if (threadIdx.x == 0) {
-      rounds += rr;
-      cyc[6] += gtime() - t0;
-    }
+    const long long t2 = gtime();
+    rounds += apply_block<1024>(M, M.s.acts, na, cnt, sh, &acc);
+    if (threadIdx.x == 0) tm[2] += gtime() - t2;
   }
+  pair_acc_flush<1024>(M, &acc);
   if (threadIdx.x == 0) {
-    st->n_targets = T;
-    st->fuse_bytes = alg;
-    st->fuse_passes = 2 * T;
-    st->fuse_points = npts;
-    st->fuse_actions = nacts;
-    st->apply_rounds = rounds;
-    for (int k = 0; k < 7; ++k) st->fuse_cycles[k] = cyc[k];
-    st->fuse_cycles[7] = gtime() - t_begin;  // whole kernel (thread 0 view)
-    st->merged = cnt[0];
-    st->observations_added = cnt[1];
-    st->stale = cnt[2];
+    lm_step_stats* st = M.s.stats;
+    st->merged += cnt[0];
+    st->observations_added += cnt[1];
+    st->stale += cnt[2];
+    st->fuse_bytes += alg;
+    st->fuse_passes += T;
+    st->fuse_points += npts;
+    st->fuse_actions += nacts;
+    st->apply_rounds += rounds;
+    st->fuse_cycles[4] += tm[0];
+    st->fuse_cycles[5] += tm[1];
+    st->fuse_cycles[6] += tm[2];
   }
 }
 

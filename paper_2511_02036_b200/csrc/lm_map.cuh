@@ -92,6 +92,10 @@ struct Scratch {
   int* ready;            // [act_cap]
   PGeo* geo;             // [pts_cap]
   ActRec* acts;          // [TMAX*kpkf_max]
+  ActRec* acts2;         // [TMAX*kpkf_max] forward gather output, per-CTA segments
+  int* blk_cnt;          // [act_cap/256 + 1]
+  int* blk_off;
+  int* fctl;             // [8] fusion control: targets, forward points, ...
   int* act_flag;         // [TMAX*kpkf_max]
   int* vis_flag;         // [TMAX*kpkf_max]
   int pts_cap;
@@ -138,8 +142,14 @@ struct DevMap {
   int* ooff;
   int2* obs;
   int* counts;
-  int* dirty;
-  int* dirty_list;
+  int* dirty;        // representative descriptor + geometry cache stale
+  int* dirty_list;   // ids whose dirty flag went 0 -> 1 (SC_DIRTY_N entries)
+  // per-point view-geometry cache (fusion.py:57-94 accumulators over the sorted
+  // observations): sum of unit rays, min/max level-0 distance, valid flag
+  double* gacc;      // [mp_cap*3]
+  double* glo;
+  double* ghi;
+  unsigned char* gval;
   // deterministic-reservation tables (apply): round-tagged min action index per entity
   unsigned long long* res_pt;    // [mp_cap]
   unsigned long long* res_slot;  // [kp_cap]
@@ -161,10 +171,57 @@ __device__ __forceinline__ int hamming(uint4 a0, uint4 a1, uint4 b0, uint4 b1) {
          __popc(a1.x ^ b1.x) + __popc(a1.y ^ b1.y) + __popc(a1.z ^ b1.z) + __popc(a1.w ^ b1.w);
 }
 
-__device__ __forceinline__ void covis_add(const DevMap& M, int a, int b, int d) {
-  if (a == b) return;
+// Shared-memory accumulator of covisibility deltas: the commutative bumps of a whole
+// kernel land in a per-CTA open-addressing table (one smem atomic each) and are flushed to
+// the dense matrix once, instead of contending global atomics on a few hot pairs.
+constexpr int PAIR_H = 2048;
+struct PairAcc {
+  unsigned key[PAIR_H];  // lo << 16 | hi, 0xffffffff = empty
+  int val[PAIR_H];
+};
+
+__device__ __forceinline__ void covis_global(const DevMap& M, int a, int b, int d) {
   atomicAdd(&M.covis[(size_t)a * M.kf_cap + b], d);
   atomicAdd(&M.covis[(size_t)b * M.kf_cap + a], d);
+}
+
+__device__ __forceinline__ void covis_add(const DevMap& M, int a, int b, int d, PairAcc* acc = nullptr) {
+  if (a == b) return;
+  if (acc) {
+    const unsigned lo = a < b ? a : b, hi = a < b ? b : a;
+    const unsigned k = lo << 16 | hi;
+    unsigned h = (k * 2654435761u) >> 21;  // 11 bits
+    for (int probe = 0; probe < 16; ++probe) {
+      const unsigned prev = atomicCAS(&acc->key[h], 0xffffffffu, k);
+      if (prev == 0xffffffffu || prev == k) {
+        atomicAdd(&acc->val[h], d);
+        return;
+      }
+      h = (h + 1) & (PAIR_H - 1);
+    }
+  }
+  covis_global(M, a, b, d);
+}
+
+template <int BLOCK>
+__device__ void pair_acc_init(PairAcc* acc) {
+  for (int h = threadIdx.x; h < PAIR_H; h += BLOCK) {
+    acc->key[h] = 0xffffffffu;
+    acc->val[h] = 0;
+  }
+  __syncthreads();
+}
+
+template <int BLOCK>
+__device__ void pair_acc_flush(const DevMap& M, PairAcc* acc) {
+  __syncthreads();
+  for (int h = threadIdx.x; h < PAIR_H; h += BLOCK) {
+    const unsigned k = acc->key[h];
+    if (k != 0xffffffffu && acc->val[h] != 0) covis_global(M, (int)(k >> 16), (int)(k & 0xffff), acc->val[h]);
+    acc->key[h] = 0xffffffffu;
+    acc->val[h] = 0;
+  }
+  __syncthreads();
 }
 
 __device__ __forceinline__ int obs_find(const DevMap& M, int mp, int slot) {
@@ -175,15 +232,16 @@ __device__ __forceinline__ int obs_find(const DevMap& M, int mp, int slot) {
   return -1;
 }
 
-// insert (slot, kp) keeping the list ordered by keyframe id; grows by doubling
-__device__ bool obs_insert(const DevMap& M, int mp, int slot, int kp) {
+// insert (slot, kp) keeping the list ordered by keyframe id; grows by doubling.
+// Returns the insert position, or -1 when the pool is exhausted.
+__device__ int obs_insert(const DevMap& M, int mp, int slot, int kp) {
   const int n = M.nobs[mp];
   if (n == M.ocap[mp]) {
     const int nc = M.ocap[mp] < 4 ? 4 : 2 * M.ocap[mp];
     const int off = atomicAdd(&M.scal[SC_OBS_HEAD], nc);
     if (off + nc > M.obs_cap) {
       set_err(M, LM_ERR_CAPACITY);
-      return false;
+      return -1;
     }
     const int2* src = M.obs + M.ooff[mp];
     for (int k = 0; k < n; ++k) M.obs[off + k] = src[k];
@@ -199,49 +257,106 @@ __device__ bool obs_insert(const DevMap& M, int mp, int slot, int kp) {
   }
   o[k] = make_int2(slot, kp);
   M.nobs[mp] = n + 1;
+  return k;
+}
+
+// the representative descriptor is stale until refreshed (rep is a pure function of the
+// observation list; read only by the fusion gather and export)
+__device__ __forceinline__ void mark_dirty(const DevMap& M, int mp) {
+  if (atomicExch(&M.dirty[mp], 1) == 0) {
+    const int at = atomicAdd(&M.scal[SC_DIRTY_N], 1);
+    if (at < M.mp_cap) M.dirty_list[at] = mp;
+  }
+}
+
+// one observation's contribution to the view geometry (fusion.py:77-84); false if skipped
+__device__ __forceinline__ bool geo_term(const DevMap& M, int mp, int2 e, double& rx, double& ry, double& rz,
+                                        double& dd, double& d0) {
+  const int s = e.x;
+  rx = M.pos[3 * mp] - M.C[3 * s];
+  ry = M.pos[3 * mp + 1] - M.C[3 * s + 1];
+  rz = M.pos[3 * mp + 2] - M.C[3 * s + 2];
+  dd = sqrt(rx * rx + ry * ry + rz * rz);
+  if (!(dd > 0)) return false;
+  d0 = dd / M.S[M.klev[M.kp_off[s] + e.y]];
   return true;
 }
 
-// the representative descriptor is stale until refresh_points / refresh_all recompute it
-__device__ __forceinline__ void mark_dirty(const DevMap& M, int mp) { M.dirty[mp] = 1; }
-
-// _record_obs: covis +1 with every current observer, bind the slot, count the level
-__device__ void link(const DevMap& M, int mp, int slot, int kp) {
+// full recompute of the cache over the sorted observation list (sequential order = the
+// reference's accumulation order, so the sums are bit-identical)
+__device__ void geo_full(const DevMap& M, int mp) {
   const int2* o = M.obs + M.ooff[mp];
   const int n = M.nobs[mp];
-  for (int k = 0; k < n; ++k) covis_add(M, slot, o[k].x, +1);
-  if (!obs_insert(M, mp, slot, kp)) return;
+  double lo = INFINITY, hi = -INFINITY, ax = 0, ay = 0, az = 0;
+  for (int k = 0; k < n; ++k) {
+    double rx, ry, rz, dd, d0;
+    if (!geo_term(M, mp, o[k], rx, ry, rz, dd, d0)) continue;
+    lo = d0 < lo ? d0 : lo;
+    hi = d0 > hi ? d0 : hi;
+    ax = ax + rx / dd;
+    ay = ay + ry / dd;
+    az = az + rz / dd;
+  }
+  M.gacc[3 * mp] = ax;
+  M.gacc[3 * mp + 1] = ay;
+  M.gacc[3 * mp + 2] = az;
+  M.glo[mp] = lo;
+  M.ghi[mp] = hi;
+  M.gval[mp] = 1;
+}
+
+// _record_obs: covis +1 with every current observer, bind the slot, count the level. An
+// observation appended after every existing one extends the cached sums exactly.
+__device__ void link(const DevMap& M, int mp, int slot, int kp, PairAcc* acc = nullptr) {
+  const int2* o = M.obs + M.ooff[mp];
+  const int n = M.nobs[mp];
+  for (int k = 0; k < n; ++k) covis_add(M, slot, o[k].x, +1, acc);
+  const int at = obs_insert(M, mp, slot, kp);
+  if (at < 0) return;
   const int g = M.kp_off[slot] + kp;
   M.kbind[g] = mp;
   M.counts[(size_t)mp * M.L + M.klev[g]] += 1;
+  if (M.gval[mp] && at == n) {
+    double rx, ry, rz, dd, d0;
+    if (geo_term(M, mp, make_int2(slot, kp), rx, ry, rz, dd, d0)) {
+      M.glo[mp] = d0 < M.glo[mp] ? d0 : M.glo[mp];
+      M.ghi[mp] = d0 > M.ghi[mp] ? d0 : M.ghi[mp];
+      M.gacc[3 * mp] = M.gacc[3 * mp] + rx / dd;
+      M.gacc[3 * mp + 1] = M.gacc[3 * mp + 1] + ry / dd;
+      M.gacc[3 * mp + 2] = M.gacc[3 * mp + 2] + rz / dd;
+    }
+  } else {
+    M.gval[mp] = 0;
+  }
 }
 
 // _unrecord_obs of list entry k: unbind, uncount, covis -1 with every remaining observer
-__device__ void unlink_at(const DevMap& M, int mp, int k) {
+__device__ void unlink_at(const DevMap& M, int mp, int k, PairAcc* acc = nullptr) {
   int2* o = M.obs + M.ooff[mp];
   const int2 e = o[k];
   const int n = M.nobs[mp] - 1;
   for (int m = k; m < n; ++m) o[m] = o[m + 1];
   M.nobs[mp] = n;
+  M.gval[mp] = 0;
   const int g = M.kp_off[e.x] + e.y;
   M.kbind[g] = -1;
   M.counts[(size_t)mp * M.L + M.klev[g]] -= 1;
-  for (int m = 0; m < n; ++m) covis_add(M, e.x, o[m].x, -1);
+  for (int m = 0; m < n; ++m) covis_add(M, e.x, o[m].x, -1, acc);
 }
 
-__device__ void kill_point(const DevMap& M, int mp) {
-  while (M.nobs[mp] > 0) unlink_at(M, mp, 0);
+__device__ void kill_point(const DevMap& M, int mp, PairAcc* acc = nullptr) {
+  while (M.nobs[mp] > 0) unlink_at(M, mp, 0, acc);
   M.alive[mp] = 0;
 }
 
 // replace_map_point(loser, winner); returns migrated observation count
-__device__ int replace_point(const DevMap& M, int loser, int winner) {
+__device__ int replace_point(const DevMap& M, int loser, int winner, PairAcc* acc = nullptr) {
   int migrated = 0;
   while (M.nobs[loser] > 0) {
     const int2 e = M.obs[M.ooff[loser]];
-    unlink_at(M, loser, 0);
+    unlink_at(M, loser, 0, acc);
     if (obs_find(M, winner, e.x) >= 0) continue;  // winner sees this keyframe: slot stays unbound
-    link(M, winner, e.x, e.y);
+    link(M, winner, e.x, e.y, acc);
     ++migrated;
   }
   M.found[winner] += M.found[loser];
@@ -252,7 +367,7 @@ __device__ int replace_point(const DevMap& M, int loser, int winner) {
 }
 
 // fusion._merge: more observations wins, ties lose the higher id; winner found += 1
-__device__ void merge_pair(const DevMap& M, int a, int b) {
+__device__ void merge_pair(const DevMap& M, int a, int b, PairAcc* acc = nullptr) {
   const int na = M.nobs[a], nb = M.nobs[b];
   int loser, winner;
   if (na == nb) {
@@ -265,7 +380,7 @@ __device__ void merge_pair(const DevMap& M, int a, int b) {
     loser = b;
     winner = a;
   }
-  replace_point(M, loser, winner);
+  replace_point(M, loser, winner, acc);
   M.found[winner] += 1;
 }
 
