@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(1024) k_stage(DevMap M, const unsigned char* b
     int cx = fx == fx ? (fx < 0 ? 0 : (fx > nx - 1 ? nx - 1 : (int)fx)) : 0;
     int cy = fy == fy ? (fy < 0 ? 0 : (fy > ny - 1 ? ny - 1 : (int)fy)) : 0;
     const int at = atomicAdd(&cnt[cy * nx + cx], 1);
-    M.cell_items[off + at] = off + i;
+    M.cell_items[off + at] = i;  // local keypoint index
   }
 }
 
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, in
     }
     case OP_FUSE_PASS: {
       int nvis = 0;
-      const int na = gather_pass<1024>(M, A.fc, A.n, A.a, false, sh, &nvis);
+      const int na = gather_pass<1024>(M, A.fc, A.n, A.a, tgt_global(M, A.a), false, sh, &nvis);
       if (tid == 0) {
         res[0] = M.scal[SC_ERR];
         res[1] = na;
@@ -456,6 +456,7 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
   }
   CU(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
   CU(cudaFuncSetAttribute(k_fuse_targets, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+  CU(cudaFuncSetAttribute(k_fuse_rev, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   CU(cudaFuncSetAttribute(k_op, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
   *out = ctx;
   return LM_OK;
@@ -549,7 +550,7 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(s.pts, s.pts_cap); A(s.geo, s.pts_cap);
   s.act_cap = TMAX * d.kpkf_max;
   A(s.acts, (size_t)s.act_cap); A(s.act_flag, (size_t)s.act_cap); A(s.vis_flag, (size_t)s.act_cap);
-  A(s.pend, (size_t)s.act_cap); A(s.ready, (size_t)s.act_cap); A(s.acts2, (size_t)s.act_cap);
+  A(s.pend, (size_t)s.act_cap); A(s.ready, (size_t)s.act_cap); A(s.merge_a, (size_t)s.act_cap); A(s.merge_b, (size_t)s.act_cap); A(s.acts2, (size_t)s.act_cap);
   A(s.blk_cnt, (size_t)s.act_cap / 256 + 2); A(s.blk_off, (size_t)s.act_cap / 256 + 2); A(s.fctl, 8);
   A(m->d_stats, 1); A(m->d_totals, 1); A(m->d_result, 4 + 1024 + TMAX);
 #undef A
@@ -748,6 +749,9 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
     kfcap = m->d.kf_cap > kfcap ? m->d.kf_cap : kfcap;
   }
   DevMap* dmaps = ctx->d_maps;
+  // reverse passes target the current keyframe: stage it in shared memory when it fits
+  size_t rev_smem = (size_t)kpkf * (16 + 1 + 32 + 4) + 4 * (GRID_CELLS + 1) + 256;
+  if (rev_smem > 160 * 1024) rev_smem = 0;
   CU(cudaMemcpyAsync(dv, h, sizeof(StepArgs) * n, cudaMemcpyHostToDevice, ctx->stream));
   const size_t dyn = 12 * (size_t)kfcap;
   std::vector<cudaEvent_t> evs;
@@ -791,7 +795,7 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   if ((rc = mark())) return rc;
   k_fuse_refresh<<<dim3(148, n), 256, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;
-  k_fuse_rev<<<n, 1024, 0, ctx->stream>>>(dmaps, dv);
+  k_fuse_rev<<<n, 1024, rev_smem, ctx->stream>>>(dmaps, dv, rev_smem);
   k_end<<<n, 32, 0, ctx->stream>>>(dmaps, dv, ctx->d_totals);
   if ((rc = mark())) return rc;
   ctx->launches += 15;

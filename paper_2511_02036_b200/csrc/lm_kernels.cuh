@@ -158,30 +158,27 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
   if (!A.do_cull) return;
   __shared__ int sh[32];
   __shared__ PairAcc acc;
+  __shared__ int kills[1024];
   pair_acc_init<1024>(&acc);
   const int n = M.scal[SC_RECENT_N];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int kept = 0, culled = 0;
   for (int base = 0; base < n; base += 1024) {
     const int e = base + threadIdx.x;
-    int keep = 0, id = -1, born = 0;
+    int keep = 0, kill = 0, id = -1, born = 0;
     if (e < n) {
       id = M.recent_id[e];
       born = M.recent_born[e];
-      if (M.alive[id]) {
+      if (M.alive[id]) {  // dead entries (merged away) just leave the list
         const double ratio = (double)M.found[id] / (double)(M.visible[id] > 1 ? M.visible[id] : 1);
-        if (ratio < A.cc.found_ratio_min) {
-          kill_point(M, id, &acc);
-          ++culled;
-        } else if (A.processed - born >= A.cc.probation_kfs) {
-          if (M.nobs[id] < A.cc.min_obs_graduate) {
-            kill_point(M, id, &acc);
-            ++culled;
-          }
-        } else {
-          keep = 1;
-        }
+        if (ratio < A.cc.found_ratio_min) kill = 1;
+        else if (A.processed - born >= A.cc.probation_kfs) kill = M.nobs[id] < A.cc.min_obs_graduate;
+        else keep = 1;
       }
     }
+    int tk;
+    const int ak = block_excl_scan<1024>(kill, sh, tk);
+    if (kill) kills[ak] = id;
     int tot;
     const int at = block_excl_scan<1024>(keep, sh, tot);
     if (keep) {  // stable in-place compaction: write index <= read index
@@ -189,13 +186,15 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
       M.recent_born[kept + at] = born;
     }
     kept += tot;
+    culled += tk;
+    __syncthreads();
+    for (int k = wid; k < tk; k += 32) kill_point_warp(M, kills[k], lane, &acc);  // independent points
     __syncthreads();
   }
-  const int tc = block_sum<1024>(culled, sh);
   pair_acc_flush<1024>(M, &acc);
   if (threadIdx.x == 0) {
     M.scal[SC_RECENT_N] = kept;
-    M.s.stats->culled = tc;
+    M.s.stats->culled = culled;
   }
 }
 
@@ -670,10 +669,26 @@ __device__ void point_geometry(const DevMap& M, int mp, double slack, PGeo& g) {
   g.ok = 1;
 }
 
+// target keyframe's keypoints + cell grid, from global memory or a shared-memory copy
+struct TgtView {
+  const double* u;
+  const double* v;
+  const unsigned char* lev;
+  const uint4* desc;
+  const int* cst;    // cell starts [cells+1]
+  const int* items;  // local keypoint index per cell entry
+};
+
+__device__ __forceinline__ TgtView tgt_global(const DevMap& M, int ts) {
+  const int off = M.kp_off[ts];
+  return TgtView{M.ku + off, M.kv + off, M.klev + off, M.kdesc + 2 * (size_t)off,
+                 M.cell_start + (size_t)ts * (GRID_CELLS + 1), M.cell_items + off};
+}
+
 // project + gates + grid window search + action build for one (point, target) pair
 // (fusion.py:97-129, 178-196, 161-174). Returns 1 if visible; *act filled when an action.
-__device__ int gather_one(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g, int pid, int ts, ActRec* act,
-                          int* has_act) {
+__device__ int gather_one(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g, int pid, int ts, const TgtView& T,
+                          ActRec* act, int* has_act) {
   *has_act = 0;
   if (!g.ok) return 0;
   const double* R = M.R + 9 * ts;
@@ -689,14 +704,15 @@ __device__ int gather_one(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g,
   const bool inview = zc > 0 && u >= 0 && u < cam[4] && v >= 0 && v < cam[5];
   const double dx = g.x - C[0], dy = g.y - C[1], dz = g.z - C[2];
   const double d = sqrt(dx * dx + dy * dy + dz * dz);
+  if (!(zc > 0 && inview && d >= g.blo && d <= g.bhi)) return 0;
   const double cosv = (dx * g.vx + dy * g.vy + dz * g.vz) / d;
+  if (!(cosv >= fc.min_view_cos)) return 0;
   double lraw = log(d / g.d0) / M.log_sf;
   if (!isfinite(lraw)) lraw = 0.0;
   double lr = rint(lraw);
   lr = lr < 0 ? 0 : (lr > M.L - 1 ? M.L - 1 : lr);
   const int lp = (int)lr;
   const double rad = fc.fuse_radius * M.S[lp];
-  if (!(zc > 0 && inview && d >= g.blo && d <= g.bhi && cosv >= fc.min_view_cos)) return 0;
   // conservative cell window, exact test inside
   const double cs = M.g_cs[ts];
   const int nx = M.g_nx[ts], ny = M.g_ny[ts];
@@ -706,21 +722,19 @@ __device__ int gather_one(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g,
   y0 = y0 < 0 ? 0 : y0;
   x1 = x1 > nx - 1 ? nx - 1 : x1;
   y1 = y1 > ny - 1 ? ny - 1 : y1;
-  const int* cst = M.cell_start + (size_t)ts * (GRID_CELLS + 1);
-  const int off = M.kp_off[ts];
   const double r2 = rad * rad;
   unsigned long long best = ~0ull;
   for (int cy = y0; cy <= y1; ++cy) {
     for (int cx = x0; cx <= x1; ++cx) {
       const int cell = cy * nx + cx;
-      for (int it = cst[cell]; it < cst[cell + 1]; ++it) {
-        const int gk = M.cell_items[off + it];
-        const double du = M.ku[gk] - u, dv = M.kv[gk] - v;
-        const int dl = (int)M.klev[gk] - lp;
+      for (int it = T.cst[cell]; it < T.cst[cell + 1]; ++it) {
+        const int k = T.items[it];
+        const double du = T.u[k] - u, dv = T.v[k] - v;
+        const int dl = (int)T.lev[k] - lp;
         if (du * du + dv * dv <= r2 && (dl < 0 ? -dl : dl) <= fc.level_window) {
-          const int dist = hamming(M.kdesc[2 * gk], M.kdesc[2 * gk + 1], g.r0, g.r1);
+          const int dist = hamming(T.desc[2 * k], T.desc[2 * k + 1], g.r0, g.r1);
           if (dist <= fc.match_max_distance) {
-            const unsigned long long key = ((unsigned long long)dist << 32) | (unsigned)(gk - off);
+            const unsigned long long key = ((unsigned long long)dist << 32) | (unsigned)k;
             best = key < best ? key : best;
           }
         }
@@ -729,7 +743,7 @@ __device__ int gather_one(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g,
   }
   if (best != ~0ull) {
     const int j = (int)(best & 0xffffffffu);
-    const int owner = M.kbind[off + j];
+    const int owner = M.kbind[M.kp_off[ts] + j];
     if (owner < 0) {
       if (obs_find(M, pid, ts) < 0) {
         *act = ActRec{ts, pid, j, -1, LM_ACT_ADD};
@@ -784,6 +798,24 @@ __device__ bool for_keys(const DevMap& M, const ActRec& x, Op op) {
   return true;
 }
 
+// outcome of action x under the current state: 0 stale, 1 add, 2 merge with *partner
+__device__ __forceinline__ int classify(const DevMap& M, const ActRec& x, int* partner) {
+  if (x.pid < 0 || !M.alive[x.pid] || M.kf_state[x.slot] != KF_LIVE) return 0;
+  const int g = M.kp_off[x.slot] + x.j;
+  if (x.kind == LM_ACT_MERGE) {
+    if (x.other < 0 || !M.alive[x.other] || x.other == x.pid || M.kbind[g] != x.other) return 0;
+    *partner = x.other;
+    return 2;
+  }
+  const int now = M.kbind[g];
+  if (now >= 0) {
+    if (!M.alive[now] || now == x.pid) return 0;
+    *partner = now;
+    return 2;
+  }
+  return obs_find(M, x.pid, x.slot) >= 0 ? 0 : 1;
+}
+
 // one action, sequential semantics; cnt = {merged, added, stale} (shared, atomic)
 __device__ void apply_one(const DevMap& M, const ActRec& x, int* cnt, PairAcc* acc) {
   if (x.pid < 0 || !M.alive[x.pid] || M.kf_state[x.slot] != KF_LIVE) {
@@ -823,7 +855,7 @@ __device__ void apply_one(const DevMap& M, const ActRec& x, int* cnt, PairAcc* a
 template <int BLOCK>
 __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh, PairAcc* acc) {
   __shared__ unsigned round_sh;
-  __shared__ int npend_sh;
+  __shared__ int npend_sh, nmerge_sh;
   for (int a = threadIdx.x; a < n; a += BLOCK) M.s.pend[a] = a;
   if (threadIdx.x == 0) npend_sh = n;
   __syncthreads();
@@ -848,8 +880,34 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
       M.s.ready[q] = for_keys(M, acts[a], [&](bool pt, int id) { return (pt ? M.res_pt[id] : M.res_slot[id]) == tag; });
     }
     __syncthreads();
-    for (int q = threadIdx.x; q < np; q += BLOCK)
-      if (M.s.ready[q]) apply_one(M, acts[M.s.pend[q]], cnt, acc);
+    // commit: stale / add per thread, merges (O(n^2) pair work) one warp each
+    if (threadIdx.x == 0) nmerge_sh = 0;
+    __syncthreads();
+    for (int q = threadIdx.x; q < np; q += BLOCK) {
+      if (!M.s.ready[q]) continue;
+      const ActRec x = acts[M.s.pend[q]];
+      int partner = -1;
+      const int kind = classify(M, x, &partner);
+      if (kind == 0) {
+        atomicAdd(&cnt[2], 1);
+      } else if (kind == 1) {
+        link(M, x.pid, x.slot, x.j, acc);
+        mark_dirty(M, x.pid);
+        M.found[x.pid] += 1;
+        atomicAdd(&cnt[1], 1);
+      } else {
+        const int at = atomicAdd(&nmerge_sh, 1);
+        M.s.merge_a[at] = x.pid;
+        M.s.merge_b[at] = partner;
+      }
+    }
+    __syncthreads();
+    {
+      const int nm = nmerge_sh;
+      const int lane = threadIdx.x & 31;
+      for (int k = threadIdx.x >> 5; k < nm; k += BLOCK / 32) merge_pair_warp(M, M.s.merge_a[k], M.s.merge_b[k], lane, acc);
+      if (threadIdx.x == 0) cnt[0] += nm;
+    }
     __syncthreads();
     int kept = 0;
     for (int b0 = 0; b0 < np; b0 += BLOCK) {  // stable compaction of the still-pending actions
@@ -1023,8 +1081,8 @@ __device__ int fusion_targets(const DevMap& M, int cur, int n1, int n2, int n_sl
 
 // points M.s.pts[0..P) into target ts: refresh, geometry, gather, (visible), compaction
 template <int BLOCK>
-__device__ int gather_pass(const DevMap& M, const lm_fuse_cfg& fc, int P, int ts, bool bump_visible, int* sh,
-                           int* vis_out, long long* tm = nullptr) {
+__device__ int gather_pass(const DevMap& M, const lm_fuse_cfg& fc, int P, int ts, const TgtView& TV,
+                           bool bump_visible, int* sh, int* vis_out, long long* tm = nullptr) {
   const long long c0 = gtime();
   refresh_points<BLOCK>(M, M.s.pts, P, sh);
   if (tm && threadIdx.x == 0) tm[0] += gtime() - c0;
@@ -1038,7 +1096,7 @@ __device__ int gather_pass(const DevMap& M, const lm_fuse_cfg& fc, int P, int ts
     int has = 0, vis = 0;
     if (p < P) {
       const int pid = M.s.pts[p];
-      vis = gather_one(M, fc, M.s.geo[p], pid, ts, &a, &has);
+      vis = gather_one(M, fc, M.s.geo[p], pid, ts, TV, &a, &has);
       if (vis && bump_visible && M.alive[pid]) atomicAdd(&M.visible[pid], 1);
       if (vis_out) M.s.vis_flag[p] = vis;
     }
@@ -1144,7 +1202,8 @@ __global__ void __launch_bounds__(256) k_fuse_gather(DevMap* maps, const StepArg
   if (it < TP) {
     const int t = it / P, p = it - t * P;
     const int pid = M.s.pts[p];
-    if (gather_one(M, A.fc, M.s.geo[p], pid, M.s.targets[t], &a, &has)) atomicAdd(&M.visible[pid], 1);
+    const int ts = M.s.targets[t];
+    if (gather_one(M, A.fc, M.s.geo[p], pid, ts, tgt_global(M, ts), &a, &has)) atomicAdd(&M.visible[pid], 1);
   }
   int tot;
   const int at = block_excl_scan<256>(has, sh, tot);
@@ -1218,12 +1277,38 @@ __global__ void __launch_bounds__(256) k_fuse_refresh(DevMap* maps, const StepAr
 }
 
 // reverse passes: each target's bound points into the current keyframe, gather -> apply
-__global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs* args) {
+__global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs* args, int smem_bytes) {
   const StepArgs& A = args[blockIdx.x];
   const DevMap& M = maps[A.map];
   if (!A.do_fuse) return;
   const int T = M.s.fctl[FC_T];
   if (T == 0) return;
+  extern __shared__ __align__(16) unsigned char dyn_rev[];
+  TgtView TV = tgt_global(M, A.cur);
+  {  // stage the current keyframe (target of every reverse pass) in shared memory
+    const int n = M.kp_n[A.cur], off = M.kp_off[A.cur];
+    const int nc = M.g_nx[A.cur] * M.g_ny[A.cur];
+    const size_t need = (size_t)n * 53 + 4 * (size_t)(nc + 1) + 64;
+    if (smem_bytes > 0 && need <= (size_t)smem_bytes) {
+      uint4* sd = (uint4*)dyn_rev;
+      double* su = (double*)(sd + 2 * n);
+      double* sv = su + n;
+      int* scs = (int*)(sv + n);
+      int* sit = scs + nc + 1;
+      unsigned char* sl = (unsigned char*)(sit + n);
+      for (int k = threadIdx.x; k < 2 * n; k += 1024) sd[k] = M.kdesc[2 * (size_t)off + k];
+      for (int k = threadIdx.x; k < n; k += 1024) {
+        su[k] = M.ku[off + k];
+        sv[k] = M.kv[off + k];
+        sit[k] = M.cell_items[off + k];
+        sl[k] = M.klev[off + k];
+      }
+      const int* gcs = M.cell_start + (size_t)A.cur * (GRID_CELLS + 1);
+      for (int k = threadIdx.x; k <= nc; k += 1024) scs[k] = gcs[k];
+      TV = TgtView{su, sv, sl, sd, scs, sit};
+    }
+  }
+  __syncthreads();
   __shared__ int sh[32];
   __shared__ int cnt[3];
   __shared__ long long tm[4];
@@ -1247,7 +1332,7 @@ __global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs*
       M.ledger[LG_SMALL_EVENTS] += 1;
     }
     const long long ob = pass_obs<1024>(M, Pt, sh);
-    const int na = gather_pass<1024>(M, fc, Pt, cur, true, sh, nullptr, tm);
+    const int na = gather_pass<1024>(M, fc, Pt, cur, TV, true, sh, nullptr, tm);
     alg += pass_bytes(Pt, ob, M.kp_n[cur], na);
     npts += Pt;
     nacts += na;

@@ -89,6 +89,8 @@ struct Scratch {
   int* rank_buf;         // [TMAX * kf_cap] second-order walk scratch
   int* pts;              // [max(kpkf_max, pts_cap)] point list of the current pass
   int* pend;             // [act_cap] pending action indices (apply rounds)
+  int* merge_a;          // [act_cap] merges committed this round (warp-cooperative)
+  int* merge_b;
   int* ready;            // [act_cap]
   PGeo* geo;             // [pts_cap]
   ActRec* acts;          // [TMAX*kpkf_max]
@@ -227,6 +229,7 @@ __device__ void pair_acc_flush(const DevMap& M, PairAcc* acc) {
 __device__ __forceinline__ int obs_find(const DevMap& M, int mp, int slot) {
   const int2* o = M.obs + M.ooff[mp];
   const int n = M.nobs[mp];
+  if (n && o[n - 1].x == slot) return n - 1;  // the newest keyframe sorts last
   for (int k = 0; k < n; ++k)
     if (o[k].x == slot) return k;
   return -1;
@@ -382,6 +385,136 @@ __device__ void merge_pair(const DevMap& M, int a, int b, PairAcc* acc = nullptr
   }
   replace_point(M, loser, winner, acc);
   M.found[winner] += 1;
+}
+
+// ------------------------------------------------------------ warp-cooperative kill / merge
+// Same net effect as the sequential unlink/link loops above (all covisibility bumps are
+// commutative), with the O(n^2) pair work spread over the 32 lanes of one warp.
+
+// kill_map_point (mapmodel.py:233-237), all lanes of a warp call it with the same mp
+__device__ void kill_point_warp(const DevMap& M, int mp, int lane, PairAcc* acc) {
+  const int2* o = M.obs + M.ooff[mp];
+  const int n = M.nobs[mp];
+  for (int a = 0; a < n; ++a)
+    for (int b = a + 1 + lane; b < n; b += 32) covis_add(M, o[a].x, o[b].x, -1, acc);
+  for (int k = lane; k < n; k += 32) M.kbind[M.kp_off[o[k].x] + o[k].y] = -1;
+  for (int l = lane; l < M.L; l += 32) M.counts[(size_t)mp * M.L + l] = 0;
+  __syncwarp();
+  if (lane == 0) {
+    M.nobs[mp] = 0;
+    M.alive[mp] = 0;
+    M.gval[mp] = 0;
+  }
+  __syncwarp();
+}
+
+// replace_map_point(loser, winner) (mapmodel.py:245-267), warp-cooperative; returns migrated
+__device__ int replace_point_warp(const DevMap& M, int loser, int winner, int lane, PairAcc* acc) {
+  int2* oL = M.obs + M.ooff[loser];
+  const int2* oW = M.obs + M.ooff[winner];
+  const int nL = M.nobs[loser], nW = M.nobs[winner];
+  // (a) covisibility -1 for every pair of the loser's observers
+  for (int a = 0; a < nL; ++a)
+    for (int b = a + 1 + lane; b < nL; b += 32) covis_add(M, oL[a].x, oL[b].x, -1, acc);
+  __syncwarp();
+  // (b) migrate the observations of keyframes the winner does not see; compact them in place
+  int nM = 0;
+  for (int c0 = 0; c0 < nL; c0 += 32) {
+    const int a = c0 + lane;
+    int2 e = make_int2(0, 0);
+    bool mig = false;
+    if (a < nL) {
+      e = oL[a];
+      mig = true;
+      for (int w = 0; w < nW; ++w) mig &= oW[w].x != e.x;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, mig);
+    __syncwarp();
+    if (a < nL) {
+      const int g = M.kp_off[e.x] + e.y;
+      M.kbind[g] = mig ? winner : -1;
+      if (mig) {
+        atomicAdd(&M.counts[(size_t)winner * M.L + M.klev[g]], 1);
+        oL[nM + __popc(bal & ((1u << lane) - 1))] = e;
+      }
+    }
+    nM += __popc(bal);
+    __syncwarp();
+  }
+  // (c) covisibility +1: migrated x winner's original observers, and migrated pairs
+  for (int q = lane; q < nM * nW; q += 32) covis_add(M, oL[q / nW].x, oW[q % nW].x, +1, acc);
+  for (int a = 0; a < nM; ++a)
+    for (int b = a + 1 + lane; b < nM; b += 32) covis_add(M, oL[a].x, oL[b].x, +1, acc);
+  // (d) winner list = sorted merge of its own and the migrated observations (distinct kfs)
+  if (nM > 0) {
+    int off = 0, cap = M.ocap[winner];
+    if (lane == 0) {
+      // the merged list is written to a fresh block (the old one is read while merging)
+      int nc = cap < 4 ? 4 : cap;
+      while (nc < nW + nM) nc *= 2;
+      off = atomicAdd(&M.scal[SC_OBS_HEAD], nc);
+      if (off + nc > M.obs_cap) {
+        set_err(M, LM_ERR_CAPACITY);
+        off = -1;
+      }
+      cap = nc;
+    }
+    off = __shfl_sync(0xffffffffu, off, 0);
+    cap = __shfl_sync(0xffffffffu, cap, 0);
+    if (off >= 0) {
+      int2* B = M.obs + off;
+      for (int i = lane; i < nW; i += 32) {
+        const long long ki = M.kf_id[oW[i].x];
+        int r = 0;
+        for (int j = 0; j < nM; ++j) r += M.kf_id[oL[j].x] < ki;
+        B[i + r] = oW[i];
+      }
+      for (int j = lane; j < nM; j += 32) {
+        const long long kj = M.kf_id[oL[j].x];
+        int r = 0;
+        for (int i = 0; i < nW; ++i) r += M.kf_id[oW[i].x] < kj;
+        B[j + r] = oL[j];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        M.ooff[winner] = off;
+        M.ocap[winner] = cap;
+        M.nobs[winner] = nW + nM;
+      }
+    }
+  }
+  __syncwarp();
+  for (int l = lane; l < M.L; l += 32) M.counts[(size_t)loser * M.L + l] = 0;
+  if (lane == 0) {
+    M.nobs[loser] = 0;
+    M.found[winner] += M.found[loser];
+    M.visible[winner] += M.visible[loser];
+    M.alive[loser] = 0;
+    M.gval[winner] = 0;
+    M.gval[loser] = 0;
+    mark_dirty(M, winner);
+  }
+  __syncwarp();
+  return nM;
+}
+
+// fusion._merge, warp-cooperative
+__device__ void merge_pair_warp(const DevMap& M, int a, int b, int lane, PairAcc* acc) {
+  const int na = M.nobs[a], nb = M.nobs[b];
+  int loser, winner;
+  if (na == nb) {
+    loser = a > b ? a : b;
+    winner = a > b ? b : a;
+  } else if (na < nb) {
+    loser = a;
+    winner = b;
+  } else {
+    loser = b;
+    winner = a;
+  }
+  replace_point_warp(M, loser, winner, lane, acc);
+  if (lane == 0) M.found[winner] += 1;
+  __syncwarp();
 }
 
 // k-th smallest of d[0..n) (quickselect, d is scratch)
