@@ -286,7 +286,7 @@ def main():
             if isinstance(v, int):
                 acc[f] = acc.get(f, 0) + v
             elif f == "fuse_cycles":
-                acc[f] = [a + b for a, b in zip(acc.get(f, [0] * 8), list(v))]
+                acc[f] = [a + b for a, b in zip(acc.get(f, [0] * 16), list(v))]
     launches = lib.lm_launch_count(ctx.h) - launches0
     clocks = sampler.stop()
     prof_ms = (C.c_double * 16)()
@@ -355,7 +355,11 @@ def main():
                               "apply_rounds": acc["apply_rounds"] / args.steps},
             "fuse_phase_ms_per_step": {n: acc["fuse_cycles"][k] / args.steps / 1e6
                                        for k, n in enumerate(["targets", "-", "fwd_assemble", "fwd_apply",
-                                                              "rev_refresh", "rev_geometry_gather", "rev_apply", "-"])
+                                                              "rev_refresh", "rev_geometry", "rev_apply", "rev_gather",
+                                                              "rev_bound_points", "rev_apply_reserve_check",
+                                                              "rev_apply_commit", "rev_apply_merges",
+                                                              "rev_apply_compaction", "fwd_apply_reserve_check",
+                                                              "fwd_apply_commit_merges", "fwd_apply_compaction"])
                                        if n != "-"}}
     if rank == 0 and world == 1 and not args.no_cpu:
         done, dt = cpu_sample(seq, args.workload, args.cpu_budget)

@@ -115,8 +115,10 @@ typedef struct lm_step_stats { /* CreationStats triangulation.py:49-60 + run_fus
   int64_t fuse_bytes;   /* algorithmic fusion bytes, SURVEY.md 8(d) formula */
   int64_t fuse_passes, fuse_points, fuse_actions;
   int64_t apply_rounds;      /* deterministic-reservation rounds over all applies */
-  int64_t fuse_cycles[8];    /* ns per fusion phase (%globaltimer): targets, -, fwd assemble,
-                                fwd apply, rev refresh, rev geometry+gather, rev apply, - */
+  int64_t fuse_cycles[16];   /* ns per fusion phase (%globaltimer): 0 targets, 2 fwd assemble,
+                                3 fwd apply, 4 rev refresh, 5 rev geometry, 6 rev apply,
+                                7 rev gather, 8 rev bound points, 9 apply reserve+check,
+                                10 apply commit (plain), 11 apply merges, 12 apply compaction */
 } lm_step_stats;
 
 typedef struct lm_candidate { /* MatchCandidate triangulation.py:41-46 */

@@ -721,7 +721,7 @@ __global__ void k_end(DevMap* maps, const StepArgs* args, lm_step_stats** totals
   t->fuse_points += st->fuse_points;
   t->fuse_actions += st->fuse_actions;
   t->apply_rounds += st->apply_rounds;
-  for (int k = 0; k < 8; ++k) t->fuse_cycles[k] += st->fuse_cycles[k];
+  for (int k = 0; k < 16; ++k) t->fuse_cycles[k] += st->fuse_cycles[k];
   t->first_new_id += 1;  // steps accumulated
 }
 

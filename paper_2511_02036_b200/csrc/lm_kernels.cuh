@@ -853,7 +853,8 @@ __device__ void apply_one(const DevMap& M, const ActRec& x, int* cnt, PairAcc* a
 }
 
 template <int BLOCK>
-__device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh, PairAcc* acc) {
+__device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh, PairAcc* acc,
+                           long long* tm = nullptr) {
   __shared__ unsigned round_sh;
   __shared__ int npend_sh, nmerge_sh;
   for (int a = threadIdx.x; a < n; a += BLOCK) M.s.pend[a] = a;
@@ -865,6 +866,7 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
     if (threadIdx.x == 0) round_sh = (unsigned)atomicAdd(&M.scal[SC_ROUND], 1) + 1u;
     __syncthreads();
     const unsigned rnd = round_sh;
+    long long tt = gtime();
     for (int q = threadIdx.x; q < np; q += BLOCK) {
       const int a = M.s.pend[q];
       const unsigned long long tag = res_tag(rnd, a);
@@ -883,6 +885,10 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
     // commit: stale / add per thread, merges (O(n^2) pair work) one warp each
     if (threadIdx.x == 0) nmerge_sh = 0;
     __syncthreads();
+    if (tm && threadIdx.x == 0) {
+      tm[9] += gtime() - tt;
+      tt = gtime();
+    }
     for (int q = threadIdx.x; q < np; q += BLOCK) {
       if (!M.s.ready[q]) continue;
       const ActRec x = acts[M.s.pend[q]];
@@ -902,6 +908,10 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
       }
     }
     __syncthreads();
+    if (tm && threadIdx.x == 0) {
+      tm[10] += gtime() - tt;
+      tt = gtime();
+    }
     {
       const int nm = nmerge_sh;
       const int lane = threadIdx.x & 31;
@@ -909,6 +919,10 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
       if (threadIdx.x == 0) cnt[0] += nm;
     }
     __syncthreads();
+    if (tm && threadIdx.x == 0) {
+      tm[11] += gtime() - tt;
+      tt = gtime();
+    }
     int kept = 0;
     for (int b0 = 0; b0 < np; b0 += BLOCK) {  // stable compaction of the still-pending actions
       const int q = b0 + threadIdx.x;
@@ -922,6 +936,7 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
     }
     if (threadIdx.x == 0) npend_sh = kept;
     __syncthreads();
+    if (tm && threadIdx.x == 0) tm[12] += gtime() - tt;
     if (++rounds > (1 << 20)) break;
   }
   return rounds;
@@ -1089,6 +1104,8 @@ __device__ int gather_pass(const DevMap& M, const lm_fuse_cfg& fc, int P, int ts
   const long long c1 = gtime();
   for (int p = threadIdx.x; p < P; p += BLOCK) point_geometry(M, M.s.pts[p], fc.dist_band_slack, M.s.geo[p]);
   __syncthreads();
+  if (tm && threadIdx.x == 0) tm[1] += gtime() - c1;
+  const long long c2 = gtime();
   int count = 0, nvis = 0;
   for (int b0 = 0; b0 < P; b0 += BLOCK) {
     const int p = b0 + threadIdx.x;
@@ -1108,7 +1125,7 @@ __device__ int gather_pass(const DevMap& M, const lm_fuse_cfg& fc, int P, int ts
   }
   if (vis_out) *vis_out = block_sum<BLOCK>(nvis, sh);
   __syncthreads();
-  if (tm && threadIdx.x == 0) tm[1] += gtime() - c1;
+  if (tm && threadIdx.x == 0) tm[3] += gtime() - c2;
   return count;
 }
 
@@ -1242,7 +1259,10 @@ __global__ void __launch_bounds__(1024) k_fuse_apply(DevMap* maps, const StepArg
   }
   __syncthreads();
   const long long t1 = gtime();
-  const int rr = apply_block<1024>(M, M.s.acts, nact, cnt, sh, &acc);
+  __shared__ long long tmf[16];
+  if (threadIdx.x < 16) tmf[threadIdx.x] = 0;
+  __syncthreads();
+  const int rr = apply_block<1024>(M, M.s.acts, nact, cnt, sh, &acc, tmf);
   pair_acc_flush<1024>(M, &acc);
   if (threadIdx.x == 0) {
     lm_step_stats* st = M.s.stats;
@@ -1254,6 +1274,10 @@ __global__ void __launch_bounds__(1024) k_fuse_apply(DevMap* maps, const StepArg
     st->apply_rounds += rr;
     st->fuse_cycles[2] += t1 - t0;
     st->fuse_cycles[3] += gtime() - t1;
+    for (int k = 13; k < 16; ++k) st->fuse_cycles[k] += 0;
+    st->fuse_cycles[13] += tmf[9];   // forward: reserve+check
+    st->fuse_cycles[14] += tmf[10] + tmf[11];  // forward: commit (plain + merges)
+    st->fuse_cycles[15] += tmf[12];  // forward: compaction
   }
 }
 
@@ -1311,10 +1335,10 @@ __global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs*
   __syncthreads();
   __shared__ int sh[32];
   __shared__ int cnt[3];
-  __shared__ long long tm[4];
+  __shared__ long long tm[16];
   __shared__ PairAcc acc;
   if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
-  if (threadIdx.x < 4) tm[threadIdx.x] = 0;
+  if (threadIdx.x < 16) tm[threadIdx.x] = 0;
   if (threadIdx.x == 0) M.scal[SC_DIRTY_N] = 0;  // k_fuse_refresh consumed the list
   pair_acc_init<1024>(&acc);
   const lm_fuse_cfg& fc = A.fc;
@@ -1324,7 +1348,9 @@ __global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs*
   int rounds = 0;
   for (int t = 0; t < T; ++t) {
     const int ts = M.s.targets[t];
+    const long long tb = gtime();
     const int Pt = bound_points<1024>(M, ts, sh);
+    if (threadIdx.x == 0) tm[8] += gtime() - tb;
     if (threadIdx.x == 0) {
       M.ledger[LG_NAIVE] += Pt * mpb;
       M.ledger[LG_PERSIST] += Pt * mpb;
@@ -1337,7 +1363,7 @@ __global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs*
     npts += Pt;
     nacts += na;
     const long long t2 = gtime();
-    rounds += apply_block<1024>(M, M.s.acts, na, cnt, sh, &acc);
+    rounds += apply_block<1024>(M, M.s.acts, na, cnt, sh, &acc, tm);
     if (threadIdx.x == 0) tm[2] += gtime() - t2;
   }
   pair_acc_flush<1024>(M, &acc);
@@ -1354,6 +1380,8 @@ __global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs*
     st->fuse_cycles[4] += tm[0];
     st->fuse_cycles[5] += tm[1];
     st->fuse_cycles[6] += tm[2];
+    st->fuse_cycles[7] += tm[3];
+    for (int k = 8; k < 16; ++k) st->fuse_cycles[k] += tm[k];
   }
 }
 
