@@ -745,7 +745,7 @@ __device__ int gather_one(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g,
     const int j = (int)(best & 0xffffffffu);
     const int owner = M.kbind[M.kp_off[ts] + j];
     if (owner < 0) {
-      if (obs_find(M, pid, ts) < 0) {
+      if (!observes(M, pid, ts)) {
         *act = ActRec{ts, pid, j, -1, LM_ACT_ADD};
         *has_act = 1;
       }
@@ -813,7 +813,7 @@ __device__ __forceinline__ int classify(const DevMap& M, const ActRec& x, int* p
     *partner = now;
     return 2;
   }
-  return obs_find(M, x.pid, x.slot) >= 0 ? 0 : 1;
+  return observes(M, x.pid, x.slot) ? 0 : 1;
 }
 
 // one action, sequential semantics; cnt = {merged, added, stale} (shared, atomic)
@@ -942,7 +942,8 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
   return rounds;
 }
 
-// recompute the representative descriptor of every dirty point in pts[0..P) (warp per point)
+// warp per point of pts[0..P) that is dirty (sort + representative descriptor) or whose
+// geometry cache is stale (rebuild), so the per-thread geometry afterwards is O(1)
 template <int BLOCK>
 __device__ void refresh_points(const DevMap& M, const int* pts, int P, int* sh) {
   int count = 0;
@@ -951,20 +952,23 @@ __device__ void refresh_points(const DevMap& M, const int* pts, int P, int* sh) 
     int mp = -1, f = 0;
     if (p < P) {
       mp = pts[p];
-      f = mp >= 0 && M.dirty[mp];
+      f = mp >= 0 && M.alive[mp] && (M.dirty[mp] || !M.gval[mp]);
     }
     int tot;
     const int at = block_excl_scan<BLOCK>(f, sh, tot);
-    if (f) M.dirty_list[count + at] = mp;
+    if (f) M.s.merge_a[count + at] = mp;  // scratch list (no apply round is in flight)
     count += tot;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int k = wid; k < count; k += BLOCK / 32) {
-    const int mp = M.dirty_list[k];
-    if (M.alive[mp]) refresh_rep_warp(M, mp, lane);
-    __syncwarp();
-    if (lane == 0) M.dirty[mp] = 0;
+    const int mp = M.s.merge_a[k];
+    if (M.dirty[mp]) {
+      refresh_rep_warp(M, mp, lane);
+      if (lane == 0) M.dirty[mp] = 0;
+      __syncwarp();
+    }
+    if (!M.gval[mp]) geo_full_warp(M, mp, lane);
   }
   __syncthreads();
 }
@@ -1191,10 +1195,13 @@ __global__ void __launch_bounds__(256) k_fuse_geo(DevMap* maps, const StepArgs* 
   const int p = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (p >= P) return;
   const int mp = M.s.pts[p];
-  if (M.dirty[mp]) {
-    if (M.alive[mp]) refresh_rep_warp(M, mp, lane);
-    __syncwarp();
-    if (lane == 0) M.dirty[mp] = 0;
+  if (M.alive[mp]) {
+    if (M.dirty[mp]) {
+      refresh_rep_warp(M, mp, lane);
+      if (lane == 0) M.dirty[mp] = 0;
+      __syncwarp();
+    }
+    if (!M.gval[mp]) geo_full_warp(M, mp, lane);
   }
   if (lane == 0) {
     point_geometry(M, mp, A.fc.dist_band_slack, M.s.geo[p]);
@@ -1293,10 +1300,12 @@ __global__ void __launch_bounds__(256) k_fuse_refresh(DevMap* maps, const StepAr
     if (!M.dirty[mp]) continue;
     if (M.alive[mp]) {
       refresh_rep_warp(M, mp, lane);
-      if (lane == 0 && !M.gval[mp]) geo_full(M, mp);
+      if (lane == 0) M.dirty[mp] = 0;
+      __syncwarp();
+      if (!M.gval[mp]) geo_full_warp(M, mp, lane);
+    } else if (lane == 0) {
+      M.dirty[mp] = 0;
     }
-    __syncwarp();
-    if (lane == 0) M.dirty[mp] = 0;
   }
 }
 

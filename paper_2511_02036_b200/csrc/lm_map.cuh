@@ -235,8 +235,10 @@ __device__ __forceinline__ int obs_find(const DevMap& M, int mp, int slot) {
   return -1;
 }
 
-// insert (slot, kp) keeping the list ordered by keyframe id; grows by doubling.
-// Returns the insert position, or -1 when the pool is exhausted.
+// append (slot, kp); grows by doubling. Lists are kept sorted by keyframe id only while the
+// point is clean: mutations append and mark the point dirty, and refresh_rep_warp sorts
+// before anything order-dependent reads the list (invariant: clean => sorted).
+// Returns the position, or -1 when the pool is exhausted.
 __device__ int obs_insert(const DevMap& M, int mp, int slot, int kp) {
   const int n = M.nobs[mp];
   if (n == M.ocap[mp]) {
@@ -251,16 +253,19 @@ __device__ int obs_insert(const DevMap& M, int mp, int slot, int kp) {
     M.ooff[mp] = off;
     M.ocap[mp] = nc;
   }
-  int2* o = M.obs + M.ooff[mp];
-  const long long kid = M.kf_id[slot];
-  int k = n;
-  while (k > 0 && M.kf_id[o[k - 1].x] > kid) {
-    o[k] = o[k - 1];
-    --k;
-  }
-  o[k] = make_int2(slot, kp);
+  M.obs[M.ooff[mp] + n] = make_int2(slot, kp);
   M.nobs[mp] = n + 1;
-  return k;
+  return n;
+}
+
+// does point mp observe keyframe slot? (branch-free scan: independent loads pipeline)
+__device__ __forceinline__ bool observes(const DevMap& M, int mp, int slot) {
+  const int2* o = M.obs + M.ooff[mp];
+  const int n = M.nobs[mp];
+  bool f = false;
+#pragma unroll 4
+  for (int k = 0; k < n; ++k) f |= o[k].x == slot;
+  return f;
 }
 
 // the representative descriptor is stale until refreshed (rep is a pure function of the
@@ -314,12 +319,14 @@ __device__ void link(const DevMap& M, int mp, int slot, int kp, PairAcc* acc = n
   const int2* o = M.obs + M.ooff[mp];
   const int n = M.nobs[mp];
   for (int k = 0; k < n; ++k) covis_add(M, slot, o[k].x, +1, acc);
+  // appended after the newest keyframe of a clean (sorted) list: the cached sums extend exactly
+  const bool newest = !M.dirty[mp] && (n == 0 || M.kf_id[o[n - 1].x] < M.kf_id[slot]);
   const int at = obs_insert(M, mp, slot, kp);
   if (at < 0) return;
   const int g = M.kp_off[slot] + kp;
   M.kbind[g] = mp;
   M.counts[(size_t)mp * M.L + M.klev[g]] += 1;
-  if (M.gval[mp] && at == n) {
+  if (M.gval[mp] && newest) {
     double rx, ry, rz, dd, d0;
     if (geo_term(M, mp, make_int2(slot, kp), rx, ry, rz, dd, d0)) {
       M.glo[mp] = d0 < M.glo[mp] ? d0 : M.glo[mp];
@@ -445,36 +452,30 @@ __device__ int replace_point_warp(const DevMap& M, int loser, int winner, int la
   for (int q = lane; q < nM * nW; q += 32) covis_add(M, oL[q / nW].x, oW[q % nW].x, +1, acc);
   for (int a = 0; a < nM; ++a)
     for (int b = a + 1 + lane; b < nM; b += 32) covis_add(M, oL[a].x, oL[b].x, +1, acc);
-  // (d) winner list = sorted merge of its own and the migrated observations (distinct kfs)
+  // (d) winner list += migrated observations (appended; the winner is marked dirty, so the
+  //     list is re-sorted by keyframe id before any order-dependent read)
   if (nM > 0) {
     int off = 0, cap = M.ocap[winner];
     if (lane == 0) {
-      // the merged list is written to a fresh block (the old one is read while merging)
-      int nc = cap < 4 ? 4 : cap;
-      while (nc < nW + nM) nc *= 2;
-      off = atomicAdd(&M.scal[SC_OBS_HEAD], nc);
-      if (off + nc > M.obs_cap) {
-        set_err(M, LM_ERR_CAPACITY);
-        off = -1;
+      off = M.ooff[winner];
+      if (nW + nM > cap) {
+        int nc = cap < 4 ? 4 : cap;
+        while (nc < nW + nM) nc *= 2;
+        off = atomicAdd(&M.scal[SC_OBS_HEAD], nc);
+        if (off + nc > M.obs_cap) {
+          set_err(M, LM_ERR_CAPACITY);
+          off = -1;
+        }
+        cap = nc;
       }
-      cap = nc;
     }
     off = __shfl_sync(0xffffffffu, off, 0);
     cap = __shfl_sync(0xffffffffu, cap, 0);
     if (off >= 0) {
       int2* B = M.obs + off;
-      for (int i = lane; i < nW; i += 32) {
-        const long long ki = M.kf_id[oW[i].x];
-        int r = 0;
-        for (int j = 0; j < nM; ++j) r += M.kf_id[oL[j].x] < ki;
-        B[i + r] = oW[i];
-      }
-      for (int j = lane; j < nM; j += 32) {
-        const long long kj = M.kf_id[oL[j].x];
-        int r = 0;
-        for (int i = 0; i < nW; ++i) r += M.kf_id[oW[i].x] < kj;
-        B[j + r] = oL[j];
-      }
+      if (off != M.ooff[winner])
+        for (int i = lane; i < nW; i += 32) B[i] = oW[i];
+      for (int j = lane; j < nM; j += 32) B[nW + j] = oL[j];
       __syncwarp();
       if (lane == 0) {
         M.ooff[winner] = off;
@@ -544,11 +545,91 @@ __device__ int kth_smallest(unsigned short* d, int n, int k) {
   return d[k];
 }
 
+// sort the observation list of mp by keyframe id (warp-cooperative rank scatter; ids are
+// distinct). Lists longer than 128 fall back to an insertion sort on lane 0.
+__device__ void sort_obs_warp(const DevMap& M, int mp, int lane) {
+  int2* o = M.obs + M.ooff[mp];
+  const int n = M.nobs[mp];
+  if (n <= 1) return;
+  if (n > 128) {
+    if (lane == 0)
+      for (int i = 1; i < n; ++i) {
+        const int2 e = o[i];
+        const long long ke = M.kf_id[e.x];
+        int k = i;
+        while (k > 0 && M.kf_id[o[k - 1].x] > ke) {
+          o[k] = o[k - 1];
+          --k;
+        }
+        o[k] = e;
+      }
+    __syncwarp();
+    return;
+  }
+  int2 e[4];
+  int r[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int i = lane + 32 * c;
+    r[c] = -1;
+    if (i < n) {
+      e[c] = o[i];
+      const long long ki = M.kf_id[e[c].x];
+      int rk = 0;
+      for (int j = 0; j < n; ++j) rk += M.kf_id[o[j].x] < ki;
+      r[c] = rk;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    if (r[c] >= 0) o[r[c]] = e[c];
+  __syncwarp();
+}
+
+// warp-parallel geometry-cache rebuild (sorted list): lanes compute the per-observation
+// terms, lane 0 accumulates them in list order (the reference's order) -> bit-identical
+__device__ void geo_full_warp(const DevMap& M, int mp, int lane) {
+  const int2* o = M.obs + M.ooff[mp];
+  const int n = M.nobs[mp];
+  double lo = INFINITY, hi = -INFINITY, ax = 0, ay = 0, az = 0;
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    const int k = c0 + lane;
+    double rx = 0, ry = 0, rz = 0, dd = 1, d0 = 0;
+    bool ok = false;
+    if (k < n) ok = geo_term(M, mp, o[k], rx, ry, rz, dd, d0);
+    const double tx = ok ? rx / dd : 0, ty = ok ? ry / dd : 0, tz = ok ? rz / dd : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, ok);
+    const int cn = n - c0 < 32 ? n - c0 : 32;
+    for (int q = 0; q < cn; ++q) {
+      const double sx = __shfl_sync(0xffffffffu, tx, q), sy = __shfl_sync(0xffffffffu, ty, q);
+      const double sz = __shfl_sync(0xffffffffu, tz, q), s0 = __shfl_sync(0xffffffffu, d0, q);
+      if (bal >> q & 1u) {
+        lo = s0 < lo ? s0 : lo;
+        hi = s0 > hi ? s0 : hi;
+        ax = ax + sx;
+        ay = ay + sy;
+        az = az + sz;
+      }
+    }
+  }
+  if (lane == 0) {
+    M.gacc[3 * mp] = ax;
+    M.gacc[3 * mp + 1] = ay;
+    M.gacc[3 * mp + 2] = az;
+    M.glo[mp] = lo;
+    M.ghi[mp] = hi;
+    M.gval[mp] = 1;
+  }
+  __syncwarp();
+}
+
 // _refresh_rep_descriptor, one warp per point: the observing descriptor whose median
 // Hamming distance to the others is smallest (first in (kf id) order wins). The median of
 // the n-1 integer distances is compared as the sum of the two middle order statistics,
-// which orders exactly like the reference's float nanmedian.
+// which orders exactly like the reference's float nanmedian. Sorts the list first.
 __device__ void refresh_rep_warp(const DevMap& M, int mp, int lane) {
+  sort_obs_warp(M, mp, lane);
   const int n = M.nobs[mp];
   if (n == 0) return;
   const int2* o = M.obs + M.ooff[mp];
@@ -558,6 +639,7 @@ __device__ void refresh_rep_warp(const DevMap& M, int mp, int lane) {
       M.rep[2 * mp] = M.kdesc[2 * g];
       M.rep[2 * mp + 1] = M.kdesc[2 * g + 1];
     }
+    __syncwarp();
     return;
   }
   if (n > REFRESH_MAXN) {
@@ -595,6 +677,7 @@ __device__ void refresh_rep_warp(const DevMap& M, int mp, int lane) {
     M.rep[2 * mp] = M.kdesc[2 * g];
     M.rep[2 * mp + 1] = M.kdesc[2 * g + 1];
   }
+  __syncwarp();
 }
 
 }  // namespace lm
