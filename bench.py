@@ -294,7 +294,7 @@ def main():
     lib.lm_profile_read(ctx.h, prof_ms, prof_n)
     lib.lm_profile_enable(ctx.h, 0)
     stages = ["insert", "cull", "select", "prep", "match", "tri", "commit", "fuse_targets", "fuse_geo",
-              "fuse_gather", "fuse_apply", "fuse_refresh", "fuse_rev"]
+              "fuse_gather", "fuse_apply", "fuse_refresh", "fuse_spec", "fuse_rev"]
     stage_ms = {s: prof_ms[k] / args.steps for k, s in enumerate(stages)}
     stage_ms["fuse"] = sum(stage_ms[s] for s in stages if s.startswith("fuse"))
     mean_ms = sum(step_ms) / len(step_ms)
@@ -355,12 +355,13 @@ def main():
                               "apply_rounds": acc["apply_rounds"] / args.steps},
             "fuse_phase_ms_per_step": {n: acc["fuse_cycles"][k] / args.steps / 1e6
                                        for k, n in enumerate(["targets", "-", "fwd_assemble", "fwd_apply",
-                                                              "rev_refresh", "rev_geometry", "rev_apply", "rev_gather",
-                                                              "rev_bound_points", "rev_apply_reserve_check",
+                                                              "rev_redo_refresh", "rev_redo_gather", "rev_apply",
+                                                              "rev_action_build", "rev_scan_reuse", "rev_apply_reserve_check",
                                                               "rev_apply_commit", "rev_apply_merges",
                                                               "rev_apply_compaction", "fwd_apply_reserve_check",
                                                               "fwd_apply_commit_merges", "fwd_apply_compaction"])
-                                       if n != "-"}}
+                                       if n != "-"},
+            "rev_recomputed_points_per_step": acc["fuse_cycles"][1] / args.steps}
     if rank == 0 and world == 1 and not args.no_cpu:
         done, dt = cpu_sample(seq, args.workload, args.cpu_budget)
         line["cpu_baseline"] = {"value": done / dt, "unit": UNIT, "cores": 1, "kind": "port",

@@ -685,12 +685,11 @@ __device__ __forceinline__ TgtView tgt_global(const DevMap& M, int ts) {
                  M.cell_start + (size_t)ts * (GRID_CELLS + 1), M.cell_items + off};
 }
 
-// project + gates + grid window search + action build for one (point, target) pair
-// (fusion.py:97-129, 178-196, 161-174). Returns 1 if visible; *act filled when an action.
-__device__ int gather_one(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g, int pid, int ts, const TgtView& T,
-                          ActRec* act, int* has_act) {
-  *has_act = 0;
-  if (!g.ok) return 0;
+// project + gates + grid window search for one (point, target) pair (fusion.py:97-129,
+// 178-196). Returns -2 if the point is not visible in the target, -1 if visible without a
+// hit, else the hit keypoint (lowest (distance, index) within the window).
+__device__ int gather_hit(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g, int ts, const TgtView& T) {
+  if (!g.ok) return -2;
   const double* R = M.R + 9 * ts;
   const double* t = M.t + 3 * ts;
   const double* C = M.C + 3 * ts;
@@ -704,9 +703,9 @@ __device__ int gather_one(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g,
   const bool inview = zc > 0 && u >= 0 && u < cam[4] && v >= 0 && v < cam[5];
   const double dx = g.x - C[0], dy = g.y - C[1], dz = g.z - C[2];
   const double d = sqrt(dx * dx + dy * dy + dz * dz);
-  if (!(zc > 0 && inview && d >= g.blo && d <= g.bhi)) return 0;
+  if (!(zc > 0 && inview && d >= g.blo && d <= g.bhi)) return -2;
   const double cosv = (dx * g.vx + dy * g.vy + dz * g.vz) / d;
-  if (!(cosv >= fc.min_view_cos)) return 0;
+  if (!(cosv >= fc.min_view_cos)) return -2;
   double lraw = log(d / g.d0) / M.log_sf;
   if (!isfinite(lraw)) lraw = 0.0;
   double lr = rint(lraw);
@@ -741,20 +740,30 @@ __device__ int gather_one(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g,
       }
     }
   }
-  if (best != ~0ull) {
-    const int j = (int)(best & 0xffffffffu);
-    const int owner = M.kbind[M.kp_off[ts] + j];
-    if (owner < 0) {
-      if (!observes(M, pid, ts)) {
-        *act = ActRec{ts, pid, j, -1, LM_ACT_ADD};
-        *has_act = 1;
-      }
-    } else if (owner != pid && M.alive[owner]) {
-      *act = ActRec{ts, pid, j, owner, LM_ACT_MERGE};
-      *has_act = 1;
-    }
+  return best == ~0ull ? -1 : (int)(best & 0xffffffffu);
+}
+
+// fuse_pass action build (fusion.py:161-174) from the hit j, against the current bindings
+__device__ __forceinline__ int build_action(const DevMap& M, int pid, int ts, int j, ActRec* act) {
+  if (j < 0) return 0;
+  const int owner = M.kbind[M.kp_off[ts] + j];
+  if (owner < 0) {
+    if (observes(M, pid, ts)) return 0;
+    *act = ActRec{ts, pid, j, -1, LM_ACT_ADD};
+    return 1;
   }
-  return 1;
+  if (owner != pid && M.alive[owner]) {
+    *act = ActRec{ts, pid, j, owner, LM_ACT_MERGE};
+    return 1;
+  }
+  return 0;
+}
+
+__device__ __forceinline__ int gather_one(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g, int pid, int ts,
+                                          const TgtView& T, ActRec* act, int* has_act) {
+  const int j = gather_hit(M, fc, g, ts, T);
+  *has_act = build_action(M, pid, ts, j, act);
+  return j >= -1;
 }
 
 // ------------------------------------------------------------------ ordered apply
@@ -856,7 +865,7 @@ template <int BLOCK>
 __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh, PairAcc* acc,
                            long long* tm = nullptr) {
   __shared__ unsigned round_sh;
-  __shared__ int npend_sh, nmerge_sh;
+  __shared__ int npend_sh, nmerge_sh, nadd_sh;
   for (int a = threadIdx.x; a < n; a += BLOCK) M.s.pend[a] = a;
   if (threadIdx.x == 0) npend_sh = n;
   __syncthreads();
@@ -883,7 +892,10 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
     }
     __syncthreads();
     // commit: stale / add per thread, merges (O(n^2) pair work) one warp each
-    if (threadIdx.x == 0) nmerge_sh = 0;
+    if (threadIdx.x == 0) {
+      nmerge_sh = 0;
+      nadd_sh = 0;
+    }
     __syncthreads();
     if (tm && threadIdx.x == 0) {
       tm[9] += gtime() - tt;
@@ -897,9 +909,13 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
       if (kind == 0) {
         atomicAdd(&cnt[2], 1);
       } else if (kind == 1) {
-        link(M, x.pid, x.slot, x.j, acc);
-        mark_dirty(M, x.pid);
-        M.found[x.pid] += 1;
+        if (M.nobs[x.pid] <= 24) {
+          link(M, x.pid, x.slot, x.j, acc);
+          mark_dirty(M, x.pid);
+          M.found[x.pid] += 1;
+        } else {  // high degree: one warp shares the covisibility bumps
+          M.s.add_list[atomicAdd(&nadd_sh, 1)] = M.s.pend[q];
+        }
         atomicAdd(&cnt[1], 1);
       } else {
         const int at = atomicAdd(&nmerge_sh, 1);
@@ -913,8 +929,16 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
       tt = gtime();
     }
     {
-      const int nm = nmerge_sh;
+      const int nm = nmerge_sh, na = nadd_sh;
       const int lane = threadIdx.x & 31;
+      for (int k = threadIdx.x >> 5; k < na; k += BLOCK / 32) {
+        const ActRec x = acts[M.s.add_list[k]];
+        link_warp(M, x.pid, x.slot, x.j, lane, acc);
+        if (lane == 0) {
+          mark_dirty(M, x.pid);
+          M.found[x.pid] += 1;
+        }
+      }
       for (int k = threadIdx.x >> 5; k < nm; k += BLOCK / 32) merge_pair_warp(M, M.s.merge_a[k], M.s.merge_b[k], lane, acc);
       if (threadIdx.x == 0) cnt[0] += nm;
     }
@@ -1309,7 +1333,34 @@ __global__ void __launch_bounds__(256) k_fuse_refresh(DevMap* maps, const StepAr
   }
 }
 
-// reverse passes: each target's bound points into the current keyframe, gather -> apply
+// speculative reverse gather: every (target, bound point) against the current keyframe,
+// on the map state after the forward apply. Thread per (target, keypoint).
+__global__ void __launch_bounds__(256) k_fuse_spec(DevMap* maps, const StepArgs* args) {
+  const StepArgs& A = args[blockIdx.z];
+  const DevMap& M = maps[A.map];
+  if (!A.do_fuse) return;
+  const int t = blockIdx.y;
+  if (t >= M.s.fctl[FC_T]) return;
+  const int ts = M.s.targets[t];
+  const int n = M.kp_n[ts];
+  const int kp = blockIdx.x * 256 + threadIdx.x;
+  if (kp >= n) return;
+  const size_t e = (size_t)t * M.kpkf_max + kp;
+  const int mp = M.kbind[M.kp_off[ts] + kp];
+  if (mp < 0 || !M.alive[mp]) {
+    M.s.spec_pid[e] = -1;
+    return;
+  }
+  PGeo g;
+  point_geometry(M, mp, A.fc.dist_band_slack, g);  // caches are valid or rebuilt (benign same-value race)
+  M.s.spec_j[e] = gather_hit(M, A.fc, g, A.cur, tgt_global(M, A.cur));
+  M.s.spec_ver[e] = M.ver[mp];
+  M.s.spec_pid[e] = mp;
+}
+
+// reverse passes: each target's bound points into the current keyframe, gather -> apply.
+// Pass t reuses the speculative hit of every point whose version is unchanged and
+// recomputes (refresh + geometry + window search) only the points earlier passes modified.
 __global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs* args, int smem_bytes) {
   const StepArgs& A = args[blockIdx.x];
   const DevMap& M = maps[A.map];
@@ -1341,7 +1392,6 @@ __global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs*
       TV = TgtView{su, sv, sl, sd, scs, sit};
     }
   }
-  __syncthreads();
   __shared__ int sh[32];
   __shared__ int cnt[3];
   __shared__ long long tm[16];
@@ -1352,28 +1402,93 @@ __global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs*
   pair_acc_init<1024>(&acc);
   const lm_fuse_cfg& fc = A.fc;
   const int cur = A.cur;
-  const long long mpb = M.mp_rec_bytes;
+  const unsigned long long mpb = M.mp_rec_bytes;
   long long alg = 0, npts = 0, nacts = 0;
   int rounds = 0;
   for (int t = 0; t < T; ++t) {
     const int ts = M.s.targets[t];
-    const long long tb = gtime();
-    const int Pt = bound_points<1024>(M, ts, sh);
-    if (threadIdx.x == 0) tm[8] += gtime() - tb;
+    const int n = M.kp_n[ts], off = M.kp_off[ts];
+    const size_t sb = (size_t)t * M.kpkf_max;
+    const long long t0 = gtime();
+    // (1) live bound points in keypoint order; reuse or schedule a recompute
+    int nredo = 0, live_n = 0, obs_n = 0;
+    for (int b0 = 0; b0 < n; b0 += 1024) {
+      const int kp = b0 + threadIdx.x;
+      int redo = 0;
+      if (kp < n) {
+        const int mp = M.kbind[off + kp];
+        int j = -3;  // -3: not a live bound point
+        if (mp >= 0 && M.alive[mp]) {
+          ++live_n;
+          obs_n += M.nobs[mp];
+          if (M.s.spec_pid[sb + kp] == mp && M.s.spec_ver[sb + kp] == M.ver[mp]) j = M.s.spec_j[sb + kp];
+          else redo = 1;
+        }
+        M.s.pass_j[kp] = j;
+      }
+      int tot;
+      const int at = block_excl_scan<1024>(redo, sh, tot);
+      if (redo) M.s.pts[nredo + at] = kp;
+      nredo += tot;
+    }
+    const int Pt = block_sum<1024>(live_n, sh);
+    const long long ob = block_sum<1024>(obs_n, sh);
     if (threadIdx.x == 0) {
+      tm[8] += gtime() - t0;
       M.ledger[LG_NAIVE] += Pt * mpb;
       M.ledger[LG_PERSIST] += Pt * mpb;
       M.ledger[LG_SMALL_FUSE] += Pt * mpb;
       M.ledger[LG_SMALL_EVENTS] += 1;
+      tm[13] += nredo;
     }
-    const long long ob = pass_obs<1024>(M, Pt, sh);
-    const int na = gather_pass<1024>(M, fc, Pt, cur, TV, true, sh, nullptr, tm);
+    // (2) recompute the modified points: refresh (warp), geometry + window search (thread)
+    if (nredo) {
+      const long long t1 = gtime();
+      for (int k = threadIdx.x; k < nredo; k += 1024) M.s.pend[k] = M.kbind[off + M.s.pts[k]];
+      __syncthreads();
+      refresh_points<1024>(M, M.s.pend, nredo, sh);
+      const long long t2 = gtime();
+      for (int k = threadIdx.x; k < nredo; k += 1024) {
+        PGeo g;
+        point_geometry(M, M.s.pend[k], fc.dist_band_slack, g);
+        M.s.pass_j[M.s.pts[k]] = gather_hit(M, fc, g, cur, TV);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        tm[0] += t2 - t1;
+        tm[1] += gtime() - t2;
+      }
+    }
+    // (3) visibility + action build in keypoint order
+    const long long t3 = gtime();
+    int na = 0;
+    for (int b0 = 0; b0 < n; b0 += 1024) {
+      const int kp = b0 + threadIdx.x;
+      ActRec a;
+      int has = 0;
+      if (kp < n) {
+        const int j = M.s.pass_j[kp];
+        if (j >= -1) {
+          const int mp = M.kbind[off + kp];
+          atomicAdd(&M.visible[mp], 1);
+          has = build_action(M, mp, cur, j, &a);
+        }
+      }
+      int tot;
+      const int at = block_excl_scan<1024>(has, sh, tot);
+      if (has) M.s.acts[na + at] = a;
+      na += tot;
+    }
+    __syncthreads();
     alg += pass_bytes(Pt, ob, M.kp_n[cur], na);
     npts += Pt;
     nacts += na;
-    const long long t2 = gtime();
+    const long long t4 = gtime();
     rounds += apply_block<1024>(M, M.s.acts, na, cnt, sh, &acc, tm);
-    if (threadIdx.x == 0) tm[2] += gtime() - t2;
+    if (threadIdx.x == 0) {
+      tm[3] += t4 - t3;
+      tm[2] += gtime() - t4;
+    }
   }
   pair_acc_flush<1024>(M, &acc);
   if (threadIdx.x == 0) {
@@ -1390,7 +1505,8 @@ __global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs*
     st->fuse_cycles[5] += tm[1];
     st->fuse_cycles[6] += tm[2];
     st->fuse_cycles[7] += tm[3];
-    for (int k = 8; k < 16; ++k) st->fuse_cycles[k] += tm[k];
+    for (int k = 8; k < 13; ++k) st->fuse_cycles[k] += tm[k];
+    st->fuse_cycles[1] += tm[13];  // recomputed (point, pass) pairs (count, not ns)
   }
 }
 

@@ -98,6 +98,11 @@ struct Scratch {
   int* blk_cnt;          // [act_cap/256 + 1]
   int* blk_off;
   int* fctl;             // [8] fusion control: targets, forward points, ...
+  int* spec_pid;         // [TMAX*kpkf_max] speculative reverse gather: point bound at (t, kp)
+  int* spec_ver;         //   its version when gathered
+  int* spec_j;           //   -2 not visible, -1 visible without a hit, else the hit keypoint
+  int* pass_j;           // [kpkf_max] per-pass resolved hit per target keypoint
+  int* add_list;         // [act_cap] high-degree ADDs committed warp-cooperatively
   int* act_flag;         // [TMAX*kpkf_max]
   int* vis_flag;         // [TMAX*kpkf_max]
   int pts_cap;
@@ -152,6 +157,7 @@ struct DevMap {
   double* glo;
   double* ghi;
   unsigned char* gval;
+  int* ver;          // bumped on every observation change (speculative reverse gather)
   // deterministic-reservation tables (apply): round-tagged min action index per entity
   unsigned long long* res_pt;    // [mp_cap]
   unsigned long long* res_slot;  // [kp_cap]
@@ -326,6 +332,7 @@ __device__ void link(const DevMap& M, int mp, int slot, int kp, PairAcc* acc = n
   const int g = M.kp_off[slot] + kp;
   M.kbind[g] = mp;
   M.counts[(size_t)mp * M.L + M.klev[g]] += 1;
+  M.ver[mp] += 1;
   if (M.gval[mp] && newest) {
     double rx, ry, rz, dd, d0;
     if (geo_term(M, mp, make_int2(slot, kp), rx, ry, rz, dd, d0)) {
@@ -340,6 +347,37 @@ __device__ void link(const DevMap& M, int mp, int slot, int kp, PairAcc* acc = n
   }
 }
 
+// link() for high-degree points: lanes share the covisibility bumps, lane 0 the rest
+__device__ void link_warp(const DevMap& M, int mp, int slot, int kp, int lane, PairAcc* acc) {
+  const int2* o = M.obs + M.ooff[mp];
+  const int n = M.nobs[mp];
+  for (int k = lane; k < n; k += 32) covis_add(M, slot, o[k].x, +1, acc);
+  __syncwarp();
+  if (lane == 0) {
+    const bool newest = !M.dirty[mp] && (n == 0 || M.kf_id[o[n - 1].x] < M.kf_id[slot]);
+    const int at = obs_insert(M, mp, slot, kp);
+    if (at >= 0) {
+      const int g = M.kp_off[slot] + kp;
+      M.kbind[g] = mp;
+      M.counts[(size_t)mp * M.L + M.klev[g]] += 1;
+      M.ver[mp] += 1;
+      double rx, ry, rz, dd, d0;
+      if (M.gval[mp] && newest) {
+        if (geo_term(M, mp, make_int2(slot, kp), rx, ry, rz, dd, d0)) {
+          M.glo[mp] = d0 < M.glo[mp] ? d0 : M.glo[mp];
+          M.ghi[mp] = d0 > M.ghi[mp] ? d0 : M.ghi[mp];
+          M.gacc[3 * mp] = M.gacc[3 * mp] + rx / dd;
+          M.gacc[3 * mp + 1] = M.gacc[3 * mp + 1] + ry / dd;
+          M.gacc[3 * mp + 2] = M.gacc[3 * mp + 2] + rz / dd;
+        }
+      } else {
+        M.gval[mp] = 0;
+      }
+    }
+  }
+  __syncwarp();
+}
+
 // _unrecord_obs of list entry k: unbind, uncount, covis -1 with every remaining observer
 __device__ void unlink_at(const DevMap& M, int mp, int k, PairAcc* acc = nullptr) {
   int2* o = M.obs + M.ooff[mp];
@@ -348,6 +386,7 @@ __device__ void unlink_at(const DevMap& M, int mp, int k, PairAcc* acc = nullptr
   for (int m = k; m < n; ++m) o[m] = o[m + 1];
   M.nobs[mp] = n;
   M.gval[mp] = 0;
+  M.ver[mp] += 1;
   const int g = M.kp_off[e.x] + e.y;
   M.kbind[g] = -1;
   M.counts[(size_t)mp * M.L + M.klev[g]] -= 1;
@@ -411,6 +450,7 @@ __device__ void kill_point_warp(const DevMap& M, int mp, int lane, PairAcc* acc)
     M.nobs[mp] = 0;
     M.alive[mp] = 0;
     M.gval[mp] = 0;
+    M.ver[mp] += 1;
   }
   __syncwarp();
 }
@@ -493,6 +533,8 @@ __device__ int replace_point_warp(const DevMap& M, int loser, int winner, int la
     M.alive[loser] = 0;
     M.gval[winner] = 0;
     M.gval[loser] = 0;
+    M.ver[winner] += 1;
+    M.ver[loser] += 1;
     mark_dirty(M, winner);
   }
   __syncwarp();
