@@ -533,7 +533,7 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(d.pos, 3 * MP); A(d.rep, 2 * MP); A(d.alive, MP); A(d.found, MP); A(d.visible, MP); A(d.first_kf, MP);
   A(d.nobs, MP); A(d.ocap, MP); A(d.ooff, MP); A(d.obs, (size_t)d.obs_cap); A(d.counts, MP * d.L);
   A(d.dirty, MP); A(d.dirty_list, MP); A(d.res_pt, MP); A(d.res_slot, KP);
-  A(d.gacc, 3 * MP); A(d.glo, MP); A(d.ghi, MP); A(d.gval, MP); A(d.ver, MP);
+  A(d.gacc, 3 * MP); A(d.glo, MP); A(d.ghi, MP); A(d.gval, MP); A(d.ver, MP); A(d.hit, MP);
   A(d.covis, K * K);
   A(d.recent_id, MP); A(d.recent_born, MP);
   A(d.scal, SC_N); A(d.ledger, LG_N);
@@ -552,13 +552,13 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(s.acts, (size_t)s.act_cap); A(s.act_flag, (size_t)s.act_cap); A(s.vis_flag, (size_t)s.act_cap);
   A(s.pend, (size_t)s.act_cap); A(s.ready, (size_t)s.act_cap); A(s.merge_a, (size_t)s.act_cap); A(s.merge_b, (size_t)s.act_cap); A(s.acts2, (size_t)s.act_cap);
   A(s.blk_cnt, (size_t)s.act_cap / 256 + 2); A(s.blk_off, (size_t)s.act_cap / 256 + 2); A(s.fctl, 8);
-  A(s.spec_pid, (size_t)s.act_cap); A(s.spec_ver, (size_t)s.act_cap); A(s.spec_j, (size_t)s.act_cap);
   A(s.pass_j, d.kpkf_max); A(s.add_list, (size_t)s.act_cap);
   A(m->d_stats, 1); A(m->d_totals, 1); A(m->d_result, 4 + 1024 + TMAX);
 #undef A
   s.stats = m->d_stats;
   CU(cudaMemsetAsync(d.res_pt, 0xff, sizeof(unsigned long long) * MP, ctx->stream));
   CU(cudaMemsetAsync(d.res_slot, 0xff, sizeof(unsigned long long) * KP, ctx->stream));
+  CU(cudaMemsetAsync(d.hit, 0xff, sizeof(int2) * MP, ctx->stream));
   m->state.assign(K, KF_FREE);
   m->kp_n.assign(K, 0);
   m->kp_off.assign(K, 0);
@@ -582,6 +582,8 @@ int lm_map_reset(lm_ctx* ctx, int32_t map) {
   CU(cudaMemsetAsync(d.counts, 0, sizeof(int) * MP * d.L, ctx->stream));
   CU(cudaMemsetAsync(d.dirty, 0, sizeof(int) * MP, ctx->stream));
   CU(cudaMemsetAsync(d.gval, 0, MP, ctx->stream));
+  CU(cudaMemsetAsync(d.hit, 0xff, sizeof(int2) * MP, ctx->stream));
+  CU(cudaMemsetAsync(d.ver, 0, sizeof(int) * MP, ctx->stream));
   CU(cudaMemsetAsync(d.scal, 0, sizeof(int) * SC_N, ctx->stream));
   CU(cudaMemsetAsync(d.ledger, 0, sizeof(unsigned long long) * LG_N, ctx->stream));
   CU(cudaMemsetAsync(m->d_totals, 0, sizeof(lm_step_stats), ctx->stream));
@@ -1407,6 +1409,8 @@ int lm_map_rewind(lm_ctx* ctx, int32_t map) {
   CU(cudaMemsetAsync(d.counts, 0, sizeof(int) * MP * d.L, st));
   CU(cudaMemsetAsync(d.dirty, 0, sizeof(int) * MP, st));
   CU(cudaMemsetAsync(d.gval, 0, MP, st));
+  CU(cudaMemsetAsync(d.hit, 0xff, sizeof(int2) * MP, st));
+  CU(cudaMemsetAsync(d.ver, 0, sizeof(int) * MP, st));
   CU(cudaMemsetAsync(d.scal, 0, sizeof(int) * SC_N, st));
   CU(cudaMemsetAsync(d.ledger, 0, sizeof(unsigned long long) * LG_N, st));
   CU(cudaMemsetAsync(m->d_totals, 0, sizeof(lm_step_stats), st));

@@ -1345,17 +1345,14 @@ __global__ void __launch_bounds__(256) k_fuse_spec(DevMap* maps, const StepArgs*
   const int n = M.kp_n[ts];
   const int kp = blockIdx.x * 256 + threadIdx.x;
   if (kp >= n) return;
-  const size_t e = (size_t)t * M.kpkf_max + kp;
   const int mp = M.kbind[M.kp_off[ts] + kp];
-  if (mp < 0 || !M.alive[mp]) {
-    M.s.spec_pid[e] = -1;
-    return;
-  }
+  if (mp < 0 || !M.alive[mp]) return;
+  // the projection target is always the current keyframe, so the result is per point;
+  // a point bound in several targets is gathered by each of them (identical values)
   PGeo g;
-  point_geometry(M, mp, A.fc.dist_band_slack, g);  // caches are valid or rebuilt (benign same-value race)
-  M.s.spec_j[e] = gather_hit(M, A.fc, g, A.cur, tgt_global(M, A.cur));
-  M.s.spec_ver[e] = M.ver[mp];
-  M.s.spec_pid[e] = mp;
+  point_geometry(M, mp, A.fc.dist_band_slack, g);  // caches valid or rebuilt (benign same-value race)
+  const int j = gather_hit(M, A.fc, g, A.cur, tgt_global(M, A.cur));
+  M.hit[mp] = make_int2(M.ver[mp], j);
 }
 
 // reverse passes: each target's bound points into the current keyframe, gather -> apply.
@@ -1408,7 +1405,6 @@ __global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs*
   for (int t = 0; t < T; ++t) {
     const int ts = M.s.targets[t];
     const int n = M.kp_n[ts], off = M.kp_off[ts];
-    const size_t sb = (size_t)t * M.kpkf_max;
     const long long t0 = gtime();
     // (1) live bound points in keypoint order; reuse or schedule a recompute
     int nredo = 0, live_n = 0, obs_n = 0;
@@ -1421,7 +1417,8 @@ __global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs*
         if (mp >= 0 && M.alive[mp]) {
           ++live_n;
           obs_n += M.nobs[mp];
-          if (M.s.spec_pid[sb + kp] == mp && M.s.spec_ver[sb + kp] == M.ver[mp]) j = M.s.spec_j[sb + kp];
+          const int2 h = M.hit[mp];
+          if (h.x == M.ver[mp]) j = h.y;
           else redo = 1;
         }
         M.s.pass_j[kp] = j;
@@ -1449,9 +1446,12 @@ __global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs*
       refresh_points<1024>(M, M.s.pend, nredo, sh);
       const long long t2 = gtime();
       for (int k = threadIdx.x; k < nredo; k += 1024) {
+        const int mp = M.s.pend[k];
         PGeo g;
-        point_geometry(M, M.s.pend[k], fc.dist_band_slack, g);
-        M.s.pass_j[M.s.pts[k]] = gather_hit(M, fc, g, cur, TV);
+        point_geometry(M, mp, fc.dist_band_slack, g);
+        const int j = gather_hit(M, fc, g, cur, TV);
+        M.s.pass_j[M.s.pts[k]] = j;
+        M.hit[mp] = make_int2(M.ver[mp], j);  // later passes reuse it until the point changes
       }
       __syncthreads();
       if (threadIdx.x == 0) {

@@ -98,9 +98,6 @@ struct Scratch {
   int* blk_cnt;          // [act_cap/256 + 1]
   int* blk_off;
   int* fctl;             // [8] fusion control: targets, forward points, ...
-  int* spec_pid;         // [TMAX*kpkf_max] speculative reverse gather: point bound at (t, kp)
-  int* spec_ver;         //   its version when gathered
-  int* spec_j;           //   -2 not visible, -1 visible without a hit, else the hit keypoint
   int* pass_j;           // [kpkf_max] per-pass resolved hit per target keypoint
   int* add_list;         // [act_cap] high-degree ADDs committed warp-cooperatively
   int* act_flag;         // [TMAX*kpkf_max]
@@ -158,6 +155,7 @@ struct DevMap {
   double* ghi;
   unsigned char* gval;
   int* ver;          // bumped on every observation change (speculative reverse gather)
+  int2* hit;         // per point: {version, hit into the current keyframe (-2/-1/j)}
   // deterministic-reservation tables (apply): round-tagged min action index per entity
   unsigned long long* res_pt;    // [mp_cap]
   unsigned long long* res_slot;  // [kp_cap]
