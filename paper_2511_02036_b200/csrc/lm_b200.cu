@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, in
       __shared__ int c[3];
       __shared__ PairAcc acc;
       if (tid < 3) c[tid] = 0;
-      pair_acc_init<1024>(&acc);
+      pair_acc_init<1024>(&acc, A.n_slots - 1);
       apply_block<1024>(M, M.s.acts, A.n, c, sh, &acc);
       pair_acc_flush<1024>(M, &acc);
       if (tid == 0) {

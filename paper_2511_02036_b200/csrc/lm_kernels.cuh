@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
   __shared__ int sh[32];
   __shared__ PairAcc acc;
   __shared__ int kills[1024];
-  pair_acc_init<1024>(&acc);
+  pair_acc_init<1024>(&acc, A.cur);
   const int n = M.scal[SC_RECENT_N];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int kept = 0, culled = 0;
@@ -872,7 +872,11 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
   int rounds = 0;
   while (npend_sh > 0) {
     const int np = npend_sh;
-    if (threadIdx.x == 0) round_sh = (unsigned)atomicAdd(&M.scal[SC_ROUND], 1) + 1u;
+    if (threadIdx.x == 0) {
+      round_sh = (unsigned)atomicAdd(&M.scal[SC_ROUND], 1) + 1u;
+      nmerge_sh = 0;
+      nadd_sh = 0;
+    }
     __syncthreads();
     const unsigned rnd = round_sh;
     long long tt = gtime();
@@ -885,25 +889,16 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
       });
     }
     __syncthreads();
+    // check + commit fused: an action holding all its keys shares no entity with any other
+    // committing action, so nothing it reads can change under it. Stale / plain adds run per
+    // thread; merges and high-degree adds (O(n) .. O(n^2) pair work) one warp each.
     for (int q = threadIdx.x; q < np; q += BLOCK) {
       const int a = M.s.pend[q];
       const unsigned long long tag = res_tag(rnd, a);
-      M.s.ready[q] = for_keys(M, acts[a], [&](bool pt, int id) { return (pt ? M.res_pt[id] : M.res_slot[id]) == tag; });
-    }
-    __syncthreads();
-    // commit: stale / add per thread, merges (O(n^2) pair work) one warp each
-    if (threadIdx.x == 0) {
-      nmerge_sh = 0;
-      nadd_sh = 0;
-    }
-    __syncthreads();
-    if (tm && threadIdx.x == 0) {
-      tm[9] += gtime() - tt;
-      tt = gtime();
-    }
-    for (int q = threadIdx.x; q < np; q += BLOCK) {
-      if (!M.s.ready[q]) continue;
-      const ActRec x = acts[M.s.pend[q]];
+      const ActRec x = acts[a];
+      const int ready = for_keys(M, x, [&](bool pt, int id) { return (pt ? M.res_pt[id] : M.res_slot[id]) == tag; });
+      M.s.ready[q] = ready;
+      if (!ready) continue;
       int partner = -1;
       const int kind = classify(M, x, &partner);
       if (kind == 0) {
@@ -914,7 +909,7 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
           mark_dirty(M, x.pid);
           M.found[x.pid] += 1;
         } else {  // high degree: one warp shares the covisibility bumps
-          M.s.add_list[atomicAdd(&nadd_sh, 1)] = M.s.pend[q];
+          M.s.add_list[atomicAdd(&nadd_sh, 1)] = a;
         }
         atomicAdd(&cnt[1], 1);
       } else {
@@ -1271,7 +1266,7 @@ __global__ void __launch_bounds__(1024) k_fuse_apply(DevMap* maps, const StepArg
   __shared__ PairAcc acc;
   const long long t0 = gtime();
   if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
-  pair_acc_init<1024>(&acc);
+  pair_acc_init<1024>(&acc, A.cur);
   const int nb = (T * P + 255) / 256;
   int base = 0;
   for (int c0 = 0; c0 < nb; c0 += 1024) {  // exclusive scan of the per-CTA counts
@@ -1396,7 +1391,7 @@ __global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs*
   if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
   if (threadIdx.x < 16) tm[threadIdx.x] = 0;
   if (threadIdx.x == 0) M.scal[SC_DIRTY_N] = 0;  // k_fuse_refresh consumed the list
-  pair_acc_init<1024>(&acc);
+  pair_acc_init<1024>(&acc, A.cur);
   const lm_fuse_cfg& fc = A.fc;
   const int cur = A.cur;
   const unsigned long long mpb = M.mp_rec_bytes;

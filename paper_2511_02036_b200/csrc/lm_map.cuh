@@ -178,10 +178,16 @@ __device__ __forceinline__ int hamming(uint4 a0, uint4 a1, uint4 b0, uint4 b1) {
 }
 
 // Shared-memory accumulator of covisibility deltas: the commutative bumps of a whole
-// kernel land in a per-CTA open-addressing table (one smem atomic each) and are flushed to
-// the dense matrix once, instead of contending global atomics on a few hot pairs.
-constexpr int PAIR_H = 2048;
+// kernel land in shared memory (one smem atomic each) and are flushed to the dense matrix
+// once, instead of contending global atomics on a few hot pairs. Pairs of keyframes in the
+// window of the PAIR_W most recent slots use a dense upper-triangle table (no probing);
+// other pairs an open-addressing hash; overflow falls back to global atomics.
+constexpr int PAIR_W = 96;
+constexpr int PAIR_T = PAIR_W * (PAIR_W - 1) / 2;
+constexpr int PAIR_H = 1024;
 struct PairAcc {
+  int wbase;
+  int win[PAIR_T];
   unsigned key[PAIR_H];  // lo << 16 | hi, 0xffffffff = empty
   int val[PAIR_H];
 };
@@ -191,17 +197,33 @@ __device__ __forceinline__ void covis_global(const DevMap& M, int a, int b, int 
   atomicAdd(&M.covis[(size_t)b * M.kf_cap + a], d);
 }
 
+__device__ __forceinline__ int tri_index(int i, int j) {  // i < j < PAIR_W
+  return i * (2 * PAIR_W - i - 1) / 2 + (j - i - 1);
+}
+
 __device__ __forceinline__ void covis_add(const DevMap& M, int a, int b, int d, PairAcc* acc = nullptr) {
   if (a == b) return;
   if (acc) {
-    const unsigned lo = a < b ? a : b, hi = a < b ? b : a;
-    const unsigned k = lo << 16 | hi;
-    unsigned h = (k * 2654435761u) >> 21;  // 11 bits
+    const int lo = a < b ? a : b, hi = a < b ? b : a;
+    const int il = lo - acc->wbase, ih = hi - acc->wbase;
+    if (il >= 0 && ih < PAIR_W) {
+      atomicAdd(&acc->win[tri_index(il, ih)], d);
+      return;
+    }
+    const unsigned k = (unsigned)lo << 16 | (unsigned)hi;
+    unsigned h = (k * 2654435761u) >> 22;  // 10 bits
     for (int probe = 0; probe < 16; ++probe) {
-      const unsigned prev = atomicCAS(&acc->key[h], 0xffffffffu, k);
-      if (prev == 0xffffffffu || prev == k) {
+      const unsigned cur = acc->key[h];
+      if (cur == k) {
         atomicAdd(&acc->val[h], d);
         return;
+      }
+      if (cur == 0xffffffffu) {
+        const unsigned prev = atomicCAS(&acc->key[h], 0xffffffffu, k);
+        if (prev == 0xffffffffu || prev == k) {
+          atomicAdd(&acc->val[h], d);
+          return;
+        }
       }
       h = (h + 1) & (PAIR_H - 1);
     }
@@ -210,22 +232,29 @@ __device__ __forceinline__ void covis_add(const DevMap& M, int a, int b, int d, 
 }
 
 template <int BLOCK>
-__device__ void pair_acc_init(PairAcc* acc) {
+__device__ void pair_acc_init(PairAcc* acc, int newest_slot) {
+  for (int q = threadIdx.x; q < PAIR_T; q += BLOCK) acc->win[q] = 0;
   for (int h = threadIdx.x; h < PAIR_H; h += BLOCK) {
     acc->key[h] = 0xffffffffu;
     acc->val[h] = 0;
   }
+  if (threadIdx.x == 0) acc->wbase = newest_slot - (PAIR_W - 1) < 0 ? 0 : newest_slot - (PAIR_W - 1);
   __syncthreads();
 }
 
 template <int BLOCK>
 __device__ void pair_acc_flush(const DevMap& M, PairAcc* acc) {
   __syncthreads();
+  for (int q = threadIdx.x; q < PAIR_W * PAIR_W; q += BLOCK) {
+    const int i = q / PAIR_W, j = q - i * PAIR_W;
+    if (i < j) {
+      const int v = acc->win[tri_index(i, j)];
+      if (v) covis_global(M, acc->wbase + i, acc->wbase + j, v);
+    }
+  }
   for (int h = threadIdx.x; h < PAIR_H; h += BLOCK) {
     const unsigned k = acc->key[h];
     if (k != 0xffffffffu && acc->val[h] != 0) covis_global(M, (int)(k >> 16), (int)(k & 0xffff), acc->val[h]);
-    acc->key[h] = 0xffffffffu;
-    acc->val[h] = 0;
   }
   __syncthreads();
 }
