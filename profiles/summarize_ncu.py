@@ -35,6 +35,7 @@ METRICS = {
     "lts__t_bytes.sum": "l2_bytes",
 }
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
+        "ns": 1e-9, "us": 1e-6, "ms": 1e-3,
         "second": 1}
 
 
