@@ -533,6 +533,7 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(d.pos, 3 * MP); A(d.rep, 2 * MP); A(d.alive, MP); A(d.found, MP); A(d.visible, MP); A(d.first_kf, MP);
   A(d.nobs, MP); A(d.ocap, MP); A(d.ooff, MP); A(d.obs, (size_t)d.obs_cap); A(d.counts, MP * d.L);
   A(d.dirty, MP); A(d.dirty_list, MP); A(d.res_pt, MP); A(d.res_slot, KP);
+  A(d.res_ex, MP); A(d.res_pair, RES_PAIR); A(d.grp_head, MP);
   A(d.gacc, 3 * MP); A(d.glo, MP); A(d.ghi, MP); A(d.gval, MP); A(d.ver, MP); A(d.hit, MP);
   A(d.covis, K * K);
   A(d.recent_id, MP); A(d.recent_born, MP);
@@ -553,11 +554,15 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(s.pend, (size_t)s.act_cap); A(s.ready, (size_t)s.act_cap); A(s.merge_a, (size_t)s.act_cap); A(s.merge_b, (size_t)s.act_cap); A(s.acts2, (size_t)s.act_cap);
   A(s.blk_cnt, (size_t)s.act_cap / 256 + 2); A(s.blk_off, (size_t)s.act_cap / 256 + 2); A(s.fctl, 8);
   A(s.pass_j, d.kpkf_max); A(s.add_list, (size_t)s.act_cap);
+  A(s.def, (size_t)s.act_cap); A(s.dnxt, (size_t)s.act_cap); A(s.grp_list, (size_t)s.act_cap);
   A(m->d_stats, 1); A(m->d_totals, 1); A(m->d_result, 4 + 1024 + TMAX);
 #undef A
   s.stats = m->d_stats;
   CU(cudaMemsetAsync(d.res_pt, 0xff, sizeof(unsigned long long) * MP, ctx->stream));
   CU(cudaMemsetAsync(d.res_slot, 0xff, sizeof(unsigned long long) * KP, ctx->stream));
+  CU(cudaMemsetAsync(d.res_ex, 0xff, sizeof(unsigned long long) * MP, ctx->stream));
+  CU(cudaMemsetAsync(d.res_pair, 0xff, sizeof(unsigned long long) * RES_PAIR, ctx->stream));
+  CU(cudaMemsetAsync(d.grp_head, 0, sizeof(unsigned long long) * MP, ctx->stream));
   CU(cudaMemsetAsync(d.hit, 0xff, sizeof(int2) * MP, ctx->stream));
   m->state.assign(K, KF_FREE);
   m->kp_n.assign(K, 0);
@@ -589,6 +594,9 @@ int lm_map_reset(lm_ctx* ctx, int32_t map) {
   CU(cudaMemsetAsync(m->d_totals, 0, sizeof(lm_step_stats), ctx->stream));
   CU(cudaMemsetAsync(d.res_pt, 0xff, sizeof(unsigned long long) * MP, ctx->stream));
   CU(cudaMemsetAsync(d.res_slot, 0xff, sizeof(unsigned long long) * d.kp_cap, ctx->stream));
+  CU(cudaMemsetAsync(d.res_ex, 0xff, sizeof(unsigned long long) * MP, ctx->stream));
+  CU(cudaMemsetAsync(d.res_pair, 0xff, sizeof(unsigned long long) * RES_PAIR, ctx->stream));
+  CU(cudaMemsetAsync(d.grp_head, 0, sizeof(unsigned long long) * MP, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   m->slot_of.clear();
   std::fill(m->state.begin(), m->state.end(), KF_FREE);
@@ -1416,6 +1424,9 @@ int lm_map_rewind(lm_ctx* ctx, int32_t map) {
   CU(cudaMemsetAsync(m->d_totals, 0, sizeof(lm_step_stats), st));
   CU(cudaMemsetAsync(d.res_pt, 0xff, sizeof(unsigned long long) * MP, st));
   CU(cudaMemsetAsync(d.res_slot, 0xff, sizeof(unsigned long long) * d.kp_cap, st));
+  CU(cudaMemsetAsync(d.res_ex, 0xff, sizeof(unsigned long long) * MP, st));
+  CU(cudaMemsetAsync(d.res_pair, 0xff, sizeof(unsigned long long) * RES_PAIR, st));
+  CU(cudaMemsetAsync(d.grp_head, 0, sizeof(unsigned long long) * MP, st));
   if (m->kp_head) CU(cudaMemsetAsync(d.kbind, 0xff, sizeof(int) * m->kp_head, st));
   if (m->n_slots) {
     k_rewind_state<<<(m->n_slots + 255) / 256, 256, 0, st>>>(d, m->n_slots);

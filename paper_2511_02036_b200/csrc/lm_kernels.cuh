@@ -774,27 +774,49 @@ __device__ __forceinline__ int gather_one(const DevMap& M, const lm_fuse_cfg& fc
 // loser) with atomicMin of a round-tagged action index; actions holding all their keys
 // commit together (their entity sets are disjoint, and no earlier pending action touches
 // them), the rest retry. Covisibility bumps are atomic adds and commute.
+//
+// Points have two access modes. Merges (and ADDs that turn into merges) need a point
+// exclusively; a plain ADD only appends a not-yet-observed keyframe to the point, and
+// such appends commute with each other (the resulting observation set, counters and
+// covisibility deltas do not depend on their order), so ADDs share the point and are
+// serialised only against earlier exclusive users. Two ADDs of the same point into the
+// same keyframe do not commute (the second is stale); they collide on a hashed
+// (point, keyframe) key. Shared-ready ADDs of one point are linked as one group.
+
+enum KeyMode { KM_SLOT = 0, KM_EX = 1, KM_SH = 2, KM_PAIR = 3 };
 
 __device__ __forceinline__ unsigned long long res_tag(unsigned round, int a) {
   return ((unsigned long long)(0xffffffffu - round) << 32) | (unsigned)a;
 }
 
-// visit the key set of action x under the current state; op(is_point, id) -> bool (false stops)
+__device__ __forceinline__ int pair_key(int pid, int slot) {
+  unsigned h = (unsigned)pid * 0x9E3779B1u + (unsigned)slot * 0x85EBCA77u;
+  h ^= h >> 15;
+  return (int)(h & (RES_PAIR - 1));
+}
+
+// visit the key set of action x under the current state; op(mode, id) -> bool (false stops).
+// A key is always visited before the state it guards is read.
 template <class Op>
 __device__ bool for_keys(const DevMap& M, const ActRec& x, Op op) {
-  if (!op(true, x.pid)) return false;
+  if (!op(KM_SH, x.pid)) return false;
   if (!M.alive[x.pid] || M.kf_state[x.slot] != KF_LIVE) return true;  // stale
   const int g = M.kp_off[x.slot] + x.j;
-  if (!op(false, g)) return false;
+  if (!op(KM_SLOT, g)) return false;
   const int now = M.kbind[g];
   int partner = -1;
   if (x.kind == LM_ACT_MERGE) {
-    if (x.other >= 0 && !op(true, x.other)) return false;
-    if (now >= 0 && now != x.other && now != x.pid && !op(true, now)) return false;
+    if (!op(KM_EX, x.pid)) return false;
+    if (x.other >= 0 && !op(KM_EX, x.other)) return false;
+    if (now >= 0 && now != x.other && now != x.pid && !op(KM_EX, now)) return false;
     if (x.other >= 0 && M.alive[x.other] && x.other != x.pid && now == x.other) partner = x.other;
   } else if (now >= 0) {
-    if (now != x.pid && !op(true, now)) return false;
-    if (M.alive[now] && now != x.pid) partner = now;
+    if (now != x.pid) {  // the slot was claimed: merge with its owner (or stale)
+      if (!op(KM_EX, x.pid) || !op(KM_EX, now)) return false;
+      if (M.alive[now]) partner = now;
+    }
+  } else if (!op(KM_PAIR, pair_key(x.pid, x.slot))) {
+    return false;
   }
   if (partner >= 0) {
     const int na = M.nobs[x.pid], nb = M.nobs[partner];
@@ -802,9 +824,27 @@ __device__ bool for_keys(const DevMap& M, const ActRec& x, Op op) {
     const int2* o = M.obs + M.ooff[loser];
     const int n = M.nobs[loser];
     for (int k = 0; k < n; ++k)
-      if (!op(false, M.kp_off[o[k].x] + o[k].y)) return false;
+      if (!op(KM_SLOT, M.kp_off[o[k].x] + o[k].y)) return false;
   }
   return true;
+}
+
+__device__ __forceinline__ void reserve_key(const DevMap& M, int mode, int id, unsigned long long tag) {
+  if (mode == KM_SLOT) {
+    atomicMin(&M.res_slot[id], tag);
+  } else if (mode == KM_PAIR) {
+    atomicMin(&M.res_pair[id], tag);
+  } else {
+    atomicMin(&M.res_pt[id], tag);
+    if (mode == KM_EX) atomicMin(&M.res_ex[id], tag);
+  }
+}
+
+__device__ __forceinline__ bool holds_key(const DevMap& M, int mode, int id, unsigned long long tag) {
+  if (mode == KM_SLOT) return M.res_slot[id] == tag;
+  if (mode == KM_PAIR) return M.res_pair[id] == tag;
+  if (mode == KM_EX) return M.res_pt[id] == tag;
+  return M.res_ex[id] >= tag;  // shared: no earlier exclusive user pending
 }
 
 // outcome of action x under the current state: 0 stale, 1 add, 2 merge with *partner
@@ -865,17 +905,20 @@ template <int BLOCK>
 __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh, PairAcc* acc,
                            long long* tm = nullptr) {
   __shared__ unsigned round_sh;
-  __shared__ int npend_sh, nmerge_sh, nadd_sh;
+  __shared__ int npend_sh, nmerge_sh, nadd_sh, ndef_sh, ngrp_sh;
   for (int a = threadIdx.x; a < n; a += BLOCK) M.s.pend[a] = a;
   if (threadIdx.x == 0) npend_sh = n;
   __syncthreads();
   int rounds = 0;
+  const int lane = threadIdx.x & 31;
   while (npend_sh > 0) {
     const int np = npend_sh;
     if (threadIdx.x == 0) {
       round_sh = (unsigned)atomicAdd(&M.scal[SC_ROUND], 1) + 1u;
       nmerge_sh = 0;
       nadd_sh = 0;
+      ndef_sh = 0;
+      ngrp_sh = 0;
     }
     __syncthreads();
     const unsigned rnd = round_sh;
@@ -883,20 +926,19 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
     for (int q = threadIdx.x; q < np; q += BLOCK) {
       const int a = M.s.pend[q];
       const unsigned long long tag = res_tag(rnd, a);
-      for_keys(M, acts[a], [&](bool pt, int id) {
-        atomicMin(pt ? &M.res_pt[id] : &M.res_slot[id], tag);
+      for_keys(M, acts[a], [&](int mode, int id) {
+        reserve_key(M, mode, id, tag);
         return true;
       });
     }
     __syncthreads();
-    // check + commit fused: an action holding all its keys shares no entity with any other
-    // committing action, so nothing it reads can change under it. Stale / plain adds run per
-    // thread; merges and high-degree adds (O(n) .. O(n^2) pair work) one warp each.
+    // check (read-only): stale actions are counted, merges queued for warps, ADDs chained
+    // per point (a point's chain is linked as one group)
     for (int q = threadIdx.x; q < np; q += BLOCK) {
       const int a = M.s.pend[q];
       const unsigned long long tag = res_tag(rnd, a);
       const ActRec x = acts[a];
-      const int ready = for_keys(M, x, [&](bool pt, int id) { return (pt ? M.res_pt[id] : M.res_slot[id]) == tag; });
+      const int ready = for_keys(M, x, [&](int mode, int id) { return holds_key(M, mode, id, tag); });
       M.s.ready[q] = ready;
       if (!ready) continue;
       int partner = -1;
@@ -904,14 +946,9 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
       if (kind == 0) {
         atomicAdd(&cnt[2], 1);
       } else if (kind == 1) {
-        if (M.nobs[x.pid] <= 24) {
-          link(M, x.pid, x.slot, x.j, acc);
-          mark_dirty(M, x.pid);
-          M.found[x.pid] += 1;
-        } else {  // high degree: one warp shares the covisibility bumps
-          M.s.add_list[atomicAdd(&nadd_sh, 1)] = a;
-        }
-        atomicAdd(&cnt[1], 1);
+        const int d = atomicAdd(&ndef_sh, 1);
+        M.s.def[d] = a;
+        M.s.dnxt[d] = atomicExch(&M.grp_head[x.pid], ((unsigned long long)rnd << 32) | (unsigned)d);
       } else {
         const int at = atomicAdd(&nmerge_sh, 1);
         M.s.merge_a[at] = x.pid;
@@ -920,12 +957,34 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
     }
     __syncthreads();
     if (tm && threadIdx.x == 0) {
+      tm[9] += gtime() - tt;
+      tt = gtime();
+    }
+    // chain heads: single low-degree ADDs link here (thread), the rest go to warps
+    const int nd = ndef_sh;
+    for (int d = threadIdx.x; d < nd; d += BLOCK) {
+      const int a = M.s.def[d];
+      const ActRec x = acts[a];
+      if (M.grp_head[x.pid] != (((unsigned long long)rnd << 32) | (unsigned)d)) continue;
+      const bool single = (unsigned)(M.s.dnxt[d] >> 32) != rnd;
+      if (single && M.nobs[x.pid] <= 24) {
+        link(M, x.pid, x.slot, x.j, acc);
+        mark_dirty(M, x.pid);
+        M.found[x.pid] += 1;
+        atomicAdd(&cnt[1], 1);
+      } else if (single) {
+        M.s.add_list[atomicAdd(&nadd_sh, 1)] = a;
+      } else {
+        M.s.grp_list[atomicAdd(&ngrp_sh, 1)] = d;
+      }
+    }
+    __syncthreads();
+    if (tm && threadIdx.x == 0) {
       tm[10] += gtime() - tt;
       tt = gtime();
     }
     {
-      const int nm = nmerge_sh, na = nadd_sh;
-      const int lane = threadIdx.x & 31;
+      const int nm = nmerge_sh, na = nadd_sh, ng = ngrp_sh;
       for (int k = threadIdx.x >> 5; k < na; k += BLOCK / 32) {
         const ActRec x = acts[M.s.add_list[k]];
         link_warp(M, x.pid, x.slot, x.j, lane, acc);
@@ -934,8 +993,14 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
           M.found[x.pid] += 1;
         }
       }
+      for (int k = threadIdx.x >> 5; k < ng; k += BLOCK / 32) {
+        const int d = M.s.grp_list[k];
+        const int got = group_link_warp(M, acts[M.s.def[d]].pid, d, rnd, acts, M.s.def, M.s.dnxt, lane, acc);
+        if (lane == 0) atomicAdd(&cnt[1], got);
+      }
       for (int k = threadIdx.x >> 5; k < nm; k += BLOCK / 32) merge_pair_warp(M, M.s.merge_a[k], M.s.merge_b[k], lane, acc);
       if (threadIdx.x == 0) cnt[0] += nm;
+      if (threadIdx.x == 32) atomicAdd(&cnt[1], na);
     }
     __syncthreads();
     if (tm && threadIdx.x == 0) {

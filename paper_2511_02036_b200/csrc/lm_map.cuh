@@ -34,6 +34,7 @@ constexpr int REFRESH_MAXN = 512;       // observations handled by the rep-refre
 constexpr int MATCH_TILE = 32;          // current keypoints per match CTA (one per lane)
 constexpr int MATCH_WARPS = 8;          // warps per match CTA, each scanning a slice of j
 constexpr int MATCH_JT = 1024;          // neighbour descriptors staged per smem chunk
+constexpr int RES_PAIR = 1 << 16;       // hashed (point, keyframe) reservation keys per map
 
 enum KfState { KF_FREE = 0, KF_STAGED = 1, KF_LIVE = 2, KF_DEAD = 3 };
 enum Scal { SC_NEXT_ID = 0, SC_OBS_HEAD, SC_RECENT_N, SC_ERR, SC_DIRTY_N, SC_ROUND, SC_N = 8 };
@@ -100,6 +101,9 @@ struct Scratch {
   int* fctl;             // [8] fusion control: targets, forward points, ...
   int* pass_j;           // [kpkf_max] per-pass resolved hit per target keypoint
   int* add_list;         // [act_cap] high-degree ADDs committed warp-cooperatively
+  int* def;              // [act_cap] ready ADDs of this round (grouped per point)
+  unsigned long long* dnxt;  // [act_cap] per-point chain of ready ADDs: (round << 32 | def index)
+  int* grp_list;         // [act_cap] multi-ADD groups committed warp-cooperatively (def index)
   int* act_flag;         // [TMAX*kpkf_max]
   int* vis_flag;         // [TMAX*kpkf_max]
   int pts_cap;
@@ -159,6 +163,9 @@ struct DevMap {
   // deterministic-reservation tables (apply): round-tagged min action index per entity
   unsigned long long* res_pt;    // [mp_cap]
   unsigned long long* res_slot;  // [kp_cap]
+  unsigned long long* res_ex;    // [mp_cap] min tag of the actions that need the point exclusively
+  unsigned long long* res_pair;  // [RES_PAIR] (point, keyframe) ADD keys, hashed (collisions only serialise)
+  unsigned long long* grp_head;  // [mp_cap] head of the point's ready-ADD chain, (round << 32 | def index)
   // covisibility
   int* covis;
   // probation list (culling.RecentPoint)
@@ -403,6 +410,94 @@ __device__ void link_warp(const DevMap& M, int mp, int slot, int kp, int lane, P
     }
   }
   __syncwarp();
+}
+
+// grow mp's list to hold `need` entries (lane-parallel copy); false when the pool is exhausted
+__device__ bool obs_reserve_warp(const DevMap& M, int mp, int need, int lane) {
+  int off = M.ooff[mp], cap = M.ocap[mp];
+  if (need <= cap) return true;
+  if (lane == 0) {
+    int nc = cap < 4 ? 4 : cap;
+    while (nc < need) nc *= 2;
+    off = atomicAdd(&M.scal[SC_OBS_HEAD], nc);
+    if (off + nc > M.obs_cap) {
+      set_err(M, LM_ERR_CAPACITY);
+      off = -1;
+    }
+    cap = nc;
+  }
+  off = __shfl_sync(0xffffffffu, off, 0);
+  cap = __shfl_sync(0xffffffffu, cap, 0);
+  if (off < 0) return false;
+  const int2* src = M.obs + M.ooff[mp];
+  const int n = M.nobs[mp];
+  for (int k = lane; k < n; k += 32) M.obs[off + k] = src[k];
+  __syncwarp();
+  if (lane == 0) {
+    M.ooff[mp] = off;
+    M.ocap[mp] = cap;
+  }
+  __syncwarp();
+  return true;
+}
+
+// A group of ADDs of one point committed in the same apply round (pairwise distinct
+// keyframes, none observed yet). Linking them in any order gives the same observation set,
+// counters and covisibility deltas (+1 for every new x old and new x new pair), so a warp
+// links them in chunks of 32: chunk members against the current list, pairs inside the
+// chunk, then an append. Members are chained through dnxt[q] = (round << 32 | q'), q
+// indexing def[] (action indices into acts). Returns the number linked.
+__device__ int group_link_warp(const DevMap& M, int mp, int q_head, unsigned rnd, const ActRec* acts,
+                               const int* def, const unsigned long long* dnxt, int lane, PairAcc* acc) {
+  int q = q_head, total = 0;
+  while (q >= 0) {
+    int my = -1, c = 0;
+    for (; c < 32 && q >= 0; ++c) {  // uniform walk (broadcast loads)
+      if (lane == c) my = q;
+      const unsigned long long v = dnxt[q];
+      q = (unsigned)(v >> 32) == rnd ? (int)(v & 0xffffffffu) : -1;
+    }
+    int slot = 0, kp = 0;
+    if (my >= 0) {
+      const ActRec x = acts[def[my]];
+      slot = x.slot;
+      kp = x.j;
+    }
+    const int n = M.nobs[mp];
+    const int2* o = M.obs + M.ooff[mp];
+    for (int b = 0; b < c * n; b += 32) {  // new x current observers
+      const int t = b + lane;
+      const int i = t / n < c ? t / n : c - 1;
+      const int si = __shfl_sync(0xffffffffu, slot, i);
+      if (t < c * n) covis_add(M, si, o[t - i * n].x, +1, acc);
+    }
+    for (int b = 0; b < c * c; b += 32) {  // new x new (each unordered pair once)
+      const int t = b + lane;
+      const int i = t / c < c ? t / c : c - 1, i2 = t - (t / c) * c;
+      const int si = __shfl_sync(0xffffffffu, slot, i);
+      const int si2 = __shfl_sync(0xffffffffu, slot, i2);
+      if (t < c * c && i < i2) covis_add(M, si, si2, +1, acc);
+    }
+    if (!obs_reserve_warp(M, mp, n + c, lane)) return total;
+    if (lane < c) {
+      M.obs[M.ooff[mp] + n + lane] = make_int2(slot, kp);
+      const int g = M.kp_off[slot] + kp;
+      M.kbind[g] = mp;
+      atomicAdd(&M.counts[(size_t)mp * M.L + M.klev[g]], 1);
+    }
+    __syncwarp();
+    if (lane == 0) M.nobs[mp] = n + c;
+    __syncwarp();
+    total += c;
+  }
+  if (lane == 0) {
+    M.found[mp] += total;
+    M.ver[mp] += 1;
+    M.gval[mp] = 0;
+    mark_dirty(M, mp);
+  }
+  __syncwarp();
+  return total;
 }
 
 // _unrecord_obs of list entry k: unbind, uncount, covis -1 with every remaining observer
