@@ -352,11 +352,15 @@ def main():
             "work_per_step": {"keyframes": len(ids), "match_pairs": per_step_pairs, "fuse_bytes": per_step_bytes,
                               "created": acc["created"] / args.steps, "merged": acc["merged"] / args.steps,
                               "observations_added": acc["observations_added"] / args.steps,
-                              "apply_rounds": acc["apply_rounds"] / args.steps},
+                              "apply_rounds": acc["apply_rounds"] / args.steps,
+                              "rev_passes": (acc["fuse_passes"] / args.steps) / 2,
+                              "rev_passes_acting": acc["rev_passes_acting"] / args.steps,
+                              "rev_passes_rescanned": acc["rev_passes_redo"] / args.steps,
+                              "rev_points_recomputed": acc["fuse_cycles"][1] / args.steps},
             "fuse_phase_ms_per_step": {n: acc["fuse_cycles"][k] / args.steps / 1e6
                                        for k, n in enumerate(["targets", "-", "fwd_assemble", "fwd_apply",
                                                               "rev_redo_refresh", "rev_redo_gather", "rev_apply",
-                                                              "rev_action_build", "rev_scan_reuse", "rev_apply_reserve_check",
+                                                              "rev_rescan", "rev_commit_invalidate", "rev_apply_reserve_check",
                                                               "rev_apply_commit", "rev_apply_merges",
                                                               "rev_apply_compaction", "fwd_apply_reserve_check",
                                                               "fwd_apply_commit_merges", "fwd_apply_compaction"])

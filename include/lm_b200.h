@@ -119,6 +119,8 @@ typedef struct lm_step_stats { /* CreationStats triangulation.py:49-60 + run_fus
                                 3 fwd apply, 4 rev refresh, 5 rev geometry, 6 rev apply,
                                 7 rev gather, 8 rev bound points, 9 apply reserve+check,
                                 10 apply commit (plain), 11 apply merges, 12 apply compaction */
+  int64_t rev_passes_acting;  /* reverse passes that produced at least one action */
+  int64_t rev_passes_redo;    /* reverse passes that recomputed at least one point */
 } lm_step_stats;
 
 typedef struct lm_candidate { /* MatchCandidate triangulation.py:41-46 */

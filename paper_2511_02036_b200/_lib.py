@@ -70,7 +70,8 @@ class StepStats(C.Structure):
                 ("merged", i32), ("observations_added", i32), ("stale", i32), ("culled", i32),
                 ("first_new_id", i64), ("error", i32), ("n_candidates", i32), ("match_pairs", i64),
                 ("fuse_bytes", i64), ("fuse_passes", i64), ("fuse_points", i64), ("fuse_actions", i64),
-                ("apply_rounds", i64), ("fuse_cycles", i64 * 16)]
+                ("apply_rounds", i64), ("fuse_cycles", i64 * 16),
+                ("rev_passes_acting", i64), ("rev_passes_redo", i64)]
 
 
 class Candidate(C.Structure):

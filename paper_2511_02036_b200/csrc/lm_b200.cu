@@ -534,7 +534,7 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(d.nobs, MP); A(d.ocap, MP); A(d.ooff, MP); A(d.obs, (size_t)d.obs_cap); A(d.counts, MP * d.L);
   A(d.dirty, MP); A(d.dirty_list, MP); A(d.res_pt, MP); A(d.res_slot, KP);
   A(d.res_ex, MP); A(d.res_pair, RES_PAIR); A(d.grp_head, MP);
-  A(d.gacc, 3 * MP); A(d.glo, MP); A(d.ghi, MP); A(d.gval, MP); A(d.ver, MP); A(d.hit, MP);
+  A(d.gacc, 3 * MP); A(d.glo, MP); A(d.ghi, MP); A(d.gval, MP); A(d.ver, MP); A(d.hit, MP); A(d.mrg, MP);
   A(d.covis, K * K);
   A(d.recent_id, MP); A(d.recent_born, MP);
   A(d.scal, SC_N); A(d.ledger, LG_N);
@@ -555,6 +555,10 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(s.blk_cnt, (size_t)s.act_cap / 256 + 2); A(s.blk_off, (size_t)s.act_cap / 256 + 2); A(s.fctl, 8);
   A(s.pass_j, d.kpkf_max); A(s.add_list, (size_t)s.act_cap);
   A(s.def, (size_t)s.act_cap); A(s.dnxt, (size_t)s.act_cap); A(s.grp_list, (size_t)s.act_cap);
+  A(s.pinfo, 3 * TMAX); A(s.hitpass, (size_t)d.kpkf_max * ((TMAX + 31) / 32)); A(s.pj, (size_t)s.act_cap);
+  A(s.pass_of, K); A(s.snap, d.kpkf_max); A(s.rmark, MP);
+  A(s.pmp, (size_t)s.act_cap); A(s.pob, (size_t)s.act_cap); A(s.itag, (size_t)s.act_cap); A(s.ilist, (size_t)s.act_cap);
+  A(s.cands, (size_t)s.act_cap); A(s.hl_cnt, d.kpkf_max); A(s.hl, (size_t)d.kpkf_max * HL); A(s.hreg, MP);
   A(m->d_stats, 1); A(m->d_totals, 1); A(m->d_result, 4 + 1024 + TMAX);
 #undef A
   s.stats = m->d_stats;
@@ -563,7 +567,13 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   CU(cudaMemsetAsync(d.res_ex, 0xff, sizeof(unsigned long long) * MP, ctx->stream));
   CU(cudaMemsetAsync(d.res_pair, 0xff, sizeof(unsigned long long) * RES_PAIR, ctx->stream));
   CU(cudaMemsetAsync(d.grp_head, 0, sizeof(unsigned long long) * MP, ctx->stream));
+  CU(cudaMemsetAsync(d.s.rmark, 0, sizeof(int) * MP, ctx->stream));
+  CU(cudaMemsetAsync(d.s.itag, 0, sizeof(int) * d.s.act_cap, ctx->stream));
+  CU(cudaMemsetAsync(d.mrg, 0, sizeof(int2) * MP, ctx->stream));
+  CU(cudaMemsetAsync(d.s.hreg, 0, sizeof(int) * MP, ctx->stream));
   CU(cudaMemsetAsync(d.hit, 0xff, sizeof(int2) * MP, ctx->stream));
+  CU(cudaMemsetAsync(s.pass_of, 0xff, sizeof(int) * K, ctx->stream));
+  CU(cudaMemsetAsync(s.hitpass, 0, sizeof(unsigned) * d.kpkf_max * ((TMAX + 31) / 32), ctx->stream));
   m->state.assign(K, KF_FREE);
   m->kp_n.assign(K, 0);
   m->kp_off.assign(K, 0);
@@ -597,6 +607,10 @@ int lm_map_reset(lm_ctx* ctx, int32_t map) {
   CU(cudaMemsetAsync(d.res_ex, 0xff, sizeof(unsigned long long) * MP, ctx->stream));
   CU(cudaMemsetAsync(d.res_pair, 0xff, sizeof(unsigned long long) * RES_PAIR, ctx->stream));
   CU(cudaMemsetAsync(d.grp_head, 0, sizeof(unsigned long long) * MP, ctx->stream));
+  CU(cudaMemsetAsync(d.s.rmark, 0, sizeof(int) * MP, ctx->stream));
+  CU(cudaMemsetAsync(d.s.itag, 0, sizeof(int) * d.s.act_cap, ctx->stream));
+  CU(cudaMemsetAsync(d.mrg, 0, sizeof(int2) * MP, ctx->stream));
+  CU(cudaMemsetAsync(d.s.hreg, 0, sizeof(int) * MP, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   m->slot_of.clear();
   std::fill(m->state.begin(), m->state.end(), KF_FREE);
@@ -734,6 +748,8 @@ __global__ void k_end(DevMap* maps, const StepArgs* args, lm_step_stats** totals
   t->fuse_actions += st->fuse_actions;
   t->apply_rounds += st->apply_rounds;
   for (int k = 0; k < 16; ++k) t->fuse_cycles[k] += st->fuse_cycles[k];
+  t->rev_passes_acting += st->rev_passes_acting;
+  t->rev_passes_redo += st->rev_passes_redo;
   t->first_new_id += 1;  // steps accumulated
 }
 
@@ -809,10 +825,11 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   if ((rc = mark())) return rc;
   k_fuse_spec<<<dim3((kpkf + 255) / 256, tfuse, n), 256, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;
-  k_fuse_rev<<<n, 1024, rev_smem, ctx->stream>>>(dmaps, dv, rev_smem);
+  k_fuse_rev<<<n, REV_THREADS, rev_smem, ctx->stream>>>(dmaps, dv, rev_smem);
+  k_fuse_visible<<<dim3((kpkf + 255) / 256, tfuse, n), 256, 0, ctx->stream>>>(dmaps, dv);
   k_end<<<n, 32, 0, ctx->stream>>>(dmaps, dv, ctx->d_totals);
   if ((rc = mark())) return rc;
-  ctx->launches += 16;
+  ctx->launches += 17;
   if (ctx->prof) ctx->prof_steps.push_back(evs);
   CHECK_LAUNCH();
   CU(cudaEventRecord(ctx->args_ev[e], ctx->stream));
@@ -1427,6 +1444,10 @@ int lm_map_rewind(lm_ctx* ctx, int32_t map) {
   CU(cudaMemsetAsync(d.res_ex, 0xff, sizeof(unsigned long long) * MP, st));
   CU(cudaMemsetAsync(d.res_pair, 0xff, sizeof(unsigned long long) * RES_PAIR, st));
   CU(cudaMemsetAsync(d.grp_head, 0, sizeof(unsigned long long) * MP, st));
+  CU(cudaMemsetAsync(d.s.rmark, 0, sizeof(int) * MP, st));
+  CU(cudaMemsetAsync(d.s.itag, 0, sizeof(int) * d.s.act_cap, st));
+  CU(cudaMemsetAsync(d.mrg, 0, sizeof(int2) * MP, st));
+  CU(cudaMemsetAsync(d.s.hreg, 0, sizeof(int) * MP, st));
   if (m->kp_head) CU(cudaMemsetAsync(d.kbind, 0xff, sizeof(int) * m->kp_head, st));
   if (m->n_slots) {
     k_rewind_state<<<(m->n_slots + 255) / 256, 256, 0, st>>>(d, m->n_slots);

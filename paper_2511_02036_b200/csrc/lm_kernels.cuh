@@ -1372,11 +1372,44 @@ __global__ void __launch_bounds__(1024) k_fuse_apply(DevMap* maps, const StepArg
   }
 }
 
-// warp per point touched since the last refresh: representative descriptor + geometry cache
+// ---------------------------------------------------------------------- reverse passes
+// Reference: for t in targets: gather(bound_points_of(t) -> current) then apply
+// (fusion.py:337-346) -- each pass sees every earlier pass's mutations. Only a few passes
+// produce actions (C2: ~6 of ~75), and a pass without actions changes nothing but visible
+// counters, so passes are evaluated speculatively, item by item ((pass, keypoint)):
+//   k_fuse_spec    evaluates every item against the post-forward map (thread per item):
+//                  the bound point, its hit into the current keyframe, its action, and per
+//                  current keypoint j the bitmap of passes hitting j.
+//   k_fuse_rev     (one CTA per map) walks to the first pass with actions, applies it, and
+//                  re-evaluates exactly the later items whose inputs that apply touched,
+//                  updating the per-pass totals by deltas; repeats until no pass acts.
+//   k_fuse_visible commits every pass's visible counters (thread per item).
+// An item's inputs are the binding of its keypoint, that point's state (version), and the
+// binding of the current keypoint it hits. An apply changes the state of the points of its
+// actions and of their slot owners (the "touched" points); the bindings that change are
+// the touched points' slots before or after the apply (touched items) and current
+// keypoints (found by comparing with a snapshot; items hitting them are found through the
+// pass bitmap). Visible bumps are deferred: a bump of a point that a later merge kills is
+// the same as a bump of its winner after the merge (the merge sums the counters), so
+// k_fuse_visible follows the loser -> winner records of this step (mrg, SC_MTAG).
+
+constexpr int HPW = (TMAX + 31) / 32;  // words of the per-current-keypoint pass bitmap
+constexpr int REV_THREADS = 1024;      // k_fuse_rev block
+enum PassInfo { PI_NACT = 0, PI_LIVE = 1, PI_OBS = 2, PI_N = 3 };
+
+// warp per point touched since the last refresh: representative descriptor + geometry cache;
+// also clears the reverse-pass bookkeeping for k_fuse_spec
 __global__ void __launch_bounds__(256) k_fuse_refresh(DevMap* maps, const StepArgs* args) {
   const StepArgs& A = args[blockIdx.y];
   const DevMap& M = maps[A.map];
   if (!A.do_fuse) return;
+  {
+    const int tid = blockIdx.x * 256 + threadIdx.x, nth = gridDim.x * 256;
+    for (int k = tid; k < PI_N * TMAX; k += nth) M.s.pinfo[k] = 0;
+    for (int k = tid; k < M.kpkf_max * HPW; k += nth) M.s.hitpass[k] = 0u;
+    for (int k = tid; k < M.kpkf_max; k += nth) M.s.hl_cnt[k] = 0;
+    if (tid == 0) M.scal[SC_MTAG] += 1;  // merges of this step's reverse phase
+  }
   const int n = M.scal[SC_DIRTY_N];
   const int lane = threadIdx.x & 31;
   for (int k = blockIdx.x * 8 + (threadIdx.x >> 5); k < n; k += gridDim.x * 8) {
@@ -1393,8 +1426,45 @@ __global__ void __launch_bounds__(256) k_fuse_refresh(DevMap* maps, const StepAr
   }
 }
 
-// speculative reverse gather: every (target, bound point) against the current keyframe,
-// on the map state after the forward apply. Thread per (target, keypoint).
+// register point mp under its hit j in the per-keypoint hit list
+__device__ __forceinline__ void hit_list_add(const DevMap& M, int j, int mp) {
+  if (j < 0) return;
+  const int at = atomicAdd(&M.s.hl_cnt[j], 1);
+  if (at < HL) M.s.hl[j * HL + at] = mp;
+}
+
+struct ItemVal {
+  int mp, j, nob, has;
+  ActRec a;
+};
+
+// evaluate item (pass t, keypoint kp of target ts) on the current state; the bound point's
+// cached hit must be current. Records the hit bit of the pass.
+__device__ __forceinline__ ItemVal eval_item(const DevMap& M, int cur, int t, int ts, int kp) {
+  ItemVal v{-1, -3, 0, 0, ActRec{0, 0, 0, 0, 0}};
+  const int mp = M.kbind[M.kp_off[ts] + kp];
+  if (mp >= 0 && M.alive[mp]) {
+    v.mp = mp;
+    v.nob = M.nobs[mp];
+    v.j = M.hit[mp].y;
+    if (v.j >= 0) {
+      atomicOr(&M.s.hitpass[v.j * HPW + (t >> 5)], 1u << (t & 31));
+      v.has = build_action(M, mp, cur, v.j, &v.a);
+    }
+  }
+  return v;
+}
+
+__device__ __forceinline__ void store_item(const DevMap& M, size_t it, const ItemVal& v) {
+  M.s.pj[it] = v.j;
+  M.s.pmp[it] = v.mp;
+  M.s.pob[it] = v.nob;
+  ActRec a = v.a;
+  if (!v.has) a.kind = 0;
+  M.s.acts2[it] = a;
+}
+
+// speculative evaluation of every reverse-pass item on the post-forward map
 __global__ void __launch_bounds__(256) k_fuse_spec(DevMap* maps, const StepArgs* args) {
   const StepArgs& A = args[blockIdx.z];
   const DevMap& M = maps[A.map];
@@ -1403,22 +1473,41 @@ __global__ void __launch_bounds__(256) k_fuse_spec(DevMap* maps, const StepArgs*
   if (t >= M.s.fctl[FC_T]) return;
   const int ts = M.s.targets[t];
   const int n = M.kp_n[ts];
+  if ((int)blockIdx.x * 256 >= n) return;
   const int kp = blockIdx.x * 256 + threadIdx.x;
-  if (kp >= n) return;
-  const int mp = M.kbind[M.kp_off[ts] + kp];
-  if (mp < 0 || !M.alive[mp]) return;
-  // the projection target is always the current keyframe, so the result is per point;
-  // a point bound in several targets is gathered by each of them (identical values)
-  PGeo g;
-  point_geometry(M, mp, A.fc.dist_band_slack, g);  // caches valid or rebuilt (benign same-value race)
-  const int j = gather_hit(M, A.fc, g, A.cur, tgt_global(M, A.cur));
-  M.hit[mp] = make_int2(M.ver[mp], j);
+  int live = 0, nob = 0, has = 0;
+  if (kp < n) {
+    const int mp = M.kbind[M.kp_off[ts] + kp];
+    if (mp >= 0 && M.alive[mp]) {
+      // the projection target is always the current keyframe, so the hit is per point; a
+      // point bound in several targets is gathered by each of them (identical values)
+      PGeo g;
+      point_geometry(M, mp, A.fc.dist_band_slack, g);  // caches valid or rebuilt (benign same-value race)
+      const int j = gather_hit(M, A.fc, g, A.cur, tgt_global(M, A.cur));
+      M.hit[mp] = make_int2(M.ver[mp], j);
+      const int stag = M.scal[SC_MTAG];
+      if (j >= 0 && atomicExch(&M.s.hreg[mp], stag) != stag) hit_list_add(M, j, mp);
+    }
+    const ItemVal v = eval_item(M, A.cur, t, ts, kp);
+    store_item(M, (size_t)t * M.kpkf_max + kp, v);
+    live = v.mp >= 0;
+    nob = v.nob;
+    has = v.has;
+  }
+  for (int off = 16; off; off >>= 1) {
+    live += __shfl_xor_sync(0xffffffffu, live, off);
+    nob += __shfl_xor_sync(0xffffffffu, nob, off);
+    has += __shfl_xor_sync(0xffffffffu, has, off);
+  }
+  if ((threadIdx.x & 31) == 0 && live) {
+    atomicAdd(&M.s.pinfo[PI_LIVE * TMAX + t], live);
+    atomicAdd(&M.s.pinfo[PI_OBS * TMAX + t], nob);
+    if (has) atomicAdd(&M.s.pinfo[PI_NACT * TMAX + t], has);
+  }
 }
 
-// reverse passes: each target's bound points into the current keyframe, gather -> apply.
-// Pass t reuses the speculative hit of every point whose version is unchanged and
-// recomputes (refresh + geometry + window search) only the points earlier passes modified.
-__global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs* args, int smem_bytes) {
+// reverse passes (fusion.py:337-346), one CTA per map; see the block comment above
+__global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const StepArgs* args, int smem_bytes) {
   const StepArgs& A = args[blockIdx.x];
   const DevMap& M = maps[A.map];
   if (!A.do_fuse) return;
@@ -1437,15 +1526,15 @@ __global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs*
       int* scs = (int*)(sv + n);
       int* sit = scs + nc + 1;
       unsigned char* sl = (unsigned char*)(sit + n);
-      for (int k = threadIdx.x; k < 2 * n; k += 1024) sd[k] = M.kdesc[2 * (size_t)off + k];
-      for (int k = threadIdx.x; k < n; k += 1024) {
+      for (int k = threadIdx.x; k < 2 * n; k += REV_THREADS) sd[k] = M.kdesc[2 * (size_t)off + k];
+      for (int k = threadIdx.x; k < n; k += REV_THREADS) {
         su[k] = M.ku[off + k];
         sv[k] = M.kv[off + k];
         sit[k] = M.cell_items[off + k];
         sl[k] = M.klev[off + k];
       }
       const int* gcs = M.cell_start + (size_t)A.cur * (GRID_CELLS + 1);
-      for (int k = threadIdx.x; k <= nc; k += 1024) scs[k] = gcs[k];
+      for (int k = threadIdx.x; k <= nc; k += REV_THREADS) scs[k] = gcs[k];
       TV = TgtView{su, sv, sl, sd, scs, sit};
     }
   }
@@ -1453,104 +1542,178 @@ __global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs*
   __shared__ int cnt[3];
   __shared__ long long tm[16];
   __shared__ PairAcc acc;
+  __shared__ int s_nact[TMAX], s_live[TMAX], s_obs[TMAX];
+  __shared__ int t1_sh, nc_sh, ni_sh, tag_sh;
+  const int K = M.kpkf_max;
+  const int cur = A.cur;
+  const int ncur = M.kp_n[cur], cur_off = M.kp_off[cur];
+  const lm_fuse_cfg& fc = A.fc;
   if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
   if (threadIdx.x < 16) tm[threadIdx.x] = 0;
   if (threadIdx.x == 0) M.scal[SC_DIRTY_N] = 0;  // k_fuse_refresh consumed the list
-  pair_acc_init<1024>(&acc, A.cur);
-  const lm_fuse_cfg& fc = A.fc;
-  const int cur = A.cur;
+  for (int t = threadIdx.x; t < T; t += REV_THREADS) {
+    s_nact[t] = M.s.pinfo[PI_NACT * TMAX + t];
+    s_live[t] = M.s.pinfo[PI_LIVE * TMAX + t];
+    s_obs[t] = M.s.pinfo[PI_OBS * TMAX + t];
+    M.s.pass_of[M.s.targets[t]] = t;
+  }
+  pair_acc_init<REV_THREADS>(&acc, A.cur);  // (barrier)
   const unsigned long long mpb = M.mp_rec_bytes;
   long long alg = 0, npts = 0, nacts = 0;
-  int rounds = 0;
-  for (int t = 0; t < T; ++t) {
-    const int ts = M.s.targets[t];
-    const int n = M.kp_n[ts], off = M.kp_off[ts];
-    const long long t0 = gtime();
-    // (1) live bound points in keypoint order; reuse or schedule a recompute
-    int nredo = 0, live_n = 0, obs_n = 0;
-    for (int b0 = 0; b0 < n; b0 += 1024) {
-      const int kp = b0 + threadIdx.x;
-      int redo = 0;
-      if (kp < n) {
-        const int mp = M.kbind[off + kp];
-        int j = -3;  // -3: not a live bound point
-        if (mp >= 0 && M.alive[mp]) {
-          ++live_n;
-          obs_n += M.nobs[mp];
-          const int2 h = M.hit[mp];
-          if (h.x == M.ver[mp]) j = h.y;
-          else redo = 1;
-        }
-        M.s.pass_j[kp] = j;
-      }
-      int tot;
-      const int at = block_excl_scan<1024>(redo, sh, tot);
-      if (redo) M.s.pts[nredo + at] = kp;
-      nredo += tot;
-    }
-    const int Pt = block_sum<1024>(live_n, sh);
-    const long long ob = block_sum<1024>(obs_n, sh);
+  int rounds = 0, pass_act = 0, reeval = 0, redo_pts = 0;
+  int t0 = 0;
+  // append item (t, kp) to the re-evaluation list once per tag
+  auto add_item = [&](int t, int kp, int tag) {
+    const size_t it = (size_t)t * K + kp;
+    if (atomicExch(&M.s.itag[it], tag) != tag) M.s.ilist[atomicAdd(&ni_sh, 1)] = (int)it;
+  };
+  while (true) {
+    // (1) first pass (>= t0) with actions; ledger / byte accounting of the passes before it
+    if (threadIdx.x == 0) t1_sh = T;
+    __syncthreads();
+    for (int t = t0 + threadIdx.x; t < T; t += REV_THREADS)
+      if (s_nact[t] > 0) atomicMin(&t1_sh, t);
+    __syncthreads();
+    const int t1 = t1_sh;
     if (threadIdx.x == 0) {
-      tm[8] += gtime() - t0;
-      M.ledger[LG_NAIVE] += Pt * mpb;
-      M.ledger[LG_PERSIST] += Pt * mpb;
-      M.ledger[LG_SMALL_FUSE] += Pt * mpb;
-      M.ledger[LG_SMALL_EVENTS] += 1;
-      tm[13] += nredo;
-    }
-    // (2) recompute the modified points: refresh (warp), geometry + window search (thread)
-    if (nredo) {
-      const long long t1 = gtime();
-      for (int k = threadIdx.x; k < nredo; k += 1024) M.s.pend[k] = M.kbind[off + M.s.pts[k]];
-      __syncthreads();
-      refresh_points<1024>(M, M.s.pend, nredo, sh);
-      const long long t2 = gtime();
-      for (int k = threadIdx.x; k < nredo; k += 1024) {
-        const int mp = M.s.pend[k];
-        PGeo g;
-        point_geometry(M, mp, fc.dist_band_slack, g);
-        const int j = gather_hit(M, fc, g, cur, TV);
-        M.s.pass_j[M.s.pts[k]] = j;
-        M.hit[mp] = make_int2(M.ver[mp], j);  // later passes reuse it until the point changes
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        tm[0] += t2 - t1;
-        tm[1] += gtime() - t2;
+      const int te = t1 < T ? t1 : T - 1;
+      for (int t = t0; t <= te; ++t) {
+        const int Pt = s_live[t];
+        M.ledger[LG_NAIVE] += Pt * mpb;
+        M.ledger[LG_PERSIST] += Pt * mpb;
+        M.ledger[LG_SMALL_FUSE] += Pt * mpb;
+        M.ledger[LG_SMALL_EVENTS] += 1;
+        alg += pass_bytes(Pt, s_obs[t], ncur, s_nact[t]);
+        npts += Pt;
+        nacts += s_nact[t];
       }
     }
-    // (3) visibility + action build in keypoint order
-    const long long t3 = gtime();
+    if (t1 >= T) break;
+    ++pass_act;
+    // (2) pass t1's actions in keypoint order; current-keyframe snapshot; touched points
+    //     (action points + current owners of the hit keypoints) and their items before
+    const long long ta = gtime();
+    if (threadIdx.x == 0) {
+      nc_sh = 0;
+      ni_sh = 0;
+      tag_sh = atomicAdd(&M.scal[SC_ROUND], 1) + 1;
+    }
     int na = 0;
-    for (int b0 = 0; b0 < n; b0 += 1024) {
+    const int n1 = M.kp_n[M.s.targets[t1]];
+    for (int b0 = 0; b0 < n1; b0 += REV_THREADS) {
       const int kp = b0 + threadIdx.x;
-      ActRec a;
-      int has = 0;
-      if (kp < n) {
-        const int j = M.s.pass_j[kp];
-        if (j >= -1) {
-          const int mp = M.kbind[off + kp];
-          atomicAdd(&M.visible[mp], 1);
-          has = build_action(M, mp, cur, j, &a);
-        }
-      }
+      ActRec x{0, 0, 0, 0, 0};
+      if (kp < n1) x = M.s.acts2[(size_t)t1 * K + kp];
+      const int has = kp < n1 && x.kind != 0;
       int tot;
-      const int at = block_excl_scan<1024>(has, sh, tot);
-      if (has) M.s.acts[na + at] = a;
+      const int at = block_excl_scan<REV_THREADS>(has, sh, tot);  // (barriers)
+      if (has) M.s.acts[na + at] = ActRec{cur, x.pid, x.j, x.other, x.kind};
       na += tot;
     }
+    for (int k = threadIdx.x; k < ncur; k += REV_THREADS) M.s.snap[k] = M.kbind[cur_off + k];
     __syncthreads();
-    alg += pass_bytes(Pt, ob, M.kp_n[cur], na);
-    npts += Pt;
-    nacts += na;
-    const long long t4 = gtime();
-    rounds += apply_block<1024>(M, M.s.acts, na, cnt, sh, &acc, tm);
-    if (threadIdx.x == 0) {
-      tm[3] += t4 - t3;
-      tm[2] += gtime() - t4;
+    const int tag = tag_sh;
+    for (int k = threadIdx.x; k < na; k += REV_THREADS) {
+      const ActRec x = M.s.acts[k];
+      const int cand[3] = {x.pid, x.other, M.s.snap[x.j]};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int p = cand[c];
+        if (p < 0 || atomicExch(&M.s.rmark[p], tag) == tag) continue;
+        M.s.cands[atomicAdd(&nc_sh, 1)] = p;
+        const int2* o = M.obs + M.ooff[p];
+        const int no = M.nobs[p];
+        for (int e = 0; e < no; ++e) {
+          const int tt = M.s.pass_of[o[e].x];
+          if (tt > t1) add_item(tt, o[e].y, tag);
+        }
+      }
     }
+    __syncthreads();
+    rounds += apply_block<REV_THREADS>(M, M.s.acts, na, cnt, sh, &acc, tm);  // (barriers)
+    if (threadIdx.x == 0) tm[2] += gtime() - ta;
+    // (3) touched points: refresh + new hits; their items after the apply; items hitting a
+    //     current keypoint whose binding changed
+    const long long tv = gtime();
+    const int ncand = nc_sh;
+    redo_pts += ncand;
+    refresh_points<REV_THREADS>(M, M.s.cands, ncand, sh);  // (barriers)
+    const long long t6 = gtime();
+    for (int k = threadIdx.x; k < ncand; k += REV_THREADS) {
+      const int p = M.s.cands[k];
+      if (!M.alive[p]) continue;
+      PGeo g;
+      point_geometry(M, p, fc.dist_band_slack, g);
+      const int j = gather_hit(M, fc, g, cur, TV);
+      M.hit[p] = make_int2(M.ver[p], j);
+      hit_list_add(M, j, p);
+      const int2* o = M.obs + M.ooff[p];
+      const int no = M.nobs[p];
+      for (int e = 0; e < no; ++e) {
+        const int tt = M.s.pass_of[o[e].x];
+        if (tt > t1) add_item(tt, o[e].y, tag);
+      }
+    }
+    if (threadIdx.x == 0) {
+      tm[0] += t6 - tv;
+      tm[1] += gtime() - t6;
+    }
+    // items of the points hitting a current keypoint whose binding changed (hit list; a
+    // keypoint whose list overflowed falls back to scanning the passes of its bitmap)
+    {
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+      for (int k = wid; k < ncur; k += REV_THREADS / 32) {
+        if (M.kbind[cur_off + k] == M.s.snap[k]) continue;
+        const int c = M.s.hl_cnt[k];
+        if (c <= HL) {
+          for (int q = lane; q < c; q += 32) {
+            const int p = M.s.hl[k * HL + q];
+            if (!M.alive[p] || M.hit[p].y != k) continue;
+            const int2* o = M.obs + M.ooff[p];
+            const int no = M.nobs[p];
+            for (int e = 0; e < no; ++e) {
+              const int tt = M.s.pass_of[o[e].x];
+              if (tt > t1) add_item(tt, o[e].y, tag);
+            }
+          }
+          continue;
+        }
+        for (int w = 0; w < HPW; ++w) {
+          unsigned bits = M.s.hitpass[k * HPW + w];
+          while (bits) {
+            const int tt = 32 * w + __ffs(bits) - 1;
+            bits &= bits - 1;
+            if (tt <= t1 || tt >= T) continue;
+            const int n = M.kp_n[M.s.targets[tt]];
+            const int* pjt = M.s.pj + (size_t)tt * K;
+            for (int kp = lane; kp < n; kp += 32)
+              if (pjt[kp] == k) add_item(tt, kp, tag);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // (4) re-evaluate the listed items; pass totals by deltas
+    const long long t7 = gtime();
+    const int ni = ni_sh;
+    reeval += ni;
+    for (int q = threadIdx.x; q < ni; q += REV_THREADS) {
+      const int it = M.s.ilist[q];
+      const int t = it / K, kp = it - t * K;
+      const int oj = M.s.pj[it], ob = M.s.pob[it], oa = M.s.acts2[it].kind != 0;
+      const ItemVal v = eval_item(M, cur, t, M.s.targets[t], kp);
+      store_item(M, it, v);
+      const int dl = (v.mp >= 0) - (oj != -3), dob = v.nob - ob, da = v.has - oa;
+      if (dl) atomicAdd(&s_live[t], dl);
+      if (dob) atomicAdd(&s_obs[t], dob);
+      if (da) atomicAdd(&s_nact[t], da);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) tm[3] += gtime() - t7;
+    t0 = t1 + 1;
   }
-  pair_acc_flush<1024>(M, &acc);
+  pair_acc_flush<REV_THREADS>(M, &acc);
+  for (int t = threadIdx.x; t < T; t += REV_THREADS) M.s.pass_of[M.s.targets[t]] = -1;
   if (threadIdx.x == 0) {
     lm_step_stats* st = M.s.stats;
     st->merged += cnt[0];
@@ -1566,8 +1729,33 @@ __global__ void __launch_bounds__(1024) k_fuse_rev(DevMap* maps, const StepArgs*
     st->fuse_cycles[6] += tm[2];
     st->fuse_cycles[7] += tm[3];
     for (int k = 8; k < 13; ++k) st->fuse_cycles[k] += tm[k];
-    st->fuse_cycles[1] += tm[13];  // recomputed (point, pass) pairs (count, not ns)
+    st->fuse_cycles[1] += redo_pts;  // touched points recomputed (count, not ns)
+    st->rev_passes_acting += pass_act;
+    st->rev_passes_redo += reeval;   // re-evaluated items (count)
   }
+}
+
+// deferred visible counters of every reverse pass (thread per item); a point merged away
+// later in this step's reverse phase passes its bump on to its winner
+__global__ void __launch_bounds__(256) k_fuse_visible(DevMap* maps, const StepArgs* args) {
+  const StepArgs& A = args[blockIdx.z];
+  const DevMap& M = maps[A.map];
+  if (!A.do_fuse) return;
+  const int t = blockIdx.y;
+  if (t >= M.s.fctl[FC_T]) return;
+  const int n = M.kp_n[M.s.targets[t]];
+  const int kp = blockIdx.x * 256 + threadIdx.x;
+  if (kp >= n) return;
+  const size_t it = (size_t)t * M.kpkf_max + kp;
+  if (M.s.pj[it] < -1) return;
+  int p = M.s.pmp[it];
+  const int tag = M.scal[SC_MTAG];
+  for (int hop = 0; hop < 1 << 20 && !M.alive[p]; ++hop) {
+    const int2 m = M.mrg[p];
+    if (m.x != tag) break;
+    p = m.y;
+  }
+  atomicAdd(&M.visible[p], 1);
 }
 
 }  // namespace lm

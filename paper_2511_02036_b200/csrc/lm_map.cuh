@@ -35,9 +35,10 @@ constexpr int MATCH_TILE = 32;          // current keypoints per match CTA (one 
 constexpr int MATCH_WARPS = 8;          // warps per match CTA, each scanning a slice of j
 constexpr int MATCH_JT = 1024;          // neighbour descriptors staged per smem chunk
 constexpr int RES_PAIR = 1 << 16;       // hashed (point, keyframe) reservation keys per map
+constexpr int HL = 16;                  // hit-list entries per current keypoint
 
 enum KfState { KF_FREE = 0, KF_STAGED = 1, KF_LIVE = 2, KF_DEAD = 3 };
-enum Scal { SC_NEXT_ID = 0, SC_OBS_HEAD, SC_RECENT_N, SC_ERR, SC_DIRTY_N, SC_ROUND, SC_N = 8 };
+enum Scal { SC_NEXT_ID = 0, SC_OBS_HEAD, SC_RECENT_N, SC_ERR, SC_DIRTY_N, SC_ROUND, SC_MTAG, SC_N = 8 };
 enum LedgerIdx { LG_PERSIST = 0, LG_NAIVE, LG_SMALL_TRI, LG_SMALL_FUSE, LG_SMALL_EVENTS, LG_EVICT, LG_N = 8 };
 enum CandStatus { CS_PASS = 0, CS_PARALLAX = 1, CS_DEPTH = 2, CS_REPROJ = 3, CS_SCALE = 4, CS_DEGEN = 5 };
 
@@ -104,6 +105,21 @@ struct Scratch {
   int* def;              // [act_cap] ready ADDs of this round (grouped per point)
   unsigned long long* dnxt;  // [act_cap] per-point chain of ready ADDs: (round << 32 | def index)
   int* grp_list;         // [act_cap] multi-ADD groups committed warp-cooperatively (def index)
+  // reverse passes
+  int* pinfo;            // [3*TMAX] per pass: actions, live bound points, observation sum
+  unsigned* hitpass;     // [kpkf_max*HPW] per current keypoint: bitmap of passes hitting it
+  int* pj;               // [TMAX*kpkf_max] per (pass, keypoint): resolved hit (-3 not bound)
+  int* pass_of;          // [kf_cap] keyframe slot -> pass index (-1)
+  int* snap;             // [kpkf_max] current keyframe bindings before an apply
+  int* rmark;            // [mp_cap] dedup tag of the touched-point list
+  int* pmp;              // [TMAX*kpkf_max] per (pass, keypoint): bound live point at evaluation
+  int* pob;              // [TMAX*kpkf_max] per (pass, keypoint): its observation count then
+  int* itag;             // [TMAX*kpkf_max] dedup tag of the re-evaluation list
+  int* ilist;            // [TMAX*kpkf_max] (pass, keypoint) items to re-evaluate
+  int* cands;            // [act_cap] points touched by an apply
+  int* hl_cnt;           // [kpkf_max] per current keypoint: points whose hit is it (count)
+  int* hl;               // [kpkf_max*HL] ... (ids; entries whose hit moved are skipped)
+  int* hreg;             // [mp_cap] step tag: point already listed by the speculative scan
   int* act_flag;         // [TMAX*kpkf_max]
   int* vis_flag;         // [TMAX*kpkf_max]
   int pts_cap;
@@ -159,6 +175,7 @@ struct DevMap {
   double* ghi;
   unsigned char* gval;
   int* ver;          // bumped on every observation change (speculative reverse gather)
+  int2* mrg;         // loser -> {merge tag, winner}: deferred visible bumps follow it (SC_MTAG)
   int2* hit;         // per point: {version, hit into the current keyframe (-2/-1/j)}
   // deterministic-reservation tables (apply): round-tagged min action index per entity
   unsigned long long* res_pt;    // [mp_cap]
@@ -533,6 +550,7 @@ __device__ int replace_point(const DevMap& M, int loser, int winner, PairAcc* ac
   M.found[winner] += M.found[loser];
   M.visible[winner] += M.visible[loser];
   M.alive[loser] = 0;
+  M.mrg[loser] = make_int2(M.scal[SC_MTAG], winner);
   mark_dirty(M, winner);
   return migrated;
 }
@@ -653,6 +671,7 @@ __device__ int replace_point_warp(const DevMap& M, int loser, int winner, int la
     M.found[winner] += M.found[loser];
     M.visible[winner] += M.visible[loser];
     M.alive[loser] = 0;
+    M.mrg[loser] = make_int2(M.scal[SC_MTAG], winner);
     M.gval[winner] = 0;
     M.gval[loser] = 0;
     M.ver[winner] += 1;
@@ -792,7 +811,88 @@ __device__ void geo_full_warp(const DevMap& M, int mp, int lane) {
 // Hamming distance to the others is smallest (first in (kf id) order wins). The median of
 // the n-1 integer distances is compared as the sum of the two middle order statistics,
 // which orders exactly like the reference's float nanmedian. Sorts the list first.
+// bitonic sorting network over a register array (all indices compile-time after unrolling)
+template <int W>
+__device__ __forceinline__ void sort_net(int (&d)[W]) {
+#pragma unroll
+  for (int k = 2; k <= W; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+      for (int i = 0; i < W; ++i) {
+        const int l = i ^ j;
+        if (l > i) {
+          const int a = d[i], b = d[l];
+          const int lo = a < b ? a : b, hi = a < b ? b : a;
+          const bool up = (i & k) == 0;
+          d[i] = up ? lo : hi;
+          d[l] = up ? hi : lo;
+        }
+      }
+}
+
+// refresh for 3 <= n <= W <= 32 observations, all in registers: lane a holds observation a
+// and its descriptor, computes its row of distances from broadcast descriptors, sorts the
+// row with a network (self and absent entries sort last) and picks its two middle order
+// statistics; the warp minimum of (med2 << 16 | kf-id rank) is the reference's first
+// argmin of the median. The list is written back sorted by keyframe id.
+template <int W>
+__device__ void refresh_rep_regs(const DevMap& M, int mp, int n, int lane) {
+  int2* o = M.obs + M.ooff[mp];
+  const bool act = lane < n;
+  const int2 e = act ? o[lane] : make_int2(0, 0);
+  const long long key = act ? M.kf_id[e.x] : 0x7fffffffffffffffll;
+  uint4 d0 = make_uint4(0, 0, 0, 0), d1 = d0;
+  if (act) {
+    const int g = M.kp_off[e.x] + e.y;
+    d0 = M.kdesc[2 * g];
+    d1 = M.kdesc[2 * g + 1];
+  }
+  int rk = 0;
+  int d[W];
+#pragma unroll
+  for (int b = 0; b < W; ++b) {
+    const long long kb = __shfl_sync(0xffffffffu, key, b);
+    rk += kb < key;
+    uint4 b0, b1;
+    b0.x = __shfl_sync(0xffffffffu, d0.x, b);
+    b0.y = __shfl_sync(0xffffffffu, d0.y, b);
+    b0.z = __shfl_sync(0xffffffffu, d0.z, b);
+    b0.w = __shfl_sync(0xffffffffu, d0.w, b);
+    b1.x = __shfl_sync(0xffffffffu, d1.x, b);
+    b1.y = __shfl_sync(0xffffffffu, d1.y, b);
+    b1.z = __shfl_sync(0xffffffffu, d1.z, b);
+    b1.w = __shfl_sync(0xffffffffu, d1.w, b);
+    d[b] = (b < n && b != lane) ? hamming(d0, d1, b0, b1) : 0x3ff;
+  }
+  __syncwarp();
+  if (act) o[rk] = e;
+  sort_net<W>(d);
+  const int m = n - 1, k0 = (m - 1) >> 1, k1 = m >> 1;
+  int v0 = 0, v1 = 0;
+#pragma unroll
+  for (int b = 0; b < W; ++b) {
+    v0 = b == k0 ? d[b] : v0;
+    v1 = b == k1 ? d[b] : v1;
+  }
+  unsigned best = act ? ((unsigned)(v0 + v1) << 16) | (unsigned)rk : 0xffffffffu;
+  for (int off = 16; off; off >>= 1) {
+    const unsigned other = __shfl_xor_sync(0xffffffffu, best, off);
+    best = other < best ? other : best;
+  }
+  if (act && rk == (int)(best & 0xffffu)) {
+    M.rep[2 * mp] = d0;
+    M.rep[2 * mp + 1] = d1;
+  }
+  __syncwarp();
+}
+
 __device__ void refresh_rep_warp(const DevMap& M, int mp, int lane) {
+  {
+    const int n = M.nobs[mp];
+    if (n >= 3 && n <= 16) return refresh_rep_regs<16>(M, mp, n, lane);
+    if (n >= 17 && n <= 32) return refresh_rep_regs<32>(M, mp, n, lane);
+  }
   sort_obs_warp(M, mp, lane);
   const int n = M.nobs[mp];
   if (n == 0) return;
