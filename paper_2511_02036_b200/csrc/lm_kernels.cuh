@@ -1613,29 +1613,36 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     for (int k = threadIdx.x; k < ncur; k += REV_THREADS) M.s.snap[k] = M.kbind[cur_off + k];
     __syncthreads();
     const int tag = tag_sh;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int k = threadIdx.x; k < na; k += REV_THREADS) {
       const ActRec x = M.s.acts[k];
       const int cand[3] = {x.pid, x.other, M.s.snap[x.j]};
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const int p = cand[c];
-        if (p < 0 || atomicExch(&M.s.rmark[p], tag) == tag) continue;
-        M.s.cands[atomicAdd(&nc_sh, 1)] = p;
-        const int2* o = M.obs + M.ooff[p];
-        const int no = M.nobs[p];
-        for (int e = 0; e < no; ++e) {
-          const int tt = M.s.pass_of[o[e].x];
-          if (tt > t1) add_item(tt, o[e].y, tag);
-        }
+        if (p >= 0 && atomicExch(&M.s.rmark[p], tag) != tag) M.s.cands[atomicAdd(&nc_sh, 1)] = p;
       }
     }
     __syncthreads();
+    const int ncand = nc_sh;
+    // items of point p (its current observations) in passes after t1; warp-cooperative
+    auto add_point_items = [&](int p) {
+      const int2* o = M.obs + M.ooff[p];
+      const int no = M.nobs[p];
+      for (int e = lane; e < no; e += 32) {
+        const int2 ob = o[e];
+        const int tt = M.s.pass_of[ob.x];
+        if (tt > t1) add_item(tt, ob.y, tag);
+      }
+    };
+    for (int k = wid; k < ncand; k += REV_THREADS / 32) add_point_items(M.s.cands[k]);  // before the apply
+    __syncthreads();
     rounds += apply_block<REV_THREADS>(M, M.s.acts, na, cnt, sh, &acc, tm);  // (barriers)
     if (threadIdx.x == 0) tm[2] += gtime() - ta;
-    // (3) touched points: refresh + new hits; their items after the apply; items hitting a
-    //     current keypoint whose binding changed
+    // (3) touched points: refresh + new hits; then the points hitting a current keypoint
+    //     whose binding changed (hit list; a keypoint whose list overflowed falls back to
+    //     scanning the passes of its bitmap); then the items of all of them after the apply
     const long long tv = gtime();
-    const int ncand = nc_sh;
     redo_pts += ncand;
     refresh_points<REV_THREADS>(M, M.s.cands, ncand, sh);  // (barriers)
     const long long t6 = gtime();
@@ -1647,50 +1654,39 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       const int j = gather_hit(M, fc, g, cur, TV);
       M.hit[p] = make_int2(M.ver[p], j);
       hit_list_add(M, j, p);
-      const int2* o = M.obs + M.ooff[p];
-      const int no = M.nobs[p];
-      for (int e = 0; e < no; ++e) {
-        const int tt = M.s.pass_of[o[e].x];
-        if (tt > t1) add_item(tt, o[e].y, tag);
-      }
     }
+    __syncthreads();
     if (threadIdx.x == 0) {
       tm[0] += t6 - tv;
       tm[1] += gtime() - t6;
     }
-    // items of the points hitting a current keypoint whose binding changed (hit list; a
-    // keypoint whose list overflowed falls back to scanning the passes of its bitmap)
-    {
-      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-      for (int k = wid; k < ncur; k += REV_THREADS / 32) {
-        if (M.kbind[cur_off + k] == M.s.snap[k]) continue;
-        const int c = M.s.hl_cnt[k];
-        if (c <= HL) {
-          for (int q = lane; q < c; q += 32) {
-            const int p = M.s.hl[k * HL + q];
-            if (!M.alive[p] || M.hit[p].y != k) continue;
-            const int2* o = M.obs + M.ooff[p];
-            const int no = M.nobs[p];
-            for (int e = 0; e < no; ++e) {
-              const int tt = M.s.pass_of[o[e].x];
-              if (tt > t1) add_item(tt, o[e].y, tag);
-            }
-          }
-          continue;
+    for (int k = wid; k < ncur; k += REV_THREADS / 32) {
+      if (M.kbind[cur_off + k] == M.s.snap[k]) continue;
+      const int c = M.s.hl_cnt[k];
+      if (c <= HL) {
+        if (lane < c) {
+          const int p = M.s.hl[k * HL + lane];
+          if (M.alive[p] && M.hit[p].y == k && M.s.rmark[p] != tag) M.s.cands[atomicAdd(&nc_sh, 1)] = p;
         }
-        for (int w = 0; w < HPW; ++w) {
-          unsigned bits = M.s.hitpass[k * HPW + w];
-          while (bits) {
-            const int tt = 32 * w + __ffs(bits) - 1;
-            bits &= bits - 1;
-            if (tt <= t1 || tt >= T) continue;
-            const int n = M.kp_n[M.s.targets[tt]];
-            const int* pjt = M.s.pj + (size_t)tt * K;
-            for (int kp = lane; kp < n; kp += 32)
-              if (pjt[kp] == k) add_item(tt, kp, tag);
-          }
+        continue;
+      }
+      for (int w = 0; w < HPW; ++w) {
+        unsigned bits = M.s.hitpass[k * HPW + w];
+        while (bits) {
+          const int tt = 32 * w + __ffs(bits) - 1;
+          bits &= bits - 1;
+          if (tt <= t1 || tt >= T) continue;
+          const int n = M.kp_n[M.s.targets[tt]];
+          const int* pjt = M.s.pj + (size_t)tt * K;
+          for (int kp = lane; kp < n; kp += 32)
+            if (pjt[kp] == k) add_item(tt, kp, tag);
         }
       }
+    }
+    __syncthreads();
+    {
+      const int nall = nc_sh;
+      for (int k = wid; k < nall; k += REV_THREADS / 32) add_point_items(M.s.cands[k]);
     }
     __syncthreads();
     // (4) re-evaluate the listed items; pass totals by deltas
