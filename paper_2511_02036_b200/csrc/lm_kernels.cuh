@@ -158,7 +158,8 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
   if (!A.do_cull) return;
   __shared__ int sh[32];
   __shared__ PairAcc acc;
-  __shared__ int kills[1024];
+  __shared__ int kills[1024], big[1024];
+  __shared__ int nbig;
   pair_acc_init<1024>(&acc, A.cur);
   const int n = M.scal[SC_RECENT_N];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -187,8 +188,15 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
     }
     kept += tot;
     culled += tk;
+    if (threadIdx.x == 0) nbig = 0;
     __syncthreads();
-    for (int k = wid; k < tk; k += 32) kill_point_warp(M, kills[k], lane, &acc);  // independent points
+    for (int k = threadIdx.x; k < tk; k += 1024) {  // independent points: low degree per thread
+      const int mp = kills[k];
+      if (M.nobs[mp] <= 8) kill_point_thread(M, mp, &acc);
+      else big[atomicAdd(&nbig, 1)] = mp;
+    }
+    __syncthreads();
+    for (int k = wid; k < nbig; k += 32) kill_point_warp(M, big[k], lane, &acc);
     __syncthreads();
   }
   pair_acc_flush<1024>(M, &acc);
@@ -1153,28 +1161,39 @@ __device__ int fusion_targets(const DevMap& M, int cur, int n1, int n2, int n_sl
     __syncwarp();
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int nt = 0;
-    seen[cur >> 5] |= 1u << (cur & 31);
-    for (int f = 0; f < n_first; ++f) {
-      tlist[nt++] = first[f];
-      seen[first[f] >> 5] |= 1u << (first[f] & 31);
+  if (wid == 0) {  // the dependent walk, one warp: lanes test 32 ranked candidates at once
+    for (int f = lane; f < n_first; f += 32) {
+      tlist[f] = first[f];
+      atomicOr(&seen[first[f] >> 5], 1u << (first[f] & 31));
     }
+    if (lane == 0) atomicOr(&seen[cur >> 5], 1u << (cur & 31));
+    __syncwarp();
+    int nt = n_first;
     for (int f = 0; f < n_first; ++f) {
       const int* buf = M.s.rank_buf + (size_t)f * stride;
       const int c = buf[0];
       int added = 0;
-      for (int q = 0; q < c && added < n2 && nt < TMAX; ++q) {
-        const int s = buf[1 + M.kf_cap + q];
-        if (!(seen[s >> 5] >> (s & 31) & 1u)) {
-          seen[s >> 5] |= 1u << (s & 31);
-          tlist[nt++] = s;
-          ++added;
+      for (int q0 = 0; q0 < c && added < n2 && nt < TMAX; q0 += 32) {
+        const int q = q0 + lane;
+        const int sl = q < c ? buf[1 + M.kf_cap + q] : -1;
+        const bool un = sl >= 0 && !(seen[sl >> 5] >> (sl & 31) & 1u);
+        const unsigned bal = __ballot_sync(0xffffffffu, un);
+        const int want = n2 - added < TMAX - nt ? n2 - added : TMAX - nt;
+        const int rk = __popc(bal & ((1u << lane) - 1));
+        if (un && rk < want) {
+          tlist[nt + rk] = sl;
+          atomicOr(&seen[sl >> 5], 1u << (sl & 31));
         }
+        const int got = __popc(bal) < want ? __popc(bal) : want;
+        nt += got;
+        added += got;
+        __syncwarp();
       }
     }
-    n_t = nt;
-    *M.s.n_targets = nt;
+    if (lane == 0) {
+      n_t = nt;
+      *M.s.n_targets = nt;
+    }
   }
   __syncthreads();
   for (int k = threadIdx.x; k < n_t; k += BLOCK) M.s.targets[k] = tlist[k];

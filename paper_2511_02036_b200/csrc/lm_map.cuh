@@ -577,6 +577,29 @@ __device__ void merge_pair(const DevMap& M, int a, int b, PairAcc* acc = nullptr
 // Same net effect as the sequential unlink/link loops above (all covisibility bumps are
 // commutative), with the O(n^2) pair work spread over the 32 lanes of one warp.
 
+// kill_map_point (mapmodel.py:233-237) of a point with at most 8 observations, one thread
+__device__ void kill_point_thread(const DevMap& M, int mp, PairAcc* acc) {
+  const int2* o = M.obs + M.ooff[mp];
+  const int n = M.nobs[mp];
+  int2 e[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (k < n) e[k] = o[k];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = a + 1; b < 8; ++b)
+      if (b < n) covis_add(M, e[a].x, e[b].x, -1, acc);
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (k < n) M.kbind[M.kp_off[e[k].x] + e[k].y] = -1;
+  for (int l = 0; l < M.L; ++l) M.counts[(size_t)mp * M.L + l] = 0;
+  M.nobs[mp] = 0;
+  M.alive[mp] = 0;
+  M.gval[mp] = 0;
+  M.ver[mp] += 1;
+}
+
 // kill_map_point (mapmodel.py:233-237), all lanes of a warp call it with the same mp
 __device__ void kill_point_warp(const DevMap& M, int mp, int lane, PairAcc* acc) {
   const int2* o = M.obs + M.ooff[mp];
