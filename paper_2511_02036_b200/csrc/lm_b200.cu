@@ -554,7 +554,7 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(s.pend, (size_t)s.act_cap); A(s.ready, (size_t)s.act_cap); A(s.merge_a, (size_t)s.act_cap); A(s.merge_b, (size_t)s.act_cap); A(s.acts2, (size_t)s.act_cap);
   A(s.blk_cnt, (size_t)s.act_cap / 256 + 2); A(s.blk_off, (size_t)s.act_cap / 256 + 2); A(s.fctl, 8);
   A(s.pass_j, d.kpkf_max); A(s.add_list, (size_t)s.act_cap);
-  A(s.def, (size_t)s.act_cap); A(s.dnxt, (size_t)s.act_cap); A(s.grp_list, (size_t)s.act_cap);
+  A(s.def, (size_t)s.act_cap); A(s.dnxt, (size_t)s.act_cap); A(s.gbase, MP);
   A(s.pinfo, 3 * TMAX); A(s.hitpass, (size_t)d.kpkf_max * ((TMAX + 31) / 32)); A(s.pj, (size_t)s.act_cap);
   A(s.pass_of, K); A(s.snap, d.kpkf_max); A(s.rmark, MP);
   A(s.pmp, (size_t)s.act_cap); A(s.pob, (size_t)s.act_cap); A(s.itag, (size_t)s.act_cap); A(s.ilist, (size_t)s.act_cap);

@@ -648,14 +648,28 @@ __global__ void __launch_bounds__(1024) k_commit(DevMap* maps, const StepArgs* a
 //   k_fuse_refresh  warp/point refresh every point the forward apply touched
 //   k_fuse_rev      1 CTA/map  reverse passes, gather -> apply per target (fusion.py:337-346)
 
-// _point_geometry row (fusion.py:57-94) from the cached accumulators
+// _point_geometry row (fusion.py:57-94) from the cached accumulators. Every field is
+// loaded up front (one round of independent loads) before the validity branches.
 __device__ void point_geometry(const DevMap& M, int mp, double slack, PGeo& g) {
   g.ok = 0;
-  if (mp < 0 || !M.alive[mp] || M.nobs[mp] == 0) return;
-  if (!M.gval[mp]) geo_full(M, mp);
-  const double lo = M.glo[mp], hi = M.ghi[mp];
+  if (mp < 0) return;
+  const bool alive = M.alive[mp] != 0;
+  const int nobs = M.nobs[mp];
+  const bool gv = M.gval[mp] != 0;
+  double lo = M.glo[mp], hi = M.ghi[mp];
+  double ax = M.gacc[3 * mp], ay = M.gacc[3 * mp + 1], az = M.gacc[3 * mp + 2];
+  const double px = M.pos[3 * mp], py = M.pos[3 * mp + 1], pz = M.pos[3 * mp + 2];
+  const uint4 r0 = M.rep[2 * mp], r1 = M.rep[2 * mp + 1];
+  if (!alive || nobs == 0) return;
+  if (!gv) {
+    geo_full(M, mp);
+    lo = M.glo[mp];
+    hi = M.ghi[mp];
+    ax = M.gacc[3 * mp];
+    ay = M.gacc[3 * mp + 1];
+    az = M.gacc[3 * mp + 2];
+  }
   if (!isfinite(lo)) return;
-  const double ax = M.gacc[3 * mp], ay = M.gacc[3 * mp + 1], az = M.gacc[3 * mp + 2];
   const double nrm = sqrt(ax * ax + ay * ay + az * az);
   if (nrm > 0) {
     g.vx = ax / nrm;
@@ -666,14 +680,14 @@ __device__ void point_geometry(const DevMap& M, int mp, double slack, PGeo& g) {
     g.vy = ay;
     g.vz = az;
   }
-  g.x = M.pos[3 * mp];
-  g.y = M.pos[3 * mp + 1];
-  g.z = M.pos[3 * mp + 2];
+  g.x = px;
+  g.y = py;
+  g.z = pz;
   g.d0 = lo;
   g.blo = lo / slack;
   g.bhi = hi * M.S[M.L - 1] * slack;
-  g.r0 = M.rep[2 * mp];
-  g.r1 = M.rep[2 * mp + 1];
+  g.r0 = r0;
+  g.r1 = r1;
   g.ok = 1;
 }
 
@@ -685,12 +699,14 @@ struct TgtView {
   const uint4* desc;
   const int* cst;    // cell starts [cells+1]
   const int* items;  // local keypoint index per cell entry
+  const double* pose;  // R[9], t[3], C[3], cam[6], cell size
+  int nx, ny;          // grid cells
 };
 
 __device__ __forceinline__ TgtView tgt_global(const DevMap& M, int ts) {
   const int off = M.kp_off[ts];
   return TgtView{M.ku + off, M.kv + off, M.klev + off, M.kdesc + 2 * (size_t)off,
-                 M.cell_start + (size_t)ts * (GRID_CELLS + 1), M.cell_items + off};
+                 M.cell_start + (size_t)ts * (GRID_CELLS + 1), M.cell_items + off, nullptr, M.g_nx[ts], M.g_ny[ts]};
 }
 
 // project + gates + grid window search for one (point, target) pair (fusion.py:97-129,
@@ -698,10 +714,10 @@ __device__ __forceinline__ TgtView tgt_global(const DevMap& M, int ts) {
 // hit, else the hit keypoint (lowest (distance, index) within the window).
 __device__ int gather_hit(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g, int ts, const TgtView& T) {
   if (!g.ok) return -2;
-  const double* R = M.R + 9 * ts;
-  const double* t = M.t + 3 * ts;
-  const double* C = M.C + 3 * ts;
-  const double* cam = M.cam + 6 * ts;
+  const double* R = T.pose ? T.pose : M.R + 9 * ts;
+  const double* t = T.pose ? T.pose + 9 : M.t + 3 * ts;
+  const double* C = T.pose ? T.pose + 12 : M.C + 3 * ts;
+  const double* cam = T.pose ? T.pose + 15 : M.cam + 6 * ts;
   const double qx = R[0] * g.x + R[1] * g.y + R[2] * g.z;
   const double qy = R[3] * g.x + R[4] * g.y + R[5] * g.z;
   const double qz = R[6] * g.x + R[7] * g.y + R[8] * g.z;
@@ -721,8 +737,8 @@ __device__ int gather_hit(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g,
   const int lp = (int)lr;
   const double rad = fc.fuse_radius * M.S[lp];
   // conservative cell window, exact test inside
-  const double cs = M.g_cs[ts];
-  const int nx = M.g_nx[ts], ny = M.g_ny[ts];
+  const double cs = T.pose ? T.pose[21] : M.g_cs[ts];
+  const int nx = T.nx, ny = T.ny;
   int x0 = (int)floor((u - rad - 1.0) / cs), x1 = (int)floor((u + rad + 1.0) / cs);
   int y0 = (int)floor((v - rad - 1.0) / cs), y1 = (int)floor((v + rad + 1.0) / cs);
   x0 = x0 < 0 ? 0 : x0;
@@ -913,7 +929,7 @@ template <int BLOCK>
 __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh, PairAcc* acc,
                            long long* tm = nullptr) {
   __shared__ unsigned round_sh;
-  __shared__ int npend_sh, nmerge_sh, nadd_sh, ndef_sh, ngrp_sh;
+  __shared__ int npend_sh, nmerge_sh, nadd_sh, ndef_sh;
   for (int a = threadIdx.x; a < n; a += BLOCK) M.s.pend[a] = a;
   if (threadIdx.x == 0) npend_sh = n;
   __syncthreads();
@@ -926,7 +942,6 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
       nmerge_sh = 0;
       nadd_sh = 0;
       ndef_sh = 0;
-      ngrp_sh = 0;
     }
     __syncthreads();
     const unsigned rnd = round_sh;
@@ -940,8 +955,8 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
       });
     }
     __syncthreads();
-    // check (read-only): stale actions are counted, merges queued for warps, ADDs chained
-    // per point (a point's chain is linked as one group)
+    // check (read-only): stale actions are counted, merges queued for warps, ADDs take a
+    // ticket in their point's group (gtick = round << 32 | members)
     for (int q = threadIdx.x; q < np; q += BLOCK) {
       const int a = M.s.pend[q];
       const unsigned long long tag = res_tag(rnd, a);
@@ -956,7 +971,17 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
       } else if (kind == 1) {
         const int d = atomicAdd(&ndef_sh, 1);
         M.s.def[d] = a;
-        M.s.dnxt[d] = atomicExch(&M.grp_head[x.pid], ((unsigned long long)rnd << 32) | (unsigned)d);
+        unsigned long long v = M.grp_head[x.pid];
+        while (true) {
+          const bool same = (unsigned)(v >> 32) == rnd;
+          const unsigned long long nv = same ? v + 1 : (((unsigned long long)rnd << 32) | 1ull);
+          const unsigned long long old = atomicCAS(&M.grp_head[x.pid], v, nv);
+          if (old == v) {
+            M.s.dnxt[d] = same ? (v & 0xffffffffull) : 0ull;
+            break;
+          }
+          v = old;
+        }
       } else {
         const int at = atomicAdd(&nmerge_sh, 1);
         M.s.merge_a[at] = x.pid;
@@ -968,31 +993,70 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
       tm[9] += gtime() - tt;
       tt = gtime();
     }
-    // chain heads: single low-degree ADDs link here (thread), the rest go to warps
+    // group leaders (ticket 0): a lone low-degree ADD links here (thread), a lone high-degree
+    // one goes to a warp; a group of m reserves m entries (base = old length) for its members
     const int nd = ndef_sh;
     for (int d = threadIdx.x; d < nd; d += BLOCK) {
-      const int a = M.s.def[d];
-      const ActRec x = acts[a];
-      if (M.grp_head[x.pid] != (((unsigned long long)rnd << 32) | (unsigned)d)) continue;
-      const bool single = (unsigned)(M.s.dnxt[d] >> 32) != rnd;
-      if (single && M.nobs[x.pid] <= 24) {
-        link(M, x.pid, x.slot, x.j, acc);
-        mark_dirty(M, x.pid);
-        M.found[x.pid] += 1;
-        atomicAdd(&cnt[1], 1);
-      } else if (single) {
-        M.s.add_list[atomicAdd(&nadd_sh, 1)] = a;
-      } else {
-        M.s.grp_list[atomicAdd(&ngrp_sh, 1)] = d;
+      if (M.s.dnxt[d] != 0ull) continue;
+      const ActRec x = acts[M.s.def[d]];
+      const int p = x.pid;
+      const int m = (int)(M.grp_head[p] & 0xffffffffull);
+      if (m == 1) {
+        if (M.nobs[p] <= 24) {
+          link(M, p, x.slot, x.j, acc);
+          mark_dirty(M, p);
+          M.found[p] += 1;
+          atomicAdd(&cnt[1], 1);
+        } else {
+          M.s.add_list[atomicAdd(&nadd_sh, 1)] = M.s.def[d];
+        }
+        continue;
       }
+      const int n0 = M.nobs[p];
+      if (n0 + m > M.ocap[p]) {  // grow by doubling, copy the current entries
+        int nc = M.ocap[p] < 4 ? 4 : M.ocap[p];
+        while (nc < n0 + m) nc *= 2;
+        const int off = atomicAdd(&M.scal[SC_OBS_HEAD], nc);
+        if (off + nc > M.obs_cap) {
+          set_err(M, LM_ERR_CAPACITY);
+          M.s.gbase[p] = -1;
+          continue;
+        }
+        const int2* src = M.obs + M.ooff[p];
+        for (int k = 0; k < n0; ++k) M.obs[off + k] = src[k];
+        M.ooff[p] = off;
+        M.ocap[p] = nc;
+      }
+      M.s.gbase[p] = n0;
+      M.nobs[p] = n0 + m;
+      M.found[p] += m;
+      M.ver[p] += 1;
+      M.gval[p] = 0;
+      mark_dirty(M, p);
+      atomicAdd(&cnt[1], m);
     }
     __syncthreads();
     if (tm && threadIdx.x == 0) {
       tm[10] += gtime() - tt;
       tt = gtime();
     }
+    // group members: own entry, binding, counter, covisibility with the old observers;
+    // warps: lone high-degree ADDs and merges (disjoint entities)
+    for (int d = threadIdx.x; d < nd; d += BLOCK) {
+      const ActRec x = acts[M.s.def[d]];
+      const int p = x.pid;
+      const int m = (int)(M.grp_head[p] & 0xffffffffull);
+      const int base = M.s.gbase[p];
+      if (m == 1 || base < 0) continue;
+      int2* o = M.obs + M.ooff[p];
+      o[base + (int)M.s.dnxt[d]] = make_int2(x.slot, x.j);
+      const int g = M.kp_off[x.slot] + x.j;
+      M.kbind[g] = p;
+      atomicAdd(&M.counts[(size_t)p * M.L + M.klev[g]], 1);
+      for (int k = 0; k < base; ++k) covis_add(M, x.slot, o[k].x, +1, acc);
+    }
     {
-      const int nm = nmerge_sh, na = nadd_sh, ng = ngrp_sh;
+      const int nm = nmerge_sh, na = nadd_sh;
       for (int k = threadIdx.x >> 5; k < na; k += BLOCK / 32) {
         const ActRec x = acts[M.s.add_list[k]];
         link_warp(M, x.pid, x.slot, x.j, lane, acc);
@@ -1001,14 +1065,21 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
           M.found[x.pid] += 1;
         }
       }
-      for (int k = threadIdx.x >> 5; k < ng; k += BLOCK / 32) {
-        const int d = M.s.grp_list[k];
-        const int got = group_link_warp(M, acts[M.s.def[d]].pid, d, rnd, acts, M.s.def, M.s.dnxt, lane, acc);
-        if (lane == 0) atomicAdd(&cnt[1], got);
-      }
       for (int k = threadIdx.x >> 5; k < nm; k += BLOCK / 32) merge_pair_warp(M, M.s.merge_a[k], M.s.merge_b[k], lane, acc);
       if (threadIdx.x == 0) cnt[0] += nm;
       if (threadIdx.x == 32) atomicAdd(&cnt[1], na);
+    }
+    __syncthreads();
+    // group members: covisibility with the members of lower ticket (each new pair once)
+    for (int d = threadIdx.x; d < nd; d += BLOCK) {
+      const ActRec x = acts[M.s.def[d]];
+      const int p = x.pid;
+      const int m = (int)(M.grp_head[p] & 0xffffffffull);
+      const int base = M.s.gbase[p];
+      if (m == 1 || base < 0) continue;
+      const int2* o = M.obs + M.ooff[p];
+      const int tk = (int)M.s.dnxt[d];
+      for (int k = 0; k < tk; ++k) covis_add(M, x.slot, o[base + k].x, +1, acc);
     }
     __syncthreads();
     if (tm && threadIdx.x == 0) {
@@ -1554,7 +1625,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       }
       const int* gcs = M.cell_start + (size_t)A.cur * (GRID_CELLS + 1);
       for (int k = threadIdx.x; k <= nc; k += REV_THREADS) scs[k] = gcs[k];
-      TV = TgtView{su, sv, sl, sd, scs, sit};
+      TV = TgtView{su, sv, sl, sd, scs, sit, nullptr, TV.nx, TV.ny};
     }
   }
   __shared__ int sh[32];
@@ -1563,6 +1634,13 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   __shared__ PairAcc acc;
   __shared__ int s_nact[TMAX], s_live[TMAX], s_obs[TMAX];
   __shared__ int t1_sh, nc_sh, ni_sh, tag_sh;
+  __shared__ double cur_pose[22];  // R, t, C, cam, cell size of the current keyframe
+  if (threadIdx.x < 22) {
+    const int c = A.cur, k = threadIdx.x;
+    cur_pose[k] = k < 9 ? M.R[9 * c + k] : k < 12 ? M.t[3 * c + k - 9] : k < 15 ? M.C[3 * c + k - 12]
+                : k < 21 ? M.cam[6 * c + k - 15] : M.g_cs[c];
+  }
+  TV.pose = cur_pose;  // visible after the first barrier below
   const int K = M.kpkf_max;
   const int cur = A.cur;
   const int ncur = M.kp_n[cur], cur_off = M.kp_off[cur];

@@ -103,8 +103,8 @@ struct Scratch {
   int* pass_j;           // [kpkf_max] per-pass resolved hit per target keypoint
   int* add_list;         // [act_cap] high-degree ADDs committed warp-cooperatively
   int* def;              // [act_cap] ready ADDs of this round (grouped per point)
-  unsigned long long* dnxt;  // [act_cap] per-point chain of ready ADDs: (round << 32 | def index)
-  int* grp_list;         // [act_cap] multi-ADD groups committed warp-cooperatively (def index)
+  unsigned long long* dnxt;  // [act_cap] ticket of a ready ADD within its point's group
+  int* gbase;            // [mp_cap] observation-list position of a group's first new entry
   // reverse passes
   int* pinfo;            // [3*TMAX] per pass: actions, live bound points, observation sum
   unsigned* hitpass;     // [kpkf_max*HPW] per current keypoint: bitmap of passes hitting it
@@ -182,7 +182,7 @@ struct DevMap {
   unsigned long long* res_slot;  // [kp_cap]
   unsigned long long* res_ex;    // [mp_cap] min tag of the actions that need the point exclusively
   unsigned long long* res_pair;  // [RES_PAIR] (point, keyframe) ADD keys, hashed (collisions only serialise)
-  unsigned long long* grp_head;  // [mp_cap] head of the point's ready-ADD chain, (round << 32 | def index)
+  unsigned long long* grp_head;  // [mp_cap] ready ADDs of the point this round: (round << 32 | count)
   // covisibility
   int* covis;
   // probation list (culling.RecentPoint)
@@ -372,26 +372,52 @@ __device__ void geo_full(const DevMap& M, int mp) {
 
 // _record_obs: covis +1 with every current observer, bind the slot, count the level. An
 // observation appended after every existing one extends the cached sums exactly.
+// Latency-shaped: the independent loads are issued together before any store.
 __device__ void link(const DevMap& M, int mp, int slot, int kp, PairAcc* acc = nullptr) {
-  const int2* o = M.obs + M.ooff[mp];
-  const int n = M.nobs[mp];
+  const int n = M.nobs[mp], cap = M.ocap[mp], off = M.ooff[mp];
+  const int dirty = M.dirty[mp], gv = M.gval[mp];
+  const int g = M.kp_off[slot] + kp;
+  const long long kf_new = M.kf_id[slot];
+  const double px = M.pos[3 * mp], py = M.pos[3 * mp + 1], pz = M.pos[3 * mp + 2];
+  const double cx = M.C[3 * slot], cy = M.C[3 * slot + 1], cz = M.C[3 * slot + 2];
+  const int2* o = M.obs + off;
+  const int last = n ? o[n - 1].x : -1;
+  const int lev = M.klev[g];
+  const long long kf_last = last >= 0 ? M.kf_id[last] : -1;
   for (int k = 0; k < n; ++k) covis_add(M, slot, o[k].x, +1, acc);
   // appended after the newest keyframe of a clean (sorted) list: the cached sums extend exactly
-  const bool newest = !M.dirty[mp] && (n == 0 || M.kf_id[o[n - 1].x] < M.kf_id[slot]);
-  const int at = obs_insert(M, mp, slot, kp);
-  if (at < 0) return;
-  const int g = M.kp_off[slot] + kp;
+  const bool newest = !dirty && (n == 0 || kf_last < kf_new);
+  int at = n;
+  if (n == cap) {
+    const int nc = cap < 4 ? 4 : 2 * cap;
+    const int noff = atomicAdd(&M.scal[SC_OBS_HEAD], nc);
+    if (noff + nc > M.obs_cap) {
+      set_err(M, LM_ERR_CAPACITY);
+      return;
+    }
+    for (int k = 0; k < n; ++k) M.obs[noff + k] = o[k];
+    M.ooff[mp] = noff;
+    M.ocap[mp] = nc;
+    M.obs[noff + n] = make_int2(slot, kp);
+  } else {
+    M.obs[off + at] = make_int2(slot, kp);
+  }
+  M.nobs[mp] = n + 1;
   M.kbind[g] = mp;
-  M.counts[(size_t)mp * M.L + M.klev[g]] += 1;
+  M.counts[(size_t)mp * M.L + lev] += 1;
   M.ver[mp] += 1;
-  if (M.gval[mp] && newest) {
-    double rx, ry, rz, dd, d0;
-    if (geo_term(M, mp, make_int2(slot, kp), rx, ry, rz, dd, d0)) {
-      M.glo[mp] = d0 < M.glo[mp] ? d0 : M.glo[mp];
-      M.ghi[mp] = d0 > M.ghi[mp] ? d0 : M.ghi[mp];
-      M.gacc[3 * mp] = M.gacc[3 * mp] + rx / dd;
-      M.gacc[3 * mp + 1] = M.gacc[3 * mp + 1] + ry / dd;
-      M.gacc[3 * mp + 2] = M.gacc[3 * mp + 2] + rz / dd;
+  if (gv && newest) {
+    const double rx = px - cx, ry = py - cy, rz = pz - cz;
+    const double dd = sqrt(rx * rx + ry * ry + rz * rz);
+    if (dd > 0) {  // geo_term
+      const double d0 = dd / M.S[lev];
+      const double lo = M.glo[mp], hi = M.ghi[mp];
+      const double ax = M.gacc[3 * mp], ay = M.gacc[3 * mp + 1], az = M.gacc[3 * mp + 2];
+      M.glo[mp] = d0 < lo ? d0 : lo;
+      M.ghi[mp] = d0 > hi ? d0 : hi;
+      M.gacc[3 * mp] = ax + rx / dd;
+      M.gacc[3 * mp + 1] = ay + ry / dd;
+      M.gacc[3 * mp + 2] = az + rz / dd;
     }
   } else {
     M.gval[mp] = 0;
@@ -427,94 +453,6 @@ __device__ void link_warp(const DevMap& M, int mp, int slot, int kp, int lane, P
     }
   }
   __syncwarp();
-}
-
-// grow mp's list to hold `need` entries (lane-parallel copy); false when the pool is exhausted
-__device__ bool obs_reserve_warp(const DevMap& M, int mp, int need, int lane) {
-  int off = M.ooff[mp], cap = M.ocap[mp];
-  if (need <= cap) return true;
-  if (lane == 0) {
-    int nc = cap < 4 ? 4 : cap;
-    while (nc < need) nc *= 2;
-    off = atomicAdd(&M.scal[SC_OBS_HEAD], nc);
-    if (off + nc > M.obs_cap) {
-      set_err(M, LM_ERR_CAPACITY);
-      off = -1;
-    }
-    cap = nc;
-  }
-  off = __shfl_sync(0xffffffffu, off, 0);
-  cap = __shfl_sync(0xffffffffu, cap, 0);
-  if (off < 0) return false;
-  const int2* src = M.obs + M.ooff[mp];
-  const int n = M.nobs[mp];
-  for (int k = lane; k < n; k += 32) M.obs[off + k] = src[k];
-  __syncwarp();
-  if (lane == 0) {
-    M.ooff[mp] = off;
-    M.ocap[mp] = cap;
-  }
-  __syncwarp();
-  return true;
-}
-
-// A group of ADDs of one point committed in the same apply round (pairwise distinct
-// keyframes, none observed yet). Linking them in any order gives the same observation set,
-// counters and covisibility deltas (+1 for every new x old and new x new pair), so a warp
-// links them in chunks of 32: chunk members against the current list, pairs inside the
-// chunk, then an append. Members are chained through dnxt[q] = (round << 32 | q'), q
-// indexing def[] (action indices into acts). Returns the number linked.
-__device__ int group_link_warp(const DevMap& M, int mp, int q_head, unsigned rnd, const ActRec* acts,
-                               const int* def, const unsigned long long* dnxt, int lane, PairAcc* acc) {
-  int q = q_head, total = 0;
-  while (q >= 0) {
-    int my = -1, c = 0;
-    for (; c < 32 && q >= 0; ++c) {  // uniform walk (broadcast loads)
-      if (lane == c) my = q;
-      const unsigned long long v = dnxt[q];
-      q = (unsigned)(v >> 32) == rnd ? (int)(v & 0xffffffffu) : -1;
-    }
-    int slot = 0, kp = 0;
-    if (my >= 0) {
-      const ActRec x = acts[def[my]];
-      slot = x.slot;
-      kp = x.j;
-    }
-    const int n = M.nobs[mp];
-    const int2* o = M.obs + M.ooff[mp];
-    for (int b = 0; b < c * n; b += 32) {  // new x current observers
-      const int t = b + lane;
-      const int i = t / n < c ? t / n : c - 1;
-      const int si = __shfl_sync(0xffffffffu, slot, i);
-      if (t < c * n) covis_add(M, si, o[t - i * n].x, +1, acc);
-    }
-    for (int b = 0; b < c * c; b += 32) {  // new x new (each unordered pair once)
-      const int t = b + lane;
-      const int i = t / c < c ? t / c : c - 1, i2 = t - (t / c) * c;
-      const int si = __shfl_sync(0xffffffffu, slot, i);
-      const int si2 = __shfl_sync(0xffffffffu, slot, i2);
-      if (t < c * c && i < i2) covis_add(M, si, si2, +1, acc);
-    }
-    if (!obs_reserve_warp(M, mp, n + c, lane)) return total;
-    if (lane < c) {
-      M.obs[M.ooff[mp] + n + lane] = make_int2(slot, kp);
-      const int g = M.kp_off[slot] + kp;
-      M.kbind[g] = mp;
-      atomicAdd(&M.counts[(size_t)mp * M.L + M.klev[g]], 1);
-    }
-    __syncwarp();
-    if (lane == 0) M.nobs[mp] = n + c;
-    __syncwarp();
-    total += c;
-  }
-  if (lane == 0) {
-    M.found[mp] += total;
-    M.ver[mp] += 1;
-    M.gval[mp] = 0;
-    mark_dirty(M, mp);
-  }
-  __syncwarp();
-  return total;
 }
 
 // _unrecord_obs of list entry k: unbind, uncount, covis -1 with every remaining observer
