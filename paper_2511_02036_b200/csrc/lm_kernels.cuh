@@ -1504,14 +1504,14 @@ __global__ void __launch_bounds__(256) k_fuse_refresh(DevMap* maps, const StepAr
   const int lane = threadIdx.x & 31;
   for (int k = blockIdx.x * 8 + (threadIdx.x >> 5); k < n; k += gridDim.x * 8) {
     const int mp = M.dirty_list[k];
-    if (!M.dirty[mp]) continue;
+    // the list can hold a point twice (dirty again after an earlier refresh): one warp
+    // claims it, so no two warps sort the same observation list
+    int claim = 0;
+    if (lane == 0) claim = atomicExch(&M.dirty[mp], 0);
+    if (!__shfl_sync(0xffffffffu, claim, 0)) continue;
     if (M.alive[mp]) {
       refresh_rep_warp(M, mp, lane);
-      if (lane == 0) M.dirty[mp] = 0;
-      __syncwarp();
       if (!M.gval[mp]) geo_full_warp(M, mp, lane);
-    } else if (lane == 0) {
-      M.dirty[mp] = 0;
     }
   }
 }

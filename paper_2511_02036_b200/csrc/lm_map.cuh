@@ -772,87 +772,210 @@ __device__ void geo_full_warp(const DevMap& M, int mp, int lane) {
 // Hamming distance to the others is smallest (first in (kf id) order wins). The median of
 // the n-1 integer distances is compared as the sum of the two middle order statistics,
 // which orders exactly like the reference's float nanmedian. Sorts the list first.
-// bitonic sorting network over a register array (all indices compile-time after unrolling)
-template <int W>
-__device__ __forceinline__ void sort_net(int (&d)[W]) {
+// k-th smallest (k from 0) of the 9-bit values whose bit-planes are pl[bit][word] over the
+// candidate set cand[word]: radix select, 9 steps of popcounts (registers only)
+template <int NW>
+__device__ __forceinline__ int plane_select(const unsigned (&pl)[9][NW], unsigned (&cand)[NW], int k) {
+  int v = 0;
 #pragma unroll
-  for (int k = 2; k <= W; k <<= 1)
+  for (int bit = 8; bit >= 0; --bit) {
+    int c0 = 0;
 #pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1)
+    for (int w = 0; w < NW; ++w) c0 += __popc(cand[w] & ~pl[bit][w]);
+    const bool zero = k < c0;
+    if (!zero) {
+      k -= c0;
+      v |= 1 << bit;
+    }
 #pragma unroll
-      for (int i = 0; i < W; ++i) {
-        const int l = i ^ j;
-        if (l > i) {
-          const int a = d[i], b = d[l];
-          const int lo = a < b ? a : b, hi = a < b ? b : a;
-          const bool up = (i & k) == 0;
-          d[i] = up ? lo : hi;
-          d[l] = up ? hi : lo;
-        }
-      }
+    for (int w = 0; w < NW; ++w) cand[w] &= zero ? ~pl[bit][w] : pl[bit][w];
+  }
+  return v;
 }
 
-// refresh for 3 <= n <= W <= 32 observations, all in registers: lane a holds observation a
-// and its descriptor, computes its row of distances from broadcast descriptors, sorts the
-// row with a network (self and absent entries sort last) and picks its two middle order
-// statistics; the warp minimum of (med2 << 16 | kf-id rank) is the reference's first
-// argmin of the median. The list is written back sorted by keyframe id.
-template <int W>
-__device__ void refresh_rep_regs(const DevMap& M, int mp, int n, int lane) {
+// refresh for 3 <= n <= 32*NW observations, in registers: lane l holds observations l,
+// l+32, ... (entry, kf-id key, descriptor). For each of its rows a lane builds the 9
+// bit-planes of the row's distances from broadcast descriptors, and radix-selects the two
+// middle order statistics of the n-1 non-self distances; the warp minimum of
+// (med2 << 16 | kf-id rank) is the reference's first argmin of the median (ties -> lower
+// kf id). The list is written back sorted by keyframe id.
+template <int NW>
+__device__ void refresh_rep_planes(const DevMap& M, int mp, int n, int lane) {
   int2* o = M.obs + M.ooff[mp];
-  const bool act = lane < n;
-  const int2 e = act ? o[lane] : make_int2(0, 0);
-  const long long key = act ? M.kf_id[e.x] : 0x7fffffffffffffffll;
-  uint4 d0 = make_uint4(0, 0, 0, 0), d1 = d0;
-  if (act) {
-    const int g = M.kp_off[e.x] + e.y;
-    d0 = M.kdesc[2 * g];
-    d1 = M.kdesc[2 * g + 1];
-  }
-  int rk = 0;
-  int d[W];
+  int2 e[NW];
+  long long key[NW];
+  uint4 d0[NW], d1[NW];
 #pragma unroll
-  for (int b = 0; b < W; ++b) {
-    const long long kb = __shfl_sync(0xffffffffu, key, b);
-    rk += kb < key;
-    uint4 b0, b1;
-    b0.x = __shfl_sync(0xffffffffu, d0.x, b);
-    b0.y = __shfl_sync(0xffffffffu, d0.y, b);
-    b0.z = __shfl_sync(0xffffffffu, d0.z, b);
-    b0.w = __shfl_sync(0xffffffffu, d0.w, b);
-    b1.x = __shfl_sync(0xffffffffu, d1.x, b);
-    b1.y = __shfl_sync(0xffffffffu, d1.y, b);
-    b1.z = __shfl_sync(0xffffffffu, d1.z, b);
-    b1.w = __shfl_sync(0xffffffffu, d1.w, b);
-    d[b] = (b < n && b != lane) ? hamming(d0, d1, b0, b1) : 0x3ff;
+  for (int s = 0; s < NW; ++s) e[s] = s * 32 + lane < n ? o[s * 32 + lane] : make_int2(0, 0);
+#pragma unroll
+  for (int s = 0; s < NW; ++s) {
+    const bool act = s * 32 + lane < n;
+    key[s] = act ? M.kf_id[e[s].x] : 0x7fffffffffffffffll;
+    const int g = M.kp_off[e[s].x] + e[s].y;
+    d0[s] = act ? M.kdesc[2 * g] : make_uint4(0, 0, 0, 0);
+    d1[s] = act ? M.kdesc[2 * g + 1] : make_uint4(0, 0, 0, 0);
   }
+  int rk[NW];
+#pragma unroll
+  for (int s = 0; s < NW; ++s) rk[s] = 0;
+#pragma unroll
+  for (int sb = 0; sb < NW; ++sb)
+    for (int l = 0; l < 32; ++l) {
+      const long long kb = __shfl_sync(0xffffffffu, key[sb], l);
+#pragma unroll
+      for (int s = 0; s < NW; ++s) rk[s] += kb < key[s];
+    }
   __syncwarp();
-  if (act) o[rk] = e;
-  sort_net<W>(d);
-  const int m = n - 1, k0 = (m - 1) >> 1, k1 = m >> 1;
-  int v0 = 0, v1 = 0;
 #pragma unroll
-  for (int b = 0; b < W; ++b) {
-    v0 = b == k0 ? d[b] : v0;
-    v1 = b == k1 ? d[b] : v1;
+  for (int s = 0; s < NW; ++s)
+    if (s * 32 + lane < n) o[rk[s]] = e[s];
+  const int m = n - 1, k0 = (m - 1) >> 1, k1 = m >> 1;
+  unsigned best = 0xffffffffu;
+#pragma unroll
+  for (int s = 0; s < NW; ++s) {  // row slot s of every lane
+    unsigned pl[9][NW];
+#pragma unroll
+    for (int bit = 0; bit < 9; ++bit)
+#pragma unroll
+      for (int w = 0; w < NW; ++w) pl[bit][w] = 0u;
+#pragma unroll
+    for (int sb = 0; sb < NW; ++sb)
+      for (int l = 0; l < 32; ++l) {
+        uint4 b0, b1;
+        b0.x = __shfl_sync(0xffffffffu, d0[sb].x, l);
+        b0.y = __shfl_sync(0xffffffffu, d0[sb].y, l);
+        b0.z = __shfl_sync(0xffffffffu, d0[sb].z, l);
+        b0.w = __shfl_sync(0xffffffffu, d0[sb].w, l);
+        b1.x = __shfl_sync(0xffffffffu, d1[sb].x, l);
+        b1.y = __shfl_sync(0xffffffffu, d1[sb].y, l);
+        b1.z = __shfl_sync(0xffffffffu, d1[sb].z, l);
+        b1.w = __shfl_sync(0xffffffffu, d1[sb].w, l);
+        const unsigned dist = (unsigned)hamming(d0[s], d1[s], b0, b1);
+#pragma unroll
+        for (int bit = 0; bit < 9; ++bit) pl[bit][sb] |= ((dist >> bit) & 1u) << l;
+      }
+    const int i = s * 32 + lane;
+    if (i < n) {
+      unsigned cand[NW];
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {  // the other real observations
+        const int lo = w * 32;
+        unsigned msk = n - lo >= 32 ? 0xffffffffu : (n - lo <= 0 ? 0u : (1u << (n - lo)) - 1u);
+        if (i >= lo && i < lo + 32) msk &= ~(1u << (i - lo));
+        cand[w] = msk;
+      }
+      unsigned c2[NW];
+#pragma unroll
+      for (int w = 0; w < NW; ++w) c2[w] = cand[w];
+      const int v0 = plane_select<NW>(pl, cand, k0);
+      const int v1 = k1 == k0 ? v0 : plane_select<NW>(pl, c2, k1);
+      const unsigned kk = ((unsigned)(v0 + v1) << 16) | (unsigned)rk[s];
+      best = kk < best ? kk : best;
+    }
   }
-  unsigned best = act ? ((unsigned)(v0 + v1) << 16) | (unsigned)rk : 0xffffffffu;
   for (int off = 16; off; off >>= 1) {
     const unsigned other = __shfl_xor_sync(0xffffffffu, best, off);
     best = other < best ? other : best;
   }
-  if (act && rk == (int)(best & 0xffffu)) {
-    M.rep[2 * mp] = d0;
-    M.rep[2 * mp + 1] = d1;
+#pragma unroll
+  for (int s = 0; s < NW; ++s)
+    if (s * 32 + lane < n && rk[s] == (int)(best & 0xffffu)) {
+      M.rep[2 * mp] = d0[s];
+      M.rep[2 * mp + 1] = d1[s];
+    }
+  __syncwarp();
+}
+
+// refresh for 32 < n <= 32*NS observations: lane l holds observations l, l+32, ...
+// (entry, key, descriptor in registers); every row's distances come from broadcast
+// descriptors (no dependent global loads), its two middle order statistics from a
+// quickselect over a per-lane scratch row (L1-resident local memory).
+template <int NS>
+__device__ void refresh_rep_lanes(const DevMap& M, int mp, int n, int lane) {
+  int2* o = M.obs + M.ooff[mp];
+  int2 e[NS];
+  long long key[NS];
+  uint4 d0[NS], d1[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int i = s * 32 + lane;
+    e[s] = i < n ? o[i] : make_int2(0, 0);
   }
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int i = s * 32 + lane;
+    key[s] = i < n ? M.kf_id[e[s].x] : 0x7fffffffffffffffll;
+    const int g = M.kp_off[e[s].x] + e[s].y;
+    d0[s] = i < n ? M.kdesc[2 * g] : make_uint4(0, 0, 0, 0);
+    d1[s] = i < n ? M.kdesc[2 * g + 1] : make_uint4(0, 0, 0, 0);
+  }
+  int rk[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) rk[s] = 0;
+#pragma unroll
+  for (int sb = 0; sb < NS; ++sb)
+    for (int l = 0; l < 32; ++l) {
+      const long long kb = __shfl_sync(0xffffffffu, key[sb], l);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) rk[s] += kb < key[s];
+    }
+  __syncwarp();
+#pragma unroll
+  for (int s = 0; s < NS; ++s)
+    if (s * 32 + lane < n) o[rk[s]] = e[s];
+  unsigned short d[NS][32 * NS];
+#pragma unroll
+  for (int sb = 0; sb < NS; ++sb)
+    for (int l = 0; l < 32; ++l) {
+      uint4 b0, b1;
+      b0.x = __shfl_sync(0xffffffffu, d0[sb].x, l);
+      b0.y = __shfl_sync(0xffffffffu, d0[sb].y, l);
+      b0.z = __shfl_sync(0xffffffffu, d0[sb].z, l);
+      b0.w = __shfl_sync(0xffffffffu, d0[sb].w, l);
+      b1.x = __shfl_sync(0xffffffffu, d1[sb].x, l);
+      b1.y = __shfl_sync(0xffffffffu, d1[sb].y, l);
+      b1.z = __shfl_sync(0xffffffffu, d1[sb].z, l);
+      b1.w = __shfl_sync(0xffffffffu, d1[sb].w, l);
+      const int b = sb * 32 + l;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) d[s][b] = (unsigned short)hamming(d0[s], d1[s], b0, b1);
+    }
+  const int m = n - 1, k0 = (m - 1) >> 1, k1 = m >> 1;
+  unsigned best = 0xffffffffu;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int i = s * 32 + lane;
+    if (i >= n) continue;
+    unsigned short* r = d[s];
+    r[i] = r[n - 1];  // drop the self distance: the last real entry moves into its place
+    const int v0 = kth_smallest(r, m, k0);
+    int v1 = v0;
+    if (k1 != k0) {
+      v1 = 0x7fffffff;
+      for (int b = k0 + 1; b < m; ++b) v1 = r[b] < v1 ? r[b] : v1;
+    }
+    const unsigned kk = ((unsigned)(v0 + v1) << 16) | (unsigned)rk[s];
+    best = kk < best ? kk : best;
+  }
+  for (int off = 16; off; off >>= 1) {
+    const unsigned other = __shfl_xor_sync(0xffffffffu, best, off);
+    best = other < best ? other : best;
+  }
+#pragma unroll
+  for (int s = 0; s < NS; ++s)
+    if (s * 32 + lane < n && rk[s] == (int)(best & 0xffffu)) {
+      M.rep[2 * mp] = d0[s];
+      M.rep[2 * mp + 1] = d1[s];
+    }
   __syncwarp();
 }
 
 __device__ void refresh_rep_warp(const DevMap& M, int mp, int lane) {
   {
     const int n = M.nobs[mp];
-    if (n >= 3 && n <= 16) return refresh_rep_regs<16>(M, mp, n, lane);
-    if (n >= 17 && n <= 32) return refresh_rep_regs<32>(M, mp, n, lane);
+    if (n >= 3 && n <= 32) return refresh_rep_planes<1>(M, mp, n, lane);
+    if (n >= 33 && n <= 64) return refresh_rep_planes<2>(M, mp, n, lane);
+    if (n >= 65 && n <= 128) return refresh_rep_lanes<4>(M, mp, n, lane);
   }
   sort_obs_warp(M, mp, lane);
   const int n = M.nobs[mp];
