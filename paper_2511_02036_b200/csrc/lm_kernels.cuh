@@ -929,7 +929,7 @@ template <int BLOCK>
 __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh, PairAcc* acc,
                            long long* tm = nullptr) {
   __shared__ unsigned round_sh;
-  __shared__ int npend_sh, nmerge_sh, nadd_sh, ndef_sh;
+  __shared__ int npend_sh, nmerge_sh, nadd_sh, ndef_sh, nready_sh, ngrpm_sh;
   for (int a = threadIdx.x; a < n; a += BLOCK) M.s.pend[a] = a;
   if (threadIdx.x == 0) npend_sh = n;
   __syncthreads();
@@ -942,6 +942,8 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
       nmerge_sh = 0;
       nadd_sh = 0;
       ndef_sh = 0;
+      nready_sh = 0;
+      ngrpm_sh = 0;
     }
     __syncthreads();
     const unsigned rnd = round_sh;
@@ -964,6 +966,7 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
       const int ready = for_keys(M, x, [&](int mode, int id) { return holds_key(M, mode, id, tag); });
       M.s.ready[q] = ready;
       if (!ready) continue;
+      atomicAdd(&nready_sh, 1);
       int partner = -1;
       const int kind = classify(M, x, &partner);
       if (kind == 0) {
@@ -1028,6 +1031,7 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
         M.ocap[p] = nc;
       }
       M.s.gbase[p] = n0;
+      atomicAdd(&ngrpm_sh, m);
       M.nobs[p] = n0 + m;
       M.found[p] += m;
       M.ver[p] += 1;
@@ -1071,7 +1075,8 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
     }
     __syncthreads();
     // group members: covisibility with the members of lower ticket (each new pair once)
-    for (int d = threadIdx.x; d < nd; d += BLOCK) {
+    const bool groups = ngrpm_sh > 0;
+    for (int d = threadIdx.x; groups && d < nd; d += BLOCK) {
       const ActRec x = acts[M.s.def[d]];
       const int p = x.pid;
       const int m = (int)(M.grp_head[p] & 0xffffffffull);
@@ -1081,13 +1086,14 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
       const int tk = (int)M.s.dnxt[d];
       for (int k = 0; k < tk; ++k) covis_add(M, x.slot, o[base + k].x, +1, acc);
     }
-    __syncthreads();
+    if (groups) __syncthreads();
     if (tm && threadIdx.x == 0) {
       tm[11] += gtime() - tt;
       tt = gtime();
     }
     int kept = 0;
-    for (int b0 = 0; b0 < np; b0 += BLOCK) {  // stable compaction of the still-pending actions
+    const bool all_ready = nready_sh == np;  // (read before any thread can reset it)
+    for (int b0 = 0; !all_ready && b0 < np; b0 += BLOCK) {  // stable compaction of the still-pending actions
       const int q = b0 + threadIdx.x;
       const int keep = q < np ? !M.s.ready[q] : 0;
       const int a = keep ? M.s.pend[q] : 0;
@@ -1656,7 +1662,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   }
   pair_acc_init<REV_THREADS>(&acc, A.cur);  // (barrier)
   const unsigned long long mpb = M.mp_rec_bytes;
-  long long alg = 0, npts = 0, nacts = 0;
+  long long alg = 0, npts = 0, nacts = 0, ledger_events = 0;
   int rounds = 0, pass_act = 0, reeval = 0, redo_pts = 0;
   int t0 = 0;
   // append item (t, kp) to the re-evaluation list once per tag
@@ -1674,16 +1680,13 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     const int t1 = t1_sh;
     if (threadIdx.x == 0) {
       const int te = t1 < T ? t1 : T - 1;
-      for (int t = t0; t <= te; ++t) {
+      for (int t = t0; t <= te; ++t) {  // ledger totals land once, after the loop
         const int Pt = s_live[t];
-        M.ledger[LG_NAIVE] += Pt * mpb;
-        M.ledger[LG_PERSIST] += Pt * mpb;
-        M.ledger[LG_SMALL_FUSE] += Pt * mpb;
-        M.ledger[LG_SMALL_EVENTS] += 1;
         alg += pass_bytes(Pt, s_obs[t], ncur, s_nact[t]);
         npts += Pt;
         nacts += s_nact[t];
       }
+      ledger_events += te - t0 + 1;
     }
     if (t1 >= T) break;
     ++pass_act;
@@ -1808,6 +1811,10 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   pair_acc_flush<REV_THREADS>(M, &acc);
   for (int t = threadIdx.x; t < T; t += REV_THREADS) M.s.pass_of[M.s.targets[t]] = -1;
   if (threadIdx.x == 0) {
+    M.ledger[LG_NAIVE] += npts * mpb;  // record_small_transfer per pass (devicestore.py:94-101)
+    M.ledger[LG_PERSIST] += npts * mpb;
+    M.ledger[LG_SMALL_FUSE] += npts * mpb;
+    M.ledger[LG_SMALL_EVENTS] += ledger_events;
     lm_step_stats* st = M.s.stats;
     st->merged += cnt[0];
     st->observations_added += cnt[1];
