@@ -120,7 +120,8 @@ typedef struct lm_step_stats { /* CreationStats triangulation.py:49-60 + run_fus
                                 7 rev gather, 8 rev bound points, 9 apply reserve+check,
                                 10 apply commit (plain), 11 apply merges, 12 apply compaction */
   int64_t rev_passes_acting;  /* reverse passes that produced at least one action */
-  int64_t rev_passes_redo;    /* reverse passes that recomputed at least one point */
+  int64_t rev_passes_redo;    /* reverse-pass items re-evaluated after applies */
+  int64_t fuse_bytes_rev;     /* algorithmic bytes of the reverse passes (part of fuse_bytes) */
 } lm_step_stats;
 
 typedef struct lm_candidate { /* MatchCandidate triangulation.py:41-46 */

@@ -750,6 +750,7 @@ __global__ void k_end(DevMap* maps, const StepArgs* args, lm_step_stats** totals
   for (int k = 0; k < 16; ++k) t->fuse_cycles[k] += st->fuse_cycles[k];
   t->rev_passes_acting += st->rev_passes_acting;
   t->rev_passes_redo += st->rev_passes_redo;
+  t->fuse_bytes_rev += st->fuse_bytes_rev;
   t->first_new_id += 1;  // steps accumulated
 }
 
@@ -826,6 +827,7 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   k_fuse_spec<<<dim3((kpkf + 255) / 256, tfuse, n), 256, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;
   k_fuse_rev<<<n, REV_THREADS, rev_smem, ctx->stream>>>(dmaps, dv, rev_smem);
+  if ((rc = mark())) return rc;
   k_fuse_visible<<<dim3((kpkf + 255) / 256, tfuse, n), 256, 0, ctx->stream>>>(dmaps, dv);
   k_end<<<n, 32, 0, ctx->stream>>>(dmaps, dv, ctx->d_totals);
   if ((rc = mark())) return rc;

@@ -1820,6 +1820,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     st->observations_added += cnt[1];
     st->stale += cnt[2];
     st->fuse_bytes += alg;
+    st->fuse_bytes_rev += alg;
     st->fuse_passes += T;
     st->fuse_points += npts;
     st->fuse_actions += nacts;

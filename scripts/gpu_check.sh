@@ -19,7 +19,7 @@ fi
 if has full; then
   # steady-state keyframes: skip the first ~100 keyframes' launches, capture the hot kernels
   timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:'k_match|k_fuse_rev|k_fuse_gather|k_tri|k_commit|k_fuse_apply' --launch-skip 600 --launch-count 12 \
+    -k regex:'k_match|k_fuse_rev|k_fuse_gather|k_fuse_spec|k_tri|k_fuse_apply' --launch-skip 600 --launch-count 12 \
     -o $OUT/full -f python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e > $OUT/full_bench.log 2>&1; echo "full rc=$?"
 fi
 ls -la $OUT
