@@ -72,6 +72,7 @@ struct lm_ctx {
   void* flush_buf = nullptr;
   size_t flush_bytes = 0;
   bool prof = false;
+  int apply_cluster = 8;                // CTAs per map of the forward-apply cluster (LM_APPLY_CLUSTER)
   std::vector<cudaEvent_t> prof_pool;   // free events
   std::vector<std::vector<cudaEvent_t>> prof_steps;  // 9 boundary events per step
 };
@@ -458,6 +459,11 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
   CU(cudaFuncSetAttribute(k_fuse_targets, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
   CU(cudaFuncSetAttribute(k_fuse_rev, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   CU(cudaFuncSetAttribute(k_op, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+  CU(cudaFuncSetAttribute(k_fuse_apply, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  if (const char* e = getenv("LM_APPLY_CLUSTER")) {
+    const int v = atoi(e);
+    ctx->apply_cluster = v < 1 ? 1 : (v > 16 ? 16 : v);
+  }
   *out = ctx;
   return LM_OK;
 }
@@ -820,7 +826,24 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   if ((rc = mark())) return rc;
   k_fuse_gather<<<dim3((tfuse * kpkf + 255) / 256, n), 256, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;
-  k_fuse_apply<<<n, 1024, 0, ctx->stream>>>(dmaps, dv);
+  {
+    // forward apply: one cluster per map, as wide as the batch leaves SMs for
+    int cl = ctx->apply_cluster / n;
+    cl = cl < 1 ? 1 : (cl > ctx->apply_cluster ? ctx->apply_cluster : cl);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(n * cl);
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CU(cudaLaunchKernelEx(&cfg, k_fuse_apply, dmaps, (const StepArgs*)dv));
+  }
   if ((rc = mark())) return rc;
   k_fuse_refresh<<<dim3(148, n), 256, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;

@@ -13,10 +13,14 @@
 //   k_fuse     SearchAndFuse (fusion.py:307-347): targets, forward gather-all/apply-all,
 //              reverse gather/apply per target; one CTA per map
 #pragma once
+#include <cooperative_groups.h>
+
 #include "lm_map.cuh"
 #include "lm_math.cuh"
 
 namespace lm {
+
+namespace cg = cooperative_groups;
 
 struct StepArgs {
   int map;            // index into the context's map table
@@ -925,81 +929,120 @@ __device__ void apply_one(const DevMap& M, const ActRec& x, int* cnt, PairAcc* a
   atomicAdd(&cnt[1], 1);
 }
 
+// A team executes apply_team: one CTA (BlockTeam) or a thread-block cluster (ClusterTeam,
+// control words in the leader CTA's shared memory, reached through distributed shared
+// memory; barrier.cluster orders global and shared::cluster accesses at cluster scope).
+enum TeamCtl { CTL_ROUND = 0, CTL_NPEND, CTL_NMERGE, CTL_NADD, CTL_NDEF, CTL_NREADY, CTL_NGRPM, CTL_TOT = 8,
+               CTL_N = 8 + 16 };
+
 template <int BLOCK>
-__device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh, PairAcc* acc,
-                           long long* tm = nullptr) {
-  __shared__ unsigned round_sh;
-  __shared__ int npend_sh, nmerge_sh, nadd_sh, ndef_sh, nready_sh, ngrpm_sh;
-  for (int a = threadIdx.x; a < n; a += BLOCK) M.s.pend[a] = a;
-  if (threadIdx.x == 0) npend_sh = n;
-  __syncthreads();
-  int rounds = 0;
-  const int lane = threadIdx.x & 31;
-  while (npend_sh > 0) {
-    const int np = npend_sh;
-    if (threadIdx.x == 0) {
-      round_sh = (unsigned)atomicAdd(&M.scal[SC_ROUND], 1) + 1u;
-      nmerge_sh = 0;
-      nadd_sh = 0;
-      ndef_sh = 0;
-      nready_sh = 0;
-      ngrpm_sh = 0;
+struct BlockTeam {
+  int* ctl;
+  int tid, nth;
+  __device__ explicit BlockTeam(int* c) : ctl(c), tid(threadIdx.x), nth(BLOCK) {}
+  __device__ void sync() const { __syncthreads(); }
+  __device__ int excl_scan(int v, int* sh, int& total) const { return block_excl_scan<BLOCK>(v, sh, total); }
+};
+
+template <int BLOCK>
+struct ClusterTeam {
+  int* ctl;
+  int tid, nth, rank, nranks;
+  __device__ ClusterTeam(int* local_ctl) {
+    cg::cluster_group cl = cg::this_cluster();
+    rank = (int)cl.block_rank();
+    nranks = (int)cl.num_blocks();
+    ctl = cl.map_shared_rank(local_ctl, 0);
+    tid = rank * BLOCK + threadIdx.x;
+    nth = nranks * BLOCK;
+  }
+  __device__ void sync() const { cg::this_cluster().sync(); }
+  __device__ int excl_scan(int v, int* sh, int& total) const {
+    int bt;
+    const int at = block_excl_scan<BLOCK>(v, sh, bt);
+    if (threadIdx.x == 0) ctl[CTL_TOT + rank] = bt;
+    sync();
+    int pre = 0, tot = 0;
+    for (int r = 0; r < nranks; ++r) {
+      const int x = ctl[CTL_TOT + r];
+      pre += r < rank ? x : 0;
+      tot += x;
     }
-    __syncthreads();
-    const unsigned rnd = round_sh;
+    sync();  // totals read before the next scan overwrites them
+    total = tot;
+    return pre + at;
+  }
+};
+
+template <class Team>
+__device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh, PairAcc* acc,
+                          long long* tm = nullptr) {
+  int* const ctl = G.ctl;  // team control words (CTL_*), in the team leader's shared memory
+  const int tid = G.tid, nth = G.nth;
+  const int lane = threadIdx.x & 31, gwarp = tid >> 5, nwarps = nth >> 5;
+  for (int a = tid; a < n; a += nth) M.s.pend[a] = a;
+  if (tid == 0) ctl[CTL_NPEND] = n;
+  G.sync();
+  int rounds = 0;
+  while (ctl[CTL_NPEND] > 0) {
+    const int np = ctl[CTL_NPEND];  // (the words reset below were last read before the round's final barrier)
+    if (tid == 0) {
+      ctl[CTL_ROUND] = atomicAdd(&M.scal[SC_ROUND], 1) + 1;
+      ctl[CTL_NMERGE] = 0;
+      ctl[CTL_NADD] = 0;
+      ctl[CTL_NDEF] = 0;
+      ctl[CTL_NREADY] = 0;
+      ctl[CTL_NGRPM] = 0;
+    }
+    G.sync();
+    const unsigned rnd = (unsigned)ctl[CTL_ROUND];
     long long tt = gtime();
-    for (int q = threadIdx.x; q < np; q += BLOCK) {
+    for (int q = tid; q < np; q += nth) {
       const int a = M.s.pend[q];
       const unsigned long long tag = res_tag(rnd, a);
-      for_keys(M, acts[a], [&](int mode, int id) {
+      const ActRec x = acts[a];
+      for_keys(M, x, [&](int mode, int id) {
         reserve_key(M, mode, id, tag);
         return true;
       });
+      // every ADD of this round opens its point's ticket counter (same value for all writers);
+      // the check phase takes tickets with a plain atomicAdd after the barrier
+      if (x.kind == LM_ACT_ADD) M.grp_head[x.pid] = (unsigned long long)rnd << 32;
     }
-    __syncthreads();
+    G.sync();
     // check (read-only): stale actions are counted, merges queued for warps, ADDs take a
     // ticket in their point's group (gtick = round << 32 | members)
-    for (int q = threadIdx.x; q < np; q += BLOCK) {
+    for (int q = tid; q < np; q += nth) {
       const int a = M.s.pend[q];
       const unsigned long long tag = res_tag(rnd, a);
       const ActRec x = acts[a];
       const int ready = for_keys(M, x, [&](int mode, int id) { return holds_key(M, mode, id, tag); });
       M.s.ready[q] = ready;
       if (!ready) continue;
-      atomicAdd(&nready_sh, 1);
+      atomicAdd(&ctl[CTL_NREADY], 1);
       int partner = -1;
       const int kind = classify(M, x, &partner);
       if (kind == 0) {
         atomicAdd(&cnt[2], 1);
       } else if (kind == 1) {
-        const int d = atomicAdd(&ndef_sh, 1);
+        const int d = atomicAdd(&ctl[CTL_NDEF], 1);
         M.s.def[d] = a;
-        unsigned long long v = M.grp_head[x.pid];
-        while (true) {
-          const bool same = (unsigned)(v >> 32) == rnd;
-          const unsigned long long nv = same ? v + 1 : (((unsigned long long)rnd << 32) | 1ull);
-          const unsigned long long old = atomicCAS(&M.grp_head[x.pid], v, nv);
-          if (old == v) {
-            M.s.dnxt[d] = same ? (v & 0xffffffffull) : 0ull;
-            break;
-          }
-          v = old;
-        }
+        M.s.dnxt[d] = atomicAdd(&M.grp_head[x.pid], 1ull) & 0xffffffffull;  // ticket
       } else {
-        const int at = atomicAdd(&nmerge_sh, 1);
+        const int at = atomicAdd(&ctl[CTL_NMERGE], 1);
         M.s.merge_a[at] = x.pid;
         M.s.merge_b[at] = partner;
       }
     }
-    __syncthreads();
-    if (tm && threadIdx.x == 0) {
+    G.sync();
+    if (tm && tid == 0) {
       tm[9] += gtime() - tt;
       tt = gtime();
     }
     // group leaders (ticket 0): a lone low-degree ADD links here (thread), a lone high-degree
     // one goes to a warp; a group of m reserves m entries (base = old length) for its members
-    const int nd = ndef_sh;
-    for (int d = threadIdx.x; d < nd; d += BLOCK) {
+    const int nd = ctl[CTL_NDEF];
+    for (int d = tid; d < nd; d += nth) {
       if (M.s.dnxt[d] != 0ull) continue;
       const ActRec x = acts[M.s.def[d]];
       const int p = x.pid;
@@ -1011,7 +1054,7 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
           M.found[p] += 1;
           atomicAdd(&cnt[1], 1);
         } else {
-          M.s.add_list[atomicAdd(&nadd_sh, 1)] = M.s.def[d];
+          M.s.add_list[atomicAdd(&ctl[CTL_NADD], 1)] = M.s.def[d];
         }
         continue;
       }
@@ -1031,7 +1074,7 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
         M.ocap[p] = nc;
       }
       M.s.gbase[p] = n0;
-      atomicAdd(&ngrpm_sh, m);
+      atomicAdd(&ctl[CTL_NGRPM], m);
       M.nobs[p] = n0 + m;
       M.found[p] += m;
       M.ver[p] += 1;
@@ -1039,14 +1082,14 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
       mark_dirty(M, p);
       atomicAdd(&cnt[1], m);
     }
-    __syncthreads();
-    if (tm && threadIdx.x == 0) {
+    G.sync();
+    if (tm && tid == 0) {
       tm[10] += gtime() - tt;
       tt = gtime();
     }
     // group members: own entry, binding, counter, covisibility with the old observers;
     // warps: lone high-degree ADDs and merges (disjoint entities)
-    for (int d = threadIdx.x; d < nd; d += BLOCK) {
+    for (int d = tid; d < nd; d += nth) {
       const ActRec x = acts[M.s.def[d]];
       const int p = x.pid;
       const int m = (int)(M.grp_head[p] & 0xffffffffull);
@@ -1060,8 +1103,8 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
       for (int k = 0; k < base; ++k) covis_add(M, x.slot, o[k].x, +1, acc);
     }
     {
-      const int nm = nmerge_sh, na = nadd_sh;
-      for (int k = threadIdx.x >> 5; k < na; k += BLOCK / 32) {
+      const int nm = ctl[CTL_NMERGE], na = ctl[CTL_NADD];
+      for (int k = gwarp; k < na; k += nwarps) {
         const ActRec x = acts[M.s.add_list[k]];
         link_warp(M, x.pid, x.slot, x.j, lane, acc);
         if (lane == 0) {
@@ -1069,14 +1112,14 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
           M.found[x.pid] += 1;
         }
       }
-      for (int k = threadIdx.x >> 5; k < nm; k += BLOCK / 32) merge_pair_warp(M, M.s.merge_a[k], M.s.merge_b[k], lane, acc);
-      if (threadIdx.x == 0) cnt[0] += nm;
-      if (threadIdx.x == 32) atomicAdd(&cnt[1], na);
+      for (int k = gwarp; k < nm; k += nwarps) merge_pair_warp(M, M.s.merge_a[k], M.s.merge_b[k], lane, acc);
+      if (tid == 0) atomicAdd(&cnt[0], nm);
+      if (tid == 32) atomicAdd(&cnt[1], na);
     }
-    __syncthreads();
+    G.sync();
     // group members: covisibility with the members of lower ticket (each new pair once)
-    const bool groups = ngrpm_sh > 0;
-    for (int d = threadIdx.x; groups && d < nd; d += BLOCK) {
+    const bool groups = ctl[CTL_NGRPM] > 0;
+    for (int d = tid; groups && d < nd; d += nth) {
       const ActRec x = acts[M.s.def[d]];
       const int p = x.pid;
       const int m = (int)(M.grp_head[p] & 0xffffffffull);
@@ -1086,29 +1129,39 @@ __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt,
       const int tk = (int)M.s.dnxt[d];
       for (int k = 0; k < tk; ++k) covis_add(M, x.slot, o[base + k].x, +1, acc);
     }
-    if (groups) __syncthreads();
-    if (tm && threadIdx.x == 0) {
+    if (groups) G.sync();
+    if (tm && tid == 0) {
       tm[11] += gtime() - tt;
       tt = gtime();
     }
     int kept = 0;
-    const bool all_ready = nready_sh == np;  // (read before any thread can reset it)
-    for (int b0 = 0; !all_ready && b0 < np; b0 += BLOCK) {  // stable compaction of the still-pending actions
-      const int q = b0 + threadIdx.x;
+    const bool all_ready = ctl[CTL_NREADY] == np;
+    for (int b0 = 0; !all_ready && b0 < np; b0 += nth) {  // stable compaction of the still-pending actions
+      const int q = b0 + tid;
       const int keep = q < np ? !M.s.ready[q] : 0;
       const int a = keep ? M.s.pend[q] : 0;
       int tot;
-      const int at = block_excl_scan<BLOCK>(keep, sh, tot);
+      const int at = G.excl_scan(keep, sh, tot);
       if (keep) M.s.pend[kept + at] = a;  // write index <= read index
       kept += tot;
-      __syncthreads();
+      G.sync();
     }
-    if (threadIdx.x == 0) npend_sh = kept;
-    __syncthreads();
-    if (tm && threadIdx.x == 0) tm[12] += gtime() - tt;
+    G.sync();  // all reads of the control words of this round are done
+    if (tid == 0) ctl[CTL_NPEND] = kept;
+    G.sync();
+    if (tm && tid == 0) tm[12] += gtime() - tt;
     if (++rounds > (1 << 20)) break;
   }
   return rounds;
+}
+
+
+template <int BLOCK>
+__device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh, PairAcc* acc,
+                           long long* tm = nullptr) {
+  __shared__ int ctl[CTL_N];
+  const BlockTeam<BLOCK> G(ctl);
+  return apply_team(G, M, acts, n, cnt, sh, acc, tm);
 }
 
 // warp per point of pts[0..P) that is dirty (sort + representative descriptor) or whose
@@ -1416,56 +1469,64 @@ __global__ void __launch_bounds__(256) k_fuse_gather(DevMap* maps, const StepArg
 }
 
 // assemble the forward batch in (target, point) order and apply it
-__global__ void __launch_bounds__(1024) k_fuse_apply(DevMap* maps, const StepArgs* args) {
-  const StepArgs& A = args[blockIdx.x];
+// Forward apply: one thread-block cluster per map (launched with cluster dims; blockIdx.x /
+// cluster size selects the map). The ~4.5k forward actions of a C2 keyframe spread over the
+// cluster's CTAs; the reservation rounds synchronise with barrier.cluster.
+__global__ void __launch_bounds__(1024, 1) k_fuse_apply(DevMap* maps, const StepArgs* args) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int ncl = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  const StepArgs& A = args[blockIdx.x / ncl];
   const DevMap& M = maps[A.map];
   if (!A.do_fuse) return;
   const int T = M.s.fctl[FC_T], P = M.s.fctl[FC_P];
   if (T == 0) return;
   __shared__ int sh[32];
   __shared__ int cnt[3];
+  __shared__ int ctl[CTL_N];
   __shared__ PairAcc acc;
+  __shared__ long long tmf[16];
   const long long t0 = gtime();
   if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
+  if (threadIdx.x < 16) tmf[threadIdx.x] = 0;
   pair_acc_init<1024>(&acc, A.cur);
+  const ClusterTeam<1024> G(ctl);
   const int nb = (T * P + 255) / 256;
   int base = 0;
-  for (int c0 = 0; c0 < nb; c0 += 1024) {  // exclusive scan of the per-CTA counts
+  for (int c0 = 0; c0 < nb; c0 += 1024) {  // exclusive scan of the per-CTA counts (every CTA)
     const int b = c0 + threadIdx.x;
     const int v = b < nb ? M.s.blk_cnt[b] : 0;
     int tot;
     const int at = block_excl_scan<1024>(v, sh, tot);
-    if (b < nb) M.s.blk_off[b] = base + at;
+    if (b < nb && rank == 0) M.s.blk_off[b] = base + at;
     base += tot;
   }
-  __syncthreads();
   const int nact = base;
-  for (int b = threadIdx.x >> 5; b < nb; b += 32) {  // warp per source CTA segment
+  G.sync();
+  for (int b = G.tid >> 5; b < nb; b += G.nth >> 5) {  // warp per source CTA segment
     const int c = M.s.blk_cnt[b], o = M.s.blk_off[b];
     for (int k = threadIdx.x & 31; k < c; k += 32) M.s.acts[o + k] = M.s.acts2[b * 256 + k];
   }
-  __syncthreads();
+  G.sync();
   const long long t1 = gtime();
-  __shared__ long long tmf[16];
-  if (threadIdx.x < 16) tmf[threadIdx.x] = 0;
-  __syncthreads();
-  const int rr = apply_block<1024>(M, M.s.acts, nact, cnt, sh, &acc, tmf);
+  const int rr = apply_team(G, M, M.s.acts, nact, cnt, sh, &acc, rank == 0 ? tmf : nullptr);
   pair_acc_flush<1024>(M, &acc);
+  lm_step_stats* st = M.s.stats;
   if (threadIdx.x == 0) {
-    lm_step_stats* st = M.s.stats;
-    st->merged += cnt[0];
-    st->observations_added += cnt[1];
-    st->stale += cnt[2];
+    atomicAdd(&st->merged, cnt[0]);
+    atomicAdd(&st->observations_added, cnt[1]);
+    atomicAdd(&st->stale, cnt[2]);
+  }
+  if (G.tid == 0) {
     st->fuse_actions += nact;
     st->fuse_bytes += 16LL * nact;
     st->apply_rounds += rr;
     st->fuse_cycles[2] += t1 - t0;
     st->fuse_cycles[3] += gtime() - t1;
-    for (int k = 13; k < 16; ++k) st->fuse_cycles[k] += 0;
     st->fuse_cycles[13] += tmf[9];   // forward: reserve+check
     st->fuse_cycles[14] += tmf[10] + tmf[11];  // forward: commit (plain + merges)
     st->fuse_cycles[15] += tmf[12];  // forward: compaction
   }
+  cl.sync();  // the leader CTA's shared control words stay alive until every CTA is done
 }
 
 // ---------------------------------------------------------------------- reverse passes
