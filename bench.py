@@ -285,8 +285,8 @@ def main():
             v = getattr(totals, f)
             if isinstance(v, int):
                 acc[f] = acc.get(f, 0) + v
-            elif f == "fuse_cycles":
-                acc[f] = [a + b for a, b in zip(acc.get(f, [0] * 16), list(v))]
+            elif f in ("fuse_cycles", "dbg"):
+                acc[f] = [a + b for a, b in zip(acc.get(f, [0] * len(v)), list(v))]
     launches = lib.lm_launch_count(ctx.h) - launches0
     clocks = sampler.stop()
     prof_ms = (C.c_double * 16)()
@@ -367,8 +367,17 @@ def main():
                               "apply_rounds": acc["apply_rounds"] / args.steps,
                               "rev_passes": (acc["fuse_passes"] / args.steps) / 2,
                               "rev_passes_acting": acc["rev_passes_acting"] / args.steps,
-                              "rev_passes_rescanned": acc["rev_passes_redo"] / args.steps,
-                              "rev_points_recomputed": acc["fuse_cycles"][1] / args.steps},
+                              "rev_items_reevaluated": acc["rev_passes_redo"] / args.steps,
+                              "rev_acting_passes_untouched_by_previous_apply": acc["rev_mergeable"] / args.steps,
+                              "rev_points_recomputed": acc["fuse_cycles"][1] / args.steps,
+                              "rev_touched_point_cycles": {"refresh": acc["dbg"][0] / max(acc["dbg"][3], 1),
+                                                           "geometry": acc["dbg"][1] / max(acc["dbg"][3], 1),
+                                                           "hit": acc["dbg"][2] / max(acc["dbg"][3], 1),
+                                                           "points": acc["dbg"][3] / args.steps},
+                              "rev_subphase_ms": {"select_actions_preitems": acc["dbg"][7] / args.steps / 1e6,
+                                                  "postitems_changed": acc["dbg"][4] / args.steps / 1e6,
+                                                  "hitlist": acc["dbg"][5] / args.steps / 1e6,
+                                                  "refresh_hits": acc["dbg"][6] / args.steps / 1e6}},
             "fuse_phase_ms_per_step": {n: acc["fuse_cycles"][k] / args.steps / 1e6
                                        for k, n in enumerate(["targets", "-", "fwd_assemble", "fwd_apply",
                                                               "rev_redo_refresh", "rev_redo_gather", "rev_apply",

@@ -562,9 +562,10 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(s.pass_j, d.kpkf_max); A(s.add_list, (size_t)s.act_cap);
   A(s.def, (size_t)s.act_cap); A(s.dnxt, (size_t)s.act_cap); A(s.gbase, MP);
   A(s.pinfo, 3 * TMAX); A(s.hitpass, (size_t)d.kpkf_max * ((TMAX + 31) / 32)); A(s.pj, (size_t)s.act_cap);
-  A(s.pass_of, K); A(s.snap, d.kpkf_max); A(s.rmark, MP);
+  A(s.pass_of, K); A(s.snap, d.kpkf_max); A(s.chg, d.kpkf_max); A(s.rmark, MP);
   A(s.pmp, (size_t)s.act_cap); A(s.pob, (size_t)s.act_cap); A(s.itag, (size_t)s.act_cap); A(s.ilist, (size_t)s.act_cap);
   A(s.cands, (size_t)s.act_cap); A(s.hl_cnt, d.kpkf_max); A(s.hl, (size_t)d.kpkf_max * HL); A(s.hreg, MP);
+  A(s.abits, (size_t)TMAX * ((d.kpkf_max + 31) / 32));
   A(m->d_stats, 1); A(m->d_totals, 1); A(m->d_result, 4 + 1024 + TMAX);
 #undef A
   s.stats = m->d_stats;
@@ -757,6 +758,8 @@ __global__ void k_end(DevMap* maps, const StepArgs* args, lm_step_stats** totals
   t->rev_passes_acting += st->rev_passes_acting;
   t->rev_passes_redo += st->rev_passes_redo;
   t->fuse_bytes_rev += st->fuse_bytes_rev;
+  t->rev_mergeable += st->rev_mergeable;
+  for (int k = 0; k < 8; ++k) t->dbg[k] += st->dbg[k];
   t->first_new_id += 1;  // steps accumulated
 }
 

@@ -1551,7 +1551,7 @@ __global__ void __launch_bounds__(1024, 1) k_fuse_apply(DevMap* maps, const Step
 // k_fuse_visible follows the loser -> winner records of this step (mrg, SC_MTAG).
 
 constexpr int HPW = (TMAX + 31) / 32;  // words of the per-current-keypoint pass bitmap
-constexpr int REV_THREADS = 1024;      // k_fuse_rev block
+constexpr int REV_THREADS = 512;       // k_fuse_rev block (128 registers: the register-resident refresh must not spill)
 enum PassInfo { PI_NACT = 0, PI_LIVE = 1, PI_OBS = 2, PI_N = 3 };
 
 // warp per point touched since the last refresh: representative descriptor + geometry cache;
@@ -1565,6 +1565,8 @@ __global__ void __launch_bounds__(256) k_fuse_refresh(DevMap* maps, const StepAr
     for (int k = tid; k < PI_N * TMAX; k += nth) M.s.pinfo[k] = 0;
     for (int k = tid; k < M.kpkf_max * HPW; k += nth) M.s.hitpass[k] = 0u;
     for (int k = tid; k < M.kpkf_max; k += nth) M.s.hl_cnt[k] = 0;
+    const int aw_all = M.s.fctl[FC_T] * ((M.kpkf_max + 31) >> 5);
+    for (int k = tid; k < aw_all; k += nth) M.s.abits[k] = 0u;
     if (tid == 0) M.scal[SC_MTAG] += 1;  // merges of this step's reverse phase
   }
   const int n = M.scal[SC_DIRTY_N];
@@ -1647,6 +1649,7 @@ __global__ void __launch_bounds__(256) k_fuse_spec(DevMap* maps, const StepArgs*
     }
     const ItemVal v = eval_item(M, A.cur, t, ts, kp);
     store_item(M, (size_t)t * M.kpkf_max + kp, v);
+    if (v.has) atomicOr(&M.s.abits[(size_t)t * ((M.kpkf_max + 31) >> 5) + (kp >> 5)], 1u << (kp & 31));
     live = v.mp >= 0;
     nob = v.nob;
     has = v.has;
@@ -1700,7 +1703,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   __shared__ long long tm[16];
   __shared__ PairAcc acc;
   __shared__ int s_nact[TMAX], s_live[TMAX], s_obs[TMAX];
-  __shared__ int t1_sh, nc_sh, ni_sh, tag_sh;
+  __shared__ int t1_sh, nc_sh, ni_sh, tag_sh, tmin_sh, na_sh, nchg_sh;
   __shared__ double cur_pose[22];  // R, t, C, cam, cell size of the current keyframe
   if (threadIdx.x < 22) {
     const int c = A.cur, k = threadIdx.x;
@@ -1714,7 +1717,13 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   const lm_fuse_cfg& fc = A.fc;
   if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
   if (threadIdx.x < 16) tm[threadIdx.x] = 0;
-  if (threadIdx.x == 0) M.scal[SC_DIRTY_N] = 0;  // k_fuse_refresh consumed the list
+  if (threadIdx.x == 0) {
+    M.scal[SC_DIRTY_N] = 0;  // k_fuse_refresh consumed the list
+    nc_sh = 0;
+    ni_sh = 0;
+    nchg_sh = 0;
+    tmin_sh = 0x7fffffff;
+  }
   for (int t = threadIdx.x; t < T; t += REV_THREADS) {
     s_nact[t] = M.s.pinfo[PI_NACT * TMAX + t];
     s_live[t] = M.s.pinfo[PI_LIVE * TMAX + t];
@@ -1724,68 +1733,95 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   pair_acc_init<REV_THREADS>(&acc, A.cur);  // (barrier)
   const unsigned long long mpb = M.mp_rec_bytes;
   long long alg = 0, npts = 0, nacts = 0, ledger_events = 0;
-  int rounds = 0, pass_act = 0, reeval = 0, redo_pts = 0;
+  int rounds = 0, pass_act = 0, reeval = 0, redo_pts = 0, mergeable = 0, touched_min = 0x7fffffff;
   int t0 = 0;
   // append item (t, kp) to the re-evaluation list once per tag
   auto add_item = [&](int t, int kp, int tag) {
     const size_t it = (size_t)t * K + kp;
     if (atomicExch(&M.s.itag[it], tag) != tag) M.s.ilist[atomicAdd(&ni_sh, 1)] = (int)it;
   };
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int AW = (K + 31) >> 5;  // words of a pass's action bitmap
   while (true) {
-    // (1) first pass (>= t0) with actions; ledger / byte accounting of the passes before it
-    if (threadIdx.x == 0) t1_sh = T;
-    __syncthreads();
-    for (int t = t0 + threadIdx.x; t < T; t += REV_THREADS)
-      if (s_nact[t] > 0) atomicMin(&t1_sh, t);
+    // (1) warp 0: first pass (>= t0) with actions, ledger / byte accounting of the passes
+    //     before it, that pass's actions in keypoint order (from its action bitmap), and the
+    //     touched points (action points + current owners of the hit keypoints, deduplicated).
+    //     The other warps snapshot the current keyframe's bindings.
+    const long long ta = gtime();
+    if (wid == 0) {
+      int t1 = T;
+      for (int tb = t0; tb < T; tb += 32) {
+        const unsigned bal = __ballot_sync(0xffffffffu, tb + lane < T && s_nact[tb + lane] > 0);
+        if (bal) {
+          t1 = tb + __ffs(bal) - 1;
+          break;
+        }
+      }
+      const int te = t1 < T ? t1 : T - 1;
+      long long a_b = 0, a_p = 0, a_n = 0;
+      for (int t = t0 + lane; t <= te; t += 32) {
+        a_b += pass_bytes(s_live[t], s_obs[t], ncur, s_nact[t]);
+        a_p += s_live[t];
+        a_n += s_nact[t];
+      }
+      for (int off = 16; off; off >>= 1) {
+        a_b += __shfl_xor_sync(0xffffffffu, a_b, off);
+        a_p += __shfl_xor_sync(0xffffffffu, a_p, off);
+        a_n += __shfl_xor_sync(0xffffffffu, a_n, off);
+      }
+      alg += a_b;  // (meaningful on thread 0)
+      npts += a_p;
+      nacts += a_n;
+      ledger_events += te - t0 + 1;
+      int na = 0, tag = 0;
+      if (lane == 0) tag = atomicAdd(&M.scal[SC_ROUND], 1) + 1;
+      const int tg = __shfl_sync(0xffffffffu, tag, 0);
+      if (t1 < T) {
+        const unsigned* bits = M.s.abits + (size_t)t1 * AW;
+        const ActRec* seg = M.s.acts2 + (size_t)t1 * K;
+        for (int wb = 0; wb < AW; wb += 32) {
+          const int w = wb + lane;
+          unsigned bw = w < AW ? bits[w] : 0u;
+          const int c = __popc(bw);
+          int pre = c;
+          for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, pre, off);
+            if (lane >= off) pre += y;
+          }
+          int at = na + pre - c;
+          while (bw) {
+            const int kp = 32 * w + __ffs(bw) - 1;
+            bw &= bw - 1;
+            const ActRec x = seg[kp];
+            M.s.acts[at++] = ActRec{cur, x.pid, x.j, x.other, x.kind};
+          }
+          na += __shfl_sync(0xffffffffu, pre, 31);
+        }
+        __syncwarp();
+        for (int k = lane; k < na; k += 32) {
+          const ActRec x = M.s.acts[k];
+          const int cand[3] = {x.pid, x.other, M.kbind[cur_off + x.j]};
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const int p = cand[c];
+            if (p >= 0 && atomicExch(&M.s.rmark[p], tg) != tg) M.s.cands[atomicAdd(&nc_sh, 1)] = p;
+          }
+        }
+      }
+      if (lane == 0) {
+        t1_sh = t1;
+        na_sh = na;
+        tag_sh = tg;
+      }
+    } else {
+      for (int k = threadIdx.x - 32; k < ncur; k += REV_THREADS - 32) M.s.snap[k] = M.kbind[cur_off + k];
+    }
     __syncthreads();
     const int t1 = t1_sh;
-    if (threadIdx.x == 0) {
-      const int te = t1 < T ? t1 : T - 1;
-      for (int t = t0; t <= te; ++t) {  // ledger totals land once, after the loop
-        const int Pt = s_live[t];
-        alg += pass_bytes(Pt, s_obs[t], ncur, s_nact[t]);
-        npts += Pt;
-        nacts += s_nact[t];
-      }
-      ledger_events += te - t0 + 1;
-    }
     if (t1 >= T) break;
+    if (pass_act > 0) mergeable += touched_min > t1;
     ++pass_act;
-    // (2) pass t1's actions in keypoint order; current-keyframe snapshot; touched points
-    //     (action points + current owners of the hit keypoints) and their items before
-    const long long ta = gtime();
-    if (threadIdx.x == 0) {
-      nc_sh = 0;
-      ni_sh = 0;
-      tag_sh = atomicAdd(&M.scal[SC_ROUND], 1) + 1;
-    }
-    int na = 0;
-    const int n1 = M.kp_n[M.s.targets[t1]];
-    for (int b0 = 0; b0 < n1; b0 += REV_THREADS) {
-      const int kp = b0 + threadIdx.x;
-      ActRec x{0, 0, 0, 0, 0};
-      if (kp < n1) x = M.s.acts2[(size_t)t1 * K + kp];
-      const int has = kp < n1 && x.kind != 0;
-      int tot;
-      const int at = block_excl_scan<REV_THREADS>(has, sh, tot);  // (barriers)
-      if (has) M.s.acts[na + at] = ActRec{cur, x.pid, x.j, x.other, x.kind};
-      na += tot;
-    }
-    for (int k = threadIdx.x; k < ncur; k += REV_THREADS) M.s.snap[k] = M.kbind[cur_off + k];
-    __syncthreads();
-    const int tag = tag_sh;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int k = threadIdx.x; k < na; k += REV_THREADS) {
-      const ActRec x = M.s.acts[k];
-      const int cand[3] = {x.pid, x.other, M.s.snap[x.j]};
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int p = cand[c];
-        if (p >= 0 && atomicExch(&M.s.rmark[p], tag) != tag) M.s.cands[atomicAdd(&nc_sh, 1)] = p;
-      }
-    }
-    __syncthreads();
-    const int ncand = nc_sh;
+    const int na = na_sh, tag = tag_sh, ncand = nc_sh;
     // items of point p (its current observations) in passes after t1; warp-cooperative
     auto add_point_items = [&](int p) {
       const int2* o = M.obs + M.ooff[p];
@@ -1798,36 +1834,28 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     };
     for (int k = wid; k < ncand; k += REV_THREADS / 32) add_point_items(M.s.cands[k]);  // before the apply
     __syncthreads();
+    if (threadIdx.x == 0) tm[7] += gtime() - ta;
     rounds += apply_block<REV_THREADS>(M, M.s.acts, na, cnt, sh, &acc, tm);  // (barriers)
     if (threadIdx.x == 0) tm[2] += gtime() - ta;
-    // (3) touched points: refresh + new hits; then the points hitting a current keypoint
-    //     whose binding changed (hit list; a keypoint whose list overflowed falls back to
-    //     scanning the passes of its bitmap); then the items of all of them after the apply
+    // (2) after the apply: the touched points' items, and the points hitting a current
+    //     keypoint whose binding changed (hit list; a keypoint whose list overflowed falls
+    //     back to scanning the passes of its bitmap) join the touched list
     const long long tv = gtime();
-    redo_pts += ncand;
-    refresh_points<REV_THREADS>(M, M.s.cands, ncand, sh);  // (barriers)
-    const long long t6 = gtime();
-    for (int k = threadIdx.x; k < ncand; k += REV_THREADS) {
-      const int p = M.s.cands[k];
-      if (!M.alive[p]) continue;
-      PGeo g;
-      point_geometry(M, p, fc.dist_band_slack, g);
-      const int j = gather_hit(M, fc, g, cur, TV);
-      M.hit[p] = make_int2(M.ver[p], j);
-      hit_list_add(M, j, p);
-    }
+    for (int k = wid; k < ncand; k += REV_THREADS / 32) add_point_items(M.s.cands[k]);
+    for (int k = threadIdx.x; k < ncur; k += REV_THREADS)  // current keypoints whose binding changed
+      if (M.kbind[cur_off + k] != M.s.snap[k]) M.s.chg[atomicAdd(&nchg_sh, 1)] = k;
     __syncthreads();
-    if (threadIdx.x == 0) {
-      tm[0] += t6 - tv;
-      tm[1] += gtime() - t6;
-    }
-    for (int k = wid; k < ncur; k += REV_THREADS / 32) {
-      if (M.kbind[cur_off + k] == M.s.snap[k]) continue;
+    if (threadIdx.x == 0) tm[4] += gtime() - tv;
+    const long long tv2 = gtime();
+    const int nchg = nchg_sh;
+    for (int q = wid; q < nchg; q += REV_THREADS / 32) {
+      const int k = M.s.chg[q];
       const int c = M.s.hl_cnt[k];
       if (c <= HL) {
         if (lane < c) {
           const int p = M.s.hl[k * HL + lane];
-          if (M.alive[p] && M.hit[p].y == k && M.s.rmark[p] != tag) M.s.cands[atomicAdd(&nc_sh, 1)] = p;
+          if (M.alive[p] && M.hit[p].y == k && atomicExch(&M.s.rmark[p], tag) != tag)
+            M.s.cands[atomicAdd(&nc_sh, 1)] = p;
         }
         continue;
       }
@@ -1845,12 +1873,49 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       }
     }
     __syncthreads();
-    {
-      const int nall = nc_sh;
-      for (int k = wid; k < nall; k += REV_THREADS / 32) add_point_items(M.s.cands[k]);
+    if (threadIdx.x == 0) tm[5] += gtime() - tv2;
+    const long long tv3 = gtime();
+    // (3) touched points, warp each: refresh (descriptor + geometry) where stale, then the new
+    //     hit (lane 0); the hit-list points' items (their state is unchanged)
+    const int nall = nc_sh;
+    redo_pts += ncand;
+    for (int k = wid; k < nall; k += REV_THREADS / 32) {
+      const int p = M.s.cands[k];
+      if (k < ncand) {
+        if (!M.alive[p]) continue;
+        const long long c0 = clock64();
+        if (M.dirty[p]) {
+          refresh_rep_warp(M, p, lane);
+          if (lane == 0) M.dirty[p] = 0;
+          __syncwarp();
+        }
+        const long long c1 = clock64();
+        if (!M.gval[p]) geo_full_warp(M, p, lane);
+        const long long c2 = clock64();
+        if (lane == 0) {
+          PGeo g;
+          point_geometry(M, p, fc.dist_band_slack, g);
+          const int j = gather_hit(M, fc, g, cur, TV);
+          M.hit[p] = make_int2(M.ver[p], j);
+          hit_list_add(M, j, p);
+          const long long c3 = clock64();
+          unsigned long long* dbg = (unsigned long long*)M.s.stats->dbg;  // diagnostics (cycles)
+          atomicAdd(&dbg[0], (unsigned long long)(c1 - c0));
+          atomicAdd(&dbg[1], (unsigned long long)(c2 - c1));
+          atomicAdd(&dbg[2], (unsigned long long)(c3 - c2));
+          atomicAdd(&dbg[3], 1ull);
+        }
+        __syncwarp();
+      } else {
+        add_point_items(p);
+      }
     }
     __syncthreads();
-    // (4) re-evaluate the listed items; pass totals by deltas
+    if (threadIdx.x == 0) {
+      tm[0] += gtime() - tv;
+      tm[6] += gtime() - tv3;
+    }
+    // (5) re-evaluate the listed items; pass totals by deltas, action bitmaps toggled
     const long long t7 = gtime();
     const int ni = ni_sh;
     reeval += ni;
@@ -1863,10 +1928,21 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       const int dl = (v.mp >= 0) - (oj != -3), dob = v.nob - ob, da = v.has - oa;
       if (dl) atomicAdd(&s_live[t], dl);
       if (dob) atomicAdd(&s_obs[t], dob);
-      if (da) atomicAdd(&s_nact[t], da);
+      if (da) {
+        atomicAdd(&s_nact[t], da);
+        atomicXor(&M.s.abits[(size_t)t * AW + (kp >> 5)], 1u << (kp & 31));
+      }
+      atomicMin(&tmin_sh, t);
     }
     __syncthreads();
-    if (threadIdx.x == 0) tm[3] += gtime() - t7;
+    touched_min = tmin_sh;
+    if (threadIdx.x == 0) {
+      tm[3] += gtime() - t7;
+      nc_sh = 0;  // counters of the next iteration (read above, before this barrier)
+      ni_sh = 0;
+      nchg_sh = 0;
+      tmin_sh = 0x7fffffff;
+    }
     t0 = t1 + 1;
   }
   pair_acc_flush<REV_THREADS>(M, &acc);
@@ -1894,6 +1970,8 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     st->fuse_cycles[1] += redo_pts;  // touched points recomputed (count, not ns)
     st->rev_passes_acting += pass_act;
     st->rev_passes_redo += reeval;   // re-evaluated items (count)
+    st->rev_mergeable += mergeable;
+    for (int k = 4; k < 8; ++k) st->dbg[k] += tm[k];
   }
 }
 

@@ -111,6 +111,7 @@ struct Scratch {
   int* pj;               // [TMAX*kpkf_max] per (pass, keypoint): resolved hit (-3 not bound)
   int* pass_of;          // [kf_cap] keyframe slot -> pass index (-1)
   int* snap;             // [kpkf_max] current keyframe bindings before an apply
+  int* chg;              // [kpkf_max] current keypoints whose binding an apply changed
   int* rmark;            // [mp_cap] dedup tag of the touched-point list
   int* pmp;              // [TMAX*kpkf_max] per (pass, keypoint): bound live point at evaluation
   int* pob;              // [TMAX*kpkf_max] per (pass, keypoint): its observation count then
@@ -120,6 +121,7 @@ struct Scratch {
   int* hl_cnt;           // [kpkf_max] per current keypoint: points whose hit is it (count)
   int* hl;               // [kpkf_max*HL] ... (ids; entries whose hit moved are skipped)
   int* hreg;             // [mp_cap] step tag: point already listed by the speculative scan
+  unsigned* abits;       // [TMAX*ceil(kpkf_max/32)] per pass: keypoints whose item has an action
   int* act_flag;         // [TMAX*kpkf_max]
   int* vis_flag;         // [TMAX*kpkf_max]
   int pts_cap;
