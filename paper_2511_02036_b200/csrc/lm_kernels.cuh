@@ -716,8 +716,15 @@ __device__ __forceinline__ TgtView tgt_global(const DevMap& M, int ts) {
 // project + gates + grid window search for one (point, target) pair (fusion.py:97-129,
 // 178-196). Returns -2 if the point is not visible in the target, -1 if visible without a
 // hit, else the hit keypoint (lowest (distance, index) within the window).
-__device__ int gather_hit(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g, int ts, const TgtView& T) {
-  if (!g.ok) return -2;
+// projection, gates and the conservative cell window of one (point, target) pair
+struct GWin {
+  double u, v, r2;
+  int lp, x0, x1, y0, y1;
+};
+
+__device__ __forceinline__ bool gather_window(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g, int ts,
+                                              const TgtView& T, GWin& w) {
+  if (!g.ok) return false;
   const double* R = T.pose ? T.pose : M.R + 9 * ts;
   const double* t = T.pose ? T.pose + 9 : M.t + 3 * ts;
   const double* C = T.pose ? T.pose + 12 : M.C + 3 * ts;
@@ -731,42 +738,75 @@ __device__ int gather_hit(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g,
   const bool inview = zc > 0 && u >= 0 && u < cam[4] && v >= 0 && v < cam[5];
   const double dx = g.x - C[0], dy = g.y - C[1], dz = g.z - C[2];
   const double d = sqrt(dx * dx + dy * dy + dz * dz);
-  if (!(zc > 0 && inview && d >= g.blo && d <= g.bhi)) return -2;
+  if (!(zc > 0 && inview && d >= g.blo && d <= g.bhi)) return false;
   const double cosv = (dx * g.vx + dy * g.vy + dz * g.vz) / d;
-  if (!(cosv >= fc.min_view_cos)) return -2;
+  if (!(cosv >= fc.min_view_cos)) return false;
   double lraw = log(d / g.d0) / M.log_sf;
   if (!isfinite(lraw)) lraw = 0.0;
   double lr = rint(lraw);
   lr = lr < 0 ? 0 : (lr > M.L - 1 ? M.L - 1 : lr);
-  const int lp = (int)lr;
-  const double rad = fc.fuse_radius * M.S[lp];
+  w.lp = (int)lr;
+  const double rad = fc.fuse_radius * M.S[w.lp];
   // conservative cell window, exact test inside
   const double cs = T.pose ? T.pose[21] : M.g_cs[ts];
   const int nx = T.nx, ny = T.ny;
   int x0 = (int)floor((u - rad - 1.0) / cs), x1 = (int)floor((u + rad + 1.0) / cs);
   int y0 = (int)floor((v - rad - 1.0) / cs), y1 = (int)floor((v + rad + 1.0) / cs);
-  x0 = x0 < 0 ? 0 : x0;
-  y0 = y0 < 0 ? 0 : y0;
-  x1 = x1 > nx - 1 ? nx - 1 : x1;
-  y1 = y1 > ny - 1 ? ny - 1 : y1;
-  const double r2 = rad * rad;
-  unsigned long long best = ~0ull;
-  for (int cy = y0; cy <= y1; ++cy) {
-    for (int cx = x0; cx <= x1; ++cx) {
-      const int cell = cy * nx + cx;
-      for (int it = T.cst[cell]; it < T.cst[cell + 1]; ++it) {
-        const int k = T.items[it];
-        const double du = T.u[k] - u, dv = T.v[k] - v;
-        const int dl = (int)T.lev[k] - lp;
-        if (du * du + dv * dv <= r2 && (dl < 0 ? -dl : dl) <= fc.level_window) {
-          const int dist = hamming(T.desc[2 * k], T.desc[2 * k + 1], g.r0, g.r1);
-          if (dist <= fc.match_max_distance) {
-            const unsigned long long key = ((unsigned long long)dist << 32) | (unsigned)k;
-            best = key < best ? key : best;
-          }
-        }
-      }
+  w.x0 = x0 < 0 ? 0 : x0;
+  w.y0 = y0 < 0 ? 0 : y0;
+  w.x1 = x1 > nx - 1 ? nx - 1 : x1;
+  w.y1 = y1 > ny - 1 ? ny - 1 : y1;
+  w.u = u;
+  w.v = v;
+  w.r2 = rad * rad;
+  return true;
+}
+
+// exact radius / level test + Hamming of one window candidate k; folds (dist, k) into best
+__device__ __forceinline__ void gather_test(const lm_fuse_cfg& fc, const PGeo& g, const TgtView& T, const GWin& w,
+                                            int k, unsigned long long& best) {
+  const double du = T.u[k] - w.u, dv = T.v[k] - w.v;
+  const int dl = (int)T.lev[k] - w.lp;
+  if (du * du + dv * dv <= w.r2 && (dl < 0 ? -dl : dl) <= fc.level_window) {
+    const int dist = hamming(T.desc[2 * k], T.desc[2 * k + 1], g.r0, g.r1);
+    if (dist <= fc.match_max_distance) {
+      const unsigned long long key = ((unsigned long long)dist << 32) | (unsigned)k;
+      best = key < best ? key : best;
     }
+  }
+}
+
+// project + gates + grid window search for one (point, target) pair (fusion.py:97-129,
+// 178-196). Returns -2 if the point is not visible in the target, -1 if visible without a
+// hit, else the hit keypoint (lowest (distance, index) within the window).
+__device__ int gather_hit(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g, int ts, const TgtView& T) {
+  GWin w;
+  if (!gather_window(M, fc, g, ts, T, w)) return -2;
+  unsigned long long best = ~0ull;
+  for (int cy = w.y0; cy <= w.y1; ++cy)
+    for (int cx = w.x0; cx <= w.x1; ++cx) {
+      const int cell = cy * T.nx + cx;
+      for (int it = T.cst[cell]; it < T.cst[cell + 1]; ++it) gather_test(fc, g, T, w, T.items[it], best);
+    }
+  return best == ~0ull ? -1 : (int)(best & 0xffffffffu);
+}
+
+// the same, warp-cooperative (every lane passes the same point): lane per window cell, so
+// the Hamming popcounts of the candidates run side by side instead of on one lane
+__device__ int gather_hit_warp(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g, int ts, const TgtView& T,
+                               int lane) {
+  GWin w;
+  if (!gather_window(M, fc, g, ts, T, w)) return -2;
+  const int wx = w.x1 - w.x0 + 1, nc = wx * (w.y1 - w.y0 + 1);
+  unsigned long long best = ~0ull;
+  for (int c = lane; c < nc; c += 32) {
+    const int cy = w.y0 + c / wx, cx = w.x0 + c % wx;
+    const int cell = cy * T.nx + cx;
+    for (int it = T.cst[cell]; it < T.cst[cell + 1]; ++it) gather_test(fc, g, T, w, T.items[it], best);
+  }
+  for (int off = 16; off; off >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(0xffffffffu, best, off);
+    best = o < best ? o : best;
   }
   return best == ~0ull ? -1 : (int)(best & 0xffffffffu);
 }
@@ -1892,10 +1932,10 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
         const long long c1 = clock64();
         if (!M.gval[p]) geo_full_warp(M, p, lane);
         const long long c2 = clock64();
+        PGeo g;
+        point_geometry(M, p, fc.dist_band_slack, g);  // (every lane: same loads, broadcast)
+        const int j = gather_hit_warp(M, fc, g, cur, TV, lane);
         if (lane == 0) {
-          PGeo g;
-          point_geometry(M, p, fc.dist_band_slack, g);
-          const int j = gather_hit(M, fc, g, cur, TV);
           M.hit[p] = make_int2(M.ver[p], j);
           hit_list_add(M, j, p);
           const long long c3 = clock64();

@@ -888,6 +888,112 @@ __device__ void refresh_rep_planes(const DevMap& M, int mp, int n, int lane) {
   __syncwarp();
 }
 
+// Symmetric variant of refresh_rep_planes: d(a, b) = d(b, a), so every unordered pair is
+// popcounted once. Row slot s of lane l is observation 32*s + l. Diagonal blocks (s, s):
+// in step r (1..16) lane l computes d(l, l+r mod 32) for its own row and hands it to lane
+// l+r (shuffle) for that lane's row; off-diagonal blocks (s1 < s2): in step r (0..31) lane l
+// computes d(32*s1 + l, 32*s2 + (l+r mod 32)) and hands it to lane l+r's row slot s2. Half the
+// popcounts of the row-by-row version (the pipe that bounds it, 16 lanes/clk/SM).
+template <int NW>
+__device__ void refresh_rep_sym(const DevMap& M, int mp, int n, int lane) {
+  int2* o = M.obs + M.ooff[mp];
+  int2 e[NW];
+  long long key[NW];
+  uint4 d0[NW], d1[NW];
+#pragma unroll
+  for (int s = 0; s < NW; ++s) e[s] = s * 32 + lane < n ? o[s * 32 + lane] : make_int2(0, 0);
+#pragma unroll
+  for (int s = 0; s < NW; ++s) {
+    const bool act = s * 32 + lane < n;
+    key[s] = act ? M.kf_id[e[s].x] : 0x7fffffffffffffffll;
+    const int g = M.kp_off[e[s].x] + e[s].y;
+    d0[s] = act ? M.kdesc[2 * g] : make_uint4(0, 0, 0, 0);
+    d1[s] = act ? M.kdesc[2 * g + 1] : make_uint4(0, 0, 0, 0);
+  }
+  int rk[NW];
+#pragma unroll
+  for (int s = 0; s < NW; ++s) rk[s] = 0;
+#pragma unroll
+  for (int sb = 0; sb < NW; ++sb)
+#pragma unroll 4
+    for (int l = 0; l < 32; ++l) {
+      const long long kb = __shfl_sync(0xffffffffu, key[sb], l);
+#pragma unroll
+      for (int s = 0; s < NW; ++s) rk[s] += kb < key[s];
+    }
+  __syncwarp();
+#pragma unroll
+  for (int s = 0; s < NW; ++s)
+    if (s * 32 + lane < n) o[rk[s]] = e[s];
+  unsigned pl[NW][9][NW];  // [row slot][bit][column word]
+#pragma unroll
+  for (int s = 0; s < NW; ++s)
+#pragma unroll
+    for (int bit = 0; bit < 9; ++bit)
+#pragma unroll
+      for (int w = 0; w < NW; ++w) pl[s][bit][w] = 0u;
+#pragma unroll
+  for (int s1 = 0; s1 < NW; ++s1)
+#pragma unroll
+    for (int s2 = s1; s2 < NW; ++s2) {
+      const int r0 = s1 == s2 ? 1 : 0, r1 = s1 == s2 ? 16 : 31;
+#pragma unroll 2
+      for (int r = r0; r <= r1; ++r) {
+        const int src = (lane + r) & 31, from = (lane - r) & 31;
+        uint4 b0, b1;
+        b0.x = __shfl_sync(0xffffffffu, d0[s2].x, src);
+        b0.y = __shfl_sync(0xffffffffu, d0[s2].y, src);
+        b0.z = __shfl_sync(0xffffffffu, d0[s2].z, src);
+        b0.w = __shfl_sync(0xffffffffu, d0[s2].w, src);
+        b1.x = __shfl_sync(0xffffffffu, d1[s2].x, src);
+        b1.y = __shfl_sync(0xffffffffu, d1[s2].y, src);
+        b1.z = __shfl_sync(0xffffffffu, d1[s2].z, src);
+        b1.w = __shfl_sync(0xffffffffu, d1[s2].w, src);
+        const unsigned dist = (unsigned)hamming(d0[s1], d1[s1], b0, b1);  // d(32*s1+lane, 32*s2+src)
+        const unsigned got = __shfl_sync(0xffffffffu, dist, from);       // d(32*s1+from, 32*s2+lane)
+#pragma unroll
+        for (int bit = 0; bit < 9; ++bit) {
+          pl[s1][bit][s2] |= ((dist >> bit) & 1u) << src;
+          if (!(s1 == s2 && r == 16)) pl[s2][bit][s1] |= ((got >> bit) & 1u) << from;
+        }
+      }
+    }
+  const int m = n - 1, k0 = (m - 1) >> 1, k1 = m >> 1;
+  unsigned best = 0xffffffffu;
+#pragma unroll
+  for (int s = 0; s < NW; ++s) {
+    const int i = s * 32 + lane;
+    if (i < n) {
+      unsigned cand[NW];
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {  // the other real observations
+        const int lo = w * 32;
+        unsigned msk = n - lo >= 32 ? 0xffffffffu : (n - lo <= 0 ? 0u : (1u << (n - lo)) - 1u);
+        if (i >= lo && i < lo + 32) msk &= ~(1u << (i - lo));
+        cand[w] = msk;
+      }
+      unsigned c2[NW];
+#pragma unroll
+      for (int w = 0; w < NW; ++w) c2[w] = cand[w];
+      const int v0 = plane_select<NW>(pl[s], cand, k0);
+      const int v1 = k1 == k0 ? v0 : plane_select<NW>(pl[s], c2, k1);
+      const unsigned kk = ((unsigned)(v0 + v1) << 16) | (unsigned)rk[s];
+      best = kk < best ? kk : best;
+    }
+  }
+  for (int off = 16; off; off >>= 1) {
+    const unsigned other = __shfl_xor_sync(0xffffffffu, best, off);
+    best = other < best ? other : best;
+  }
+#pragma unroll
+  for (int s = 0; s < NW; ++s)
+    if (s * 32 + lane < n && rk[s] == (int)(best & 0xffffu)) {
+      M.rep[2 * mp] = d0[s];
+      M.rep[2 * mp + 1] = d1[s];
+    }
+  __syncwarp();
+}
+
 // refresh for 32 < n <= 32*NS observations: lane l holds observations l, l+32, ...
 // (entry, key, descriptor in registers); every row's distances come from broadcast
 // descriptors (no dependent global loads), its two middle order statistics from a
@@ -975,8 +1081,8 @@ __device__ void refresh_rep_lanes(const DevMap& M, int mp, int n, int lane) {
 __device__ void refresh_rep_warp(const DevMap& M, int mp, int lane) {
   {
     const int n = M.nobs[mp];
-    if (n >= 3 && n <= 32) return refresh_rep_planes<1>(M, mp, n, lane);
-    if (n >= 33 && n <= 64) return refresh_rep_planes<2>(M, mp, n, lane);
+    if (n >= 3 && n <= 32) return refresh_rep_sym<1>(M, mp, n, lane);
+    if (n >= 33 && n <= 64) return refresh_rep_sym<2>(M, mp, n, lane);
     if (n >= 65 && n <= 128) return refresh_rep_lanes<4>(M, mp, n, lane);
   }
   sort_obs_warp(M, mp, lane);
