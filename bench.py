@@ -443,26 +443,55 @@ def run_c5(args, rank, world, local, dist):
 
     for _ in range(args.warmup):
         one_step()
+    lib.lm_profile_enable(ctx.h, 1)
+    lib.lm_profile_read(ctx.h, (C.c_double * 16)(), (C.c_int64 * 16)())  # drop warm-up events
     sampler = ClockSampler(local)
     l0 = lib.lm_launch_count(ctx.h)
-    times = [max_over_ranks(one_step(), dev) for _ in range(args.steps)]
+    times, tot_err, pairs, fbytes = [], 0, 0, 0
+    for _ in range(args.steps):
+        times.append(max_over_ranks(one_step(), dev))
+        for m in mappers:  # this step's totals (the rewind of the next step clears them)
+            t = _lib.StepStats()
+            ctx.call("lm_totals_fetch", m.map, C.byref(t))
+            tot_err |= t.error
+            pairs += t.match_pairs
+            fbytes += t.fuse_bytes
     launches = lib.lm_launch_count(ctx.h) - l0
     clocks = sampler.stop()
-    tot_err = 0
-    for m in mappers:
-        t = _lib.StepStats()
-        ctx.call("lm_totals_fetch", m.map, C.byref(t))
-        tot_err |= t.error
+    prof_ms = (C.c_double * 16)()
+    prof_n = (C.c_int64 * 16)()
+    lib.lm_profile_read(ctx.h, prof_ms, prof_n)
+    lib.lm_profile_enable(ctx.h, 0)
     if tot_err:
         raise RuntimeError(f"device error {tot_err}")
+    stages = ["insert", "cull", "select", "prep", "match", "tri", "commit", "fuse_targets", "fuse_geo",
+              "fuse_gather", "fuse_apply", "fuse_refresh", "fuse_spec", "fuse_rev", "fuse_visible"]
+    stage_ms = {s_: prof_ms[k] / args.steps for k, s_ in enumerate(stages)}
     mean_ms = sum(times) / len(times)
     total_kf = n_kf * args.sessions
+    popc_peak = C.c_double()
+    ctx.call("lm_bench_popc", C.byref(popc_peak))
+    match_s = stage_ms["match"] * 1e-3
+    popc_achieved = 8 * (pairs / args.steps) / match_s if match_s > 0 else 0.0
+    roof_popc = {"kernel": "k_match", "bound": "popc", "achieved": popc_achieved / 1e12,
+                 "peak": popc_peak.value / 1e12, "unit": "Tpopc32/s", "frac": popc_achieved / popc_peak.value,
+                 "algorithmic_popc_per_launch": 8 * pairs / args.steps / n_kf, "launch_ms": stage_ms["match"] / n_kf,
+                 "peak_source": "lm_bench_popc microbenchmark on this GPU (measured)"}
+    fuse_s = sum(v for k_, v in stage_ms.items() if k_.startswith("fuse")) * 1e-3
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6457.4)
+    fuse_gbs = (fbytes / args.steps) / fuse_s / 1e9 if fuse_s > 0 else 0.0
+    roof_fuse = {"kernel": "k_fuse_* (whole SearchAndFuse stage, all sessions)", "bound": "hbm", "achieved": fuse_gbs,
+                 "peak": hbm_peak, "unit": "GB/s", "frac": fuse_gbs / hbm_peak}
     line = {"metric": METRIC, "value": total_kf / (mean_ms * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms,
             "ms_per_keyframe": mean_ms / n_kf, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32 popc / f64 geometry", "data": "synthetic", "config": config_of(args),
             "parallelism": f"{args.sessions} sessions sharded contiguously over {world} GPU(s), batched launches",
-            "sessions_this_rank": len(seeds), "clocks": clocks, "gpu_launches": int(launches), "e2e": None}
+            "sessions_this_rank": len(seeds), "clocks": clocks, "gpu_launches": int(launches), "e2e": None,
+            "roofline": roof_popc if stage_ms["match"] >= max(stage_ms.values()) else roof_fuse,
+            "roofline_popc": roof_popc, "roofline_fusion_stage": roof_fuse,
+            "stage_ms_per_step": stage_ms}
     if rank == 0:
         print(json.dumps(line), flush=True)
 

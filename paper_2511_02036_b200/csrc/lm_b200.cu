@@ -564,7 +564,7 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(s.pinfo, 3 * TMAX); A(s.hitpass, (size_t)d.kpkf_max * ((TMAX + 31) / 32)); A(s.pj, (size_t)s.act_cap);
   A(s.pass_of, K); A(s.snap, d.kpkf_max); A(s.chg, d.kpkf_max); A(s.rmark, MP);
   A(s.pmp, (size_t)s.act_cap); A(s.pob, (size_t)s.act_cap); A(s.itag, (size_t)s.act_cap); A(s.ilist, (size_t)s.act_cap);
-  A(s.cands, (size_t)s.act_cap); A(s.hl_cnt, d.kpkf_max); A(s.hl, (size_t)d.kpkf_max * HL); A(s.hreg, MP);
+  A(s.cands, (size_t)s.act_cap); A(s.hl_cnt, d.kpkf_max); A(s.hl, (size_t)d.kpkf_max * HL); A(s.hreg, MP); A(s.upts, (size_t)s.act_cap);
   A(s.abits, (size_t)TMAX * ((d.kpkf_max + 31) / 32));
   A(m->d_stats, 1); A(m->d_totals, 1); A(m->d_result, 4 + 1024 + TMAX);
 #undef A
@@ -850,7 +850,14 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   if ((rc = mark())) return rc;
   k_fuse_refresh<<<dim3(148, n), 256, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;
-  k_fuse_spec<<<dim3((kpkf + 255) / 256, tfuse, n), 256, 0, ctx->stream>>>(dmaps, dv);
+  if (n == 1) {
+    k_fuse_spec<true><<<dim3((kpkf + 255) / 256, tfuse, n), 256, 0, ctx->stream>>>(dmaps, dv);
+  } else {  // batches: one gather per distinct point instead of one per (pass, point)
+    k_fuse_spec_pts<<<dim3((kpkf + 255) / 256, tfuse, n), 256, 0, ctx->stream>>>(dmaps, dv);
+    k_fuse_spec_hit<<<dim3(16, n), 256, 0, ctx->stream>>>(dmaps, dv);
+    k_fuse_spec<false><<<dim3((kpkf + 255) / 256, tfuse, n), 256, 0, ctx->stream>>>(dmaps, dv);
+    ctx->launches += 2;
+  }
   if ((rc = mark())) return rc;
   k_fuse_rev<<<n, REV_THREADS, rev_smem, ctx->stream>>>(dmaps, dv, rev_smem);
   if ((rc = mark())) return rc;

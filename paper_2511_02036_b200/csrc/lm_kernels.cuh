@@ -1420,7 +1420,7 @@ __device__ __forceinline__ long long pass_bytes(long long pts, long long obs, lo
   return 56 * pts + 9 * obs + 53 * tkp + 16 * acts;
 }
 
-enum FuseCtl { FC_T = 0, FC_P = 1, FC_NACT = 2, FC_N = 8 };
+enum FuseCtl { FC_T = 0, FC_P = 1, FC_NACT = 2, FC_NU = 3, FC_N = 8 };
 
 __global__ void __launch_bounds__(1024) k_fuse_targets(DevMap* maps, const StepArgs* args, int n_slots_max) {
   const StepArgs& A = args[blockIdx.x];
@@ -1607,7 +1607,10 @@ __global__ void __launch_bounds__(256) k_fuse_refresh(DevMap* maps, const StepAr
     for (int k = tid; k < M.kpkf_max; k += nth) M.s.hl_cnt[k] = 0;
     const int aw_all = M.s.fctl[FC_T] * ((M.kpkf_max + 31) >> 5);
     for (int k = tid; k < aw_all; k += nth) M.s.abits[k] = 0u;
-    if (tid == 0) M.scal[SC_MTAG] += 1;  // merges of this step's reverse phase
+    if (tid == 0) {
+      M.scal[SC_MTAG] += 1;  // merges of this step's reverse phase
+      M.s.fctl[FC_NU] = 0;
+    }
   }
   const int n = M.scal[SC_DIRTY_N];
   const int lane = threadIdx.x & 31;
@@ -1663,7 +1666,48 @@ __device__ __forceinline__ void store_item(const DevMap& M, size_t it, const Ite
   M.s.acts2[it] = a;
 }
 
-// speculative evaluation of every reverse-pass item on the post-forward map
+// speculative evaluation of every reverse-pass item on the post-forward map, in three wide
+// kernels: the distinct bound points of all passes (a point is bound in up to ~all targets,
+// and its hit into the current keyframe does not depend on the pass), their hits, the items
+
+// (1) thread per (pass, keypoint): each live bound point joins the distinct list once
+__global__ void __launch_bounds__(256) k_fuse_spec_pts(DevMap* maps, const StepArgs* args) {
+  const StepArgs& A = args[blockIdx.z];
+  const DevMap& M = maps[A.map];
+  if (!A.do_fuse) return;
+  const int t = blockIdx.y;
+  if (t >= M.s.fctl[FC_T]) return;
+  const int ts = M.s.targets[t];
+  const int kp = blockIdx.x * 256 + threadIdx.x;
+  if (kp >= M.kp_n[ts]) return;
+  const int mp = M.kbind[M.kp_off[ts] + kp];
+  if (mp < 0 || !M.alive[mp]) return;
+  const int stag = M.scal[SC_MTAG];
+  if (atomicExch(&M.s.hreg[mp], stag) != stag) M.s.upts[atomicAdd(&M.s.fctl[FC_NU], 1)] = mp;
+}
+
+// (2) thread per distinct point (grid-stride): geometry, window search, hit list
+__global__ void __launch_bounds__(256) k_fuse_spec_hit(DevMap* maps, const StepArgs* args) {
+  const StepArgs& A = args[blockIdx.y];
+  const DevMap& M = maps[A.map];
+  if (!A.do_fuse) return;
+  if (M.s.fctl[FC_T] == 0) return;
+  const int nu = M.s.fctl[FC_NU];
+  const TgtView T = tgt_global(M, A.cur);
+  for (int k = blockIdx.x * 256 + threadIdx.x; k < nu; k += gridDim.x * 256) {
+    const int mp = M.s.upts[k];
+    PGeo g;
+    point_geometry(M, mp, A.fc.dist_band_slack, g);
+    const int j = gather_hit(M, A.fc, g, A.cur, T);
+    M.hit[mp] = make_int2(M.ver[mp], j);
+    hit_list_add(M, j, mp);
+  }
+}
+
+// (3) thread per (pass, keypoint): the item (bound point, hit, action), pass totals. With
+// GATHER (a single session: launches cost more than the redundant gathers) the item computes
+// its point's hit itself and (1)/(2) are skipped.
+template <bool GATHER>
 __global__ void __launch_bounds__(256) k_fuse_spec(DevMap* maps, const StepArgs* args) {
   const StepArgs& A = args[blockIdx.z];
   const DevMap& M = maps[A.map];
@@ -1676,16 +1720,16 @@ __global__ void __launch_bounds__(256) k_fuse_spec(DevMap* maps, const StepArgs*
   const int kp = blockIdx.x * 256 + threadIdx.x;
   int live = 0, nob = 0, has = 0;
   if (kp < n) {
-    const int mp = M.kbind[M.kp_off[ts] + kp];
-    if (mp >= 0 && M.alive[mp]) {
-      // the projection target is always the current keyframe, so the hit is per point; a
-      // point bound in several targets is gathered by each of them (identical values)
-      PGeo g;
-      point_geometry(M, mp, A.fc.dist_band_slack, g);  // caches valid or rebuilt (benign same-value race)
-      const int j = gather_hit(M, A.fc, g, A.cur, tgt_global(M, A.cur));
-      M.hit[mp] = make_int2(M.ver[mp], j);
-      const int stag = M.scal[SC_MTAG];
-      if (j >= 0 && atomicExch(&M.s.hreg[mp], stag) != stag) hit_list_add(M, j, mp);
+    if (GATHER) {
+      const int mp = M.kbind[M.kp_off[ts] + kp];
+      if (mp >= 0 && M.alive[mp]) {  // identical values from every pass binding the point
+        PGeo g;
+        point_geometry(M, mp, A.fc.dist_band_slack, g);  // caches valid (k_fuse_refresh)
+        const int j = gather_hit(M, A.fc, g, A.cur, tgt_global(M, A.cur));
+        M.hit[mp] = make_int2(M.ver[mp], j);
+        const int stag = M.scal[SC_MTAG];
+        if (j >= 0 && atomicExch(&M.s.hreg[mp], stag) != stag) hit_list_add(M, j, mp);
+      }
     }
     const ItemVal v = eval_item(M, A.cur, t, ts, kp);
     store_item(M, (size_t)t * M.kpkf_max + kp, v);

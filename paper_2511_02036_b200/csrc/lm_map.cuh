@@ -121,6 +121,7 @@ struct Scratch {
   int* hl_cnt;           // [kpkf_max] per current keypoint: points whose hit is it (count)
   int* hl;               // [kpkf_max*HL] ... (ids; entries whose hit moved are skipped)
   int* hreg;             // [mp_cap] step tag: point already listed by the speculative scan
+  int* upts;             // [act_cap] distinct bound points of all reverse passes
   unsigned* abits;       // [TMAX*ceil(kpkf_max/32)] per pass: keypoints whose item has an action
   int* act_flag;         // [TMAX*kpkf_max]
   int* vis_flag;         // [TMAX*kpkf_max]
