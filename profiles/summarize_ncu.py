@@ -28,6 +28,8 @@ METRICS = {
     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "fma_cycles_pct",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_cycles_pct",
     "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "xu_pipe_active_pct",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_elapsed": "xu_pipe_elapsed_pct",
     "launch__grid_size": "grid",
     "launch__block_size": "block",
     "launch__registers_per_thread": "registers",
@@ -89,13 +91,15 @@ def main():
     for k, n, mean, share in launch_shares(launches):
         lines.append(f"| {k} | {n} | {mean * 1e6:.1f} | {100 * share:.1f}% |")
     lines += ["", f"# {tag}: `ncu --set full` per-launch averages", "",
-              "| kernel | us | dram B/launch | occupancy % | issue active % | alu % | fp64 % |", "|---|---|---|---|---|---|---|"]
+              "| kernel | us | dram B/launch | occupancy % | issue active % | alu % | xu (POPC) % active / elapsed | fp64 % |",
+              "|---|---|---|---|---|---|---|---|"]
     for k, d in sorted(summ.items()):
         if not isinstance(d, dict):
             continue
         lines.append(f"| {k} | {d.get('duration', 0) * 1e6:.1f} | {d.get('dram_bytes_per_launch', 0):.0f} | "
                      f"{d.get('achieved_occupancy_pct', 0):.1f} | {d.get('issue_active_pct', 0):.1f} | "
-                     f"{d.get('alu_cycles_pct', 0):.1f} | {d.get('fp64_cycles_pct', 0):.1f} |")
+                     f"{d.get('alu_cycles_pct', 0):.1f} | {d.get('xu_pipe_active_pct', 0):.1f} / "
+                     f"{d.get('xu_pipe_elapsed_pct', 0):.1f} | {d.get('fp64_cycles_pct', 0):.1f} |")
     with open(os.path.join(HERE, f"{tag}_summary.md"), "w") as fh:
         fh.write("\n".join(lines) + "\n")
     print("\n".join(lines))
