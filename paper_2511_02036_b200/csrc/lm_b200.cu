@@ -564,7 +564,7 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(s.pinfo, 3 * TMAX); A(s.hitpass, (size_t)d.kpkf_max * ((TMAX + 31) / 32)); A(s.pj, (size_t)s.act_cap);
   A(s.pass_of, K); A(s.snap, d.kpkf_max); A(s.chg, d.kpkf_max); A(s.rmark, MP);
   A(s.pmp, (size_t)s.act_cap); A(s.pob, (size_t)s.act_cap); A(s.itag, (size_t)s.act_cap); A(s.ilist, (size_t)s.act_cap);
-  A(s.cands, (size_t)s.act_cap); A(s.hl_cnt, d.kpkf_max); A(s.hl, (size_t)d.kpkf_max * HL); A(s.hreg, MP); A(s.upts, (size_t)s.act_cap);
+  A(s.cands, (size_t)s.act_cap); A(s.cneed, (size_t)s.act_cap); A(s.hl_cnt, d.kpkf_max); A(s.hl, (size_t)d.kpkf_max * HL); A(s.hreg, MP); A(s.upts, (size_t)s.act_cap);
   A(s.abits, (size_t)TMAX * ((d.kpkf_max + 31) / 32));
   A(m->d_stats, 1); A(m->d_totals, 1); A(m->d_result, 4 + 1024 + TMAX);
 #undef A

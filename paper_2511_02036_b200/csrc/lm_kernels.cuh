@@ -891,8 +891,17 @@ __device__ bool for_keys(const DevMap& M, const ActRec& x, Op op) {
     const int loser = na == nb ? (x.pid > partner ? x.pid : partner) : (na < nb ? x.pid : partner);
     const int2* o = M.obs + M.ooff[loser];
     const int n = M.nobs[loser];
-    for (int k = 0; k < n; ++k)
-      if (!op(KM_SLOT, M.kp_off[o[k].x] + o[k].y)) return false;
+    for (int k0 = 0; k0 < n; k0 += 8) {  // entries and keypoint offsets loaded 8 at a time
+      int2 e[8];
+      int g[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) e[j] = k0 + j < n ? o[k0 + j] : make_int2(0, 0);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) g[j] = k0 + j < n ? M.kp_off[e[j].x] + e[j].y : 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (k0 + j < n && !op(KM_SLOT, g[j])) return false;
+    }
   }
   return true;
 }
@@ -1089,9 +1098,7 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
       const int m = (int)(M.grp_head[p] & 0xffffffffull);
       if (m == 1) {
         if (M.nobs[p] <= 24) {
-          link(M, p, x.slot, x.j, acc);
-          mark_dirty(M, p);
-          M.found[p] += 1;
+          link(M, p, x.slot, x.j, acc, true);
           atomicAdd(&cnt[1], 1);
         } else {
           M.s.add_list[atomicAdd(&ctl[CTL_NADD], 1)] = M.s.def[d];
@@ -1140,7 +1147,7 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
       const int g = M.kp_off[x.slot] + x.j;
       M.kbind[g] = p;
       atomicAdd(&M.counts[(size_t)p * M.L + M.klev[g]], 1);
-      for (int k = 0; k < base; ++k) covis_add(M, x.slot, o[k].x, +1, acc);
+      covis_list(M, x.slot, o, base, +1, acc);
     }
     {
       const int nm = ctl[CTL_NMERGE], na = ctl[CTL_NADD];
@@ -1166,8 +1173,7 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
       const int base = M.s.gbase[p];
       if (m == 1 || base < 0) continue;
       const int2* o = M.obs + M.ooff[p];
-      const int tk = (int)M.s.dnxt[d];
-      for (int k = 0; k < tk; ++k) covis_add(M, x.slot, o[base + k].x, +1, acc);
+      covis_list(M, x.slot, o + base, (int)M.s.dnxt[d], +1, acc);
     }
     if (groups) G.sync();
     if (tm && tid == 0) {
@@ -1907,14 +1913,19 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     ++pass_act;
     const int na = na_sh, tag = tag_sh, ncand = nc_sh;
     // items of point p (its current observations) in passes after t1; warp-cooperative
-    auto add_point_items = [&](int p) {
+    auto add_point_items = [&](int p) -> bool {  // true when p has an item after t1
       const int2* o = M.obs + M.ooff[p];
       const int no = M.nobs[p];
+      bool any = false;
       for (int e = lane; e < no; e += 32) {
         const int2 ob = o[e];
         const int tt = M.s.pass_of[ob.x];
-        if (tt > t1) add_item(tt, ob.y, tag);
+        if (tt > t1) {
+          add_item(tt, ob.y, tag);
+          any = true;
+        }
       }
+      return __any_sync(0xffffffffu, any);
     };
     for (int k = wid; k < ncand; k += REV_THREADS / 32) add_point_items(M.s.cands[k]);  // before the apply
     __syncthreads();
@@ -1925,7 +1936,10 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     //     keypoint whose binding changed (hit list; a keypoint whose list overflowed falls
     //     back to scanning the passes of its bitmap) join the touched list
     const long long tv = gtime();
-    for (int k = wid; k < ncand; k += REV_THREADS / 32) add_point_items(M.s.cands[k]);
+    for (int k = wid; k < ncand; k += REV_THREADS / 32) {
+      const bool later = add_point_items(M.s.cands[k]);
+      if (lane == 0) M.s.cneed[k] = later;  // no later item: its new hit is not needed this step
+    }
     for (int k = threadIdx.x; k < ncur; k += REV_THREADS)  // current keypoints whose binding changed
       if (M.kbind[cur_off + k] != M.s.snap[k]) M.s.chg[atomicAdd(&nchg_sh, 1)] = k;
     __syncthreads();
@@ -1966,7 +1980,9 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     for (int k = wid; k < nall; k += REV_THREADS / 32) {
       const int p = M.s.cands[k];
       if (k < ncand) {
-        if (!M.alive[p]) continue;
+        // a touched point without items in later passes keeps its dirty flag (the next
+        // step's refresh picks it up) and a stale hit (nothing reads it: the version differs)
+        if (!M.alive[p] || !M.s.cneed[k]) continue;
         const long long c0 = clock64();
         if (M.dirty[p]) {
           refresh_rep_warp(M, p, lane);

@@ -118,6 +118,7 @@ struct Scratch {
   int* itag;             // [TMAX*kpkf_max] dedup tag of the re-evaluation list
   int* ilist;            // [TMAX*kpkf_max] (pass, keypoint) items to re-evaluate
   int* cands;            // [act_cap] points touched by an apply
+  int* cneed;            // [act_cap] touched point has items in later passes
   int* hl_cnt;           // [kpkf_max] per current keypoint: points whose hit is it (count)
   int* hl;               // [kpkf_max*HL] ... (ids; entries whose hit moved are skipped)
   int* hreg;             // [mp_cap] step tag: point already listed by the speculative scan
@@ -258,6 +259,19 @@ __device__ __forceinline__ void covis_add(const DevMap& M, int a, int b, int d, 
   covis_global(M, a, b, d);
 }
 
+// covisibility delta d between keyframe `slot` and every observer of o[0..n): the list
+// entries are loaded 8 at a time before their atomics (one L2 round trip per 8 entries
+// instead of one per entry: the compiler does not hoist loads across the atomics)
+__device__ __forceinline__ void covis_list(const DevMap& M, int slot, const int2* o, int n, int d, PairAcc* acc) {
+  for (int k0 = 0; k0 < n; k0 += 8) {
+    int s[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s[j] = k0 + j < n ? o[k0 + j].x : slot;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) covis_add(M, slot, s[j], d, acc);  // (slot, slot) is a no-op
+  }
+}
+
 template <int BLOCK>
 __device__ void pair_acc_init(PairAcc* acc, int newest_slot) {
   for (int q = threadIdx.x; q < PAIR_T; q += BLOCK) acc->win[q] = 0;
@@ -337,6 +351,15 @@ __device__ __forceinline__ void mark_dirty(const DevMap& M, int mp) {
   }
 }
 
+// mark_dirty for a caller that is the only one touching mp's flag in this phase and already
+// read it (`was`): one returning atomic instead of two
+__device__ __forceinline__ void mark_dirty_owned(const DevMap& M, int mp, int was) {
+  if (was) return;
+  M.dirty[mp] = 1;
+  const int at = atomicAdd(&M.scal[SC_DIRTY_N], 1);
+  if (at < M.mp_cap) M.dirty_list[at] = mp;
+}
+
 // one observation's contribution to the view geometry (fusion.py:77-84); false if skipped
 __device__ __forceinline__ bool geo_term(const DevMap& M, int mp, int2 e, double& rx, double& ry, double& rz,
                                         double& dd, double& d0) {
@@ -376,9 +399,12 @@ __device__ void geo_full(const DevMap& M, int mp) {
 // _record_obs: covis +1 with every current observer, bind the slot, count the level. An
 // observation appended after every existing one extends the cached sums exactly.
 // Latency-shaped: the independent loads are issued together before any store.
-__device__ void link(const DevMap& M, int mp, int slot, int kp, PairAcc* acc = nullptr) {
+// fuse=true: fusion's ADD_OBSERVATION on top (found += 1, representative descriptor marked
+// stale), with the flag/counter loads in the same first round.
+__device__ void link(const DevMap& M, int mp, int slot, int kp, PairAcc* acc = nullptr, bool fuse = false) {
   const int n = M.nobs[mp], cap = M.ocap[mp], off = M.ooff[mp];
   const int dirty = M.dirty[mp], gv = M.gval[mp];
+  const int found = fuse ? M.found[mp] : 0;
   const int g = M.kp_off[slot] + kp;
   const long long kf_new = M.kf_id[slot];
   const double px = M.pos[3 * mp], py = M.pos[3 * mp + 1], pz = M.pos[3 * mp + 2];
@@ -387,7 +413,7 @@ __device__ void link(const DevMap& M, int mp, int slot, int kp, PairAcc* acc = n
   const int last = n ? o[n - 1].x : -1;
   const int lev = M.klev[g];
   const long long kf_last = last >= 0 ? M.kf_id[last] : -1;
-  for (int k = 0; k < n; ++k) covis_add(M, slot, o[k].x, +1, acc);
+  covis_list(M, slot, o, n, +1, acc);
   // appended after the newest keyframe of a clean (sorted) list: the cached sums extend exactly
   const bool newest = !dirty && (n == 0 || kf_last < kf_new);
   int at = n;
@@ -409,6 +435,10 @@ __device__ void link(const DevMap& M, int mp, int slot, int kp, PairAcc* acc = n
   M.kbind[g] = mp;
   M.counts[(size_t)mp * M.L + lev] += 1;
   M.ver[mp] += 1;
+  if (fuse) {
+    M.found[mp] = found + 1;
+    mark_dirty_owned(M, mp, dirty);
+  }
   if (gv && newest) {
     const double rx = px - cx, ry = py - cy, rz = pz - cz;
     const double dd = sqrt(rx * rx + ry * ry + rz * rz);
@@ -470,7 +500,7 @@ __device__ void unlink_at(const DevMap& M, int mp, int k, PairAcc* acc = nullptr
   const int g = M.kp_off[e.x] + e.y;
   M.kbind[g] = -1;
   M.counts[(size_t)mp * M.L + M.klev[g]] -= 1;
-  for (int m = 0; m < n; ++m) covis_add(M, e.x, o[m].x, -1, acc);
+  covis_list(M, e.x, o, n, -1, acc);
 }
 
 __device__ void kill_point(const DevMap& M, int mp, PairAcc* acc = nullptr) {
@@ -518,6 +548,42 @@ __device__ void merge_pair(const DevMap& M, int a, int b, PairAcc* acc = nullptr
 // Same net effect as the sequential unlink/link loops above (all covisibility bumps are
 // commutative), with the O(n^2) pair work spread over the 32 lanes of one warp.
 
+// covisibility delta d for every unordered pair of o[0..n) (warp; n <= 64 from registers:
+// lane l holds entries l and l+32, entry a is broadcast by a shuffle)
+__device__ void covis_pairs_warp(const DevMap& M, const int2* o, int n, int d, int lane, PairAcc* acc) {
+  if (n <= 64) {
+    const int s0 = lane < n ? o[lane].x : -1, s1 = lane + 32 < n ? o[lane + 32].x : -1;
+    for (int a = 0; a < n - 1; ++a) {
+      const int sa = __shfl_sync(0xffffffffu, a < 32 ? s0 : s1, a & 31);
+      if (lane > a && lane < n) covis_add(M, sa, s0, d, acc);
+      if (lane + 32 > a && lane + 32 < n) covis_add(M, sa, s1, d, acc);
+    }
+    return;
+  }
+  for (int a = 0; a < n; ++a)
+    for (int b = a + 1 + lane; b < n; b += 32) covis_add(M, o[a].x, o[b].x, d, acc);
+}
+
+// covisibility delta d for every pair (x in oa[0..na), y in ob[0..nb)) (warp; nb <= 64 from
+// registers, oa entries broadcast one by one)
+__device__ void covis_cross_warp(const DevMap& M, const int2* oa, int na, const int2* ob, int nb, int d, int lane,
+                                 PairAcc* acc) {
+  if (nb <= 64) {
+    const int t0 = lane < nb ? ob[lane].x : -1, t1 = lane + 32 < nb ? ob[lane + 32].x : -1;
+    for (int a0 = 0; a0 < na; a0 += 32) {
+      const int sv = a0 + lane < na ? oa[a0 + lane].x : -1;
+      const int m = na - a0 < 32 ? na - a0 : 32;
+      for (int a = 0; a < m; ++a) {
+        const int sa = __shfl_sync(0xffffffffu, sv, a);
+        if (lane < nb) covis_add(M, sa, t0, d, acc);
+        if (lane + 32 < nb) covis_add(M, sa, t1, d, acc);
+      }
+    }
+    return;
+  }
+  for (int q = lane; q < na * nb; q += 32) covis_add(M, oa[q / nb].x, ob[q % nb].x, d, acc);
+}
+
 // kill_map_point (mapmodel.py:233-237) of a point with at most 8 observations, one thread
 __device__ void kill_point_thread(const DevMap& M, int mp, PairAcc* acc) {
   const int2* o = M.obs + M.ooff[mp];
@@ -545,8 +611,7 @@ __device__ void kill_point_thread(const DevMap& M, int mp, PairAcc* acc) {
 __device__ void kill_point_warp(const DevMap& M, int mp, int lane, PairAcc* acc) {
   const int2* o = M.obs + M.ooff[mp];
   const int n = M.nobs[mp];
-  for (int a = 0; a < n; ++a)
-    for (int b = a + 1 + lane; b < n; b += 32) covis_add(M, o[a].x, o[b].x, -1, acc);
+  covis_pairs_warp(M, o, n, -1, lane, acc);
   for (int k = lane; k < n; k += 32) M.kbind[M.kp_off[o[k].x] + o[k].y] = -1;
   for (int l = lane; l < M.L; l += 32) M.counts[(size_t)mp * M.L + l] = 0;
   __syncwarp();
@@ -565,8 +630,7 @@ __device__ int replace_point_warp(const DevMap& M, int loser, int winner, int la
   const int2* oW = M.obs + M.ooff[winner];
   const int nL = M.nobs[loser], nW = M.nobs[winner];
   // (a) covisibility -1 for every pair of the loser's observers
-  for (int a = 0; a < nL; ++a)
-    for (int b = a + 1 + lane; b < nL; b += 32) covis_add(M, oL[a].x, oL[b].x, -1, acc);
+  covis_pairs_warp(M, oL, nL, -1, lane, acc);
   __syncwarp();
   // (b) migrate the observations of keyframes the winner does not see; compact them in place
   int nM = 0;
@@ -593,9 +657,8 @@ __device__ int replace_point_warp(const DevMap& M, int loser, int winner, int la
     __syncwarp();
   }
   // (c) covisibility +1: migrated x winner's original observers, and migrated pairs
-  for (int q = lane; q < nM * nW; q += 32) covis_add(M, oL[q / nW].x, oW[q % nW].x, +1, acc);
-  for (int a = 0; a < nM; ++a)
-    for (int b = a + 1 + lane; b < nM; b += 32) covis_add(M, oL[a].x, oL[b].x, +1, acc);
+  covis_cross_warp(M, oL, nM, oW, nW, +1, lane, acc);
+  covis_pairs_warp(M, oL, nM, +1, lane, acc);
   // (d) winner list += migrated observations (appended; the winner is marked dirty, so the
   //     list is re-sorted by keyframe id before any order-dependent read)
   if (nM > 0) {
