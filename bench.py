@@ -210,13 +210,20 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks (one-GPU rehearsal of the multi-rank path): every rank on device 0, gloo
+    if os.environ.get("LM_BENCH_SAME_DEVICE") == "1":
+        local = 0
     dist = None
     if world > 1:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("LM_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     from paper_2511_02036_b200 import _lib
     from paper_2511_02036_b200.session import LocalMapper, store_for
@@ -248,7 +255,8 @@ def main():
             return x
         import torch
 
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([x], dtype=torch.float64,
+                         device=f"cuda:{local}" if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -424,7 +432,7 @@ def run_c5(args, rank, world, local, dist):
         kf_lists.append([kf.kf_id for kf in kfs])
     batch = SessionBatch(mappers)
     n_kf = min(len(x) for x in kf_lists)
-    dev = f"cuda:{local}" if dist is not None else None
+    dev = f"cuda:{local}" if dist is not None and dist.get_backend() == "nccl" else None
 
     def one_step():
         for m in mappers:
