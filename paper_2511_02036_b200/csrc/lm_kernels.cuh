@@ -1116,7 +1116,7 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
           continue;
         }
         const int2* src = M.obs + M.ooff[p];
-        for (int k = 0; k < n0; ++k) M.obs[off + k] = src[k];
+        copy_obs(M.obs + off, src, n0);
         M.ooff[p] = off;
         M.ocap[p] = nc;
       }

@@ -300,6 +300,20 @@ __device__ void pair_acc_flush(const DevMap& M, PairAcc* acc) {
   __syncthreads();
 }
 
+// copy n observation entries (8 loads in flight before their stores: source and
+// destination are the same pool, so the compiler will not overlap them on its own)
+__device__ __forceinline__ void copy_obs(int2* dst, const int2* src, int n) {
+  for (int k0 = 0; k0 < n; k0 += 8) {
+    int2 e[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (k0 + j < n) e[j] = src[k0 + j];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (k0 + j < n) dst[k0 + j] = e[j];
+  }
+}
+
 __device__ __forceinline__ int obs_find(const DevMap& M, int mp, int slot) {
   const int2* o = M.obs + M.ooff[mp];
   const int n = M.nobs[mp];
@@ -323,7 +337,7 @@ __device__ int obs_insert(const DevMap& M, int mp, int slot, int kp) {
       return -1;
     }
     const int2* src = M.obs + M.ooff[mp];
-    for (int k = 0; k < n; ++k) M.obs[off + k] = src[k];
+    copy_obs(M.obs + off, src, n);
     M.ooff[mp] = off;
     M.ocap[mp] = nc;
   }
@@ -424,7 +438,7 @@ __device__ void link(const DevMap& M, int mp, int slot, int kp, PairAcc* acc = n
       set_err(M, LM_ERR_CAPACITY);
       return;
     }
-    for (int k = 0; k < n; ++k) M.obs[noff + k] = o[k];
+    copy_obs(M.obs + noff, o, n);
     M.ooff[mp] = noff;
     M.ocap[mp] = nc;
     M.obs[noff + n] = make_int2(slot, kp);
