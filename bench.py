@@ -327,6 +327,29 @@ def main():
         e2e = {"value": total_kf / (sum(e_ms) / len(e_ms) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": sum(e_ms) / len(e_ms),
                "timing": "wall clock around stage+step+readback of every keyframe"}
+        # the same through the binary ingest wire format (LMKF records in host memory)
+        from paper_2511_02036_b200 import ingest
+
+        recs = [ingest.pack_keyframe(kf) for kf in kfs]
+        bufs = [(C.create_string_buffer(r, len(r)), len(r)) for r in recs]
+        kid = C.c_int64()
+        st = _lib.StepStats()
+        r_ms = []
+        for it in range(args.warmup + args.steps):
+            mapper.reset()
+            barrier()
+            t0 = time.perf_counter()
+            for b, ln in bufs:
+                ctx.call("lm_kf_stage_record", mapper.map, b, ln, C.byref(kid))
+                p = mapper.params()
+                ctx.call("lm_step", mapper.map, kid.value, C.byref(p), C.byref(st))
+                mapper.processed += 1
+            dt = (time.perf_counter() - t0) * 1e3
+            if it >= args.warmup:
+                r_ms.append(max_over_ranks(dt))
+        e2e["records"] = {"value": total_kf / (sum(r_ms) / len(r_ms) * 1e-3), "unit": UNIT,
+                          "h2d_bytes_per_step": sum(len(r) for r in recs), "d2h_bytes_per_step": d2h,
+                          "timing": "wall clock: lm_kf_stage_record (LMKF wire records) + lm_step + stats readback"}
 
     # -------- roofline of the dominant kernel (k_fuse_rev), the whole fusion stage, and the
     # matching kernel's popc roofline. Achieved = algorithmic work per launch (SURVEY.md 8(d),

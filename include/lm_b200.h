@@ -170,6 +170,31 @@ int lm_synchronize(lm_ctx* ctx);
 int lm_kf_stage(lm_ctx* ctx, int32_t map, int64_t kf_id, const double quat[4], const double trans[3],
                 const double cam[6], int32_t n, const double* u, const double* v, const int64_t* level,
                 const uint8_t* desc, const int64_t* bindings);
+/* Binary keyframe record ("LMKF" v1), the ingest wire format replacing the reference's
+ * JSON keyframe payload (service/schemas.py:111-126: KeyframePayload, hex descriptors) and
+ * JSONL sequence lines (synth.py:376-439). Little-endian, 8-byte aligned:
+ *   lm_kf_record_hdr (160 bytes), then double u[n], double v[n], uint8 level[n] padded to a
+ *   multiple of 8, uint8 desc[32*n], and int64 bindings[n] when (flags & LM_REC_BINDINGS).
+ * The record's pyramid (num_levels, scale_factor) must equal the map's. */
+#define LM_REC_MAGIC 0x464B4D4Cu /* "LMKF" */
+#define LM_REC_VERSION 1
+#define LM_REC_BINDINGS 1u
+typedef struct lm_kf_record_hdr {
+  uint32_t magic;
+  uint16_t version, flags;
+  uint32_t n, header_bytes; /* keypoints; sizeof(lm_kf_record_hdr) */
+  int64_t kf_id, frame_index;
+  double quat[4];           /* x, y, z, w */
+  double trans[3];          /* world -> camera */
+  double fx, fy, cx, cy;
+  int32_t width, height, num_levels, pad;
+  double scale_factor;
+  double reserved[2];
+} lm_kf_record_hdr;
+/* bytes of a record with n keypoints */
+uint64_t lm_kf_record_bytes(int32_t n, uint32_t flags);
+/* Validate one record and stage it like lm_kf_stage (kf_id_out may be NULL). */
+int lm_kf_stage_record(lm_ctx* ctx, int32_t map, const void* record, uint64_t bytes, int64_t* kf_id_out);
 /* Insert a staged keyframe into the map (insert_keyframe + upload_keyframe). */
 int lm_kf_insert(lm_ctx* ctx, int32_t map, int64_t kf_id);
 int lm_kf_kill(lm_ctx* ctx, int32_t map, int64_t kf_id); /* MapModel.kill_keyframe */

@@ -973,6 +973,45 @@ static int single_stage(lm_ctx* ctx, int32_t map, int64_t kf_id, lm_step_params&
   return lm_step(ctx, map, kf_id, &p, out ? out : &tmp);
 }
 
+static_assert(sizeof(lm_kf_record_hdr) == 160, "record header layout");
+
+uint64_t lm_kf_record_bytes(int32_t n, uint32_t flags) {
+  if (n < 0) return 0;
+  const uint64_t nn = (uint64_t)n;
+  return sizeof(lm_kf_record_hdr) + 16 * nn + ((nn + 7) & ~7ull) + 32 * nn + ((flags & LM_REC_BINDINGS) ? 8 * nn : 0);
+}
+
+int lm_kf_stage_record(lm_ctx* ctx, int32_t map, const void* record, uint64_t bytes, int64_t* kf_id_out) {
+  if (!ctx || !record) return LM_ERR_INVALID_ARGUMENT;
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  if (bytes < sizeof(lm_kf_record_hdr)) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "record shorter than its header");
+  lm_kf_record_hdr h;
+  memcpy(&h, record, sizeof h);
+  if (h.magic != LM_REC_MAGIC || h.version != LM_REC_VERSION || h.header_bytes != sizeof(lm_kf_record_hdr))
+    return fail(ctx, LM_ERR_INVALID_ARGUMENT, "not an LMKF v1 keyframe record");
+  if ((h.flags & ~LM_REC_BINDINGS) != 0) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "unknown record flags %u", h.flags);
+  if (h.n > (uint32_t)0x7fffffff || lm_kf_record_bytes((int32_t)h.n, h.flags) != bytes)
+    return fail(ctx, LM_ERR_INVALID_ARGUMENT, "record size %llu does not match %u keypoints", (unsigned long long)bytes, h.n);
+  if (h.num_levels != m->d.L || h.scale_factor != m->d.sf)
+    return fail(ctx, LM_ERR_INVALID_ARGUMENT, "record pyramid (%d levels, %g) differs from the map's (%d, %g)",
+                h.num_levels, h.scale_factor, m->d.L, m->d.sf);
+  const int n = (int)h.n;
+  const unsigned char* p = (const unsigned char*)record + sizeof(lm_kf_record_hdr);
+  const double* u = (const double*)p;
+  const double* v = u + n;
+  const unsigned char* lv8 = (const unsigned char*)(v + n);
+  const uint8_t* desc = lv8 + ((n + 7) & ~7);
+  const int64_t* bind = (h.flags & LM_REC_BINDINGS) ? (const int64_t*)(desc + 32 * (size_t)n) : nullptr;
+  std::vector<int64_t> level(n);
+  for (int i = 0; i < n; ++i) level[i] = lv8[i];
+  const double cam[6] = {h.fx, h.fy, h.cx, h.cy, (double)h.width, (double)h.height};
+  rc = lm_kf_stage(ctx, map, h.kf_id, h.quat, h.trans, cam, n, u, v, level.data(), desc, bind);
+  if (rc == LM_OK && kf_id_out) *kf_id_out = h.kf_id;
+  return rc;
+}
+
 int lm_kf_insert(lm_ctx* ctx, int32_t map, int64_t kf_id) {
   HostMap* m;
   int rc = check_map(ctx, map, &m);
