@@ -817,7 +817,7 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   if ((rc = mark())) return rc;
   k_prep<<<dim3(1 + nbr_dim, n), 256, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;
-  k_match<<<dim3(tiles, nbr_dim, n), MATCH_WARPS * 32, 0, ctx->stream>>>(dmaps, dv);
+  k_match<<<dim3(nbr_dim, tiles, n), MATCH_WARPS * 32, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;
   k_tri<<<dim3(nbr_dim, n), 256, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;

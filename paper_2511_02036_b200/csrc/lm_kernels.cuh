@@ -335,17 +335,46 @@ __global__ void __launch_bounds__(256) k_prep(DevMap* maps, const StepArgs* args
       }
     }
     if (threadIdx.x <= L) M.s.cur_bucket[threadIdx.x] = lstart[threadIdx.x];
-    if (threadIdx.x == 0) {  // tiles never straddle a level
+    // tiles never straddle a level; they are listed longest first (k_match dispatches tiles
+    // in this order, every neighbour's copy of a tile side by side), so the tail of the
+    // wave is made of short tiles. Work proxy: tile size x the current keyframe's unbound
+    // population of the tile's level window. Rank sort in shared memory.
+    constexpr int TCAP = 512;
+    __shared__ int t_l[TCAP], t_s[TCAP], t_c[TCAP], t_w[TCAP];
+    __shared__ int nt_sh;
+    if (threadIdx.x == 0) {
       int nt = 0;
-      for (int l = 0; l < L; ++l)
+      const int w = A.mc.level_window;
+      for (int l = 0; l < L; ++l) {
+        int win = 0;
+        for (int q = l - w; q <= l + w; ++q)
+          if (q >= 0 && q < L) win += lcount[q];
         for (int s = lstart[l]; s < lstart[l + 1]; s += MATCH_TILE) {
-          const int c = lstart[l + 1] - s;
-          M.s.tiles[3 * nt] = l;
-          M.s.tiles[3 * nt + 1] = s;
-          M.s.tiles[3 * nt + 2] = c < MATCH_TILE ? c : MATCH_TILE;
+          const int c = lstart[l + 1] - s < MATCH_TILE ? lstart[l + 1] - s : MATCH_TILE;
+          if (nt < TCAP) {
+            t_l[nt] = l;
+            t_s[nt] = s;
+            t_c[nt] = c;
+            t_w[nt] = c * win;
+          } else {
+            M.s.tiles[3 * nt] = l;  // (beyond the sort capacity: appended unsorted)
+            M.s.tiles[3 * nt + 1] = s;
+            M.s.tiles[3 * nt + 2] = c;
+          }
           ++nt;
         }
+      }
+      nt_sh = nt;
       *M.s.n_tiles = nt;
+    }
+    __syncthreads();
+    const int ns = nt_sh < TCAP ? nt_sh : TCAP;
+    for (int a = threadIdx.x; a < ns; a += 256) {
+      int rk = 0;
+      for (int b = 0; b < ns; ++b) rk += t_w[b] > t_w[a] || (t_w[b] == t_w[a] && b < a);
+      M.s.tiles[3 * rk] = t_l[a];
+      M.s.tiles[3 * rk + 1] = t_s[a];
+      M.s.tiles[3 * rk + 2] = t_c[a];
     }
   } else {
     const size_t base = (size_t)r * M.kpkf_max;
@@ -382,9 +411,9 @@ __global__ void __launch_bounds__(MATCH_WARPS * 32) k_match(DevMap* maps, const 
   const StepArgs& A = args[blockIdx.z];
   const DevMap& M = maps[A.map];
   if (!A.do_create) return;
-  const int r = blockIdx.y;
+  const int r = blockIdx.x;  // neighbour fastest: each tile's copies dispatch side by side
   if (r >= M.s.stats->n_neighbors || M.s.deg[r]) return;
-  const int tile = blockIdx.x;
+  const int tile = blockIdx.y;
   if (tile >= *M.s.n_tiles) return;
   __shared__ uint4 sd[2 * MATCH_JT];
   __shared__ unsigned long long best_sh[MATCH_TILE];

@@ -121,8 +121,8 @@ def test_stage_record_validation():
         ingest.stage_record(m.ctx, m.map, b"XXXX" + buf[4:])
     with pytest.raises(InvalidArgumentError):
         ingest.stage_record(m.ctx, m.map, buf[:-8])
-    other = CameraIntrinsics(intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height, num_levels=4,
-                             scale_factor=intr.scale_factor)
+    other = CameraIntrinsics(intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height,
+                             num_levels=intr.num_levels, scale_factor=1.3)
     kf2 = device_kf(s.records[1], other)
     with pytest.raises(InvalidArgumentError):
         ingest.stage_record(m.ctx, m.map, ingest.pack_keyframe(kf2))
