@@ -252,6 +252,13 @@ int lm_recent_import(lm_ctx* ctx, int32_t map, const int64_t* ids, const int32_t
 int lm_map_rewind(lm_ctx* ctx, int32_t map);
 int lm_timer_start(lm_ctx* ctx);                 /* CUDA event on the context stream */
 int lm_timer_stop(lm_ctx* ctx, float* ms);       /* event + synchronize, elapsed since start */
+/* Timing across two contexts (streams) of one device: start on ctx (other waits for it),
+ * stop = the later of both streams. */
+int lm_timer_start_joint(lm_ctx* ctx, lm_ctx* other);
+int lm_timer_stop_joint(lm_ctx* ctx, lm_ctx* other, float* ms);
+/* the same over n contexts (start on ctxs[0], stop = the latest stream) */
+int lm_timer_start_multi(lm_ctx* const* ctxs, int32_t n);
+int lm_timer_stop_multi(lm_ctx* const* ctxs, int32_t n, float* ms);
 int lm_flush_l2(lm_ctx* ctx, int64_t bytes);     /* write a scratch buffer larger than L2 */
 int64_t lm_launch_count(lm_ctx* ctx);
 /* Running totals since map creation/reset/rewind (first_new_id holds the step count). */

@@ -136,6 +136,10 @@ _SIGS = {
     "lm_map_rewind": ([C.c_void_p, i32], i32),
     "lm_timer_start": ([C.c_void_p], i32),
     "lm_timer_stop": ([C.c_void_p, P(C.c_float)], i32),
+    "lm_timer_start_joint": ([C.c_void_p, C.c_void_p], i32),
+    "lm_timer_stop_joint": ([C.c_void_p, C.c_void_p, P(C.c_float)], i32),
+    "lm_timer_start_multi": ([P(C.c_void_p), i32], i32),
+    "lm_timer_stop_multi": ([P(C.c_void_p), i32, P(C.c_float)], i32),
     "lm_flush_l2": ([C.c_void_p, i64], i32),
     "lm_launch_count": ([C.c_void_p], i64),
     "lm_totals_fetch": ([C.c_void_p, i32, P(StepStats)], i32),

@@ -1550,6 +1550,63 @@ int lm_timer_stop(lm_ctx* ctx, float* ms) {
   return LM_OK;
 }
 
+int lm_timer_start_joint(lm_ctx* ctx, lm_ctx* other) {
+  // start on ctx's stream; other's stream waits for it, so other's later work is inside
+  int rc = lm_timer_start(ctx);
+  if (rc) return rc;
+  if (other && other != ctx) CU(cudaStreamWaitEvent(other->stream, ctx->t0, 0));
+  return LM_OK;
+}
+
+int lm_timer_stop_joint(lm_ctx* ctx, lm_ctx* other, float* ms) {
+  // elapsed from ctx's start event to the later of the two streams' stop events
+  if (!other || other == ctx) return lm_timer_stop(ctx, ms);
+  if (!other->t0) {
+    CU(cudaEventCreate(&other->t0));
+    CU(cudaEventCreate(&other->t1));
+  }
+  CU(cudaEventRecord(ctx->t1, ctx->stream));
+  CU(cudaEventRecord(other->t1, other->stream));
+  CU(cudaEventSynchronize(ctx->t1));
+  CU(cudaEventSynchronize(other->t1));
+  float a = 0, b = 0;
+  CU(cudaEventElapsedTime(&a, ctx->t0, ctx->t1));
+  CU(cudaEventElapsedTime(&b, ctx->t0, other->t1));
+  *ms = a > b ? a : b;
+  return LM_OK;
+}
+
+int lm_timer_start_multi(lm_ctx* const* ctxs, int32_t n) {
+  if (!ctxs || n < 1 || !ctxs[0]) return LM_ERR_INVALID_ARGUMENT;
+  lm_ctx* ctx = ctxs[0];
+  int rc = lm_timer_start(ctx);
+  if (rc) return rc;
+  for (int i = 1; i < n; ++i) CU(cudaStreamWaitEvent(ctxs[i]->stream, ctxs[0]->t0, 0));
+  return LM_OK;
+}
+
+int lm_timer_stop_multi(lm_ctx* const* ctxs, int32_t n, float* ms) {
+  if (!ctxs || n < 1 || !ctxs[0] || !ms) return LM_ERR_INVALID_ARGUMENT;
+  lm_ctx* ctx = ctxs[0];
+  float best = 0;
+  for (int i = 0; i < n; ++i) {
+    lm_ctx* c = ctxs[i];
+    if (!c->t0) {
+      CU(cudaEventCreate(&c->t0));
+      CU(cudaEventCreate(&c->t1));
+    }
+    CU(cudaEventRecord(c->t1, c->stream));
+  }
+  for (int i = 0; i < n; ++i) {
+    CU(cudaEventSynchronize(ctxs[i]->t1));
+    float t = 0;
+    CU(cudaEventElapsedTime(&t, ctxs[0]->t0, ctxs[i]->t1));
+    best = t > best ? t : best;
+  }
+  *ms = best;
+  return LM_OK;
+}
+
 int lm_flush_l2(lm_ctx* ctx, int64_t bytes) {
   if (bytes <= 0) return LM_OK;
   if ((size_t)bytes > ctx->flush_bytes) {
