@@ -406,6 +406,10 @@ def main():
                                                            "geometry": acc["dbg"][1] / max(acc["dbg"][3], 1),
                                                            "hit": acc["dbg"][2] / max(acc["dbg"][3], 1),
                                                            "points": acc["dbg"][3] / args.steps},
+                              "fwd_apply_detail": {"heads_ms": acc["dbg"][8] / args.steps / 1e6,
+                                                   "members_merges_ms": acc["dbg"][9] / args.steps / 1e6,
+                                                   "rounds": acc["dbg"][10] / args.steps,
+                                                   "actions": acc["dbg"][11] / args.steps},
                               "rev_subphase_ms": {"select_actions_preitems": acc["dbg"][7] / args.steps / 1e6,
                                                   "postitems_changed": acc["dbg"][4] / args.steps / 1e6,
                                                   "hitlist": acc["dbg"][5] / args.steps / 1e6,

@@ -123,7 +123,7 @@ typedef struct lm_step_stats { /* CreationStats triangulation.py:49-60 + run_fus
   int64_t rev_passes_redo;    /* reverse-pass items re-evaluated after applies */
   int64_t fuse_bytes_rev;     /* algorithmic bytes of the reverse passes (part of fuse_bytes) */
   int64_t rev_mergeable;      /* acting passes none of whose (or earlier) items the previous apply touched */
-  int64_t dbg[8];             /* diagnostic counters (meaning documented in bench.py) */
+  int64_t dbg[16];            /* diagnostic counters (meaning documented in bench.py) */
 } lm_step_stats;
 
 typedef struct lm_candidate { /* MatchCandidate triangulation.py:41-46 */

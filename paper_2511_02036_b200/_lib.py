@@ -71,7 +71,7 @@ class StepStats(C.Structure):
                 ("first_new_id", i64), ("error", i32), ("n_candidates", i32), ("match_pairs", i64),
                 ("fuse_bytes", i64), ("fuse_passes", i64), ("fuse_points", i64), ("fuse_actions", i64),
                 ("apply_rounds", i64), ("fuse_cycles", i64 * 16),
-                ("rev_passes_acting", i64), ("rev_passes_redo", i64), ("fuse_bytes_rev", i64), ("rev_mergeable", i64), ("dbg", i64 * 8)]
+                ("rev_passes_acting", i64), ("rev_passes_redo", i64), ("fuse_bytes_rev", i64), ("rev_mergeable", i64), ("dbg", i64 * 16)]
 
 
 class Candidate(C.Structure):

@@ -759,7 +759,7 @@ __global__ void k_end(DevMap* maps, const StepArgs* args, lm_step_stats** totals
   t->rev_passes_redo += st->rev_passes_redo;
   t->fuse_bytes_rev += st->fuse_bytes_rev;
   t->rev_mergeable += st->rev_mergeable;
-  for (int k = 0; k < 8; ++k) t->dbg[k] += st->dbg[k];
+  for (int k = 0; k < 16; ++k) t->dbg[k] += st->dbg[k];
   t->first_new_id += 1;  // steps accumulated
 }
 

@@ -1600,6 +1600,10 @@ __global__ void __launch_bounds__(1024, 1) k_fuse_apply(DevMap* maps, const Step
     st->fuse_cycles[13] += tmf[9];   // forward: reserve+check
     st->fuse_cycles[14] += tmf[10] + tmf[11];  // forward: commit (plain + merges)
     st->fuse_cycles[15] += tmf[12];  // forward: compaction
+    st->dbg[8] += tmf[10];           // forward: group leaders (heads)
+    st->dbg[9] += tmf[11];           // forward: members / merges / member pairs
+    st->dbg[10] += rr;               // forward: rounds
+    st->dbg[11] += nact;             // forward: actions
   }
   cl.sync();  // the leader CTA's shared control words stay alive until every CTA is done
 }

@@ -3,6 +3,8 @@
 // globaltimer resolution. nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o latency_probe latency_probe.cu
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 __global__ void k_chain_load(int* p, int n, long long* out) {
   int i = 0;
   long long t0 = clock64();
@@ -51,6 +53,13 @@ __global__ void k_gtimer(long long* out) {
   do { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(b)); } while (b == a);
   out[0] = (long long)(b - a);
 }
+__global__ void k_cluster_sync(int n, long long* out) {
+  cg::cluster_group cl = cg::this_cluster();
+  long long t0 = clock64();
+  for (int k = 0; k < n; ++k) cl.sync();
+  long long t1 = clock64();
+  if (threadIdx.x == 0 && cl.block_rank() == 0) out[0] = (t1 - t0) / n;
+}
 int main() {
   int* p; long long* o; long long h[2];
   cudaMalloc(&p, 1 << 24); cudaMalloc(&o, 64);
@@ -71,6 +80,15 @@ int main() {
   cudaMemset(p, 0, 4);
   k_contended<<<1, 1024>>>(p, 64, o); cudaMemcpy(h, o, 16, cudaMemcpyDeviceToHost);
   printf("1024 threads atomicAdd one word, per iteration: %lld cycles\n", h[0]);
+  for (int cs : {2, 4, 8, 16}) {
+    cudaFuncSetAttribute(k_cluster_sync, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {}; cfg.gridDim = dim3(cs); cfg.blockDim = dim3(1024);
+    cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_cluster_sync, 1 << 12, o); cudaMemcpy(h, o, 8, cudaMemcpyDeviceToHost);
+    printf("cluster.sync, %d CTAs x 1024 threads: %lld cycles (%s)\n", cs, h[0], cudaGetErrorString(cudaGetLastError()));
+  }
   k_gtimer<<<1, 1>>>(o); cudaMemcpy(h, o, 8, cudaMemcpyDeviceToHost); printf("globaltimer tick: %lld ns\n", h[0]);
   int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0); printf("clock %d kHz\n", clk);
   return 0;
