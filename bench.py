@@ -410,6 +410,7 @@ def main():
                                                    "members_merges_ms": acc["dbg"][9] / args.steps / 1e6,
                                                    "rounds": acc["dbg"][10] / args.steps,
                                                    "actions": acc["dbg"][11] / args.steps},
+                              "rev_touched_points_from_post_add_speculation": acc["dbg"][12] / args.steps,
                               "rev_subphase_ms": {"select_actions_preitems": acc["dbg"][7] / args.steps / 1e6,
                                                   "postitems_changed": acc["dbg"][4] / args.steps / 1e6,
                                                   "hitlist": acc["dbg"][5] / args.steps / 1e6,

@@ -541,6 +541,8 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(d.dirty, MP); A(d.dirty_list, MP); A(d.res_pt, MP); A(d.res_slot, KP);
   A(d.res_ex, MP); A(d.res_pair, RES_PAIR); A(d.grp_head, MP);
   A(d.gacc, 3 * MP); A(d.glo, MP); A(d.ghi, MP); A(d.gval, MP); A(d.ver, MP); A(d.hit, MP); A(d.mrg, MP);
+  A(d.sp_tag, MP); A(d.sp_j, MP); A(d.sp_ver0, MP); A(d.sp_nobs0, MP); A(d.sp_hit, MP); A(d.sp_rep, 2 * MP);
+  A(d.sp_geo, 5 * MP);
   A(d.covis, K * K);
   A(d.recent_id, MP); A(d.recent_born, MP);
   A(d.scal, SC_N); A(d.ledger, LG_N);
@@ -564,7 +566,7 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(s.pinfo, 3 * TMAX); A(s.hitpass, (size_t)d.kpkf_max * ((TMAX + 31) / 32)); A(s.pj, (size_t)s.act_cap);
   A(s.pass_of, K); A(s.snap, d.kpkf_max); A(s.chg, d.kpkf_max); A(s.rmark, MP);
   A(s.pmp, (size_t)s.act_cap); A(s.pob, (size_t)s.act_cap); A(s.itag, (size_t)s.act_cap); A(s.ilist, (size_t)s.act_cap);
-  A(s.cands, (size_t)s.act_cap); A(s.cneed, (size_t)s.act_cap); A(s.hl_cnt, d.kpkf_max); A(s.hl, (size_t)d.kpkf_max * HL); A(s.hreg, MP); A(s.upts, (size_t)s.act_cap);
+  A(s.cands, (size_t)s.act_cap); A(s.cneed, (size_t)s.act_cap); A(s.hl_cnt, d.kpkf_max); A(s.hl, (size_t)d.kpkf_max * HL); A(s.hreg, MP); A(s.upts, (size_t)s.act_cap); A(s.sp_list, (size_t)s.act_cap); A(s.sp_obs, (size_t)16 * 8 * (POST_MAXN + 1));
   A(s.abits, (size_t)TMAX * ((d.kpkf_max + 31) / 32));
   A(m->d_stats, 1); A(m->d_totals, 1); A(m->d_result, 4 + 1024 + TMAX);
 #undef A
@@ -578,6 +580,7 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   CU(cudaMemsetAsync(d.s.itag, 0, sizeof(int) * d.s.act_cap, ctx->stream));
   CU(cudaMemsetAsync(d.mrg, 0, sizeof(int2) * MP, ctx->stream));
   CU(cudaMemsetAsync(d.s.hreg, 0, sizeof(int) * MP, ctx->stream));
+  CU(cudaMemsetAsync(d.sp_tag, 0, sizeof(int) * MP, ctx->stream));
   CU(cudaMemsetAsync(d.hit, 0xff, sizeof(int2) * MP, ctx->stream));
   CU(cudaMemsetAsync(s.pass_of, 0xff, sizeof(int) * K, ctx->stream));
   CU(cudaMemsetAsync(s.hitpass, 0, sizeof(unsigned) * d.kpkf_max * ((TMAX + 31) / 32), ctx->stream));
@@ -618,6 +621,7 @@ int lm_map_reset(lm_ctx* ctx, int32_t map) {
   CU(cudaMemsetAsync(d.s.itag, 0, sizeof(int) * d.s.act_cap, ctx->stream));
   CU(cudaMemsetAsync(d.mrg, 0, sizeof(int2) * MP, ctx->stream));
   CU(cudaMemsetAsync(d.s.hreg, 0, sizeof(int) * MP, ctx->stream));
+  CU(cudaMemsetAsync(d.sp_tag, 0, sizeof(int) * MP, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   m->slot_of.clear();
   std::fill(m->state.begin(), m->state.end(), KF_FREE);
@@ -859,12 +863,13 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
     ctx->launches += 2;
   }
   if ((rc = mark())) return rc;
+  k_fuse_post<<<dim3(16, n), 256, 0, ctx->stream>>>(dmaps, dv);
   k_fuse_rev<<<n, REV_THREADS, rev_smem, ctx->stream>>>(dmaps, dv, rev_smem);
   if ((rc = mark())) return rc;
   k_fuse_visible<<<dim3((kpkf + 255) / 256, tfuse, n), 256, 0, ctx->stream>>>(dmaps, dv);
   k_end<<<n, 32, 0, ctx->stream>>>(dmaps, dv, ctx->d_totals);
   if ((rc = mark())) return rc;
-  ctx->launches += 17;
+  ctx->launches += 18;
   if (ctx->prof) ctx->prof_steps.push_back(evs);
   CHECK_LAUNCH();
   CU(cudaEventRecord(ctx->args_ev[e], ctx->stream));
@@ -1522,6 +1527,7 @@ int lm_map_rewind(lm_ctx* ctx, int32_t map) {
   CU(cudaMemsetAsync(d.s.itag, 0, sizeof(int) * d.s.act_cap, st));
   CU(cudaMemsetAsync(d.mrg, 0, sizeof(int2) * MP, st));
   CU(cudaMemsetAsync(d.s.hreg, 0, sizeof(int) * MP, st));
+  CU(cudaMemsetAsync(d.sp_tag, 0, sizeof(int) * MP, st));
   if (m->kp_head) CU(cudaMemsetAsync(d.kbind, 0xff, sizeof(int) * m->kp_head, st));
   if (m->n_slots) {
     k_rewind_state<<<(m->n_slots + 255) / 256, 256, 0, st>>>(d, m->n_slots);

@@ -1455,7 +1455,7 @@ __device__ __forceinline__ long long pass_bytes(long long pts, long long obs, lo
   return 56 * pts + 9 * obs + 53 * tkp + 16 * acts;
 }
 
-enum FuseCtl { FC_T = 0, FC_P = 1, FC_NACT = 2, FC_NU = 3, FC_N = 8 };
+enum FuseCtl { FC_T = 0, FC_P = 1, FC_NACT = 2, FC_NU = 3, FC_NSP = 4, FC_N = 8 };
 
 __global__ void __launch_bounds__(1024) k_fuse_targets(DevMap* maps, const StepArgs* args, int n_slots_max) {
   const StepArgs& A = args[blockIdx.x];
@@ -1649,6 +1649,7 @@ __global__ void __launch_bounds__(256) k_fuse_refresh(DevMap* maps, const StepAr
     if (tid == 0) {
       M.scal[SC_MTAG] += 1;  // merges of this step's reverse phase
       M.s.fctl[FC_NU] = 0;
+      M.s.fctl[FC_NSP] = 0;
     }
   }
   const int n = M.scal[SC_DIRTY_N];
@@ -1773,6 +1774,13 @@ __global__ void __launch_bounds__(256) k_fuse_spec(DevMap* maps, const StepArgs*
     const ItemVal v = eval_item(M, A.cur, t, ts, kp);
     store_item(M, (size_t)t * M.kpkf_max + kp, v);
     if (v.has) atomicOr(&M.s.abits[(size_t)t * ((M.kpkf_max + 31) >> 5) + (kp >> 5)], 1u << (kp & 31));
+    if (v.has && v.a.kind == LM_ACT_ADD) {  // post-ADD state of this point, precomputed by k_fuse_post
+      const int stag = M.scal[SC_MTAG];
+      if (atomicExch(&M.sp_tag[v.mp], stag) != stag) {
+        M.sp_j[v.mp] = v.a.j;
+        M.s.sp_list[atomicAdd(&M.s.fctl[FC_NSP], 1)] = v.mp;
+      }
+    }
     live = v.mp >= 0;
     nob = v.nob;
     has = v.has;
@@ -1786,6 +1794,83 @@ __global__ void __launch_bounds__(256) k_fuse_spec(DevMap* maps, const StepArgs*
     atomicAdd(&M.s.pinfo[PI_LIVE * TMAX + t], live);
     atomicAdd(&M.s.pinfo[PI_OBS * TMAX + t], nob);
     if (has) atomicAdd(&M.s.pinfo[PI_NACT * TMAX + t], has);
+  }
+}
+
+// Speculative post-ADD states. Most reverse-pass actions are ADDs of a point into the
+// current keyframe, and each such point's state after that ADD (observations + (cur, j))
+// is known before the reverse walk starts: its representative descriptor, view geometry
+// and new hit are computed here, wide (warp per point). k_fuse_rev takes them instead of
+// refreshing when the apply did exactly that (one mutation, one observation more, slot j
+// bound to the point: the same observation set).
+constexpr int POST_MAXN = 128;
+__global__ void __launch_bounds__(256) k_fuse_post(DevMap* maps, const StepArgs* args) {
+  const StepArgs& A = args[blockIdx.y];
+  const DevMap& M = maps[A.map];
+  if (!A.do_fuse || M.s.fctl[FC_T] == 0) return;
+  const int nsp = M.s.fctl[FC_NSP];
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * 8 + (threadIdx.x >> 5), nw = gridDim.x * 8;
+  int2* scratch = M.s.sp_obs + (size_t)gw * (POST_MAXN + 1);
+  const int cur = A.cur;
+  const TgtView T = tgt_global(M, cur);
+  for (int k = gw; k < nsp; k += nw) {
+    const int p = M.s.sp_list[k];
+    const int n0 = M.nobs[p], j = M.sp_j[p];
+    if (!M.alive[p] || n0 + 1 > POST_MAXN) {
+      if (lane == 0) M.sp_ver0[p] = -1;
+      continue;
+    }
+    if (!M.gval[p]) geo_full_warp(M, p, lane);  // (current-state cache: a pure function)
+    const int2* o = M.obs + M.ooff[p];
+    for (int e = lane; e < n0; e += 32) scratch[e] = o[e];
+    if (lane == 0) scratch[n0] = make_int2(cur, j);
+    __syncwarp();
+    refresh_rep_list(M, scratch, n0 + 1, M.sp_rep + 2 * (size_t)p, lane);
+    __syncwarp();
+    // geometry: the current keyframe is the newest, so its term extends the sums exactly
+    double ax = M.gacc[3 * p], ay = M.gacc[3 * p + 1], az = M.gacc[3 * p + 2], lo = M.glo[p], hi = M.ghi[p];
+    const double rx = M.pos[3 * p] - M.C[3 * cur], ry = M.pos[3 * p + 1] - M.C[3 * cur + 1];
+    const double rz = M.pos[3 * p + 2] - M.C[3 * cur + 2];
+    const double dd = sqrt(rx * rx + ry * ry + rz * rz);
+    if (dd > 0) {
+      const double d0 = dd / M.S[M.klev[M.kp_off[cur] + j]];
+      lo = d0 < lo ? d0 : lo;
+      hi = d0 > hi ? d0 : hi;
+      ax = ax + rx / dd;
+      ay = ay + ry / dd;
+      az = az + rz / dd;
+    }
+    PGeo g;
+    g.ok = 0;
+    if (isfinite(lo)) {
+      const double nrm = sqrt(ax * ax + ay * ay + az * az);
+      g.vx = nrm > 0 ? ax / nrm : ax;
+      g.vy = nrm > 0 ? ay / nrm : ay;
+      g.vz = nrm > 0 ? az / nrm : az;
+      g.x = M.pos[3 * p];
+      g.y = M.pos[3 * p + 1];
+      g.z = M.pos[3 * p + 2];
+      g.d0 = lo;
+      g.blo = lo / A.fc.dist_band_slack;
+      g.bhi = hi * M.S[M.L - 1] * A.fc.dist_band_slack;
+      g.r0 = M.sp_rep[2 * (size_t)p];
+      g.r1 = M.sp_rep[2 * (size_t)p + 1];
+      g.ok = 1;
+    }
+    const int hit = gather_hit_warp(M, A.fc, g, cur, T, lane);
+    if (lane == 0) {
+      double* sg = M.sp_geo + 5 * (size_t)p;
+      sg[0] = ax;
+      sg[1] = ay;
+      sg[2] = az;
+      sg[3] = lo;
+      sg[4] = hi;
+      M.sp_hit[p] = hit;
+      M.sp_ver0[p] = M.ver[p];
+      M.sp_nobs0[p] = n0;
+    }
+    __syncwarp();
   }
 }
 
@@ -2016,6 +2101,28 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
         // a touched point without items in later passes keeps its dirty flag (the next
         // step's refresh picks it up) and a stale hit (nothing reads it: the version differs)
         if (!M.alive[p] || !M.s.cneed[k]) continue;
+        if (M.sp_tag[p] == M.scal[SC_MTAG] && M.sp_ver0[p] >= 0 && M.ver[p] == M.sp_ver0[p] + 1 &&
+            M.nobs[p] == M.sp_nobs0[p] + 1 && M.kbind[cur_off + M.sp_j[p]] == p) {
+          // the apply did exactly the speculated ADD: same observation set as k_fuse_post's
+          // (the list is sorted: clean before, the current keyframe appended last)
+          if (lane == 0) {
+            M.rep[2 * (size_t)p] = M.sp_rep[2 * (size_t)p];
+            M.rep[2 * (size_t)p + 1] = M.sp_rep[2 * (size_t)p + 1];
+            const double* sg = M.sp_geo + 5 * (size_t)p;
+            M.gacc[3 * p] = sg[0];
+            M.gacc[3 * p + 1] = sg[1];
+            M.gacc[3 * p + 2] = sg[2];
+            M.glo[p] = sg[3];
+            M.ghi[p] = sg[4];
+            M.gval[p] = 1;
+            M.dirty[p] = 0;
+            M.hit[p] = make_int2(M.ver[p], M.sp_hit[p]);
+            hit_list_add(M, M.sp_hit[p], p);
+            atomicAdd((unsigned long long*)&M.s.stats->dbg[12], 1ull);
+          }
+          __syncwarp();
+          continue;
+        }
         const long long c0 = clock64();
         if (M.dirty[p]) {
           refresh_rep_warp(M, p, lane);

@@ -123,6 +123,8 @@ struct Scratch {
   int* hl;               // [kpkf_max*HL] ... (ids; entries whose hit moved are skipped)
   int* hreg;             // [mp_cap] step tag: point already listed by the speculative scan
   int* upts;             // [act_cap] distinct bound points of all reverse passes
+  int* sp_list;          // [act_cap] points with a speculative reverse-pass ADD
+  int2* sp_obs;          // [POST_WARPS*(POST_MAXN+1)] per-warp virtual observation lists
   unsigned* abits;       // [TMAX*ceil(kpkf_max/32)] per pass: keypoints whose item has an action
   int* act_flag;         // [TMAX*kpkf_max]
   int* vis_flag;         // [TMAX*kpkf_max]
@@ -180,6 +182,15 @@ struct DevMap {
   unsigned char* gval;
   int* ver;          // bumped on every observation change (speculative reverse gather)
   int2* mrg;         // loser -> {merge tag, winner}: deferred visible bumps follow it (SC_MTAG)
+  // speculative post-ADD state of points with a reverse-pass ADD (k_fuse_post), valid when
+  // sp_tag == SC_MTAG and the point changed exactly by that ADD
+  int* sp_tag;
+  int* sp_j;
+  int* sp_ver0;
+  int* sp_nobs0;
+  int* sp_hit;
+  uint4* sp_rep;     // [mp_cap*2]
+  double* sp_geo;    // [mp_cap*5] gacc xyz, lo, hi
   int2* hit;         // per point: {version, hit into the current keyframe (-2/-1/j)}
   // deterministic-reservation tables (apply): round-tagged min action index per entity
   unsigned long long* res_pt;    // [mp_cap]
@@ -771,9 +782,7 @@ __device__ int kth_smallest(unsigned short* d, int n, int k) {
 
 // sort the observation list of mp by keyframe id (warp-cooperative rank scatter; ids are
 // distinct). Lists longer than 128 fall back to an insertion sort on lane 0.
-__device__ void sort_obs_warp(const DevMap& M, int mp, int lane) {
-  int2* o = M.obs + M.ooff[mp];
-  const int n = M.nobs[mp];
+__device__ void sort_obs_warp(const DevMap& M, int2* o, int n, int lane) {
   if (n <= 1) return;
   if (n > 128) {
     if (lane == 0)
@@ -873,108 +882,14 @@ __device__ __forceinline__ int plane_select(const unsigned (&pl)[9][NW], unsigne
   return v;
 }
 
-// refresh for 3 <= n <= 32*NW observations, in registers: lane l holds observations l,
-// l+32, ... (entry, kf-id key, descriptor). For each of its rows a lane builds the 9
-// bit-planes of the row's distances from broadcast descriptors, and radix-selects the two
-// middle order statistics of the n-1 non-self distances; the warp minimum of
-// (med2 << 16 | kf-id rank) is the reference's first argmin of the median (ties -> lower
-// kf id). The list is written back sorted by keyframe id.
-template <int NW>
-__device__ void refresh_rep_planes(const DevMap& M, int mp, int n, int lane) {
-  int2* o = M.obs + M.ooff[mp];
-  int2 e[NW];
-  long long key[NW];
-  uint4 d0[NW], d1[NW];
-#pragma unroll
-  for (int s = 0; s < NW; ++s) e[s] = s * 32 + lane < n ? o[s * 32 + lane] : make_int2(0, 0);
-#pragma unroll
-  for (int s = 0; s < NW; ++s) {
-    const bool act = s * 32 + lane < n;
-    key[s] = act ? M.kf_id[e[s].x] : 0x7fffffffffffffffll;
-    const int g = M.kp_off[e[s].x] + e[s].y;
-    d0[s] = act ? M.kdesc[2 * g] : make_uint4(0, 0, 0, 0);
-    d1[s] = act ? M.kdesc[2 * g + 1] : make_uint4(0, 0, 0, 0);
-  }
-  int rk[NW];
-#pragma unroll
-  for (int s = 0; s < NW; ++s) rk[s] = 0;
-#pragma unroll
-  for (int sb = 0; sb < NW; ++sb)
-    for (int l = 0; l < 32; ++l) {
-      const long long kb = __shfl_sync(0xffffffffu, key[sb], l);
-#pragma unroll
-      for (int s = 0; s < NW; ++s) rk[s] += kb < key[s];
-    }
-  __syncwarp();
-#pragma unroll
-  for (int s = 0; s < NW; ++s)
-    if (s * 32 + lane < n) o[rk[s]] = e[s];
-  const int m = n - 1, k0 = (m - 1) >> 1, k1 = m >> 1;
-  unsigned best = 0xffffffffu;
-#pragma unroll
-  for (int s = 0; s < NW; ++s) {  // row slot s of every lane
-    unsigned pl[9][NW];
-#pragma unroll
-    for (int bit = 0; bit < 9; ++bit)
-#pragma unroll
-      for (int w = 0; w < NW; ++w) pl[bit][w] = 0u;
-#pragma unroll
-    for (int sb = 0; sb < NW; ++sb)
-      for (int l = 0; l < 32; ++l) {
-        uint4 b0, b1;
-        b0.x = __shfl_sync(0xffffffffu, d0[sb].x, l);
-        b0.y = __shfl_sync(0xffffffffu, d0[sb].y, l);
-        b0.z = __shfl_sync(0xffffffffu, d0[sb].z, l);
-        b0.w = __shfl_sync(0xffffffffu, d0[sb].w, l);
-        b1.x = __shfl_sync(0xffffffffu, d1[sb].x, l);
-        b1.y = __shfl_sync(0xffffffffu, d1[sb].y, l);
-        b1.z = __shfl_sync(0xffffffffu, d1[sb].z, l);
-        b1.w = __shfl_sync(0xffffffffu, d1[sb].w, l);
-        const unsigned dist = (unsigned)hamming(d0[s], d1[s], b0, b1);
-#pragma unroll
-        for (int bit = 0; bit < 9; ++bit) pl[bit][sb] |= ((dist >> bit) & 1u) << l;
-      }
-    const int i = s * 32 + lane;
-    if (i < n) {
-      unsigned cand[NW];
-#pragma unroll
-      for (int w = 0; w < NW; ++w) {  // the other real observations
-        const int lo = w * 32;
-        unsigned msk = n - lo >= 32 ? 0xffffffffu : (n - lo <= 0 ? 0u : (1u << (n - lo)) - 1u);
-        if (i >= lo && i < lo + 32) msk &= ~(1u << (i - lo));
-        cand[w] = msk;
-      }
-      unsigned c2[NW];
-#pragma unroll
-      for (int w = 0; w < NW; ++w) c2[w] = cand[w];
-      const int v0 = plane_select<NW>(pl, cand, k0);
-      const int v1 = k1 == k0 ? v0 : plane_select<NW>(pl, c2, k1);
-      const unsigned kk = ((unsigned)(v0 + v1) << 16) | (unsigned)rk[s];
-      best = kk < best ? kk : best;
-    }
-  }
-  for (int off = 16; off; off >>= 1) {
-    const unsigned other = __shfl_xor_sync(0xffffffffu, best, off);
-    best = other < best ? other : best;
-  }
-#pragma unroll
-  for (int s = 0; s < NW; ++s)
-    if (s * 32 + lane < n && rk[s] == (int)(best & 0xffffu)) {
-      M.rep[2 * mp] = d0[s];
-      M.rep[2 * mp + 1] = d1[s];
-    }
-  __syncwarp();
-}
-
-// Symmetric variant of refresh_rep_planes: d(a, b) = d(b, a), so every unordered pair is
+// Representative descriptor, all in registers (3 <= n <= 32*NW): d(a, b) = d(b, a), so every unordered pair is
 // popcounted once. Row slot s of lane l is observation 32*s + l. Diagonal blocks (s, s):
 // in step r (1..16) lane l computes d(l, l+r mod 32) for its own row and hands it to lane
 // l+r (shuffle) for that lane's row; off-diagonal blocks (s1 < s2): in step r (0..31) lane l
 // computes d(32*s1 + l, 32*s2 + (l+r mod 32)) and hands it to lane l+r's row slot s2. Half the
 // popcounts of the row-by-row version (the pipe that bounds it, 16 lanes/clk/SM).
 template <int NW>
-__device__ void refresh_rep_sym(const DevMap& M, int mp, int n, int lane) {
-  int2* o = M.obs + M.ooff[mp];
+__device__ void refresh_rep_sym(const DevMap& M, int2* o, int n, uint4* rep, int lane) {
   int2 e[NW];
   long long key[NW];
   uint4 d0[NW], d1[NW];
@@ -1066,8 +981,8 @@ __device__ void refresh_rep_sym(const DevMap& M, int mp, int n, int lane) {
 #pragma unroll
   for (int s = 0; s < NW; ++s)
     if (s * 32 + lane < n && rk[s] == (int)(best & 0xffffu)) {
-      M.rep[2 * mp] = d0[s];
-      M.rep[2 * mp + 1] = d1[s];
+      rep[0] = d0[s];
+      rep[1] = d1[s];
     }
   __syncwarp();
 }
@@ -1077,8 +992,7 @@ __device__ void refresh_rep_sym(const DevMap& M, int mp, int n, int lane) {
 // descriptors (no dependent global loads), its two middle order statistics from a
 // quickselect over a per-lane scratch row (L1-resident local memory).
 template <int NS>
-__device__ void refresh_rep_lanes(const DevMap& M, int mp, int n, int lane) {
-  int2* o = M.obs + M.ooff[mp];
+__device__ void refresh_rep_lanes(const DevMap& M, int2* o, int n, uint4* rep, int lane) {
   int2 e[NS];
   long long key[NS];
   uint4 d0[NS], d1[NS];
@@ -1150,28 +1064,25 @@ __device__ void refresh_rep_lanes(const DevMap& M, int mp, int n, int lane) {
 #pragma unroll
   for (int s = 0; s < NS; ++s)
     if (s * 32 + lane < n && rk[s] == (int)(best & 0xffffu)) {
-      M.rep[2 * mp] = d0[s];
-      M.rep[2 * mp + 1] = d1[s];
+      rep[0] = d0[s];
+      rep[1] = d1[s];
     }
   __syncwarp();
 }
 
-__device__ void refresh_rep_warp(const DevMap& M, int mp, int lane) {
-  {
-    const int n = M.nobs[mp];
-    if (n >= 3 && n <= 32) return refresh_rep_sym<1>(M, mp, n, lane);
-    if (n >= 33 && n <= 64) return refresh_rep_sym<2>(M, mp, n, lane);
-    if (n >= 65 && n <= 128) return refresh_rep_lanes<4>(M, mp, n, lane);
-  }
-  sort_obs_warp(M, mp, lane);
-  const int n = M.nobs[mp];
+// _refresh_rep_descriptor of the observation list o[0..n) (sorted in place by keyframe id),
+// result into rep[0..1]; one warp
+__device__ void refresh_rep_list(const DevMap& M, int2* o, int n, uint4* rep, int lane) {
+  if (n >= 3 && n <= 32) return refresh_rep_sym<1>(M, o, n, rep, lane);
+  if (n >= 33 && n <= 64) return refresh_rep_sym<2>(M, o, n, rep, lane);
+  if (n >= 65 && n <= 128) return refresh_rep_lanes<4>(M, o, n, rep, lane);
+  sort_obs_warp(M, o, n, lane);
   if (n == 0) return;
-  const int2* o = M.obs + M.ooff[mp];
   if (n <= 2) {  // one observation, or two (equal medians -> the first)
     if (lane == 0) {
       const int g = M.kp_off[o[0].x] + o[0].y;
-      M.rep[2 * mp] = M.kdesc[2 * g];
-      M.rep[2 * mp + 1] = M.kdesc[2 * g + 1];
+      rep[0] = M.kdesc[2 * g];
+      rep[1] = M.kdesc[2 * g + 1];
     }
     __syncwarp();
     return;
@@ -1208,10 +1119,14 @@ __device__ void refresh_rep_warp(const DevMap& M, int mp, int lane) {
   if (lane == 0) {
     const int a = best & 0xffff;
     const int g = M.kp_off[o[a].x] + o[a].y;
-    M.rep[2 * mp] = M.kdesc[2 * g];
-    M.rep[2 * mp + 1] = M.kdesc[2 * g + 1];
+    rep[0] = M.kdesc[2 * g];
+    rep[1] = M.kdesc[2 * g + 1];
   }
   __syncwarp();
+}
+
+__device__ void refresh_rep_warp(const DevMap& M, int mp, int lane) {
+  refresh_rep_list(M, M.obs + M.ooff[mp], M.nobs[mp], M.rep + 2 * (size_t)mp, lane);
 }
 
 }  // namespace lm
