@@ -1911,7 +1911,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   __shared__ long long tm[16];
   __shared__ PairAcc acc;
   __shared__ int s_nact[TMAX], s_live[TMAX], s_obs[TMAX];
-  __shared__ int t1_sh, nc_sh, ni_sh, tag_sh, tmin_sh, na_sh, nchg_sh;
+  __shared__ int t1_sh, nc_sh, ni_sh, tag_sh, tmin_sh, na_sh, nchg_sh, fast_sh;
   __shared__ double cur_pose[22];  // R, t, C, cam, cell size of the current keyframe
   if (threadIdx.x < 22) {
     const int c = A.cur, k = threadIdx.x;
@@ -2006,6 +2006,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
           na += __shfl_sync(0xffffffffu, pre, 31);
         }
         __syncwarp();
+        bool simple = na <= 32;  // every action a plain ADD into a distinct keypoint
         for (int k = lane; k < na; k += 32) {
           const ActRec x = M.s.acts[k];
           const int cand[3] = {x.pid, x.other, M.kbind[cur_off + x.j]};
@@ -2015,6 +2016,12 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
             if (p >= 0 && atomicExch(&M.s.rmark[p], tg) != tg) M.s.cands[atomicAdd(&nc_sh, 1)] = p;
           }
         }
+        if (simple) {
+          const ActRec x = lane < na ? M.s.acts[lane] : ActRec{0, 0, -1 - lane, 0, LM_ACT_ADD};
+          const unsigned same = __match_any_sync(0xffffffffu, x.j);
+          simple = __all_sync(0xffffffffu, x.kind == LM_ACT_ADD && __popc(same) == 1);
+        }
+        if (lane == 0) fast_sh = simple;
       }
       if (lane == 0) {
         t1_sh = t1;
@@ -2045,10 +2052,27 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       }
       return __any_sync(0xffffffffu, any);
     };
-    for (int k = wid; k < ncand; k += REV_THREADS / 32) add_point_items(M.s.cands[k]);  // before the apply
-    __syncthreads();
-    if (threadIdx.x == 0) tm[7] += gtime() - ta;
-    rounds += apply_block<REV_THREADS>(M, M.s.acts, na, cnt, sh, &acc, tm);  // (barriers)
+    if (fast_sh) {
+      // every action a plain ADD of a distinct point into a distinct unbound keypoint (the
+      // pass's item is current, so slot j is free and the point does not see the current
+      // keyframe): the actions touch disjoint entities and commute; apply them directly.
+      // An ADD only adds an observation, so the touched points' items are collected after.
+      for (int k = threadIdx.x; k < na; k += REV_THREADS) {
+        const ActRec x = M.s.acts[k];
+        link(M, x.pid, cur, x.j, &acc, true);
+      }
+      if (threadIdx.x == 0) {
+        cnt[1] += na;
+        ++rounds;
+        tm[7] += gtime() - ta;
+      }
+      __syncthreads();
+    } else {
+      for (int k = wid; k < ncand; k += REV_THREADS / 32) add_point_items(M.s.cands[k]);  // before the apply
+      __syncthreads();
+      if (threadIdx.x == 0) tm[7] += gtime() - ta;
+      rounds += apply_block<REV_THREADS>(M, M.s.acts, na, cnt, sh, &acc, tm);  // (barriers)
+    }
     if (threadIdx.x == 0) tm[2] += gtime() - ta;
     // (2) after the apply: the touched points' items, and the points hitting a current
     //     keypoint whose binding changed (hit list; a keypoint whose list overflowed falls
