@@ -411,6 +411,9 @@ def main():
                                                    "rounds": acc["dbg"][10] / args.steps,
                                                    "actions": acc["dbg"][11] / args.steps},
                               "rev_touched_points_from_post_add_speculation": acc["dbg"][12] / args.steps,
+                              "culled": acc["culled"] / args.steps,
+                              "cull_probation_entries": acc["dbg"][13] / args.steps,
+                              "cull_kills_over_8_obs": acc["dbg"][14] / args.steps,
                               "rev_subphase_ms": {"select_actions_preitems": acc["dbg"][7] / args.steps / 1e6,
                                                   "postitems_changed": acc["dbg"][4] / args.steps / 1e6,
                                                   "hitlist": acc["dbg"][5] / args.steps / 1e6,

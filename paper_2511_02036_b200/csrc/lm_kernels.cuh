@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
   pair_acc_init<1024>(&acc, A.cur);
   const int n = M.scal[SC_RECENT_N];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int kept = 0, culled = 0;
+  int kept = 0, culled = 0, nbig_total = 0;
   for (int base = 0; base < n; base += 1024) {
     const int e = base + threadIdx.x;
     int keep = 0, kill = 0, id = -1, born = 0;
@@ -196,17 +196,20 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
     __syncthreads();
     for (int k = threadIdx.x; k < tk; k += 1024) {  // independent points: low degree per thread
       const int mp = kills[k];
-      if (M.nobs[mp] <= 8) kill_point_thread(M, mp, &acc);
+      if (M.nobs[mp] <= 8) kill_point_thread<8>(M, mp, &acc);
       else big[atomicAdd(&nbig, 1)] = mp;
     }
     __syncthreads();
     for (int k = wid; k < nbig; k += 32) kill_point_warp(M, big[k], lane, &acc);
+    nbig_total += nbig;
     __syncthreads();
   }
   pair_acc_flush<1024>(M, &acc);
   if (threadIdx.x == 0) {
     M.scal[SC_RECENT_N] = kept;
     M.s.stats->culled = culled;
+    M.s.stats->dbg[13] += n;  // diagnostics: probation list length
+    M.s.stats->dbg[14] += nbig_total;
   }
 }
 

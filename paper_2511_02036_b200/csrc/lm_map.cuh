@@ -609,22 +609,27 @@ __device__ void covis_cross_warp(const DevMap& M, const int2* oa, int na, const 
   for (int q = lane; q < na * nb; q += 32) covis_add(M, oa[q / nb].x, ob[q % nb].x, d, acc);
 }
 
-// kill_map_point (mapmodel.py:233-237) of a point with at most 8 observations, one thread
+// kill_map_point (mapmodel.py:233-237) of a point with at most KT observations, one thread
+template <int KT>
 __device__ void kill_point_thread(const DevMap& M, int mp, PairAcc* acc) {
   const int2* o = M.obs + M.ooff[mp];
   const int n = M.nobs[mp];
-  int2 e[8];
+  int sl[KT], kp[KT];
 #pragma unroll
-  for (int k = 0; k < 8; ++k)
-    if (k < n) e[k] = o[k];
+  for (int k = 0; k < KT; ++k)
+    if (k < n) {
+      const int2 e = o[k];
+      sl[k] = e.x;
+      kp[k] = e.y;
+    }
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
+  for (int a = 0; a < KT; ++a)
 #pragma unroll
-    for (int b = a + 1; b < 8; ++b)
-      if (b < n) covis_add(M, e[a].x, e[b].x, -1, acc);
+    for (int b = a + 1; b < KT; ++b)
+      if (b < n) covis_add(M, sl[a], sl[b], -1, acc);
 #pragma unroll
-  for (int k = 0; k < 8; ++k)
-    if (k < n) M.kbind[M.kp_off[e[k].x] + e[k].y] = -1;
+  for (int k = 0; k < KT; ++k)
+    if (k < n) M.kbind[M.kp_off[sl[k]] + kp[k]] = -1;
   for (int l = 0; l < M.L; ++l) M.counts[(size_t)mp * M.L + l] = 0;
   M.nobs[mp] = 0;
   M.alive[mp] = 0;
