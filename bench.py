@@ -402,10 +402,10 @@ def main():
                               "rev_items_reevaluated": acc["rev_passes_redo"] / args.steps,
                               "rev_acting_passes_untouched_by_previous_apply": acc["rev_mergeable"] / args.steps,
                               "rev_points_recomputed": acc["fuse_cycles"][1] / args.steps,
-                              "rev_touched_point_cycles": {"refresh": acc["dbg"][0] / max(acc["dbg"][3], 1),
-                                                           "geometry": acc["dbg"][1] / max(acc["dbg"][3], 1),
-                                                           "hit": acc["dbg"][2] / max(acc["dbg"][3], 1),
-                                                           "points": acc["dbg"][3] / args.steps},
+                              "cull_phase_ms": {"init": acc["dbg"][0] / args.steps / 1e6,
+                                                "classify": acc["dbg"][1] / args.steps / 1e6,
+                                                "kills": acc["dbg"][2] / args.steps / 1e6,
+                                                "flush": acc["dbg"][3] / args.steps / 1e6},
                               "fwd_apply_detail": {"heads_ms": acc["dbg"][8] / args.steps / 1e6,
                                                    "members_merges_ms": acc["dbg"][9] / args.steps / 1e6,
                                                    "rounds": acc["dbg"][10] / args.steps,

@@ -460,6 +460,7 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
   CU(cudaFuncSetAttribute(k_fuse_rev, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   CU(cudaFuncSetAttribute(k_op, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
   CU(cudaFuncSetAttribute(k_fuse_apply, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CU(cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, CULL_DYN_SMEM));
   if (const char* e = getenv("LM_APPLY_CLUSTER")) {
     const int v = atoi(e);
     ctx->apply_cluster = v < 1 ? 1 : (v > 16 ? 16 : v);
@@ -815,7 +816,7 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   k_begin<<<n, 128, 0, ctx->stream>>>(dmaps, dv);
   k_insert<<<n, 256, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;
-  k_cull<<<n, 1024, 0, ctx->stream>>>(dmaps, dv);
+  k_cull<<<n, 1024, CULL_DYN_SMEM, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;
   k_select<<<n, 256, dyn, ctx->stream>>>(dmaps, dv, slots);
   if ((rc = mark())) return rc;

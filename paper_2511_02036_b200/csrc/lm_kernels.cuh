@@ -156,6 +156,8 @@ __global__ void __launch_bounds__(256) k_insert(DevMap* maps, const StepArgs* ar
 
 // ---------------------------------------------------------------------------------- cull
 
+constexpr int CULL_DYN_SMEM = (3 * 1024 + PAIR_W * 32) * 4;  // kill rows + transposed columns
+
 __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* args) {
   const StepArgs& A = args[blockIdx.x];
   const DevMap& M = maps[A.map];
@@ -163,8 +165,15 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
   __shared__ int sh[32];
   __shared__ PairAcc acc;
   __shared__ int kills[1024], big[1024];
-  __shared__ int nbig;
+  __shared__ int nbig, nact_sh;
+  extern __shared__ unsigned cull_dyn[];
+  unsigned* krow = cull_dyn;                 // [3*1024] per kill: observer window mask
+  unsigned* kcol = cull_dyn + 3 * 1024;      // [PAIR_W*32] per window slot: mask over the kills
+  __shared__ int kact[PAIR_W], kidx[PAIR_W];
+  const long long c_t0 = gtime();
   pair_acc_init<1024>(&acc, A.cur);
+  const long long c_t1 = gtime();
+  long long c_scan = 0, c_kill = 0;
   const int n = M.scal[SC_RECENT_N];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int kept = 0, culled = 0, nbig_total = 0;
@@ -194,22 +203,77 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
     culled += tk;
     if (threadIdx.x == 0) nbig = 0;
     __syncthreads();
-    for (int k = threadIdx.x; k < tk; k += 1024) {  // independent points: low degree per thread
-      const int mp = kills[k];
-      if (M.nobs[mp] <= 8) kill_point_thread<8>(M, mp, &acc);
-      else big[atomicAdd(&nbig, 1)] = mp;
+    const long long c_a = gtime();
+    // independent points, warp each: bindings and counters cleared, the observer set as a
+    // window bitmask (rows); the covisibility decrements of all of them are the pair counts
+    // of the rows' Gram matrix, counted with popcounts over the transposed masks instead of
+    // one contended shared atomic per observer pair. Kills with an observer outside the
+    // window take the per-pair path.
+    for (int k = threadIdx.x; k < tk; k += 1024) {
+      if (!kill_point_rows_thread(M, kills[k], &acc, &krow[3 * k])) {
+        krow[3 * k] = krow[3 * k + 1] = krow[3 * k + 2] = 0u;
+        big[atomicAdd(&nbig, 1)] = kills[k];
+      }
     }
     __syncthreads();
-    for (int k = wid; k < nbig; k += 32) kill_point_warp(M, big[k], lane, &acc);
+    for (int k = wid; k < nbig; k += 32) kill_point_warp(M, big[k], lane, &acc);  // outside the window
     nbig_total += nbig;
+    {
+      // transpose: column mask of window slot a over the kills (warp w: kills 32w..32w+31)
+      const int nkw = (tk + 31) >> 5;
+      for (int w = wid; w < nkw; w += 32) {
+        const int k = 32 * w + lane;
+        const unsigned r0 = k < tk ? krow[3 * k] : 0u, r1 = k < tk ? krow[3 * k + 1] : 0u;
+        const unsigned r2 = k < tk ? krow[3 * k + 2] : 0u;
+        for (int a = 0; a < PAIR_W; ++a) {
+          const unsigned bit = a < 32 ? (r0 >> a) & 1u : a < 64 ? (r1 >> (a - 32)) & 1u : (r2 >> (a - 64)) & 1u;
+          const unsigned col = __ballot_sync(0xffffffffu, bit);
+          if (lane == 0) kcol[a * 32 + w] = col;
+        }
+      }
+      __syncthreads();
+      // slots with any killed observer, then their pairs
+      if (threadIdx.x < PAIR_W) {
+        unsigned any = 0u;
+        for (int w = 0; w < nkw; ++w) any |= kcol[threadIdx.x * 32 + w];
+        kact[threadIdx.x] = any != 0u;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int m = 0;
+        for (int a = 0; a < PAIR_W; ++a)
+          if (kact[a]) kidx[m++] = a;
+        nact_sh = m;
+      }
+      __syncthreads();
+      const int m = nact_sh, np = m * (m - 1) / 2;
+      for (int q = threadIdx.x; q < np; q += 1024) {
+        int i = 0, rem = q;  // q -> (i < j) over the active slots
+        while (rem >= m - 1 - i) {
+          rem -= m - 1 - i;
+          ++i;
+        }
+        const int a = kidx[i], b = kidx[i + 1 + rem];
+        int c = 0;
+        for (int w = 0; w < nkw; ++w) c += __popc(kcol[a * 32 + w] & kcol[b * 32 + w]);
+        if (c) atomicAdd(&acc.win[tri_index(a, b)], -c);
+      }
+    }
     __syncthreads();
+    c_kill += gtime() - c_a;
   }
+  const long long c_t2 = gtime();
   pair_acc_flush<1024>(M, &acc);
+  const long long c_t3 = gtime();
   if (threadIdx.x == 0) {
     M.scal[SC_RECENT_N] = kept;
     M.s.stats->culled = culled;
     M.s.stats->dbg[13] += n;  // diagnostics: probation list length
     M.s.stats->dbg[14] += nbig_total;
+    M.s.stats->dbg[0] += c_t1 - c_t0;            // cull: accumulator init (ns)
+    M.s.stats->dbg[1] += c_t2 - c_t1 - c_kill;   // cull: classification + compaction
+    M.s.stats->dbg[2] += c_kill;                 // cull: kills
+    M.s.stats->dbg[3] += c_t3 - c_t2;            // cull: covisibility flush
   }
 }
 
@@ -2166,11 +2230,10 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
           M.hit[p] = make_int2(M.ver[p], j);
           hit_list_add(M, j, p);
           const long long c3 = clock64();
-          unsigned long long* dbg = (unsigned long long*)M.s.stats->dbg;  // diagnostics (cycles)
-          atomicAdd(&dbg[0], (unsigned long long)(c1 - c0));
-          atomicAdd(&dbg[1], (unsigned long long)(c2 - c1));
-          atomicAdd(&dbg[2], (unsigned long long)(c3 - c2));
-          atomicAdd(&dbg[3], 1ull);
+          (void)c0;
+          (void)c1;
+          (void)c2;
+          (void)c3;
         }
         __syncwarp();
       } else {

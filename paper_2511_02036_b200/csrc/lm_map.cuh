@@ -637,6 +637,80 @@ __device__ void kill_point_thread(const DevMap& M, int mp, PairAcc* acc) {
   M.ver[mp] += 1;
 }
 
+// kill_map_point without its covisibility update, for a batch of kills whose observers all
+// lie in the accumulator's window: the point's observer set goes to row[0..2] (96-bit mask
+// over window slots) and the caller subtracts the pair counts of all rows at once (a Gram
+// matrix of the masks). Returns false (nothing done) when an observer is outside the window.
+__device__ bool kill_point_rows_warp(const DevMap& M, int mp, int lane, const PairAcc* acc, unsigned* row) {
+  const int2* o = M.obs + M.ooff[mp];
+  const int n = M.nobs[mp];
+  unsigned r[3] = {0u, 0u, 0u};
+  bool inside = true;
+  for (int k = lane; k < n; k += 32) {
+    const int w = o[k].x - acc->wbase;
+    inside &= w >= 0 && w < PAIR_W;
+    if (w >= 0 && w < PAIR_W) r[w >> 5] |= 1u << (w & 31);
+  }
+  if (!__all_sync(0xffffffffu, inside)) return false;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) r[q] = __reduce_or_sync(0xffffffffu, r[q]);
+  for (int k = lane; k < n; k += 32) M.kbind[M.kp_off[o[k].x] + o[k].y] = -1;
+  for (int l = lane; l < M.L; l += 32) M.counts[(size_t)mp * M.L + l] = 0;
+  __syncwarp();
+  if (lane == 0) {
+    row[0] = r[0];
+    row[1] = r[1];
+    row[2] = r[2];
+    M.nobs[mp] = 0;
+    M.alive[mp] = 0;
+    M.gval[mp] = 0;
+    M.ver[mp] += 1;
+  }
+  __syncwarp();
+  return true;
+}
+
+// the same, one thread (entries loaded 8 at a time)
+__device__ bool kill_point_rows_thread(const DevMap& M, int mp, const PairAcc* acc, unsigned* row) {
+  const int2* o = M.obs + M.ooff[mp];
+  const int n = M.nobs[mp];
+  unsigned r0 = 0u, r1 = 0u, r2 = 0u;
+  for (int k0 = 0; k0 < n; k0 += 8) {
+    int2 e[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) e[j] = k0 + j < n ? o[k0 + j] : make_int2(acc->wbase, 0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (k0 + j >= n) continue;
+      const int w = e[j].x - acc->wbase;
+      if (w < 0 || w >= PAIR_W) return false;
+      r0 |= w < 32 ? 1u << w : 0u;
+      r1 |= w >= 32 && w < 64 ? 1u << (w - 32) : 0u;
+      r2 |= w >= 64 ? 1u << (w - 64) : 0u;
+    }
+  }
+  for (int k0 = 0; k0 < n; k0 += 8) {
+    int2 e[8];
+    int g[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) e[j] = k0 + j < n ? o[k0 + j] : make_int2(0, 0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) g[j] = k0 + j < n ? M.kp_off[e[j].x] + e[j].y : 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (k0 + j < n) M.kbind[g[j]] = -1;
+  }
+  for (int l = 0; l < M.L; ++l) M.counts[(size_t)mp * M.L + l] = 0;
+  row[0] = r0;
+  row[1] = r1;
+  row[2] = r2;
+  M.nobs[mp] = 0;
+  M.alive[mp] = 0;
+  M.gval[mp] = 0;
+  M.ver[mp] += 1;
+  return true;
+}
+
 // kill_map_point (mapmodel.py:233-237), all lanes of a warp call it with the same mp
 __device__ void kill_point_warp(const DevMap& M, int mp, int lane, PairAcc* acc) {
   const int2* o = M.obs + M.ooff[mp];
