@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
   __shared__ int nbig, nact_sh;
   extern __shared__ unsigned cull_dyn[];
   unsigned* krow = cull_dyn;                 // [3*1024] per kill: observer window mask
-  unsigned* kcol = cull_dyn + 3 * 1024;      // [PAIR_W*32] per window slot: mask over the kills
+  unsigned* kcol = cull_dyn + 3 * 1024;      // [32][PAIR_W] per window slot: mask over the kills
   __shared__ int kact[PAIR_W], kidx[PAIR_W];
   const long long c_t0 = gtime();
   pair_acc_init<1024>(&acc, A.cur);
@@ -228,14 +228,14 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
         for (int a = 0; a < PAIR_W; ++a) {
           const unsigned bit = a < 32 ? (r0 >> a) & 1u : a < 64 ? (r1 >> (a - 32)) & 1u : (r2 >> (a - 64)) & 1u;
           const unsigned col = __ballot_sync(0xffffffffu, bit);
-          if (lane == 0) kcol[a * 32 + w] = col;
+          if (lane == 0) kcol[w * PAIR_W + a] = col;
         }
       }
       __syncthreads();
       // slots with any killed observer, then their pairs
       if (threadIdx.x < PAIR_W) {
         unsigned any = 0u;
-        for (int w = 0; w < nkw; ++w) any |= kcol[threadIdx.x * 32 + w];
+        for (int w = 0; w < nkw; ++w) any |= kcol[w * PAIR_W + threadIdx.x];
         kact[threadIdx.x] = any != 0u;
       }
       __syncthreads();
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
         }
         const int a = kidx[i], b = kidx[i + 1 + rem];
         int c = 0;
-        for (int w = 0; w < nkw; ++w) c += __popc(kcol[a * 32 + w] & kcol[b * 32 + w]);
+        for (int w = 0; w < nkw; ++w) c += __popc(kcol[w * PAIR_W + a] & kcol[w * PAIR_W + b]);
         if (c) atomicAdd(&acc.win[tri_index(a, b)], -c);
       }
     }
