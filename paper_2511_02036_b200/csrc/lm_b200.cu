@@ -732,40 +732,48 @@ __global__ void k_begin(DevMap* maps, const StepArgs* args) {
   for (int k = threadIdx.x; k < (int)(sizeof(lm_step_stats) / 4); k += blockDim.x) p[k] = 0;
 }
 
+// per-step statistics into the running totals: both records are read whole first (their
+// fields are independent loads) and the sums written back, instead of one dependent
+// read-modify-write round trip per field
 __global__ void k_end(DevMap* maps, const StepArgs* args, lm_step_stats** totals) {
   const DevMap& M = maps[args[blockIdx.x].map];
   if (threadIdx.x) return;
   lm_step_stats* st = M.s.stats;
-  st->error = M.scal[SC_ERR];
   lm_step_stats* t = totals[args[blockIdx.x].map];
-  t->created += st->created;
-  t->conflicts += st->conflicts;
-  t->degenerate += st->degenerate;
-  t->gate_parallax += st->gate_parallax;
-  t->gate_depth += st->gate_depth;
-  t->gate_reprojection += st->gate_reprojection;
-  t->gate_scale += st->gate_scale;
-  t->n_neighbors += st->n_neighbors;
-  t->n_targets += st->n_targets;
-  t->merged += st->merged;
-  t->observations_added += st->observations_added;
-  t->stale += st->stale;
-  t->culled += st->culled;
-  t->error = st->error;
-  t->n_candidates += st->n_candidates;
-  t->match_pairs += st->match_pairs;
-  t->fuse_bytes += st->fuse_bytes;
-  t->fuse_passes += st->fuse_passes;
-  t->fuse_points += st->fuse_points;
-  t->fuse_actions += st->fuse_actions;
-  t->apply_rounds += st->apply_rounds;
-  for (int k = 0; k < 16; ++k) t->fuse_cycles[k] += st->fuse_cycles[k];
-  t->rev_passes_acting += st->rev_passes_acting;
-  t->rev_passes_redo += st->rev_passes_redo;
-  t->fuse_bytes_rev += st->fuse_bytes_rev;
-  t->rev_mergeable += st->rev_mergeable;
-  for (int k = 0; k < 16; ++k) t->dbg[k] += st->dbg[k];
-  t->first_new_id += 1;  // steps accumulated
+  const int err = M.scal[SC_ERR];
+  lm_step_stats s = *st;
+  lm_step_stats u = *t;
+  s.error = err;
+  u.created += s.created;
+  u.conflicts += s.conflicts;
+  u.degenerate += s.degenerate;
+  u.gate_parallax += s.gate_parallax;
+  u.gate_depth += s.gate_depth;
+  u.gate_reprojection += s.gate_reprojection;
+  u.gate_scale += s.gate_scale;
+  u.n_neighbors += s.n_neighbors;
+  u.n_targets += s.n_targets;
+  u.merged += s.merged;
+  u.observations_added += s.observations_added;
+  u.stale += s.stale;
+  u.culled += s.culled;
+  u.error = err;
+  u.n_candidates += s.n_candidates;
+  u.match_pairs += s.match_pairs;
+  u.fuse_bytes += s.fuse_bytes;
+  u.fuse_passes += s.fuse_passes;
+  u.fuse_points += s.fuse_points;
+  u.fuse_actions += s.fuse_actions;
+  u.apply_rounds += s.apply_rounds;
+  for (int k = 0; k < 16; ++k) u.fuse_cycles[k] += s.fuse_cycles[k];
+  u.rev_passes_acting += s.rev_passes_acting;
+  u.rev_passes_redo += s.rev_passes_redo;
+  u.fuse_bytes_rev += s.fuse_bytes_rev;
+  u.rev_mergeable += s.rev_mergeable;
+  for (int k = 0; k < 16; ++k) u.dbg[k] += s.dbg[k];
+  u.first_new_id += 1;  // steps accumulated
+  st->error = err;
+  *t = u;
 }
 
 static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args) {
