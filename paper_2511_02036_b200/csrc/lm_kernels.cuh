@@ -705,8 +705,11 @@ __global__ void __launch_bounds__(1024) k_commit(DevMap* maps, const StepArgs* a
         M.obs[oo + 1] = cur_first ? make_int2(nb, j) : make_int2(cur, i);
         M.dirty[id] = 0;
         M.gval[id] = 0;
-        M.counts[(size_t)id * M.L + M.klev[ga]] += 1;
-        M.counts[(size_t)id * M.L + M.klev[gb]] += 1;
+        {  // a new point's counter row, written whole (no read-modify-write)
+          const int la = M.klev[ga], lb = M.klev[gb];
+          int* crow = M.counts + (size_t)id * M.L;
+          for (int l = 0; l < M.L; ++l) crow[l] = (l == la) + (l == lb);
+        }
         M.kbind[ga] = id;
         M.kbind[gb] = id;
         atomicAdd(&per_r[r], 1);
@@ -1393,6 +1396,8 @@ __device__ int fusion_targets(const DevMap& M, int cur, int n1, int n2, int n_sl
   __shared__ int tlist[TMAX];
   __shared__ int n_first, n_t;
   __shared__ unsigned seen[128];  // kf_cap <= 4096 slots
+  constexpr int HR = 64;          // rows whose 32 best-ranked entries are kept in shared memory
+  __shared__ int head[HR][32], hcnt[HR];
   const int nf = ranked_neighbors<BLOCK>(M, cur, n1 < TMAX ? n1 : TMAX, sh_slot, sh_key, first, n_slots);
   if (threadIdx.x == 0) n_first = nf;
   if (threadIdx.x < 128) seen[threadIdx.x] = 0;
@@ -1428,8 +1433,12 @@ __device__ int fusion_targets(const DevMap& M, int cur, int n1, int n2, int n_sl
       int rk = 0;
       for (int q = 0; q < c; ++q) rk += keys[q] < ke;
       buf[1 + M.kf_cap + rk] = buf[1 + e];
+      if (f < HR && rk < 32) head[f][rk] = buf[1 + e];
     }
-    if (lane == 0) buf[0] = c;
+    if (lane == 0) {
+      buf[0] = c;
+      if (f < HR) hcnt[f] = c;
+    }
     __syncwarp();
   }
   __syncthreads();
@@ -1443,11 +1452,11 @@ __device__ int fusion_targets(const DevMap& M, int cur, int n1, int n2, int n_sl
     int nt = n_first;
     for (int f = 0; f < n_first; ++f) {
       const int* buf = M.s.rank_buf + (size_t)f * stride;
-      const int c = buf[0];
+      const int c = f < HR ? hcnt[f] : buf[0];
       int added = 0;
       for (int q0 = 0; q0 < c && added < n2 && nt < TMAX; q0 += 32) {
         const int q = q0 + lane;
-        const int sl = q < c ? buf[1 + M.kf_cap + q] : -1;
+        const int sl = q < c ? (f < HR && q < 32 ? head[f][q] : buf[1 + M.kf_cap + q]) : -1;
         const bool un = sl >= 0 && !(seen[sl >> 5] >> (sl & 31) & 1u);
         const unsigned bal = __ballot_sync(0xffffffffu, un);
         const int want = n2 - added < TMAX - nt ? n2 - added : TMAX - nt;
