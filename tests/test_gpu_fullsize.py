@@ -137,3 +137,43 @@ def test_empty_keyframe_and_unmatched_descriptors():
                      rng.integers(0, 256, r.descriptors.shape, dtype=np.uint8))
     res = dev.process(noise)
     assert res.created == 0 and res.merged == 0 and res.observations_added == 0
+
+
+def _stage_mapper(name, seq):
+    n, n1, n2 = W.BENCH_STAGE[name]
+    return LocalMapper(seq.intrinsics(), neighbor_count=n, match=MatchConfig(neighbor_count=n),
+                       fuse=FuseConfig(n1=n1, n2=n2), store=store_for(len(seq.records), seq.config.features_per_kf + 64))
+
+
+@pytest.mark.parametrize("name,prefix", [("c3", 8), ("c4", 3)])
+def test_large_configs_prefix_match_oracle(name, prefix):
+    """TUM-VI shape (1500 features, 30 neighbours) and the stress shape (5000 features, 50
+    neighbours, up to 300 fusion targets): the first keyframes against the oracle."""
+    s = W.generate_sequence(W.bench_world(name))
+    intr, cam = s.intrinsics(), cam_of(s)
+    n, n1, n2 = W.BENCH_STAGE[name]
+    dev = _stage_mapper(name, s)
+    ora = O.OraclePipeline(intr.num_levels, n, fc=O.FuseCfg(n1=n1, n2=n2))
+    for rec in s.records[:prefix]:
+        dev.process(device_kf(rec, intr))
+        ora.step(O.okf_from_record(rec, cam))
+        snap = dev.snapshot(with_covis=False)
+        cmp = compare_state(snap, ora.map)
+        assert (dev.stats.created, dev.stats.conflicts) == (ora.stats.created, ora.stats.conflicts), rec.kf_id
+        assert dev.fused == ora.fused, rec.kf_id
+        assert cmp["structural_equal"], (rec.kf_id, first_difference(snap, ora.map))
+        assert cmp["pos_ok"], (rec.kf_id, cmp["pos_worst_rel"])
+
+
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_large_configs_full_run_audit(name):
+    """Whole C3 (500 keyframes) / C4 (60 keyframes, 5000 features) sequences: map audit."""
+    s = W.generate_sequence(W.bench_world(name))
+    intr = s.intrinsics()
+    kfs = [device_kf(r, intr) for r in s.records]
+    dev = _stage_mapper(name, s)
+    for kf in kfs:
+        dev.process(kf)
+    snap = dev.snapshot(with_covis=True)
+    bad = audit_snapshot(snap, kfs, sample_rep=2000)
+    assert bad == [], bad[:10]
