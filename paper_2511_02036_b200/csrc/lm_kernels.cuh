@@ -10,8 +10,17 @@
 //   k_tri      candidate compaction in current-index order + fused DLT + creation gates
 //   k_commit   winner = lowest neighbour rank whose candidate passes; ids by block scan in
 //              (rank, i) order; point / binding / counter / covisibility writes (257-299)
-//   k_fuse     SearchAndFuse (fusion.py:307-347): targets, forward gather-all/apply-all,
-//              reverse gather/apply per target; one CTA per map
+//   k_fuse_*   SearchAndFuse (fusion.py:307-347):
+//              targets    collect_fusion_targets + forward point list (1 CTA / map)
+//              geo        stale descriptors + geometry rows of the forward points (warp / point)
+//              gather     forward gather-all, thread per (target, point)
+//              apply      forward apply-all, reservation rounds on a CTA cluster per map
+//              refresh    every point the forward apply touched (warp / point)
+//              spec*      every reverse pass's items, speculatively (thread per item)
+//              post       post-ADD states of the speculative reverse ADDs (warp / point)
+//              rev        the ordered reverse passes (1 CTA / map), re-evaluating only what an
+//                         acting pass touched
+//              visible    the reverse passes' visible counters (thread per item)
 #pragma once
 #include <cooperative_groups.h>
 
@@ -1041,41 +1050,6 @@ __device__ __forceinline__ int classify(const DevMap& M, const ActRec& x, int* p
   return observes(M, x.pid, x.slot) ? 0 : 1;
 }
 
-// one action, sequential semantics; cnt = {merged, added, stale} (shared, atomic)
-__device__ void apply_one(const DevMap& M, const ActRec& x, int* cnt, PairAcc* acc) {
-  if (x.pid < 0 || !M.alive[x.pid] || M.kf_state[x.slot] != KF_LIVE) {
-    atomicAdd(&cnt[2], 1);
-    return;
-  }
-  const int g = M.kp_off[x.slot] + x.j;
-  if (x.kind == LM_ACT_MERGE) {
-    if (x.other < 0 || !M.alive[x.other] || x.other == x.pid || M.kbind[g] != x.other) {
-      atomicAdd(&cnt[2], 1);
-      return;
-    }
-    merge_pair(M, x.pid, x.other, acc);
-    atomicAdd(&cnt[0], 1);
-    return;
-  }
-  const int now = M.kbind[g];
-  if (now >= 0) {
-    if (!M.alive[now] || now == x.pid) {
-      atomicAdd(&cnt[2], 1);
-      return;
-    }
-    merge_pair(M, x.pid, now, acc);
-    atomicAdd(&cnt[0], 1);
-    return;
-  }
-  if (obs_find(M, x.pid, x.slot) >= 0) {
-    atomicAdd(&cnt[2], 1);
-    return;
-  }
-  link(M, x.pid, x.slot, x.j, acc);
-  mark_dirty(M, x.pid);
-  M.found[x.pid] += 1;
-  atomicAdd(&cnt[1], 1);
-}
 
 // A team executes apply_team: one CTA (BlockTeam) or a thread-block cluster (ClusterTeam,
 // control words in the leader CTA's shared memory, reached through distributed shared
@@ -1517,13 +1491,6 @@ __device__ int gather_pass(const DevMap& M, const lm_fuse_cfg& fc, int P, int ts
   return count;
 }
 
-// sum of observation counts of M.s.pts[0..P) (algorithmic-bytes accounting)
-template <int BLOCK>
-__device__ long long pass_obs(const DevMap& M, int P, int* sh) {
-  int c = 0;
-  for (int p = threadIdx.x; p < P; p += BLOCK) c += M.nobs[M.s.pts[p]];
-  return block_sum<BLOCK>(c, sh);
-}
 
 // per pass 56 B per point (pos 24 + rep 32), 9 B per observation, 53 B per
 // target keypoint (u,v 16 + level 1 + desc 32 + binding 4), 16 B per action
