@@ -325,9 +325,32 @@ def main():
             dt = (time.perf_counter() - t0) * 1e3
             if it >= args.warmup:
                 e_ms.append(max_over_ranks(dt))
-        e2e = {"value": total_kf / (sum(e_ms) / len(e_ms) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": sum(e_ms) / len(e_ms),
-               "timing": "wall clock around stage+step+readback of every keyframe"}
+        sync_each = {"value": total_kf / (sum(e_ms) / len(e_ms) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                     "d2h_bytes_per_step": d2h, "ms_per_step": sum(e_ms) / len(e_ms),
+                     "timing": "wall clock around stage (H2D) + step + statistics readback (D2H, synchronising) "
+                               "of every keyframe"}
+        # streaming: every keyframe staged from host memory (pinned ring, H2D) and stepped
+        # without waiting; the sequence's statistics read back once at the end (D2H)
+        p_ms = []
+        tot = _lib.StepStats()
+        for it in range(args.warmup + args.steps):
+            mapper.reset()
+            barrier()
+            t0 = time.perf_counter()
+            for kf in kfs:
+                mapper.stage(kf)
+                mapper.step(kf.kf_id, sync=False)
+            ctx.call("lm_totals_fetch", mapper.map, C.byref(tot))
+            dt = (time.perf_counter() - t0) * 1e3
+            if tot.error or tot.created <= 0:
+                raise RuntimeError(f"streaming e2e: device error {tot.error}")
+            if it >= args.warmup:
+                p_ms.append(max_over_ranks(dt))
+        e2e = {"value": total_kf / (sum(p_ms) / len(p_ms) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": C.sizeof(_lib.StepStats), "ms_per_step": sum(p_ms) / len(p_ms),
+               "timing": "wall clock: every keyframe staged from host memory (H2D) and stepped through the C ABI, "
+                         "the sequence's statistics read back (D2H) at the end",
+               "sync_each_keyframe": sync_each}
         # the same through the binary ingest wire format (LMKF records in host memory)
         from paper_2511_02036_b200 import ingest
 
