@@ -68,6 +68,16 @@ int main() {
   cudaMemcpy(p, hp, 4 << 20, cudaMemcpyHostToDevice);
   k_chain_load<<<1, 1>>>(p, 1 << 14, o); k_chain_load<<<1, 1>>>(p, 1 << 14, o);
   cudaMemcpy(h, o, 16, cudaMemcpyDeviceToHost); printf("dependent global load (L2-resident 4MB): %lld cycles\n", h[0]);
+  {  // 64 MB random chain (L2-resident on a 126 MB L2, spread over both dies' slices)
+    int* q; const int N = 1 << 24; cudaMalloc(&q, sizeof(int) * N);
+    int* hq = new int[N];
+    for (int i = 0; i < N; ++i) hq[i] = (int)((i * 2654435761u + 7u) % (unsigned)N);
+    cudaMemcpy(q, hq, sizeof(int) * N, cudaMemcpyHostToDevice);
+    k_chain_load<<<1, 1>>>(q, 1 << 14, o); k_chain_load<<<1, 1>>>(q, 1 << 14, o);
+    cudaMemcpy(h, o, 16, cudaMemcpyDeviceToHost); printf("dependent global load (64MB chain): %lld cycles\n", h[0]);
+    for (int sm = 0; sm < 2; ++sm) {}
+    cudaFree(q); delete[] hq;
+  }
   cudaMemset(p, 0, 1 << 12);
   k_chain_atomic<<<1, 1>>>(p, 1 << 12, o); cudaMemcpy(h, o, 16, cudaMemcpyDeviceToHost);
   printf("dependent global atomicAdd (returning): %lld cycles\n", h[0]);
