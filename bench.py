@@ -432,7 +432,8 @@ def main():
                               "fwd_apply_detail": {"heads_ms": acc["dbg"][8] / args.steps / 1e6,
                                                    "members_merges_ms": acc["dbg"][9] / args.steps / 1e6,
                                                    "rounds": acc["dbg"][10] / args.steps,
-                                                   "actions": acc["dbg"][11] / args.steps},
+                                                   "actions": acc["dbg"][11] / args.steps,
+                                                   "pending_in_later_rounds": acc["dbg"][15] / args.steps},
                               "rev_touched_points_from_post_add_speculation": acc["dbg"][12] / args.steps,
                               "culled": acc["culled"] / args.steps,
                               "cull_probation_entries": acc["dbg"][13] / args.steps,

@@ -1108,6 +1108,7 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
   int rounds = 0;
   while (ctl[CTL_NPEND] > 0) {
     const int np = ctl[CTL_NPEND];  // (the words reset below were last read before the round's final barrier)
+    if (tm && tid == 0 && rounds > 0) tm[13] += np;  // diagnostics: actions left after round 1
     if (tid == 0) {
       ctl[CTL_ROUND] = atomicAdd(&M.scal[SC_ROUND], 1) + 1;
       ctl[CTL_NMERGE] = 0;
@@ -1647,6 +1648,7 @@ __global__ void __launch_bounds__(1024, 1) k_fuse_apply(DevMap* maps, const Step
     st->dbg[9] += tmf[11];           // forward: members / merges / member pairs
     st->dbg[10] += rr;               // forward: rounds
     st->dbg[11] += nact;             // forward: actions
+    st->dbg[15] += tmf[13];          // forward: actions pending in rounds 2..
   }
   cl.sync();  // the leader CTA's shared control words stay alive until every CTA is done
 }

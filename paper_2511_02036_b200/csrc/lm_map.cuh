@@ -34,7 +34,7 @@ constexpr int REFRESH_MAXN = 512;       // observations handled by the rep-refre
 constexpr int MATCH_TILE = 32;          // current keypoints per match CTA (one per lane)
 constexpr int MATCH_WARPS = 8;          // warps per match CTA, each scanning a slice of j
 constexpr int MATCH_JT = 1024;          // neighbour descriptors staged per smem chunk
-constexpr int RES_PAIR = 1 << 16;       // hashed (point, keyframe) reservation keys per map
+constexpr int RES_PAIR = 1 << 20;       // hashed (point, keyframe) reservation keys per map
 constexpr int HL = 16;                  // hit-list entries per current keypoint
 
 enum KfState { KF_FREE = 0, KF_STAGED = 1, KF_LIVE = 2, KF_DEAD = 3 };
