@@ -72,7 +72,7 @@ struct lm_ctx {
   void* flush_buf = nullptr;
   size_t flush_bytes = 0;
   bool prof = false;
-  int apply_cluster = 8;                // CTAs per map of the forward-apply cluster (LM_APPLY_CLUSTER)
+  int apply_cluster = 16;               // CTAs per map of the forward-apply cluster (LM_APPLY_CLUSTER)
   std::vector<cudaEvent_t> prof_pool;   // free events
   std::vector<std::vector<cudaEvent_t>> prof_steps;  // 9 boundary events per step
 };
@@ -848,7 +848,7 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
     cl = cl < 1 ? 1 : (cl > ctx->apply_cluster ? ctx->apply_cluster : cl);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(n * cl);
-    cfg.blockDim = dim3(1024);
+    cfg.blockDim = dim3(APPLY_THREADS);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = ctx->stream;
     cudaLaunchAttribute at[1];

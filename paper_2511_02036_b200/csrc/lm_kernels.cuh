@@ -1588,10 +1588,12 @@ __global__ void __launch_bounds__(256) k_fuse_gather(DevMap* maps, const StepArg
 }
 
 // assemble the forward batch in (target, point) order and apply it
+constexpr int APPLY_THREADS = 512;  // k_fuse_apply CTA (128 registers: apply_team does not spill)
+
 // Forward apply: one thread-block cluster per map (launched with cluster dims; blockIdx.x /
 // cluster size selects the map). The ~4.5k forward actions of a C2 keyframe spread over the
 // cluster's CTAs; the reservation rounds synchronise with barrier.cluster.
-__global__ void __launch_bounds__(1024, 1) k_fuse_apply(DevMap* maps, const StepArgs* args) {
+__global__ void __launch_bounds__(APPLY_THREADS, 1) k_fuse_apply(DevMap* maps, const StepArgs* args) {
   cg::cluster_group cl = cg::this_cluster();
   const int ncl = (int)cl.num_blocks(), rank = (int)cl.block_rank();
   const StepArgs& A = args[blockIdx.x / ncl];
@@ -1607,15 +1609,15 @@ __global__ void __launch_bounds__(1024, 1) k_fuse_apply(DevMap* maps, const Step
   const long long t0 = gtime();
   if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
   if (threadIdx.x < 16) tmf[threadIdx.x] = 0;
-  pair_acc_init<1024>(&acc, A.cur);
-  const ClusterTeam<1024> G(ctl);
+  pair_acc_init<APPLY_THREADS>(&acc, A.cur);
+  const ClusterTeam<APPLY_THREADS> G(ctl);
   const int nb = (T * P + 255) / 256;
   int base = 0;
-  for (int c0 = 0; c0 < nb; c0 += 1024) {  // exclusive scan of the per-CTA counts (every CTA)
+  for (int c0 = 0; c0 < nb; c0 += APPLY_THREADS) {  // exclusive scan of the per-CTA counts (every CTA)
     const int b = c0 + threadIdx.x;
     const int v = b < nb ? M.s.blk_cnt[b] : 0;
     int tot;
-    const int at = block_excl_scan<1024>(v, sh, tot);
+    const int at = block_excl_scan<APPLY_THREADS>(v, sh, tot);
     if (b < nb && rank == 0) M.s.blk_off[b] = base + at;
     base += tot;
   }
@@ -1628,7 +1630,7 @@ __global__ void __launch_bounds__(1024, 1) k_fuse_apply(DevMap* maps, const Step
   G.sync();
   const long long t1 = gtime();
   const int rr = apply_team(G, M, M.s.acts, nact, cnt, sh, &acc, rank == 0 ? tmf : nullptr);
-  pair_acc_flush<1024>(M, &acc);
+  pair_acc_flush<APPLY_THREADS>(M, &acc);
   lm_step_stats* st = M.s.stats;
   if (threadIdx.x == 0) {
     atomicAdd(&st->merged, cnt[0]);
