@@ -425,8 +425,8 @@ def main():
                               "rev_items_reevaluated": acc["rev_passes_redo"] / args.steps,
                               "rev_acting_passes_untouched_by_previous_apply": acc["rev_mergeable"] / args.steps,
                               "rev_points_recomputed": acc["fuse_cycles"][1] / args.steps,
-                              "cull_phase_ms": {"init": acc["dbg"][0] / args.steps / 1e6,
-                                                "classify": acc["dbg"][1] / args.steps / 1e6,
+                              "rev_passes_direct_all_add": acc["dbg"][0] / args.steps,
+                              "cull_phase_ms": {"classify": acc["dbg"][1] / args.steps / 1e6,
                                                 "kills": acc["dbg"][2] / args.steps / 1e6,
                                                 "flush": acc["dbg"][3] / args.steps / 1e6},
                               "fwd_apply_detail": {"heads_ms": acc["dbg"][8] / args.steps / 1e6,

@@ -279,8 +279,8 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
     M.s.stats->culled = culled;
     M.s.stats->dbg[13] += n;  // diagnostics: probation list length
     M.s.stats->dbg[14] += nbig_total;
-    M.s.stats->dbg[0] += c_t1 - c_t0;            // cull: accumulator init (ns)
-    M.s.stats->dbg[1] += c_t2 - c_t1 - c_kill;   // cull: classification + compaction
+    M.s.stats->dbg[1] += c_t1 - c_t0;            // cull: accumulator init (ns)
+    M.s.stats->dbg[1] += c_t2 - c_t1 - c_kill;   // cull: init + classification + compaction
     M.s.stats->dbg[2] += c_kill;                 // cull: kills
     M.s.stats->dbg[3] += c_t3 - c_t2;            // cull: covisibility flush
   }
@@ -1988,7 +1988,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   pair_acc_init<REV_THREADS>(&acc, A.cur);  // (barrier)
   const unsigned long long mpb = M.mp_rec_bytes;
   long long alg = 0, npts = 0, nacts = 0, ledger_events = 0;
-  int rounds = 0, pass_act = 0, reeval = 0, redo_pts = 0, mergeable = 0, touched_min = 0x7fffffff;
+  int rounds = 0, pass_act = 0, reeval = 0, redo_pts = 0, mergeable = 0, touched_min = 0x7fffffff, fast_passes = 0;
   int t0 = 0;
   // append item (t, kp) to the re-evaluation list once per tag
   auto add_item = [&](int t, int kp, int tag) {
@@ -2111,6 +2111,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       if (threadIdx.x == 0) {
         cnt[1] += na;
         ++rounds;
+        ++fast_passes;
         tm[7] += gtime() - ta;
       }
       __syncthreads();
@@ -2282,6 +2283,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     st->rev_passes_redo += reeval;   // re-evaluated items (count)
     st->rev_mergeable += mergeable;
     for (int k = 4; k < 8; ++k) st->dbg[k] += tm[k];
+    st->dbg[0] += fast_passes;  // diagnostics: acting passes applied directly (all plain ADDs)
   }
 }
 
