@@ -162,9 +162,10 @@ def load():
     global _lib
     with _lock:
         if _lib is None:
-            if not os.path.exists(LIB_PATH):
-                raise DeviceError(f"native library {LIB_PATH} is missing; run __graft_entry__.build()")
-            lib = C.CDLL(LIB_PATH)
+            path = os.environ.get("LM_B200_LIB", LIB_PATH)  # (experiments: an alternative build)
+            if not os.path.exists(path):
+                raise DeviceError(f"native library {path} is missing; run __graft_entry__.build()")
+            lib = C.CDLL(path)
             for name, (args, res) in _SIGS.items():
                 fn = getattr(lib, name)
                 fn.argtypes = args

@@ -32,7 +32,10 @@ constexpr int LMAX = 16;                // pyramid levels
 constexpr int GRID_CELLS = 4096;        // cells per keyframe grid
 constexpr int REFRESH_MAXN = 512;       // observations handled by the rep-refresh fast path
 constexpr int MATCH_TILE = 32;          // current keypoints per match CTA (one per lane)
-constexpr int MATCH_WARPS = 8;          // warps per match CTA, each scanning a slice of j
+#ifndef LM_MATCH_WARPS
+#define LM_MATCH_WARPS 8
+#endif
+constexpr int MATCH_WARPS = LM_MATCH_WARPS;  // warps per match CTA, each scanning a slice of j
 constexpr int MATCH_JT = 1024;          // neighbour descriptors staged per smem chunk
 constexpr int RES_PAIR = 1 << 20;       // hashed (point, keyframe) reservation keys per map
 constexpr int HL = 16;                  // hit-list entries per current keypoint
