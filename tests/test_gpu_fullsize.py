@@ -177,3 +177,37 @@ def test_large_configs_full_run_audit(name):
     snap = dev.snapshot(with_covis=True)
     bad = audit_snapshot(snap, kfs, sample_rep=2000)
     assert bad == [], bad[:10]
+
+
+def test_stream_groups_equal_independent_runs():
+    """C5's multi-stream form: sessions in two contexts (one stream each), steps issued
+    without synchronisation and interleaved, equal independent runs."""
+    from paper_2511_02036_b200 import _lib
+
+    seqs = [W.generate_sequence(W.WorldConfig(**c)) for c in SESS]
+    ctxs = [_lib.Context.get(0), _lib.Context(0)]
+    groups = [[0, 2], [1]]
+    mk = lambda q, ctx: LocalMapper(q.intrinsics(), neighbor_count=10, ctx=ctx,  # noqa: E731
+                                    store=store_for(len(q.records), q.config.features_per_kf * 2))
+    mappers = {}
+    batches = []
+    for g, members in enumerate(groups):
+        ms = [mk(seqs[i], ctxs[g]) for i in members]
+        for i, m in zip(members, ms):
+            mappers[i] = m
+            for r in seqs[i].records:
+                m.stage(device_kf(r, seqs[i].intrinsics()))
+        batches.append((SessionBatch(ms), members))
+    nk = min(len(q.records) for q in seqs)
+    for k in range(nk):
+        for b, members in batches:
+            b.step([int(seqs[i].records[k].kf_id) for i in members], sync=False)
+    for c in ctxs:
+        c.call("lm_synchronize")
+    for i, q in enumerate(seqs):
+        alone = mk(q, None)
+        for r in q.records[:nk]:
+            alone.process(device_kf(r, q.intrinsics()))
+        sb, sa = mappers[i].snapshot(), alone.snapshot()
+        assert sb.structural_digest() == sa.structural_digest()
+        assert np.array_equal(sb.pos, sa.pos)
