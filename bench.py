@@ -444,8 +444,8 @@ def main():
                                                   "refresh_hits": acc["dbg"][6] / args.steps / 1e6}},
             "fuse_phase_ms_per_step": {n: acc["fuse_cycles"][k] / args.steps / 1e6
                                        for k, n in enumerate(["targets", "-", "fwd_assemble", "fwd_apply",
-                                                              "rev_redo_refresh", "rev_redo_gather", "rev_apply",
-                                                              "rev_rescan", "rev_commit_invalidate", "rev_apply_reserve_check",
+                                                              "rev_redo_refresh", "rev_select", "rev_apply",
+                                                              "rev_rescan", "rev_prologue", "rev_apply_reserve_check",
                                                               "rev_apply_commit", "rev_apply_merges",
                                                               "rev_apply_compaction", "fwd_apply_reserve_check",
                                                               "fwd_apply_commit_merges", "fwd_apply_compaction"])

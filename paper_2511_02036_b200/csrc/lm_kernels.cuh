@@ -1928,6 +1928,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   if (!A.do_fuse) return;
   const int T = M.s.fctl[FC_T];
   if (T == 0) return;
+  const long long t_entry = gtime();
   extern __shared__ __align__(16) unsigned char dyn_rev[];
   TgtView TV = tgt_global(M, A.cur);
   {  // stage the current keyframe (target of every reverse pass) in shared memory
@@ -1959,6 +1960,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   __shared__ PairAcc acc;
   __shared__ int s_nact[TMAX], s_live[TMAX], s_obs[TMAX];
   __shared__ int t1_sh, nc_sh, ni_sh, tag_sh, tmin_sh, na_sh, nchg_sh, fast_sh;
+  __shared__ int s_inst[32];  // direct pass: action k's point took its speculated state
   __shared__ double cur_pose[22];  // R, t, C, cam, cell size of the current keyframe
   if (threadIdx.x < 22) {
     const int c = A.cur, k = threadIdx.x;
@@ -1987,6 +1989,110 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   }
   pair_acc_init<REV_THREADS>(&acc, A.cur);  // (barrier)
   const unsigned long long mpb = M.mp_rec_bytes;
+  const int mtag = M.scal[SC_MTAG];
+  // install point p's speculated post-ADD state (k_fuse_post): descriptor, geometry, hit
+  auto install_post = [&](int p) {
+    M.rep[2 * (size_t)p] = M.sp_rep[2 * (size_t)p];
+    M.rep[2 * (size_t)p + 1] = M.sp_rep[2 * (size_t)p + 1];
+    const double* sg = M.sp_geo + 5 * (size_t)p;
+    M.gacc[3 * p] = sg[0];
+    M.gacc[3 * p + 1] = sg[1];
+    M.gacc[3 * p + 2] = sg[2];
+    M.glo[p] = sg[3];
+    M.ghi[p] = sg[4];
+    M.gval[p] = 1;
+    M.dirty[p] = 0;
+    M.hit[p] = make_int2(M.ver[p], M.sp_hit[p]);
+    hit_list_add(M, M.sp_hit[p], p);
+    atomicAdd((unsigned long long*)&M.s.stats->dbg[12], 1ull);
+  };
+  const long long kf_cur = M.kf_id[A.cur];
+  // link(M, p, cur, j, acc, fuse=true) of a direct-pass ADD, one warp: the lanes take the
+  // covisibility bumps, lane 0 the record; every load is issued in the first rounds, before
+  // any store (the keypoint level and the current keyframe's centre come from shared memory).
+  // When the point's speculated post-ADD state (k_fuse_post) matches this ADD, the point takes
+  // it at once (descriptor, geometry, hit) instead of the incremental geometry / stale flag.
+  auto add_direct = [&](const ActRec x, int k) {
+    const int lane = threadIdx.x & 31;
+    const int p = x.pid, j = x.j;
+    const int n = M.nobs[p], off = M.ooff[p], cap = M.ocap[p];
+    const int dirty = M.dirty[p], gv = M.gval[p], vr = M.ver[p], found = M.found[p];
+    const int lev = TV.lev[j];
+    const int stag = M.sp_tag[p], sv0 = M.sp_ver0[p], sn0 = M.sp_nobs0[p], sj = M.sp_j[p];
+    const double px = M.pos[3 * p], py = M.pos[3 * p + 1], pz = M.pos[3 * p + 2];
+    const double lo = M.glo[p], hi = M.ghi[p];
+    const double ax = M.gacc[3 * p], ay = M.gacc[3 * p + 1], az = M.gacc[3 * p + 2];
+    int* cntp = M.counts + (size_t)p * M.L + lev;
+    const int cv = *cntp;
+    const double Sl = M.S[lev];
+    const int2* o = M.obs + off;
+    const int o0 = lane < n ? o[lane].x : cur, o1 = lane + 32 < n ? o[lane + 32].x : cur;
+    const int last = n ? o[n - 1].x : -1;
+    const bool spec = stag == mtag && sv0 == vr && sn0 == n && sj == j;
+    covis_add(M, cur, o0, +1, &acc);
+    covis_add(M, cur, o1, +1, &acc);
+    for (int e = lane + 64; e < n; e += 32) covis_add(M, cur, o[e].x, +1, &acc);
+    if (lane == 0) {
+      int2* dst = M.obs + off;
+      if (n == cap) {
+        const int nc = cap < 4 ? 4 : 2 * cap;
+        const int noff = atomicAdd(&M.scal[SC_OBS_HEAD], nc);
+        if (noff + nc > M.obs_cap) {
+          set_err(M, LM_ERR_CAPACITY);
+          s_inst[k] = 1;
+          return;
+        }
+        copy_obs(M.obs + noff, o, n);
+        M.ooff[p] = noff;
+        M.ocap[p] = nc;
+        dst = M.obs + noff;
+      }
+      dst[n] = make_int2(cur, j);
+      M.nobs[p] = n + 1;
+      M.kbind[cur_off + j] = p;
+      *cntp = cv + 1;
+      M.ver[p] = vr + 1;
+      M.found[p] = found + 1;
+      if (spec) {
+        const uint4 r0 = M.sp_rep[2 * (size_t)p], r1 = M.sp_rep[2 * (size_t)p + 1];
+        const double* sg = M.sp_geo + 5 * (size_t)p;
+        const double g0 = sg[0], g1 = sg[1], g2 = sg[2], g3 = sg[3], g4 = sg[4];
+        const int sh_ = M.sp_hit[p];
+        M.rep[2 * (size_t)p] = r0;
+        M.rep[2 * (size_t)p + 1] = r1;
+        M.gacc[3 * p] = g0;
+        M.gacc[3 * p + 1] = g1;
+        M.gacc[3 * p + 2] = g2;
+        M.glo[p] = g3;
+        M.ghi[p] = g4;
+        M.gval[p] = 1;
+        M.dirty[p] = 0;
+        M.hit[p] = make_int2(vr + 1, sh_);
+        hit_list_add(M, sh_, p);
+        atomicAdd((unsigned long long*)&M.s.stats->dbg[12], 1ull);
+      } else {
+        mark_dirty_owned(M, p, dirty);
+        const long long kf_last = last >= 0 ? M.kf_id[last] : -1;
+        if (gv && !dirty && (n == 0 || kf_last < kf_cur)) {
+          const double rx = px - cur_pose[12], ry = py - cur_pose[13], rz = pz - cur_pose[14];
+          const double dd = sqrt(rx * rx + ry * ry + rz * rz);
+          if (dd > 0) {  // geo_term
+            const double d0 = dd / Sl;
+            M.glo[p] = d0 < lo ? d0 : lo;
+            M.ghi[p] = d0 > hi ? d0 : hi;
+            M.gacc[3 * p] = ax + rx / dd;
+            M.gacc[3 * p + 1] = ay + ry / dd;
+            M.gacc[3 * p + 2] = az + rz / dd;
+          }
+        } else {
+          M.gval[p] = 0;
+        }
+      }
+      s_inst[k] = spec;
+    }
+    __syncwarp();
+  };
+  if (threadIdx.x == 0) tm[8] = gtime() - t_entry;  // prologue
   long long alg = 0, npts = 0, nacts = 0, ledger_events = 0;
   int rounds = 0, pass_act = 0, reeval = 0, redo_pts = 0, mergeable = 0, touched_min = 0x7fffffff, fast_passes = 0;
   int t0 = 0;
@@ -2079,6 +2185,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       for (int k = threadIdx.x - 32; k < ncur; k += REV_THREADS - 32) M.s.snap[k] = M.kbind[cur_off + k];
     }
     __syncthreads();
+    if (threadIdx.x == 0) tm[1] += gtime() - ta;
     const int t1 = t1_sh;
     if (t1 >= T) break;
     if (pass_act > 0) mergeable += touched_min > t1;
@@ -2099,15 +2206,65 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       }
       return __any_sync(0xffffffffu, any);
     };
+    // touched point p after the apply, one warp: its post-ADD state when the apply did exactly
+    // the speculated ADD (same observation set as k_fuse_post's; the list is sorted: clean
+    // before, the current keyframe appended last), else refresh (descriptor + geometry) and
+    // a new hit
+    auto settle_point = [&](int p) {
+      if (M.sp_tag[p] == mtag && M.sp_ver0[p] >= 0 && M.ver[p] == M.sp_ver0[p] + 1 &&
+          M.nobs[p] == M.sp_nobs0[p] + 1 && M.kbind[cur_off + M.sp_j[p]] == p) {
+        if (lane == 0) install_post(p);
+        __syncwarp();
+        return;
+      }
+      if (M.dirty[p]) {
+        refresh_rep_warp(M, p, lane);
+        if (lane == 0) M.dirty[p] = 0;
+        __syncwarp();
+      }
+      if (!M.gval[p]) geo_full_warp(M, p, lane);
+      PGeo g;
+      point_geometry(M, p, fc.dist_band_slack, g);  // (every lane: same loads, broadcast)
+      const int j = gather_hit_warp(M, fc, g, cur, TV, lane);
+      if (lane == 0) {
+        M.hit[p] = make_int2(M.ver[p], j);
+        hit_list_add(M, j, p);
+      }
+      __syncwarp();
+    };
+    // points hitting current keypoint k, whose binding changed, join the touched list (hit
+    // list; a keypoint whose list overflowed falls back to scanning the passes of its bitmap)
+    auto hit_list_points = [&](int k) {
+      const int c = M.s.hl_cnt[k];
+      if (c <= HL) {
+        if (lane < c) {
+          const int p = M.s.hl[k * HL + lane];
+          if (M.alive[p] && M.hit[p].y == k && atomicExch(&M.s.rmark[p], tag) != tag)
+            M.s.cands[atomicAdd(&nc_sh, 1)] = p;
+        }
+        return;
+      }
+      for (int w = 0; w < HPW; ++w) {
+        unsigned bits = M.s.hitpass[k * HPW + w];
+        while (bits) {
+          const int tt = 32 * w + __ffs(bits) - 1;
+          bits &= bits - 1;
+          if (tt <= t1 || tt >= T) continue;
+          const int n = M.kp_n[M.s.targets[tt]];
+          const int* pjt = M.s.pj + (size_t)tt * K;
+          for (int kp = lane; kp < n; kp += 32)
+            if (pjt[kp] == k) add_item(tt, kp, tag);
+        }
+      }
+    };
     if (fast_sh) {
       // every action a plain ADD of a distinct point into a distinct unbound keypoint (the
       // pass's item is current, so slot j is free and the point does not see the current
-      // keyframe): the actions touch disjoint entities and commute; apply them directly.
-      // An ADD only adds an observation, so the touched points' items are collected after.
-      for (int k = threadIdx.x; k < na; k += REV_THREADS) {
-        const ActRec x = M.s.acts[k];
-        link(M, x.pid, cur, x.j, &acc, true);
-      }
+      // keyframe): the actions touch disjoint entities and commute; apply them directly, each
+      // point taking its speculated post-ADD state at once. The changed current keypoints are
+      // exactly the actions' keypoints, and an ADD only adds an observation, so the touched
+      // items are the points' observations after the apply.
+      for (int k = wid; k < na; k += REV_THREADS / 32) add_direct(M.s.acts[k], k);
       if (threadIdx.x == 0) {
         cnt[1] += na;
         ++rounds;
@@ -2115,12 +2272,35 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
         tm[7] += gtime() - ta;
       }
       __syncthreads();
+      if (threadIdx.x == 0) tm[2] += gtime() - ta;
+      const long long tv = gtime();
+      for (int k = wid; k < na; k += REV_THREADS / 32) {
+        const ActRec x = M.s.acts[k];
+        add_point_items(x.pid);
+        hit_list_points(x.j);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) tm[4] += gtime() - tv;
+      const long long tv3 = gtime();
+      const int nall = nc_sh;
+      redo_pts += ncand;
+      for (int k = wid; k < na + (nall - ncand); k += REV_THREADS / 32) {
+        if (k < na) {
+          if (!s_inst[k]) settle_point(M.s.acts[k].pid);
+        } else {
+          add_point_items(M.s.cands[ncand + k - na]);
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        tm[0] += gtime() - tv;
+        tm[6] += gtime() - tv3;
+      }
     } else {
       for (int k = wid; k < ncand; k += REV_THREADS / 32) add_point_items(M.s.cands[k]);  // before the apply
       __syncthreads();
       if (threadIdx.x == 0) tm[7] += gtime() - ta;
       rounds += apply_block<REV_THREADS>(M, M.s.acts, na, cnt, sh, &acc, tm);  // (barriers)
-    }
     if (threadIdx.x == 0) tm[2] += gtime() - ta;
     // (2) after the apply: the touched points' items, and the points hitting a current
     //     keypoint whose binding changed (hit list; a keypoint whose list overflowed falls
@@ -2173,50 +2353,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
         // a touched point without items in later passes keeps its dirty flag (the next
         // step's refresh picks it up) and a stale hit (nothing reads it: the version differs)
         if (!M.alive[p] || !M.s.cneed[k]) continue;
-        if (M.sp_tag[p] == M.scal[SC_MTAG] && M.sp_ver0[p] >= 0 && M.ver[p] == M.sp_ver0[p] + 1 &&
-            M.nobs[p] == M.sp_nobs0[p] + 1 && M.kbind[cur_off + M.sp_j[p]] == p) {
-          // the apply did exactly the speculated ADD: same observation set as k_fuse_post's
-          // (the list is sorted: clean before, the current keyframe appended last)
-          if (lane == 0) {
-            M.rep[2 * (size_t)p] = M.sp_rep[2 * (size_t)p];
-            M.rep[2 * (size_t)p + 1] = M.sp_rep[2 * (size_t)p + 1];
-            const double* sg = M.sp_geo + 5 * (size_t)p;
-            M.gacc[3 * p] = sg[0];
-            M.gacc[3 * p + 1] = sg[1];
-            M.gacc[3 * p + 2] = sg[2];
-            M.glo[p] = sg[3];
-            M.ghi[p] = sg[4];
-            M.gval[p] = 1;
-            M.dirty[p] = 0;
-            M.hit[p] = make_int2(M.ver[p], M.sp_hit[p]);
-            hit_list_add(M, M.sp_hit[p], p);
-            atomicAdd((unsigned long long*)&M.s.stats->dbg[12], 1ull);
-          }
-          __syncwarp();
-          continue;
-        }
-        const long long c0 = clock64();
-        if (M.dirty[p]) {
-          refresh_rep_warp(M, p, lane);
-          if (lane == 0) M.dirty[p] = 0;
-          __syncwarp();
-        }
-        const long long c1 = clock64();
-        if (!M.gval[p]) geo_full_warp(M, p, lane);
-        const long long c2 = clock64();
-        PGeo g;
-        point_geometry(M, p, fc.dist_band_slack, g);  // (every lane: same loads, broadcast)
-        const int j = gather_hit_warp(M, fc, g, cur, TV, lane);
-        if (lane == 0) {
-          M.hit[p] = make_int2(M.ver[p], j);
-          hit_list_add(M, j, p);
-          const long long c3 = clock64();
-          (void)c0;
-          (void)c1;
-          (void)c2;
-          (void)c3;
-        }
-        __syncwarp();
+        settle_point(p);
       } else {
         add_point_items(p);
       }
@@ -2226,6 +2363,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       tm[0] += gtime() - tv;
       tm[6] += gtime() - tv3;
     }
+    }  // general path
     // (5) re-evaluate the listed items; pass totals by deltas, action bitmaps toggled
     const long long t7 = gtime();
     const int ni = ni_sh;

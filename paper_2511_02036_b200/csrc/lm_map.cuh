@@ -277,12 +277,17 @@ __device__ __forceinline__ void covis_add(const DevMap& M, int a, int b, int d, 
 // entries are loaded 8 at a time before their atomics (one L2 round trip per 8 entries
 // instead of one per entry: the compiler does not hoist loads across the atomics)
 __device__ __forceinline__ void covis_list(const DevMap& M, int slot, const int2* o, int n, int d, PairAcc* acc) {
-  for (int k0 = 0; k0 < n; k0 += 8) {
-    int s[8];
+  int s[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) s[j] = k0 + j < n ? o[k0 + j].x : slot;
+  for (int j = 0; j < 8; ++j) s[j] = j < n ? o[j].x : slot;
+  for (int k0 = 0; k0 < n; k0 += 8) {
+    int nx[8];  // the next chunk's loads are in flight while this chunk's bumps run
+#pragma unroll
+    for (int j = 0; j < 8; ++j) nx[j] = k0 + 8 + j < n ? o[k0 + 8 + j].x : slot;
 #pragma unroll
     for (int j = 0; j < 8; ++j) covis_add(M, slot, s[j], d, acc);  // (slot, slot) is a no-op
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s[j] = nx[j];
   }
 }
 
@@ -430,16 +435,22 @@ __device__ void geo_full(const DevMap& M, int mp) {
 // fuse=true: fusion's ADD_OBSERVATION on top (found += 1, representative descriptor marked
 // stale), with the flag/counter loads in the same first round.
 __device__ void link(const DevMap& M, int mp, int slot, int kp, PairAcc* acc = nullptr, bool fuse = false) {
+  // every load first: the stores below would otherwise serialise them (aliasing)
   const int n = M.nobs[mp], cap = M.ocap[mp], off = M.ooff[mp];
-  const int dirty = M.dirty[mp], gv = M.gval[mp];
+  const int dirty = M.dirty[mp], gv = M.gval[mp], vr = M.ver[mp];
   const int found = fuse ? M.found[mp] : 0;
   const int g = M.kp_off[slot] + kp;
   const long long kf_new = M.kf_id[slot];
   const double px = M.pos[3 * mp], py = M.pos[3 * mp + 1], pz = M.pos[3 * mp + 2];
   const double cx = M.C[3 * slot], cy = M.C[3 * slot + 1], cz = M.C[3 * slot + 2];
+  const double lo = M.glo[mp], hi = M.ghi[mp];
+  const double ax = M.gacc[3 * mp], ay = M.gacc[3 * mp + 1], az = M.gacc[3 * mp + 2];
   const int2* o = M.obs + off;
   const int last = n ? o[n - 1].x : -1;
   const int lev = M.klev[g];
+  int* cnt = M.counts + (size_t)mp * M.L + lev;
+  const int cv = *cnt;
+  const double Sl = M.S[lev];
   const long long kf_last = last >= 0 ? M.kf_id[last] : -1;
   covis_list(M, slot, o, n, +1, acc);
   // appended after the newest keyframe of a clean (sorted) list: the cached sums extend exactly
@@ -461,8 +472,8 @@ __device__ void link(const DevMap& M, int mp, int slot, int kp, PairAcc* acc = n
   }
   M.nobs[mp] = n + 1;
   M.kbind[g] = mp;
-  M.counts[(size_t)mp * M.L + lev] += 1;
-  M.ver[mp] += 1;
+  *cnt = cv + 1;
+  M.ver[mp] = vr + 1;
   if (fuse) {
     M.found[mp] = found + 1;
     mark_dirty_owned(M, mp, dirty);
@@ -471,9 +482,7 @@ __device__ void link(const DevMap& M, int mp, int slot, int kp, PairAcc* acc = n
     const double rx = px - cx, ry = py - cy, rz = pz - cz;
     const double dd = sqrt(rx * rx + ry * ry + rz * rz);
     if (dd > 0) {  // geo_term
-      const double d0 = dd / M.S[lev];
-      const double lo = M.glo[mp], hi = M.ghi[mp];
-      const double ax = M.gacc[3 * mp], ay = M.gacc[3 * mp + 1], az = M.gacc[3 * mp + 2];
+      const double d0 = dd / Sl;
       M.glo[mp] = d0 < lo ? d0 : lo;
       M.ghi[mp] = d0 > hi ? d0 : hi;
       M.gacc[3 * mp] = ax + rx / dd;
