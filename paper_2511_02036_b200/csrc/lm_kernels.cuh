@@ -1961,6 +1961,8 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   __shared__ int s_nact[TMAX], s_live[TMAX], s_obs[TMAX];
   __shared__ int t1_sh, nc_sh, ni_sh, tag_sh, tmin_sh, na_sh, nchg_sh, fast_sh;
   __shared__ int s_inst[32];  // direct pass: action k's point took its speculated state
+  __shared__ int s_nset, tag_base;
+  __shared__ ActRec s_acts[32];  // the pass's first 32 actions
   __shared__ double cur_pose[22];  // R, t, C, cam, cell size of the current keyframe
   if (threadIdx.x < 22) {
     const int c = A.cur, k = threadIdx.x;
@@ -1980,6 +1982,8 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     ni_sh = 0;
     nchg_sh = 0;
     tmin_sh = 0x7fffffff;
+    s_nset = 0;
+    tag_base = atomicAdd(&M.scal[SC_ROUND], T + 2);  // one dedupe tag per iteration (<= T + 1)
   }
   for (int t = threadIdx.x; t < T; t += REV_THREADS) {
     s_nact[t] = M.s.pinfo[PI_NACT * TMAX + t];
@@ -2007,12 +2011,38 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     atomicAdd((unsigned long long*)&M.s.stats->dbg[12], 1ull);
   };
   const long long kf_cur = M.kf_id[A.cur];
+  if (threadIdx.x == 0) tm[8] = gtime() - t_entry;  // prologue
+  long long alg = 0, npts = 0, nacts = 0, ledger_events = 0;
+  int iter = 0, rounds = 0, pass_act = 0, reeval = 0, redo_pts = 0, mergeable = 0, touched_min = 0x7fffffff, fast_passes = 0;
+  int t0 = 0;
+  // append item (t, kp) to the re-evaluation list once per tag
+  auto add_item = [&](int t, int kp, int tag) {
+    const size_t it = (size_t)t * K + kp;
+    if (atomicExch(&M.s.itag[it], tag) != tag) M.s.ilist[atomicAdd(&ni_sh, 1)] = (int)it;
+  };
+  // items of point p (its current observations) in passes after t1; warp-cooperative; true
+  // when p has one
+  auto point_items = [&](int p, int t1, int tag) -> bool {
+    const int lane = threadIdx.x & 31;
+    const int2* o = M.obs + M.ooff[p];
+    const int no = M.nobs[p];
+    bool any = false;
+    for (int e = lane; e < no; e += 32) {
+      const int2 ob = o[e];
+      const int tt = M.s.pass_of[ob.x];
+      if (tt > t1) {
+        add_item(tt, ob.y, tag);
+        any = true;
+      }
+    }
+    return __any_sync(0xffffffffu, any);
+  };
   // link(M, p, cur, j, acc, fuse=true) of a direct-pass ADD, one warp: the lanes take the
   // covisibility bumps, lane 0 the record; every load is issued in the first rounds, before
   // any store (the keypoint level and the current keyframe's centre come from shared memory).
   // When the point's speculated post-ADD state (k_fuse_post) matches this ADD, the point takes
   // it at once (descriptor, geometry, hit) instead of the incremental geometry / stale flag.
-  auto add_direct = [&](const ActRec x, int k) {
+  auto add_direct = [&](const ActRec x, int k, int t1, int tag) {
     const int lane = threadIdx.x & 31;
     const int p = x.pid, j = x.j;
     const int n = M.nobs[p], off = M.ooff[p], cap = M.ocap[p];
@@ -2025,28 +2055,68 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     int* cntp = M.counts + (size_t)p * M.L + lev;
     const int cv = *cntp;
     const double Sl = M.S[lev];
+    const int hc = M.s.hl_cnt[j];
+    const int hp = lane < hc && lane < HL ? M.s.hl[j * HL + lane] : -1;
     const int2* o = M.obs + off;
-    const int o0 = lane < n ? o[lane].x : cur, o1 = lane + 32 < n ? o[lane + 32].x : cur;
+    const int2 e0 = lane < n ? o[lane] : make_int2(cur, 0), e1 = lane + 32 < n ? o[lane + 32] : make_int2(cur, 0);
+    const int o0 = e0.x, o1 = e1.x;
     const int last = n ? o[n - 1].x : -1;
+    // the point's items in passes after t1 (its observations after the ADD: the old ones and
+    // (cur, j)), and the points hitting j (hit list): their hits are unchanged by the apply
+    const int tt0 = M.s.pass_of[o0], tt1 = M.s.pass_of[o1], ttc = lane == 0 ? M.s.pass_of[cur] : -1;
+    const bool hq = hp >= 0 && M.alive[hp] && M.hit[hp].y == j;
+    if (lane < n && tt0 > t1) add_item(tt0, e0.y, tag);
+    if (lane + 32 < n && tt1 > t1) add_item(tt1, e1.y, tag);
+    if (ttc > t1) add_item(ttc, j, tag);
+    for (int e = lane + 64; e < n; e += 32) {
+      const int2 ob = o[e];
+      const int tt = M.s.pass_of[ob.x];
+      if (tt > t1) add_item(tt, ob.y, tag);
+    }
+    unsigned hm = __ballot_sync(0xffffffffu, hq && atomicExch(&M.s.rmark[hp], tag) != tag);
+    while (hm) {  // hit-list points' items (their state is unchanged)
+      const int src = __ffs(hm) - 1;
+      hm &= hm - 1;
+      const int q = __shfl_sync(0xffffffffu, hp, src);
+      if (lane == 0) M.s.cands[atomicAdd(&nc_sh, 1)] = q;
+      point_items(q, t1, tag);
+    }
+    if (hc > HL) {  // overflowed list: scan the passes of the keypoint's bitmap
+      for (int w = 0; w < HPW; ++w) {
+        unsigned bits = M.s.hitpass[j * HPW + w];
+        while (bits) {
+          const int tt = 32 * w + __ffs(bits) - 1;
+          bits &= bits - 1;
+          if (tt <= t1 || tt >= T) continue;
+          const int nn = M.kp_n[M.s.targets[tt]];
+          const int* pjt = M.s.pj + (size_t)tt * K;
+          for (int kp = lane; kp < nn; kp += 32)
+            if (pjt[kp] == j) add_item(tt, kp, tag);
+        }
+      }
+    }
     const bool spec = stag == mtag && sv0 == vr && sn0 == n && sj == j;
     covis_add(M, cur, o0, +1, &acc);
     covis_add(M, cur, o1, +1, &acc);
     for (int e = lane + 64; e < n; e += 32) covis_add(M, cur, o[e].x, +1, &acc);
+    int2* dst = nullptr;
     if (lane == 0) {
-      int2* dst = M.obs + off;
+      dst = M.obs + off;
       if (n == cap) {
         const int nc = cap < 4 ? 4 : 2 * cap;
         const int noff = atomicAdd(&M.scal[SC_OBS_HEAD], nc);
         if (noff + nc > M.obs_cap) {
-          set_err(M, LM_ERR_CAPACITY);
-          s_inst[k] = 1;
-          return;
+          set_err(M, LM_ERR_CAPACITY);  // (the step fails; the record is left as it was)
+          dst = nullptr;
+        } else {
+          copy_obs(M.obs + noff, o, n);
+          M.ooff[p] = noff;
+          M.ocap[p] = nc;
+          dst = M.obs + noff;
         }
-        copy_obs(M.obs + noff, o, n);
-        M.ooff[p] = noff;
-        M.ocap[p] = nc;
-        dst = M.obs + noff;
       }
+    }
+    if (lane == 0 && dst) {
       dst[n] = make_int2(cur, j);
       M.nobs[p] = n + 1;
       M.kbind[cur_off + j] = p;
@@ -2089,17 +2159,9 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
         }
       }
       s_inst[k] = spec;
+      if (!spec) atomicAdd(&s_nset, 1);
     }
     __syncwarp();
-  };
-  if (threadIdx.x == 0) tm[8] = gtime() - t_entry;  // prologue
-  long long alg = 0, npts = 0, nacts = 0, ledger_events = 0;
-  int rounds = 0, pass_act = 0, reeval = 0, redo_pts = 0, mergeable = 0, touched_min = 0x7fffffff, fast_passes = 0;
-  int t0 = 0;
-  // append item (t, kp) to the re-evaluation list once per tag
-  auto add_item = [&](int t, int kp, int tag) {
-    const size_t it = (size_t)t * K + kp;
-    if (atomicExch(&M.s.itag[it], tag) != tag) M.s.ilist[atomicAdd(&ni_sh, 1)] = (int)it;
   };
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int AW = (K + 31) >> 5;  // words of a pass's action bitmap
@@ -2134,9 +2196,8 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       npts += a_p;
       nacts += a_n;
       ledger_events += te - t0 + 1;
-      int na = 0, tag = 0;
-      if (lane == 0) tag = atomicAdd(&M.scal[SC_ROUND], 1) + 1;
-      const int tg = __shfl_sync(0xffffffffu, tag, 0);
+      int na = 0;
+      const int tg = tag_base + 1 + iter;
       if (t1 < T) {
         const unsigned* bits = M.s.abits + (size_t)t1 * AW;
         const ActRec* seg = M.s.acts2 + (size_t)t1 * K;
@@ -2154,25 +2215,35 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
             const int kp = 32 * w + __ffs(bw) - 1;
             bw &= bw - 1;
             const ActRec x = seg[kp];
-            M.s.acts[at++] = ActRec{cur, x.pid, x.j, x.other, x.kind};
+            const ActRec y{cur, x.pid, x.j, x.other, x.kind};
+            if (at < 32) s_acts[at] = y;
+            M.s.acts[at++] = y;
           }
           na += __shfl_sync(0xffffffffu, pre, 31);
         }
         __syncwarp();
-        bool simple = na <= 32;  // every action a plain ADD into a distinct keypoint
-        for (int k = lane; k < na; k += 32) {
-          const ActRec x = M.s.acts[k];
-          const int cand[3] = {x.pid, x.other, M.kbind[cur_off + x.j]};
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const int p = cand[c];
-            if (p >= 0 && atomicExch(&M.s.rmark[p], tg) != tg) M.s.cands[atomicAdd(&nc_sh, 1)] = p;
+        bool simple = na <= 32;  // every action a plain ADD of a distinct point into a distinct keypoint
+        if (simple) {
+          const ActRec x = lane < na ? s_acts[lane] : ActRec{0, -1 - lane, -1 - lane, 0, LM_ACT_ADD};
+          const unsigned mj = __match_any_sync(0xffffffffu, x.j), mp = __match_any_sync(0xffffffffu, x.pid);
+          simple = __all_sync(0xffffffffu, x.kind == LM_ACT_ADD && __popc(mj) == 1 && __popc(mp) == 1);
+          if (simple && lane < na) {  // touched points: the action points (distinct)
+            M.s.rmark[x.pid] = tg;
+            M.s.cands[lane] = x.pid;
           }
         }
         if (simple) {
-          const ActRec x = lane < na ? M.s.acts[lane] : ActRec{0, 0, -1 - lane, 0, LM_ACT_ADD};
-          const unsigned same = __match_any_sync(0xffffffffu, x.j);
-          simple = __all_sync(0xffffffffu, x.kind == LM_ACT_ADD && __popc(same) == 1);
+          if (lane == 0) nc_sh = na;
+        } else {
+          for (int k = lane; k < na; k += 32) {
+            const ActRec x = M.s.acts[k];
+            const int cand[3] = {x.pid, x.other, M.kbind[cur_off + x.j]};
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              const int p = cand[c];
+              if (p >= 0 && atomicExch(&M.s.rmark[p], tg) != tg) M.s.cands[atomicAdd(&nc_sh, 1)] = p;
+            }
+          }
         }
         if (lane == 0) fast_sh = simple;
       }
@@ -2192,20 +2263,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     ++pass_act;
     const int na = na_sh, tag = tag_sh, ncand = nc_sh;
     // items of point p (its current observations) in passes after t1; warp-cooperative
-    auto add_point_items = [&](int p) -> bool {  // true when p has an item after t1
-      const int2* o = M.obs + M.ooff[p];
-      const int no = M.nobs[p];
-      bool any = false;
-      for (int e = lane; e < no; e += 32) {
-        const int2 ob = o[e];
-        const int tt = M.s.pass_of[ob.x];
-        if (tt > t1) {
-          add_item(tt, ob.y, tag);
-          any = true;
-        }
-      }
-      return __any_sync(0xffffffffu, any);
-    };
+    auto add_point_items = [&](int p) -> bool { return point_items(p, t1, tag); };
     // touched point p after the apply, one warp: its post-ADD state when the apply did exactly
     // the speculated ADD (same observation set as k_fuse_post's; the list is sorted: clean
     // before, the current keyframe appended last), else refresh (descriptor + geometry) and
@@ -2264,37 +2322,22 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       // point taking its speculated post-ADD state at once. The changed current keypoints are
       // exactly the actions' keypoints, and an ADD only adds an observation, so the touched
       // items are the points' observations after the apply.
-      for (int k = wid; k < na; k += REV_THREADS / 32) add_direct(M.s.acts[k], k);
+      for (int k = wid; k < na; k += REV_THREADS / 32) add_direct(s_acts[k], k, t1, tag);
+      __syncthreads();
       if (threadIdx.x == 0) {
         cnt[1] += na;
         ++rounds;
         ++fast_passes;
         tm[7] += gtime() - ta;
+        tm[2] += gtime() - ta;
       }
-      __syncthreads();
-      if (threadIdx.x == 0) tm[2] += gtime() - ta;
-      const long long tv = gtime();
-      for (int k = wid; k < na; k += REV_THREADS / 32) {
-        const ActRec x = M.s.acts[k];
-        add_point_items(x.pid);
-        hit_list_points(x.j);
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) tm[4] += gtime() - tv;
-      const long long tv3 = gtime();
-      const int nall = nc_sh;
       redo_pts += ncand;
-      for (int k = wid; k < na + (nall - ncand); k += REV_THREADS / 32) {
-        if (k < na) {
-          if (!s_inst[k]) settle_point(M.s.acts[k].pid);
-        } else {
-          add_point_items(M.s.cands[ncand + k - na]);
-        }
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        tm[0] += gtime() - tv;
-        tm[6] += gtime() - tv3;
+      if (s_nset) {  // points whose speculated state did not apply: refresh + new hit
+        const long long tv = gtime();
+        for (int k = wid; k < na; k += REV_THREADS / 32)
+          if (!s_inst[k]) settle_point(s_acts[k].pid);
+        __syncthreads();
+        if (threadIdx.x == 0) tm[0] += gtime() - tv;
       }
     } else {
       for (int k = wid; k < ncand; k += REV_THREADS / 32) add_point_items(M.s.cands[k]);  // before the apply
@@ -2391,8 +2434,10 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       ni_sh = 0;
       nchg_sh = 0;
       tmin_sh = 0x7fffffff;
+      s_nset = 0;
     }
     t0 = t1 + 1;
+    ++iter;
   }
   pair_acc_flush<REV_THREADS>(M, &acc);
   for (int t = threadIdx.x; t < T; t += REV_THREADS) M.s.pass_of[M.s.targets[t]] = -1;
