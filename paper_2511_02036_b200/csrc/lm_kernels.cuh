@@ -1962,6 +1962,9 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   __shared__ int t1_sh, nc_sh, ni_sh, tag_sh, tmin_sh, na_sh, nchg_sh, fast_sh;
   __shared__ int s_inst[32];  // direct pass: action k's point took its speculated state
   __shared__ int s_nset, tag_base;
+  constexpr int ILS = 1024;
+  __shared__ int s_il[ILS];     // the iteration's item list (overflow: M.s.ilist)
+  __shared__ int s_toff[TMAX];  // keypoint offset of each pass's target
   __shared__ ActRec s_acts[32];  // the pass's first 32 actions
   __shared__ double cur_pose[22];  // R, t, C, cam, cell size of the current keyframe
   if (threadIdx.x < 22) {
@@ -1989,7 +1992,9 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     s_nact[t] = M.s.pinfo[PI_NACT * TMAX + t];
     s_live[t] = M.s.pinfo[PI_LIVE * TMAX + t];
     s_obs[t] = M.s.pinfo[PI_OBS * TMAX + t];
-    M.s.pass_of[M.s.targets[t]] = t;
+    const int ts = M.s.targets[t];
+    M.s.pass_of[ts] = t;
+    s_toff[t] = M.kp_off[ts];
   }
   pair_acc_init<REV_THREADS>(&acc, A.cur);  // (barrier)
   const unsigned long long mpb = M.mp_rec_bytes;
@@ -2018,7 +2023,11 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   // append item (t, kp) to the re-evaluation list once per tag
   auto add_item = [&](int t, int kp, int tag) {
     const size_t it = (size_t)t * K + kp;
-    if (atomicExch(&M.s.itag[it], tag) != tag) M.s.ilist[atomicAdd(&ni_sh, 1)] = (int)it;
+    if (atomicExch(&M.s.itag[it], tag) != tag) {
+      const int at = atomicAdd(&ni_sh, 1);
+      if (at < ILS) s_il[at] = (int)it;
+      else M.s.ilist[at] = (int)it;
+    }
   };
   // items of point p (its current observations) in passes after t1; warp-cooperative; true
   // when p has one
@@ -2036,6 +2045,35 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       }
     }
     return __any_sync(0xffffffffu, any);
+  };
+  // eval_item(M, cur, t, targets[t], kp) with the pass's keypoint offset from shared memory and
+  // the point's list offset loaded in the first round
+  auto eval_rev = [&](int t, int kp) -> ItemVal {
+    ItemVal v{-1, -3, 0, 0, ActRec{0, 0, 0, 0, 0}};
+    const int mp = M.kbind[s_toff[t] + kp];
+    if (mp < 0) return v;
+    const int al = M.alive[mp], nob = M.nobs[mp], off = M.ooff[mp], j = M.hit[mp].y;
+    if (!al) return v;
+    v.mp = mp;
+    v.nob = nob;
+    v.j = j;
+    if (j < 0) return v;
+    atomicOr(&M.s.hitpass[j * HPW + (t >> 5)], 1u << (t & 31));
+    const int owner = M.kbind[cur_off + j];
+    if (owner < 0) {
+      const int2* o = M.obs + off;
+      bool f = false;
+#pragma unroll 4
+      for (int k = 0; k < nob; ++k) f |= o[k].x == cur;
+      if (!f) {
+        v.a = ActRec{cur, mp, j, -1, LM_ACT_ADD};
+        v.has = 1;
+      }
+    } else if (owner != mp && M.alive[owner]) {
+      v.a = ActRec{cur, mp, j, owner, LM_ACT_MERGE};
+      v.has = 1;
+    }
+    return v;
   };
   // link(M, p, cur, j, acc, fuse=true) of a direct-pass ADD, one warp: the lanes take the
   // covisibility bumps, lane 0 the record; every load is issued in the first rounds, before
@@ -2252,8 +2290,6 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
         na_sh = na;
         tag_sh = tg;
       }
-    } else {
-      for (int k = threadIdx.x - 32; k < ncur; k += REV_THREADS - 32) M.s.snap[k] = M.kbind[cur_off + k];
     }
     __syncthreads();
     if (threadIdx.x == 0) tm[1] += gtime() - ta;
@@ -2341,6 +2377,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       }
     } else {
       for (int k = wid; k < ncand; k += REV_THREADS / 32) add_point_items(M.s.cands[k]);  // before the apply
+      for (int k = threadIdx.x; k < ncur; k += REV_THREADS) M.s.snap[k] = M.kbind[cur_off + k];  // bindings before
       __syncthreads();
       if (threadIdx.x == 0) tm[7] += gtime() - ta;
       rounds += apply_block<REV_THREADS>(M, M.s.acts, na, cnt, sh, &acc, tm);  // (barriers)
@@ -2412,10 +2449,10 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     const int ni = ni_sh;
     reeval += ni;
     for (int q = threadIdx.x; q < ni; q += REV_THREADS) {
-      const int it = M.s.ilist[q];
+      const int it = q < ILS ? s_il[q] : M.s.ilist[q];
       const int t = it / K, kp = it - t * K;
       const int oj = M.s.pj[it], ob = M.s.pob[it], oa = M.s.acts2[it].kind != 0;
-      const ItemVal v = eval_item(M, cur, t, M.s.targets[t], kp);
+      const ItemVal v = eval_rev(t, kp);
       store_item(M, it, v);
       const int dl = (v.mp >= 0) - (oj != -3), dob = v.nob - ob, da = v.has - oa;
       if (dl) atomicAdd(&s_live[t], dl);
