@@ -1960,12 +1960,15 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   __shared__ PairAcc acc;
   __shared__ int s_nact[TMAX], s_live[TMAX], s_obs[TMAX];
   __shared__ int t1_sh, nc_sh, ni_sh, tag_sh, tmin_sh, na_sh, nchg_sh, fast_sh;
-  __shared__ int s_inst[32];  // direct pass: action k's point took its speculated state
+  constexpr int DMAX = 128;  // largest direct pass
+  constexpr int JBW = 64;    // words of the direct pass's keypoint bitmap
+  __shared__ int s_inst[DMAX];  // direct pass: action k's point took its speculated state
+  __shared__ unsigned s_jb[JBW];
   __shared__ int s_nset, tag_base;
   constexpr int ILS = 1024;
   __shared__ int s_il[ILS];     // the iteration's item list (overflow: M.s.ilist)
   __shared__ int s_toff[TMAX];  // keypoint offset of each pass's target
-  __shared__ ActRec s_acts[32];  // the pass's first 32 actions
+  __shared__ ActRec s_acts[DMAX];  // the pass's first DMAX actions
   __shared__ double cur_pose[22];  // R, t, C, cam, cell size of the current keyframe
   if (threadIdx.x < 22) {
     const int c = A.cur, k = threadIdx.x;
@@ -2254,23 +2257,37 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
             bw &= bw - 1;
             const ActRec x = seg[kp];
             const ActRec y{cur, x.pid, x.j, x.other, x.kind};
-            if (at < 32) s_acts[at] = y;
+            if (at < DMAX) s_acts[at] = y;
             M.s.acts[at++] = y;
           }
           na += __shfl_sync(0xffffffffu, pre, 31);
         }
         __syncwarp();
-        bool simple = na <= 32;  // every action a plain ADD of a distinct point into a distinct keypoint
+        // direct pass: every action a plain ADD of a distinct point into a distinct keypoint
+        bool simple = na <= 32;
         if (simple) {
           const ActRec x = lane < na ? s_acts[lane] : ActRec{0, -1 - lane, -1 - lane, 0, LM_ACT_ADD};
           const unsigned mj = __match_any_sync(0xffffffffu, x.j), mp = __match_any_sync(0xffffffffu, x.pid);
           simple = __all_sync(0xffffffffu, x.kind == LM_ACT_ADD && __popc(mj) == 1 && __popc(mp) == 1);
-          if (simple && lane < na) {  // touched points: the action points (distinct)
-            M.s.rmark[x.pid] = tg;
-            M.s.cands[lane] = x.pid;
+        } else if (na <= DMAX && AW <= JBW) {
+          // distinct keypoints by a bitmap (the points of one pass are distinct: the bound points
+          // of one keyframe's keypoints)
+          for (int w = lane; w < AW; w += 32) s_jb[w] = 0u;
+          __syncwarp();
+          bool ok = true;
+          for (int k = lane; k < na; k += 32) {
+            const ActRec x = s_acts[k];
+            const unsigned b = 1u << (x.j & 31);
+            ok &= x.kind == LM_ACT_ADD && !(atomicOr(&s_jb[x.j >> 5], b) & b);
           }
+          simple = __all_sync(0xffffffffu, ok);
         }
         if (simple) {
+          for (int k = lane; k < na; k += 32) {  // touched points: the action points
+            const int p = s_acts[k].pid;
+            M.s.rmark[p] = tg;
+            M.s.cands[k] = p;
+          }
           if (lane == 0) nc_sh = na;
         } else {
           for (int k = lane; k < na; k += 32) {
