@@ -50,9 +50,13 @@ struct StepArgs {
 // ---------------------------------------------------------------------------------- helpers
 
 __device__ __forceinline__ long long gtime() {  // ns, device-wide clock
+#ifdef LM_NO_PHASE_TIMERS
+  return 0;
+#else
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return (long long)t;
+#endif
 }
 
 template <int BLOCK>
@@ -1511,7 +1515,16 @@ __global__ void __launch_bounds__(1024) k_fuse_targets(DevMap* maps, const StepA
   __shared__ int sh[32];
   const long long t0 = gtime();
   const int T = fusion_targets<1024>(M, A.cur, A.fc.n1, A.fc.n2, n_slots_max, sh_slot, sh_key);
-  const int P = T ? bound_points<1024>(M, A.cur, sh) : 0;
+  __shared__ unsigned long long s_tkp;
+  if (threadIdx.x == 0) s_tkp = 0;
+  const int P = T ? bound_points<1024>(M, A.cur, sh) : 0;  // (barriers)
+  {  // keypoints of the targets, block-parallel
+    int tk = 0;
+    for (int k = threadIdx.x; k < T; k += 1024) tk += M.kp_n[M.s.targets[k]];
+    for (int off = 16; off; off >>= 1) tk += __shfl_xor_sync(0xffffffffu, tk, off);
+    if ((threadIdx.x & 31) == 0 && tk) atomicAdd(&s_tkp, (unsigned long long)tk);
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
     M.s.fctl[FC_T] = T;
     M.s.fctl[FC_P] = P;
@@ -1519,12 +1532,8 @@ __global__ void __launch_bounds__(1024) k_fuse_targets(DevMap* maps, const StepA
     st->n_targets = T;
     if (T) {
       const unsigned long long mpb = M.mp_rec_bytes;
-      unsigned long long naive = 0;
-      long long tkp = 0;
-      for (int k = 0; k < T; ++k) {
-        naive += (unsigned long long)payload_bytes(M, M.s.targets[k]);
-        tkp += M.kp_n[M.s.targets[k]];
-      }
+      const long long tkp = (long long)s_tkp;
+      const unsigned long long naive = (unsigned long long)tkp * (M.kp_rec_bytes + M.desc_bytes);  // payload_bytes
       M.ledger[LG_NAIVE] += naive + P * mpb;
       M.ledger[LG_PERSIST] += P * mpb;
       M.ledger[LG_SMALL_FUSE] += P * mpb;
