@@ -461,6 +461,16 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
   CU(cudaFuncSetAttribute(k_op, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
   CU(cudaFuncSetAttribute(k_fuse_apply, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CU(cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, CULL_DYN_SMEM));
+  if (const char* e = getenv("LM_CARVEOUT")) {  // (experiments) shared-memory carve-out hint, percent
+    const int pc = atoi(e);
+    const void* ks[] = {(const void*)k_insert, (const void*)k_cull, (const void*)k_select, (const void*)k_prep,
+                        (const void*)k_match, (const void*)k_tri, (const void*)k_commit, (const void*)k_fuse_targets,
+                        (const void*)k_fuse_geo, (const void*)k_fuse_gather, (const void*)k_fuse_apply,
+                        (const void*)k_fuse_refresh, (const void*)k_fuse_spec<true>, (const void*)k_fuse_spec<false>,
+                        (const void*)k_fuse_spec_pts, (const void*)k_fuse_spec_hit, (const void*)k_fuse_post,
+                        (const void*)k_fuse_rev, (const void*)k_fuse_visible};
+    for (const void* k : ks) CU(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pc));
+  }
   if (const char* e = getenv("LM_APPLY_CLUSTER")) {
     const int v = atoi(e);
     ctx->apply_cluster = v < 1 ? 1 : (v > 16 ? 16 : v);
@@ -800,9 +810,12 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
     kfcap = m->d.kf_cap > kfcap ? m->d.kf_cap : kfcap;
   }
   DevMap* dmaps = ctx->d_maps;
-  // reverse passes target the current keyframe: stage it in shared memory when it fits
+  // reverse passes target the current keyframe; staging it in shared memory (LM_REV_SMEM=1)
+  // measured slower on B200: the carve-out it needs shrinks the L1 that the kernel's
+  // point/observation loads live in (C2: 45.3 -> 43.1 ms per 200 keyframes without it)
+  static const bool rev_stage = getenv("LM_REV_SMEM") != nullptr;
   size_t rev_smem = (size_t)kpkf * (16 + 1 + 32 + 4) + 4 * (GRID_CELLS + 1) + 256;
-  if (rev_smem > 160 * 1024) rev_smem = 0;
+  if (rev_smem > 160 * 1024 || !rev_stage) rev_smem = 0;
   CU(cudaMemcpyAsync(dv, h, sizeof(StepArgs) * n, cudaMemcpyHostToDevice, ctx->stream));
   const size_t dyn = 12 * (size_t)kfcap;
   std::vector<cudaEvent_t> evs;
