@@ -577,7 +577,7 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(s.pinfo, 3 * TMAX); A(s.hitpass, (size_t)d.kpkf_max * ((TMAX + 31) / 32)); A(s.pj, (size_t)s.act_cap);
   A(s.pass_of, K); A(s.snap, d.kpkf_max); A(s.chg, d.kpkf_max); A(s.rmark, MP);
   A(s.pmp, (size_t)s.act_cap); A(s.pob, (size_t)s.act_cap); A(s.itag, (size_t)s.act_cap); A(s.ilist, (size_t)s.act_cap);
-  A(s.cands, (size_t)s.act_cap); A(s.cneed, (size_t)s.act_cap); A(s.hl_cnt, d.kpkf_max); A(s.hl, (size_t)d.kpkf_max * HL); A(s.hreg, MP); A(s.upts, (size_t)s.act_cap); A(s.sp_list, (size_t)s.act_cap); A(s.sp_obs, (size_t)16 * 8 * (POST_MAXN + 1));
+  A(s.cands, (size_t)s.act_cap); A(s.cneed, (size_t)s.act_cap); A(s.hl_cnt, d.kpkf_max); A(s.hl, (size_t)d.kpkf_max * HL); A(s.hreg, MP); A(s.upts, (size_t)s.act_cap); A(s.sp_list, (size_t)s.act_cap); A(s.sp_obs, (size_t)POST_BLOCKS * 8 * (POST_MAXN + 1));
   A(s.abits, (size_t)TMAX * ((d.kpkf_max + 31) / 32));
   A(m->d_stats, 1); A(m->d_totals, 1); A(m->d_result, 4 + 1024 + TMAX);
 #undef A
@@ -885,7 +885,7 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
     ctx->launches += 2;
   }
   if ((rc = mark())) return rc;
-  k_fuse_post<<<dim3(16, n), 256, 0, ctx->stream>>>(dmaps, dv);
+  k_fuse_post<<<dim3(POST_BLOCKS, n), 256, 0, ctx->stream>>>(dmaps, dv);
   k_fuse_rev<<<n, REV_THREADS, rev_smem, ctx->stream>>>(dmaps, dv, rev_smem);
   if ((rc = mark())) return rc;
   k_fuse_visible<<<dim3((kpkf + 255) / 256, tfuse, n), 256, 0, ctx->stream>>>(dmaps, dv);

@@ -1860,6 +1860,7 @@ __global__ void __launch_bounds__(256) k_fuse_spec(DevMap* maps, const StepArgs*
 // refreshing when the apply did exactly that (one mutation, one observation more, slot j
 // bound to the point: the same observation set).
 constexpr int POST_MAXN = 128;
+constexpr int POST_BLOCKS = 148;  // k_fuse_post grid (x): one warp per speculated point at C2 sizes
 __global__ void __launch_bounds__(256) k_fuse_post(DevMap* maps, const StepArgs* args) {
   const StepArgs& A = args[blockIdx.y];
   const DevMap& M = maps[A.map];

@@ -127,7 +127,7 @@ struct Scratch {
   int* hreg;             // [mp_cap] step tag: point already listed by the speculative scan
   int* upts;             // [act_cap] distinct bound points of all reverse passes
   int* sp_list;          // [act_cap] points with a speculative reverse-pass ADD
-  int2* sp_obs;          // [POST_WARPS*(POST_MAXN+1)] per-warp virtual observation lists
+  int2* sp_obs;          // [POST_BLOCKS*8*(POST_MAXN+1)] per-warp virtual observation lists
   unsigned* abits;       // [TMAX*ceil(kpkf_max/32)] per pass: keypoints whose item has an action
   int* act_flag;         // [TMAX*kpkf_max]
   int* vis_flag;         // [TMAX*kpkf_max]
