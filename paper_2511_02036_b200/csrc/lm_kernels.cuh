@@ -1974,6 +1974,8 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   constexpr int JBW = 64;    // words of the direct pass's keypoint bitmap
   __shared__ int s_inst[DMAX];  // direct pass: action k's point took its speculated state
   __shared__ unsigned s_jb[JBW];
+  __shared__ int s_wpre[64];         // direct action extraction: prefix counts of the bitmap words
+  __shared__ unsigned s_wbits[64];
   __shared__ int s_nset, tag_base;
   constexpr int ILS = 1024;
   __shared__ int s_il[ILS];     // the iteration's item list (overflow: M.s.ilist)
@@ -2252,7 +2254,54 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       if (t1 < T) {
         const unsigned* bits = M.s.abits + (size_t)t1 * AW;
         const ActRec* seg = M.s.acts2 + (size_t)t1 * K;
-        for (int wb = 0; wb < AW; wb += 32) {
+        if (AW <= 64) {
+          // lane per action: both bitmap words per lane loaded at once, word prefix counts in
+          // shared memory, action a = the (a - pre[w])-th set bit of the word w holding it;
+          // all record loads issued before any store
+          const unsigned b0 = lane < AW ? bits[lane] : 0u, b1 = lane + 32 < AW ? bits[lane + 32] : 0u;
+          const int c0 = __popc(b0), c1 = __popc(b1);
+          int p0 = c0, p1 = c1;
+          for (int off = 1; off < 32; off <<= 1) {
+            const int y0 = __shfl_up_sync(0xffffffffu, p0, off), y1 = __shfl_up_sync(0xffffffffu, p1, off);
+            if (lane >= off) {
+              p0 += y0;
+              p1 += y1;
+            }
+          }
+          const int tot0 = __shfl_sync(0xffffffffu, p0, 31);
+          na = tot0 + __shfl_sync(0xffffffffu, p1, 31);
+          s_wpre[lane] = p0 - c0;
+          s_wpre[32 + lane] = tot0 + p1 - c1;
+          s_wbits[lane] = b0;
+          s_wbits[32 + lane] = b1;
+          __syncwarp();
+          auto kp_of = [&](int a) -> int {  // largest w with pre[w] <= a
+            int lo = 0;
+#pragma unroll
+            for (int step = 32; step; step >>= 1)
+              if (s_wpre[lo + step] <= a && lo + step < 64) lo += step;
+            return 32 * lo + (int)__fns(s_wbits[lo], 0, a - s_wpre[lo] + 1);
+          };
+          ActRec xr[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (lane + 32 * i < na) xr[i] = seg[kp_of(lane + 32 * i)];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int a = lane + 32 * i;
+            if (a < na) {
+              const ActRec y{cur, xr[i].pid, xr[i].j, xr[i].other, xr[i].kind};
+              if (a < DMAX) s_acts[a] = y;
+              M.s.acts[a] = y;
+            }
+          }
+          for (int a = lane + 128; a < na; a += 32) {
+            const ActRec x = seg[kp_of(a)];
+            const ActRec y{cur, x.pid, x.j, x.other, x.kind};
+            if (a < DMAX) s_acts[a] = y;
+            M.s.acts[a] = y;
+          }
+        } else for (int wb = 0; wb < AW; wb += 32) {
           const int w = wb + lane;
           unsigned bw = w < AW ? bits[w] : 0u;
           const int c = __popc(bw);
