@@ -169,7 +169,8 @@ __global__ void __launch_bounds__(256) k_insert(DevMap* maps, const StepArgs* ar
 
 // ---------------------------------------------------------------------------------- cull
 
-constexpr int CULL_DYN_SMEM = (3 * 1024 + PAIR_W * 32) * 4;  // kill rows + transposed columns
+constexpr int CULL_CHUNK = 2048;  // probation entries per k_cull iteration (two per thread)
+constexpr int CULL_DYN_SMEM = (3 * CULL_CHUNK + PAIR_W * (CULL_CHUNK / 32)) * 4;  // kill rows + transposed columns
 
 __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* args) {
   const StepArgs& A = args[blockIdx.x];
@@ -177,11 +178,11 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
   if (!A.do_cull) return;
   __shared__ int sh[32];
   __shared__ PairAcc acc;
-  __shared__ int kills[1024], big[1024];
+  __shared__ int kills[CULL_CHUNK], big[CULL_CHUNK];
   __shared__ int nbig, nact_sh;
   extern __shared__ unsigned cull_dyn[];
-  unsigned* krow = cull_dyn;                 // [3*1024] per kill: observer window mask
-  unsigned* kcol = cull_dyn + 3 * 1024;      // [32][PAIR_W] per window slot: mask over the kills
+  unsigned* krow = cull_dyn;                   // [3*CULL_CHUNK] per kill: observer window mask
+  unsigned* kcol = cull_dyn + 3 * CULL_CHUNK;  // [CULL_CHUNK/32][PAIR_W] per window slot: mask over the kills
   __shared__ int kact[PAIR_W], kidx[PAIR_W];
   const long long c_t0 = gtime();
   pair_acc_init<1024>(&acc, A.cur);
@@ -190,27 +191,40 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
   const int n = M.scal[SC_RECENT_N];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int kept = 0, culled = 0, nbig_total = 0;
-  for (int base = 0; base < n; base += 1024) {
-    const int e = base + threadIdx.x;
-    int keep = 0, kill = 0, id = -1, born = 0;
-    if (e < n) {
-      id = M.recent_id[e];
-      born = M.recent_born[e];
-      if (M.alive[id]) {  // dead entries (merged away) just leave the list
-        const double ratio = (double)M.found[id] / (double)(M.visible[id] > 1 ? M.visible[id] : 1);
-        if (ratio < A.cc.found_ratio_min) kill = 1;
-        else if (A.processed - born >= A.cc.probation_kfs) kill = M.nobs[id] < A.cc.min_obs_graduate;
-        else keep = 1;
+  for (int base = 0; base < n; base += CULL_CHUNK) {
+    // two consecutive entries per thread (order-stable compaction)
+    int keep[2] = {0, 0}, kill[2] = {0, 0}, id[2] = {-1, -1}, born[2] = {0, 0};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = base + 2 * threadIdx.x + h;
+      if (e < n) {
+        id[h] = M.recent_id[e];
+        born[h] = M.recent_born[e];
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = id[h];
+      if (i >= 0 && M.alive[i]) {  // dead entries (merged away) just leave the list
+        const double ratio = (double)M.found[i] / (double)(M.visible[i] > 1 ? M.visible[i] : 1);
+        if (ratio < A.cc.found_ratio_min) kill[h] = 1;
+        else if (A.processed - born[h] >= A.cc.probation_kfs) kill[h] = M.nobs[i] < A.cc.min_obs_graduate;
+        else keep[h] = 1;
       }
     }
     int tk;
-    const int ak = block_excl_scan<1024>(kill, sh, tk);
-    if (kill) kills[ak] = id;
+    const int ak = block_excl_scan<1024>(kill[0] + kill[1], sh, tk);
+    if (kill[0]) kills[ak] = id[0];
+    if (kill[1]) kills[ak + kill[0]] = id[1];
     int tot;
-    const int at = block_excl_scan<1024>(keep, sh, tot);
-    if (keep) {  // stable in-place compaction: write index <= read index
-      M.recent_id[kept + at] = id;
-      M.recent_born[kept + at] = born;
+    const int at = block_excl_scan<1024>(keep[0] + keep[1], sh, tot);
+    if (keep[0]) {  // stable in-place compaction: write index <= read index
+      M.recent_id[kept + at] = id[0];
+      M.recent_born[kept + at] = born[0];
+    }
+    if (keep[1]) {
+      M.recent_id[kept + at + keep[0]] = id[1];
+      M.recent_born[kept + at + keep[0]] = born[1];
     }
     kept += tot;
     culled += tk;
@@ -246,17 +260,23 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
       }
       __syncthreads();
       // slots with any killed observer, then their pairs
-      if (threadIdx.x < PAIR_W) {
+      unsigned abal = 0u;
+      if (wid < PAIR_W / 32) {
         unsigned any = 0u;
         for (int w = 0; w < nkw; ++w) any |= kcol[w * PAIR_W + threadIdx.x];
-        kact[threadIdx.x] = any != 0u;
+        abal = __ballot_sync(0xffffffffu, any != 0u);
+        if (lane == 0) kact[wid] = __popc(abal);
       }
       __syncthreads();
-      if (threadIdx.x == 0) {
-        int m = 0;
-        for (int a = 0; a < PAIR_W; ++a)
-          if (kact[a]) kidx[m++] = a;
-        nact_sh = m;
+      if (wid < PAIR_W / 32) {  // active slots in order
+        int off = 0;
+        for (int w = 0; w < wid; ++w) off += kact[w];
+        if (abal >> lane & 1u) kidx[off + __popc(abal & ((1u << lane) - 1))] = threadIdx.x;
+        if (threadIdx.x == 0) {
+          int m = 0;
+          for (int w = 0; w < PAIR_W / 32; ++w) m += kact[w];
+          nact_sh = m;
+        }
       }
       __syncthreads();
       const int m = nact_sh, np = m * (m - 1) / 2;
