@@ -73,6 +73,7 @@ struct lm_ctx {
   size_t flush_bytes = 0;
   bool prof = false;
   int apply_cluster = 16;               // CTAs per map of the forward-apply cluster (LM_APPLY_CLUSTER)
+  int cull_cluster = 8;                 // CTAs per map of the recent-point cull cluster (LM_CULL_CLUSTER)
   std::vector<cudaEvent_t> prof_pool;   // free events
   std::vector<std::vector<cudaEvent_t>> prof_steps;  // 9 boundary events per step
 };
@@ -471,6 +472,10 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
                         (const void*)k_fuse_rev, (const void*)k_fuse_visible};
     for (const void* k : ks) CU(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pc));
   }
+  if (const char* e = getenv("LM_CULL_CLUSTER")) {
+    const int v = atoi(e);
+    ctx->cull_cluster = v < 1 ? 1 : (v > 8 ? 8 : v);
+  }
   if (const char* e = getenv("LM_APPLY_CLUSTER")) {
     const int v = atoi(e);
     ctx->apply_cluster = v < 1 ? 1 : (v > 16 ? 16 : v);
@@ -837,7 +842,24 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   k_begin<<<n, 128, 0, ctx->stream>>>(dmaps, dv);
   k_insert<<<n, 256, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;
-  k_cull<<<n, 1024, CULL_DYN_SMEM, ctx->stream>>>(dmaps, dv);
+  {
+    // recent-point cull: one cluster per map, as wide as the batch leaves SMs for
+    int cl = ctx->cull_cluster / n;
+    cl = cl < 1 ? 1 : cl;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(n * cl);
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = CULL_DYN_SMEM;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CU(cudaLaunchKernelEx(&cfg, k_cull, dmaps, (const StepArgs*)dv));
+  }
   if ((rc = mark())) return rc;
   k_select<<<n, 256, dyn, ctx->stream>>>(dmaps, dv, slots);
   if ((rc = mark())) return rc;

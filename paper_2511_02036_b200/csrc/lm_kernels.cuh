@@ -173,9 +173,13 @@ constexpr int CULL_CHUNK = 2048;  // probation entries per k_cull iteration (two
 constexpr int CULL_DYN_SMEM = (3 * CULL_CHUNK + PAIR_W * (CULL_CHUNK / 32)) * 4;  // kill rows + transposed columns
 
 __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* args) {
-  const StepArgs& A = args[blockIdx.x];
+  // one cluster per map: rank 0 classifies and owns the accumulator; every rank takes a share
+  // of the kills' scattered record updates (one SM's load/store pipe was their bound)
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank(), nranks = (int)cl.num_blocks();
+  const StepArgs& A = args[blockIdx.x / nranks];
   const DevMap& M = maps[A.map];
-  if (!A.do_cull) return;
+  if (!A.do_cull) return;  // (uniform over the cluster)
   __shared__ int sh[32];
   __shared__ PairAcc acc;
   __shared__ int kills[CULL_CHUNK], big[CULL_CHUNK];
@@ -184,6 +188,12 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
   unsigned* krow = cull_dyn;                   // [3*CULL_CHUNK] per kill: observer window mask
   unsigned* kcol = cull_dyn + 3 * CULL_CHUNK;  // [CULL_CHUNK/32][PAIR_W] per window slot: mask over the kills
   __shared__ int kact[PAIR_W], kidx[PAIR_W];
+  __shared__ int tk_sh;
+  int* kills0 = cl.map_shared_rank(kills, 0);
+  int* big0 = cl.map_shared_rank(big, 0);
+  int* nbig0 = cl.map_shared_rank(&nbig, 0);
+  unsigned* krow0 = cl.map_shared_rank(krow, 0);
+  const int* tk0 = cl.map_shared_rank(&tk_sh, 0);
   const long long c_t0 = gtime();
   pair_acc_init<1024>(&acc, A.cur);
   const long long c_t1 = gtime();
@@ -192,6 +202,8 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int kept = 0, culled = 0, nbig_total = 0;
   for (int base = 0; base < n; base += CULL_CHUNK) {
+    int tk = 0;
+    if (rank == 0) {
     // two consecutive entries per thread (order-stable compaction)
     int keep[2] = {0, 0}, kill[2] = {0, 0}, id[2] = {-1, -1}, born[2] = {0, 0};
 #pragma unroll
@@ -212,7 +224,6 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
         else keep[h] = 1;
       }
     }
-    int tk;
     const int ak = block_excl_scan<1024>(kill[0] + kill[1], sh, tk);
     if (kill[0]) kills[ak] = id[0];
     if (kill[1]) kills[ak + kill[0]] = id[1];
@@ -228,21 +239,32 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
     }
     kept += tot;
     culled += tk;
-    if (threadIdx.x == 0) nbig = 0;
-    __syncthreads();
-    const long long c_a = gtime();
-    // independent points, warp each: bindings and counters cleared, the observer set as a
-    // window bitmask (rows); the covisibility decrements of all of them are the pair counts
-    // of the rows' Gram matrix, counted with popcounts over the transposed masks instead of
-    // one contended shared atomic per observer pair. Kills with an observer outside the
-    // window take the per-pair path.
-    for (int k = threadIdx.x; k < tk; k += 1024) {
-      if (!kill_point_rows_thread(M, kills[k], &acc, &krow[3 * k])) {
-        krow[3 * k] = krow[3 * k + 1] = krow[3 * k + 2] = 0u;
-        big[atomicAdd(&nbig, 1)] = kills[k];
-      }
+    if (threadIdx.x == 0) {
+      nbig = 0;
+      tk_sh = tk;
     }
-    __syncthreads();
+    }
+    cl.sync();  // the chunk's kill list (rank 0) is published
+    const long long c_a = gtime();
+    // independent points, thread each, spread over the cluster: bindings and counters
+    // cleared, the observer set as a window bitmask (rows, into rank 0); the covisibility
+    // decrements of all of them are the pair counts of the rows' Gram matrix, counted with
+    // popcounts over the transposed masks instead of one contended shared atomic per
+    // observer pair. Kills with an observer outside the window take the per-pair path.
+    tk = *tk0;
+    for (int k = rank + nranks * threadIdx.x; k < tk; k += nranks * 1024) {
+      const int id = kills0[k];
+      unsigned r[3];
+      if (!kill_point_rows_thread(M, id, &acc, r)) {
+        r[0] = r[1] = r[2] = 0u;
+        big0[atomicAdd(nbig0, 1)] = id;
+      }
+      krow0[3 * k] = r[0];
+      krow0[3 * k + 1] = r[1];
+      krow0[3 * k + 2] = r[2];
+    }
+    cl.sync();  // rows complete; ranks > 0 go on to the next chunk
+    if (rank != 0) continue;
     for (int k = wid; k < nbig; k += 32) kill_point_warp(M, big[k], lane, &acc);  // outside the window
     nbig_total += nbig;
     {
@@ -295,6 +317,7 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
     __syncthreads();
     c_kill += gtime() - c_a;
   }
+  if (rank != 0) return;
   const long long c_t2 = gtime();
   pair_acc_flush<1024>(M, &acc);
   const long long c_t3 = gtime();
