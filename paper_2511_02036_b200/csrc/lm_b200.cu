@@ -569,7 +569,7 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(s.nb_n, NMAX); A(s.nb_bucket, NMAX * (LMAX + 1)); A(s.nb_j, NK); A(s.nb_desc, 2 * NK);
   A(s.nb_u, NK); A(s.nb_v, NK); A(s.nb_thr, NK); A(s.pick, NK); A(s.bestj, NK);
   A(s.cand_n, NMAX); A(s.cand_i, NK); A(s.cand_j, NK); A(s.cand_d, NK); A(s.cand_st, NK); A(s.cand_X, 3 * NK);
-  A(s.win_rank, d.kpkf_max); A(s.mask_cur, d.kpkf_max); A(s.mask_nbr, d.kpkf_max);
+  A(s.win_rank, d.kpkf_max); A(s.crank, NK); A(s.cmeta, 4); A(s.mask_cur, d.kpkf_max); A(s.mask_nbr, d.kpkf_max);
   A(s.targets, TMAX); A(s.n_targets, 1); A(s.rank_buf, (size_t)TMAX * (3 * K + 1) + (size_t)TMAX * K * 2 + 2);
   s.pts_cap = d.kpkf_max;
   A(s.pts, s.pts_cap); A(s.geo, s.pts_cap);
@@ -870,6 +870,7 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   k_tri<<<dim3(nbr_dim, n), 256, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;
   k_commit<<<n, 1024, 0, ctx->stream>>>(dmaps, dv);
+  k_commit_write<<<dim3((kpkf + 127) / 128, NMAX, n), 128, 0, ctx->stream>>>(dmaps, dv);
   if ((rc = mark())) return rc;
   k_fuse_targets<<<n, 1024, dyn, ctx->stream>>>(dmaps, dv, slots);
   if ((rc = mark())) return rc;
@@ -913,7 +914,7 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   k_fuse_visible<<<dim3((kpkf + 255) / 256, tfuse, n), 256, 0, ctx->stream>>>(dmaps, dv);
   k_end<<<n, 32, 0, ctx->stream>>>(dmaps, dv, ctx->d_totals);
   if ((rc = mark())) return rc;
-  ctx->launches += 18;
+  ctx->launches += 19;
   if (ctx->prof) ctx->prof_steps.push_back(evs);
   CHECK_LAUNCH();
   CU(cudaEventRecord(ctx->args_ev[e], ctx->stream));

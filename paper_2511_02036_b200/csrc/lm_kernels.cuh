@@ -727,7 +727,14 @@ __global__ void __launch_bounds__(1024) k_commit(DevMap* maps, const StepArgs* a
     }
   }
   __syncthreads();
-  if (okcap) {
+  // creation ranks (the records are written wide by k_commit_write: one SM's load/store
+  // pipe bounds ~900 scattered record writes)
+  if (threadIdx.x == 0) {
+    M.s.cmeta[0] = id0;
+    M.s.cmeta[1] = obs0;
+    M.s.cmeta[2] = rec0;
+  }
+  {
     int run = 0;
     for (int b0 = 0; b0 < total; b0 += 1024) {
       const int g = b0 + threadIdx.x;
@@ -735,43 +742,8 @@ __global__ void __launch_bounds__(1024) k_commit(DevMap* maps, const StepArgs* a
       if (g < total) oc = outcome(g, r, k);
       int tot;
       const int at = block_excl_scan<1024>(oc == 0, sh, tot);
-      if (oc == 0) {
-        const int rank = run + at;
-        const int id = id0 + rank;
-        const size_t e = (size_t)r * M.kpkf_max + k;
-        const int i = M.s.cand_i[e], j = M.s.cand_j[e];
-        const int nb = M.s.nbr[r];
-        const int ga = M.kp_off[cur] + i, gb = M.kp_off[nb] + j;
-        M.pos[3 * id] = M.s.cand_X[3 * e];
-        M.pos[3 * id + 1] = M.s.cand_X[3 * e + 1];
-        M.pos[3 * id + 2] = M.s.cand_X[3 * e + 2];
-        const bool cur_first = M.kf_id[cur] < M.kf_id[nb];
-        const int grep = cur_first ? ga : gb;
-        M.rep[2 * id] = M.kdesc[2 * grep];
-        M.rep[2 * id + 1] = M.kdesc[2 * grep + 1];
-        M.alive[id] = 1;
-        M.found[id] = 1;
-        M.visible[id] = 1;
-        M.first_kf[id] = M.kf_id[cur];
-        const int oo = obs0 + 4 * rank;
-        M.ooff[id] = oo;
-        M.ocap[id] = 4;
-        M.nobs[id] = 2;
-        M.obs[oo] = cur_first ? make_int2(cur, i) : make_int2(nb, j);
-        M.obs[oo + 1] = cur_first ? make_int2(nb, j) : make_int2(cur, i);
-        M.dirty[id] = 0;
-        M.gval[id] = 0;
-        {  // a new point's counter row, written whole (no read-modify-write)
-          const int la = M.klev[ga], lb = M.klev[gb];
-          int* crow = M.counts + (size_t)id * M.L;
-          for (int l = 0; l < M.L; ++l) crow[l] = (l == la) + (l == lb);
-        }
-        M.kbind[ga] = id;
-        M.kbind[gb] = id;
-        atomicAdd(&per_r[r], 1);
-        M.recent_id[rec0 + rank] = id;
-        M.recent_born[rec0 + rank] = A.processed;
-      }
+      if (g < total) M.s.crank[(size_t)r * M.kpkf_max + k] = okcap && oc == 0 ? run + at : -1;
+      if (okcap && oc == 0) atomicAdd(&per_r[r], 1);
       run += tot;
     }
   }
@@ -794,6 +766,54 @@ __global__ void __launch_bounds__(1024) k_commit(DevMap* maps, const StepArgs* a
       M.scal[SC_RECENT_N] = rec0 + created;
     }
   }
+}
+
+// the new points' records, thread per (neighbour, candidate) of k_commit's ranks
+__global__ void __launch_bounds__(128) k_commit_write(DevMap* maps, const StepArgs* args) {
+  const StepArgs& A = args[blockIdx.z];
+  const DevMap& M = maps[A.map];
+  if (!A.do_create || A.search_only) return;
+  const int r = blockIdx.y;
+  if (r >= M.s.stats->n_neighbors) return;
+  const int k = blockIdx.x * 128 + threadIdx.x;
+  if (k >= M.s.cand_n[r]) return;
+  const size_t e = (size_t)r * M.kpkf_max + k;
+  const int rank = M.s.crank[e];
+  if (rank < 0) return;
+  const int cur = A.cur;
+  const int id0 = M.s.cmeta[0], obs0 = M.s.cmeta[1], rec0 = M.s.cmeta[2];
+  const int id = id0 + rank;
+  const int i = M.s.cand_i[e], j = M.s.cand_j[e];
+  const int nb = M.s.nbr[r];
+  const int ga = M.kp_off[cur] + i, gb = M.kp_off[nb] + j;
+  M.pos[3 * id] = M.s.cand_X[3 * e];
+  M.pos[3 * id + 1] = M.s.cand_X[3 * e + 1];
+  M.pos[3 * id + 2] = M.s.cand_X[3 * e + 2];
+  const bool cur_first = M.kf_id[cur] < M.kf_id[nb];
+  const int grep = cur_first ? ga : gb;
+  M.rep[2 * id] = M.kdesc[2 * grep];
+  M.rep[2 * id + 1] = M.kdesc[2 * grep + 1];
+  M.alive[id] = 1;
+  M.found[id] = 1;
+  M.visible[id] = 1;
+  M.first_kf[id] = M.kf_id[cur];
+  const int oo = obs0 + 4 * rank;
+  M.ooff[id] = oo;
+  M.ocap[id] = 4;
+  M.nobs[id] = 2;
+  M.obs[oo] = cur_first ? make_int2(cur, i) : make_int2(nb, j);
+  M.obs[oo + 1] = cur_first ? make_int2(nb, j) : make_int2(cur, i);
+  M.dirty[id] = 0;
+  M.gval[id] = 0;
+  {  // a new point's counter row, written whole (no read-modify-write)
+    const int la = M.klev[ga], lb = M.klev[gb];
+    int* crow = M.counts + (size_t)id * M.L;
+    for (int l = 0; l < M.L; ++l) crow[l] = (l == la) + (l == lb);
+  }
+  M.kbind[ga] = id;
+  M.kbind[gb] = id;
+  M.recent_id[rec0 + rank] = id;
+  M.recent_born[rec0 + rank] = A.processed;
 }
 
 // ---------------------------------------------------------------------------------- fusion

@@ -86,6 +86,8 @@ struct Scratch {
   int* cand_st;
   double* cand_X;        // [NMAX*kpkf_max*3]
   int* win_rank;         // [kpkf_max]
+  int* crank;            // [NMAX*kpkf_max] creation rank of a candidate (-1: not created)
+  int* cmeta;            // [4] first new id, observation head, probation length at commit
   unsigned char* mask_cur;  // optional explicit unbound masks (lm_search)
   unsigned char* mask_nbr;
   // fusion
