@@ -74,6 +74,7 @@ struct lm_ctx {
   bool prof = false;
   int apply_cluster = 16;               // CTAs per map of the forward-apply cluster (LM_APPLY_CLUSTER)
   int cull_cluster = 8;                 // CTAs per map of the recent-point cull cluster (LM_CULL_CLUSTER)
+  bool pdl = true;                      // programmatic dependent launch of the step kernels (LM_PDL)
   std::vector<cudaEvent_t> prof_pool;   // free events
   std::vector<std::vector<cudaEvent_t>> prof_steps;  // 9 boundary events per step
 };
@@ -426,6 +427,35 @@ static int op_status(lm_ctx* ctx, int code, const char* what) {
 }
 
 // ------------------------------------------------------------------- ABI
+// step-kernel launch: programmatic dependent launch (LM_PDL=0 disables) and an optional
+// cluster dimension
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(lm_ctx* ctx, void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, int cluster,
+                            Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (ctx->pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (cluster > 0) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = cluster;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 extern "C" {
 
 int lm_version(void) { return 1; }
@@ -472,6 +502,7 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
                         (const void*)k_fuse_rev, (const void*)k_fuse_visible};
     for (const void* k : ks) CU(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pc));
   }
+  if (const char* e = getenv("LM_PDL")) ctx->pdl = atoi(e) != 0;
   if (const char* e = getenv("LM_CULL_CLUSTER")) {
     const int v = atoi(e);
     ctx->cull_cluster = v < 1 ? 1 : (v > 8 ? 8 : v);
@@ -742,6 +773,7 @@ int lm_kf_stage(lm_ctx* ctx, int32_t map, int64_t kf_id, const double quat[4], c
 
 // ------------------------------------------------------------------- steps
 __global__ void k_begin(DevMap* maps, const StepArgs* args) {
+  pdl_enter();
   const DevMap& M = maps[args[blockIdx.x].map];
   int* p = (int*)M.s.stats;
   for (int k = threadIdx.x; k < (int)(sizeof(lm_step_stats) / 4); k += blockDim.x) p[k] = 0;
@@ -751,6 +783,7 @@ __global__ void k_begin(DevMap* maps, const StepArgs* args) {
 // fields are independent loads) and the sums written back, instead of one dependent
 // read-modify-write round trip per field
 __global__ void k_end(DevMap* maps, const StepArgs* args, lm_step_stats** totals) {
+  pdl_enter();
   const DevMap& M = maps[args[blockIdx.x].map];
   if (threadIdx.x) return;
   lm_step_stats* st = M.s.stats;
@@ -839,80 +872,56 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   };
   int rc = LM_OK;
   if ((rc = mark())) return rc;
-  k_begin<<<n, 128, 0, ctx->stream>>>(dmaps, dv);
-  k_insert<<<n, 256, 0, ctx->stream>>>(dmaps, dv);
+  CU(launch_k(ctx, k_begin, dim3(n), dim3(128), 0, 0, dmaps, dv));
+  CU(launch_k(ctx, k_insert, dim3(n), dim3(256), 0, 0, dmaps, dv));
   if ((rc = mark())) return rc;
   {
     // recent-point cull: one cluster per map, as wide as the batch leaves SMs for
     int cl = ctx->cull_cluster / n;
     cl = cl < 1 ? 1 : cl;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(n * cl);
-    cfg.blockDim = dim3(1024);
-    cfg.dynamicSmemBytes = CULL_DYN_SMEM;
-    cfg.stream = ctx->stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cl;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    CU(cudaLaunchKernelEx(&cfg, k_cull, dmaps, (const StepArgs*)dv));
+    CU(launch_k(ctx, k_cull, dim3(n * cl), dim3(1024), CULL_DYN_SMEM, cl, dmaps, (const StepArgs*)dv));
   }
   if ((rc = mark())) return rc;
-  k_select<<<n, 256, dyn, ctx->stream>>>(dmaps, dv, slots);
+  CU(launch_k(ctx, k_select, dim3(n), dim3(256), dyn, 0, dmaps, dv, slots));
   if ((rc = mark())) return rc;
-  k_prep<<<dim3(1 + nbr_dim, n), 256, 0, ctx->stream>>>(dmaps, dv);
+  CU(launch_k(ctx, k_prep, dim3(1 + nbr_dim, n), dim3(256), 0, 0, dmaps, dv));
   if ((rc = mark())) return rc;
-  k_match<<<dim3(nbr_dim, tiles, n), MATCH_WARPS * 32, 0, ctx->stream>>>(dmaps, dv);
+  CU(launch_k(ctx, k_match, dim3(nbr_dim, tiles, n), dim3(MATCH_WARPS * 32), 0, 0, dmaps, dv));
   if ((rc = mark())) return rc;
-  k_tri<<<dim3(nbr_dim, n), 256, 0, ctx->stream>>>(dmaps, dv);
+  CU(launch_k(ctx, k_tri, dim3(nbr_dim, n), dim3(256), 0, 0, dmaps, dv));
   if ((rc = mark())) return rc;
-  k_commit<<<n, 1024, 0, ctx->stream>>>(dmaps, dv);
-  k_commit_write<<<dim3((kpkf + 127) / 128, NMAX, n), 128, 0, ctx->stream>>>(dmaps, dv);
+  CU(launch_k(ctx, k_commit, dim3(n), dim3(1024), 0, 0, dmaps, dv));
+  CU(launch_k(ctx, k_commit_write, dim3((kpkf + 127) / 128, NMAX, n), dim3(128), 0, 0, dmaps, dv));
   if ((rc = mark())) return rc;
-  k_fuse_targets<<<n, 1024, dyn, ctx->stream>>>(dmaps, dv, slots);
+  CU(launch_k(ctx, k_fuse_targets, dim3(n), dim3(1024), dyn, 0, dmaps, dv, slots));
   if ((rc = mark())) return rc;
-  k_fuse_geo<<<dim3((kpkf + 7) / 8, n), 256, 0, ctx->stream>>>(dmaps, dv);
+  CU(launch_k(ctx, k_fuse_geo, dim3((kpkf + 7) / 8, n), dim3(256), 0, 0, dmaps, dv));
   if ((rc = mark())) return rc;
-  k_fuse_gather<<<dim3((tfuse * kpkf + 255) / 256, n), 256, 0, ctx->stream>>>(dmaps, dv);
+  CU(launch_k(ctx, k_fuse_gather, dim3((tfuse * kpkf + 255) / 256, n), dim3(256), 0, 0, dmaps, dv));
   if ((rc = mark())) return rc;
   {
     // forward apply: one cluster per map, as wide as the batch leaves SMs for
     int cl = ctx->apply_cluster / n;
     cl = cl < 1 ? 1 : (cl > ctx->apply_cluster ? ctx->apply_cluster : cl);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(n * cl);
-    cfg.blockDim = dim3(APPLY_THREADS);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = ctx->stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cl;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    CU(cudaLaunchKernelEx(&cfg, k_fuse_apply, dmaps, (const StepArgs*)dv));
+    CU(launch_k(ctx, k_fuse_apply, dim3(n * cl), dim3(APPLY_THREADS), 0, cl, dmaps, (const StepArgs*)dv));
   }
   if ((rc = mark())) return rc;
-  k_fuse_refresh<<<dim3(148, n), 256, 0, ctx->stream>>>(dmaps, dv);
+  CU(launch_k(ctx, k_fuse_refresh, dim3(148, n), dim3(256), 0, 0, dmaps, dv));
   if ((rc = mark())) return rc;
   if (n == 1) {
-    k_fuse_spec<true><<<dim3((kpkf + 255) / 256, tfuse, n), 256, 0, ctx->stream>>>(dmaps, dv);
+    CU(launch_k(ctx, k_fuse_spec<true>, dim3((kpkf + 255) / 256, tfuse, n), dim3(256), 0, 0, dmaps, dv));
   } else {  // batches: one gather per distinct point instead of one per (pass, point)
-    k_fuse_spec_pts<<<dim3((kpkf + 255) / 256, tfuse, n), 256, 0, ctx->stream>>>(dmaps, dv);
-    k_fuse_spec_hit<<<dim3(16, n), 256, 0, ctx->stream>>>(dmaps, dv);
-    k_fuse_spec<false><<<dim3((kpkf + 255) / 256, tfuse, n), 256, 0, ctx->stream>>>(dmaps, dv);
+    CU(launch_k(ctx, k_fuse_spec_pts, dim3((kpkf + 255) / 256, tfuse, n), dim3(256), 0, 0, dmaps, dv));
+    CU(launch_k(ctx, k_fuse_spec_hit, dim3(16, n), dim3(256), 0, 0, dmaps, dv));
+    CU(launch_k(ctx, k_fuse_spec<false>, dim3((kpkf + 255) / 256, tfuse, n), dim3(256), 0, 0, dmaps, dv));
     ctx->launches += 2;
   }
   if ((rc = mark())) return rc;
-  k_fuse_post<<<dim3(POST_BLOCKS, n), 256, 0, ctx->stream>>>(dmaps, dv);
-  k_fuse_rev<<<n, REV_THREADS, rev_smem, ctx->stream>>>(dmaps, dv, rev_smem);
+  CU(launch_k(ctx, k_fuse_post, dim3(POST_BLOCKS, n), dim3(256), 0, 0, dmaps, dv));
+  CU(launch_k(ctx, k_fuse_rev, dim3(n), dim3(REV_THREADS), rev_smem, 0, dmaps, dv, (int)rev_smem));
   if ((rc = mark())) return rc;
-  k_fuse_visible<<<dim3((kpkf + 255) / 256, tfuse, n), 256, 0, ctx->stream>>>(dmaps, dv);
-  k_end<<<n, 32, 0, ctx->stream>>>(dmaps, dv, ctx->d_totals);
+  CU(launch_k(ctx, k_fuse_visible, dim3((kpkf + 255) / 256, tfuse, n), dim3(256), 0, 0, dmaps, dv));
+  CU(launch_k(ctx, k_end, dim3(n), dim3(32), 0, 0, dmaps, dv, ctx->d_totals));
   if ((rc = mark())) return rc;
   ctx->launches += 19;
   if (ctx->prof) ctx->prof_steps.push_back(evs);

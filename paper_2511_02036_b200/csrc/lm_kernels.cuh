@@ -49,6 +49,14 @@ struct StepArgs {
 
 // ---------------------------------------------------------------------------------- helpers
 
+// programmatic dependent launch: a step kernel first waits for its predecessor's completion
+// (and memory), then lets its own successor be scheduled, so each launch's dispatch overlaps
+// the previous kernel instead of following it (no-ops when launched without the attribute)
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ long long gtime() {  // ns, device-wide clock
 #ifdef LM_NO_PHASE_TIMERS
   return 0;
@@ -137,6 +145,7 @@ __device__ int ranked_neighbors(const DevMap& M, int k, int n, int* sh_slot, uns
 // ---------------------------------------------------------------------------------- insert
 
 __global__ void __launch_bounds__(256) k_insert(DevMap* maps, const StepArgs* args) {
+  pdl_enter();
   const StepArgs& A = args[blockIdx.x];
   const DevMap& M = maps[A.map];
   if (!A.do_insert) return;
@@ -173,6 +182,7 @@ constexpr int CULL_CHUNK = 2048;  // probation entries per k_cull iteration (two
 constexpr int CULL_DYN_SMEM = (3 * CULL_CHUNK + PAIR_W * (CULL_CHUNK / 32)) * 4;  // kill rows + transposed columns
 
 __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* args) {
+  pdl_enter();
   // one cluster per map: rank 0 classifies and owns the accumulator; every rank takes a share
   // of the kills' scattered record updates (one SM's load/store pipe was their bound)
   cg::cluster_group cl = cg::this_cluster();
@@ -336,6 +346,7 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
 // ---------------------------------------------------------------------------------- select
 
 __global__ void __launch_bounds__(256) k_select(DevMap* maps, const StepArgs* args, int n_slots_max) {
+  pdl_enter();
   const StepArgs& A = args[blockIdx.x];
   const DevMap& M = maps[A.map];
   if (!A.do_create) return;
@@ -415,6 +426,7 @@ __device__ __forceinline__ bool is_unbound(const DevMap& M, const StepArgs& A, i
 }
 
 __global__ void __launch_bounds__(256) k_prep(DevMap* maps, const StepArgs* args) {
+  pdl_enter();
   const StepArgs& A = args[blockIdx.y];
   const DevMap& M = maps[A.map];
   if (!A.do_create) return;
@@ -531,6 +543,7 @@ __global__ void __launch_bounds__(256) k_prep(DevMap* maps, const StepArgs* args
 // The running minimum is the lexicographic (dist, j) key of the reference's first-argmin;
 // warp slices combine with a shared atomicMin, neighbour one-to-one with a global one.
 __global__ void __launch_bounds__(MATCH_WARPS * 32) k_match(DevMap* maps, const StepArgs* args) {
+  pdl_enter();
   const StepArgs& A = args[blockIdx.z];
   const DevMap& M = maps[A.map];
   if (!A.do_create) return;
@@ -607,6 +620,7 @@ __global__ void __launch_bounds__(MATCH_WARPS * 32) k_match(DevMap* maps, const 
 // ---------------------------------------------------------------------------------- tri
 
 __global__ void __launch_bounds__(256) k_tri(DevMap* maps, const StepArgs* args) {
+  pdl_enter();
   const StepArgs& A = args[blockIdx.y];
   const DevMap& M = maps[A.map];
   if (!A.do_create) return;
@@ -669,6 +683,7 @@ __global__ void __launch_bounds__(256) k_tri(DevMap* maps, const StepArgs* args)
 // ---------------------------------------------------------------------------------- commit
 
 __global__ void __launch_bounds__(1024) k_commit(DevMap* maps, const StepArgs* args) {
+  pdl_enter();
   const StepArgs& A = args[blockIdx.x];
   const DevMap& M = maps[A.map];
   if (!A.do_create || A.search_only) return;
@@ -770,6 +785,7 @@ __global__ void __launch_bounds__(1024) k_commit(DevMap* maps, const StepArgs* a
 
 // the new points' records, thread per (neighbour, candidate) of k_commit's ranks
 __global__ void __launch_bounds__(128) k_commit_write(DevMap* maps, const StepArgs* args) {
+  pdl_enter();
   const StepArgs& A = args[blockIdx.z];
   const DevMap& M = maps[A.map];
   if (!A.do_create || A.search_only) return;
@@ -1569,6 +1585,7 @@ __device__ __forceinline__ long long pass_bytes(long long pts, long long obs, lo
 enum FuseCtl { FC_T = 0, FC_P = 1, FC_NACT = 2, FC_NU = 3, FC_NSP = 4, FC_N = 8 };
 
 __global__ void __launch_bounds__(1024) k_fuse_targets(DevMap* maps, const StepArgs* args, int n_slots_max) {
+  pdl_enter();
   const StepArgs& A = args[blockIdx.x];
   const DevMap& M = maps[A.map];
   if (!A.do_fuse) return;
@@ -1611,6 +1628,7 @@ __global__ void __launch_bounds__(1024) k_fuse_targets(DevMap* maps, const StepA
 
 // warp per forward point: refresh a stale rep descriptor, then the geometry row
 __global__ void __launch_bounds__(256) k_fuse_geo(DevMap* maps, const StepArgs* args) {
+  pdl_enter();
   const StepArgs& A = args[blockIdx.y];
   const DevMap& M = maps[A.map];
   if (!A.do_fuse) return;
@@ -1636,6 +1654,7 @@ __global__ void __launch_bounds__(256) k_fuse_geo(DevMap* maps, const StepArgs* 
 
 // thread per (target, point) of the forward gather; per-CTA ordered compaction
 __global__ void __launch_bounds__(256) k_fuse_gather(DevMap* maps, const StepArgs* args) {
+  pdl_enter();
   const StepArgs& A = args[blockIdx.y];
   const DevMap& M = maps[A.map];
   if (!A.do_fuse) return;
@@ -1666,6 +1685,7 @@ constexpr int APPLY_THREADS = 512;  // k_fuse_apply CTA (128 registers: apply_te
 // cluster size selects the map). The ~4.5k forward actions of a C2 keyframe spread over the
 // cluster's CTAs; the reservation rounds synchronise with barrier.cluster.
 __global__ void __launch_bounds__(APPLY_THREADS, 1) k_fuse_apply(DevMap* maps, const StepArgs* args) {
+  pdl_enter();
   cg::cluster_group cl = cg::this_cluster();
   const int ncl = (int)cl.num_blocks(), rank = (int)cl.block_rank();
   const StepArgs& A = args[blockIdx.x / ncl];
@@ -1755,6 +1775,7 @@ enum PassInfo { PI_NACT = 0, PI_LIVE = 1, PI_OBS = 2, PI_N = 3 };
 // warp per point touched since the last refresh: representative descriptor + geometry cache;
 // also clears the reverse-pass bookkeeping for k_fuse_spec
 __global__ void __launch_bounds__(256) k_fuse_refresh(DevMap* maps, const StepArgs* args) {
+  pdl_enter();
   const StepArgs& A = args[blockIdx.y];
   const DevMap& M = maps[A.map];
   if (!A.do_fuse) return;
@@ -1831,6 +1852,7 @@ __device__ __forceinline__ void store_item(const DevMap& M, size_t it, const Ite
 
 // (1) thread per (pass, keypoint): each live bound point joins the distinct list once
 __global__ void __launch_bounds__(256) k_fuse_spec_pts(DevMap* maps, const StepArgs* args) {
+  pdl_enter();
   const StepArgs& A = args[blockIdx.z];
   const DevMap& M = maps[A.map];
   if (!A.do_fuse) return;
@@ -1847,6 +1869,7 @@ __global__ void __launch_bounds__(256) k_fuse_spec_pts(DevMap* maps, const StepA
 
 // (2) thread per distinct point (grid-stride): geometry, window search, hit list
 __global__ void __launch_bounds__(256) k_fuse_spec_hit(DevMap* maps, const StepArgs* args) {
+  pdl_enter();
   const StepArgs& A = args[blockIdx.y];
   const DevMap& M = maps[A.map];
   if (!A.do_fuse) return;
@@ -1868,6 +1891,7 @@ __global__ void __launch_bounds__(256) k_fuse_spec_hit(DevMap* maps, const StepA
 // its point's hit itself and (1)/(2) are skipped.
 template <bool GATHER>
 __global__ void __launch_bounds__(256) k_fuse_spec(DevMap* maps, const StepArgs* args) {
+  pdl_enter();
   const StepArgs& A = args[blockIdx.z];
   const DevMap& M = maps[A.map];
   if (!A.do_fuse) return;
@@ -1925,6 +1949,7 @@ __global__ void __launch_bounds__(256) k_fuse_spec(DevMap* maps, const StepArgs*
 constexpr int POST_MAXN = 128;
 constexpr int POST_BLOCKS = 148;  // k_fuse_post grid (x): one warp per speculated point at C2 sizes
 __global__ void __launch_bounds__(256) k_fuse_post(DevMap* maps, const StepArgs* args) {
+  pdl_enter();
   const StepArgs& A = args[blockIdx.y];
   const DevMap& M = maps[A.map];
   if (!A.do_fuse || M.s.fctl[FC_T] == 0) return;
@@ -1996,6 +2021,7 @@ __global__ void __launch_bounds__(256) k_fuse_post(DevMap* maps, const StepArgs*
 
 // reverse passes (fusion.py:337-346), one CTA per map; see the block comment above
 __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const StepArgs* args, int smem_bytes) {
+  pdl_enter();
   const StepArgs& A = args[blockIdx.x];
   const DevMap& M = maps[A.map];
   if (!A.do_fuse) return;
@@ -2649,6 +2675,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
 // deferred visible counters of every reverse pass (thread per item); a point merged away
 // later in this step's reverse phase passes its bump on to its winner
 __global__ void __launch_bounds__(256) k_fuse_visible(DevMap* maps, const StepArgs* args) {
+  pdl_enter();
   const StepArgs& A = args[blockIdx.z];
   const DevMap& M = maps[A.map];
   if (!A.do_fuse) return;
