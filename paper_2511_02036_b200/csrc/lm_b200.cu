@@ -74,7 +74,11 @@ struct lm_ctx {
   bool prof = false;
   int apply_cluster = 16;               // CTAs per map of the forward-apply cluster (LM_APPLY_CLUSTER)
   int cull_cluster = 8;                 // CTAs per map of the recent-point cull cluster (LM_CULL_CLUSTER)
-  bool pdl = true;                      // programmatic dependent launch of the step kernels (LM_PDL)
+  // programmatic dependent launch of the step kernels (LM_PDL=0/1 overrides): on for
+  // single-session launches; off for batches, whose concurrent stream groups lose SMs to
+  // successor CTAs parked in griddepcontrol.wait (C5: 16.2k -> 11.6k KF/s with it)
+  int pdl = -1;
+  bool pdl_now = false;                 // this launch sequence
   std::vector<cudaEvent_t> prof_pool;   // free events
   std::vector<std::vector<cudaEvent_t>> prof_steps;  // 9 boundary events per step
 };
@@ -427,7 +431,7 @@ static int op_status(lm_ctx* ctx, int code, const char* what) {
 }
 
 // ------------------------------------------------------------------- ABI
-// step-kernel launch: programmatic dependent launch (LM_PDL=0 disables) and an optional
+// step-kernel launch: programmatic dependent launch  and an optional
 // cluster dimension
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_k(lm_ctx* ctx, void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, int cluster,
@@ -439,7 +443,7 @@ static cudaError_t launch_k(lm_ctx* ctx, void (*k)(KArgs...), dim3 g, dim3 b, si
   cfg.stream = ctx->stream;
   cudaLaunchAttribute at[2];
   int na = 0;
-  if (ctx->pdl) {
+  if (ctx->pdl_now) {
     at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
@@ -502,7 +506,7 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
                         (const void*)k_fuse_rev, (const void*)k_fuse_visible};
     for (const void* k : ks) CU(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pc));
   }
-  if (const char* e = getenv("LM_PDL")) ctx->pdl = atoi(e) != 0;
+  if (const char* e = getenv("LM_PDL")) ctx->pdl = atoi(e) != 0 ? 1 : 0;
   if (const char* e = getenv("LM_CULL_CLUSTER")) {
     const int v = atoi(e);
     ctx->cull_cluster = v < 1 ? 1 : (v > 8 ? 8 : v);
@@ -871,6 +875,7 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
     return LM_OK;
   };
   int rc = LM_OK;
+  ctx->pdl_now = ctx->pdl < 0 ? n == 1 : ctx->pdl == 1;
   if ((rc = mark())) return rc;
   CU(launch_k(ctx, k_begin, dim3(n), dim3(128), 0, 0, dmaps, dv));
   CU(launch_k(ctx, k_insert, dim3(n), dim3(256), 0, 0, dmaps, dv));
