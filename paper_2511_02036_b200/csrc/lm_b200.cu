@@ -776,12 +776,6 @@ int lm_kf_stage(lm_ctx* ctx, int32_t map, int64_t kf_id, const double quat[4], c
 }
 
 // ------------------------------------------------------------------- steps
-__global__ void k_begin(DevMap* maps, const StepArgs* args) {
-  pdl_enter();
-  const DevMap& M = maps[args[blockIdx.x].map];
-  int* p = (int*)M.s.stats;
-  for (int k = threadIdx.x; k < (int)(sizeof(lm_step_stats) / 4); k += blockDim.x) p[k] = 0;
-}
 
 // per-step statistics into the running totals: both records are read whole first (their
 // fields are independent loads) and the sums written back, instead of one dependent
@@ -877,7 +871,6 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   int rc = LM_OK;
   ctx->pdl_now = ctx->pdl < 0 ? n == 1 : ctx->pdl == 1;
   if ((rc = mark())) return rc;
-  CU(launch_k(ctx, k_begin, dim3(n), dim3(128), 0, 0, dmaps, dv));
   CU(launch_k(ctx, k_insert, dim3(n), dim3(256), 0, 0, dmaps, dv));
   if ((rc = mark())) return rc;
   {
@@ -928,7 +921,7 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   CU(launch_k(ctx, k_fuse_visible, dim3((kpkf + 255) / 256, tfuse, n), dim3(256), 0, 0, dmaps, dv));
   CU(launch_k(ctx, k_end, dim3(n), dim3(32), 0, 0, dmaps, dv, ctx->d_totals));
   if ((rc = mark())) return rc;
-  ctx->launches += 19;
+  ctx->launches += 18;
   if (ctx->prof) ctx->prof_steps.push_back(evs);
   CHECK_LAUNCH();
   CU(cudaEventRecord(ctx->args_ev[e], ctx->stream));

@@ -148,6 +148,11 @@ __global__ void __launch_bounds__(256) k_insert(DevMap* maps, const StepArgs* ar
   pdl_enter();
   const StepArgs& A = args[blockIdx.x];
   const DevMap& M = maps[A.map];
+  {  // the step's statistics record starts from zero
+    int* p = (int*)M.s.stats;
+    for (int k = threadIdx.x; k < (int)(sizeof(lm_step_stats) / 4); k += blockDim.x) p[k] = 0;
+    __syncthreads();
+  }
   if (!A.do_insert) return;
   const int slot = A.cur;
   const int off = M.kp_off[slot], n = M.kp_n[slot];
