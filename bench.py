@@ -123,50 +123,47 @@ def ncu_traffic(kernel: str):
         return None
 
 
-def cpu_sample(seq, name, budget_s: float):
-    """Oracle (NumPy port of the reference path) on the host: keyframes 0.. until budget."""
-    from oracle import lm_oracle as O
-
-    n, mc, fc = stage_params(name)
-    c = seq.config
-    cam = O.Cam(c.fx, c.fy, c.cx, c.cy, c.width, c.height, c.num_levels, c.scale_factor)
-    pipe = O.OraclePipeline(c.num_levels, n, fc=O.FuseCfg(n1=fc.n1, n2=fc.n2))
-    t0 = time.perf_counter()
-    done = 0
-    for rec in seq.records:
-        pipe.step(O.okf_from_record(rec, cam))
-        done += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
-    return done, dt
-
-
 def run_reference(args):
+    """--impl reference: the real reference (baseline/_ref) on this host's cores, every step one
+    steady-state keyframe of C2 (KFs 100.. resumed from the reference's own state) through its
+    stock LocalMappingPipeline in mode="optimized" (engine="batch", WorkerPool(all host
+    threads)); value = keyframes / (triangulation_ms + fusion_ms). Falls back to the NumPy port
+    (labelled) when the reference or its pickled state is absent."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    seq = load_workload(args.workload, None)
-    sample_kfs = args.ref_kfs
-    from oracle import lm_oracle as O  # noqa: F401
+    import bench_ref
 
-    times = []
-    for step in range(args.warmup + args.steps):
-        seq_k = seq
-        t0 = time.perf_counter()
-        done, dt = cpu_sample(seq_k, args.workload, budget_s=1e9 if sample_kfs else args.ref_budget)
-        times.append((done, dt))
-    timed = times[args.warmup:]
-    kfs = sum(d for d, _ in timed)
-    secs = sum(t for _, t in timed)
-    v = kfs / secs
-    sample = f"oracle port, keyframes 0..{timed[0][0] - 1} of {args.workload} from an empty map per step"
+    name = "c2" if args.workload == "c5" else args.workload
+    if bench_ref.reference_available():
+        w = bench_ref.ReferenceWindow(name, "optimized", start=args.ref_start)
+        ms = []
+        try:
+            for _ in range(args.warmup + args.steps):
+                if w.next >= len(w.kfs):
+                    break
+                tri, fus = w.step()
+                ms.append(tri + fus)
+        finally:
+            w.close()
+        timed = ms[args.warmup:] or ms
+        secs = sum(timed) * 1e-3
+        v = len(timed) / secs
+        first = w.next - len(timed)
+        sample = (f"real reference (baseline/_ref) {name} keyframe{'s' if len(timed) > 1 else ''} {first}-{w.next - 1}, "
+                  + (f"resumed from its own state after {w.start} keyframes" if w.resumed else "from an empty map")
+                  + f"; one keyframe per step; StageTimings.triangulation_ms + fusion_ms; mode=optimized "
+                    f"(engine=batch, {w.workers} threads) on {bench_ref.cpu_model()}")
+        cores, kind, ms_step = w.workers, "reference", 1e3 * secs / len(timed)
+    else:
+        seq = load_workload(name, None)
+        rec = bench_ref.time_port(seq, name, args.ref_budget)
+        v, cores, kind, sample, ms_step = rec["value"], 1, "port", rec["sample"], 1e3 / rec["value"]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / len(timed),
-            "ms_per_keyframe": 1e3 * secs / kfs, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u32 popc / f64 geometry", "data": "synthetic",
-            "config": config_of(args), "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
-                                                       "sample": sample},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_keyframe": 1e3 / v,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 popc / f64 geometry",
+            "data": "synthetic", "config": config_of(args),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -198,10 +195,12 @@ def main():
     ap.add_argument("--sessions", type=int, default=64, help="c5: total sessions over all ranks")
     ap.add_argument("--c5-groups", type=int, default=8, help="c5: session groups per rank (one stream each)")
     ap.add_argument("--kfs", type=int, default=None, help="limit keyframes per step (debug)")
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--ref-budget", type=float, default=8.0)
-    ap.add_argument("--ref-kfs", type=int, default=0)
+    ap.add_argument("--cpu-budget", type=float, default=24.0, help="cpu_baseline: seconds of reference stage time")
+    ap.add_argument("--ref-budget", type=float, default=8.0, help="port fallback budget (s)")
+    ap.add_argument("--ref-start", type=int, default=100, help="reference steady-state window start (keyframe)")
+    ap.add_argument("--window", type=int, default=20, help="device steady-state window length (keyframes)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=1, help="separate per-stage profiling pass")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -274,19 +273,8 @@ def main():
         ctx.call("lm_timer_stop", C.byref(ms))
         return ms.value
 
-    # -------- device-resident timed region (per-stage CUDA events on the library stream)
-    for _ in range(args.warmup):
-        one_step(False)
-    lib.lm_profile_enable(ctx.h, 1)
-    lib.lm_profile_read(ctx.h, (C.c_double * 16)(), (C.c_int64 * 16)())  # drop warm-up events
-    sampler = ClockSampler(local)
-    launches0 = lib.lm_launch_count(ctx.h)
-    step_ms = []
-    acc = {}
-    totals = _lib.StepStats()
-    for _ in range(args.steps):
-        ms = one_step(True)
-        step_ms.append(max_over_ranks(ms))
+    def absorb_totals(acc):
+        totals = _lib.StepStats()
         ctx.call("lm_totals_fetch", mapper.map, C.byref(totals))  # this step's totals (rewind clears)
         if totals.error:
             raise RuntimeError(f"device error {totals.error}")
@@ -294,21 +282,67 @@ def main():
             v = getattr(totals, f)
             if isinstance(v, int):
                 acc[f] = acc.get(f, 0) + v
-            elif f in ("fuse_cycles", "dbg"):
+            elif f in ("fuse_cycles", "dbg", "borderline"):
                 acc[f] = [a + b for a, b in zip(acc.get(f, [0] * len(v)), list(v))]
+
+    # -------- device-resident timed region: the bare launch sequence (no profiling events)
+    for _ in range(args.warmup):
+        one_step(False)
+    sampler = ClockSampler(local)
+    launches0 = lib.lm_launch_count(ctx.h)
+    step_ms = []
+    acc = {}
+    for _ in range(args.steps):
+        ms = one_step(False)
+        step_ms.append(max_over_ranks(ms))
+        absorb_totals(acc)
     launches = lib.lm_launch_count(ctx.h) - launches0
     clocks = sampler.stop()
+    mean_ms = sum(step_ms) / len(step_ms)
+    total_kf = len(ids) * world
+    value = total_kf / (mean_ms * 1e-3)
+
+    # -------- profile pass (separate, untimed for `value`): per-stage CUDA events between the
+    # step's kernels on the library stream, for the rooflines and the stage breakdown
+    prof_steps = max(1, args.profile_steps)
+    lib.lm_profile_enable(ctx.h, 1)
+    lib.lm_profile_read(ctx.h, (C.c_double * 16)(), (C.c_int64 * 16)())
+    prof_acc = {}
+    prof_total = 0.0
+    for _ in range(prof_steps):
+        prof_total += one_step(True)
+        absorb_totals(prof_acc)
     prof_ms = (C.c_double * 16)()
     prof_n = (C.c_int64 * 16)()
     lib.lm_profile_read(ctx.h, prof_ms, prof_n)
     lib.lm_profile_enable(ctx.h, 0)
     stages = ["insert", "cull", "select", "prep", "match", "tri", "commit", "fuse_targets", "fuse_geo",
               "fuse_gather", "fuse_apply", "fuse_refresh", "fuse_spec", "fuse_rev", "fuse_visible"]
-    stage_ms = {s: prof_ms[k] / args.steps for k, s in enumerate(stages)}
+    stage_ms = {s: prof_ms[k] / prof_steps for k, s in enumerate(stages)}
     stage_ms["fuse"] = sum(stage_ms[s] for s in stages if s.startswith("fuse"))
-    mean_ms = sum(step_ms) / len(step_ms)
-    total_kf = len(ids) * world
-    value = total_kf / (mean_ms * 1e-3)
+    profiled_step_ms = prof_total / prof_steps
+
+    # -------- steady-state window on the device (the keyframes the CPU reference is timed on):
+    # replay keyframes 0..lo-1 untimed, then time lo..hi-1 with CUDA events
+    lo = min(args.ref_start, max(0, len(ids) - 1))
+    hi = min(len(ids), lo + args.window)
+    win_ms = []
+    for _ in range(3):
+        ctx.call("lm_map_rewind", mapper.map)
+        mapper.processed = 0
+        for k in ids[:lo]:
+            mapper.step(k, sync=False)
+        lib.lm_flush_l2(ctx.h, L2_FLUSH_BYTES)
+        ctx.call("lm_synchronize")
+        ctx.call("lm_timer_start")
+        for k in ids[lo:hi]:
+            mapper.step(k, sync=False)
+        ms = C.c_float()
+        ctx.call("lm_timer_stop", C.byref(ms))
+        win_ms.append(ms.value)
+    window = {"keyframes": [lo, hi - 1], "ms_per_keyframe": sum(win_ms) / len(win_ms) / (hi - lo),
+              "keyframes_per_s": (hi - lo) / (sum(win_ms) / len(win_ms) * 1e-3),
+              "timing": "CUDA events around keyframes lo..hi-1 after an untimed replay of 0..lo-1 (L2 flushed)"}
 
     # -------- end-to-end through the C ABI with host buffers
     e2e = None
@@ -451,15 +485,51 @@ def main():
                                                               "fwd_apply_commit_merges", "fwd_apply_compaction"])
                                        if n != "-"},
             "rev_recomputed_points_per_step": acc["fuse_cycles"][1] / args.steps}
+    line["profiled_ms_per_step"] = profiled_step_ms
+    line["device_window"] = window
+    bl = [x / args.steps for x in acc.get("borderline", [0, 0, 0, 0])]
+    line["borderline"] = {"per_step": {"epipolar": bl[0], "creation_gates": bl[1], "fusion_gates": bl[2],
+                                       "level_rint_ties": bl[3]}, "total_per_step": sum(bl),
+                          "rel_band": 1e-10,
+                          "meaning": "threshold compares whose two sides are within 1e-10 relative (lm_math.cuh "
+                                     "kFlipRel): an upper bound of decisions that could flip against the reference"}
+    line["parity"] = golden_parity(args, seed, mapper, ids)
     if rank == 0 and world == 1 and not args.no_cpu:
-        done, dt = cpu_sample(seq, args.workload, args.cpu_budget)
-        line["cpu_baseline"] = {"value": done / dt, "unit": UNIT, "cores": 1, "kind": "port",
-                                "sample": f"oracle (NumPy port) keyframes 0..{done - 1} of the same sequence, "
-                                          f"from an empty map, {dt:.1f} s"}
+        import bench_ref
+
+        name = "c2" if args.workload == "c5" else args.workload
+        if bench_ref.reference_available():
+            cb = bench_ref.time_reference(name, budget_s=args.cpu_budget, start=args.ref_start)
+            cb["device_same_window_kf_per_s"] = window["keyframes_per_s"] if cb["window"][0] == lo else None
+        else:
+            cb = bench_ref.time_port(seq, name, args.cpu_budget)
+        line["cpu_baseline"] = cb
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def golden_parity(args, seed, mapper, ids):
+    """Final structural digest of the timed sequence against the REAL reference's frozen
+    per-keyframe digest (tests/golden/steady_<workload>.json, make_golden_steady.py). Equality
+    after the last keyframe means no decision anywhere in the sequence flipped."""
+    path = os.path.join(ROOT, "tests", "golden", f"steady_{args.workload}.json")
+    try:
+        g = json.load(open(path))
+    except (OSError, ValueError):
+        return {"checked": False, "why": "no golden for this workload"}
+    n_kf = len(ids)
+    if g["config"].get("seed") != seed or n_kf > len(g["steps"]):
+        return {"checked": False, "why": "sequence differs from the golden's (seed / length)"}
+    want = g["steps"][n_kf - 1]
+    mapper.ctx.call("lm_map_rewind", mapper.map)  # replay the whole sequence once more
+    mapper.processed = 0
+    for k in ids:
+        mapper.step(k, sync=False)
+    got = mapper.snapshot(with_covis=False).structural_digest()
+    return {"checked": True, "keyframes": n_kf, "final_digest_equal_reference": got == want["digest"],
+            "golden": os.path.relpath(path, ROOT)}
 
 
 def run_c5(args, rank, world, local, dist):

@@ -96,6 +96,7 @@ typedef struct lm_step_params {
 } lm_step_params;
 
 #define LM_MAX_NEIGHBORS 64
+#define LM_MAX_KF_SLOTS 8192 /* lm_map_caps.max_keyframes upper bound (shared-memory slot tables) */
 #define LM_MAX_TARGETS 320
 
 typedef struct lm_step_stats { /* CreationStats triangulation.py:49-60 + run_fusion counts */
@@ -124,6 +125,12 @@ typedef struct lm_step_stats { /* CreationStats triangulation.py:49-60 + run_fus
   int64_t fuse_bytes_rev;     /* algorithmic bytes of the reverse passes (part of fuse_bytes) */
   int64_t rev_mergeable;      /* acting passes none of whose (or earlier) items the previous apply touched */
   int64_t dbg[16];            /* diagnostic counters (meaning documented in bench.py) */
+  /* borderline float compares (sides within 1e-10 relative, lm_math.cuh kFlipRel): the
+   * decisions that could differ from the reference's (LAPACK SVD / NumPy log inputs).
+   * [0] epipolar d^2 <= thr (k_match survivors), [1] triangulation degeneracy + creation
+   * gates, [2] fusion projection / band / view-cos / radius gates (forward gather and the
+   * speculative reverse evaluation), [3] rint ties of the fusion level prediction. */
+  int64_t borderline[4];
 } lm_step_stats;
 
 typedef struct lm_candidate { /* MatchCandidate triangulation.py:41-46 */
@@ -201,8 +208,11 @@ int lm_kf_kill(lm_ctx* ctx, int32_t map, int64_t kf_id); /* MapModel.kill_keyfra
 
 /* ---- the hot path ---- */
 int lm_step(lm_ctx* ctx, int32_t map, int64_t kf_id, const lm_step_params* p, lm_step_stats* out);
-/* Enqueue one step for each (map, keyframe) pair in one batched launch sequence. If out is
- * NULL the call does not synchronise (stats stay on the device until lm_step_stats_fetch). */
+/* Enqueue one step for each (map, keyframe) pair in one batched launch sequence. p points to
+ * n lm_step_params, one per entry (each session keeps its own processed_index and stage
+ * configs); a map may appear only once per batch. If out is NULL the call does not
+ * synchronise (stats stay on the device until lm_step_stats_fetch, which also reports a
+ * device-side error of the last step). */
 int lm_step_batch(lm_ctx* ctx, int32_t n, const int32_t* maps, const int64_t* kf_ids, const lm_step_params* p,
                   lm_step_stats* out);
 int lm_step_stats_fetch(lm_ctx* ctx, int32_t n, const int32_t* maps, lm_step_stats* out);
@@ -231,6 +241,95 @@ int lm_mp_set_counts(lm_ctx* ctx, int32_t map, int64_t mp, int32_t found, int32_
 int lm_covisible_neighbors(lm_ctx* ctx, int32_t map, int64_t kf, int32_t n, int64_t* out, int32_t cap,
                            int32_t* n_out);
 int lm_ledger(lm_ctx* ctx, int32_t map, lm_ledger_t* out);
+/* explicit DeviceStore.record_neighbor_access / record_small_transfer (devicestore.py:80-101):
+ * naive += naive_bytes; with small_events = 1 one small transfer of small_bytes (stage
+ * "triangulation" if small_stage_triangulation, else "fusion") in both counters */
+int lm_ledger_add(lm_ctx* ctx, int32_t map, int64_t naive_bytes, int32_t small_stage_triangulation,
+                  int64_t small_bytes, int32_t small_events);
+/* TransferLedger.per_stage_small_transfers: bytes of events first.. (at most cap), in order;
+ * a negative entry b is a "triangulation" event of -b-1 bytes, others are "fusion" (the
+ * stages log theirs: one forward pass + one per reverse pass). The first 65536 events of a
+ * map are kept (the totals in lm_ledger are always exact). */
+int lm_ledger_log(lm_ctx* ctx, int32_t map, int64_t first, int64_t* bytes, int32_t cap, int32_t* n_out);
+
+/* ---- DeviceStore residency (devicestore.py:51-109) ----
+ * lm_kf_insert is MapModel.insert_keyframe only; lm_kf_upload is DeviceStore.upload_keyframe
+ * (residency + persistent ledger bytes; errors: already resident -> INVALID_STATE, capacity
+ * -> CAPACITY). lm_step on a staged keyframe does both. A stage whose neighbours / fusion
+ * targets include a non-resident keyframe fails with INVALID_STATE before touching the map
+ * (record_neighbor_access devicestore.py:80-92). lm_kf_evict: evict_keyframe (not resident
+ * -> INVALID_ARGUMENT). */
+int lm_kf_upload(lm_ctx* ctx, int32_t map, int64_t kf_id);
+int lm_kf_evict(lm_ctx* ctx, int32_t map, int64_t kf_id);
+int lm_kf_resident(lm_ctx* ctx, int32_t map, int64_t kf_id, int32_t* resident, int32_t* count);
+
+/* ---- LBA write-back (localba.py:571-574 writes kf.pose and mp.position) ----
+ * Poses and positions changed outside the hot path: the keyframe's R, t, C, P tables are
+ * recomputed (same host code as staging) and the cached view geometry / hits of every
+ * affected point invalidated, so the next stages see exactly the new values. */
+int lm_kf_set_pose(lm_ctx* ctx, int32_t map, int64_t kf_id, const double quat[4], const double trans[3]);
+int lm_mp_patch_positions(lm_ctx* ctx, int32_t map, int32_t n, const int64_t* ids, const double* pos);
+
+/* ---- O(touched) reads for the MapModel facade ---- */
+typedef struct lm_point_record { /* MapPoint mapmodel.py:65-77 */
+  double pos[3];
+  uint8_t rep[32];
+  int64_t first_kf_id;
+  int32_t alive, found, visible, nobs;
+  int32_t counts[16]; /* scale_counts, num_levels used */
+} lm_point_record;
+/* one point (its representative descriptor refreshed if stale) + observations sorted by kf id */
+int lm_mp_get(lm_ctx* ctx, int32_t map, int64_t mp, lm_point_record* out, int64_t* obs_kf, int32_t* obs_kp,
+              int32_t obs_cap);
+int lm_kf_bindings(lm_ctx* ctx, int32_t map, int64_t kf_id, int64_t* out, int32_t cap, int32_t* n_out);
+int lm_bound_points(lm_ctx* ctx, int32_t map, int64_t kf_id, int64_t* out, int32_t cap, int32_t* n_out);
+/* nonzero covisibility entries of one keyframe (any order): CovisibilityGraph adjacency */
+int lm_covis_row(lm_ctx* ctx, int32_t map, int64_t kf_id, int64_t* kf_ids, int32_t* weights, int32_t cap,
+                 int32_t* n_out);
+
+/* ---- snapshot import (per-step parity from a reference state; SURVEY.md 5 checkpoint row) ----
+ * Keyframes in insertion (kf id) order; keypoint arrays concatenated (kp_n per keyframe).
+ * Dead keyframes carry no bindings. Points are ids 0..n_points-1 (dead ones included).
+ * The map must be empty (fresh or lm_map_reset). */
+typedef struct lm_snapshot {
+  int32_t n_kf;
+  const int64_t* kf_id;
+  const uint8_t* kf_alive;
+  const uint8_t* kf_resident; /* may be NULL: none resident */
+  const double* quat;         /* 4 per keyframe (x, y, z, w) */
+  const double* trans;        /* 3 per keyframe */
+  const double* cam;          /* 6 per keyframe: fx, fy, cx, cy, width, height */
+  const int32_t* kp_n;
+  const double* u;
+  const double* v;
+  const int64_t* level;
+  const uint8_t* desc;     /* 32 per keypoint */
+  const int64_t* bindings; /* -1 = unbound */
+  int32_t n_points;
+  const double* pos;       /* 3 per point */
+  const uint8_t* rep;      /* 32 per point */
+  const uint8_t* alive;
+  const int32_t* found;
+  const int32_t* visible;
+  const int64_t* first_kf; /* may be NULL */
+  int32_t n_recent;        /* probation list (culling.RecentPoint) */
+  const int64_t* recent_id;
+  const int32_t* recent_born;
+  lm_ledger_t ledger;
+} lm_snapshot;
+int lm_import_snapshot(lm_ctx* ctx, int32_t map, const lm_snapshot* snapshot);
+
+/* ---- device audit (MapModel.audit mapmodel.py:304-353) ----
+ * codes: 1 dead point keeps observations (mp); 2 point observes a dead keyframe (mp, kf_a);
+ * 3 binding mismatch (mp, kf_a, kp); 4 scale_counts mismatch (mp); 5 scale_counts sum
+ * mismatch (mp); 6 slot bound to a dead point (kf_a, kp, mp); 7 slot not in the point's
+ * observations (kf_a, kp, mp); 8 covisibility weight mismatch (kf_a, kf_b). Order unspecified;
+ * *n_out = total found (records beyond cap are dropped). */
+typedef struct lm_audit_record {
+  int32_t code, kp;
+  int64_t mp, kf_a, kf_b;
+} lm_audit_record;
+int lm_audit(lm_ctx* ctx, int32_t map, lm_audit_record* out, int32_t cap, int32_t* n_out);
 
 /* ---- state export (parity, snapshots) ---- */
 /* keyframe table: per slot kf_id, state (1 staged, 2 live, 3 dead), kp_off, kp_n */

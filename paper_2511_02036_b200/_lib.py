@@ -71,7 +71,8 @@ class StepStats(C.Structure):
                 ("first_new_id", i64), ("error", i32), ("n_candidates", i32), ("match_pairs", i64),
                 ("fuse_bytes", i64), ("fuse_passes", i64), ("fuse_points", i64), ("fuse_actions", i64),
                 ("apply_rounds", i64), ("fuse_cycles", i64 * 16),
-                ("rev_passes_acting", i64), ("rev_passes_redo", i64), ("fuse_bytes_rev", i64), ("rev_mergeable", i64), ("dbg", i64 * 16)]
+                ("rev_passes_acting", i64), ("rev_passes_redo", i64), ("fuse_bytes_rev", i64), ("rev_mergeable", i64), ("dbg", i64 * 16),
+                ("borderline", i64 * 4)]
 
 
 class Candidate(C.Structure):
@@ -87,6 +88,23 @@ class FuseActionC(C.Structure):
 class Ledger(C.Structure):
     _fields_ = [("persistent_bytes_up", i64), ("naive_bytes_up", i64), ("small_bytes_triangulation", i64),
                 ("small_bytes_fusion", i64), ("small_transfer_events", i64), ("evictions", i64)]
+
+
+class PointRecord(C.Structure):
+    _fields_ = [("pos", f64 * 3), ("rep", u8 * 32), ("first_kf_id", i64), ("alive", i32), ("found", i32),
+                ("visible", i32), ("nobs", i32), ("counts", i32 * 16)]
+
+
+class Snapshot(C.Structure):
+    _fields_ = [("n_kf", i32), ("kf_id", P(i64)), ("kf_alive", P(u8)), ("kf_resident", P(u8)), ("quat", P(f64)),
+                ("trans", P(f64)), ("cam", P(f64)), ("kp_n", P(i32)), ("u", P(f64)), ("v", P(f64)),
+                ("level", P(i64)), ("desc", P(u8)), ("bindings", P(i64)), ("n_points", i32), ("pos", P(f64)),
+                ("rep", P(u8)), ("alive", P(u8)), ("found", P(i32)), ("visible", P(i32)), ("first_kf", P(i64)),
+                ("n_recent", i32), ("recent_id", P(i64)), ("recent_born", P(i32)), ("ledger", Ledger)]
+
+
+class AuditRecord(C.Structure):
+    _fields_ = [("code", i32), ("kp", i32), ("mp", i64), ("kf_a", i64), ("kf_b", i64)]
 
 
 class MapSizes(C.Structure):
@@ -126,6 +144,19 @@ _SIGS = {
     "lm_mp_set_counts": ([C.c_void_p, i32, i64, i32, i32], i32),
     "lm_covisible_neighbors": ([C.c_void_p, i32, i64, i32, P(i64), i32, P(i32)], i32),
     "lm_ledger": ([C.c_void_p, i32, P(Ledger)], i32),
+    "lm_ledger_log": ([C.c_void_p, i32, i64, P(i64), i32, P(i32)], i32),
+    "lm_ledger_add": ([C.c_void_p, i32, i64, i32, i64, i32], i32),
+    "lm_audit": ([C.c_void_p, i32, P(AuditRecord), i32, P(i32)], i32),
+    "lm_kf_upload": ([C.c_void_p, i32, i64], i32),
+    "lm_kf_evict": ([C.c_void_p, i32, i64], i32),
+    "lm_kf_resident": ([C.c_void_p, i32, i64, P(i32), P(i32)], i32),
+    "lm_kf_set_pose": ([C.c_void_p, i32, i64, P(f64), P(f64)], i32),
+    "lm_mp_patch_positions": ([C.c_void_p, i32, i32, P(i64), P(f64)], i32),
+    "lm_mp_get": ([C.c_void_p, i32, i64, P(PointRecord), P(i64), P(i32), i32], i32),
+    "lm_kf_bindings": ([C.c_void_p, i32, i64, P(i64), i32, P(i32)], i32),
+    "lm_bound_points": ([C.c_void_p, i32, i64, P(i64), i32, P(i32)], i32),
+    "lm_covis_row": ([C.c_void_p, i32, i64, P(i64), P(i32), i32, P(i32)], i32),
+    "lm_import_snapshot": ([C.c_void_p, i32, P(Snapshot)], i32),
     "lm_export_keyframes": ([C.c_void_p, i32, P(i64), P(i32), P(i32), P(i32), i32, P(i32)], i32),
     "lm_export_bindings": ([C.c_void_p, i32, P(i32), i32], i32),
     "lm_export_points": ([C.c_void_p, i32, i32, P(f64), P(u8), P(u8), P(i32), P(i32), P(i32), P(i32), P(i64),

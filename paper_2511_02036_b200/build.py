@@ -14,7 +14,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "lm_b200.cu")
-DEPS = [os.path.join(HERE, "csrc", f) for f in ("lm_b200.cu", "lm_kernels.cuh", "lm_map.cuh", "lm_math.cuh")] + [
+DEPS = [os.path.join(HERE, "csrc", f) for f in ("lm_b200.cu", "lm_kernels.cuh", "lm_map.cuh", "lm_math.cuh",
+                                                          "lm_audit.cuh")] + [
     os.path.join(ROOT, "include", "lm_b200.h")]
 LIB = os.path.join(HERE, "liblm_b200.so")
 

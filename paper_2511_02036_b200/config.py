@@ -55,7 +55,7 @@ class StoreConfig:
     map_point_record_bytes: int = 100
     capacity: int = 4096
     # device arenas (this package only)
-    max_keyframes: int = 1024
+    max_keyframes: int = 4096  # = capacity; <= LM_MAX_KF_SLOTS (8192)
     max_keypoints: int = 1 << 21
     max_points: int = 1 << 20
     obs_pool_entries: int = 1 << 24

@@ -10,11 +10,13 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <cmath>
 #include <string>
 #include <unordered_map>
 #include <vector>
 
 #include "lm_kernels.cuh"
+#include "lm_audit.cuh"
 
 using namespace lm;
 
@@ -36,6 +38,7 @@ struct HostMap {
   lm_map_caps caps{};
   std::unordered_map<long long, int> slot_of;
   std::vector<int> state;  // host mirror of kf_state
+  std::vector<char> res;   // host mirror of kf_res (DeviceStore residency)
   std::vector<int> kp_n, kp_off;
   std::vector<long long> ids;
   int n_slots = 0, kp_head = 0, resident = 0;
@@ -43,6 +46,8 @@ struct HostMap {
   lm_step_stats* d_stats = nullptr;
   lm_step_stats* d_totals = nullptr;
   int* d_result = nullptr;  // single-op results
+  void* d_io = nullptr;     // single-op input/output scratch (grown on demand)
+  size_t io_bytes = 0;
 };
 
 }  // namespace
@@ -218,7 +223,17 @@ __global__ void __launch_bounds__(1024) k_stage(DevMap M, const unsigned char* b
 
 // ------------------------------------------------------------------- single-op map kernel
 enum MapOp { OP_NEW = 1, OP_OBS_ADD, OP_OBS_ERASE, OP_KILL, OP_REPLACE, OP_SET_COUNTS, OP_KF_KILL, OP_NEIGHBORS,
-             OP_REFRESH, OP_APPLY, OP_TARGETS, OP_FUSE_PASS, OP_CULL };
+             OP_REFRESH, OP_APPLY, OP_TARGETS, OP_FUSE_PASS, OP_CULL, OP_SET_POSE, OP_PATCH_POS, OP_UPLOAD, OP_EVICT,
+             OP_MP_GET, OP_BOUND, OP_IMPORT_POINTS, OP_LEDGER_ADD };
+
+// packed single-point record of OP_MP_GET (lm_mp_get), followed by nobs int2 (slot, kp)
+struct PointRec {
+  double pos[3];
+  uint4 rep[2];
+  long long first_kf;
+  int alive, found, visible, nobs;
+  int counts[LMAX];
+};
 
 struct OpArgs {
   int op;
@@ -232,6 +247,9 @@ struct OpArgs {
   lm_cull_cfg cc;
   int processed;
   int n_slots;
+  double pose[4 + 9 + 3 + 3 + 12];  // OP_SET_POSE: q, R, t, C, P
+  void* buf;                        // OP_PATCH_POS / OP_MP_GET / OP_BOUND / OP_IMPORT_POINTS: io scratch
+  long long v0, v1;                 // OP_LEDGER_ADD: naive bytes, small-transfer bytes
 };
 
 __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, int* res) {
@@ -403,6 +421,130 @@ __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, in
       }
       return;
     }
+    case OP_SET_POSE: {  // LBA pose write-back (localba.py:571-574): tables + geometry caches
+      const int slot = A.a;
+      if (tid == 0) {
+        for (int k = 0; k < 4; ++k) M.q[4 * slot + k] = A.pose[k];
+        for (int k = 0; k < 9; ++k) M.R[9 * slot + k] = A.pose[4 + k];
+        for (int k = 0; k < 3; ++k) M.t[3 * slot + k] = A.pose[13 + k];
+        for (int k = 0; k < 3; ++k) M.C[3 * slot + k] = A.pose[16 + k];
+        for (int k = 0; k < 12; ++k) M.P[12 * slot + k] = A.pose[19 + k];
+      }
+      // every point observed here has a ray from this camera centre in its cached
+      // _point_geometry sums (fusion.py:57-94) and a cached hit: both stale now. A point
+      // observes a keyframe at most once, so each is touched by one thread.
+      const int off = M.kp_off[slot], n = M.kp_n[slot];
+      for (int i = tid; i < n; i += 1024) {
+        const int mp = M.kbind[off + i];
+        if (mp >= 0) {
+          M.gval[mp] = 0;
+          M.ver[mp] += 1;
+        }
+      }
+      if (tid == 0) res[0] = LM_OK;
+      return;
+    }
+    case OP_PATCH_POS: {  // LBA position write-back: buf = n x (int id, pad, double xyz)
+      const int n = A.n;
+      const char* b = (const char*)A.buf;
+      for (int k = tid; k < n; k += 1024) {
+        const int mp = *(const int*)(b + 32 * (size_t)k);
+        const double* x = (const double*)(b + 32 * (size_t)k + 8);
+        M.pos[3 * mp] = x[0];
+        M.pos[3 * mp + 1] = x[1];
+        M.pos[3 * mp + 2] = x[2];
+        M.gval[mp] = 0;
+        M.ver[mp] += 1;
+      }
+      if (tid == 0) res[0] = LM_OK;
+      return;
+    }
+    case OP_UPLOAD: {  // DeviceStore.upload_keyframe devicestore.py:68-78
+      if (tid) return;
+      M.kf_res[A.a] = 1;
+      M.ledger[LG_PERSIST] += (unsigned long long)payload_bytes(M, A.a);
+      res[0] = LM_OK;
+      return;
+    }
+    case OP_EVICT: {  // DeviceStore.evict_keyframe devicestore.py:103-109
+      if (tid) return;
+      M.kf_res[A.a] = 0;
+      M.ledger[LG_EVICT] += 1;
+      res[0] = LM_OK;
+      return;
+    }
+    case OP_MP_GET: {  // one point's record (refreshing a stale representative descriptor)
+      const int mp = A.a;
+      if (tid < 32 && M.dirty[mp] && M.alive[mp]) refresh_rep_warp(M, mp, tid);
+      __syncthreads();
+      PointRec* r = (PointRec*)A.buf;
+      int2* o = (int2*)(r + 1);
+      const int n = M.nobs[mp];
+      for (int k = tid; k < n; k += 1024) o[k] = M.obs[M.ooff[mp] + k];
+      if (tid == 0) {
+        if (M.dirty[mp] && M.alive[mp]) M.dirty[mp] = 0;  // the dirty list keeps the id; refresh_all skips clean ones
+        for (int k = 0; k < 3; ++k) r->pos[k] = M.pos[3 * mp + k];
+        r->rep[0] = M.rep[2 * mp];
+        r->rep[1] = M.rep[2 * mp + 1];
+        r->first_kf = M.first_kf[mp];
+        r->alive = M.alive[mp];
+        r->found = M.found[mp];
+        r->visible = M.visible[mp];
+        r->nobs = n;
+        for (int l = 0; l < LMAX; ++l) r->counts[l] = l < M.L ? M.counts[(size_t)mp * M.L + l] : 0;
+        res[0] = LM_OK;
+      }
+      return;
+    }
+    case OP_BOUND: {  // bound_points_of mapmodel.py:291-300: live bound ids in keypoint order
+      const int P = bound_points<1024>(M, A.a, sh);
+      int* out = (int*)A.buf;
+      for (int k = tid; k < P; k += 1024) out[k] = M.s.pts[k];
+      if (tid == 0) {
+        res[0] = LM_OK;
+        res[1] = P;
+      }
+      return;
+    }
+    case OP_IMPORT_POINTS: {  // lm_import_snapshot: points 0..n-1, no observations yet
+      const int n = A.n;
+      const char* b = (const char*)A.buf;  // n x (pos 24, rep 32, found 4, visible 4, alive 1, pad 7, first kf 8)
+      for (int id = tid; id < n; id += 1024) {
+        const char* e = b + 80 * (size_t)id;
+        const double* x = (const double*)e;
+        for (int k = 0; k < 3; ++k) M.pos[3 * id + k] = x[k];
+        M.rep[2 * id] = *(const uint4*)(e + 24);
+        M.rep[2 * id + 1] = *(const uint4*)(e + 40);
+        M.found[id] = *(const int*)(e + 56);
+        M.visible[id] = *(const int*)(e + 60);
+        M.alive[id] = *(const unsigned char*)(e + 64);
+        M.first_kf[id] = *(const long long*)(e + 72);
+        M.nobs[id] = 0;
+        M.ocap[id] = 0;
+        M.ooff[id] = 0;
+        M.gval[id] = 0;
+        M.dirty[id] = 0;
+      }
+      if (tid == 0) {
+        M.scal[SC_NEXT_ID] = n;
+        res[0] = LM_OK;
+      }
+      return;
+    }
+    case OP_LEDGER_ADD: {  // explicit record_neighbor_access / record_small_transfer (devicestore.py:80-101)
+      if (tid) return;
+      M.ledger[LG_NAIVE] += (unsigned long long)A.v0;
+      if (A.n) {  // one small-transfer event of A.v1 bytes (stage: A.b = 1 triangulation, else fusion)
+        const unsigned long long ev = M.ledger[LG_SMALL_EVENTS];
+        if (ev < (unsigned long long)LG_LOG_CAP) M.lg_log[ev] = A.b ? -(long long)A.v1 - 1 : A.v1;
+        M.ledger[LG_SMALL_EVENTS] = ev + 1;
+        M.ledger[A.b ? LG_SMALL_TRI : LG_SMALL_FUSE] += (unsigned long long)A.v1;
+        M.ledger[LG_NAIVE] += (unsigned long long)A.v1;
+        M.ledger[LG_PERSIST] += (unsigned long long)A.v1;
+      }
+      res[0] = LM_OK;
+      return;
+    }
     default:
       if (tid == 0) res[0] = LM_ERR_INVALID_ARGUMENT;
   }
@@ -461,6 +603,8 @@ static cudaError_t launch_k(lm_ctx* ctx, void (*k)(KArgs...), dim3 g, dim3 b, si
 }
 
 extern "C" {
+
+static int refresh(lm_ctx* ctx, HostMap* m, int map);
 
 int lm_version(void) { return 1; }
 
@@ -556,6 +700,11 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
       c->max_keypoints_per_kf < 1 || c->max_keypoints < c->max_keypoints_per_kf || c->max_points < 1 ||
       c->obs_pool_entries < 8)
     return fail(ctx, LM_ERR_INVALID_ARGUMENT, "invalid map capacities");
+  // k_select / k_fuse_targets / k_op stage 12 bytes per keyframe slot in shared memory and
+  // the pair-reservation hash packs slot ids into 16 bits
+  if (c->max_keyframes > LM_MAX_KF_SLOTS)
+    return fail(ctx, LM_ERR_CAPACITY, "max_keyframes %d exceeds the device limit %d", c->max_keyframes,
+                LM_MAX_KF_SLOTS);
   CU(cudaSetDevice(ctx->device));
   HostMap* m = new HostMap();
   m->caps = *c;
@@ -582,7 +731,7 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   int rc = LM_OK;
 #define A(ptr, n) \
   if ((rc = arena(ctx, m, &(ptr), (n))) != LM_OK) return rc
-  A(d.kf_id, K); A(d.kf_state, K); A(d.kp_off, K); A(d.kp_n, K);
+  A(d.kf_id, K); A(d.kf_state, K); A(d.kf_res, K); A(d.kp_off, K); A(d.kp_n, K);
   A(d.q, 4 * K); A(d.R, 9 * K); A(d.t, 3 * K); A(d.C, 3 * K); A(d.P, 12 * K); A(d.cam, 6 * K);
   A(d.g_cs, K); A(d.g_nx, K); A(d.g_ny, K);
   A(d.cell_start, K * (GRID_CELLS + 1)); A(d.cell_items, KP);
@@ -596,7 +745,7 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(d.sp_geo, 5 * MP);
   A(d.covis, K * K);
   A(d.recent_id, MP); A(d.recent_born, MP);
-  A(d.scal, SC_N); A(d.ledger, LG_N);
+  A(d.scal, SC_N); A(d.ledger, LG_N); A(d.lg_log, LG_LOG_CAP);
   Scratch& s = d.s;
   A(s.nbr, NMAX); A(s.deg, NMAX); A(s.F, 9 * NMAX);
   A(s.cur_sorted, d.kpkf_max); A(s.cur_bucket, LMAX + 1);
@@ -636,6 +785,7 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   CU(cudaMemsetAsync(s.pass_of, 0xff, sizeof(int) * K, ctx->stream));
   CU(cudaMemsetAsync(s.hitpass, 0, sizeof(unsigned) * d.kpkf_max * ((TMAX + 31) / 32), ctx->stream));
   m->state.assign(K, KF_FREE);
+  m->res.assign(K, 0);
   m->kp_n.assign(K, 0);
   m->kp_off.assign(K, 0);
   m->ids.assign(K, 0);
@@ -651,6 +801,7 @@ int lm_map_reset(lm_ctx* ctx, int32_t map) {
   DevMap& d = m->d;
   const size_t K = d.kf_cap, MP = d.mp_cap;
   CU(cudaMemsetAsync(d.kf_state, 0, sizeof(int) * K, ctx->stream));
+  CU(cudaMemsetAsync(d.kf_res, 0, K, ctx->stream));
   CU(cudaMemsetAsync(d.covis, 0, sizeof(int) * K * K, ctx->stream));
   CU(cudaMemsetAsync(d.alive, 0, MP, ctx->stream));
   CU(cudaMemsetAsync(d.nobs, 0, sizeof(int) * MP, ctx->stream));
@@ -676,6 +827,7 @@ int lm_map_reset(lm_ctx* ctx, int32_t map) {
   CU(cudaStreamSynchronize(ctx->stream));
   m->slot_of.clear();
   std::fill(m->state.begin(), m->state.end(), KF_FREE);
+  std::fill(m->res.begin(), m->res.end(), 0);
   m->n_slots = m->kp_head = m->resident = 0;
   return LM_OK;
 }
@@ -786,10 +938,10 @@ __global__ void k_end(DevMap* maps, const StepArgs* args, lm_step_stats** totals
   if (threadIdx.x) return;
   lm_step_stats* st = M.s.stats;
   lm_step_stats* t = totals[args[blockIdx.x].map];
-  const int err = M.scal[SC_ERR];
+  const int err = M.scal[SC_ERR], soft = M.scal[SC_SOFT];
   lm_step_stats s = *st;
   lm_step_stats u = *t;
-  s.error = err;
+  s.error = err ? err : soft;
   u.created += s.created;
   u.conflicts += s.conflicts;
   u.degenerate += s.degenerate;
@@ -817,8 +969,9 @@ __global__ void k_end(DevMap* maps, const StepArgs* args, lm_step_stats** totals
   u.fuse_bytes_rev += s.fuse_bytes_rev;
   u.rev_mergeable += s.rev_mergeable;
   for (int k = 0; k < 16; ++k) u.dbg[k] += s.dbg[k];
+  for (int k = 0; k < 4; ++k) u.borderline[k] += s.borderline[k];
   u.first_new_id += 1;  // steps accumulated
-  st->error = err;
+  st->error = s.error;
   *t = u;
 }
 
@@ -929,7 +1082,8 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   return LM_OK;
 }
 
-static int fill_args(lm_ctx* ctx, HostMap* m, int64_t kf_id, const lm_step_params* p, StepArgs& a, bool insert) {
+static int fill_args(lm_ctx* ctx, HostMap* m, int64_t kf_id, const lm_step_params* p, StepArgs& a, bool insert,
+                     bool upload = true) {
   int slot;
   int rc = slot_of(ctx, m, kf_id, &slot, false);
   if (rc) return rc;
@@ -938,9 +1092,10 @@ static int fill_args(lm_ctx* ctx, HostMap* m, int64_t kf_id, const lm_step_param
   a.do_insert = 0;
   if (m->state[slot] == KF_STAGED) {
     if (!insert) return fail(ctx, LM_ERR_INVALID_STATE, "keyframe %lld is staged, not inserted", (long long)kf_id);
-    if (m->resident >= m->caps.store_capacity && m->caps.store_capacity > 0)
-      return fail(ctx, LM_ERR_CAPACITY, "store capacity %d exceeded; size the pre-allocation", m->caps.store_capacity);
     a.do_insert = 1;
+    a.do_upload = upload;
+    if (upload && m->resident >= m->caps.store_capacity && m->caps.store_capacity > 0)
+      return fail(ctx, LM_ERR_CAPACITY, "store capacity %d exceeded; size the pre-allocation", m->caps.store_capacity);
   } else if (m->state[slot] != KF_LIVE) {
     return fail(ctx, LM_ERR_INVALID_STATE, "keyframe %lld is dead", (long long)kf_id);
   }
@@ -962,10 +1117,18 @@ static int fill_args(lm_ctx* ctx, HostMap* m, int64_t kf_id, const lm_step_param
 }
 
 static void after_insert(HostMap* m, const StepArgs& a) {
-  if (a.do_insert) {
-    m->state[a.cur] = KF_LIVE;
+  if (a.do_insert) m->state[a.cur] = KF_LIVE;
+  if (a.do_upload && !m->res[a.cur]) {
+    m->res[a.cur] = 1;
     m->resident++;
   }
+}
+
+static int step_error(lm_ctx* ctx, int code, int map) {
+  if (code == LM_ERR_INVALID_STATE)
+    return fail(ctx, code, "map %d: a stage accessed a non-resident keyframe (upload it to the store first)", map);
+  if (code == LM_ERR_CAPACITY) return fail(ctx, code, "map %d: device arena capacity exceeded", map);
+  return fail(ctx, code, "map %d: invalid pre-bound slot or device error %d", map, code);
 }
 
 static int run_batch(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args, lm_step_stats* out) {
@@ -980,7 +1143,7 @@ static int run_batch(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args, lm
   CU(cudaStreamSynchronize(ctx->stream));
   memcpy(out, ctx->h_stats, sizeof(lm_step_stats) * n);
   for (int k = 0; k < n; ++k)
-    if (out[k].error) return fail(ctx, out[k].error, "device arena overflow or invalid pre-bound slot in map %d", maps[k]);
+    if (out[k].error) return step_error(ctx, out[k].error, maps[k]);
   return LM_OK;
 }
 
@@ -996,13 +1159,19 @@ int lm_step(lm_ctx* ctx, int32_t map, int64_t kf_id, const lm_step_params* p, lm
 
 int lm_step_batch(lm_ctx* ctx, int32_t n, const int32_t* maps, const int64_t* kf_ids, const lm_step_params* p,
                   lm_step_stats* out) {
-  if (!ctx || n < 1 || n > kMaxBatch) return LM_ERR_INVALID_ARGUMENT;
+  if (!ctx) return LM_ERR_INVALID_ARGUMENT;
+  if (n < 1 || n > kMaxBatch || !maps || !kf_ids || !p)
+    return fail(ctx, LM_ERR_INVALID_ARGUMENT, "batch of %d maps (1..%d, maps/kf_ids/params required)", n, kMaxBatch);
   std::vector<StepArgs> args(n);
   for (int k = 0; k < n; ++k) {
     HostMap* m;
     int rc = check_map(ctx, maps[k], &m);
     if (rc) return rc;
-    rc = fill_args(ctx, m, kf_ids[k], p, args[k], true);
+    // every kernel of the batch runs one CTA (cluster) per entry on that entry's map: a
+    // map listed twice would be stepped twice concurrently (a data race), so reject it
+    for (int q = 0; q < k; ++q)
+      if (maps[q] == maps[k]) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "map %d listed twice in one batch", maps[k]);
+    rc = fill_args(ctx, m, kf_ids[k], p + k, args[k], true);  // one lm_step_params per entry
     if (rc) return rc;
   }
   return run_batch(ctx, n, maps, args.data(), out);
@@ -1016,6 +1185,8 @@ int lm_step_stats_fetch(lm_ctx* ctx, int32_t n, const int32_t* maps, lm_step_sta
     CU(cudaMemcpyAsync(out + k, m->d_stats, sizeof(lm_step_stats), cudaMemcpyDeviceToHost, ctx->stream));
   }
   CU(cudaStreamSynchronize(ctx->stream));
+  for (int k = 0; k < n; ++k)  // async steps surface device errors here, like run_batch does
+    if (out[k].error) return step_error(ctx, out[k].error, maps[k]);
   return LM_OK;
 }
 
@@ -1077,10 +1248,12 @@ int lm_kf_insert(lm_ctx* ctx, int32_t map, int64_t kf_id) {
   rc = slot_of(ctx, m, kf_id, &slot, false);
   if (rc) return rc;
   if (m->state[slot] != KF_STAGED) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "duplicate keyframe id %lld", (long long)kf_id);
-  lm_step_params p;
-  memset(&p, 0, sizeof p);
+  // MapModel.insert_keyframe only: residency and the upload ledger entry are the store's
+  // (lm_kf_upload), as in the reference pipeline (pipeline.py:163-164)
+  StepArgs a;
+  if ((rc = fill_args(ctx, m, kf_id, nullptr, a, true, false))) return rc;
   lm_step_stats st;
-  return lm_step(ctx, map, kf_id, &p, &st);
+  return run_batch(ctx, 1, &map, &a, &st);
 }
 
 int lm_create_map_points(lm_ctx* ctx, int32_t map, int64_t kf_id, int32_t neighbor_count, const lm_match_cfg* mc,
@@ -1411,6 +1584,103 @@ int lm_covisible_neighbors(lm_ctx* ctx, int32_t map, int64_t kf, int32_t n, int6
   return LM_OK;
 }
 
+int lm_ledger_log(lm_ctx* ctx, int32_t map, int64_t first, int64_t* bytes, int32_t cap, int32_t* n_out) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  unsigned long long lg[LG_N];
+  CU(cudaStreamSynchronize(ctx->stream));
+  CU(cudaMemcpy(lg, m->d.ledger, sizeof lg, cudaMemcpyDeviceToHost));
+  long long avail = (long long)lg[LG_SMALL_EVENTS];
+  if (avail > LG_LOG_CAP) avail = LG_LOG_CAP;
+  long long n = avail - first;
+  if (first < 0 || n < 0) n = 0;
+  if (n > cap) n = cap;
+  if (n_out) *n_out = (int32_t)n;
+  if (n) CU(cudaMemcpy(bytes, m->d.lg_log + first, sizeof(long long) * n, cudaMemcpyDeviceToHost));
+  return LM_OK;
+}
+
+int lm_ledger_add(lm_ctx* ctx, int32_t map, int64_t naive_bytes, int32_t small_stage_triangulation,
+                  int64_t small_bytes, int32_t small_events) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  if (naive_bytes < 0 || small_bytes < 0 || small_events < 0 || small_events > 1)
+    return fail(ctx, LM_ERR_INVALID_ARGUMENT, "transfer size must be non-negative");
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_LEDGER_ADD;
+  a.v0 = naive_bytes;
+  a.v1 = small_bytes;
+  a.n = small_events;
+  a.b = small_stage_triangulation ? 1 : 0;
+  int res[1];
+  if ((rc = run_op(ctx, m, map, a, res, 1))) return rc;
+  return op_status(ctx, res[0], "ledger");
+}
+
+int lm_audit(lm_ctx* ctx, int32_t map, lm_audit_record* out, int32_t cap, int32_t* n_out) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  if ((rc = refresh(ctx, m, map))) return rc;  // clean lists are sorted (not required, but cheap)
+  int next = 0;
+  CU(cudaMemcpy(&next, m->d.scal + SC_NEXT_ID, sizeof(int), cudaMemcpyDeviceToHost));
+  const size_t K = m->d.kf_cap;
+  const int rcap = 1 << 16;
+  void* scratch = nullptr;
+  CU(cudaMalloc(&scratch, sizeof(int) * (K * K + 4) + sizeof(int4) * rcap));
+  AuditOut O;
+  O.count = (int*)scratch;
+  O.expect = O.count + 4;
+  O.rec = (int4*)(O.expect + K * K);
+  O.cap = rcap;
+  cudaStream_t st = ctx->stream;
+  int rc2 = LM_OK;
+  do {
+    if (cudaMemsetAsync(scratch, 0, sizeof(int) * (K * K + 4), st) != cudaSuccess) { rc2 = LM_ERR_CUDA; break; }
+    if (next) k_audit_points<<<(next + 255) / 256, 256, 0, st>>>(m->d, O, next);
+    if (m->n_slots) {
+      k_audit_slots<<<dim3((m->d.kpkf_max + 255) / 256, m->n_slots < 1024 ? m->n_slots : 1024), 256, 0, st>>>(
+          m->d, O, m->n_slots, next);
+      const long long np = (long long)m->n_slots * m->n_slots;
+      const int blocks = (int)((np + 255) / 256 < 4096 ? (np + 255) / 256 : 4096);
+      k_audit_covis<<<blocks, 256, 0, st>>>(m->d, O, m->n_slots);
+    }
+    ctx->launches += 3;
+  } while (0);
+  int total = 0;
+  std::vector<int4> rec;
+  if (rc2 == LM_OK && cudaGetLastError() == cudaSuccess && cudaStreamSynchronize(st) == cudaSuccess &&
+      cudaMemcpy(&total, O.count, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess) {
+    const int got = total < rcap ? total : rcap;
+    rec.resize(got > 0 ? got : 1);
+    if (got) cudaMemcpy(rec.data(), O.rec, sizeof(int4) * got, cudaMemcpyDeviceToHost);
+    rec.resize(got);
+  } else {
+    rc2 = LM_ERR_CUDA;
+  }
+  cudaFree(scratch);
+  if (rc2) return fail(ctx, rc2, "audit kernels failed");
+  if (n_out) *n_out = total;
+  const int w = (int)rec.size() < cap ? (int)rec.size() : cap;
+  for (int k = 0; k < w; ++k) {  // slots -> keyframe ids
+    const int4 r = rec[k];
+    lm_audit_record& o = out[k];
+    o.code = r.x;
+    switch (r.x) {
+      case AV_OBS_DEAD_KF: o.mp = r.y; o.kf_a = m->ids[r.z]; o.kf_b = -1; o.kp = -1; break;
+      case AV_BIND_MISMATCH: o.mp = r.y; o.kf_a = m->ids[r.z]; o.kf_b = -1; o.kp = r.w; break;
+      case AV_SLOT_DEAD:
+      case AV_SLOT_NOT_OBS: o.mp = r.w; o.kf_a = m->ids[r.y]; o.kf_b = -1; o.kp = r.z; break;
+      case AV_COVIS: o.mp = -1; o.kf_a = m->ids[r.y]; o.kf_b = m->ids[r.z]; o.kp = -1; break;
+      default: o.mp = r.y; o.kf_a = -1; o.kf_b = -1; o.kp = -1;
+    }
+  }
+  return LM_OK;
+}
+
 int lm_ledger(lm_ctx* ctx, int32_t map, lm_ledger_t* out) {
   HostMap* m;
   int rc = check_map(ctx, map, &m);
@@ -1545,6 +1815,304 @@ int lm_recent_import(lm_ctx* ctx, int32_t map, const int64_t* ids, const int32_t
   return LM_OK;
 }
 
+// ------------------------------------------------------------------- store / LBA write-back / import
+
+static int io_reserve(lm_ctx* ctx, HostMap* m, size_t bytes) {
+  if (bytes <= m->io_bytes) return LM_OK;
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (m->d_io) CU(cudaFree(m->d_io));
+  size_t sz = m->io_bytes ? m->io_bytes : 65536;
+  while (sz < bytes) sz *= 2;
+  CU(cudaMalloc(&m->d_io, sz));
+  m->io_bytes = sz;
+  return LM_OK;
+}
+
+int lm_kf_upload(lm_ctx* ctx, int32_t map, int64_t kf_id) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  int slot;
+  if ((rc = slot_of(ctx, m, kf_id, &slot, false))) return rc;
+  if (m->state[slot] == KF_STAGED)
+    return fail(ctx, LM_ERR_INVALID_STATE, "keyframe %lld is staged, not inserted", (long long)kf_id);
+  if (m->res[slot]) return fail(ctx, LM_ERR_INVALID_STATE, "keyframe %lld already resident", (long long)kf_id);
+  if (m->caps.store_capacity > 0 && m->resident >= m->caps.store_capacity)
+    return fail(ctx, LM_ERR_CAPACITY, "store capacity %d exceeded; size the pre-allocation", m->caps.store_capacity);
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_UPLOAD;
+  a.a = slot;
+  int res[1];
+  if ((rc = run_op(ctx, m, map, a, res, 1))) return rc;
+  m->res[slot] = 1;
+  m->resident++;
+  return op_status(ctx, res[0], "upload_keyframe");
+}
+
+int lm_kf_evict(lm_ctx* ctx, int32_t map, int64_t kf_id) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  auto it = m->slot_of.find(kf_id);
+  if (it == m->slot_of.end() || !m->res[it->second])
+    return fail(ctx, LM_ERR_INVALID_ARGUMENT, "keyframe %lld is not resident", (long long)kf_id);
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_EVICT;
+  a.a = it->second;
+  int res[1];
+  if ((rc = run_op(ctx, m, map, a, res, 1))) return rc;
+  m->res[it->second] = 0;
+  m->resident--;
+  return op_status(ctx, res[0], "evict_keyframe");
+}
+
+int lm_kf_resident(lm_ctx* ctx, int32_t map, int64_t kf_id, int32_t* resident, int32_t* count) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  auto it = m->slot_of.find(kf_id);
+  if (resident) *resident = it != m->slot_of.end() && m->res[it->second];
+  if (count) *count = m->resident;
+  return LM_OK;
+}
+
+int lm_kf_set_pose(lm_ctx* ctx, int32_t map, int64_t kf_id, const double quat[4], const double trans[3]) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  if (!quat || !trans) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "pose arrays required");
+  int slot;
+  if ((rc = slot_of(ctx, m, kf_id, &slot, false))) return rc;
+  if (m->state[slot] == KF_DEAD) return fail(ctx, LM_ERR_INVALID_STATE, "keyframe %lld is dead", (long long)kf_id);
+  for (int k = 0; k < 4; ++k)
+    if (!std::isfinite(quat[k])) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "non-finite quaternion");
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_SET_POSE;
+  a.a = slot;
+  double* q = a.pose;
+  double *R = q + 4, *t = q + 13, *Cc = q + 16, *P = q + 19;
+  for (int k = 0; k < 4; ++k) q[k] = quat[k];
+  for (int k = 0; k < 3; ++k) t[k] = trans[k];
+  // the same host code as staging (tables bit-identical to a fresh stage of the new pose);
+  // the camera is the slot's (read back from the host mirror of the staged record)
+  double cam[6];
+  CU(cudaMemcpy(cam, m->d.cam + 6 * slot, sizeof cam, cudaMemcpyDeviceToHost));
+  quat_to_rot(q, R);
+  camera_center(R, t, Cc);
+  proj_matrix(cam[0], cam[1], cam[2], cam[3], R, t, P);
+  int res[1];
+  if ((rc = run_op(ctx, m, map, a, res, 1))) return rc;
+  return op_status(ctx, res[0], "set_pose");
+}
+
+int lm_mp_patch_positions(lm_ctx* ctx, int32_t map, int32_t n, const int64_t* ids, const double* pos) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  if (n < 0 || (n && (!ids || !pos))) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "ids/pos required");
+  if (n == 0) return LM_OK;
+  int next = 0;
+  CU(cudaStreamSynchronize(ctx->stream));
+  CU(cudaMemcpy(&next, m->d.scal + SC_NEXT_ID, sizeof(int), cudaMemcpyDeviceToHost));
+  std::vector<unsigned char> alive(next > 0 ? next : 1);
+  if (next) CU(cudaMemcpy(alive.data(), m->d.alive, next, cudaMemcpyDeviceToHost));
+  std::vector<char> buf(32 * (size_t)n);
+  for (int k = 0; k < n; ++k) {
+    if (ids[k] < 0 || ids[k] >= next) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "unknown map point %lld", (long long)ids[k]);
+    if (!alive[ids[k]]) return fail(ctx, LM_ERR_INVALID_STATE, "map point %lld is dead", (long long)ids[k]);
+    const int id = (int)ids[k];
+    memcpy(&buf[32 * (size_t)k], &id, 4);
+    memcpy(&buf[32 * (size_t)k + 8], pos + 3 * (size_t)k, 24);
+  }
+  if ((rc = io_reserve(ctx, m, buf.size()))) return rc;
+  CU(cudaMemcpyAsync(m->d_io, buf.data(), buf.size(), cudaMemcpyHostToDevice, ctx->stream));
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_PATCH_POS;
+  a.n = n;
+  a.buf = m->d_io;
+  int res[1];
+  if ((rc = run_op(ctx, m, map, a, res, 1))) return rc;
+  return op_status(ctx, res[0], "patch_positions");
+}
+
+int lm_mp_get(lm_ctx* ctx, int32_t map, int64_t mp, lm_point_record* out, int64_t* obs_kf, int32_t* obs_kp,
+              int32_t obs_cap) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  if (!out) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "output record required");
+  int next = 0;
+  CU(cudaStreamSynchronize(ctx->stream));
+  CU(cudaMemcpy(&next, m->d.scal + SC_NEXT_ID, sizeof(int), cudaMemcpyDeviceToHost));
+  if (mp < 0 || mp >= next) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "unknown map point %lld", (long long)mp);
+  const size_t bytes = sizeof(PointRec) + sizeof(int2) * (size_t)m->d.kf_cap;
+  if ((rc = io_reserve(ctx, m, bytes))) return rc;
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_MP_GET;
+  a.a = (int)mp;
+  a.buf = m->d_io;
+  int res[1];
+  if ((rc = run_op(ctx, m, map, a, res, 1))) return rc;
+  std::vector<char> h(sizeof(PointRec));
+  CU(cudaMemcpy(h.data(), m->d_io, sizeof(PointRec), cudaMemcpyDeviceToHost));
+  const PointRec* r = (const PointRec*)h.data();
+  std::vector<int2> o(r->nobs > 0 ? r->nobs : 1);
+  if (r->nobs) CU(cudaMemcpy(o.data(), (char*)m->d_io + sizeof(PointRec), sizeof(int2) * r->nobs, cudaMemcpyDeviceToHost));
+  memcpy(out->pos, r->pos, 24);
+  memcpy(out->rep, r->rep, 32);
+  out->first_kf_id = r->first_kf;
+  out->alive = r->alive;
+  out->found = r->found;
+  out->visible = r->visible;
+  out->nobs = r->nobs;
+  for (int l = 0; l < 16; ++l) out->counts[l] = r->counts[l];
+  if (r->nobs > obs_cap) return fail(ctx, LM_ERR_CAPACITY, "observation buffer too small (%d)", r->nobs);
+  for (int k = 0; k < r->nobs; ++k) {
+    if (obs_kf) obs_kf[k] = m->ids[o[k].x];
+    if (obs_kp) obs_kp[k] = o[k].y;
+  }
+  return op_status(ctx, res[0], "mp_get");
+}
+
+int lm_kf_bindings(lm_ctx* ctx, int32_t map, int64_t kf_id, int64_t* out, int32_t cap, int32_t* n_out) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  int slot;
+  if ((rc = slot_of(ctx, m, kf_id, &slot, false))) return rc;
+  const int n = m->kp_n[slot];
+  if (n_out) *n_out = n;
+  if (n > cap) return fail(ctx, LM_ERR_CAPACITY, "binding buffer too small");
+  std::vector<int> b(n > 0 ? n : 1);
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (n) CU(cudaMemcpy(b.data(), m->d.kbind + m->kp_off[slot], sizeof(int) * n, cudaMemcpyDeviceToHost));
+  for (int k = 0; k < n; ++k) out[k] = b[k];
+  return LM_OK;
+}
+
+int lm_bound_points(lm_ctx* ctx, int32_t map, int64_t kf_id, int64_t* out, int32_t cap, int32_t* n_out) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  int slot;
+  if ((rc = slot_of(ctx, m, kf_id, &slot, false))) return rc;
+  if ((rc = io_reserve(ctx, m, sizeof(int) * (size_t)(m->kp_n[slot] + 1)))) return rc;
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_BOUND;
+  a.a = slot;
+  a.buf = m->d_io;
+  int res[2];
+  if ((rc = run_op(ctx, m, map, a, res, 2))) return rc;
+  const int P = res[1];
+  if (n_out) *n_out = P;
+  if (P > cap) return fail(ctx, LM_ERR_CAPACITY, "point buffer too small");
+  std::vector<int> b(P > 0 ? P : 1);
+  if (P) CU(cudaMemcpy(b.data(), m->d_io, sizeof(int) * P, cudaMemcpyDeviceToHost));
+  for (int k = 0; k < P; ++k) out[k] = b[k];
+  return LM_OK;
+}
+
+int lm_covis_row(lm_ctx* ctx, int32_t map, int64_t kf_id, int64_t* kf_ids, int32_t* weights, int32_t cap,
+                 int32_t* n_out) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  int slot;
+  if ((rc = slot_of(ctx, m, kf_id, &slot, false))) return rc;
+  const int K = m->d.kf_cap;
+  std::vector<int> row(K);
+  CU(cudaStreamSynchronize(ctx->stream));
+  CU(cudaMemcpy(row.data(), m->d.covis + (size_t)slot * K, sizeof(int) * K, cudaMemcpyDeviceToHost));
+  int n = 0;
+  for (int s = 0; s < m->n_slots; ++s)
+    if (row[s] != 0 && s != slot) {
+      if (n < cap) {
+        kf_ids[n] = m->ids[s];
+        weights[n] = row[s];
+      }
+      ++n;
+    }
+  if (n_out) *n_out = n;
+  if (n > cap) return fail(ctx, LM_ERR_CAPACITY, "covisibility buffer too small");
+  return LM_OK;
+}
+
+// Import a whole reference map state (MapModel + DeviceStore ledger + probation list) into an
+// empty map: points first (ids 0..n-1, no observations), then every keyframe staged with its
+// bindings and inserted in the given order, which registers the observations exactly as
+// insert_keyframe does (mapmodel.py:185-199: sorted lists, per-level counters, covisibility
+// as the shared-point counts), then dead keyframes tombstoned, residency, ledger and the
+// probation list set. Representative descriptors are recomputed (a pure function of the
+// observation list, equal to the reference's stored one).
+int lm_import_snapshot(lm_ctx* ctx, int32_t map, const lm_snapshot* S) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  if (!S || S->n_kf < 0 || S->n_points < 0) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "bad snapshot");
+  {
+    int next = 0;
+    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaMemcpy(&next, m->d.scal + SC_NEXT_ID, sizeof(int), cudaMemcpyDeviceToHost));
+    if (m->n_slots || next) return fail(ctx, LM_ERR_INVALID_STATE, "import needs an empty map (lm_map_reset)");
+  }
+  if (S->n_points > m->d.mp_cap) return fail(ctx, LM_ERR_CAPACITY, "snapshot has %d points, map capacity %d",
+                                              S->n_points, m->d.mp_cap);
+  if (S->n_points) {
+    std::vector<char> buf(80 * (size_t)S->n_points, 0);
+    for (int i = 0; i < S->n_points; ++i) {
+      char* e = &buf[80 * (size_t)i];
+      memcpy(e, S->pos + 3 * (size_t)i, 24);
+      memcpy(e + 24, S->rep + 32 * (size_t)i, 32);
+      memcpy(e + 56, S->found + i, 4);
+      memcpy(e + 60, S->visible + i, 4);
+      e[64] = S->alive[i] ? 1 : 0;
+      const long long fk = S->first_kf ? (long long)S->first_kf[i] : -1;
+      memcpy(e + 72, &fk, 8);
+    }
+    if ((rc = io_reserve(ctx, m, buf.size()))) return rc;
+    CU(cudaMemcpyAsync(m->d_io, buf.data(), buf.size(), cudaMemcpyHostToDevice, ctx->stream));
+    OpArgs a;
+    memset(&a, 0, sizeof a);
+    a.op = OP_IMPORT_POINTS;
+    a.n = S->n_points;
+    a.buf = m->d_io;
+    int res[1];
+    if ((rc = run_op(ctx, m, map, a, res, 1))) return rc;
+    if (res[0]) return op_status(ctx, res[0], "import points");
+  }
+  size_t off = 0;
+  for (int k = 0; k < S->n_kf; ++k) {
+    const int n = S->kp_n[k];
+    const bool live = S->kf_alive[k] != 0;
+    if ((rc = lm_kf_stage(ctx, map, S->kf_id[k], S->quat + 4 * (size_t)k, S->trans + 3 * (size_t)k,
+                          S->cam + 6 * (size_t)k, n, S->u + off, S->v + off, S->level + off, S->desc + 32 * off,
+                          live ? S->bindings + off : nullptr)))
+      return rc;
+    if ((rc = lm_kf_insert(ctx, map, S->kf_id[k]))) return rc;
+    if (!live && (rc = lm_kf_kill(ctx, map, S->kf_id[k]))) return rc;
+    if (S->kf_resident && S->kf_resident[k] && (rc = lm_kf_upload(ctx, map, S->kf_id[k]))) return rc;
+    off += n;
+  }
+  // representative descriptors and sorted lists: refresh every dirty point now
+  if ((rc = refresh(ctx, m, map))) return rc;
+  unsigned long long lg[LG_N] = {0};
+  lg[LG_PERSIST] = S->ledger.persistent_bytes_up;
+  lg[LG_NAIVE] = S->ledger.naive_bytes_up;
+  lg[LG_SMALL_TRI] = S->ledger.small_bytes_triangulation;
+  lg[LG_SMALL_FUSE] = S->ledger.small_bytes_fusion;
+  lg[LG_SMALL_EVENTS] = S->ledger.small_transfer_events;
+  lg[LG_EVICT] = S->ledger.evictions;
+  CU(cudaMemcpy(m->d.ledger, lg, sizeof lg, cudaMemcpyHostToDevice));
+  if (S->n_recent && (rc = lm_recent_import(ctx, map, S->recent_id, S->recent_born, S->n_recent))) return rc;
+  return LM_OK;
+}
+
 // ------------------------------------------------------------------- measurement
 __global__ void k_rewind_state(DevMap M, int n_slots) {
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n_slots; s += gridDim.x * blockDim.x)
@@ -1559,6 +2127,7 @@ int lm_map_rewind(lm_ctx* ctx, int32_t map) {
   const size_t K = d.kf_cap, MP = d.mp_cap;
   cudaStream_t st = ctx->stream;
   CU(cudaMemsetAsync(d.covis, 0, sizeof(int) * K * K, st));
+  CU(cudaMemsetAsync(d.kf_res, 0, K, st));
   CU(cudaMemsetAsync(d.alive, 0, MP, st));
   CU(cudaMemsetAsync(d.nobs, 0, sizeof(int) * MP, st));
   CU(cudaMemsetAsync(d.ocap, 0, sizeof(int) * MP, st));
@@ -1588,6 +2157,7 @@ int lm_map_rewind(lm_ctx* ctx, int32_t map) {
   CU(cudaStreamSynchronize(st));
   for (int s = 0; s < m->n_slots; ++s)
     if (m->state[s] != KF_FREE) m->state[s] = KF_STAGED;
+  std::fill(m->res.begin(), m->res.end(), 0);
   m->resident = 0;
   return LM_OK;
 }

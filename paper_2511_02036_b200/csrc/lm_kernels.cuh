@@ -36,6 +36,7 @@ struct StepArgs {
   int cur;            // current keyframe slot
   int n_nbr_req;      // neighbor_count
   int do_insert, do_cull, do_create, do_fuse;
+  int do_upload;      // with do_insert: also DeviceStore.upload_keyframe (residency + ledger)
   int processed;      // pipeline._processed
   int explicit_nbr;   // lm_search: neighbour list given (nbr0), masks optional
   int nbr0;
@@ -151,6 +152,7 @@ __global__ void __launch_bounds__(256) k_insert(DevMap* maps, const StepArgs* ar
   {  // the step's statistics record starts from zero
     int* p = (int*)M.s.stats;
     for (int k = threadIdx.x; k < (int)(sizeof(lm_step_stats) / 4); k += blockDim.x) p[k] = 0;
+    if (threadIdx.x == 0) M.scal[SC_SOFT] = 0;
     __syncthreads();
   }
   if (!A.do_insert) return;
@@ -164,7 +166,10 @@ __global__ void __launch_bounds__(256) k_insert(DevMap* maps, const StepArgs* ar
   __syncthreads();
   if (threadIdx.x) return;
   M.kf_state[slot] = KF_LIVE;
-  M.ledger[LG_PERSIST] += (unsigned long long)payload_bytes(M, slot);
+  if (A.do_upload) {  // upload_keyframe devicestore.py:68-78
+    M.kf_res[slot] = 1;
+    M.ledger[LG_PERSIST] += (unsigned long long)payload_bytes(M, slot);
+  }
   if (!any) return;
   // pre-bound slots register their observations in keypoint order (insert_keyframe
   // mapmodel.py:185-199); rare (tests, externally seeded maps), so one thread
@@ -396,7 +401,11 @@ __global__ void __launch_bounds__(256) k_select(DevMap* maps, const StepArgs* ar
       __syncthreads();
     }
   }
-  const int nn = n_out;
+  // record_neighbor_access (devicestore.py:80-92): every neighbour must be resident, else
+  // the stage fails before touching the map (InvalidStateError in the reference)
+  const bool nonres = __syncthreads_or(threadIdx.x < n_out && !A.explicit_nbr && !M.kf_res[out[threadIdx.x]]);
+  if (nonres && threadIdx.x == 0) atomicCAS(&M.scal[SC_SOFT], 0, LM_ERR_INVALID_STATE);
+  const int nn = nonres ? 0 : n_out;
   lm_step_stats* st = M.s.stats;
   if (threadIdx.x < nn) {
     const int s = out[threadIdx.x];
@@ -583,6 +592,7 @@ __global__ void __launch_bounds__(MATCH_WARPS * 32) k_match(DevMap* maps, const 
   }
   const int maxd = A.mc.match_max_distance;
   unsigned long long best = ~0ull;
+  int border = 0;
   for (int c0 = jb; c0 < je; c0 += MATCH_JT) {
     const int cn = je - c0 < MATCH_JT ? je - c0 : MATCH_JT;
     __syncthreads();
@@ -601,7 +611,9 @@ __global__ void __launch_bounds__(MATCH_WARPS * 32) k_match(DevMap* maps, const 
           dist += __popc(a1.x ^ b1.x) + __popc(a1.y ^ b1.y) + __popc(a1.z ^ b1.z) + __popc(a1.w ^ b1.w);
           if (dist <= maxd) {
             const size_t e = base + c0 + k;
-            if (epi_d2(l, den, M.s.nb_u[e], M.s.nb_v[e]) <= M.s.nb_thr[e]) {
+            const double d2 = epi_d2(l, den, M.s.nb_u[e], M.s.nb_v[e]), thr = M.s.nb_thr[e];
+            border += near_tie(d2, thr, thr);
+            if (d2 <= thr) {
               const unsigned long long key = ((unsigned long long)dist << 32) | (unsigned)M.s.nb_j[e];
               best = key < best ? key : best;
             }
@@ -611,6 +623,10 @@ __global__ void __launch_bounds__(MATCH_WARPS * 32) k_match(DevMap* maps, const 
     }
   }
   if (active && best != ~0ull) atomicMin(&best_sh[lane], best);
+  if (__any_sync(0xffffffffu, border)) {
+    for (int o = 16; o; o >>= 1) border += __shfl_xor_sync(0xffffffffu, border, o);
+    if (lane == 0) atomicAdd((unsigned long long*)&M.s.stats->borderline[0], (unsigned long long)border);
+  }
   __syncthreads();
   if (wid == 0 && active) {
     const unsigned long long b = best_sh[lane];
@@ -665,9 +681,9 @@ __global__ void __launch_bounds__(256) k_tri(DevMap* maps, const StepArgs* args)
     const int i = M.s.cand_i[base + k], j = M.s.cand_j[base + k];
     const int ga = offa + i, gb = offb + j;
     double X[3] = {0, 0, 0};
-    int st;
+    int st, border = 0;
     if (!triangulate(M.P + 12 * cur, M.P + 12 * nb, M.C + 3 * cur, M.C + 3 * nb, M.ku[ga], M.kv[ga], M.ku[gb],
-                     M.kv[gb], X)) {
+                     M.kv[gb], X, &border)) {
       st = CS_DEGEN;
     } else {
       const int la = M.klev[ga], lb = M.klev[gb];
@@ -675,8 +691,9 @@ __global__ void __launch_bounds__(256) k_tri(DevMap* maps, const StepArgs* args)
                  M.cam[6 * cur + 2], M.cam[6 * cur + 3], M.ku[ga], M.kv[ga], M.S2[la], M.S[la], M.sf};
       ViewGeo vb{M.R + 9 * nb, M.t + 3 * nb, M.C + 3 * nb, M.cam[6 * nb], M.cam[6 * nb + 1],
                  M.cam[6 * nb + 2], M.cam[6 * nb + 3], M.ku[gb], M.kv[gb], M.S2[lb], M.S[lb], M.sf};
-      st = creation_gates(va, vb, X, A.gc.cos_parallax_max, A.gc.chi2_mono, A.gc.scale_ratio_slack);
+      st = creation_gates(va, vb, X, A.gc.cos_parallax_max, A.gc.chi2_mono, A.gc.scale_ratio_slack, &border);
     }
+    if (border) atomicAdd((unsigned long long*)&M.s.stats->borderline[1], (unsigned long long)border);
     M.s.cand_st[base + k] = st;
     M.s.cand_X[3 * (base + k)] = X[0];
     M.s.cand_X[3 * (base + k) + 1] = X[1];
@@ -918,8 +935,11 @@ struct GWin {
   int lp, x0, x1, y0, y1;
 };
 
+// border (optional): +1 to border[0] when the visibility decision rests on a borderline
+// compare (no clearly failing one, at least one near_tie), +1 to border[1] for a rint tie of
+// the predicted level
 __device__ __forceinline__ bool gather_window(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g, int ts,
-                                              const TgtView& T, GWin& w) {
+                                              const TgtView& T, GWin& w, int* border = nullptr) {
   if (!g.ok) return false;
   const double* R = T.pose ? T.pose : M.R + 9 * ts;
   const double* t = T.pose ? T.pose + 9 : M.t + 3 * ts;
@@ -934,11 +954,24 @@ __device__ __forceinline__ bool gather_window(const DevMap& M, const lm_fuse_cfg
   const bool inview = zc > 0 && u >= 0 && u < cam[4] && v >= 0 && v < cam[5];
   const double dx = g.x - C[0], dy = g.y - C[1], dz = g.z - C[2];
   const double d = sqrt(dx * dx + dy * dy + dz * dz);
-  if (!(zc > 0 && inview && d >= g.blo && d <= g.bhi)) return false;
   const double cosv = (dx * g.vx + dy * g.vy + dz * g.vz) / d;
+  if (border) {
+    const int near = near_tie(zc, 0.0, fabs(qz) + fabs(t[2])) + near_tie(u, 0.0, cam[4]) + near_tie(u, cam[4], cam[4]) +
+                     near_tie(v, 0.0, cam[5]) + near_tie(v, cam[5], cam[5]) + near_tie(d, g.blo, d) +
+                     near_tie(d, g.bhi, d) + near_tie(cosv, fc.min_view_cos, 1.0);
+    if (near) {  // a clearly failing compare decides regardless of the borderline ones
+      const double e = kFlipRel;
+      const bool clear_fail = zc < -e * (fabs(qz) + fabs(t[2])) || u < -e * cam[4] || u > cam[4] * (1 + e) ||
+                              v < -e * cam[5] || v > cam[5] * (1 + e) || d < g.blo - e * d || d > g.bhi + e * d ||
+                              cosv < fc.min_view_cos - e;
+      if (!clear_fail) border[0] += 1;
+    }
+  }
+  if (!(zc > 0 && inview && d >= g.blo && d <= g.bhi)) return false;
   if (!(cosv >= fc.min_view_cos)) return false;
   double lraw = log(d / g.d0) / M.log_sf;
   if (!isfinite(lraw)) lraw = 0.0;
+  if (border) border[1] += near_tie(lraw - floor(lraw), 0.5, lraw > 1.0 ? lraw : 1.0);
   double lr = rint(lraw);
   lr = lr < 0 ? 0 : (lr > M.L - 1 ? M.L - 1 : lr);
   w.lp = (int)lr;
@@ -960,9 +993,10 @@ __device__ __forceinline__ bool gather_window(const DevMap& M, const lm_fuse_cfg
 
 // exact radius / level test + Hamming of one window candidate k; folds (dist, k) into best
 __device__ __forceinline__ void gather_test(const lm_fuse_cfg& fc, const PGeo& g, const TgtView& T, const GWin& w,
-                                            int k, unsigned long long& best) {
+                                            int k, unsigned long long& best, int* border = nullptr) {
   const double du = T.u[k] - w.u, dv = T.v[k] - w.v;
   const int dl = (int)T.lev[k] - w.lp;
+  if (border && (dl < 0 ? -dl : dl) <= fc.level_window) border[0] += near_tie(du * du + dv * dv, w.r2, w.r2);
   if (du * du + dv * dv <= w.r2 && (dl < 0 ? -dl : dl) <= fc.level_window) {
     const int dist = hamming(T.desc[2 * k], T.desc[2 * k + 1], g.r0, g.r1);
     if (dist <= fc.match_max_distance) {
@@ -975,14 +1009,15 @@ __device__ __forceinline__ void gather_test(const lm_fuse_cfg& fc, const PGeo& g
 // project + gates + grid window search for one (point, target) pair (fusion.py:97-129,
 // 178-196). Returns -2 if the point is not visible in the target, -1 if visible without a
 // hit, else the hit keypoint (lowest (distance, index) within the window).
-__device__ int gather_hit(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g, int ts, const TgtView& T) {
+__device__ __forceinline__ int gather_hit(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g, int ts, const TgtView& T,
+                          int* border = nullptr) {
   GWin w;
-  if (!gather_window(M, fc, g, ts, T, w)) return -2;
+  if (!gather_window(M, fc, g, ts, T, w, border)) return -2;
   unsigned long long best = ~0ull;
   for (int cy = w.y0; cy <= w.y1; ++cy)
     for (int cx = w.x0; cx <= w.x1; ++cx) {
       const int cell = cy * T.nx + cx;
-      for (int it = T.cst[cell]; it < T.cst[cell + 1]; ++it) gather_test(fc, g, T, w, T.items[it], best);
+      for (int it = T.cst[cell]; it < T.cst[cell + 1]; ++it) gather_test(fc, g, T, w, T.items[it], best, border);
     }
   return best == ~0ull ? -1 : (int)(best & 0xffffffffu);
 }
@@ -1023,9 +1058,23 @@ __device__ __forceinline__ int build_action(const DevMap& M, int pid, int ts, in
   return 0;
 }
 
+// fusion borderline counts of this thread into the step record (warp-aggregated)
+__device__ __forceinline__ void add_borderline(const DevMap& M, const int border[2]) {
+  if (!__any_sync(0xffffffffu, border[0] | border[1])) return;
+  int b0 = border[0], b1 = border[1];
+  for (int o = 16; o; o >>= 1) {
+    b0 += __shfl_xor_sync(0xffffffffu, b0, o);
+    b1 += __shfl_xor_sync(0xffffffffu, b1, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (b0) atomicAdd((unsigned long long*)&M.s.stats->borderline[2], (unsigned long long)b0);
+    if (b1) atomicAdd((unsigned long long*)&M.s.stats->borderline[3], (unsigned long long)b1);
+  }
+}
+
 __device__ __forceinline__ int gather_one(const DevMap& M, const lm_fuse_cfg& fc, const PGeo& g, int pid, int ts,
-                                          const TgtView& T, ActRec* act, int* has_act) {
-  const int j = gather_hit(M, fc, g, ts, T);
+                                          const TgtView& T, ActRec* act, int* has_act, int* border = nullptr) {
+  const int j = gather_hit(M, fc, g, ts, T, border);
   *has_act = build_action(M, pid, ts, j, act);
   return j >= -1;
 }
@@ -1599,7 +1648,15 @@ __global__ void __launch_bounds__(1024) k_fuse_targets(DevMap* maps, const StepA
   int* sh_slot = (int*)(dynk + M.kf_cap);
   __shared__ int sh[32];
   const long long t0 = gtime();
-  const int T = fusion_targets<1024>(M, A.cur, A.fc.n1, A.fc.n2, n_slots_max, sh_slot, sh_key);
+  int T = fusion_targets<1024>(M, A.cur, A.fc.n1, A.fc.n2, n_slots_max, sh_slot, sh_key);
+  {  // record_neighbor_access("fusion", targets): all resident, else the stage fails untouched
+    int bad = 0;
+    for (int k = threadIdx.x; k < T; k += 1024) bad |= !M.kf_res[M.s.targets[k]];
+    if (__syncthreads_or(bad)) {
+      if (threadIdx.x == 0) atomicCAS(&M.scal[SC_SOFT], 0, LM_ERR_INVALID_STATE);
+      T = 0;
+    }
+  }
   __shared__ unsigned long long s_tkp;
   if (threadIdx.x == 0) s_tkp = 0;
   const int P = T ? bound_points<1024>(M, A.cur, sh) : 0;  // (barriers)
@@ -1618,6 +1675,8 @@ __global__ void __launch_bounds__(1024) k_fuse_targets(DevMap* maps, const StepA
     if (T) {
       const unsigned long long mpb = M.mp_rec_bytes;
       const long long tkp = (long long)s_tkp;
+      const unsigned long long ev = M.ledger[LG_SMALL_EVENTS];
+      if (ev < (unsigned long long)LG_LOG_CAP) M.lg_log[ev] = (long long)(P * mpb);
       const unsigned long long naive = (unsigned long long)tkp * (M.kp_rec_bytes + M.desc_bytes);  // payload_bytes
       M.ledger[LG_NAIVE] += naive + P * mpb;
       M.ledger[LG_PERSIST] += P * mpb;
@@ -1671,12 +1730,14 @@ __global__ void __launch_bounds__(256) k_fuse_gather(DevMap* maps, const StepArg
   const int it = b0 + threadIdx.x;
   ActRec a;
   int has = 0;
+  int border[2] = {0, 0};
   if (it < TP) {
     const int t = it / P, p = it - t * P;
     const int pid = M.s.pts[p];
     const int ts = M.s.targets[t];
-    if (gather_one(M, A.fc, M.s.geo[p], pid, ts, tgt_global(M, ts), &a, &has)) atomicAdd(&M.visible[pid], 1);
+    if (gather_one(M, A.fc, M.s.geo[p], pid, ts, tgt_global(M, ts), &a, &has, border)) atomicAdd(&M.visible[pid], 1);
   }
+  add_borderline(M, border);
   int tot;
   const int at = block_excl_scan<256>(has, sh, tot);
   if (has) M.s.acts2[b0 + at] = a;
@@ -1885,9 +1946,12 @@ __global__ void __launch_bounds__(256) k_fuse_spec_hit(DevMap* maps, const StepA
     const int mp = M.s.upts[k];
     PGeo g;
     point_geometry(M, mp, A.fc.dist_band_slack, g);
-    const int j = gather_hit(M, A.fc, g, A.cur, T);
+    int border[2] = {0, 0};
+    const int j = gather_hit(M, A.fc, g, A.cur, T, border);
     M.hit[mp] = make_int2(M.ver[mp], j);
     hit_list_add(M, j, mp);
+    if (border[0]) atomicAdd((unsigned long long*)&M.s.stats->borderline[2], (unsigned long long)border[0]);
+    if (border[1]) atomicAdd((unsigned long long*)&M.s.stats->borderline[3], (unsigned long long)border[1]);
   }
 }
 
@@ -1913,10 +1977,17 @@ __global__ void __launch_bounds__(256) k_fuse_spec(DevMap* maps, const StepArgs*
       if (mp >= 0 && M.alive[mp]) {  // identical values from every pass binding the point
         PGeo g;
         point_geometry(M, mp, A.fc.dist_band_slack, g);  // caches valid (k_fuse_refresh)
-        const int j = gather_hit(M, A.fc, g, A.cur, tgt_global(M, A.cur));
+        int border[2] = {0, 0};
+        const int j = gather_hit(M, A.fc, g, A.cur, tgt_global(M, A.cur), border);
         M.hit[mp] = make_int2(M.ver[mp], j);
         const int stag = M.scal[SC_MTAG];
-        if (j >= 0 && atomicExch(&M.s.hreg[mp], stag) != stag) hit_list_add(M, j, mp);
+        // every pass binding the point computes the same (j, border); the first one to
+        // register it lists the hit and counts its borderline compares
+        if ((j >= 0 || (border[0] | border[1])) && atomicExch(&M.s.hreg[mp], stag) != stag) {
+          if (j >= 0) hit_list_add(M, j, mp);
+          if (border[0]) atomicAdd((unsigned long long*)&M.s.stats->borderline[2], (unsigned long long)border[0]);
+          if (border[1]) atomicAdd((unsigned long long*)&M.s.stats->borderline[3], (unsigned long long)border[1]);
+        }
       }
     }
     const ItemVal v = eval_item(M, A.cur, t, ts, kp);
@@ -2342,6 +2413,11 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       alg += a_b;  // (meaningful on thread 0)
       npts += a_p;
       nacts += a_n;
+      {  // one record_small_transfer per reverse pass, in pass order (after the forward one)
+        const unsigned long long ev0 = M.ledger[LG_SMALL_EVENTS];
+        for (int t = t0 + lane; t <= te; t += 32)
+          if (ev0 + t < (unsigned long long)LG_LOG_CAP) M.lg_log[ev0 + t] = (long long)s_live[t] * (long long)mpb;
+      }
       ledger_events += te - t0 + 1;
       int na = 0;
       const int tg = tag_base + 1 + iter;

@@ -39,9 +39,12 @@ constexpr int MATCH_WARPS = LM_MATCH_WARPS;  // warps per match CTA, each scanni
 constexpr int MATCH_JT = 1024;          // neighbour descriptors staged per smem chunk
 constexpr int RES_PAIR = 1 << 20;       // hashed (point, keyframe) reservation keys per map
 constexpr int HL = 16;                  // hit-list entries per current keypoint
+constexpr int LG_LOG_CAP = 1 << 16;     // logged small-transfer events per map
 
 enum KfState { KF_FREE = 0, KF_STAGED = 1, KF_LIVE = 2, KF_DEAD = 3 };
-enum Scal { SC_NEXT_ID = 0, SC_OBS_HEAD, SC_RECENT_N, SC_ERR, SC_DIRTY_N, SC_ROUND, SC_MTAG, SC_N = 8 };
+// SC_ERR: sticky (arena overflow: the map is unusable); SC_SOFT: this step's recoverable
+// contract error (a stage touched a non-resident keyframe), cleared at every step start
+enum Scal { SC_NEXT_ID = 0, SC_OBS_HEAD, SC_RECENT_N, SC_ERR, SC_DIRTY_N, SC_ROUND, SC_MTAG, SC_SOFT, SC_N = 8 };
 enum LedgerIdx { LG_PERSIST = 0, LG_NAIVE, LG_SMALL_TRI, LG_SMALL_FUSE, LG_SMALL_EVENTS, LG_EVICT, LG_N = 8 };
 enum CandStatus { CS_PASS = 0, CS_PARALLAX = 1, CS_DEPTH = 2, CS_REPROJ = 3, CS_SCALE = 4, CS_DEGEN = 5 };
 
@@ -146,6 +149,7 @@ struct DevMap {
   // keyframes
   long long* kf_id;
   int* kf_state;
+  unsigned char* kf_res;  // DeviceStore residency (devicestore.py:62-78): 1 after upload, 0 after evict
   int* kp_off;
   int* kp_n;
   double* q;
@@ -211,6 +215,10 @@ struct DevMap {
   // scalars
   int* scal;
   unsigned long long* ledger;
+  // per_stage_small_transfers (devicestore.py:94-101): bytes of every record_small_transfer
+  // event in order (all are "fusion": one forward pass + one per reverse pass), entry k =
+  // event k; events past LG_LOG_CAP keep counting in the ledger totals only
+  long long* lg_log;
   Scratch s;
 };
 

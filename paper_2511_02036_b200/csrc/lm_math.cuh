@@ -29,6 +29,17 @@ namespace lm {
 constexpr double kBaselineEps = 1e-9;
 constexpr double kHomogEps = 1e-12;
 
+// Borderline-flip detector (north_star: "bit-exact, except borderline float threshold flips,
+// whose count is reported"). The only path values that are not bit-identical to the
+// reference's are the DLT null vector (Jacobi here, LAPACK dgesdd there: positions agree to
+// ~1e-14 relative) and log() in the fusion level prediction (1 ulp class). A threshold
+// compare fed by such a value can only decide differently from the reference when its two
+// sides are closer than that noise, so every compare whose sides lie within kFlipRel of
+// each other (relative to the compare's natural scale) is counted as borderline: an upper
+// bound of the decisions that could flip. 1e-10 is ~10^4 x the measured position noise.
+constexpr double kFlipRel = 1e-10;
+LM_HD int near_tie(double a, double b, double scale) { return fabs(a - b) <= kFlipRel * fabs(scale); }
+
 // rotation matrix (row-major) of a unit quaternion (x, y, z, w)
 LM_HD void quat_to_rot(const double q[4], double R[9]) {
   const double x = q[0], y = q[1], z = q[2], w = q[3];
@@ -206,7 +217,7 @@ LM_HD void null_vector4(double A[16], double v[4]) {
 // Two-view DLT (geometry.py:258-284). Pa/Pb are K[R|t]; Ca/Cb camera centres.
 // Returns false when degenerate (baseline < 1e-9 or point at infinity).
 LM_HD bool triangulate(const double Pa[12], const double Pb[12], const double Ca[3], const double Cb[3],
-                       double ua, double va, double ub, double vb, double X[3]) {
+                       double ua, double va, double ub, double vb, double X[3], int* border = nullptr) {
   const double dx = Ca[0] - Cb[0], dy = Ca[1] - Cb[1], dz = Ca[2] - Cb[2];
   if (sqrt(dx * dx + dy * dy + dz * dz) < kBaselineEps) return false;
   double A[16];
@@ -218,6 +229,7 @@ LM_HD bool triangulate(const double Pa[12], const double Pb[12], const double Ca
   }
   double h[4];
   null_vector4(A, h);
+  if (border) *border += near_tie(fabs(h[3]), kHomogEps, kHomogEps);
   if (fabs(h[3]) < kHomogEps) return false;
   X[0] = h[0] / h[3];
   X[1] = h[1] / h[3];
@@ -239,9 +251,9 @@ struct ViewGeo {
   double sf;        // pyramid scale factor
 };
 
-// check_creation_gates (geometry.py:407-459), first failing gate wins
-LM_HD int creation_gates(const ViewGeo& a, const ViewGeo& b, const double X[3], double cos_max, double chi2_mono,
-                         double slack) {
+// the gates proper; nb_ counts borderline compares
+LM_HD int creation_gates_impl(const ViewGeo& a, const ViewGeo& b, const double X[3], double cos_max,
+                              double chi2_mono, double slack, int& nb_) {
   const double ra0 = X[0] - a.C[0], ra1 = X[1] - a.C[1], ra2 = X[2] - a.C[2];
   const double rb0 = X[0] - b.C[0], rb1 = X[1] - b.C[1], rb2 = X[2] - b.C[2];
   const double na = sqrt(ra0 * ra0 + ra1 * ra1 + ra2 * ra2);
@@ -249,21 +261,25 @@ LM_HD int creation_gates(const ViewGeo& a, const ViewGeo& b, const double X[3], 
   if (na < kHomogEps || nb < kHomogEps) return kGateParallax;
   double c = (ra0 * rb0 + ra1 * rb1 + ra2 * rb2) / (na * nb);
   c = c > 1.0 ? 1.0 : (c < -1.0 ? -1.0 : c);
+  nb_ += near_tie(c, cos_max, 1.0);
   if (!(c < cos_max)) return kGateParallax;
   double pa[3], pb[3];
   rot_apply(a.R, X[0], X[1], X[2], pa);
   pa[0] = pa[0] + a.t[0]; pa[1] = pa[1] + a.t[1]; pa[2] = pa[2] + a.t[2];
   rot_apply(b.R, X[0], X[1], X[2], pb);
   pb[0] = pb[0] + b.t[0]; pb[1] = pb[1] + b.t[1]; pb[2] = pb[2] + b.t[2];
+  nb_ += near_tie(pa[2], 0.0, na) + near_tie(pb[2], 0.0, nb);
   if (pa[2] <= 0 || pb[2] <= 0) return kGateDepth;
   {
     const double u = a.fx * (pa[0] / pa[2]) + a.cx, v = a.fy * (pa[1] / pa[2]) + a.cy;
     const double eu = u - a.u, ev = v - a.v;
+    nb_ += near_tie(eu * eu + ev * ev, chi2_mono * a.sigma2, chi2_mono * a.sigma2);
     if (eu * eu + ev * ev > chi2_mono * a.sigma2) return kGateReproj;
   }
   {
     const double u = b.fx * (pb[0] / pb[2]) + b.cx, v = b.fy * (pb[1] / pb[2]) + b.cy;
     const double eu = u - b.u, ev = v - b.v;
+    nb_ += near_tie(eu * eu + ev * ev, chi2_mono * b.sigma2, chi2_mono * b.sigma2);
     if (eu * eu + ev * ev > chi2_mono * b.sigma2) return kGateReproj;
   }
   const double da = sqrt(ra0 * ra0 + ra1 * ra1 + ra2 * ra2);
@@ -272,8 +288,20 @@ LM_HD int creation_gates(const ViewGeo& a, const ViewGeo& b, const double X[3], 
   const double rd = da / db;
   const double rs = a.scale / b.scale;
   const double sl = slack * (a.sf > b.sf ? a.sf : b.sf);
+  nb_ += near_tie(rd, rs / sl, rd) + near_tie(rd, rs * sl, rd);
   if (!(rs / sl <= rd && rd <= rs * sl)) return kGateScale;
   return kGatePass;
+}
+
+// check_creation_gates (geometry.py:407-459), first failing gate wins. border (optional)
+// counts the evaluated compares that are borderline (near_tie): the decision up to and
+// including the first failing gate is what the reference's could differ on.
+LM_HD int creation_gates(const ViewGeo& a, const ViewGeo& b, const double X[3], double cos_max, double chi2_mono,
+                         double slack, int* border = nullptr) {
+  int nb_ = 0;
+  const int r_ = creation_gates_impl(a, b, X, cos_max, chi2_mono, slack, nb_);
+  if (border) *border += nb_;
+  return r_;
 }
 
 }  // namespace lm

@@ -1,18 +1,26 @@
-"""Device-backed map with the reference's MapModel interface.
+"""Device-backed map with the reference's MapModel interface, and the DeviceStore /
+TransferLedger of the persistent keyframe store as views of the device ledger.
 
-The state lives on the GPU (csrc/lm_map.cuh); this class is the host handle. Reads
-(``keyframes``, ``points``, ``graph``, ``counter_matrix``, ``audit``) come from a state
-export that is refreshed lazily after any mutation; mutations are single-op kernels that
-run the same device code as the hot-path stages. Mirrors
-pkg/src/localmap/mapmodel.py (KeyFrame 24-62, MapPoint 65-77, CovisibilityGraph 80-110,
-MapModel 113-353) and devicestore.py (TransferLedger 25-48, DeviceStore 51-109).
+The state lives on the GPU (csrc/lm_map.cuh); this module is the host handle. Every read
+costs O(what it returns), never a whole-map export, except the reads that are O(map) in the
+reference too (``live_points``, ``counter_matrix``, ``audit``, iterating ``points``):
+  * ``keyframes[k]`` refreshes that keyframe's ``mp_bindings`` (one D2H of its slots) only
+    when the map changed since it was last read; keyframe liveness is tracked host-side;
+  * ``points[i]`` / ``points.get(i)`` export one point record (lm_mp_get), cached until the
+    next mutation;
+  * ``graph`` reads one covisibility row (lm_covis_row); ``bound_points_of`` is a device
+    compaction (lm_bound_points).
+Mutations are single-op kernels that run the same device code as the hot-path stages.
+Mirrors pkg/src/localmap/mapmodel.py (KeyFrame 24-62, MapPoint 65-77, CovisibilityGraph
+80-110, MapModel 113-353) and devicestore.py (TransferLedger 25-48, DeviceStore 51-109).
 """
 
 from __future__ import annotations
 
 import ctypes as C
+import weakref
+from collections.abc import Mapping
 from dataclasses import dataclass, field
-from itertools import combinations
 
 import numpy as np
 
@@ -219,27 +227,81 @@ def create_map(ctx: Context, num_levels: int, scale_factor: float, store: StoreC
 
 
 class CovisibilityView:
-    """Read view of the device covisibility matrix with the reference graph's queries."""
+    """Read view of the device covisibility matrix with CovisibilityGraph's queries
+    (mapmodel.py:80-110): one row per call."""
 
     def __init__(self, model: "MapModel"):
         self._m = model
 
+    def _row(self, kf_id: int) -> list[tuple[int, int]]:
+        m = self._m
+        if kf_id not in m._kfs:
+            return []
+        cap = max(16, len(m._kfs))
+        ids = np.zeros(cap, np.int64)
+        w = np.zeros(cap, np.int32)
+        n = C.c_int32()
+        m.ctx.call("lm_covis_row", m.map, int(kf_id), ptr(ids, C.c_int64), ptr(w, C.c_int32), cap, C.byref(n))
+        return [(int(ids[k]), int(w[k])) for k in range(n.value)]
+
     def weight(self, a: int, b: int) -> int:
-        s = self._m._snapshot()
-        so = s.slot_of()
-        if a not in so or b not in so:
-            return 0
-        return int(s.covis[so[a], so[b]])
+        return dict(self._row(a)).get(b, 0)
 
     def neighbors(self, kf_id: int, min_weight: int = 1) -> list[tuple[int, int]]:
-        s = self._m._snapshot()
-        so = s.slot_of()
-        if kf_id not in so:
-            return []
-        row = s.covis[so[kf_id]]
-        items = [(int(s.kf_ids[t]), int(row[t])) for t in range(len(s.kf_ids)) if row[t] >= min_weight and row[t] > 0]
+        items = [(k, w) for k, w in self._row(kf_id) if w >= min_weight]
         items.sort(key=lambda p: (-p[1], p[0]))
         return items
+
+
+class KeyframeTable(Mapping):
+    """``MapModel.keyframes``: the caller's KeyFrame objects, each one's ``mp_bindings``
+    brought up to date (one keyframe's slots, D2H) when the map changed since its last read."""
+
+    def __init__(self, model: "MapModel"):
+        self._m = model
+
+    def __getitem__(self, kf_id):
+        kf = self._m._kfs[kf_id]
+        self._m._sync_bindings(kf)
+        return kf
+
+    def __iter__(self):
+        return iter(self._m._kfs)
+
+    def __len__(self):
+        return len(self._m._kfs)
+
+    def __contains__(self, kf_id):
+        return kf_id in self._m._kfs
+
+
+class PointTable(Mapping):
+    """``MapModel.points``: id -> MapPoint snapshot (dead points included, like the
+    reference's dict). Single lookups export one record; iteration exports the map."""
+
+    def __init__(self, model: "MapModel"):
+        self._m = model
+
+    def __getitem__(self, mp_id):
+        m = self._m
+        if not isinstance(mp_id, (int, np.integer)) or not 0 <= int(mp_id) < m._next_id():
+            raise KeyError(mp_id)
+        return m._point(int(mp_id))
+
+    def __iter__(self):
+        return iter(range(self._m._next_id()))
+
+    def __len__(self):
+        return self._m._next_id()
+
+    def __contains__(self, mp_id):
+        return isinstance(mp_id, (int, np.integer)) and 0 <= int(mp_id) < self._m._next_id()
+
+    def values(self):
+        return self._m._all_points()
+
+    def items(self):
+        return [(p.mp_id, p) for p in self._m._all_points()]
 
 
 class MapModel:
@@ -254,31 +316,79 @@ class MapModel:
         self.ctx = Context.get(device)
         self.map = create_map(self.ctx, num_levels, scale_factor, self.store_config, self.config)
         self._kfs: dict[int, KeyFrame] = {}
+        self._kf_seen: dict[int, int] = {}  # kf id -> map version its bindings were read at
         self._version = 0
         self._snap = None
         self._snap_version = -1
+        self._cache_version = -1
+        self._cache: dict[int, MapPoint] = {}
+        self._n_points = 0
 
     # ------------------------------------------------------------------ plumbing
     def _call(self, name, *args):
+        self._version += 1  # even a failing call may have changed the map
         self.ctx.call(name, *args)
-        self._version += 1
-
-    def _snapshot(self) -> MapSnapshot:
-        if self._snap_version != self._version:
-            self._snap = export_snapshot(self.ctx, self.map)
-            self._snap_version = self._version
-            so = self._snap.slot_of()
-            for k, kf in self._kfs.items():
-                s = so[k]
-                kf.mp_bindings[:] = self._snap.kf_bindings(s)
-                kf.alive = int(self._snap.kf_state[s]) == 2
-        return self._snap
 
     def invalidate(self):
         self._version += 1
 
+    def _fresh(self):
+        if self._cache_version != self._version:
+            self._cache.clear()
+            sizes = _lib.MapSizes()
+            check(self.ctx.lib.lm_map_sizes_get(self.ctx.h, self.map, C.byref(sizes)), self.ctx.h)
+            self._n_points = sizes.n_points
+            self._cache_version = self._version
+
+    def _next_id(self) -> int:
+        self._fresh()
+        return self._n_points
+
+    def _snapshot(self) -> MapSnapshot:
+        """Whole-map export (audit, iteration): O(map), cached until the next mutation."""
+        if self._snap_version != self._version:
+            self._snap = export_snapshot(self.ctx, self.map)
+            self._snap_version = self._version
+        return self._snap
+
+    def _sync_bindings(self, kf):
+        if self._kf_seen.get(kf.kf_id) == self._version:
+            return
+        n = kf.num_keypoints
+        buf = np.zeros(max(n, 1), np.int64)
+        got = C.c_int32()
+        self.ctx.call("lm_kf_bindings", self.map, int(kf.kf_id), ptr(buf, C.c_int64), len(buf), C.byref(got))
+        kf.mp_bindings[:] = buf[:n]
+        self._kf_seen[kf.kf_id] = self._version
+
+    def _point(self, mp_id: int) -> MapPoint:
+        self._fresh()
+        p = self._cache.get(mp_id)
+        if p is None:
+            rec = _lib.PointRecord()
+            cap = max(16, len(self._kfs))
+            okf = np.zeros(cap, np.int64)
+            okp = np.zeros(cap, np.int32)
+            self.ctx.call("lm_mp_get", self.map, mp_id, C.byref(rec), ptr(okf, C.c_int64), ptr(okp, C.c_int32), cap)
+            n = rec.nobs
+            p = MapPoint(mp_id, np.array(rec.pos[:], np.float64), np.frombuffer(bytes(rec.rep), np.uint8).copy(),
+                         int(rec.first_kf_id), {int(okf[k]): int(okp[k]) for k in range(n)}, int(rec.found),
+                         int(rec.visible), bool(rec.alive), np.array(rec.counts[:self.num_levels], np.int64))
+            self._cache[mp_id] = p
+        return p
+
+    def _all_points(self) -> list[MapPoint]:
+        s = self._snapshot()
+        obs = s.observations()
+        first = [-1] * len(s.alive)
+        return [MapPoint(i, s.pos[i].copy(), s.rep[i].copy(), first[i], obs[i], int(s.found[i]), int(s.visible[i]),
+                         bool(s.alive[i]), s.counts[i].astype(np.int64)) for i in range(len(s.alive))]
+
     # ------------------------------------------------------------------ keyframes
-    def insert_keyframe(self, kf: KeyFrame) -> int:
+    def insert_keyframe(self, kf) -> int:
+        """insert_keyframe (mapmodel.py:185-199): pre-bound slots become observations. Any
+        KeyFrame-shaped object works (this package's or the reference's). Residency and the
+        upload ledger entry belong to the store (DeviceStore.upload_keyframe)."""
         if kf.kf_id in self._kfs:
             raise InvalidArgumentError(f"duplicate keyframe id {kf.kf_id}")
         k = kf.intrinsics
@@ -287,41 +397,53 @@ class MapModel:
         stage_keyframe(self.ctx, self.map, kf)
         self._call("lm_kf_insert", self.map, int(kf.kf_id))
         self._kfs[kf.kf_id] = kf
+        kf.alive = True
+        _HOME[id(kf)] = (weakref.ref(self), kf.kf_id)
         return kf.kf_id
 
     @property
-    def keyframes(self) -> dict:
-        self._snapshot()
-        return self._kfs
+    def keyframes(self) -> KeyframeTable:
+        return KeyframeTable(self)
 
     def kill_keyframe(self, kf_id: int):
         self._require_kf(kf_id)
         self._call("lm_kf_kill", self.map, int(kf_id))
+        self._kfs[kf_id].alive = False
 
-    def live_keyframes(self) -> list[KeyFrame]:
-        return [kf for kf in self.keyframes.values() if kf.alive]
+    def live_keyframes(self) -> list:
+        return [self.keyframes[k] for k, kf in self._kfs.items() if kf.alive]
 
     def _require_kf(self, kf_id):
-        kf = self.keyframes.get(kf_id)
+        kf = self._kfs.get(kf_id)
         if kf is None:
             raise InvalidArgumentError(f"unknown keyframe {kf_id}")
         if not kf.alive:
             raise InvalidStateError(f"keyframe {kf_id} is dead")
         return kf
 
+    def set_pose(self, kf_id: int, pose: SE3Pose):
+        """LBA pose write-back (localba.py:571-574 assigns kf.pose): device tables follow."""
+        kf = self._kfs.get(kf_id)
+        if kf is None:
+            raise InvalidArgumentError(f"unknown keyframe {kf_id}")
+        q = np.ascontiguousarray(pose.quat, dtype=np.float64)
+        t = np.ascontiguousarray(pose.trans, dtype=np.float64)
+        self._call("lm_kf_set_pose", self.map, int(kf_id), ptr(q, C.c_double), ptr(t, C.c_double))
+        kf.pose = pose
+
+    def patch_positions(self, ids, positions):
+        """LBA position write-back (localba.py:571-574 assigns mp.position), batched."""
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        pos = np.ascontiguousarray(positions, dtype=np.float64).reshape(len(ids), 3)
+        self._call("lm_mp_patch_positions", self.map, len(ids), ptr(ids, C.c_int64), ptr(pos, C.c_double))
+
     # ------------------------------------------------------------------ points
     @property
-    def points(self) -> dict:
-        s = self._snapshot()
-        obs = s.observations()
-        out = {}
-        for i in range(len(s.alive)):
-            out[i] = MapPoint(i, s.pos[i].copy(), s.rep[i].copy(), -1, obs[i], int(s.found[i]), int(s.visible[i]),
-                              bool(s.alive[i]), s.counts[i].astype(np.int64))
-        return out
+    def points(self) -> PointTable:
+        return PointTable(self)
 
     def live_points(self) -> list[MapPoint]:
-        return [p for p in self.points.values() if p.alive]
+        return [p for p in self._all_points() if p.alive]
 
     @property
     def counter_matrix(self) -> np.ndarray:
@@ -335,8 +457,7 @@ class MapModel:
         return self.points[out.value]
 
     def add_observation(self, mp_id: int, kf_id: int, kp_index: int):
-        if kf_id not in self._kfs:
-            raise InvalidArgumentError(f"unknown keyframe {kf_id}")
+        self._require_kf(kf_id)
         self._call("lm_obs_add", self.map, int(mp_id), int(kf_id), int(kp_index))
 
     def erase_observation(self, mp_id: int, kf_id: int):
@@ -360,57 +481,43 @@ class MapModel:
 
     def covisible_neighbors(self, kf_id: int, n: int | None = None) -> list[int]:
         self._require_kf(kf_id)
-        buf = np.zeros(1024, np.int64)
+        buf = np.zeros(max(1024, len(self._kfs)), np.int64)
         got = C.c_int32()
         self.ctx.call("lm_covisible_neighbors", self.map, int(kf_id), -1 if n is None else int(n),
                       ptr(buf, C.c_int64), len(buf), C.byref(got))
         return [int(x) for x in buf[:got.value]]
 
     def bound_points_of(self, kf_id: int) -> list[int]:
-        s = self._snapshot()
-        b = s.kf_bindings(s.slot_of()[kf_id])
-        return [int(m) for m in b if m != UNBOUND and s.alive[m]]
+        if kf_id not in self._kfs:
+            raise KeyError(kf_id)
+        n = self._kfs[kf_id].num_keypoints
+        buf = np.zeros(max(n, 1), np.int64)
+        got = C.c_int32()
+        self.ctx.call("lm_bound_points", self.map, int(kf_id), ptr(buf, C.c_int64), len(buf), C.byref(got))
+        return [int(x) for x in buf[:got.value]]
 
     def audit(self) -> list[str]:
-        """Brute-force recheck of counters, weights and binding bijectivity (mapmodel.py:304-353)."""
-        s = self._snapshot()
-        bad = []
-        obs = s.observations()
-        so = s.slot_of()
-        for i in range(len(s.alive)):
-            if not s.alive[i]:
-                if obs[i]:
-                    bad.append(f"dead map point {i} retains observations")
-                continue
-            exp = np.zeros(self.num_levels, np.int64)
-            for k, kp in obs[i].items():
-                st = so[k]
-                if s.kf_state[st] != 2:
-                    bad.append(f"map point {i} observes dead keyframe {k}")
-                    continue
-                if s.kf_bindings(st)[kp] != i:
-                    bad.append(f"binding mismatch: map point {i} vs slot ({k}, {kp})")
-                exp[int(self._kfs[k].kp_level[kp])] += 1
-            if not np.array_equal(exp, s.counts[i].astype(np.int64)):
-                bad.append(f"scale_counts mismatch for map point {i}")
-        live = sorted(k for k, st in so.items() if s.kf_state[st] == 2)
-        bound = {}
-        for k in live:
-            b = s.kf_bindings(so[k])
-            for kp in np.flatnonzero(b != UNBOUND):
-                m = int(b[kp])
-                if m >= len(s.alive) or not s.alive[m]:
-                    bad.append(f"slot ({k}, {int(kp)}) bound to dead point {m}")
-                elif obs[m].get(k) != int(kp):
-                    bad.append(f"slot ({k}, {int(kp)}) not in map point {m} observations")
-            bound[k] = {int(m) for m in b if m != UNBOUND and m < len(s.alive) and s.alive[m]}
-        for a, b in combinations(live, 2):
-            if len(bound[a] & bound[b]) != int(s.covis[so[a], so[b]]):
-                bad.append(f"covisibility weight mismatch for pair ({a}, {b})")
-        return bad
+        """Brute-force recheck of counters, weights and binding bijectivity (mapmodel.py:304-353),
+        run on the device (lm_audit); violations formatted like the reference's."""
+        from .audit import device_audit
+
+        return device_audit(self)
+
+    # ------------------------------------------------------------------ snapshots
+    def import_reference(self, ref_model, ref_store=None, recent=None):
+        """Load a reference MapModel's state (plus its DeviceStore residency and ledger, and
+        the pipeline's probation list) into this empty device map (lm_import_snapshot)."""
+        from .snapshot import import_reference
+
+        import_reference(self, ref_model, ref_store, recent)
 
 
-# ---------------------------------------------------------------------- ledger (host model)
+# keyframe object -> (model, kf id): lets a DeviceStore find the device map a keyframe was
+# inserted into (the reference pipeline creates the model and the store independently)
+_HOME: dict[int, tuple] = {}
+
+
+# ---------------------------------------------------------------------- store (device ledger views)
 
 
 @dataclass
@@ -420,72 +527,143 @@ class StoredKeyFrame:
     resident: bool = True
 
 
-@dataclass
 class TransferLedger:
-    persistent_bytes_up: int = 0
-    naive_bytes_up: int = 0
-    per_stage_small_transfers: list = field(default_factory=list)
-    evictions: int = 0
+    """TransferLedger (devicestore.py:25-48) read from the device ledger (lm_ledger,
+    lm_ledger_log): the kernels account every upload, neighbour access and small transfer."""
+
+    def __init__(self, store: "DeviceStore"):
+        self._s = store
+
+    def _raw(self) -> _lib.Ledger:
+        lg = _lib.Ledger()
+        m = self._s._model
+        if m is not None:
+            m.ctx.call("lm_ledger", m.map, C.byref(lg))
+        return lg
+
+    @property
+    def persistent_bytes_up(self) -> int:
+        return int(self._raw().persistent_bytes_up)
+
+    @property
+    def naive_bytes_up(self) -> int:
+        return int(self._raw().naive_bytes_up)
+
+    @property
+    def evictions(self) -> int:
+        return int(self._raw().evictions)
+
+    @property
+    def per_stage_small_transfers(self) -> list[tuple[str, int]]:
+        m = self._s._model
+        if m is None:
+            return []
+        n = int(self._raw().small_transfer_events)
+        buf = np.zeros(max(n, 1), np.int64)
+        got = C.c_int32()
+        m.ctx.call("lm_ledger_log", m.map, 0, ptr(buf, C.c_int64), len(buf), C.byref(got))
+        return [("triangulation", -int(b) - 1) if b < 0 else ("fusion", int(b)) for b in buf[:got.value]]
 
     def as_dict(self) -> dict:
-        small: dict[str, int] = {}
-        for stage, nbytes in self.per_stage_small_transfers:
-            small[stage] = small.get(stage, 0) + nbytes
-        ratio = self.naive_bytes_up / self.persistent_bytes_up if self.persistent_bytes_up > 0 else 0.0
-        return {"persistent_bytes_up": self.persistent_bytes_up, "naive_bytes_up": self.naive_bytes_up,
-                "naive_over_persistent": ratio, "small_transfer_bytes_by_stage": small,
-                "small_transfer_events": len(self.per_stage_small_transfers), "evictions": self.evictions}
+        lg = self._raw()
+        small = {}
+        if lg.small_bytes_triangulation:
+            small["triangulation"] = int(lg.small_bytes_triangulation)
+        if lg.small_bytes_fusion or lg.small_transfer_events:
+            small["fusion"] = int(lg.small_bytes_fusion)
+        p, nv = int(lg.persistent_bytes_up), int(lg.naive_bytes_up)
+        return {"persistent_bytes_up": p, "naive_bytes_up": nv, "naive_over_persistent": nv / p if p > 0 else 0.0,
+                "small_transfer_bytes_by_stage": small, "small_transfer_events": int(lg.small_transfer_events),
+                "evictions": int(lg.evictions)}
 
 
 class DeviceStore:
-    """Transfer ledger of the persistent keyframe store (devicestore.py:51-109 semantics)."""
+    """DeviceStore (devicestore.py:51-109) over the device map that holds the keyframes:
+    residency is the map's per-slot flag, the ledger is the one the kernels keep. It binds
+    to the MapModel its first uploaded keyframe was inserted into; a keyframe that is in no
+    map is staged into a private ledger-only device map."""
 
-    def __init__(self, config: StoreConfig | None = None):
+    def __init__(self, config: StoreConfig | None = None, model: MapModel | None = None):
         self.config = config or StoreConfig()
-        self.ledger = TransferLedger()
-        self._stored: dict[int, StoredKeyFrame] = {}
+        self._model = model
+        self.ledger = TransferLedger(self)
 
-    def payload_bytes(self, n: int) -> int:
-        return n * self.config.keypoint_record_bytes + n * self.config.descriptor_bytes
+    def _bind(self, kf) -> MapModel:
+        home = _HOME.get(id(kf))
+        m = home[0]() if home and home[1] == kf.kf_id else None
+        if m is None:  # not in any map: the store's own device map
+            if self._model is None:
+                k = kf.intrinsics
+                self._model = MapModel(k.num_levels, scale_factor=k.scale_factor, store=StoreConfig(
+                    capacity=self.config.capacity, max_keyframes=min(4096, max(16, self.config.capacity + 8)),
+                    max_points=16, obs_pool_entries=64, max_keypoints=1 << 22,
+                    max_keypoints_per_kf=max(8192, kf.num_keypoints)))
+            m = self._model
+            if kf.kf_id not in m._kfs:
+                m.insert_keyframe(kf)
+        if self._model is None:
+            self._model = m
+        elif self._model is not m:
+            raise InvalidArgumentError(f"keyframe {kf.kf_id} belongs to another map than this store's")
+        return m
+
+    def payload_bytes(self, num_keypoints: int) -> int:
+        return num_keypoints * self.config.keypoint_record_bytes + num_keypoints * self.config.descriptor_bytes
+
+    def _resident(self, kf_id: int) -> tuple[bool, int]:
+        if self._model is None:
+            return False, 0
+        r, n = C.c_int32(), C.c_int32()
+        self._model.ctx.call("lm_kf_resident", self._model.map, int(kf_id), C.byref(r), C.byref(n))
+        return bool(r.value), int(n.value)
 
     def is_resident(self, kf_id: int) -> bool:
-        e = self._stored.get(kf_id)
-        return e is not None and e.resident
+        return self._resident(kf_id)[0]
 
     def resident_count(self) -> int:
-        return sum(1 for e in self._stored.values() if e.resident)
+        return self._resident(-1)[1]
 
-    def upload_keyframe(self, kf: KeyFrame) -> StoredKeyFrame:
-        if self.is_resident(kf.kf_id):
+    def upload_keyframe(self, kf) -> StoredKeyFrame:
+        m = self._bind(kf)
+        res, count = self._resident(kf.kf_id)
+        if res:
             raise InvalidStateError(f"keyframe {kf.kf_id} already resident")
-        if self.resident_count() >= self.config.capacity:
+        if count >= self.config.capacity:
             raise StoreCapacityError(f"store capacity {self.config.capacity} exceeded; size the pre-allocation")
-        e = StoredKeyFrame(kf.kf_id, self.payload_bytes(kf.num_keypoints))
-        self._stored[kf.kf_id] = e
-        self.ledger.persistent_bytes_up += e.payload_bytes
-        return e
+        m._call("lm_kf_upload", m.map, int(kf.kf_id))
+        return StoredKeyFrame(kf.kf_id, self.payload_bytes(kf.num_keypoints))
 
     def record_neighbor_access(self, stage: str, neighbor_ids) -> int:
+        """Explicit access accounting (the device stages account their own accesses)."""
+        m = self._model
         delta = 0
         for k in neighbor_ids:
-            e = self._stored.get(k)
-            if e is None or not e.resident:
+            if m is None or not self.is_resident(k):
                 raise InvalidStateError(f"stage {stage!r} accessed non-resident keyframe {k}")
-            delta += e.payload_bytes
-        self.ledger.naive_bytes_up += delta
+            delta += self.payload_bytes(m._kfs[k].num_keypoints)
+        if delta:
+            _ledger_add(m, naive=delta)
         return delta
 
     def record_small_transfer(self, stage: str, nbytes: int):
         if nbytes < 0:
             raise InvalidArgumentError("transfer size must be non-negative")
-        self.ledger.per_stage_small_transfers.append((stage, nbytes))
-        self.ledger.persistent_bytes_up += nbytes
-        self.ledger.naive_bytes_up += nbytes
+        if stage not in ("fusion", "triangulation"):
+            raise InvalidArgumentError(f"the device ledger keeps stages 'fusion' and 'triangulation', not {stage!r}")
+        if self._model is None:
+            raise InvalidStateError("store has no device map yet (upload a keyframe first)")
+        _ledger_add(self._model, small=(stage, nbytes))
 
     def evict_keyframe(self, kf_id: int) -> StoredKeyFrame:
-        e = self._stored.get(kf_id)
-        if e is None or not e.resident:
+        m = self._model
+        if m is None or not self.is_resident(kf_id):
             raise InvalidArgumentError(f"keyframe {kf_id} is not resident")
-        e.resident = False
-        self.ledger.evictions += 1
-        return e
+        m._call("lm_kf_evict", m.map, int(kf_id))
+        kf = m._kfs.get(kf_id)
+        return StoredKeyFrame(kf_id, self.payload_bytes(kf.num_keypoints) if kf is not None else 0, False)
+
+
+def _ledger_add(m: MapModel, naive: int = 0, small: tuple | None = None):
+    """Host-initiated ledger entries (explicit record_* calls): one device ledger update."""
+    m.ctx.call("lm_ledger_add", m.map, int(naive), 1 if small and small[0] == "triangulation" else 0,
+               int(small[1]) if small else 0, 1 if small else 0)

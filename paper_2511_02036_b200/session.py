@@ -128,6 +128,15 @@ class LocalMapper:
     def snapshot(self, with_covis: bool = True) -> MapSnapshot:
         return export_snapshot(self.ctx, self.map, with_covis)
 
+    def totals(self) -> _lib.StepStats:
+        """Running totals on the device since creation / reset / rewind (lm_totals_fetch);
+        first_new_id holds the number of steps accumulated. Covers async steps too."""
+        st = _lib.StepStats()
+        self.ctx.call("lm_totals_fetch", self.map, C.byref(st))
+        if st.error:
+            _lib.check(int(st.error))
+        return st
+
     def ledger(self) -> dict:
         lg = _lib.Ledger()
         self.ctx.call("lm_ledger", self.map, C.byref(lg))
@@ -148,6 +157,8 @@ class SessionBatch:
     def __init__(self, mappers: list[LocalMapper]):
         if len({id(m.ctx) for m in mappers}) != 1:
             raise ValueError("all sessions of a batch must share one context")
+        if len({m.map for m in mappers}) != len(mappers):
+            raise ValueError("a map may appear only once in a batch")
         self.mappers = mappers
         self.ctx = mappers[0].ctx
         self._maps = (C.c_int32 * len(mappers))(*[m.map for m in mappers])
