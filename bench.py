@@ -202,6 +202,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=1, help="separate per-stage profiling pass")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-api", action="store_true", help="skip the Python-API e2e variant")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -409,6 +410,13 @@ def main():
                           "h2d_bytes_per_step": sum(len(r) for r in recs), "d2h_bytes_per_step": d2h,
                           "timing": "wall clock: lm_kf_stage_record (LMKF wire records) + lm_step + stats readback"}
 
+    # -------- end to end through the reference-shaped Python API (the drop-in a user of the
+    # reference calls): per keyframe MapModel.insert_keyframe (H2D) +
+    # DeviceStore.upload_keyframe + cull_recent_map_points + create_map_points + run_fusion
+    # (each call returns its result to the host, as the reference's functions do)
+    if e2e is not None and not args.no_api:
+        e2e["api"] = api_e2e(args, kfs, intr, n, mc, fc, total_kf, barrier, max_over_ranks)
+
     # -------- roofline of the dominant kernel (k_fuse_rev), the whole fusion stage, and the
     # matching kernel's popc roofline. Achieved = algorithmic work per launch (SURVEY.md 8(d),
     # counted on the device from the inputs) / the kernel's average launch time (CUDA events
@@ -508,6 +516,54 @@ def main():
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def api_e2e(args, kfs, intr, n, mc, fc, total_kf, barrier, max_over_ranks) -> dict:
+    from paper_2511_02036_b200.config import CullConfig, GateConfig
+    from paper_2511_02036_b200.culling import RecentPoint, cull_recent_map_points
+    from paper_2511_02036_b200.fusion import run_fusion
+    from paper_2511_02036_b200.mapmodel import DeviceStore, MapModel
+    from paper_2511_02036_b200.session import store_for
+    from paper_2511_02036_b200.triangulation import CreationStats, create_map_points
+
+    model = MapModel(intr.num_levels, scale_factor=intr.scale_factor,
+                     store=store_for(len(kfs), max(k.num_keypoints for k in kfs) + 64))
+    gc, cc = GateConfig(), CullConfig()
+    ms = []
+    stage_ms = 0.0
+    for it in range(args.warmup + args.steps):
+        model.reset()
+        store = DeviceStore(model=model)
+        stats = CreationStats()
+        fused = {"merged": 0, "observations_added": 0, "stale": 0}
+        recent = []
+        barrier()
+        t0 = time.perf_counter()
+        t_stage = 0.0
+        for processed, kf in enumerate(kfs):
+            kf.mp_bindings[:] = -1
+            model.insert_keyframe(kf)
+            store.upload_keyframe(kf)
+            _, recent = cull_recent_map_points(model, recent, processed, cc)
+            ts = time.perf_counter()
+            made = create_map_points(model, store, kf.kf_id, n, mc, gc, stats=stats)
+            recent.extend(RecentPoint(i, processed) for i in made)
+            for k, v in run_fusion(model, store, kf.kf_id, fc).items():
+                fused[k] += v
+            t_stage += time.perf_counter() - ts
+        dt = (time.perf_counter() - t0) * 1e3
+        if it >= args.warmup:
+            ms.append(max_over_ranks(dt))
+            stage_ms += t_stage * 1e3
+    timed = len(ms)
+    h2d = sum(k.num_keypoints * (8 + 8 + 32 + 4 + 1) + 208 for k in kfs)
+    return {"value": total_kf / (sum(ms) / timed * 1e-3), "unit": UNIT, "ms_per_step": sum(ms) / timed,
+            "stage_only_keyframes_per_s": total_kf / (stage_ms / timed * 1e-3),
+            "h2d_bytes_per_step": h2d, "created": stats.created, "fusion": fused,
+            "timing": "wall clock per sequence through the reference-shaped Python API: per keyframe "
+                      "MapModel.insert_keyframe (H2D) + DeviceStore.upload_keyframe + cull_recent_map_points + "
+                      "create_map_points + run_fusion, each returning its result (D2H); stage_only = the "
+                      "create_map_points + run_fusion calls alone (the reference's StageTimings window)"}
 
 
 def golden_parity(args, seed, mapper, ids):

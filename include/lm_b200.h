@@ -262,6 +262,9 @@ int lm_ledger_log(lm_ctx* ctx, int32_t map, int64_t first, int64_t* bytes, int32
 int lm_kf_upload(lm_ctx* ctx, int32_t map, int64_t kf_id);
 int lm_kf_evict(lm_ctx* ctx, int32_t map, int64_t kf_id);
 int lm_kf_resident(lm_ctx* ctx, int32_t map, int64_t kf_id, int32_t* resident, int32_t* count);
+/* enforce = 0: the stages skip the residency check (the caller accounts residency in a store
+ * of its own, e.g. the reference's DeviceStore); default 1 */
+int lm_map_enforce_residency(lm_ctx* ctx, int32_t map, int32_t enforce);
 
 /* ---- LBA write-back (localba.py:571-574 writes kf.pose and mp.position) ----
  * Poses and positions changed outside the hot path: the keyframe's R, t, C, P tables are
@@ -282,6 +285,7 @@ typedef struct lm_point_record { /* MapPoint mapmodel.py:65-77 */
 int lm_mp_get(lm_ctx* ctx, int32_t map, int64_t mp, lm_point_record* out, int64_t* obs_kf, int32_t* obs_kp,
               int32_t obs_cap);
 int lm_kf_bindings(lm_ctx* ctx, int32_t map, int64_t kf_id, int64_t* out, int32_t cap, int32_t* n_out);
+int lm_mp_alive(lm_ctx* ctx, int32_t map, int32_t n, const int64_t* ids, uint8_t* out); /* MapPoint.alive of n ids */
 int lm_bound_points(lm_ctx* ctx, int32_t map, int64_t kf_id, int64_t* out, int32_t cap, int32_t* n_out);
 /* nonzero covisibility entries of one keyframe (any order): CovisibilityGraph adjacency */
 int lm_covis_row(lm_ctx* ctx, int32_t map, int64_t kf_id, int64_t* kf_ids, int32_t* weights, int32_t cap,
@@ -330,6 +334,9 @@ typedef struct lm_audit_record {
   int64_t mp, kf_a, kf_b;
 } lm_audit_record;
 int lm_audit(lm_ctx* ctx, int32_t map, lm_audit_record* out, int32_t cap, int32_t* n_out);
+/* fault injection for audit tests: what 0 = counter cell (mp a, level b) += delta; what 1 =
+ * covisibility (kf a, kf b) += delta, both directions (CovisibilityGraph.bump) */
+int lm_debug_corrupt(lm_ctx* ctx, int32_t map, int32_t what, int64_t a, int64_t b, int32_t delta);
 
 /* ---- state export (parity, snapshots) ---- */
 /* keyframe table: per slot kf_id, state (1 staged, 2 live, 3 dead), kp_off, kp_n */

@@ -293,6 +293,17 @@ class OracleMap:
         lo.alive = False
         self.refresh_rep(wi)
 
+    def kill_keyframe(self, kf_id):
+        """mapmodel.py:275-283 (+ CovisibilityGraph.drop_keyframe 107-110)."""
+        kf = self.kfs[kf_id]
+        for mp_id in sorted(set(int(m) for m in kf.bind if m != UNBOUND)):
+            p = self.pts[mp_id]
+            if p.alive and kf_id in p.obs:
+                self.erase_obs(mp_id, kf_id)
+        kf.alive = False
+        for other in self.adj.pop(kf_id, {}):
+            self.adj.get(other, {}).pop(kf_id, None)
+
     def bound_points(self, kf_id):
         out = []
         for m in self.kfs[kf_id].bind:

@@ -147,12 +147,15 @@ _SIGS = {
     "lm_ledger_log": ([C.c_void_p, i32, i64, P(i64), i32, P(i32)], i32),
     "lm_ledger_add": ([C.c_void_p, i32, i64, i32, i64, i32], i32),
     "lm_audit": ([C.c_void_p, i32, P(AuditRecord), i32, P(i32)], i32),
+    "lm_debug_corrupt": ([C.c_void_p, i32, i32, i64, i64, i32], i32),
     "lm_kf_upload": ([C.c_void_p, i32, i64], i32),
     "lm_kf_evict": ([C.c_void_p, i32, i64], i32),
     "lm_kf_resident": ([C.c_void_p, i32, i64, P(i32), P(i32)], i32),
+    "lm_map_enforce_residency": ([C.c_void_p, i32, i32], i32),
     "lm_kf_set_pose": ([C.c_void_p, i32, i64, P(f64), P(f64)], i32),
     "lm_mp_patch_positions": ([C.c_void_p, i32, i32, P(i64), P(f64)], i32),
     "lm_mp_get": ([C.c_void_p, i32, i64, P(PointRecord), P(i64), P(i32), i32], i32),
+    "lm_mp_alive": ([C.c_void_p, i32, i32, P(i64), P(u8)], i32),
     "lm_kf_bindings": ([C.c_void_p, i32, i64, P(i64), i32, P(i32)], i32),
     "lm_bound_points": ([C.c_void_p, i32, i64, P(i64), i32, P(i32)], i32),
     "lm_covis_row": ([C.c_void_p, i32, i64, P(i64), P(i32), i32, P(i32)], i32),

@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(1024) k_stage(DevMap M, const unsigned char* b
 // ------------------------------------------------------------------- single-op map kernel
 enum MapOp { OP_NEW = 1, OP_OBS_ADD, OP_OBS_ERASE, OP_KILL, OP_REPLACE, OP_SET_COUNTS, OP_KF_KILL, OP_NEIGHBORS,
              OP_REFRESH, OP_APPLY, OP_TARGETS, OP_FUSE_PASS, OP_CULL, OP_SET_POSE, OP_PATCH_POS, OP_UPLOAD, OP_EVICT,
-             OP_MP_GET, OP_BOUND, OP_IMPORT_POINTS, OP_LEDGER_ADD };
+             OP_MP_GET, OP_BOUND, OP_IMPORT_POINTS, OP_LEDGER_ADD, OP_CORRUPT };
 
 // packed single-point record of OP_MP_GET (lm_mp_get), followed by nobs int2 (slot, kp)
 struct PointRec {
@@ -341,33 +341,33 @@ __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, in
       return;
     }
     case OP_KF_KILL: {  // kill_keyframe mapmodel.py:275-283
-      if (tid) return;
+      // The reference erases this keyframe's observation of every bound point in id order;
+      // each erase touches only its own point (list, counters, and a possible kill_point)
+      // plus commutative covisibility decrements, and a point is bound at most once per
+      // keyframe, so the erases are independent: thread per keypoint.
       const int slot = A.a;
       const int off = M.kp_off[slot], n = M.kp_n[slot];
-      // sorted unique bound ids; erase each observation of this keyframe
-      for (;;) {
-        int lo = 0x7fffffff;
-        for (int i = 0; i < n; ++i) {
-          const int mp = M.kbind[off + i];
-          if (mp >= 0 && mp < lo) lo = mp;
-        }
-        if (lo == 0x7fffffff) break;
-        const int k = obs_find(M, lo, slot);
-        if (M.alive[lo] && k >= 0) {
-          unlink_at(M, lo, k);
-          if (M.nobs[lo] < M.min_obs_keep) kill_point(M, lo);
-          else mark_dirty(M, lo);
+      for (int i = tid; i < n; i += 1024) {
+        const int mp = M.kbind[off + i];
+        if (mp < 0) continue;
+        const int k = M.alive[mp] ? obs_find(M, mp, slot) : -1;
+        if (k >= 0) {
+          unlink_at(M, mp, k);
+          if (M.nobs[mp] < M.min_obs_keep) kill_point(M, mp);
+          else mark_dirty(M, mp);
         } else {
-          for (int i = 0; i < n; ++i)
-            if (M.kbind[off + i] == lo) M.kbind[off + i] = -1;
+          M.kbind[off + i] = -1;
         }
       }
-      M.kf_state[slot] = KF_DEAD;
-      for (int s = 0; s < M.kf_cap; ++s) {
+      __syncthreads();
+      for (int s = tid; s < M.kf_cap; s += 1024) {  // graph.drop_keyframe
         M.covis[(size_t)slot * M.kf_cap + s] = 0;
         M.covis[(size_t)s * M.kf_cap + slot] = 0;
       }
-      res[0] = LM_OK;
+      if (tid == 0) {
+        M.kf_state[slot] = KF_DEAD;
+        res[0] = LM_OK;
+      }
       return;
     }
     case OP_NEIGHBORS: {
@@ -508,17 +508,18 @@ __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, in
     }
     case OP_IMPORT_POINTS: {  // lm_import_snapshot: points 0..n-1, no observations yet
       const int n = A.n;
-      const char* b = (const char*)A.buf;  // n x (pos 24, rep 32, found 4, visible 4, alive 1, pad 7, first kf 8)
+      // n x 96 B: pos @0 (24), rep @32 (32), first kf @64, found @72, visible @76, alive @80
+      const char* b = (const char*)A.buf;
       for (int id = tid; id < n; id += 1024) {
-        const char* e = b + 80 * (size_t)id;
+        const char* e = b + 96 * (size_t)id;
         const double* x = (const double*)e;
         for (int k = 0; k < 3; ++k) M.pos[3 * id + k] = x[k];
-        M.rep[2 * id] = *(const uint4*)(e + 24);
-        M.rep[2 * id + 1] = *(const uint4*)(e + 40);
-        M.found[id] = *(const int*)(e + 56);
-        M.visible[id] = *(const int*)(e + 60);
-        M.alive[id] = *(const unsigned char*)(e + 64);
-        M.first_kf[id] = *(const long long*)(e + 72);
+        M.rep[2 * id] = *(const uint4*)(e + 32);
+        M.rep[2 * id + 1] = *(const uint4*)(e + 48);
+        M.first_kf[id] = *(const long long*)(e + 64);
+        M.found[id] = *(const int*)(e + 72);
+        M.visible[id] = *(const int*)(e + 76);
+        M.alive[id] = *(const unsigned char*)(e + 80);
         M.nobs[id] = 0;
         M.ocap[id] = 0;
         M.ooff[id] = 0;
@@ -529,6 +530,13 @@ __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, in
         M.scal[SC_NEXT_ID] = n;
         res[0] = LM_OK;
       }
+      return;
+    }
+    case OP_CORRUPT: {  // fault injection for the audit tests (test_mapmodel.py:238-255)
+      if (tid) return;
+      if (A.n == 0) M.counts[(size_t)A.a * M.L + A.b] += A.c;
+      else covis_global(M, A.a, A.b, A.c);
+      res[0] = LM_OK;
       return;
     }
     case OP_LEDGER_ADD: {  // explicit record_neighbor_access / record_small_transfer (devicestore.py:80-101)
@@ -1601,6 +1609,33 @@ int lm_ledger_log(lm_ctx* ctx, int32_t map, int64_t first, int64_t* bytes, int32
   return LM_OK;
 }
 
+int lm_debug_corrupt(lm_ctx* ctx, int32_t map, int32_t what, int64_t a, int64_t b, int32_t delta) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  OpArgs o;
+  memset(&o, 0, sizeof o);
+  o.op = OP_CORRUPT;
+  o.n = what;
+  o.c = delta;
+  if (what == 0) {
+    int next = 0;
+    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaMemcpy(&next, m->d.scal + SC_NEXT_ID, sizeof(int), cudaMemcpyDeviceToHost));
+    if (a < 0 || a >= next || b < 0 || b >= m->d.L) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "bad counter cell");
+    o.a = (int)a;
+    o.b = (int)b;
+  } else {
+    int sa, sb;
+    if ((rc = slot_of(ctx, m, a, &sa, false)) || (rc = slot_of(ctx, m, b, &sb, false))) return rc;
+    o.a = sa;
+    o.b = sb;
+  }
+  int res[1];
+  if ((rc = run_op(ctx, m, map, o, res, 1))) return rc;
+  return op_status(ctx, res[0], "corrupt");
+}
+
 int lm_ledger_add(lm_ctx* ctx, int32_t map, int64_t naive_bytes, int32_t small_stage_triangulation,
                   int64_t small_bytes, int32_t small_events) {
   HostMap* m;
@@ -1868,6 +1903,16 @@ int lm_kf_evict(lm_ctx* ctx, int32_t map, int64_t kf_id) {
   return op_status(ctx, res[0], "evict_keyframe");
 }
 
+int lm_map_enforce_residency(lm_ctx* ctx, int32_t map, int32_t enforce) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  const int v = enforce ? 0 : 1;
+  CU(cudaMemcpyAsync(m->d.scal + SC_NORES, &v, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return LM_OK;
+}
+
 int lm_kf_resident(lm_ctx* ctx, int32_t map, int64_t kf_id, int32_t* resident, int32_t* count) {
   HostMap* m;
   int rc = check_map(ctx, map, &m);
@@ -1979,6 +2024,27 @@ int lm_mp_get(lm_ctx* ctx, int32_t map, int64_t mp, lm_point_record* out, int64_
   return op_status(ctx, res[0], "mp_get");
 }
 
+int lm_mp_alive(lm_ctx* ctx, int32_t map, int32_t n, const int64_t* ids, uint8_t* out) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  if (n <= 0) return LM_OK;
+  int next = 0;
+  CU(cudaStreamSynchronize(ctx->stream));
+  CU(cudaMemcpy(&next, m->d.scal + SC_NEXT_ID, sizeof(int), cudaMemcpyDeviceToHost));
+  // ids are probation entries: a contiguous window of recent ids, so one range copy
+  long long lo = next, hi = -1;
+  for (int k = 0; k < n; ++k) {
+    if (ids[k] < 0 || ids[k] >= next) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "unknown map point %lld", (long long)ids[k]);
+    lo = ids[k] < lo ? ids[k] : lo;
+    hi = ids[k] > hi ? ids[k] : hi;
+  }
+  std::vector<unsigned char> a(hi - lo + 1);
+  CU(cudaMemcpy(a.data(), m->d.alive + lo, a.size(), cudaMemcpyDeviceToHost));
+  for (int k = 0; k < n; ++k) out[k] = a[ids[k] - lo];
+  return LM_OK;
+}
+
 int lm_kf_bindings(lm_ctx* ctx, int32_t map, int64_t kf_id, int64_t* out, int32_t cap, int32_t* n_out) {
   HostMap* m;
   int rc = check_map(ctx, map, &m);
@@ -2064,16 +2130,16 @@ int lm_import_snapshot(lm_ctx* ctx, int32_t map, const lm_snapshot* S) {
   if (S->n_points > m->d.mp_cap) return fail(ctx, LM_ERR_CAPACITY, "snapshot has %d points, map capacity %d",
                                               S->n_points, m->d.mp_cap);
   if (S->n_points) {
-    std::vector<char> buf(80 * (size_t)S->n_points, 0);
+    std::vector<char> buf(96 * (size_t)S->n_points, 0);
     for (int i = 0; i < S->n_points; ++i) {
-      char* e = &buf[80 * (size_t)i];
+      char* e = &buf[96 * (size_t)i];
       memcpy(e, S->pos + 3 * (size_t)i, 24);
-      memcpy(e + 24, S->rep + 32 * (size_t)i, 32);
-      memcpy(e + 56, S->found + i, 4);
-      memcpy(e + 60, S->visible + i, 4);
-      e[64] = S->alive[i] ? 1 : 0;
+      memcpy(e + 32, S->rep + 32 * (size_t)i, 32);
       const long long fk = S->first_kf ? (long long)S->first_kf[i] : -1;
-      memcpy(e + 72, &fk, 8);
+      memcpy(e + 64, &fk, 8);
+      memcpy(e + 72, S->found + i, 4);
+      memcpy(e + 76, S->visible + i, 4);
+      e[80] = S->alive[i] ? 1 : 0;
     }
     if ((rc = io_reserve(ctx, m, buf.size()))) return rc;
     CU(cudaMemcpyAsync(m->d_io, buf.data(), buf.size(), cudaMemcpyHostToDevice, ctx->stream));

@@ -403,7 +403,8 @@ __global__ void __launch_bounds__(256) k_select(DevMap* maps, const StepArgs* ar
   }
   // record_neighbor_access (devicestore.py:80-92): every neighbour must be resident, else
   // the stage fails before touching the map (InvalidStateError in the reference)
-  const bool nonres = __syncthreads_or(threadIdx.x < n_out && !A.explicit_nbr && !M.kf_res[out[threadIdx.x]]);
+  const bool nonres = __syncthreads_or(threadIdx.x < n_out && !A.explicit_nbr && !M.scal[SC_NORES] &&
+                                       !M.kf_res[out[threadIdx.x]]);
   if (nonres && threadIdx.x == 0) atomicCAS(&M.scal[SC_SOFT], 0, LM_ERR_INVALID_STATE);
   const int nn = nonres ? 0 : n_out;
   lm_step_stats* st = M.s.stats;
@@ -1651,7 +1652,8 @@ __global__ void __launch_bounds__(1024) k_fuse_targets(DevMap* maps, const StepA
   int T = fusion_targets<1024>(M, A.cur, A.fc.n1, A.fc.n2, n_slots_max, sh_slot, sh_key);
   {  // record_neighbor_access("fusion", targets): all resident, else the stage fails untouched
     int bad = 0;
-    for (int k = threadIdx.x; k < T; k += 1024) bad |= !M.kf_res[M.s.targets[k]];
+    const bool enforce = !M.scal[SC_NORES];
+    for (int k = threadIdx.x; k < T; k += 1024) bad |= enforce && !M.kf_res[M.s.targets[k]];
     if (__syncthreads_or(bad)) {
       if (threadIdx.x == 0) atomicCAS(&M.scal[SC_SOFT], 0, LM_ERR_INVALID_STATE);
       T = 0;

@@ -44,7 +44,9 @@ constexpr int LG_LOG_CAP = 1 << 16;     // logged small-transfer events per map
 enum KfState { KF_FREE = 0, KF_STAGED = 1, KF_LIVE = 2, KF_DEAD = 3 };
 // SC_ERR: sticky (arena overflow: the map is unusable); SC_SOFT: this step's recoverable
 // contract error (a stage touched a non-resident keyframe), cleared at every step start
-enum Scal { SC_NEXT_ID = 0, SC_OBS_HEAD, SC_RECENT_N, SC_ERR, SC_DIRTY_N, SC_ROUND, SC_MTAG, SC_SOFT, SC_N = 8 };
+// SC_NORES: 1 = the stages do not enforce residency (the caller's store is not this map's)
+enum Scal { SC_NEXT_ID = 0, SC_OBS_HEAD, SC_RECENT_N, SC_ERR, SC_DIRTY_N, SC_ROUND, SC_MTAG, SC_SOFT, SC_NORES,
+            SC_N = 16 };
 enum LedgerIdx { LG_PERSIST = 0, LG_NAIVE, LG_SMALL_TRI, LG_SMALL_FUSE, LG_SMALL_EVENTS, LG_EVICT, LG_N = 8 };
 enum CandStatus { CS_PASS = 0, CS_PARALLAX = 1, CS_DEPTH = 2, CS_REPROJ = 3, CS_SCALE = 4, CS_DEGEN = 5 };
 

@@ -96,12 +96,19 @@ def apply_fusion(model: MapModel, actions: list[FuseAction]) -> dict[str, int]:
 
 def run_fusion(model: MapModel, store, current_kf_id: int, cfg: FuseConfig | None = None, *,
                engine: str = "b200", pool=None) -> dict[str, int]:
-    """Forward pass (current keyframe's points into every target), then reverse (fusion.py:307-347)."""
+    """Forward pass (current keyframe's points into every target), then reverse (fusion.py:307-347).
+
+    With this map's DeviceStore the kernels keep the ledger (neighbour access, one small
+    transfer per pass). A foreign store (e.g. the reference's DeviceStore) gets the same
+    calls the reference makes: record_neighbor_access("fusion", targets), then one
+    record_small_transfer("fusion", len(points) * its map_point_record_bytes) per pass, read
+    back from the device's per-pass log."""
     _check_engine(engine)
     cfg = cfg or FuseConfig()
     model._require_kf(current_kf_id)
-    rec = store is not None and hasattr(store, "record_neighbor_access")
-    if rec:
+    own = model._use_store(store)
+    foreign = not own and store is not None
+    if foreign:
         targets = collect_fusion_targets(model, current_kf_id, cfg.n1, cfg.n2)
         if not targets:
             return {"merged": 0, "observations_added": 0, "stale": 0}
@@ -110,11 +117,15 @@ def run_fusion(model: MapModel, store, current_kf_id: int, cfg: FuseConfig | Non
         model.ctx.call("lm_ledger", model.map, C.byref(before))
     st = _lib.StepStats()
     model._call("lm_run_fusion", model.map, int(current_kf_id), C.byref(fuse_cfg_c(cfg)), C.byref(st))
-    if rec:  # per-pass point-record transfers, as measured by the device ledger
+    if foreign:
         after = _lib.Ledger()
         model.ctx.call("lm_ledger", model.map, C.byref(after))
-        events = after.small_transfer_events - before.small_transfer_events
-        nbytes = after.small_bytes_fusion - before.small_bytes_fusion
-        for k in range(events):
-            store.record_small_transfer("fusion", nbytes if k == 0 else 0)
+        n = int(after.small_transfer_events - before.small_transfer_events)
+        log = np.zeros(max(n, 1), np.int64)
+        got = C.c_int32()
+        model.ctx.call("lm_ledger_log", model.map, int(before.small_transfer_events), ptr(log, C.c_int64), n,
+                       C.byref(got))
+        per_point = model.store_config.map_point_record_bytes
+        for b in log[:got.value]:
+            store.record_small_transfer("fusion", int(b) // per_point * store.config.map_point_record_bytes)
     return {"merged": st.merged, "observations_added": st.observations_added, "stale": st.stale}

@@ -323,6 +323,17 @@ class MapModel:
         self._cache_version = -1
         self._cache: dict[int, MapPoint] = {}
         self._n_points = 0
+        self._foreign = False
+
+    def reset(self):
+        """Back to an empty map (device arenas kept, lm_map_reset)."""
+        self.ctx.call("lm_map_reset", self.map)
+        for kf in self._kfs.values():
+            _HOME.pop(id(kf), None)
+        self._kfs.clear()
+        self._kf_seen.clear()
+        self._foreign = False
+        self._version += 1
 
     # ------------------------------------------------------------------ plumbing
     def _call(self, name, *args):
@@ -503,6 +514,20 @@ class MapModel:
 
         return device_audit(self)
 
+    # ------------------------------------------------------------------ store binding
+    def _use_store(self, store) -> bool:
+        """Bind the store a stage was called with. Returns True when it is this map's
+        device store (the kernels do the accounting); a foreign store (e.g. the reference's
+        DeviceStore) keeps its own ledger, fed by the facade, and residency is not enforced
+        on the device."""
+        if isinstance(store, DeviceStore):
+            store._attach(self)
+            return True
+        if not self._foreign:
+            self.ctx.call("lm_map_enforce_residency", self.map, 0)
+            self._foreign = True
+        return False
+
     # ------------------------------------------------------------------ snapshots
     def import_reference(self, ref_model, ref_store=None, recent=None):
         """Load a reference MapModel's state (plus its DeviceStore residency and ledger, and
@@ -606,6 +631,12 @@ class DeviceStore:
         elif self._model is not m:
             raise InvalidArgumentError(f"keyframe {kf.kf_id} belongs to another map than this store's")
         return m
+
+    def _attach(self, model: MapModel):
+        if self._model is None:
+            self._model = model
+        elif self._model is not model:
+            raise InvalidArgumentError("this DeviceStore holds the keyframes of another map")
 
     def payload_bytes(self, num_keypoints: int) -> int:
         return num_keypoints * self.config.keypoint_record_bytes + num_keypoints * self.config.descriptor_bytes

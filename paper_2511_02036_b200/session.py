@@ -85,6 +85,19 @@ class LocalMapper:
         self.fused = {"merged": 0, "observations_added": 0, "stale": 0}
         self.culled = 0
 
+    def _call(self, name, *args):
+        self.ctx.call(name, *args)
+
+    def import_state(self, arrays: dict, processed: int = 0):
+        """Start from an imported map state (snapshot.import_arrays layout, e.g. a reference
+        MapModel after k keyframes): the map is reset first; `processed` is the pipeline's
+        keyframe counter at that point (probation ages)."""
+        from .snapshot import import_arrays
+
+        self.reset()
+        import_arrays(self, arrays)
+        self.processed = int(processed)
+
     def reset(self):
         self.ctx.call("lm_map_reset", self.map)
         self.processed = 0

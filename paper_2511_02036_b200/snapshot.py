@@ -43,16 +43,15 @@ def state_arrays(ref_model, ref_store=None, recent=None, keypoints: bool = True)
         a["level"] = np.concatenate([np.asarray(kf.kp_level, np.int64) for kf in kfs]) if kfs else np.zeros(0, np.int64)
         a["desc"] = np.concatenate([np.asarray(kf.descriptors, np.uint8) for kf in kfs]) if kfs else np.zeros((0, 32),
                                                                                                            np.uint8)
-    pts = ref_model.points
-    n = len(pts)
-    if sorted(pts) != list(range(n)):
+    pts = sorted(ref_model.points.values(), key=lambda p: p.mp_id)
+    if [p.mp_id for p in pts] != list(range(len(pts))):
         raise ValueError("map point ids must be 0..n-1")
-    a["pos"] = np.array([np.asarray(pts[i].position, np.float64) for i in range(n)]).reshape(-1, 3)
-    a["rep"] = np.array([np.asarray(pts[i].rep_descriptor, np.uint8) for i in range(n)]).reshape(-1, 32)
-    a["alive"] = np.array([bool(pts[i].alive) for i in range(n)], np.uint8)
-    a["found"] = np.array([pts[i].found_count for i in range(n)], np.int32)
-    a["visible"] = np.array([pts[i].visible_count for i in range(n)], np.int32)
-    a["first_kf"] = np.array([pts[i].first_kf_id for i in range(n)], np.int64)
+    a["pos"] = np.array([np.asarray(p.position, np.float64) for p in pts]).reshape(-1, 3)
+    a["rep"] = np.array([np.asarray(p.rep_descriptor, np.uint8) for p in pts]).reshape(-1, 32)
+    a["alive"] = np.array([bool(p.alive) for p in pts], np.uint8)
+    a["found"] = np.array([p.found_count for p in pts], np.int32)
+    a["visible"] = np.array([p.visible_count for p in pts], np.int32)
+    a["first_kf"] = np.array([p.first_kf_id for p in pts], np.int64)
     recent = recent or []
     a["recent_id"] = np.array([r.mp_id for r in recent], np.int64)
     a["recent_born"] = np.array([r.created_at for r in recent], np.int32)

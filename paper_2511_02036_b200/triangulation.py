@@ -47,14 +47,20 @@ class CreationStats:
             self.gate_failures[reason] = self.gate_failures.get(reason, 0) + n
 
     def absorb(self, st: _lib.StepStats):
-        self.created += st.created
-        self.conflicts += st.conflicts
-        self.degenerate += st.degenerate
-        self.count_gate("parallax", st.gate_parallax)
-        self.count_gate("positive-depth", st.gate_depth)
-        self.count_gate("reprojection", st.gate_reprojection)
-        self.count_gate("scale", st.gate_scale)
-        self.degenerate_neighbors.extend(int(st.degenerate_neighbors[k]) for k in range(st.n_degenerate_neighbors))
+        absorb_stats(self, st)
+
+
+def absorb_stats(stats, st: _lib.StepStats):
+    """Add one device step's creation outcome to any CreationStats-shaped object (this
+    package's or the reference's, triangulation.py:49-60)."""
+    stats.created += st.created
+    stats.conflicts += st.conflicts
+    stats.degenerate += st.degenerate
+    for reason, n in (("parallax", st.gate_parallax), ("positive-depth", st.gate_depth),
+                      ("reprojection", st.gate_reprojection), ("scale", st.gate_scale)):
+        if n:
+            stats.gate_failures[reason] = stats.gate_failures.get(reason, 0) + n
+    stats.degenerate_neighbors.extend(int(st.degenerate_neighbors[k]) for k in range(st.n_degenerate_neighbors))
 
 
 def _check_engine(engine: str):
@@ -144,13 +150,14 @@ def create_map_points(model: MapModel, store, current_kf_id: int, neighbor_count
     model._require_kf(current_kf_id)
     if neighbor_count <= 0:
         return []
+    own = model._use_store(store)  # this map's DeviceStore: k_select accounts the neighbour access
     st = _lib.StepStats()
     model._call("lm_create_map_points", model.map, int(current_kf_id), int(neighbor_count),
                 C.byref(match_cfg_c(match_cfg)), C.byref(gate_cfg_c(gate_cfg)), C.byref(st))
     nbrs = [int(st.neighbors[k]) for k in range(st.n_neighbors)]
     if not nbrs:
         return []
-    if store is not None and hasattr(store, "record_neighbor_access"):
+    if not own and store is not None:  # a foreign store keeps its own ledger (triangulation.py:232)
         store.record_neighbor_access("triangulation", nbrs)
-    stats.absorb(st)
+    absorb_stats(stats, st)
     return list(range(int(st.first_new_id), int(st.first_new_id) + st.created))

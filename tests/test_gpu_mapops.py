@@ -1,0 +1,198 @@
+"""Device map bookkeeping against the oracle, op for op.
+
+A restatement of the reference's long random-operation test (pkg/tests/test_mapmodel.py:
+257-298), widened to every bookkeeping op the device exposes: insert_keyframe with pre-bound
+slots, new_map_point + add_observation, erase_observation (with the min_obs_keep kill),
+kill_map_point, replace_map_point and kill_keyframe. The same seeded op stream drives the
+device MapModel and the oracle's OracleMap (oracle/lm_oracle.py, the reference's
+mapmodel.py:113-353 restated); the op choices are drawn from the oracle's state, so the
+device is read only at checkpoints: structural digest (bindings, live ids, representative
+descriptors, observations, counters) and covisibility neighbour lists every 500 ops, and
+the device audit (lm_audit) clean at the end. Plus the reference's audit fault-injection
+tests (test_mapmodel.py:238-255) on the device audit.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import lm_oracle as O
+from paper_2511_02036_b200.geometry import CameraIntrinsics, SE3Pose
+from paper_2511_02036_b200.mapmodel import UNBOUND, KeyFrame, MapModel
+from paper_2511_02036_b200.session import store_for
+
+pytestmark = pytest.mark.gpu
+
+CAM = CameraIntrinsics(fx=460.0, fy=460.0, cx=320.0, cy=240.0, width=640, height=480)
+
+
+def make_pair(rng, kf_id, n, bind=None):
+    u = rng.uniform(0, 640, n)
+    v = rng.uniform(0, 480, n)
+    lev = rng.integers(0, CAM.num_levels, n)
+    desc = rng.integers(0, 256, (n, 32), dtype=np.uint8)
+    pose = SE3Pose(np.array([0.0, 0.0, 0.0, 1.0]), np.array([0.1 * kf_id, 0.0, 0.0]))
+    b = np.full(n, UNBOUND, np.int64) if bind is None else bind.copy()
+    kf = KeyFrame(kf_id, pose, CAM, u, v, lev, desc, mp_bindings=b.copy())
+    cam = O.Cam(CAM.fx, CAM.fy, CAM.cx, CAM.cy, CAM.width, CAM.height, CAM.num_levels, CAM.scale_factor)
+    okf = O.OKF(kf_id, pose.quat, pose.trans, cam, u, v, lev, desc, b.copy())
+    return kf, okf
+
+
+def neighbours_equal(m: MapModel, o: O.OracleMap) -> bool:
+    for k, kf in o.kfs.items():
+        if not kf.alive:
+            continue
+        if m.covisible_neighbors(k) != o.neighbors(k):
+            return False
+    return True
+
+
+def test_long_random_sequence_matches_oracle():
+    rng = np.random.default_rng(2025)
+    n_kf0, n_slots, n_ops = 12, 40, 10000
+    m = MapModel(CAM.num_levels, store=store_for(64, n_slots, points=1 << 15))
+    o = O.OracleMap(CAM.num_levels)
+    next_kf = 0
+    for _ in range(n_kf0):
+        kf, okf = make_pair(rng, next_kf, n_slots)
+        m.insert_keyframe(kf)
+        o.insert_keyframe(okf)
+        next_kf += 1
+    counts = dict.fromkeys(["new", "add", "erase", "kill", "replace", "insert_bound", "kill_kf"], 0)
+    for step in range(n_ops):
+        op = int(rng.integers(0, 100))
+        live = [p for p in o.pts.values() if p.alive]
+        live_kfs = [k for k, kf in o.kfs.items() if kf.alive]
+        if op < 30 or not live:  # new point + first observation
+            k = int(rng.choice(live_kfs))
+            free = np.flatnonzero(o.kfs[k].bind == UNBOUND)
+            if len(free) == 0:
+                continue
+            i = int(rng.choice(free))
+            pos = rng.normal(0, 5, 3)
+            p = o.new_point(pos, o.kfs[k].desc[i], k)
+            mp = m.new_map_point(pos, o.kfs[k].desc[i], k)
+            assert mp.mp_id == p.mp_id
+            o.add_obs(p.mp_id, k, i)
+            m.add_observation(p.mp_id, k, i)
+            counts["new"] += 1
+        elif op < 62:  # add an observation
+            p = live[int(rng.integers(0, len(live)))]
+            k = int(rng.choice(live_kfs))
+            if k in p.obs:
+                continue
+            free = np.flatnonzero(o.kfs[k].bind == UNBOUND)
+            if len(free) == 0:
+                continue
+            i = int(rng.choice(free))
+            o.add_obs(p.mp_id, k, i)
+            m.add_observation(p.mp_id, k, i)
+            counts["add"] += 1
+        elif op < 82:  # erase one (kills below min_obs_keep)
+            p = live[int(rng.integers(0, len(live)))]
+            if not p.obs:
+                continue
+            k = int(rng.choice(sorted(p.obs)))
+            o.erase_obs(p.mp_id, k)
+            m.erase_observation(p.mp_id, k)
+            counts["erase"] += 1
+        elif op < 87:  # kill a point
+            p = live[int(rng.integers(0, len(live)))]
+            o.kill_point(p.mp_id)
+            m.kill_map_point(p.mp_id)
+            counts["kill"] += 1
+        elif op < 97:  # merge two points
+            if len(live) < 2:
+                continue
+            a, b = rng.choice(len(live), size=2, replace=False)
+            lo, wi = live[int(a)], live[int(b)]
+            if len(lo.obs) > len(wi.obs):
+                lo, wi = wi, lo
+            o.replace(lo.mp_id, wi.mp_id)
+            m.replace_map_point(lo.mp_id, wi.mp_id)
+            counts["replace"] += 1
+        elif op < 99:  # a new keyframe with pre-bound slots (insert_keyframe registers them)
+            bind = np.full(n_slots, UNBOUND, np.int64)
+            for q in rng.permutation(len(live))[: int(rng.integers(1, 8))]:
+                bind[int(rng.integers(0, n_slots))] = live[int(q)].mp_id
+            # one slot per point and no duplicates
+            _, first = np.unique(bind, return_index=True)
+            keep = np.full(n_slots, UNBOUND, np.int64)
+            keep[first] = bind[first]
+            kf, okf = make_pair(rng, next_kf, n_slots, keep)
+            o.insert_keyframe(okf)
+            m.insert_keyframe(kf)
+            next_kf += 1
+            counts["insert_bound"] += 1
+        else:  # kill a keyframe (keep a few alive)
+            if len(live_kfs) <= 4:
+                continue
+            k = int(rng.choice(live_kfs))
+            o.kill_keyframe(k)
+            m.kill_keyframe(k)
+            counts["kill_kf"] += 1
+        if step % 500 == 499:
+            assert m._snapshot().structural_digest() == O.structural_digest(o), step
+            assert neighbours_equal(m, o), step
+    assert m._snapshot().structural_digest() == O.structural_digest(o)
+    assert neighbours_equal(m, o)
+    assert m.audit() == []
+    assert o.audit() == []
+    assert min(counts.values()) > 0, counts
+
+
+def _small_world():
+    rng = np.random.default_rng(5)
+    m = MapModel(CAM.num_levels, store=store_for(16, 64, points=1024))
+    kfs = []
+    for k in range(3):
+        kf, _ = make_pair(rng, k, 20)
+        m.insert_keyframe(kf)
+        kfs.append(kf)
+    return m, kfs
+
+
+def test_device_audit_clean_and_fault_injection():
+    m, kfs = _small_world()
+    mp = m.new_map_point([0, 0, 5.0], kfs[0].descriptors[0], 0)
+    m.add_observation(mp.mp_id, 0, 0)
+    m.add_observation(mp.mp_id, 1, 0)
+    assert m.audit() == []
+    # test_corrupted_scale_counts_detected
+    m.ctx.call("lm_debug_corrupt", m.map, 0, mp.mp_id, 0, 1)
+    m.invalidate()
+    v = m.audit()
+    assert f"scale_counts mismatch for map point {mp.mp_id}" in v
+    assert f"scale_counts sum mismatch for map point {mp.mp_id}" in v
+    m.ctx.call("lm_debug_corrupt", m.map, 0, mp.mp_id, 0, -1)
+    m.invalidate()
+    assert m.audit() == []
+    # test_corrupted_edge_detected
+    m.ctx.call("lm_debug_corrupt", m.map, 1, 0, 1, 1)
+    m.invalidate()
+    v = m.audit()
+    assert v and any("(0, 1)" in x for x in v)
+
+
+def test_kill_keyframe_matches_oracle_on_a_pipeline_map():
+    """kill_keyframe on a map built by the hot path (thousands of bindings, points dying
+    below min_obs_keep) against the oracle on the same map."""
+    from helpers import cam_of, device_kf
+    from paper_2511_02036_b200 import workload as W
+    from paper_2511_02036_b200.session import LocalMapper
+
+    seq = W.generate_sequence(W.WorldConfig(seed=41, landmark_count=2000, keyframe_count=10, features_per_kf=400,
+                                            pixel_noise_sigma=0.8, descriptor_flip_bits=3, trajectory="line",
+                                            extent=6.0))
+    intr, cam = seq.intrinsics(), cam_of(seq)
+    dev = LocalMapper(intr, neighbor_count=6, store=store_for(16, 512))
+    ora = O.OraclePipeline(intr.num_levels, 6)
+    for rec in seq.records:
+        dev.process(device_kf(rec, intr))
+        ora.step(O.okf_from_record(rec, cam))
+    for k in (4, 7, 0):
+        dev.ctx.call("lm_kf_kill", dev.map, k)
+        ora.map.kill_keyframe(k)
+        assert dev.snapshot(with_covis=False).structural_digest() == O.structural_digest(ora.map), k

@@ -123,3 +123,49 @@ def test_c5_sessions_batched_match_reference_every_keyframe():
     for d, (g, pos) in zip(devs, golds):
         if n_kf == g["keyframes"]:
             check_positions(d, pos)
+
+
+SNAPS = sorted(glob.glob(os.path.join(HERE, "golden", "snap_*_kf*.npz")))
+
+
+@pytest.mark.parametrize("path", [p for p in SNAPS
+                                  if os.path.basename(p).split("_kf")[0][len("snap_"):] in GOLD])
+def test_from_reference_state_every_keyframe(path):
+    """Per-step parity from the REAL reference's map state: import its map after K
+    keyframes (lm_import_snapshot of tests/golden/snap_<name>_kf<K>.npz, written by
+    make_snapshot.py), then step K.. natively; every keyframe's digest, counter deltas and
+    ledger must equal the reference's. No position drift from earlier keyframes can
+    cascade here: the device starts from the reference's own LAPACK positions."""
+    base = os.path.basename(path)
+    name, k0 = base[len("snap_"):].split("_kf")
+    k0 = int(k0[:-len(".npz")])
+    g, pos = load(name)
+    seq = seq_of(g)
+    intr = seq.intrinsics()
+    recs = seq.records
+    snap = dict(np.load(path))
+    snap["cam"] = np.array([[intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height]] * k0)
+    snap["u"] = np.concatenate([r.kp_u for r in recs[:k0]])
+    snap["v"] = np.concatenate([r.kp_v for r in recs[:k0]])
+    snap["level"] = np.concatenate([r.kp_level for r in recs[:k0]])
+    snap["desc"] = np.concatenate([r.descriptors for r in recs[:k0]])
+    snap["rep"] = np.zeros((len(snap["pos"]), 32), np.uint8)
+    dev = mapper_for(g, seq)
+    dev.import_state(snap, processed=int(snap["processed"]))
+    prev = g["steps"][k0 - 1]
+    assert dev.snapshot(with_covis=False).structural_digest() == prev["digest"]
+    assert ledger_matches(dev.ledger(), prev["ledger"])
+    for k in range(k0, g["keyframes"]):
+        dev.process(device_kf(recs[k], intr))
+        want = g["steps"][k]
+        st = dev.stats
+        assert st.created == want["created"] - prev["created"], k
+        assert st.conflicts == want["conflicts"] - prev["conflicts"], k
+        assert {r: n for r, n in st.gate_failures.items()} == {
+            r: n - prev["gates"].get(r, 0) for r, n in want["gates"].items() if n - prev["gates"].get(r, 0)}, k
+        assert {f: dev.fused[f] for f in dev.fused} == {f: want["fusion"][f] - prev["fusion"][f] for f in dev.fused}, k
+        assert dev.culled == want["culled"] - prev["culled"], k
+        assert dev.snapshot(with_covis=False).structural_digest() == want["digest"], k
+        assert ledger_matches(dev.ledger(), want["ledger"]), k
+    if g["keyframes"] == len(g["steps"]):
+        check_positions(dev, pos)
