@@ -166,6 +166,7 @@ int lm_ctx_destroy(lm_ctx* ctx);
 const char* lm_last_error(lm_ctx* ctx);
 int lm_map_create(lm_ctx* ctx, const lm_map_caps* caps, int32_t* map_out);
 int lm_map_reset(lm_ctx* ctx, int32_t map); /* back to an empty map, arenas kept */
+int lm_map_destroy(lm_ctx* ctx, int32_t map); /* free the map's arenas (index not reused) */
 int lm_map_sizes_get(lm_ctx* ctx, int32_t map, lm_map_sizes* out);
 int lm_synchronize(lm_ctx* ctx);
 
@@ -205,6 +206,17 @@ int lm_kf_stage_record(lm_ctx* ctx, int32_t map, const void* record, uint64_t by
 /* Insert a staged keyframe into the map (insert_keyframe + upload_keyframe). */
 int lm_kf_insert(lm_ctx* ctx, int32_t map, int64_t kf_id);
 int lm_kf_kill(lm_ctx* ctx, int32_t map, int64_t kf_id); /* MapModel.kill_keyframe */
+/* cull_keyframes culling.py:127-154 (redundancy by the per-level counter prefix,
+ * is_redundant_fast 95-117 == is_redundant_baseline 60-92): candidates in ascending id order
+ * (deduplicated, keyframe 0 and unknown/dead ids skipped), removal immediate (later
+ * candidates see it), removed keyframes evicted from the store when resident. removed holds
+ * up to n ids. */
+typedef struct lm_kf_cull_cfg { /* CullConfig config.py:63-72 (keyframe fields) */
+  double redundancy_ratio;
+  int32_t min_redundant_observers, scale_tolerance_levels;
+} lm_kf_cull_cfg;
+int lm_cull_keyframes(lm_ctx* ctx, int32_t map, const int64_t* candidates, int32_t n, const lm_kf_cull_cfg* cfg,
+                      int64_t* removed, int32_t* n_removed);
 
 /* ---- the hot path ---- */
 int lm_step(lm_ctx* ctx, int32_t map, int64_t kf_id, const lm_step_params* p, lm_step_stats* out);
@@ -220,6 +232,12 @@ int lm_create_map_points(lm_ctx* ctx, int32_t map, int64_t kf_id, int32_t neighb
                          const lm_match_cfg* mc, const lm_gate_cfg* gc, lm_step_stats* out);
 int lm_run_fusion(lm_ctx* ctx, int32_t map, int64_t kf_id, const lm_fuse_cfg* fc, lm_step_stats* out);
 int lm_cull_recent(lm_ctx* ctx, int32_t map, int32_t processed_index, const lm_cull_cfg* cc, int32_t* culled);
+/* cull_recent_map_points(model, recent, current_index, cfg) culling.py:28-59 in one call: the
+ * probation list (ids, born) in, (removed ids, kept entries) out, each in list order; removed
+ * and keep buffers hold n entries */
+int lm_cull_recent_list(lm_ctx* ctx, int32_t map, int32_t processed_index, const lm_cull_cfg* cc, int32_t n,
+                        const int64_t* ids, const int32_t* born, int64_t* removed, int32_t* n_removed,
+                        int64_t* keep_ids, int32_t* keep_born, int32_t* n_keep);
 int lm_search(lm_ctx* ctx, int32_t map, int64_t cur_kf, int64_t nbr_kf, const lm_match_cfg* mc,
               const uint8_t* unbound_cur, const uint8_t* unbound_nbr, lm_candidate* out, int32_t cap,
               int32_t* n_out);

@@ -721,6 +721,40 @@ def cull_recent(m: OracleMap, recent: list, now: int, cc: CullCfg = None):
     return removed, keep
 
 
+@dataclass
+class KfCullCfg:
+    redundancy_ratio: float = 0.9
+    min_redundant_observers: int = 3
+    scale_tolerance_levels: int = 0
+
+
+def kf_redundant(m: OracleMap, kf_id: int, cc: KfCullCfg) -> bool:
+    """is_redundant_baseline culling.py:60-92 (observation-list walk)."""
+    kf = m.kfs[kf_id]
+    red = considered = 0
+    for kp, mp_id in enumerate(kf.bind):
+        if mp_id == UNBOUND or not m.pts[int(mp_id)].alive:
+            continue
+        considered += 1
+        limit = int(kf.level[kp]) + cc.scale_tolerance_levels
+        others = sum(1 for k2, kp2 in m.pts[int(mp_id)].obs.items() if k2 != kf_id and int(m.kfs[k2].level[kp2]) <= limit)
+        red += others >= cc.min_redundant_observers
+    return considered > 0 and red >= cc.redundancy_ratio * considered
+
+
+def cull_keyframes(m: OracleMap, candidates, cc: KfCullCfg = None) -> list[int]:
+    """culling.py:127-154 (the store's eviction is the caller's)."""
+    cc = cc or KfCullCfg()
+    removed = []
+    for k in sorted(set(candidates)):
+        if k == 0 or k not in m.kfs or not m.kfs[k].alive:
+            continue
+        if kf_redundant(m, k, cc):
+            m.kill_keyframe(k)
+            removed.append(k)
+    return removed
+
+
 class OraclePipeline:
     """Per keyframe: insert -> recent-point cull -> create -> fuse (pipeline.py:152-195,
     with LBA and keyframe culling force-skipped as in the throughput benches)."""

@@ -6,6 +6,7 @@ every entry point raises ``DeviceError``.
 
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
 import threading
@@ -107,6 +108,10 @@ class AuditRecord(C.Structure):
     _fields_ = [("code", i32), ("kp", i32), ("mp", i64), ("kf_a", i64), ("kf_b", i64)]
 
 
+class KfCullCfg(C.Structure):
+    _fields_ = [("redundancy_ratio", f64), ("min_redundant_observers", i32), ("scale_tolerance_levels", i32)]
+
+
 class MapSizes(C.Structure):
     _fields_ = [("n_kf_slots", i32), ("n_points", i32), ("n_keypoints", i32), ("obs_used", i32),
                 ("recent_n", i32)]
@@ -119,6 +124,7 @@ _SIGS = {
     "lm_last_error": ([C.c_void_p], C.c_char_p),
     "lm_map_create": ([C.c_void_p, P(MapCaps), P(i32)], i32),
     "lm_map_reset": ([C.c_void_p, i32], i32),
+    "lm_map_destroy": ([C.c_void_p, i32], i32),
     "lm_map_sizes_get": ([C.c_void_p, i32, P(MapSizes)], i32),
     "lm_synchronize": ([C.c_void_p], i32),
     "lm_kf_stage": ([C.c_void_p, i32, i64, P(f64), P(f64), P(f64), i32, P(f64), P(f64), P(i64), P(u8), P(i64)], i32),
@@ -126,12 +132,15 @@ _SIGS = {
     "lm_kf_stage_record": ([C.c_void_p, i32, C.c_void_p, C.c_uint64, P(i64)], i32),
     "lm_kf_insert": ([C.c_void_p, i32, i64], i32),
     "lm_kf_kill": ([C.c_void_p, i32, i64], i32),
+    "lm_cull_keyframes": ([C.c_void_p, i32, P(i64), i32, P(KfCullCfg), P(i64), P(i32)], i32),
     "lm_step": ([C.c_void_p, i32, i64, P(StepParams), P(StepStats)], i32),
     "lm_step_batch": ([C.c_void_p, i32, P(i32), P(i64), P(StepParams), P(StepStats)], i32),
     "lm_step_stats_fetch": ([C.c_void_p, i32, P(i32), P(StepStats)], i32),
     "lm_create_map_points": ([C.c_void_p, i32, i64, i32, P(MatchCfg), P(GateCfg), P(StepStats)], i32),
     "lm_run_fusion": ([C.c_void_p, i32, i64, P(FuseCfg), P(StepStats)], i32),
     "lm_cull_recent": ([C.c_void_p, i32, i32, P(CullCfg), P(i32)], i32),
+    "lm_cull_recent_list": ([C.c_void_p, i32, i32, P(CullCfg), i32, P(i64), P(i32), P(i64), P(i32), P(i64), P(i32),
+                             P(i32)], i32),
     "lm_search": ([C.c_void_p, i32, i64, i64, P(MatchCfg), P(u8), P(u8), P(Candidate), i32, P(i32)], i32),
     "lm_fusion_targets": ([C.c_void_p, i32, i64, i32, i32, P(i64), i32, P(i32)], i32),
     "lm_fuse_pass": ([C.c_void_p, i32, P(i64), i32, i64, P(FuseCfg), P(FuseActionC), i32, P(i32), P(i64), P(i32)], i32),
@@ -240,6 +249,14 @@ class Context:
         self.h = h
         self.device = device
         self.lib = lib
+        atexit.register(self.close)
+
+    def close(self):
+        """Free every device buffer of this context (lm_ctx_destroy); idempotent."""
+        if self.h:
+            self.lib.lm_ctx_destroy(self.h)
+            self.h = None
+            Context._by_device.pop(self.device, None)
 
     @classmethod
     def get(cls, device: int = 0) -> "Context":

@@ -44,6 +44,9 @@ class CullConfig:
     found_ratio_min: float = 0.25
     probation_kfs: int = 3
     min_obs_graduate: int = 3
+    redundancy_ratio: float = 0.9
+    min_redundant_observers: int = 3
+    scale_tolerance_levels: int = 0
 
 
 @dataclass

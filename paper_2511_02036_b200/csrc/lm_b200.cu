@@ -10,6 +10,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <cmath>
 #include <string>
 #include <unordered_map>
@@ -39,6 +40,7 @@ struct HostMap {
   std::unordered_map<long long, int> slot_of;
   std::vector<int> state;  // host mirror of kf_state
   std::vector<char> res;   // host mirror of kf_res (DeviceStore residency)
+  std::vector<char> prebound;  // staged with pre-bound slots (insert must report their errors)
   std::vector<int> kp_n, kp_off;
   std::vector<long long> ids;
   int n_slots = 0, kp_head = 0, resident = 0;
@@ -141,12 +143,12 @@ static int upload_maps(lm_ctx* ctx) {
     CU(cudaMalloc(&ctx->d_maps, sizeof(DevMap) * ctx->d_maps_cap));
   }
   std::vector<DevMap> h(n);
-  for (int i = 0; i < n; ++i) h[i] = ctx->maps[i]->d;
+  for (int i = 0; i < n; ++i) h[i] = ctx->maps[i] ? ctx->maps[i]->d : DevMap{};
   CU(cudaMemcpyAsync(ctx->d_maps, h.data(), sizeof(DevMap) * n, cudaMemcpyHostToDevice, ctx->stream));
   if (ctx->d_totals) CU(cudaFree(ctx->d_totals));
   CU(cudaMalloc(&ctx->d_totals, sizeof(lm_step_stats*) * n));
   std::vector<lm_step_stats*> tp(n);
-  for (int i = 0; i < n; ++i) tp[i] = ctx->maps[i]->d_totals;
+  for (int i = 0; i < n; ++i) tp[i] = ctx->maps[i] ? ctx->maps[i]->d_totals : nullptr;
   CU(cudaMemcpyAsync(ctx->d_totals, tp.data(), sizeof(lm_step_stats*) * n, cudaMemcpyHostToDevice, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   return LM_OK;
@@ -224,7 +226,36 @@ __global__ void __launch_bounds__(1024) k_stage(DevMap M, const unsigned char* b
 // ------------------------------------------------------------------- single-op map kernel
 enum MapOp { OP_NEW = 1, OP_OBS_ADD, OP_OBS_ERASE, OP_KILL, OP_REPLACE, OP_SET_COUNTS, OP_KF_KILL, OP_NEIGHBORS,
              OP_REFRESH, OP_APPLY, OP_TARGETS, OP_FUSE_PASS, OP_CULL, OP_SET_POSE, OP_PATCH_POS, OP_UPLOAD, OP_EVICT,
-             OP_MP_GET, OP_BOUND, OP_IMPORT_POINTS, OP_LEDGER_ADD, OP_CORRUPT };
+             OP_MP_GET, OP_BOUND, OP_IMPORT_POINTS, OP_LEDGER_ADD, OP_CORRUPT, OP_KF_CULL };
+
+// kill_keyframe (mapmodel.py:275-283), whole block. The reference erases this keyframe's
+// observation of every bound point in id order; each erase touches only its own point (list,
+// counters, a possible kill_point) plus commutative covisibility decrements, and a point is
+// bound at most once per keyframe, so the erases are independent: thread per keypoint.
+__device__ void kill_keyframe_block(const DevMap& M, int slot) {
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int off = M.kp_off[slot], n = M.kp_n[slot];
+  __syncthreads();
+  for (int i = tid; i < n; i += nth) {
+    const int mp = M.kbind[off + i];
+    if (mp < 0) continue;
+    const int k = M.alive[mp] ? obs_find(M, mp, slot) : -1;
+    if (k >= 0) {
+      unlink_at(M, mp, k);
+      if (M.nobs[mp] < M.min_obs_keep) kill_point(M, mp);
+      else mark_dirty(M, mp);
+    } else {
+      M.kbind[off + i] = -1;
+    }
+  }
+  __syncthreads();
+  for (int s = tid; s < M.kf_cap; s += nth) {  // graph.drop_keyframe
+    M.covis[(size_t)slot * M.kf_cap + s] = 0;
+    M.covis[(size_t)s * M.kf_cap + slot] = 0;
+  }
+  if (tid == 0) M.kf_state[slot] = KF_DEAD;
+  __syncthreads();
+}
 
 // packed single-point record of OP_MP_GET (lm_mp_get), followed by nobs int2 (slot, kp)
 struct PointRec {
@@ -250,6 +281,8 @@ struct OpArgs {
   double pose[4 + 9 + 3 + 3 + 12];  // OP_SET_POSE: q, R, t, C, P
   void* buf;                        // OP_PATCH_POS / OP_MP_GET / OP_BOUND / OP_IMPORT_POINTS: io scratch
   long long v0, v1;                 // OP_LEDGER_ADD: naive bytes, small-transfer bytes
+  double kc_ratio;                  // OP_KF_CULL: CullConfig redundancy_ratio,
+  int kc_min_obs, kc_tol;           //   min_redundant_observers, scale_tolerance_levels
 };
 
 __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, int* res) {
@@ -341,32 +374,55 @@ __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, in
       return;
     }
     case OP_KF_KILL: {  // kill_keyframe mapmodel.py:275-283
-      // The reference erases this keyframe's observation of every bound point in id order;
-      // each erase touches only its own point (list, counters, and a possible kill_point)
-      // plus commutative covisibility decrements, and a point is bound at most once per
-      // keyframe, so the erases are independent: thread per keypoint.
-      const int slot = A.a;
-      const int off = M.kp_off[slot], n = M.kp_n[slot];
-      for (int i = tid; i < n; i += 1024) {
-        const int mp = M.kbind[off + i];
-        if (mp < 0) continue;
-        const int k = M.alive[mp] ? obs_find(M, mp, slot) : -1;
-        if (k >= 0) {
-          unlink_at(M, mp, k);
-          if (M.nobs[mp] < M.min_obs_keep) kill_point(M, mp);
-          else mark_dirty(M, mp);
-        } else {
-          M.kbind[off + i] = -1;
+      kill_keyframe_block(M, A.a);
+      if (tid == 0) res[0] = LM_OK;
+      return;
+    }
+    case OP_KF_CULL: {  // cull_keyframes culling.py:127-154 with is_redundant_* 60-117
+      // candidates (slots, ascending kf id, deduplicated, slot of kf 0 dropped) in A.buf;
+      // removed slots appended after them. Sequential over candidates: a removal is visible
+      // to every later candidate's check.
+      int* cand = (int*)A.buf;
+      int* removed = cand + A.n;
+      __shared__ int nrem, red_pts, considered;
+      if (tid == 0) nrem = 0;
+      for (int c = 0; c < A.n; ++c) {
+        const int slot = cand[c];
+        __syncthreads();
+        if (M.kf_state[slot] != KF_LIVE) continue;  // (uniform)
+        if (tid == 0) red_pts = considered = 0;
+        __syncthreads();
+        const int off = M.kp_off[slot], n = M.kp_n[slot];
+        int rp = 0, cs = 0;
+        for (int i = tid; i < n; i += 1024) {
+          const int mp = M.kbind[off + i];
+          if (mp < 0 || !M.alive[mp]) continue;
+          ++cs;
+          // counter prefix up to the keypoint's level + tolerance (is_redundant_fast), minus
+          // the keyframe's own observation (== the baseline's observation-list walk)
+          int lim = (int)M.klev[off + i] + A.kc_tol;
+          lim = lim > M.L - 1 ? M.L - 1 : lim;
+          int pre = 0;
+          for (int l = 0; l <= lim; ++l) pre += M.counts[(size_t)mp * M.L + l];
+          rp += pre - 1 >= A.kc_min_obs;
+        }
+        rp = block_sum<1024>(rp, sh);
+        cs = block_sum<1024>(cs, sh);
+        const bool redundant = cs > 0 && (double)rp >= A.kc_ratio * (double)cs;
+        if (!redundant) continue;  // (uniform)
+        kill_keyframe_block(M, slot);
+        if (tid == 0) {
+          if (M.kf_res[slot]) {  // store.evict_keyframe when resident
+            M.kf_res[slot] = 0;
+            M.ledger[LG_EVICT] += 1;
+          }
+          removed[nrem++] = slot;
         }
       }
       __syncthreads();
-      for (int s = tid; s < M.kf_cap; s += 1024) {  // graph.drop_keyframe
-        M.covis[(size_t)slot * M.kf_cap + s] = 0;
-        M.covis[(size_t)s * M.kf_cap + slot] = 0;
-      }
       if (tid == 0) {
-        M.kf_state[slot] = KF_DEAD;
         res[0] = LM_OK;
+        res[1] = nrem;
       }
       return;
     }
@@ -569,6 +625,27 @@ static int run_op(lm_ctx* ctx, HostMap* m, int map, OpArgs& a, int* res_host, in
   return LM_OK;
 }
 
+static int io_reserve(lm_ctx* ctx, HostMap* m, size_t bytes) {
+  if (bytes <= m->io_bytes) return LM_OK;
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (m->d_io) CU(cudaFree(m->d_io));
+  size_t sz = m->io_bytes ? m->io_bytes : 65536;
+  while (sz < bytes) sz *= 2;
+  CU(cudaMalloc(&m->d_io, sz));
+  m->io_bytes = sz;
+  return LM_OK;
+}
+
+// fire-and-forget op (its status is validated on the host): no result readback, no sync
+static int run_op_async(lm_ctx* ctx, HostMap* m, int map, OpArgs& a) {
+  a.n_slots = m->n_slots;
+  const size_t dyn = 12 * (size_t)m->d.kf_cap;
+  k_op<<<1, 1024, dyn, ctx->stream>>>(ctx->d_maps, map, a, m->d_result);
+  CHECK_LAUNCH();
+  ctx->launches += 1;
+  return LM_OK;
+}
+
 static int op_status(lm_ctx* ctx, int code, const char* what) {
   switch (code) {
     case LM_OK: return LM_OK;
@@ -677,9 +754,19 @@ int lm_ctx_destroy(lm_ctx* ctx) {
   for (HostMap* m : ctx->maps) {
     if (!m) continue;
     for (void* p : m->allocs) cudaFree(p);
+    if (m->d_io) cudaFree(m->d_io);
     delete m;
   }
   if (ctx->d_maps) cudaFree(ctx->d_maps);
+  if (ctx->d_totals) cudaFree(ctx->d_totals);
+  if (ctx->flush_buf) cudaFree(ctx->flush_buf);
+  if (ctx->t0) cudaEventDestroy(ctx->t0);
+  if (ctx->t1) cudaEventDestroy(ctx->t1);
+  for (int i = 0; i < kRing; ++i) cudaEventDestroy(ctx->args_ev[i]);
+  for (int i = 0; i < kStageRing; ++i) cudaEventDestroy(ctx->stage_ev[i]);
+  for (cudaEvent_t e : ctx->prof_pool) cudaEventDestroy(e);
+  for (auto& v : ctx->prof_steps)
+    for (cudaEvent_t e : v) cudaEventDestroy(e);
   if (ctx->h_args) cudaFreeHost(ctx->h_args);
   if (ctx->d_args) cudaFree(ctx->d_args);
   if (ctx->h_stats) cudaFreeHost(ctx->h_stats);
@@ -794,12 +881,25 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   CU(cudaMemsetAsync(s.hitpass, 0, sizeof(unsigned) * d.kpkf_max * ((TMAX + 31) / 32), ctx->stream));
   m->state.assign(K, KF_FREE);
   m->res.assign(K, 0);
+  m->prebound.assign(K, 0);
   m->kp_n.assign(K, 0);
   m->kp_off.assign(K, 0);
   m->ids.assign(K, 0);
   ctx->maps.push_back(m);
   *map_out = (int32_t)ctx->maps.size() - 1;
   return upload_maps(ctx);
+}
+
+int lm_map_destroy(lm_ctx* ctx, int32_t map) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  CU(cudaStreamSynchronize(ctx->stream));
+  for (void* p : m->allocs) CU(cudaFree(p));
+  if (m->d_io) CU(cudaFree(m->d_io));
+  delete m;
+  ctx->maps[map] = nullptr;  // the index is not reused; other maps keep theirs
+  return LM_OK;
 }
 
 int lm_map_reset(lm_ctx* ctx, int32_t map) {
@@ -927,6 +1027,7 @@ int lm_kf_stage(lm_ctx* ctx, int32_t map, int64_t kf_id, const double quat[4], c
   ctx->stage_used[b] = true;
   m->slot_of[kf_id] = slot;
   m->state[slot] = KF_STAGED;
+  m->prebound[slot] = bindings != nullptr;
   m->kp_n[slot] = n;
   m->kp_off[slot] = m->kp_head;
   m->ids[slot] = kf_id;
@@ -1260,8 +1361,9 @@ int lm_kf_insert(lm_ctx* ctx, int32_t map, int64_t kf_id) {
   // (lm_kf_upload), as in the reference pipeline (pipeline.py:163-164)
   StepArgs a;
   if ((rc = fill_args(ctx, m, kf_id, nullptr, a, true, false))) return rc;
+  // without pre-bound slots the insert cannot fail on the device: no readback, no sync
   lm_step_stats st;
-  return run_batch(ctx, 1, &map, &a, &st);
+  return run_batch(ctx, 1, &map, &a, m->prebound[slot] ? &st : nullptr);
 }
 
 int lm_create_map_points(lm_ctx* ctx, int32_t map, int64_t kf_id, int32_t neighbor_count, const lm_match_cfg* mc,
@@ -1309,6 +1411,37 @@ int lm_cull_recent(lm_ctx* ctx, int32_t map, int32_t processed_index, const lm_c
   rc = lm_step(ctx, map, m->ids[anchor], &p, &st);
   if (culled) *culled = st.culled;
   return rc;
+}
+
+int lm_cull_recent_list(lm_ctx* ctx, int32_t map, int32_t processed_index, const lm_cull_cfg* cc, int32_t n,
+                        const int64_t* ids, const int32_t* born, int64_t* removed, int32_t* n_removed,
+                        int64_t* keep_ids, int32_t* keep_born, int32_t* n_keep) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  *n_removed = 0;
+  *n_keep = 0;
+  if (n <= 0) return lm_recent_import(ctx, map, ids, born, 0);
+  int next = 0;
+  CU(cudaStreamSynchronize(ctx->stream));
+  CU(cudaMemcpy(&next, m->d.scal + SC_NEXT_ID, sizeof(int), cudaMemcpyDeviceToHost));
+  long long lo = next, hi = -1;
+  for (int k = 0; k < n; ++k) {
+    if (ids[k] < 0 || ids[k] >= next) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "unknown map point %lld", (long long)ids[k]);
+    lo = ids[k] < lo ? ids[k] : lo;
+    hi = ids[k] > hi ? ids[k] : hi;
+  }
+  std::vector<unsigned char> before(hi - lo + 1), after(hi - lo + 1);
+  CU(cudaMemcpy(before.data(), m->d.alive + lo, before.size(), cudaMemcpyDeviceToHost));
+  if ((rc = lm_recent_import(ctx, map, ids, born, n))) return rc;
+  int culled = 0;
+  if ((rc = lm_cull_recent(ctx, map, processed_index, cc, &culled))) return rc;
+  CU(cudaMemcpy(after.data(), m->d.alive + lo, after.size(), cudaMemcpyDeviceToHost));
+  int r = 0;
+  for (int k = 0; k < n; ++k)  // removed = alive before, dead after, in probation order
+    if (before[ids[k] - lo] && !after[ids[k] - lo]) removed[r++] = ids[k];
+  *n_removed = r;
+  return lm_recent_export(ctx, map, keep_ids, keep_born, n, n_keep);
 }
 
 int lm_search(lm_ctx* ctx, int32_t map, int64_t cur_kf, int64_t nbr_kf, const lm_match_cfg* mc,
@@ -1553,6 +1686,49 @@ int lm_mp_set_counts(lm_ctx* ctx, int32_t map, int64_t mp, int32_t found, int32_
   a.visible = visible;
   int res[1];
   return run_op(ctx, m, map, a, res, 1);
+}
+
+int lm_cull_keyframes(lm_ctx* ctx, int32_t map, const int64_t* candidates, int32_t n, const lm_kf_cull_cfg* cfg,
+                      int64_t* removed, int32_t* n_removed) {
+  HostMap* m;
+  int rc = check_map(ctx, map, &m);
+  if (rc) return rc;
+  if (!cfg || n < 0 || (n && !candidates)) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "bad keyframe-cull arguments");
+  *n_removed = 0;
+  std::vector<long long> ids;
+  for (int k = 0; k < n; ++k)
+    if (candidates[k] != 0 && m->slot_of.count(candidates[k])) ids.push_back(candidates[k]);  // kf 0: map anchor
+  std::sort(ids.begin(), ids.end());
+  ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+  if (ids.empty()) return LM_OK;
+  std::vector<int> slots(ids.size());
+  for (size_t k = 0; k < ids.size(); ++k) slots[k] = m->slot_of[ids[k]];
+  if ((rc = io_reserve(ctx, m, 2 * sizeof(int) * slots.size()))) return rc;
+  CU(cudaMemcpyAsync(m->d_io, slots.data(), sizeof(int) * slots.size(), cudaMemcpyHostToDevice, ctx->stream));
+  OpArgs a;
+  memset(&a, 0, sizeof a);
+  a.op = OP_KF_CULL;
+  a.n = (int)slots.size();
+  a.buf = m->d_io;
+  a.kc_ratio = cfg->redundancy_ratio;
+  a.kc_min_obs = cfg->min_redundant_observers;
+  a.kc_tol = cfg->scale_tolerance_levels;
+  int res[2];
+  if ((rc = run_op(ctx, m, map, a, res, 2))) return rc;
+  if (res[0]) return op_status(ctx, res[0], "cull_keyframes");
+  const int nr = res[1];
+  std::vector<int> rs(nr > 0 ? nr : 1);
+  if (nr) CU(cudaMemcpy(rs.data(), (int*)m->d_io + slots.size(), sizeof(int) * nr, cudaMemcpyDeviceToHost));
+  for (int k = 0; k < nr; ++k) {
+    removed[k] = m->ids[rs[k]];
+    m->state[rs[k]] = KF_DEAD;
+    if (m->res[rs[k]]) {
+      m->res[rs[k]] = 0;
+      m->resident--;
+    }
+  }
+  *n_removed = nr;
+  return LM_OK;
 }
 
 int lm_kf_kill(lm_ctx* ctx, int32_t map, int64_t kf_id) {
@@ -1852,16 +2028,6 @@ int lm_recent_import(lm_ctx* ctx, int32_t map, const int64_t* ids, const int32_t
 
 // ------------------------------------------------------------------- store / LBA write-back / import
 
-static int io_reserve(lm_ctx* ctx, HostMap* m, size_t bytes) {
-  if (bytes <= m->io_bytes) return LM_OK;
-  CU(cudaStreamSynchronize(ctx->stream));
-  if (m->d_io) CU(cudaFree(m->d_io));
-  size_t sz = m->io_bytes ? m->io_bytes : 65536;
-  while (sz < bytes) sz *= 2;
-  CU(cudaMalloc(&m->d_io, sz));
-  m->io_bytes = sz;
-  return LM_OK;
-}
 
 int lm_kf_upload(lm_ctx* ctx, int32_t map, int64_t kf_id) {
   HostMap* m;
@@ -1878,11 +2044,10 @@ int lm_kf_upload(lm_ctx* ctx, int32_t map, int64_t kf_id) {
   memset(&a, 0, sizeof a);
   a.op = OP_UPLOAD;
   a.a = slot;
-  int res[1];
-  if ((rc = run_op(ctx, m, map, a, res, 1))) return rc;
+  if ((rc = run_op_async(ctx, m, map, a))) return rc;  // validated above; cannot fail on the device
   m->res[slot] = 1;
   m->resident++;
-  return op_status(ctx, res[0], "upload_keyframe");
+  return LM_OK;
 }
 
 int lm_kf_evict(lm_ctx* ctx, int32_t map, int64_t kf_id) {

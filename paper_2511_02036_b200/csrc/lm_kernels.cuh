@@ -2712,8 +2712,8 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       atomicMin(&tmin_sh, t);
     }
     __syncthreads();
-    touched_min = tmin_sh;
     if (threadIdx.x == 0) {
+      touched_min = tmin_sh;  // (diagnostic, thread 0's only: read here, before the reset below)
       tm[3] += gtime() - t7;
       nc_sh = 0;  // counters of the next iteration (read above, before this barrier)
       ni_sh = 0;

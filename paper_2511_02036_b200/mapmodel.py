@@ -72,7 +72,10 @@ class KeyFrame:
 
 @dataclass
 class MapPoint:
-    """Snapshot of one device map point (read-only view)."""
+    """Snapshot of one device map point. Assigning ``position``, ``found_count`` or
+    ``visible_count`` on a point read from a MapModel writes through to the device (batched,
+    before the model's next device call): the reference's LBA writes positions back this way
+    (localba.py:573-574)."""
 
     mp_id: int
     position: np.ndarray
@@ -83,6 +86,15 @@ class MapPoint:
     visible_count: int = 1
     alive: bool = True
     scale_counts: np.ndarray = None
+
+    def __setattr__(self, name, value):
+        object.__setattr__(self, name, value)
+        m = self.__dict__.get("_model")
+        if m is not None and name in _WRITE_THROUGH:
+            m._pending[self.mp_id] = self
+
+
+_WRITE_THROUGH = ("position", "found_count", "visible_count")
 
 
 def stage_keyframe(ctx: Context, map_idx: int, kf: KeyFrame, bindings: bool = True):
@@ -324,6 +336,14 @@ class MapModel:
         self._cache: dict[int, MapPoint] = {}
         self._n_points = 0
         self._foreign = False
+        self._pending: dict[int, MapPoint] = {}
+        self._pose_ref: dict = {}
+
+    def close(self):
+        """Free the device map (lm_map_destroy); the model is unusable afterwards."""
+        if self.map is not None and self.ctx.h:
+            self.ctx.call("lm_map_destroy", self.map)
+        self.map = None
 
     def reset(self):
         """Back to an empty map (device arenas kept, lm_map_reset)."""
@@ -332,18 +352,47 @@ class MapModel:
             _HOME.pop(id(kf), None)
         self._kfs.clear()
         self._kf_seen.clear()
+        self._pose_ref.clear()
+        self._pending.clear()
         self._foreign = False
         self._version += 1
 
     # ------------------------------------------------------------------ plumbing
     def _call(self, name, *args):
+        if self._pending:
+            self._flush_points()
         self._version += 1  # even a failing call may have changed the map
         self.ctx.call(name, *args)
+
+    def _flush_points(self):
+        """Write back attribute assignments on MapPoint snapshots (LBA positions, counters)."""
+        pend, self._pending = self._pending, {}
+        moved = [p for p in pend.values() if p.alive]
+        if moved:
+            ids = np.array([p.mp_id for p in moved], np.int64)
+            pos = np.array([np.asarray(p.position, np.float64).reshape(3) for p in moved])
+            self._version += 1
+            self.ctx.call("lm_mp_patch_positions", self.map, len(ids), ptr(ids, C.c_int64), ptr(pos, C.c_double))
+        for p in pend.values():
+            self._version += 1
+            self.ctx.call("lm_mp_set_counts", self.map, int(p.mp_id), int(p.found_count), int(p.visible_count))
+
+    def sync_host_writes(self):
+        """Push host-side writes the reference makes directly on its objects (LBA assigns
+        ``kf.pose`` and ``mp.position``, localba.py:571-574) to the device. The stage
+        functions call this on entry, so a reference pipeline with LBA needs nothing else."""
+        if self._pending:
+            self._flush_points()
+        for k, kf in self._kfs.items():
+            if kf.pose is not self._pose_ref.get(k) and kf.alive:
+                self.set_pose(k, kf.pose)
 
     def invalidate(self):
         self._version += 1
 
     def _fresh(self):
+        if self._pending:
+            self._flush_points()
         if self._cache_version != self._version:
             self._cache.clear()
             sizes = _lib.MapSizes()
@@ -357,6 +406,8 @@ class MapModel:
 
     def _snapshot(self) -> MapSnapshot:
         """Whole-map export (audit, iteration): O(map), cached until the next mutation."""
+        if self._pending:
+            self._flush_points()
         if self._snap_version != self._version:
             self._snap = export_snapshot(self.ctx, self.map)
             self._snap_version = self._version
@@ -385,6 +436,7 @@ class MapModel:
             p = MapPoint(mp_id, np.array(rec.pos[:], np.float64), np.frombuffer(bytes(rec.rep), np.uint8).copy(),
                          int(rec.first_kf_id), {int(okf[k]): int(okp[k]) for k in range(n)}, int(rec.found),
                          int(rec.visible), bool(rec.alive), np.array(rec.counts[:self.num_levels], np.int64))
+            object.__setattr__(p, "_model", self)
             self._cache[mp_id] = p
         return p
 
@@ -392,8 +444,11 @@ class MapModel:
         s = self._snapshot()
         obs = s.observations()
         first = [-1] * len(s.alive)
-        return [MapPoint(i, s.pos[i].copy(), s.rep[i].copy(), first[i], obs[i], int(s.found[i]), int(s.visible[i]),
-                         bool(s.alive[i]), s.counts[i].astype(np.int64)) for i in range(len(s.alive))]
+        out = [MapPoint(i, s.pos[i].copy(), s.rep[i].copy(), first[i], obs[i], int(s.found[i]), int(s.visible[i]),
+                        bool(s.alive[i]), s.counts[i].astype(np.int64)) for i in range(len(s.alive))]
+        for p in out:
+            object.__setattr__(p, "_model", self)
+        return out
 
     # ------------------------------------------------------------------ keyframes
     def insert_keyframe(self, kf) -> int:
@@ -408,6 +463,7 @@ class MapModel:
         stage_keyframe(self.ctx, self.map, kf)
         self._call("lm_kf_insert", self.map, int(kf.kf_id))
         self._kfs[kf.kf_id] = kf
+        self._pose_ref[kf.kf_id] = kf.pose
         kf.alive = True
         _HOME[id(kf)] = (weakref.ref(self), kf.kf_id)
         return kf.kf_id
@@ -441,6 +497,7 @@ class MapModel:
         t = np.ascontiguousarray(pose.trans, dtype=np.float64)
         self._call("lm_kf_set_pose", self.map, int(kf_id), ptr(q, C.c_double), ptr(t, C.c_double))
         kf.pose = pose
+        self._pose_ref[kf_id] = pose
 
     def patch_positions(self, ids, positions):
         """LBA position write-back (localba.py:571-574 assigns mp.position), batched."""
@@ -520,6 +577,7 @@ class MapModel:
         device store (the kernels do the accounting); a foreign store (e.g. the reference's
         DeviceStore) keeps its own ledger, fed by the facade, and residency is not enforced
         on the device."""
+        self.sync_host_writes()
         if isinstance(store, DeviceStore):
             store._attach(self)
             return True

@@ -88,6 +88,12 @@ class LocalMapper:
     def _call(self, name, *args):
         self.ctx.call(name, *args)
 
+    def close(self):
+        """Free the device map (lm_map_destroy)."""
+        if self.map is not None and self.ctx.h:
+            self.ctx.call("lm_map_destroy", self.map)
+        self.map = None
+
     def import_state(self, arrays: dict, processed: int = 0):
         """Start from an imported map state (snapshot.import_arrays layout, e.g. a reference
         MapModel after k keyframes): the map is reset first; `processed` is the pipeline's

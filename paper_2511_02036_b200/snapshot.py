@@ -119,5 +119,6 @@ def import_reference(model, ref_model, ref_store=None, recent=None, keyframes=No
 
     for kf in kfs:
         model._kfs[kf.kf_id] = kf
+        model._pose_ref[kf.kf_id] = kf.pose
         _HOME[id(kf)] = (weakref.ref(model), kf.kf_id)
     model.invalidate()

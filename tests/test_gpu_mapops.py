@@ -52,7 +52,7 @@ def neighbours_equal(m: MapModel, o: O.OracleMap) -> bool:
 def test_long_random_sequence_matches_oracle():
     rng = np.random.default_rng(2025)
     n_kf0, n_slots, n_ops = 12, 40, 10000
-    m = MapModel(CAM.num_levels, store=store_for(64, n_slots, points=1 << 15))
+    m = MapModel(CAM.num_levels, store=store_for(400, n_slots, points=1 << 15))
     o = O.OracleMap(CAM.num_levels)
     next_kf = 0
     for _ in range(n_kf0):
@@ -196,3 +196,48 @@ def test_kill_keyframe_matches_oracle_on_a_pipeline_map():
         dev.ctx.call("lm_kf_kill", dev.map, k)
         ora.map.kill_keyframe(k)
         assert dev.snapshot(with_covis=False).structural_digest() == O.structural_digest(ora.map), k
+
+
+def test_cull_keyframes_matches_oracle_on_a_pipeline_map():
+    """§8(f) row 4: the device keyframe cull (counter prefix, lm_cull_keyframes) against the
+    oracle's observation-walk restatement (is_redundant_baseline) on the same hot-path map,
+    candidates = every live keyframe's covisible neighbours in turn (pipeline.py:215-221)."""
+    from helpers import cam_of, device_kf
+    from paper_2511_02036_b200 import workload as W
+    from paper_2511_02036_b200.config import CullConfig
+    from paper_2511_02036_b200.culling import cull_keyframes
+    from paper_2511_02036_b200.mapmodel import DeviceStore
+    from paper_2511_02036_b200.session import LocalMapper
+
+    seq = W.generate_sequence(W.WorldConfig(seed=41, landmark_count=2000, keyframe_count=14, features_per_kf=400,
+                                            pixel_noise_sigma=0.8, descriptor_flip_bits=3, trajectory="line",
+                                            extent=6.0))
+    intr, cam = seq.intrinsics(), cam_of(seq)
+    ora = O.OraclePipeline(intr.num_levels, 8)
+    m = MapModel(intr.num_levels, store=store_for(16, 512))
+    st = DeviceStore()
+    from paper_2511_02036_b200.culling import RecentPoint, cull_recent_map_points
+    from paper_2511_02036_b200.fusion import run_fusion
+    from paper_2511_02036_b200.triangulation import create_map_points
+
+    recent, total = [], []
+    for processed, rec in enumerate(seq.records):
+        kf = device_kf(rec, intr)
+        m.insert_keyframe(kf)
+        st.upload_keyframe(kf)
+        _, recent = cull_recent_map_points(m, recent, processed)
+        recent += [RecentPoint(i, processed) for i in create_map_points(m, st, kf.kf_id, 8)]
+        run_fusion(m, st, kf.kf_id)
+        ora.step(O.okf_from_record(rec, cam))
+        cand = [k for k in m.covisible_neighbors(kf.kf_id) if k != kf.kf_id]
+        assert cand == [k for k in ora.map.neighbors(kf.kf_id) if k != kf.kf_id]
+        cc = CullConfig(redundancy_ratio=0.6)  # a looser ratio so this short run culls
+        got = cull_keyframes(m, st, cand, impl="fast", cfg=cc)
+        want = O.cull_keyframes(ora.map, cand, O.KfCullCfg(redundancy_ratio=0.6))
+        assert got == want, processed
+        total += got
+        for k in got:
+            assert not st.is_resident(k)
+        assert m._snapshot().structural_digest() == O.structural_digest(ora.map), processed
+    assert total, "the run should cull at least one keyframe"
+    assert st.ledger.evictions == len(total)

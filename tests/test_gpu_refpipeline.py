@@ -56,13 +56,14 @@ def device_bound(store_cfg, own_cull=True):
     from paper_2511_02036_b200.mapmodel import DeviceStore, MapModel
 
     saved = {k: getattr(P, k) for k in ("MapModel", "DeviceStore", "create_map_points", "run_fusion",
-                                        "cull_recent_map_points")}
+                                        "cull_recent_map_points", "cull_keyframes")}
     P.MapModel = lambda num_levels=8, config=None: MapModel(num_levels, config, store=store_cfg)
     P.DeviceStore = DeviceStore
     P.create_map_points = triangulation.create_map_points
     P.run_fusion = fusion.run_fusion
     if own_cull:
         P.cull_recent_map_points = culling.cull_recent_map_points
+    P.cull_keyframes = culling.cull_keyframes
     try:
         yield lm
     finally:
@@ -70,13 +71,13 @@ def device_bound(store_cfg, own_cull=True):
             setattr(P, k, v)
 
 
-def run_reference_pipeline(lm, cfg_kw, n_nbr, n1, n_kf, check):
+def run_reference_pipeline(lm, cfg_kw, n_nbr, n1, n_kf, check, kf_cull=False, lba=False):
     from localmap import synth
     from localmap.config import FuseConfig, MatchConfig, PipelineConfig
     from localmap.pipeline import LocalMappingPipeline
 
     seq = synth.generate_sequence(synth.WorldConfig(**cfg_kw))
-    pc = PipelineConfig(mode="optimized", worker_count=2, force_skip_lba=True, force_skip_culling=True,
+    pc = PipelineConfig(mode="optimized", worker_count=2, force_skip_lba=not lba, force_skip_culling=not kf_cull,
                         match=MatchConfig(neighbor_count=n_nbr), fuse=FuseConfig(n1=n1))
     with LocalMappingPipeline(pc, num_levels=seq.intrinsics().num_levels) as pipe:
         for k, kf in enumerate(seq.to_keyframes()[:n_kf]):
@@ -217,3 +218,34 @@ def test_lba_write_back_pose_and_positions():
     import_reference(m2, m1, None, None, keyframes=list(m1.keyframes.values()))
     a2 = fuse_pass(m2, [p.mp_id for p in m2.live_points()], 3)
     assert a1 == a2
+
+
+KFCULL = os.path.join(HERE, "golden", "kfcull.json")
+
+
+@pytest.mark.parametrize("name", sorted(json.load(open(KFCULL))) if os.path.isfile(KFCULL) else [])
+def test_reference_pipeline_with_keyframe_culling_on_device(name):
+    """§8(f) row 4 end to end: the reference pipeline with keyframe culling enabled
+    (pipeline.py:210-223) and cull_keyframes bound to the device fast path must cull the same
+    keyframes and leave the same map (digest, ledger incl. evictions) after every keyframe as
+    the reference's own run (tests/golden/kfcull.json, make_golden_kfcull.py). The "default_*"
+    cases are the reference's DEFAULT pipeline: its own LBA (out of scope, run on the host)
+    reads the device map through the MapModel API and writes poses and positions back
+    (localba.py:571-574), which the device takes over (lm_kf_set_pose,
+    lm_mp_patch_positions) before the next stage."""
+    from paper_2511_02036_b200.session import store_for
+
+    g = json.load(open(KFCULL))[name]
+
+    def check(k, pipe):
+        want = g["steps"][k]
+        assert list(pipe.culled_keyframes) == want["culled_keyframes"], (name, k)
+        got = counters(pipe)
+        for key in ("created", "conflicts", "gates", "fusion", "culled"):
+            assert got[key] == want[key], (name, k, key)
+        assert ref_digest(pipe.model) == want["digest"], (name, k)
+        assert pipe.store.ledger.as_dict() == want["ledger"], (name, k)
+
+    with device_bound(store_for(g["keyframes"], g["config"]["features_per_kf"] + 64)) as lm:
+        run_reference_pipeline(lm, g["config"], g["neighbor_count"], g["n1"], g["keyframes"], check, kf_cull=True,
+                               lba=g.get("lba", False))
