@@ -2180,6 +2180,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   }
   pair_acc_init<REV_THREADS>(&acc, A.cur);  // (barrier)
   const unsigned long long mpb = M.mp_rec_bytes;
+  const unsigned long long ev_base = M.ledger[LG_SMALL_EVENTS];  // (the ledger changes only at the end)
   const int mtag = M.scal[SC_MTAG];
   // install point p's speculated post-ADD state (k_fuse_post): descriptor, geometry, hit
   auto install_post = [&](int p) {
@@ -2416,7 +2417,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       npts += a_p;
       nacts += a_n;
       {  // one record_small_transfer per reverse pass, in pass order (after the forward one)
-        const unsigned long long ev0 = M.ledger[LG_SMALL_EVENTS];
+        const unsigned long long ev0 = ev_base;
         for (int t = t0 + lane; t <= te; t += 32)
           if (ev0 + t < (unsigned long long)LG_LOG_CAP) M.lg_log[ev0 + t] = (long long)s_live[t] * (long long)mpb;
       }

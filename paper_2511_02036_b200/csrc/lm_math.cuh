@@ -169,12 +169,13 @@ LM_HD void jacobi_rotate(double A[16], double V[16], int p, int q, bool& rotated
     beta += aq * aq;
     gamma += ap * aq;
   }
-  // converged pair: columns orthogonal to working precision
-  if (gamma == 0.0 || fabs(gamma) <= 1e-15 * sqrt(alpha * beta)) return;
+  // converged pair: columns orthogonal to working precision, |gamma| <= 1e-15 sqrt(alpha beta)
+  // tested squared (no sqrt on the critical path)
+  if (gamma == 0.0 || gamma * gamma <= 1e-30 * (alpha * beta)) return;
   rotated = true;
   const double zeta = (beta - alpha) / (2.0 * gamma);
   const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-  const double c = 1.0 / sqrt(1.0 + tt * tt);
+  const double c = rsqrt(1.0 + tt * tt);  // (1 ulp; positions are tolerance-pinned, 1e-4 rel)
   const double s = c * tt;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -202,11 +203,25 @@ LM_HD void null_vector4(double A[16], double v[4]) {
   double n[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) n[j] = A[j] * A[j] + A[4 + j] * A[4 + j] + A[8 + j] * A[8 + j] + A[12 + j] * A[12 + j];
+  // column of the smallest norm; selected with constant indices only (a dynamic V[best]
+  // would put A and V in local memory for the whole Jacobi loop)
   int best = 0;
+  double nb = n[0];
 #pragma unroll
   for (int j = 1; j < 4; ++j)
-    if (n[j] < n[best]) best = j;
-  double c0 = V[best], c1 = V[4 + best], c2 = V[8 + best], c3 = V[12 + best];
+    if (n[j] < nb) {
+      nb = n[j];
+      best = j;
+    }
+  double c0 = V[0], c1 = V[4], c2 = V[8], c3 = V[12];
+#pragma unroll
+  for (int j = 1; j < 4; ++j)
+    if (best == j) {
+      c0 = V[j];
+      c1 = V[4 + j];
+      c2 = V[8 + j];
+      c3 = V[12 + j];
+    }
   const double nv = sqrt(c0 * c0 + c1 * c1 + c2 * c2 + c3 * c3);
   v[0] = c0 / nv;
   v[1] = c1 / nv;
