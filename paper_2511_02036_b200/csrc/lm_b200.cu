@@ -11,6 +11,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cmath>
 #include <string>
 #include <unordered_map>
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(1024) k_stage(DevMap M, const unsigned char* b
 // ------------------------------------------------------------------- single-op map kernel
 enum MapOp { OP_NEW = 1, OP_OBS_ADD, OP_OBS_ERASE, OP_KILL, OP_REPLACE, OP_SET_COUNTS, OP_KF_KILL, OP_NEIGHBORS,
              OP_REFRESH, OP_APPLY, OP_TARGETS, OP_FUSE_PASS, OP_CULL, OP_SET_POSE, OP_PATCH_POS, OP_UPLOAD, OP_EVICT,
-             OP_MP_GET, OP_BOUND, OP_IMPORT_POINTS, OP_LEDGER_ADD, OP_CORRUPT, OP_KF_CULL };
+             OP_MP_GET, OP_BOUND, OP_IMPORT_POINTS, OP_LEDGER_ADD, OP_CORRUPT, OP_KF_CULL, OP_GEO_ALL };
 
 // kill_keyframe (mapmodel.py:275-283), whole block. The reference erases this keyframe's
 // observation of every bound point in id order; each erase touches only its own point (list,
@@ -489,12 +490,17 @@ __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, in
       // every point observed here has a ray from this camera centre in its cached
       // _point_geometry sums (fusion.py:57-94) and a cached hit: both stale now. A point
       // observes a keyframe at most once, so each is touched by one thread.
+      // Invariant kept for the stages: a live point's geometry cache is valid unless the point
+      // is listed dirty (the refresh recomputes it then); several gather threads may read one
+      // point's cache concurrently, so a stale-but-clean cache must never be left behind.
       const int off = M.kp_off[slot], n = M.kp_n[slot];
+      __syncthreads();  // (thread 0's pose writes before any geometry term reads them)
       for (int i = tid; i < n; i += 1024) {
         const int mp = M.kbind[off + i];
         if (mp >= 0) {
-          M.gval[mp] = 0;
           M.ver[mp] += 1;
+          if (M.alive[mp] && !M.dirty[mp]) geo_full(M, mp);
+          else M.gval[mp] = 0;
         }
       }
       if (tid == 0) res[0] = LM_OK;
@@ -509,8 +515,9 @@ __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, in
         M.pos[3 * mp] = x[0];
         M.pos[3 * mp + 1] = x[1];
         M.pos[3 * mp + 2] = x[2];
-        M.gval[mp] = 0;
         M.ver[mp] += 1;
+        if (!M.dirty[mp]) geo_full(M, mp);  // (see OP_SET_POSE: no stale clean caches)
+        else M.gval[mp] = 0;
       }
       if (tid == 0) res[0] = LM_OK;
       return;
@@ -586,6 +593,13 @@ __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, in
         M.scal[SC_NEXT_ID] = n;
         res[0] = LM_OK;
       }
+      return;
+    }
+    case OP_GEO_ALL: {  // view-geometry caches of every live clean point (after an import)
+      const int n = M.scal[SC_NEXT_ID];
+      for (int mp = tid; mp < n; mp += 1024)
+        if (M.alive[mp] && !M.dirty[mp] && M.nobs[mp]) geo_full(M, mp);
+      if (tid == 0) res[0] = LM_OK;
       return;
     }
     case OP_CORRUPT: {  // fault injection for the audit tests (test_mapmodel.py:238-255)
@@ -1038,50 +1052,53 @@ int lm_kf_stage(lm_ctx* ctx, int32_t map, int64_t kf_id, const double quat[4], c
 
 // ------------------------------------------------------------------- steps
 
-// per-step statistics into the running totals: both records are read whole first (their
-// fields are independent loads) and the sums written back, instead of one dependent
-// read-modify-write round trip per field
-__global__ void k_end(DevMap* maps, const StepArgs* args, lm_step_stats** totals) {
+// per-step statistics into the running totals, field-parallel: thread k adds summed field k
+// (a table of offsets), so every load is independent and nothing spills (a single thread
+// copying both records whole needed 255 registers + 600 B of spills: ~10 us per step)
+#define LM_SUM32(f) {(int)offsetof(lm_step_stats, f), 4}
+#define LM_SUM64(f) {(int)offsetof(lm_step_stats, f), 8}
+struct SumField {
+  int off, size;
+};
+__constant__ SumField k_sum_fields[] = {
+    LM_SUM32(created), LM_SUM32(conflicts), LM_SUM32(degenerate), LM_SUM32(gate_parallax), LM_SUM32(gate_depth),
+    LM_SUM32(gate_reprojection), LM_SUM32(gate_scale), LM_SUM32(n_neighbors), LM_SUM32(n_targets),
+    LM_SUM32(merged), LM_SUM32(observations_added), LM_SUM32(stale), LM_SUM32(culled), LM_SUM32(n_candidates),
+    LM_SUM64(match_pairs), LM_SUM64(fuse_bytes), LM_SUM64(fuse_passes), LM_SUM64(fuse_points),
+    LM_SUM64(fuse_actions), LM_SUM64(apply_rounds), LM_SUM64(rev_passes_acting), LM_SUM64(rev_passes_redo),
+    LM_SUM64(fuse_bytes_rev), LM_SUM64(rev_mergeable),
+#define LM_ARR(f, k) {(int)(offsetof(lm_step_stats, f) + 8 * (k)), 8}
+    LM_ARR(fuse_cycles, 0), LM_ARR(fuse_cycles, 1), LM_ARR(fuse_cycles, 2), LM_ARR(fuse_cycles, 3),
+    LM_ARR(fuse_cycles, 4), LM_ARR(fuse_cycles, 5), LM_ARR(fuse_cycles, 6), LM_ARR(fuse_cycles, 7),
+    LM_ARR(fuse_cycles, 8), LM_ARR(fuse_cycles, 9), LM_ARR(fuse_cycles, 10), LM_ARR(fuse_cycles, 11),
+    LM_ARR(fuse_cycles, 12), LM_ARR(fuse_cycles, 13), LM_ARR(fuse_cycles, 14), LM_ARR(fuse_cycles, 15),
+    LM_ARR(dbg, 0), LM_ARR(dbg, 1), LM_ARR(dbg, 2), LM_ARR(dbg, 3), LM_ARR(dbg, 4), LM_ARR(dbg, 5),
+    LM_ARR(dbg, 6), LM_ARR(dbg, 7), LM_ARR(dbg, 8), LM_ARR(dbg, 9), LM_ARR(dbg, 10), LM_ARR(dbg, 11),
+    LM_ARR(dbg, 12), LM_ARR(dbg, 13), LM_ARR(dbg, 14), LM_ARR(dbg, 15),
+    LM_ARR(borderline, 0), LM_ARR(borderline, 1), LM_ARR(borderline, 2), LM_ARR(borderline, 3),
+#undef LM_ARR
+};
+#undef LM_SUM32
+#undef LM_SUM64
+constexpr int kSumFields = sizeof(k_sum_fields) / sizeof(SumField);
+
+__global__ void __launch_bounds__(128) k_end(DevMap* maps, const StepArgs* args, lm_step_stats** totals) {
   pdl_enter();
   const DevMap& M = maps[args[blockIdx.x].map];
-  if (threadIdx.x) return;
-  lm_step_stats* st = M.s.stats;
-  lm_step_stats* t = totals[args[blockIdx.x].map];
-  const int err = M.scal[SC_ERR], soft = M.scal[SC_SOFT];
-  lm_step_stats s = *st;
-  lm_step_stats u = *t;
-  s.error = err ? err : soft;
-  u.created += s.created;
-  u.conflicts += s.conflicts;
-  u.degenerate += s.degenerate;
-  u.gate_parallax += s.gate_parallax;
-  u.gate_depth += s.gate_depth;
-  u.gate_reprojection += s.gate_reprojection;
-  u.gate_scale += s.gate_scale;
-  u.n_neighbors += s.n_neighbors;
-  u.n_targets += s.n_targets;
-  u.merged += s.merged;
-  u.observations_added += s.observations_added;
-  u.stale += s.stale;
-  u.culled += s.culled;
-  u.error = err;
-  u.n_candidates += s.n_candidates;
-  u.match_pairs += s.match_pairs;
-  u.fuse_bytes += s.fuse_bytes;
-  u.fuse_passes += s.fuse_passes;
-  u.fuse_points += s.fuse_points;
-  u.fuse_actions += s.fuse_actions;
-  u.apply_rounds += s.apply_rounds;
-  for (int k = 0; k < 16; ++k) u.fuse_cycles[k] += s.fuse_cycles[k];
-  u.rev_passes_acting += s.rev_passes_acting;
-  u.rev_passes_redo += s.rev_passes_redo;
-  u.fuse_bytes_rev += s.fuse_bytes_rev;
-  u.rev_mergeable += s.rev_mergeable;
-  for (int k = 0; k < 16; ++k) u.dbg[k] += s.dbg[k];
-  for (int k = 0; k < 4; ++k) u.borderline[k] += s.borderline[k];
-  u.first_new_id += 1;  // steps accumulated
-  st->error = s.error;
-  *t = u;
+  char* st = (char*)M.s.stats;
+  char* t = (char*)totals[args[blockIdx.x].map];
+  const int k = threadIdx.x;
+  if (k < kSumFields) {
+    const SumField f = k_sum_fields[k];
+    if (f.size == 4) *(int*)(t + f.off) += *(const int*)(st + f.off);
+    else *(long long*)(t + f.off) += *(const long long*)(st + f.off);
+  } else if (k == kSumFields) {
+    const int err = M.scal[SC_ERR], soft = M.scal[SC_SOFT];
+    const int e = err ? err : soft;
+    ((lm_step_stats*)st)->error = e;
+    ((lm_step_stats*)t)->error = err;
+    ((lm_step_stats*)t)->first_new_id += 1;  // steps accumulated
+  }
 }
 
 static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args) {
@@ -1181,7 +1198,7 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   CU(launch_k(ctx, k_fuse_rev, dim3(n), dim3(REV_THREADS), rev_smem, 0, dmaps, dv, (int)rev_smem));
   if ((rc = mark())) return rc;
   CU(launch_k(ctx, k_fuse_visible, dim3((kpkf + 255) / 256, tfuse, n), dim3(256), 0, 0, dmaps, dv));
-  CU(launch_k(ctx, k_end, dim3(n), dim3(32), 0, 0, dmaps, dv, ctx->d_totals));
+  CU(launch_k(ctx, k_end, dim3(n), dim3(128), 0, 0, dmaps, dv, ctx->d_totals));
   if ((rc = mark())) return rc;
   ctx->launches += 18;
   if (ctx->prof) ctx->prof_steps.push_back(evs);
@@ -1220,6 +1237,10 @@ static int fill_args(lm_ctx* ctx, HostMap* m, int64_t kf_id, const lm_step_param
     a.cc = p->cull;
   }
   if (a.n_nbr_req > NMAX) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "neighbor_count > %d", NMAX);
+  // the new keyframe's covisibility row is empty unless it was staged with pre-bound slots,
+  // so neighbour selection does not depend on the cull (LM_SELECT_EARLY=0 disables)
+  static const bool early_ok = getenv("LM_SELECT_EARLY") == nullptr || atoi(getenv("LM_SELECT_EARLY")) != 0;
+  a.select_early = early_ok && a.do_create && !a.explicit_nbr && (!a.do_cull || (a.do_insert && !m->prebound[slot]));
   if (a.do_fuse && a.fc.n1 + a.fc.n1 * a.fc.n2 > TMAX)
     return fail(ctx, LM_ERR_INVALID_ARGUMENT, "n1 + n1*n2 > %d", TMAX);
   return LM_OK;
@@ -2330,8 +2351,16 @@ int lm_import_snapshot(lm_ctx* ctx, int32_t map, const lm_snapshot* S) {
     if (S->kf_resident && S->kf_resident[k] && (rc = lm_kf_upload(ctx, map, S->kf_id[k]))) return rc;
     off += n;
   }
-  // representative descriptors and sorted lists: refresh every dirty point now
+  // representative descriptors and sorted lists: refresh every dirty point now; then every
+  // point's view-geometry cache (the stages expect clean points to carry valid caches)
   if ((rc = refresh(ctx, m, map))) return rc;
+  {
+    OpArgs a;
+    memset(&a, 0, sizeof a);
+    a.op = OP_GEO_ALL;
+    int res[1];
+    if ((rc = run_op(ctx, m, map, a, res, 1))) return rc;
+  }
   unsigned long long lg[LG_N] = {0};
   lg[LG_PERSIST] = S->ledger.persistent_bytes_up;
   lg[LG_NAIVE] = S->ledger.naive_bytes_up;

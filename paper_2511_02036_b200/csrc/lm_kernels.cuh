@@ -37,6 +37,7 @@ struct StepArgs {
   int n_nbr_req;      // neighbor_count
   int do_insert, do_cull, do_create, do_fuse;
   int do_upload;      // with do_insert: also DeviceStore.upload_keyframe (residency + ledger)
+  int select_early;   // k_select may run concurrently with k_cull (see k_select)
   int processed;      // pipeline._processed
   int explicit_nbr;   // lm_search: neighbour list given (nbr0), masks optional
   int nbr0;
@@ -355,8 +356,7 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
 
 // ---------------------------------------------------------------------------------- select
 
-__global__ void __launch_bounds__(256) k_select(DevMap* maps, const StepArgs* args, int n_slots_max) {
-  pdl_enter();
+__device__ __forceinline__ void k_select_body(DevMap* maps, const StepArgs* args, int n_slots_max) {
   const StepArgs& A = args[blockIdx.x];
   const DevMap& M = maps[A.map];
   if (!A.do_create) return;
@@ -432,6 +432,20 @@ __global__ void __launch_bounds__(256) k_select(DevMap* maps, const StepArgs* ar
     if (!A.explicit_nbr) M.ledger[LG_NAIVE] += naive;
   }
 }
+
+// With select_early (a freshly inserted keyframe without pre-bound slots: its covisibility
+// row is empty, so the ranking reads nothing the recent-point cull writes) this kernel runs
+// concurrently with k_cull: it lets its successor launch at once and waits for its
+// predecessor (k_cull) only at the very end, so its own completion still implies k_cull's
+// and the launch chain stays ordered.
+__global__ void __launch_bounds__(256) k_select(DevMap* maps, const StepArgs* args, int n_slots_max) {
+  const bool early = args[blockIdx.x].select_early != 0;
+  if (early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  else pdl_enter();
+  k_select_body(maps, args, n_slots_max);
+  if (early) asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 
 // ---------------------------------------------------------------------------------- prep
 
@@ -1639,11 +1653,18 @@ __device__ __forceinline__ long long pass_bytes(long long pts, long long obs, lo
 
 enum FuseCtl { FC_T = 0, FC_P = 1, FC_NACT = 2, FC_NU = 3, FC_NSP = 4, FC_N = 8 };
 
+// Starts while its predecessor (k_commit_write: the new points' records and the current
+// keyframe's new bindings) still runs: target selection reads only covisibility, which
+// k_commit wrote before k_commit_write started; the wait comes right before the current
+// keyframe's bound points are read (and on every exit path, so completion stays ordered).
 __global__ void __launch_bounds__(1024) k_fuse_targets(DevMap* maps, const StepArgs* args, int n_slots_max) {
-  pdl_enter();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const StepArgs& A = args[blockIdx.x];
   const DevMap& M = maps[A.map];
-  if (!A.do_fuse) return;
+  if (!A.do_fuse) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
   extern __shared__ unsigned long long dynk[];
   unsigned long long* sh_key = dynk;
   int* sh_slot = (int*)(dynk + M.kf_cap);
@@ -1661,6 +1682,7 @@ __global__ void __launch_bounds__(1024) k_fuse_targets(DevMap* maps, const StepA
   }
   __shared__ unsigned long long s_tkp;
   if (threadIdx.x == 0) s_tkp = 0;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // k_commit_write's bindings from here on
   const int P = T ? bound_points<1024>(M, A.cur, sh) : 0;  // (barriers)
   {  // keypoints of the targets, block-parallel
     int tk = 0;

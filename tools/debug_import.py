@@ -44,3 +44,15 @@ for i in range(n):
         break
 print("bad", bad, "stats", dev.stats, dev.fused, dev.culled)
 print("ref recent after", len(w.pipe._recent), "dev recent", len(dev.recent()))
+print("borderline (epi, gates, fusion, rint) after the imported step:", list(dev.totals().borderline))
+# the same keyframe natively from an empty map, for comparison
+nat = LocalMapper(intr, neighbor_count=20, match=MatchConfig(neighbor_count=20), fuse=FuseConfig(n1=20, n2=5),
+                  store=store_for(200, 1264))
+for k in range(101):
+    nat.process(device_kf(seq.records[k], intr))
+t = nat.totals()
+print("native run 0..100 borderline", list(t.borderline))
+sn = nat.snapshot(with_covis=False)
+for i in (902, 1292, 2010):
+    print(i, "native vis", int(sn.visible[i]), "import vis", int(s.visible[i]), "ref", m.points[i].visible_count,
+          "pos native-ref", np.abs(sn.pos[i] - m.points[i].position).max())
