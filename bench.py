@@ -607,6 +607,9 @@ def run_c5(args, rank, world, local, dist):
     # single-CTA fusion kernels overlap the other group's wide kernels
     ngroups = max(1, min(args.c5_groups, len(seqs)))
     ctxs = [_lib.Context.get(local)] + [_lib.Context(local) for _ in range(ngroups - 1)]
+    if ngroups > 1:  # concurrent groups: no programmatic dependent launch (parked successor CTAs
+        for c in ctxs:  # of one group's chain would hold SMs the other groups' kernels need)
+            c.call("lm_ctx_set_pdl", 0)
     ctx = ctxs[0]
     lib = ctx.lib
     mappers, kf_lists, owner, kf_objs = [], [], [], []

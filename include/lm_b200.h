@@ -169,6 +169,10 @@ int lm_map_reset(lm_ctx* ctx, int32_t map); /* back to an empty map, arenas kept
 int lm_map_destroy(lm_ctx* ctx, int32_t map); /* free the map's arenas (index not reused) */
 int lm_map_sizes_get(lm_ctx* ctx, int32_t map, lm_map_sizes* out);
 int lm_synchronize(lm_ctx* ctx);
+/* programmatic dependent launch of the step kernels: 1 on, 0 off, -1 default (on for
+ * single-map launch sequences); turn it off when several contexts step concurrently on one
+ * device (a chain's parked successor CTAs hold SMs the other streams need) */
+int lm_ctx_set_pdl(lm_ctx* ctx, int32_t mode);
 
 /* ---- keyframes ---- */
 /* Copy a keyframe into the map's pool without inserting it (not visible to any stage).

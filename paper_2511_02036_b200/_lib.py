@@ -127,6 +127,7 @@ _SIGS = {
     "lm_map_destroy": ([C.c_void_p, i32], i32),
     "lm_map_sizes_get": ([C.c_void_p, i32, P(MapSizes)], i32),
     "lm_synchronize": ([C.c_void_p], i32),
+    "lm_ctx_set_pdl": ([C.c_void_p, i32], i32),
     "lm_kf_stage": ([C.c_void_p, i32, i64, P(f64), P(f64), P(f64), i32, P(f64), P(f64), P(i64), P(u8), P(i64)], i32),
     "lm_kf_record_bytes": ([i32, C.c_uint32], C.c_uint64),
     "lm_kf_stage_record": ([C.c_void_p, i32, C.c_void_p, C.c_uint64, P(i64)], i32),
