@@ -1247,8 +1247,6 @@ static int fill_args(lm_ctx* ctx, HostMap* m, int64_t kf_id, const lm_step_param
   // so neighbour selection does not depend on the cull (LM_SELECT_EARLY=0 disables)
   static const bool early_ok = getenv("LM_SELECT_EARLY") == nullptr || atoi(getenv("LM_SELECT_EARLY")) != 0;
   a.select_early = early_ok && a.do_create && !a.explicit_nbr && (!a.do_cull || (a.do_insert && !m->prebound[slot]));
-  static const bool rev_tiles = getenv("LM_REV_TILES") == nullptr || atoi(getenv("LM_REV_TILES")) != 0;
-  a.rev_tiles = rev_tiles;
   if (a.do_fuse && a.fc.n1 + a.fc.n1 * a.fc.n2 > TMAX)
     return fail(ctx, LM_ERR_INVALID_ARGUMENT, "n1 + n1*n2 > %d", TMAX);
   return LM_OK;

@@ -38,7 +38,6 @@ struct StepArgs {
   int do_insert, do_cull, do_create, do_fuse;
   int do_upload;      // with do_insert: also DeviceStore.upload_keyframe (residency + ledger)
   int select_early;   // k_select may run concurrently with k_cull (see k_select)
-  int rev_tiles;      // k_fuse_rev direct passes: 8 lanes per action (LM_REV_TILES=0: a warp each)
   int processed;      // pipeline._processed
   int explicit_nbr;   // lm_search: neighbour list given (nbr0), masks optional
   int nbr0;
@@ -2195,7 +2194,6 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   pair_acc_init<REV_THREADS>(&acc, A.cur);  // (barrier)
   const unsigned long long mpb = M.mp_rec_bytes;
   const unsigned long long ev_base = M.ledger[LG_SMALL_EVENTS];  // (the ledger changes only at the end)
-  const bool direct_tiles = A.rev_tiles != 0;
   const int mtag = M.scal[SC_MTAG];
   // install point p's speculated post-ADD state (k_fuse_post): descriptor, geometry, hit
   auto install_post = [&](int p) {
@@ -2398,144 +2396,6 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       if (!spec) atomicAdd(&s_nset, 1);
     }
     __syncwarp();
-  };
-  // add_direct with DT (8) lanes per action: four actions per warp at once (a direct pass's
-  // actions touch disjoint entities, so they are independent; each is a chain of L2 round
-  // trips, and 16 warps x 1 action left most of the pass's actions waiting for a warp)
-  constexpr int DT = 8;
-  auto add_direct8 = [&](const ActRec x, int k, int t1, int tag, const cg::thread_block_tile<DT>& tile) {
-    const int lane = (int)tile.thread_rank();
-    const int p = x.pid, j = x.j;
-    const int n = M.nobs[p], off = M.ooff[p], cap = M.ocap[p];
-    const int dirty = M.dirty[p], gv = M.gval[p], vr = M.ver[p], found = M.found[p];
-    const int lev = TV.lev[j];
-    const int stag = M.sp_tag[p], sv0 = M.sp_ver0[p], sn0 = M.sp_nobs0[p], sj = M.sp_j[p];
-    const double px = M.pos[3 * p], py = M.pos[3 * p + 1], pz = M.pos[3 * p + 2];
-    const double lo = M.glo[p], hi = M.ghi[p];
-    const double ax = M.gacc[3 * p], ay = M.gacc[3 * p + 1], az = M.gacc[3 * p + 2];
-    int* cntp = M.counts + (size_t)p * M.L + lev;
-    const int cv = *cntp;
-    const double Sl = M.S[lev];
-    const int hc = M.s.hl_cnt[j];
-    const int hp = lane < hc && lane < HL ? M.s.hl[j * HL + lane] : -1;
-    const int hp2 = lane + DT < hc && lane + DT < HL ? M.s.hl[j * HL + lane + DT] : -1;
-    const int2* o = M.obs + off;
-    const int2 e0 = lane < n ? o[lane] : make_int2(cur, 0), e1 = lane + DT < n ? o[lane + DT] : make_int2(cur, 0);
-    const int o0 = e0.x, o1 = e1.x;
-    const int last = n ? o[n - 1].x : -1;
-    // the point's items in passes after t1 (its observations after the ADD: the old ones and
-    // (cur, j)), and the points hitting j (hit list): their hits are unchanged by the apply
-    const int tt0 = M.s.pass_of[o0], tt1 = M.s.pass_of[o1], ttc = lane == 0 ? M.s.pass_of[cur] : -1;
-    const bool hq = hp >= 0 && M.alive[hp] && M.hit[hp].y == j;
-    const bool hq2 = hp2 >= 0 && M.alive[hp2] && M.hit[hp2].y == j;
-    if (lane < n && tt0 > t1) add_item(tt0, e0.y, tag);
-    if (lane + DT < n && tt1 > t1) add_item(tt1, e1.y, tag);
-    if (ttc > t1) add_item(ttc, j, tag);
-    for (int e = lane + 2 * DT; e < n; e += DT) {
-      const int2 ob = o[e];
-      const int tt = M.s.pass_of[ob.x];
-      if (tt > t1) add_item(tt, ob.y, tag);
-    }
-    // hit-list points' items (their state is unchanged): entries lane and lane + DT
-    const unsigned hm1 = tile.ballot(hq && atomicExch(&M.s.rmark[hp], tag) != tag);
-    const unsigned hm2 = tile.ballot(hq2 && atomicExch(&M.s.rmark[hp2], tag) != tag);
-    for (int half = 0; half < 2; ++half) {
-      unsigned hm = half ? hm2 : hm1;
-      while (hm) {
-        const int src = __ffs(hm) - 1;
-        hm &= hm - 1;
-        const int q = tile.shfl(half ? hp2 : hp, src);
-        if (lane == 0) M.s.cands[atomicAdd(&nc_sh, 1)] = q;
-        const int2* oq = M.obs + M.ooff[q];
-        const int nq = M.nobs[q];
-        for (int e = lane; e < nq; e += DT) {
-          const int2 ob = oq[e];
-          const int tt = M.s.pass_of[ob.x];
-          if (tt > t1) add_item(tt, ob.y, tag);
-        }
-      }
-    }
-    if (hc > HL) {  // overflowed list: scan the passes of the keypoint's bitmap
-      for (int w = 0; w < HPW; ++w) {
-        unsigned bits = M.s.hitpass[j * HPW + w];
-        while (bits) {
-          const int tt = 32 * w + __ffs(bits) - 1;
-          bits &= bits - 1;
-          if (tt <= t1 || tt >= T) continue;
-          const int nn = M.kp_n[M.s.targets[tt]];
-          const int* pjt = M.s.pj + (size_t)tt * K;
-          for (int kp = lane; kp < nn; kp += DT)
-            if (pjt[kp] == j) add_item(tt, kp, tag);
-        }
-      }
-    }
-    const bool spec = stag == mtag && sv0 == vr && sn0 == n && sj == j;
-    covis_add(M, cur, o0, +1, &acc);
-    covis_add(M, cur, o1, +1, &acc);
-    for (int e = lane + 2 * DT; e < n; e += DT) covis_add(M, cur, o[e].x, +1, &acc);
-    int2* dst = nullptr;
-    if (lane == 0) {
-      dst = M.obs + off;
-      if (n == cap) {
-        const int nc = cap < 4 ? 4 : 2 * cap;
-        const int noff = atomicAdd(&M.scal[SC_OBS_HEAD], nc);
-        if (noff + nc > M.obs_cap) {
-          set_err(M, LM_ERR_CAPACITY);  // (the step fails; the record is left as it was)
-          dst = nullptr;
-        } else {
-          copy_obs(M.obs + noff, o, n);
-          M.ooff[p] = noff;
-          M.ocap[p] = nc;
-          dst = M.obs + noff;
-        }
-      }
-    }
-    if (lane == 0 && dst) {
-      dst[n] = make_int2(cur, j);
-      M.nobs[p] = n + 1;
-      M.kbind[cur_off + j] = p;
-      *cntp = cv + 1;
-      M.ver[p] = vr + 1;
-      M.found[p] = found + 1;
-      if (spec) {
-        const uint4 r0 = M.sp_rep[2 * (size_t)p], r1 = M.sp_rep[2 * (size_t)p + 1];
-        const double* sg = M.sp_geo + 5 * (size_t)p;
-        const double g0 = sg[0], g1 = sg[1], g2 = sg[2], g3 = sg[3], g4 = sg[4];
-        const int sh_ = M.sp_hit[p];
-        M.rep[2 * (size_t)p] = r0;
-        M.rep[2 * (size_t)p + 1] = r1;
-        M.gacc[3 * p] = g0;
-        M.gacc[3 * p + 1] = g1;
-        M.gacc[3 * p + 2] = g2;
-        M.glo[p] = g3;
-        M.ghi[p] = g4;
-        M.gval[p] = 1;
-        M.dirty[p] = 0;
-        M.hit[p] = make_int2(vr + 1, sh_);
-        hit_list_add(M, sh_, p);
-        atomicAdd((unsigned long long*)&M.s.stats->dbg[12], 1ull);
-      } else {
-        mark_dirty_owned(M, p, dirty);
-        const long long kf_last = last >= 0 ? M.kf_id[last] : -1;
-        if (gv && !dirty && (n == 0 || kf_last < kf_cur)) {
-          const double rx = px - cur_pose[12], ry = py - cur_pose[13], rz = pz - cur_pose[14];
-          const double dd = sqrt(rx * rx + ry * ry + rz * rz);
-          if (dd > 0) {  // geo_term
-            const double d0 = dd / Sl;
-            M.glo[p] = d0 < lo ? d0 : lo;
-            M.ghi[p] = d0 > hi ? d0 : hi;
-            M.gacc[3 * p] = ax + rx / dd;
-            M.gacc[3 * p + 1] = ay + ry / dd;
-            M.gacc[3 * p + 2] = az + rz / dd;
-          }
-        } else {
-          M.gval[p] = 0;
-        }
-      }
-      s_inst[k] = spec;
-      if (!spec) atomicAdd(&s_nset, 1);
-    }
-    tile.sync();
   };
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int AW = (K + 31) >> 5;  // words of a pass's action bitmap
@@ -2760,12 +2620,9 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       // point taking its speculated post-ADD state at once. The changed current keypoints are
       // exactly the actions' keypoints, and an ADD only adds an observation, so the touched
       // items are the points' observations after the apply.
-      if (direct_tiles) {
-        const cg::thread_block_tile<DT> tile = cg::tiled_partition<DT>(cg::this_thread_block());
-        for (int k = threadIdx.x / DT; k < na; k += REV_THREADS / DT) add_direct8(s_acts[k], k, t1, tag, tile);
-      } else {
-        for (int k = wid; k < na; k += REV_THREADS / 32) add_direct(s_acts[k], k, t1, tag);
-      }
+      // (8 lanes per action, four actions per warp, measured 5% slower on C2: more registers
+      // spilled and the tile syncs; a warp per action stays)
+      for (int k = wid; k < na; k += REV_THREADS / 32) add_direct(s_acts[k], k, t1, tag);
       __syncthreads();
       if (threadIdx.x == 0) {
         cnt[1] += na;
