@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(256) k_prep(DevMap* maps, const StepArgs* args
 // non-matching pair, so the second half and the fp64 epipolar test run only on survivors.
 // The running minimum is the lexicographic (dist, j) key of the reference's first-argmin;
 // warp slices combine with a shared atomicMin, neighbour one-to-one with a global one.
-__global__ void __launch_bounds__(MATCH_WARPS * 32) k_match(DevMap* maps, const StepArgs* args) {
+__global__ void __launch_bounds__(MATCH_WARPS * 32, 5) k_match(DevMap* maps, const StepArgs* args) {
   pdl_enter();
   const StepArgs& A = args[blockIdx.z];
   const DevMap& M = maps[A.map];
