@@ -630,7 +630,7 @@ __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, in
 
 static int run_op(lm_ctx* ctx, HostMap* m, int map, OpArgs& a, int* res_host, int nres) {
   a.n_slots = m->n_slots;
-  const size_t dyn = 12 * (size_t)m->d.kf_cap;
+  const size_t dyn = 13 * (size_t)m->d.kf_cap + 16;  // ranked slots (12 B/slot) + target flags
   k_op<<<1, 1024, dyn, ctx->stream>>>(ctx->d_maps, map, a, m->d_result);
   CHECK_LAUNCH();
   ctx->launches += 1;
@@ -653,7 +653,7 @@ static int io_reserve(lm_ctx* ctx, HostMap* m, size_t bytes) {
 // fire-and-forget op (its status is validated on the host): no result readback, no sync
 static int run_op_async(lm_ctx* ctx, HostMap* m, int map, OpArgs& a) {
   a.n_slots = m->n_slots;
-  const size_t dyn = 12 * (size_t)m->d.kf_cap;
+  const size_t dyn = 13 * (size_t)m->d.kf_cap + 16;
   k_op<<<1, 1024, dyn, ctx->stream>>>(ctx->d_maps, map, a, m->d_result);
   CHECK_LAUNCH();
   ctx->launches += 1;
@@ -734,9 +734,9 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
     ctx->d_stage[i] = nullptr;
   }
   CU(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-  CU(cudaFuncSetAttribute(k_fuse_targets, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+  CU(cudaFuncSetAttribute(k_fuse_targets, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
   CU(cudaFuncSetAttribute(k_fuse_rev, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-  CU(cudaFuncSetAttribute(k_op, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+  CU(cudaFuncSetAttribute(k_op, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
   CU(cudaFuncSetAttribute(k_fuse_apply, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CU(cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, CULL_DYN_SMEM));
   if (const char* e = getenv("LM_CARVEOUT")) {  // (experiments) shared-memory carve-out hint, percent
@@ -1176,7 +1176,7 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   CU(launch_k(ctx, k_commit, dim3(n), dim3(1024), 0, 0, dmaps, dv));
   CU(launch_k(ctx, k_commit_write, dim3((kpkf + 127) / 128, NMAX, n), dim3(128), 0, 0, dmaps, dv));
   if ((rc = mark())) return rc;
-  CU(launch_k(ctx, k_fuse_targets, dim3(n), dim3(1024), dyn, 0, dmaps, dv, slots));
+  CU(launch_k(ctx, k_fuse_targets, dim3(n), dim3(1024), dyn + kfcap + 16, 0, dmaps, dv, slots));
   if ((rc = mark())) return rc;
   CU(launch_k(ctx, k_fuse_geo, dim3((kpkf + 7) / 8, n), dim3(256), 0, 0, dmaps, dv));
   if ((rc = mark())) return rc;

@@ -741,32 +741,87 @@ __global__ void __launch_bounds__(1024) k_commit(DevMap* maps, const StepArgs* a
   __syncthreads();
   const int total = coff[nn];
   const int cur = A.cur;
-  // outcome of candidate g: 0 created, 1 conflict, 2+ failure status
-  auto outcome = [&](int g, int& r, int& k) -> int {
-    r = 0;
-    while (coff[r + 1] <= g) ++r;
+  // outcome of candidate g: 0 created, 1 conflict, 2+ failure status. Every thread's
+  // candidates (g = tid + 1024 q) are classified once, their loads issued together, and kept
+  // in registers for the ranking pass below (candidate totals beyond CQ*1024 fall back to
+  // recomputing).
+  constexpr int CQ = 8;
+  auto locate = [&](int g, int& r, int& k) {
+    int lo = 0, hi = nn;  // largest r with coff[r] <= g (binary search over <= 64 neighbours)
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (coff[mid] <= g) lo = mid;
+      else hi = mid;
+    }
+    r = lo;
     k = g - coff[r];
+  };
+  auto outcome = [&](int g, int& r, int& k) -> int {
+    locate(g, r, k);
     const size_t e = (size_t)r * M.kpkf_max + k;
     const int i = M.s.cand_i[e];
     if (M.s.win_rank[i] < r) return 1;
     const int st = M.s.cand_st[e];
     return st == CS_PASS ? 0 : 1 + st;
   };
-  // pass 1: totals and capacity
-  int c_created = 0, c_conf = 0, c_deg = 0, c_g[5] = {0, 0, 0, 0, 0};
-  for (int g = threadIdx.x; g < total; g += 1024) {
-    int r, k;
-    const int oc = outcome(g, r, k);
-    if (oc == 0) ++c_created;
-    else if (oc == 1) ++c_conf;
-    else if (oc == 1 + CS_DEGEN) ++c_deg;
-    else ++c_g[oc - 1];
+  int ocs[CQ], rs[CQ], ks[CQ];
+  {
+    int ci[CQ], cst[CQ];
+#pragma unroll
+    for (int q = 0; q < CQ; ++q) {
+      const int g = threadIdx.x + 1024 * q;
+      rs[q] = ks[q] = 0;
+      ci[q] = 0;
+      cst[q] = 0;
+      if (g < total) {
+        locate(g, rs[q], ks[q]);
+        const size_t e = (size_t)rs[q] * M.kpkf_max + ks[q];
+        ci[q] = M.s.cand_i[e];
+        cst[q] = M.s.cand_st[e];
+      }
+    }
+    int wr[CQ];
+#pragma unroll
+    for (int q = 0; q < CQ; ++q) wr[q] = threadIdx.x + 1024 * q < total ? M.s.win_rank[ci[q]] : 0;
+#pragma unroll
+    for (int q = 0; q < CQ; ++q)
+      ocs[q] = threadIdx.x + 1024 * q >= total ? -1 : (wr[q] < rs[q] ? 1 : (cst[q] == CS_PASS ? 0 : 1 + cst[q]));
   }
-  const int created = block_sum<1024>(c_created, sh);
-  const int conflicts = block_sum<1024>(c_conf, sh);
-  const int degen = block_sum<1024>(c_deg, sh);
+  // pass 1: totals and capacity (one combined block reduction)
+  int cnt7[7] = {0, 0, 0, 0, 0, 0, 0};  // created, conflicts, degenerate, parallax, depth, reproj, scale
+  auto tally = [&](int oc) {  // (constant indices only: the counters stay in registers)
+#pragma unroll
+    for (int c = 0; c < 7; ++c) {
+      const int want = c == 0 ? 0 : c == 1 ? 1 : c == 2 ? 1 + CS_DEGEN : 1 + (c - 2);
+      cnt7[c] += oc == want;
+    }
+  };
+#pragma unroll
+  for (int q = 0; q < CQ; ++q) tally(ocs[q]);
+  for (int g = threadIdx.x + 1024 * CQ; g < total; g += 1024) {
+    int r, k;
+    tally(outcome(g, r, k));
+  }
+  __shared__ int red[32][7];
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int c = 0; c < 7; ++c) {
+      int v = cnt7[c];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[wid][c] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 7) {
+      int v = 0;
+      for (int w = 0; w < 32; ++w) v += red[w][threadIdx.x];
+      red[0][threadIdx.x] = v;  // (row 0 read back by thread threadIdx.x only, then synced)
+    }
+    __syncthreads();
+  }
+  const int created = red[0][0], conflicts = red[0][1], degen = red[0][2];
   int gates[4];
-  for (int q = 0; q < 4; ++q) gates[q] = block_sum<1024>(c_g[q + 1], sh);
+  for (int q = 0; q < 4; ++q) gates[q] = red[0][3 + q];
   const int id0 = M.scal[SC_NEXT_ID];
   const int obs0 = M.scal[SC_OBS_HEAD];
   const int rec0 = M.scal[SC_RECENT_N];
@@ -788,10 +843,20 @@ __global__ void __launch_bounds__(1024) k_commit(DevMap* maps, const StepArgs* a
   }
   {
     int run = 0;
-    for (int b0 = 0; b0 < total; b0 += 1024) {
+    for (int b0 = 0, q = 0; b0 < total; b0 += 1024, ++q) {
       const int g = b0 + threadIdx.x;
       int r = 0, k = 0, oc = -1;
-      if (g < total) oc = outcome(g, r, k);
+      if (q < CQ) {
+#pragma unroll
+        for (int u = 0; u < CQ; ++u)
+          if (u == q) {
+            oc = ocs[u];
+            r = rs[u];
+            k = ks[u];
+          }
+      } else if (g < total) {
+        oc = outcome(g, r, k);
+      }
       int tot;
       const int at = block_excl_scan<1024>(oc == 0, sh, tot);
       if (g < total) M.s.crank[(size_t)r * M.kpkf_max + k] = okcap && oc == 0 ? run + at : -1;
@@ -1513,12 +1578,13 @@ __device__ int fusion_targets(const DevMap& M, int cur, int n1, int n2, int n_sl
   __shared__ int first[TMAX];
   __shared__ int tlist[TMAX];
   __shared__ int n_first, n_t;
-  __shared__ unsigned seen[128];  // kf_cap <= 4096 slots
+  // per slot: already a target (plain byte stores), in the dynamic area after sh_slot
+  unsigned char* seen = (unsigned char*)(sh_slot + M.kf_cap);
   constexpr int HR = 64;          // rows whose 32 best-ranked entries are kept in shared memory
   __shared__ int head[HR][32], hcnt[HR];
   const int nf = ranked_neighbors<BLOCK>(M, cur, n1 < TMAX ? n1 : TMAX, sh_slot, sh_key, first, n_slots);
   if (threadIdx.x == 0) n_first = nf;
-  if (threadIdx.x < 128) seen[threadIdx.x] = 0;
+  for (int k = threadIdx.x; k < n_slots; k += BLOCK) seen[k] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const size_t stride = 3 * (size_t)M.kf_cap + 1;
@@ -1529,21 +1595,30 @@ __device__ int fusion_targets(const DevMap& M, int cur, int n1, int n2, int n_sl
     const int row_slot = first[f];
     const int* row = M.covis + (size_t)row_slot * M.kf_cap;
     int c = 0;
-    for (int s0 = 0; s0 < n_slots; s0 += 32) {
-      const int s = s0 + lane;
-      int w = 0;
-      bool take = false;
-      if (s < n_slots) {
-        w = row[s];
-        take = s != row_slot && w >= M.min_w && w > 0 && M.kf_state[s] == KF_LIVE;
+    constexpr int PF = 8;  // row chunks whose loads are issued together (one L2 round trip per 8)
+    for (int s00 = 0; s00 < n_slots; s00 += 32 * PF) {
+      int wv[PF], st[PF];
+      long long kid[PF];
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        const int s = s00 + 32 * u + lane;
+        wv[u] = s < n_slots ? row[s] : 0;
+        st[u] = s < n_slots ? M.kf_state[s] : 0;
+        kid[u] = s < n_slots ? M.kf_id[s] : 0;
       }
-      const unsigned bal = __ballot_sync(0xffffffffu, take);
-      if (take) {
-        const int at = c + __popc(bal & ((1u << lane) - 1));
-        buf[1 + at] = s;
-        keys[at] = covis_key(M, s, w);
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        const int s = s00 + 32 * u + lane;
+        const int w = wv[u];
+        const bool take = s < n_slots && s != row_slot && w >= M.min_w && w > 0 && st[u] == KF_LIVE;
+        const unsigned bal = __ballot_sync(0xffffffffu, take);
+        if (take) {
+          const int at = c + __popc(bal & ((1u << lane) - 1));
+          buf[1 + at] = s;
+          keys[at] = ((unsigned long long)(0x7fffffff - w) << 32) | (unsigned)kid[u];  // covis_key
+        }
+        c += __popc(bal);
       }
-      c += __popc(bal);
     }
     __syncwarp();
     for (int e = lane; e < c; e += 32) {
@@ -1563,9 +1638,9 @@ __device__ int fusion_targets(const DevMap& M, int cur, int n1, int n2, int n_sl
   if (wid == 0) {  // the dependent walk, one warp: lanes test 32 ranked candidates at once
     for (int f = lane; f < n_first; f += 32) {
       tlist[f] = first[f];
-      atomicOr(&seen[first[f] >> 5], 1u << (first[f] & 31));
+      seen[first[f]] = 1;
     }
-    if (lane == 0) atomicOr(&seen[cur >> 5], 1u << (cur & 31));
+    if (lane == 0) seen[cur] = 1;
     __syncwarp();
     int nt = n_first;
     for (int f = 0; f < n_first; ++f) {
@@ -1575,13 +1650,13 @@ __device__ int fusion_targets(const DevMap& M, int cur, int n1, int n2, int n_sl
       for (int q0 = 0; q0 < c && added < n2 && nt < TMAX; q0 += 32) {
         const int q = q0 + lane;
         const int sl = q < c ? (f < HR && q < 32 ? head[f][q] : buf[1 + M.kf_cap + q]) : -1;
-        const bool un = sl >= 0 && !(seen[sl >> 5] >> (sl & 31) & 1u);
+        const bool un = sl >= 0 && !seen[sl];
         const unsigned bal = __ballot_sync(0xffffffffu, un);
         const int want = n2 - added < TMAX - nt ? n2 - added : TMAX - nt;
         const int rk = __popc(bal & ((1u << lane) - 1));
         if (un && rk < want) {
           tlist[nt + rk] = sl;
-          atomicOr(&seen[sl >> 5], 1u << (sl & 31));
+          seen[sl] = 1;
         }
         const int got = __popc(bal) < want ? __popc(bal) : want;
         nt += got;
