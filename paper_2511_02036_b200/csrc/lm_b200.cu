@@ -704,6 +704,7 @@ static cudaError_t launch_k(lm_ctx* ctx, void (*k)(KArgs...), dim3 g, dim3 b, si
 extern "C" {
 
 static int refresh(lm_ctx* ctx, HostMap* m, int map);
+__global__ void __launch_bounds__(256) k_fuse_visible_end(DevMap* maps, const StepArgs* args, lm_step_stats** totals);
 
 int lm_version(void) { return 1; }
 
@@ -746,7 +747,7 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
                         (const void*)k_fuse_geo, (const void*)k_fuse_gather, (const void*)k_fuse_apply,
                         (const void*)k_fuse_refresh, (const void*)k_fuse_spec<true>, (const void*)k_fuse_spec<false>,
                         (const void*)k_fuse_spec_pts, (const void*)k_fuse_spec_hit, (const void*)k_fuse_post,
-                        (const void*)k_fuse_rev, (const void*)k_fuse_visible};
+                        (const void*)k_fuse_rev, (const void*)k_fuse_visible_end};
     for (const void* k : ks) CU(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pc));
   }
   if (const char* e = getenv("LM_PDL")) ctx->pdl = atoi(e) != 0 ? 1 : 0;
@@ -1088,11 +1089,10 @@ __constant__ SumField k_sum_fields[] = {
 #undef LM_SUM64
 constexpr int kSumFields = sizeof(k_sum_fields) / sizeof(SumField);
 
-__global__ void __launch_bounds__(128) k_end(DevMap* maps, const StepArgs* args, lm_step_stats** totals) {
-  pdl_enter();
-  const DevMap& M = maps[args[blockIdx.x].map];
+// the step's statistics into the map's running totals (threads 0..kSumFields of one block)
+__device__ __forceinline__ void end_step(const DevMap& M, lm_step_stats* totals) {
   char* st = (char*)M.s.stats;
-  char* t = (char*)totals[args[blockIdx.x].map];
+  char* t = (char*)totals;
   const int k = threadIdx.x;
   if (k < kSumFields) {
     const SumField f = k_sum_fields[k];
@@ -1105,6 +1105,28 @@ __global__ void __launch_bounds__(128) k_end(DevMap* maps, const StepArgs* args,
     ((lm_step_stats*)t)->error = err;
     ((lm_step_stats*)t)->first_new_id += 1;  // steps accumulated
   }
+}
+
+// last kernel of a step: the reverse passes' deferred visible counters (thread per item),
+// then the last block of each map to finish adds the step's statistics to the running totals
+// (one launch fewer than a separate end kernel)
+__global__ void __launch_bounds__(256) k_fuse_visible_end(DevMap* maps, const StepArgs* args,
+                                                          lm_step_stats** totals) {
+  pdl_enter();
+  const StepArgs& A = args[blockIdx.z];
+  const DevMap& M = maps[A.map];
+  visible_item(M, A);
+  __shared__ int last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&M.s.fctl[FC_DONE], 1) == (int)(gridDim.x * gridDim.y) - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  end_step(M, totals[A.map]);
+  if (threadIdx.x == 0) M.s.fctl[FC_DONE] = 0;
 }
 
 static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args) {
@@ -1203,10 +1225,10 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   CU(launch_k(ctx, k_fuse_post, dim3(POST_BLOCKS, n), dim3(256), 0, 0, dmaps, dv));
   CU(launch_k(ctx, k_fuse_rev, dim3(n), dim3(REV_THREADS), rev_smem, 0, dmaps, dv, (int)rev_smem));
   if ((rc = mark())) return rc;
-  CU(launch_k(ctx, k_fuse_visible, dim3((kpkf + 255) / 256, tfuse, n), dim3(256), 0, 0, dmaps, dv));
-  CU(launch_k(ctx, k_end, dim3(n), dim3(128), 0, 0, dmaps, dv, ctx->d_totals));
+  CU(launch_k(ctx, k_fuse_visible_end, dim3((kpkf + 255) / 256, tfuse, n), dim3(256), 0, 0, dmaps, dv,
+              ctx->d_totals));
   if ((rc = mark())) return rc;
-  ctx->launches += 18;
+  ctx->launches += 17;
   if (ctx->prof) ctx->prof_steps.push_back(evs);
   CHECK_LAUNCH();
   CU(cudaEventRecord(ctx->args_ev[e], ctx->stream));
@@ -1247,6 +1269,7 @@ static int fill_args(lm_ctx* ctx, HostMap* m, int64_t kf_id, const lm_step_param
   // so neighbour selection does not depend on the cull (LM_SELECT_EARLY=0 disables)
   static const bool early_ok = getenv("LM_SELECT_EARLY") == nullptr || atoi(getenv("LM_SELECT_EARLY")) != 0;
   a.select_early = early_ok && a.do_create && !a.explicit_nbr && (!a.do_cull || (a.do_insert && !m->prebound[slot]));
+  a.prebound = m->prebound[slot];
   if (a.do_fuse && a.fc.n1 + a.fc.n1 * a.fc.n2 > TMAX)
     return fail(ctx, LM_ERR_INVALID_ARGUMENT, "n1 + n1*n2 > %d", TMAX);
   return LM_OK;

@@ -38,6 +38,7 @@ struct StepArgs {
   int do_insert, do_cull, do_create, do_fuse;
   int do_upload;      // with do_insert: also DeviceStore.upload_keyframe (residency + ledger)
   int select_early;   // k_select may run concurrently with k_cull (see k_select)
+  int prebound;       // the inserted keyframe was staged with pre-bound slots
   int processed;      // pipeline._processed
   int explicit_nbr;   // lm_search: neighbour list given (nbr0), masks optional
   int nbr0;
@@ -150,22 +151,18 @@ __global__ void __launch_bounds__(256) k_insert(DevMap* maps, const StepArgs* ar
   pdl_enter();
   const StepArgs& A = args[blockIdx.x];
   const DevMap& M = maps[A.map];
-  {  // the step's statistics record starts from zero
-    int* p = (int*)M.s.stats;
-    for (int k = threadIdx.x; k < (int)(sizeof(lm_step_stats) / 4); k += blockDim.x) p[k] = 0;
+  {  // the step's statistics record starts from zero (16-byte stores; the record is 8-aligned)
+    static_assert(sizeof(lm_step_stats) % 8 == 0, "stats record layout");
+    long long* p = (long long*)M.s.stats;
+    for (int k = threadIdx.x; k < (int)(sizeof(lm_step_stats) / 8); k += blockDim.x) p[k] = 0;
     if (threadIdx.x == 0) M.scal[SC_SOFT] = 0;
-    __syncthreads();
   }
-  if (!A.do_insert) return;
+  // (no barrier needed: thread 0 below writes none of the zeroed words; the kernel boundary
+  // orders the zeroing before every later stage)
+  if (!A.do_insert || threadIdx.x) return;
   const int slot = A.cur;
   const int off = M.kp_off[slot], n = M.kp_n[slot];
-  __shared__ int any;
-  if (threadIdx.x == 0) any = 0;
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += 256)
-    if (M.kbind[off + i] >= 0) any = 1;
-  __syncthreads();
-  if (threadIdx.x) return;
+  const bool any = A.prebound != 0;  // staged with pre-bound slots (host-side flag)
   M.kf_state[slot] = KF_LIVE;
   if (A.do_upload) {  // upload_keyframe devicestore.py:68-78
     M.kf_res[slot] = 1;
@@ -1717,7 +1714,7 @@ __device__ __forceinline__ long long pass_bytes(long long pts, long long obs, lo
   return 56 * pts + 9 * obs + 53 * tkp + 16 * acts;
 }
 
-enum FuseCtl { FC_T = 0, FC_P = 1, FC_NACT = 2, FC_NU = 3, FC_NSP = 4, FC_N = 8 };
+enum FuseCtl { FC_T = 0, FC_P = 1, FC_NACT = 2, FC_NU = 3, FC_NSP = 4, FC_DONE = 5, FC_N = 8 };
 
 // Starts while its predecessor (k_commit_write: the new points' records and the current
 // keyframe's new bindings) still runs: target selection reads only covisibility, which
@@ -2848,10 +2845,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
 
 // deferred visible counters of every reverse pass (thread per item); a point merged away
 // later in this step's reverse phase passes its bump on to its winner
-__global__ void __launch_bounds__(256) k_fuse_visible(DevMap* maps, const StepArgs* args) {
-  pdl_enter();
-  const StepArgs& A = args[blockIdx.z];
-  const DevMap& M = maps[A.map];
+__device__ __forceinline__ void visible_item(const DevMap& M, const StepArgs& A) {
   if (!A.do_fuse) return;
   const int t = blockIdx.y;
   if (t >= M.s.fctl[FC_T]) return;
