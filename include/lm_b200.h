@@ -131,6 +131,8 @@ typedef struct lm_step_stats { /* CreationStats triangulation.py:49-60 + run_fus
    * gates, [2] fusion projection / band / view-cos / radius gates (forward gather and the
    * speculative reverse evaluation), [3] rint ties of the fusion level prediction. */
   int64_t borderline[4];
+  int64_t match_second_half;  /* pairs whose first 128 bits passed: the popcounts k_match executes
+                                 are 4 * match_pairs + 4 * match_second_half */
 } lm_step_stats;
 
 typedef struct lm_candidate { /* MatchCandidate triangulation.py:41-46 */

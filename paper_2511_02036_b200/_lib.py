@@ -73,7 +73,7 @@ class StepStats(C.Structure):
                 ("fuse_bytes", i64), ("fuse_passes", i64), ("fuse_points", i64), ("fuse_actions", i64),
                 ("apply_rounds", i64), ("fuse_cycles", i64 * 16),
                 ("rev_passes_acting", i64), ("rev_passes_redo", i64), ("fuse_bytes_rev", i64), ("rev_mergeable", i64), ("dbg", i64 * 16),
-                ("borderline", i64 * 4)]
+                ("borderline", i64 * 4), ("match_second_half", i64)]
 
 
 class Candidate(C.Structure):

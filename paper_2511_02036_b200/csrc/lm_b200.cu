@@ -1083,6 +1083,7 @@ __constant__ SumField k_sum_fields[] = {
     LM_ARR(dbg, 6), LM_ARR(dbg, 7), LM_ARR(dbg, 8), LM_ARR(dbg, 9), LM_ARR(dbg, 10), LM_ARR(dbg, 11),
     LM_ARR(dbg, 12), LM_ARR(dbg, 13), LM_ARR(dbg, 14), LM_ARR(dbg, 15),
     LM_ARR(borderline, 0), LM_ARR(borderline, 1), LM_ARR(borderline, 2), LM_ARR(borderline, 3),
+    LM_SUM64(match_second_half),
 #undef LM_ARR
 };
 #undef LM_SUM32

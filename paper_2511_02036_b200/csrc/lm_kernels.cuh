@@ -604,7 +604,7 @@ __global__ void __launch_bounds__(MATCH_WARPS * 32, 5) k_match(DevMap* maps, con
   }
   const int maxd = A.mc.match_max_distance;
   unsigned long long best = ~0ull;
-  int border = 0;
+  int border = 0, second = 0;
   for (int c0 = jb; c0 < je; c0 += MATCH_JT) {
     const int cn = je - c0 < MATCH_JT ? je - c0 : MATCH_JT;
     __syncthreads();
@@ -619,6 +619,7 @@ __global__ void __launch_bounds__(MATCH_WARPS * 32, 5) k_match(DevMap* maps, con
         const uint4 b0 = sd[2 * k];
         int dist = __popc(a0.x ^ b0.x) + __popc(a0.y ^ b0.y) + __popc(a0.z ^ b0.z) + __popc(a0.w ^ b0.w);
         if (dist <= maxd) {
+          ++second;
           const uint4 b1 = sd[2 * k + 1];
           dist += __popc(a1.x ^ b1.x) + __popc(a1.y ^ b1.y) + __popc(a1.z ^ b1.z) + __popc(a1.w ^ b1.w);
           if (dist <= maxd) {
@@ -638,6 +639,16 @@ __global__ void __launch_bounds__(MATCH_WARPS * 32, 5) k_match(DevMap* maps, con
   if (__any_sync(0xffffffffu, border)) {
     for (int o = 16; o; o >>= 1) border += __shfl_xor_sync(0xffffffffu, border, o);
     if (lane == 0) atomicAdd((unsigned long long*)&M.s.stats->borderline[0], (unsigned long long)border);
+  }
+  {  // executed-popcount diagnostic: one same-address atomic per CTA, not per warp
+    __shared__ int sec_sh;
+    if (threadIdx.x == 0) sec_sh = 0;
+    for (int o = 16; o; o >>= 1) second += __shfl_xor_sync(0xffffffffu, second, o);
+    __syncthreads();
+    if (lane == 0 && second) atomicAdd(&sec_sh, second);
+    __syncthreads();
+    if (threadIdx.x == 0 && sec_sh)
+      atomicAdd((unsigned long long*)&M.s.stats->match_second_half, (unsigned long long)sec_sh);
   }
   __syncthreads();
   if (wid == 0 && active) {
@@ -1786,9 +1797,9 @@ __global__ void __launch_bounds__(256) k_fuse_geo(DevMap* maps, const StepArgs* 
   const int P = M.s.fctl[FC_P];
   const int lane = threadIdx.x & 31;
   const int p = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (p >= P) return;
-  const int mp = M.s.pts[p];
-  if (M.alive[mp]) {
+  if (blockIdx.x * 8 >= P) return;  // (whole block: uniform)
+  const int mp = p < P ? M.s.pts[p] : -1;
+  if (mp >= 0 && M.alive[mp]) {
     if (M.dirty[mp]) {
       refresh_rep_warp(M, mp, lane);
       if (lane == 0) M.dirty[mp] = 0;
@@ -1796,11 +1807,15 @@ __global__ void __launch_bounds__(256) k_fuse_geo(DevMap* maps, const StepArgs* 
     }
     if (!M.gval[mp]) geo_full_warp(M, mp, lane);
   }
-  if (lane == 0) {
+  __shared__ unsigned long long fb_sh;
+  if (threadIdx.x == 0) fb_sh = 0;
+  __syncthreads();
+  if (lane == 0 && mp >= 0) {
     point_geometry(M, mp, A.fc.dist_band_slack, M.s.geo[p]);
-    atomicAdd((unsigned long long*)&M.s.stats->fuse_bytes,
-              (unsigned long long)(M.s.fctl[FC_T] * (56LL + 9LL * M.nobs[mp])));
+    atomicAdd(&fb_sh, (unsigned long long)(M.s.fctl[FC_T] * (56LL + 9LL * M.nobs[mp])));
   }
+  __syncthreads();  // algorithmic bytes: one same-address global atomic per block, not per point
+  if (threadIdx.x == 0) atomicAdd((unsigned long long*)&M.s.stats->fuse_bytes, fb_sh);
 }
 
 // thread per (target, point) of the forward gather; per-CTA ordered compaction
