@@ -89,3 +89,25 @@ def test_oracle_audit_clean_after_pipeline():
     for rec in s.records:
         pipe.step(O.okf_from_record(rec, cam))
     assert pipe.map.audit() == []
+
+
+KFCULL = json.load(open(os.path.join(HERE, "golden", "kfcull.json")))
+
+
+@pytest.mark.parametrize("name", ["line14dup", "orbit20", "corridor12"])
+def test_oracle_keyframe_cull_matches_reference_pipeline(name):
+    """Pins the oracle's keyframe cull (kill_keyframe + is_redundant_baseline + cull_keyframes,
+    culling.py:60-154, mapmodel.py:275-283) to the real reference pipeline with keyframe culling
+    (tests/golden/kfcull.json): culled keyframes and structural digest after every keyframe."""
+    g = KFCULL[name]
+    s = W.generate_sequence(W.WorldConfig(**g["config"]))
+    cam = cam_of(s)
+    pipe = O.OraclePipeline(s.config.num_levels, g["neighbor_count"], fc=O.FuseCfg(n1=g["n1"]))
+    culled = []
+    for rec, want in zip(s.records[:g["keyframes"]], g["steps"]):
+        kf = O.okf_from_record(rec, cam)
+        pipe.step(kf)
+        cand = [k for k in pipe.map.neighbors(kf.kf_id) if k != kf.kf_id]
+        culled += O.cull_keyframes(pipe.map, cand)
+        assert culled == want["culled_keyframes"], (name, rec.kf_id)
+        assert O.structural_digest(pipe.map) == want["digest"], (name, rec.kf_id)
