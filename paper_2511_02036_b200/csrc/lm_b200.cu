@@ -1271,8 +1271,6 @@ static int fill_args(lm_ctx* ctx, HostMap* m, int64_t kf_id, const lm_step_param
   static const bool early_ok = getenv("LM_SELECT_EARLY") == nullptr || atoi(getenv("LM_SELECT_EARLY")) != 0;
   a.select_early = early_ok && a.do_create && !a.explicit_nbr && (!a.do_cull || (a.do_insert && !m->prebound[slot]));
   a.prebound = m->prebound[slot];
-  static const int shrink = getenv("LM_APPLY_SHRINK") ? atoi(getenv("LM_APPLY_SHRINK")) : 0;
-  a.apply_shrink = shrink;
   if (a.do_fuse && a.fc.n1 + a.fc.n1 * a.fc.n2 > TMAX)
     return fail(ctx, LM_ERR_INVALID_ARGUMENT, "n1 + n1*n2 > %d", TMAX);
   return LM_OK;

@@ -39,7 +39,6 @@ struct StepArgs {
   int do_upload;      // with do_insert: also DeviceStore.upload_keyframe (residency + ledger)
   int select_early;   // k_select may run concurrently with k_cull (see k_select)
   int prebound;       // the inserted keyframe was staged with pre-bound slots
-  int apply_shrink;   // forward apply: pending count at which the leader CTA finishes alone
   int processed;      // pipeline._processed
   int explicit_nbr;   // lm_search: neighbour list given (nbr0), masks optional
   int nbr0;
@@ -1285,24 +1284,18 @@ enum TeamCtl { CTL_ROUND = 0, CTL_NPEND, CTL_NMERGE, CTL_NADD, CTL_NDEF, CTL_NRE
 
 template <int BLOCK>
 struct BlockTeam {
-  static constexpr int kBlock = BLOCK;
   int* ctl;
   int tid, nth;
-  int shrink = 0;
   __device__ explicit BlockTeam(int* c) : ctl(c), tid(threadIdx.x), nth(BLOCK) {}
-  __device__ bool shrinkable() const { return false; }
-  __device__ bool leader() const { return true; }
   __device__ void sync() const { __syncthreads(); }
   __device__ int excl_scan(int v, int* sh, int& total) const { return block_excl_scan<BLOCK>(v, sh, total); }
 };
 
 template <int BLOCK>
 struct ClusterTeam {
-  static constexpr int kBlock = BLOCK;
   int* ctl;
   int tid, nth, rank, nranks;
-  int shrink;  // pending-action count at or below which the leader CTA finishes alone (0: never)
-  __device__ ClusterTeam(int* local_ctl, int shrink_at = 0) : shrink(shrink_at) {
+  __device__ ClusterTeam(int* local_ctl) {
     cg::cluster_group cl = cg::this_cluster();
     rank = (int)cl.block_rank();
     nranks = (int)cl.num_blocks();
@@ -1310,8 +1303,6 @@ struct ClusterTeam {
     tid = rank * BLOCK + threadIdx.x;
     nth = nranks * BLOCK;
   }
-  __device__ bool shrinkable() const { return shrink > 0 && nranks > 1; }
-  __device__ bool leader() const { return rank == 0; }
   __device__ void sync() const { cg::this_cluster().sync(); }
   __device__ int excl_scan(int v, int* sh, int& total) const {
     int bt;
@@ -1330,13 +1321,20 @@ struct ClusterTeam {
   }
 };
 
-// one reservation round of apply_team (see above) over the pending actions of acts[0..n)
 template <class Team>
-__device__ void apply_round(const Team& G, const DevMap& M, const ActRec* acts, int n, int* cnt, PairAcc* acc,
-                            long long* tm, int rounds) {
-  int* const ctl = G.ctl;
+__device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh, PairAcc* acc,
+                          long long* tm = nullptr) {
+  int* const ctl = G.ctl;  // team control words (CTL_*), in the team leader's shared memory
   const int tid = G.tid, nth = G.nth;
   const int lane = threadIdx.x & 31, gwarp = tid >> 5, nwarps = nth >> 5;
+  // pend[a]: action a still pending. Done actions are skipped in place (every round walks all
+  // n actions: one iteration per thread at these sizes) instead of compacting the pending
+  // list with a team-wide scan each round.
+  for (int a = tid; a < n; a += nth) M.s.pend[a] = 1;
+  if (tid == 0) ctl[CTL_NPEND] = n;
+  G.sync();
+  int rounds = 0;
+  while (ctl[CTL_NPEND] > 0) {
     const int np = ctl[CTL_NPEND];  // (the words reset below were last read before the round's final barrier)
     if (tm && tid == 0 && rounds > 0) tm[13] += np;  // diagnostics: actions left after round 1
     if (tid == 0) {
@@ -1488,39 +1486,11 @@ __device__ void apply_round(const Team& G, const DevMap& M, const ActRec* acts, 
     if (tid == 0) ctl[CTL_NPEND] = np - ctl[CTL_NREADY];
     G.sync();
     if (tm && tid == 0) tm[12] += gtime() - tt;
-}
-
-template <class Team>
-__device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh, PairAcc* acc,
-                          long long* tm = nullptr) {
-  int* const ctl = G.ctl;  // team control words (CTL_*), in the team leader's shared memory
-  const int tid = G.tid, nth = G.nth;
-  // pend[a]: action a still pending. Done actions are skipped in place (every round walks all
-  // n actions: one iteration per thread at these sizes) instead of compacting the pending
-  // list with a team-wide scan each round.
-  for (int a = tid; a < n; a += nth) M.s.pend[a] = 1;
-  if (tid == 0) ctl[CTL_NPEND] = n;
-  G.sync();
-  int rounds = 0;
-  while (ctl[CTL_NPEND] > 0) {
-    // a cluster team hands the last few pending actions to its leader CTA: their rounds then
-    // synchronise with block barriers instead of cluster-wide ones (team_shrink, 0 = never)
-    if (G.shrinkable() && ctl[CTL_NPEND] <= G.shrink) break;
-    apply_round(G, M, acts, n, cnt, acc, tm, rounds);
     if (++rounds > (1 << 20)) break;
-  }
-  if (G.shrinkable() && ctl[CTL_NPEND] > 0) {
-    G.sync();  // every CTA has read NPEND above before the leader goes on alone
-    if (G.leader()) {
-      const BlockTeam<Team::kBlock> B(ctl);
-      while (ctl[CTL_NPEND] > 0) {
-        apply_round(B, M, acts, n, cnt, acc, tm, rounds);
-        if (++rounds > (1 << 20)) break;
-      }
-    }
   }
   return rounds;
 }
+
 
 template <int BLOCK>
 __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh, PairAcc* acc,
@@ -1900,7 +1870,7 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) k_fuse_apply(DevMap* maps, c
   if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
   if (threadIdx.x < 16) tmf[threadIdx.x] = 0;
   pair_acc_init<APPLY_THREADS>(&acc, A.cur);
-  const ClusterTeam<APPLY_THREADS> G(ctl, A.apply_shrink);
+  const ClusterTeam<APPLY_THREADS> G(ctl);
   const int nb = (T * P + 255) / 256;
   int base = 0;
   for (int c0 = 0; c0 < nb; c0 += APPLY_THREADS) {  // exclusive scan of the per-CTA counts (every CTA)
