@@ -207,6 +207,8 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
   unsigned* kcol = cull_dyn + 3 * CULL_CHUNK;  // [CULL_CHUNK/32][PAIR_W] per window slot: mask over the kills
   __shared__ int kact[PAIR_W], kidx[PAIR_W];
   __shared__ int tk_sh;
+  constexpr int CULL_HEAVY = 256;        // high-degree kills of this CTA handled warp-wide
+  __shared__ int heavy[CULL_HEAVY], nheavy;
   int* kills0 = cl.map_shared_rank(kills, 0);
   int* big0 = cl.map_shared_rank(big, 0);
   int* nbig0 = cl.map_shared_rank(&nbig, 0);
@@ -270,8 +272,22 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
     // popcounts over the transposed masks instead of one contended shared atomic per
     // observer pair. Kills with an observer outside the window take the per-pair path.
     tk = *tk0;
+    // a kill's chain is ~3 dependent L2 round trips per 8 observations on one thread, so the
+    // few long-lived probation points (tens of observations, most of them fusion ADDs) set the
+    // phase's critical path: points with more than HEAVY observations go to a warp each (lanes
+    // over the observations) after the thread pass
+    constexpr int HEAVY = 16;
+    if (threadIdx.x == 0) nheavy = 0;
+    __syncthreads();
     for (int k = rank + nranks * threadIdx.x; k < tk; k += nranks * 1024) {
       const int id = kills0[k];
+      if (M.nobs[id] > HEAVY) {
+        const int at = atomicAdd(&nheavy, 1);
+        if (at < CULL_HEAVY) {
+          heavy[at] = k;
+          continue;
+        }
+      }
       unsigned r[3];
       if (!kill_point_rows_thread(M, id, &acc, r)) {
         r[0] = r[1] = r[2] = 0u;
@@ -280,6 +296,24 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
       krow0[3 * k] = r[0];
       krow0[3 * k + 1] = r[1];
       krow0[3 * k + 2] = r[2];
+    }
+    __syncthreads();
+    {
+      const int nh = nheavy < CULL_HEAVY ? nheavy : CULL_HEAVY;
+      for (int h = wid; h < nh; h += 32) {
+        const int k = heavy[h];
+        const int id = kills0[k];
+        unsigned r[3] = {0u, 0u, 0u};
+        if (!kill_point_rows_warp(M, id, lane, &acc, r)) {
+          if (lane == 0) big0[atomicAdd(nbig0, 1)] = id;
+          r[0] = r[1] = r[2] = 0u;
+        }
+        if (lane == 0) {
+          krow0[3 * k] = r[0];
+          krow0[3 * k + 1] = r[1];
+          krow0[3 * k + 2] = r[2];
+        }
+      }
     }
     cl.sync();  // rows complete; ranks > 0 go on to the next chunk
     if (rank != 0) continue;
