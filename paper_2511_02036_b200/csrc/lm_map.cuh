@@ -1173,6 +1173,65 @@ __device__ void refresh_rep_lanes(const DevMap& M, int2* o, int n, uint4* rep, i
   __syncwarp();
 }
 
+// refresh_rep_list for lists longer than REFRESH_MAXN (no per-row distance array): each
+// row's two middle order statistics by a 9-bit radix select whose every step recounts the
+// row's distances (recomputed popcounts), so memory stays O(1) per lane for any n. Slow
+// (~11 passes over the list per row) but exact; only points observed by > 512 keyframes
+// take it. o must already be sorted by keyframe id.
+__device__ void refresh_rep_radix(const DevMap& M, const int2* o, int n, uint4* rep, int lane) {
+  const int m = n - 1, k0 = (m - 1) >> 1, k1 = m >> 1;
+  unsigned best = 0xffffffffu;  // (med2 << 16) | row
+  for (int a = lane; a < n; a += 32) {
+    const int ga = M.kp_off[o[a].x] + o[a].y;
+    const uint4 a0 = M.kdesc[2 * ga], a1 = M.kdesc[2 * ga + 1];
+    auto dist = [&](int b) -> int {
+      const int gb = M.kp_off[o[b].x] + o[b].y;
+      return hamming(a0, a1, M.kdesc[2 * gb], M.kdesc[2 * gb + 1]);
+    };
+    // k0-th smallest (from 0) of d(a, b), b != a
+    int prefix = 0, k = k0;
+    for (int bit = 8; bit >= 0; --bit) {
+      int c0 = 0;
+      for (int b = 0; b < n; ++b) {
+        if (b == a) continue;
+        const int d = dist(b);
+        c0 += (d >> (bit + 1)) == prefix && !((d >> bit) & 1);
+      }
+      if (k < c0) {
+        prefix = prefix << 1;
+      } else {
+        k -= c0;
+        prefix = (prefix << 1) | 1;
+      }
+    }
+    const int v0 = prefix;
+    int v1 = v0;
+    if (k1 != k0) {  // next order statistic: v0 again if it repeats, else the smallest larger value
+      int le = 0, nxt = 0x7fffffff;
+      for (int b = 0; b < n; ++b) {
+        if (b == a) continue;
+        const int d = dist(b);
+        le += d <= v0;
+        if (d > v0 && d < nxt) nxt = d;
+      }
+      v1 = le > k1 ? v0 : nxt;
+    }
+    const unsigned key = ((unsigned)(v0 + v1) << 16) | (unsigned)a;
+    best = key < best ? key : best;
+  }
+  for (int off = 16; off; off >>= 1) {
+    const unsigned other = __shfl_xor_sync(0xffffffffu, best, off);
+    best = other < best ? other : best;
+  }
+  if (lane == 0) {
+    const int a = best & 0xffff;
+    const int g = M.kp_off[o[a].x] + o[a].y;
+    rep[0] = M.kdesc[2 * g];
+    rep[1] = M.kdesc[2 * g + 1];
+  }
+  __syncwarp();
+}
+
 // _refresh_rep_descriptor of the observation list o[0..n) (sorted in place by keyframe id),
 // result into rep[0..1]; one warp
 __device__ void refresh_rep_list(const DevMap& M, int2* o, int n, uint4* rep, int lane) {
@@ -1190,10 +1249,7 @@ __device__ void refresh_rep_list(const DevMap& M, int2* o, int n, uint4* rep, in
     __syncwarp();
     return;
   }
-  if (n > REFRESH_MAXN) {
-    if (lane == 0) set_err(M, LM_ERR_CAPACITY);
-    return;
-  }
+  if (n > REFRESH_MAXN) return refresh_rep_radix(M, o, n, rep, lane);
   unsigned short d[REFRESH_MAXN];
   const int m = n - 1, k0 = (m - 1) >> 1, k1 = m >> 1;
   unsigned best = 0xffffffffu;  // (med2 << 16) | row

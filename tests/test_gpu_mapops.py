@@ -241,3 +241,33 @@ def test_cull_keyframes_matches_oracle_on_a_pipeline_map():
         assert m._snapshot().structural_digest() == O.structural_digest(ora.map), processed
     assert total, "the run should cull at least one keyframe"
     assert st.ledger.evictions == len(total)
+
+
+@pytest.mark.parametrize("n_obs", [3, 31, 33, 64, 65, 128, 129, 300, 513, 700])
+def test_representative_descriptor_every_refresh_path(n_obs):
+    """_refresh_rep_descriptor (mapmodel.py:165-181) on one point observed n times, through
+    every device path: register symmetric (<= 64), lane rows (<= 128), per-row distance
+    array (<= 512) and the radix select without a size limit (> 512). Descriptors share a
+    few prototypes plus bit flips, so the medians have many ties (first row wins)."""
+    from helpers import rep_descriptor
+
+    rng = np.random.default_rng(n_obs)
+    protos = rng.integers(0, 256, (3, 32), dtype=np.uint8)
+    m = MapModel(CAM.num_levels, store=store_for(n_obs + 8, 8, points=64))
+    descs = []
+    for k in range(n_obs):
+        d = protos[rng.integers(0, 3)].copy()
+        for _ in range(int(rng.integers(0, 12))):
+            b = int(rng.integers(0, 256))
+            d[b >> 3] ^= np.uint8(1 << (b & 7))
+        desc = np.vstack([d, rng.integers(0, 256, (1, 32), dtype=np.uint8)])
+        kf = KeyFrame(k, SE3Pose(np.array([0.0, 0.0, 0.0, 1.0]), np.array([0.01 * k, 0.0, 0.0])), CAM,
+                      np.array([100.0, 200.0]), np.array([100.0, 200.0]), np.zeros(2, np.int64), desc)
+        m.insert_keyframe(kf)
+        descs.append(d)
+    p = m.new_map_point([0.0, 0.0, 5.0], descs[0], 0)
+    for k in range(n_obs):
+        m.add_observation(p.mp_id, k, 0)
+    got = m.points[p.mp_id].rep_descriptor
+    want = rep_descriptor(np.stack(descs))
+    assert np.array_equal(got, want)
