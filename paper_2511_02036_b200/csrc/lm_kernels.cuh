@@ -508,8 +508,26 @@ __global__ void __launch_bounds__(256) k_prep(DevMap* maps, const StepArgs* args
   }
   if (threadIdx.x < LMAX) lcount[threadIdx.x] = 0;
   __syncthreads();
-  for (int i = threadIdx.x; i < n; i += 256)
-    if (is_unbound(M, A, off + i, i, list == 0)) atomicAdd(&lcount[M.klev[off + i]], 1);
+  // each thread's keypoints (i = tid + 256 q): unbound flag and level loaded in one round (the
+  // per-keypoint shared atomics would otherwise put one L2 round trip per iteration on the chain)
+  constexpr int PQ = 8;
+  unsigned char lv[PQ];
+  unsigned ub = 0u;
+  const bool fits = n <= 256 * PQ;
+  if (fits) {
+#pragma unroll
+    for (int q = 0; q < PQ; ++q) {
+      const int i = threadIdx.x + 256 * q;
+      lv[q] = i < n ? M.klev[off + i] : 0;
+      if (i < n && is_unbound(M, A, off + i, i, list == 0)) ub |= 1u << q;
+    }
+#pragma unroll
+    for (int q = 0; q < PQ; ++q)
+      if (ub >> q & 1u) atomicAdd(&lcount[lv[q]], 1);
+  } else {
+    for (int i = threadIdx.x; i < n; i += 256)
+      if (is_unbound(M, A, off + i, i, list == 0)) atomicAdd(&lcount[M.klev[off + i]], 1);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     int acc = 0;
@@ -522,11 +540,20 @@ __global__ void __launch_bounds__(256) k_prep(DevMap* maps, const StepArgs* args
   }
   __syncthreads();
   if (list == 0) {
-    for (int i = threadIdx.x; i < n; i += 256) {
-      M.s.win_rank[i] = 0x7fffffff;
-      if (is_unbound(M, A, off + i, i, true)) {
-        const int at = atomicAdd(&lcur[M.klev[off + i]], 1);
-        M.s.cur_sorted[at] = i;
+    if (fits) {
+#pragma unroll
+      for (int q = 0; q < PQ; ++q) {
+        const int i = threadIdx.x + 256 * q;
+        if (i < n) M.s.win_rank[i] = 0x7fffffff;
+        if (ub >> q & 1u) M.s.cur_sorted[atomicAdd(&lcur[lv[q]], 1)] = i;
+      }
+    } else {
+      for (int i = threadIdx.x; i < n; i += 256) {
+        M.s.win_rank[i] = 0x7fffffff;
+        if (is_unbound(M, A, off + i, i, true)) {
+          const int at = atomicAdd(&lcur[M.klev[off + i]], 1);
+          M.s.cur_sorted[at] = i;
+        }
       }
     }
     if (threadIdx.x <= L) M.s.cur_bucket[threadIdx.x] = lstart[threadIdx.x];
@@ -573,17 +600,28 @@ __global__ void __launch_bounds__(256) k_prep(DevMap* maps, const StepArgs* args
     }
   } else {
     const size_t base = (size_t)r * M.kpkf_max;
-    for (int i = threadIdx.x; i < n; i += 256) {
-      M.s.bestj[base + i] = ~0ull;
-      if (is_unbound(M, A, off + i, i, false)) {
-        const int lv = M.klev[off + i];
-        const int at = atomicAdd(&lcur[lv], 1);
-        M.s.nb_j[base + at] = i;
-        M.s.nb_desc[2 * (base + at)] = M.kdesc[2 * (off + i)];
-        M.s.nb_desc[2 * (base + at) + 1] = M.kdesc[2 * (off + i) + 1];
-        M.s.nb_u[base + at] = M.ku[off + i];
-        M.s.nb_v[base + at] = M.kv[off + i];
-        M.s.nb_thr[base + at] = A.mc.chi2_epi * M.S2[lv];
+    auto put = [&](int i, int lvi) {  // (the copies' loads issue before the slot atomic)
+      const uint4 d0 = M.kdesc[2 * (off + i)], d1 = M.kdesc[2 * (off + i) + 1];
+      const double u = M.ku[off + i], v = M.kv[off + i];
+      const int at = atomicAdd(&lcur[lvi], 1);
+      M.s.nb_j[base + at] = i;
+      M.s.nb_desc[2 * (base + at)] = d0;
+      M.s.nb_desc[2 * (base + at) + 1] = d1;
+      M.s.nb_u[base + at] = u;
+      M.s.nb_v[base + at] = v;
+      M.s.nb_thr[base + at] = A.mc.chi2_epi * M.S2[lvi];
+    };
+    if (fits) {
+#pragma unroll
+      for (int q = 0; q < PQ; ++q) {
+        const int i = threadIdx.x + 256 * q;
+        if (i < n) M.s.bestj[base + i] = ~0ull;
+        if (ub >> q & 1u) put(i, lv[q]);
+      }
+    } else {
+      for (int i = threadIdx.x; i < n; i += 256) {
+        M.s.bestj[base + i] = ~0ull;
+        if (is_unbound(M, A, off + i, i, false)) put(i, M.klev[off + i]);
       }
     }
     for (int i = threadIdx.x; i < ncur; i += 256) M.s.pick[base + i] = ~0ull;
@@ -709,25 +747,31 @@ __global__ void __launch_bounds__(256) k_tri(DevMap* maps, const StepArgs* args)
   const int cur = A.cur;
   const int ncur = M.kp_n[cur];
   const size_t base = (size_t)r * M.kpkf_max;
+  // one-to-one survivors in current-index order: each thread owns TQ consecutive keypoints
+  // (all their pick / bestj loads in two rounds), one block scan per 256 * TQ keypoints
+  constexpr int TQ = 8;
   int count = 0;
-  for (int b0 = 0; b0 < ncur; b0 += 256) {
-    const int i = b0 + threadIdx.x;
-    int flag = 0;
-    unsigned long long pk = ~0ull;
-    if (i < ncur) {
-      pk = M.s.pick[base + i];
-      if (pk != ~0ull) {
-        const unsigned j = (unsigned)(pk & 0xffffffffu);
-        flag = M.s.bestj[base + j] == ((pk & 0xffffffff00000000ull) | (unsigned)i);
-      }
-    }
+  for (int b0 = 0; b0 < ncur; b0 += 256 * TQ) {
+    const int i0 = b0 + threadIdx.x * TQ;
+    unsigned long long pk[TQ], bj[TQ];
+#pragma unroll
+    for (int q = 0; q < TQ; ++q) pk[q] = i0 + q < ncur ? M.s.pick[base + i0 + q] : ~0ull;
+#pragma unroll
+    for (int q = 0; q < TQ; ++q) bj[q] = pk[q] != ~0ull ? M.s.bestj[base + (unsigned)(pk[q] & 0xffffffffu)] : 0ull;
+    unsigned fl = 0u;
+#pragma unroll
+    for (int q = 0; q < TQ; ++q)
+      if (pk[q] != ~0ull && bj[q] == ((pk[q] & 0xffffffff00000000ull) | (unsigned)(i0 + q))) fl |= 1u << q;
     int tot;
-    const int at = block_excl_scan<256>(flag, sh, tot);
-    if (flag) {
-      M.s.cand_i[base + count + at] = i;
-      M.s.cand_j[base + count + at] = (int)(pk & 0xffffffffu);
-      M.s.cand_d[base + count + at] = (int)(pk >> 32);
-    }
+    int at = block_excl_scan<256>(__popc(fl), sh, tot);
+#pragma unroll
+    for (int q = 0; q < TQ; ++q)
+      if (fl >> q & 1u) {
+        M.s.cand_i[base + count + at] = i0 + q;
+        M.s.cand_j[base + count + at] = (int)(pk[q] & 0xffffffffu);
+        M.s.cand_d[base + count + at] = (int)(pk[q] >> 32);
+        ++at;
+      }
     count += tot;
   }
   if (threadIdx.x == 0) M.s.cand_n[r] = count;
