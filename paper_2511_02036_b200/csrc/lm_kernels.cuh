@@ -774,6 +774,9 @@ __global__ void __launch_bounds__(256) k_tri(DevMap* maps, const StepArgs* args)
       }
     count += tot;
   }
+  // the triangulation loop below reads candidate records other threads just wrote (global
+  // memory: they are visible block-wide only after a barrier)
+  __syncthreads();
   if (threadIdx.x == 0) M.s.cand_n[r] = count;
   if (A.search_only) return;
   const int nb = M.s.nbr[r];
