@@ -125,7 +125,7 @@ __device__ int ranked_neighbors(const DevMap& M, int k, int n, int* sh_slot, uns
   __syncthreads();
   const int* row = M.covis + (size_t)k * M.kf_cap;
   for (int s = threadIdx.x; s < n_slots; s += BLOCK) {
-    const int w = row[s];
+    const int w = __ldcg(row + s);  // (L2: the row may change between kernels that run early under PDL)
     if (w >= M.min_w && w > 0 && s != k && M.kf_state[s] == KF_LIVE) {
       const int at = atomicAdd(&cnt, 1);
       sh_slot[at] = s;
@@ -1691,7 +1691,7 @@ __device__ int fusion_targets(const DevMap& M, int cur, int n1, int n2, int n_sl
 #pragma unroll
       for (int u = 0; u < PF; ++u) {
         const int s = s00 + 32 * u + lane;
-        wv[u] = s < n_slots ? row[s] : 0;
+        wv[u] = s < n_slots ? __ldcg(row + s) : 0;  // (L2, see ranked_neighbors)
         st[u] = s < n_slots ? M.kf_state[s] : 0;
         kid[u] = s < n_slots ? M.kf_id[s] : 0;
       }
