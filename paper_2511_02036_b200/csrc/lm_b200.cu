@@ -82,6 +82,7 @@ struct lm_ctx {
   bool prof = false;
   int apply_cluster = 16;               // CTAs per map of the forward-apply cluster (LM_APPLY_CLUSTER)
   int cull_cluster = 8;                 // CTAs per map of the recent-point cull cluster (LM_CULL_CLUSTER)
+  int rev_cluster = 8;                  // CTAs per map of the reverse walk (LM_REV_CLUSTER; 1 = CTA 0 alone)
   // programmatic dependent launch of the step kernels (LM_PDL=0/1 overrides): on for
   // single-session launches; off for batches, whose concurrent stream groups lose SMs to
   // successor CTAs parked in griddepcontrol.wait (C5: 16.2k -> 11.6k KF/s with it)
@@ -739,6 +740,7 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
   CU(cudaFuncSetAttribute(k_fuse_rev, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   CU(cudaFuncSetAttribute(k_op, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
   CU(cudaFuncSetAttribute(k_fuse_apply, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CU(cudaFuncSetAttribute(k_fuse_rev, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CU(cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, CULL_DYN_SMEM));
   if (const char* e = getenv("LM_CARVEOUT")) {  // (experiments) shared-memory carve-out hint, percent
     const int pc = atoi(e);
@@ -751,6 +753,7 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
     for (const void* k : ks) CU(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pc));
   }
   if (const char* e = getenv("LM_PDL")) ctx->pdl = atoi(e) != 0 ? 1 : 0;
+  if (const char* e = getenv("LM_REV_CLUSTER")) ctx->rev_cluster = atoi(e) > 0 ? atoi(e) : 1;
   if (const char* e = getenv("LM_CULL_CLUSTER")) {
     const int v = atoi(e);
     ctx->cull_cluster = v < 1 ? 1 : (v > 8 ? 8 : v);
@@ -1224,7 +1227,12 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   }
   if ((rc = mark())) return rc;
   CU(launch_k(ctx, k_fuse_post, dim3(POST_BLOCKS, n), dim3(256), 0, 0, dmaps, dv));
-  CU(launch_k(ctx, k_fuse_rev, dim3(n), dim3(REV_THREADS), rev_smem, 0, dmaps, dv, (int)rev_smem));
+  {
+    // reverse walk: one cluster per map, CTA 0 walks, the others help with direct passes
+    int cl = ctx->rev_cluster / n;
+    cl = cl < 1 ? 1 : cl;
+    CU(launch_k(ctx, k_fuse_rev, dim3(n * cl), dim3(REV_THREADS), rev_smem, cl, dmaps, dv, (int)rev_smem));
+  }
   if ((rc = mark())) return rc;
   CU(launch_k(ctx, k_fuse_visible_end, dim3((kpkf + 255) / 256, tfuse, n), dim3(256), 0, 0, dmaps, dv,
               ctx->d_totals));

@@ -2281,9 +2281,13 @@ __global__ void __launch_bounds__(256) k_fuse_post(DevMap* maps, const StepArgs*
 // reverse passes (fusion.py:337-346), one CTA per map; see the block comment above
 __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const StepArgs* args, int smem_bytes) {
   pdl_enter();
-  const StepArgs& A = args[blockIdx.x];
+  // one cluster per map: CTA 0 walks the passes; the other CTAs (if any) only help apply the
+  // direct passes' actions, on command (rcmd in CTA 0's shared memory, cluster barriers)
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank(), nranks = (int)cl.num_blocks();
+  const StepArgs& A = args[blockIdx.x / nranks];
   const DevMap& M = maps[A.map];
-  if (!A.do_fuse) return;
+  if (!A.do_fuse) return;  // (uniform over the cluster)
   const int T = M.s.fctl[FC_T];
   if (T == 0) return;
   const long long t_entry = gtime();
@@ -2293,7 +2297,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     const int n = M.kp_n[A.cur], off = M.kp_off[A.cur];
     const int nc = M.g_nx[A.cur] * M.g_ny[A.cur];
     const size_t need = (size_t)n * 53 + 4 * (size_t)(nc + 1) + 64;
-    if (smem_bytes > 0 && need <= (size_t)smem_bytes) {
+    if (rank == 0 && smem_bytes > 0 && need <= (size_t)smem_bytes) {
       uint4* sd = (uint4*)dyn_rev;
       double* su = (double*)(sd + 2 * n);
       double* sv = su + n;
@@ -2330,6 +2334,15 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   __shared__ int s_toff[TMAX];  // keypoint offset of each pass's target
   __shared__ ActRec s_acts[DMAX];  // the pass's first DMAX actions
   __shared__ double cur_pose[22];  // R, t, C, cam, cell size of the current keyframe
+  __shared__ int rcmd[4];          // CTA 0 -> helpers: command, t1, tag, action count
+  enum { RC_DIRECT = 1, RC_EXIT = 2 };
+  // CTA 0's counters and lists, reached by the helper CTAs through distributed shared memory
+  int* const ni_p = rank ? cl.map_shared_rank(&ni_sh, 0) : &ni_sh;
+  int* const nc_p = rank ? cl.map_shared_rank(&nc_sh, 0) : &nc_sh;
+  int* const nset_p = rank ? cl.map_shared_rank(&s_nset, 0) : &s_nset;
+  int* const il_p = rank ? cl.map_shared_rank(s_il, 0) : s_il;
+  int* const inst_p = rank ? cl.map_shared_rank(s_inst, 0) : s_inst;
+  const int* const rcmd0 = cl.map_shared_rank(rcmd, 0);
   if (threadIdx.x < 22) {
     const int c = A.cur, k = threadIdx.x;
     cur_pose[k] = k < 9 ? M.R[9 * c + k] : k < 12 ? M.t[3 * c + k - 9] : k < 15 ? M.C[3 * c + k - 12]
@@ -2342,7 +2355,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   const lm_fuse_cfg& fc = A.fc;
   if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
   if (threadIdx.x < 16) tm[threadIdx.x] = 0;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && rank == 0) {
     M.scal[SC_DIRTY_N] = 0;  // k_fuse_refresh consumed the list
     nc_sh = 0;
     ni_sh = 0;
@@ -2351,7 +2364,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     s_nset = 0;
     tag_base = atomicAdd(&M.scal[SC_ROUND], T + 2);  // one dedupe tag per iteration (<= T + 1)
   }
-  for (int t = threadIdx.x; t < T; t += REV_THREADS) {
+  for (int t = threadIdx.x; rank == 0 && t < T; t += REV_THREADS) {
     s_nact[t] = M.s.pinfo[PI_NACT * TMAX + t];
     s_live[t] = M.s.pinfo[PI_LIVE * TMAX + t];
     s_obs[t] = M.s.pinfo[PI_OBS * TMAX + t];
@@ -2388,8 +2401,8 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   auto add_item = [&](int t, int kp, int tag) {
     const size_t it = (size_t)t * K + kp;
     if (atomicExch(&M.s.itag[it], tag) != tag) {
-      const int at = atomicAdd(&ni_sh, 1);
-      if (at < ILS) s_il[at] = (int)it;
+      const int at = atomicAdd(ni_p, 1);
+      if (at < ILS) il_p[at] = (int)it;
       else M.s.ilist[at] = (int)it;
     }
   };
@@ -2480,7 +2493,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       const int src = __ffs(hm) - 1;
       hm &= hm - 1;
       const int q = __shfl_sync(0xffffffffu, hp, src);
-      if (lane == 0) M.s.cands[atomicAdd(&nc_sh, 1)] = q;
+      if (lane == 0) M.s.cands[atomicAdd(nc_p, 1)] = q;
       point_items(q, t1, tag);
     }
     if (hc > HL) {  // overflowed list: scan the passes of the keypoint's bitmap
@@ -2560,13 +2573,27 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
           M.gval[p] = 0;
         }
       }
-      s_inst[k] = spec;
-      if (!spec) atomicAdd(&s_nset, 1);
+      inst_p[k] = spec;
+      if (!spec) atomicAdd(nset_p, 1);
     }
     __syncwarp();
   };
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int AW = (K + 31) >> 5;  // words of a pass's action bitmap
+  const int AW = (K + 31) >> 5;
+  constexpr int RW = REV_THREADS / 32;  // warps per CTA
+  if (rank > 0) {  // helper CTA: direct-pass actions k = rank*RW + wid (+ nranks*RW) on command
+    for (;;) {
+      cl.sync();  // (A) a command is published
+      const int cmd = rcmd0[0];
+      if (cmd == RC_EXIT) break;
+      const int ht1 = rcmd0[1], htag = rcmd0[2], hna = rcmd0[3];
+      for (int k = rank * RW + wid; k < hna; k += nranks * RW) add_direct(M.s.acts[k], k, ht1, htag);
+      cl.sync();  // (B) this helper's actions are applied
+    }
+    pair_acc_flush<REV_THREADS>(M, &acc);
+    cl.sync();  // (C) CTA 0's shared memory stays alive until every helper is done with it
+    return;
+  }  // words of a pass's action bitmap
   while (true) {
     // (1) warp 0: first pass (>= t0) with actions, ledger / byte accounting of the passes
     //     before it, that pass's actions in keypoint order (from its action bitmap), and the
@@ -2790,7 +2817,17 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       // items are the points' observations after the apply.
       // (8 lanes per action, four actions per warp, measured 5% slower on C2: more registers
       // spilled and the tile syncs; a warp per action stays)
-      for (int k = wid; k < na; k += REV_THREADS / 32) add_direct(s_acts[k], k, t1, tag);
+      if (nranks > 1) {  // the helper CTAs take their share of the actions
+        if (threadIdx.x == 0) {
+          rcmd[0] = RC_DIRECT;
+          rcmd[1] = t1;
+          rcmd[2] = tag;
+          rcmd[3] = na;
+        }
+        cl.sync();  // (A)
+      }
+      for (int k = wid; k < na; k += nranks * RW) add_direct(s_acts[k], k, t1, tag);
+      if (nranks > 1) cl.sync();  // (B)
       __syncthreads();
       if (threadIdx.x == 0) {
         cnt[1] += na;
@@ -2908,6 +2945,10 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     t0 = t1 + 1;
     ++iter;
   }
+  if (nranks > 1) {
+    if (threadIdx.x == 0) rcmd[0] = RC_EXIT;
+    cl.sync();  // (A) helpers leave their loop
+  }
   pair_acc_flush<REV_THREADS>(M, &acc);
   for (int t = threadIdx.x; t < T; t += REV_THREADS) M.s.pass_of[M.s.targets[t]] = -1;
   if (threadIdx.x == 0) {
@@ -2937,6 +2978,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     for (int k = 4; k < 8; ++k) st->dbg[k] += tm[k];
     st->dbg[0] += fast_passes;  // diagnostics: acting passes applied directly (all plain ADDs)
   }
+  if (nranks > 1) cl.sync();  // (C) the helpers are done with this CTA's shared memory
 }
 
 // deferred visible counters of every reverse pass (thread per item); a point merged away
