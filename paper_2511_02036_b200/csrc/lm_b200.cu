@@ -386,14 +386,12 @@ __global__ void __launch_bounds__(1024) k_op(DevMap* maps, int map, OpArgs A, in
       // to every later candidate's check.
       int* cand = (int*)A.buf;
       int* removed = cand + A.n;
-      __shared__ int nrem, red_pts, considered;
+      __shared__ int nrem;
       if (tid == 0) nrem = 0;
       for (int c = 0; c < A.n; ++c) {
         const int slot = cand[c];
         __syncthreads();
         if (M.kf_state[slot] != KF_LIVE) continue;  // (uniform)
-        if (tid == 0) red_pts = considered = 0;
-        __syncthreads();
         const int off = M.kp_off[slot], n = M.kp_n[slot];
         int rp = 0, cs = 0;
         for (int i = tid; i < n; i += 1024) {
@@ -824,6 +822,9 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   if (c->max_keyframes > LM_MAX_KF_SLOTS)
     return fail(ctx, LM_ERR_CAPACITY, "max_keyframes %d exceeds the device limit %d", c->max_keyframes,
                 LM_MAX_KF_SLOTS);
+  // the fusion apply packs keypoint and point ids into 28 bits (reservation key sets)
+  if (c->max_keypoints >= (1 << 28) || c->max_points >= (1 << 28))
+    return fail(ctx, LM_ERR_CAPACITY, "max_keypoints / max_points must be below 2^28 per map");
   CU(cudaSetDevice(ctx->device));
   HostMap* m = new HostMap();
   m->caps = *c;
@@ -1843,6 +1844,18 @@ int lm_ledger_log(lm_ctx* ctx, int32_t map, int64_t first, int64_t* bytes, int32
   if (n) CU(cudaMemcpy(bytes, m->d.lg_log + first, sizeof(long long) * n, cudaMemcpyDeviceToHost));
   return LM_OK;
 }
+
+#ifdef LM_DIAG
+// diagnostics build only: read (and clear) the device diagnostic words
+int lm_debug_diag(uint64_t* out, int n) {
+  if (n > 64) n = 64;
+  if (cudaDeviceSynchronize() != cudaSuccess) return LM_ERR_CUDA;
+  if (cudaMemcpyFromSymbol(out, lm::g_diag, n * sizeof(uint64_t)) != cudaSuccess) return LM_ERR_CUDA;
+  static const unsigned long long zero[64] = {0};
+  cudaMemcpyToSymbol(lm::g_diag, zero, sizeof(zero));
+  return LM_OK;
+}
+#endif
 
 int lm_debug_corrupt(lm_ctx* ctx, int32_t map, int32_t what, int64_t a, int64_t b, int32_t delta) {
   HostMap* m;

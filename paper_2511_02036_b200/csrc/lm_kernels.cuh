@@ -97,6 +97,45 @@ __device__ __forceinline__ int block_excl_scan(int v, int* sh, int& total) {
   return base + x - v;
 }
 
+#ifdef LM_DIAG
+// diagnostics build only (-DLM_DIAG): per apply-round maximum of each phase's per-thread
+// elapsed time, summed over rounds (g_diag[8 + phase]); g_diag[0..7] per-round scratch
+__device__ unsigned long long g_diag[64];
+__device__ __forceinline__ void diag_fold(int bank) {  // per-round maxima of one bank -> sums
+  for (int ph = 0; ph < 5; ++ph) {
+    g_diag[8 + ph] += g_diag[5 * bank + ph + 32];
+    g_diag[5 * bank + ph + 32] = 0;
+  }
+  g_diag[16] += 1;
+}
+__device__ __forceinline__ void diag_max(int phase, long long t_start) {
+  unsigned long long e = (unsigned long long)(gtime() - t_start);
+  for (int off = 16; off; off >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(__activemask(), e, off);
+    e = o > e ? o : e;
+  }
+  atomicMax(&g_diag[phase + 32], e);
+}
+#define DIAG_T0 long long diag_t0 = gtime();
+#define DIAG_RESTART diag_t0 = gtime();
+#define DIAG_MAX(ph) if (Team::kCluster) diag_max(ph + 5 * (rounds & 1), diag_t0);
+#else
+#define DIAG_T0
+#define DIAG_RESTART
+#define DIAG_MAX(ph)
+#endif
+
+// warp-aggregated atomicAdd(p, 1) over the threads active here: one atomic per warp (the
+// team control words live in one CTA's shared memory and every CTA of a cluster hits them)
+__device__ __forceinline__ int agg_inc(int* p) {
+  const unsigned am = __activemask();
+  const int lane = threadIdx.x & 31, leader = __ffs(am) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(p, __popc(am));
+  base = __shfl_sync(am, base, leader);
+  return base + __popc(am & ((1u << lane) - 1));
+}
+
 template <int BLOCK>
 __device__ __forceinline__ int block_sum(int v, int* sh) {
   int t;
@@ -217,7 +256,7 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
   const long long c_t0 = gtime();
   pair_acc_init<1024>(&acc, A.cur);
   const long long c_t1 = gtime();
-  long long c_scan = 0, c_kill = 0;
+  long long c_kill = 0;
   const int n = M.scal[SC_RECENT_N];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int kept = 0, culled = 0, nbig_total = 0;
@@ -1301,19 +1340,19 @@ __device__ bool for_keys(const DevMap& M, const ActRec& x, Op op) {
     return false;
   }
   if (partner >= 0) {
-    const int na = M.nobs[x.pid], nb = M.nobs[partner];
-    const int loser = na == nb ? (x.pid > partner ? x.pid : partner) : (na < nb ? x.pid : partner);
-    const int2* o = M.obs + M.ooff[loser];
-    const int n = M.nobs[loser];
-    for (int k0 = 0; k0 < n; k0 += 8) {  // entries and keypoint offsets loaded 8 at a time
-      int2 e[8];
-      int g[8];
+    const int na = M.nobs[x.pid], nb = M.nobs[partner], fa = M.ooff[x.pid], fb = M.ooff[partner];
+    const bool la = na == nb ? x.pid > partner : na < nb;  // the loser's list is the one rebound
+    const int2* o = M.obs + (la ? fa : fb);
+    const int n = la ? na : nb;
+    for (int k0 = 0; k0 < n; k0 += 16) {  // entries and keypoint offsets loaded 16 at a time
+      int2 e[16];
+      int g[16];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) e[j] = k0 + j < n ? o[k0 + j] : make_int2(0, 0);
+      for (int j = 0; j < 16; ++j) e[j] = k0 + j < n ? o[k0 + j] : make_int2(0, 0);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) g[j] = k0 + j < n ? M.kp_off[e[j].x] + e[j].y : 0;
+      for (int j = 0; j < 16; ++j) g[j] = k0 + j < n ? M.kp_off[e[j].x] + e[j].y : 0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
+      for (int j = 0; j < 16; ++j)
         if (k0 + j < n && !op(KM_SLOT, g[j])) return false;
     }
   }
@@ -1360,20 +1399,25 @@ __device__ __forceinline__ int classify(const DevMap& M, const ActRec& x, int* p
 // A team executes apply_team: one CTA (BlockTeam) or a thread-block cluster (ClusterTeam,
 // control words in the leader CTA's shared memory, reached through distributed shared
 // memory; barrier.cluster orders global and shared::cluster accesses at cluster scope).
-enum TeamCtl { CTL_ROUND = 0, CTL_NPEND, CTL_NMERGE, CTL_NADD, CTL_NDEF, CTL_NREADY, CTL_NGRPM, CTL_TOT = 8,
-               CTL_N = 8 + 16 };
+// two banks of control words (round parity): the leader prepares round r + 1's bank while
+// round r's later phases read their own, so a round needs no barriers of its own
+enum TeamCtl { CTL_ROUND = 0, CTL_NPEND, CTL_NMERGE, CTL_NADD, CTL_NDEF, CTL_NREADY, CTL_NGRPM, CTL_W = 8,
+               CTL_N = 2 * CTL_W };
 
 template <int BLOCK>
 struct BlockTeam {
+  static constexpr int kBlock = BLOCK;
+  static constexpr bool kCluster = false;
   int* ctl;
   int tid, nth;
   __device__ explicit BlockTeam(int* c) : ctl(c), tid(threadIdx.x), nth(BLOCK) {}
   __device__ void sync() const { __syncthreads(); }
-  __device__ int excl_scan(int v, int* sh, int& total) const { return block_excl_scan<BLOCK>(v, sh, total); }
 };
 
 template <int BLOCK>
 struct ClusterTeam {
+  static constexpr int kBlock = BLOCK;
+  static constexpr bool kCluster = true;
   int* ctl;
   int tid, nth, rank, nranks;
   __device__ ClusterTeam(int* local_ctl) {
@@ -1385,21 +1429,6 @@ struct ClusterTeam {
     nth = nranks * BLOCK;
   }
   __device__ void sync() const { cg::this_cluster().sync(); }
-  __device__ int excl_scan(int v, int* sh, int& total) const {
-    int bt;
-    const int at = block_excl_scan<BLOCK>(v, sh, bt);
-    if (threadIdx.x == 0) ctl[CTL_TOT + rank] = bt;
-    sync();
-    int pre = 0, tot = 0;
-    for (int r = 0; r < nranks; ++r) {
-      const int x = ctl[CTL_TOT + r];
-      pre += r < rank ? x : 0;
-      tot += x;
-    }
-    sync();  // totals read before the next scan overwrites them
-    total = tot;
-    return pre + at;
-  }
 };
 
 template <class Team>
@@ -1412,23 +1441,32 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
   // n actions: one iteration per thread at these sizes) instead of compacting the pending
   // list with a team-wide scan each round.
   for (int a = tid; a < n; a += nth) M.s.pend[a] = 1;
-  if (tid == 0) ctl[CTL_NPEND] = n;
+  // bank `rounds & 1` serves round `rounds`; the leader fills the next round's bank after the
+  // check barrier (its words were last read in the round before, ahead of this round's first
+  // barrier)
+  auto open_bank = [&](int* w, int npend) {
+    w[CTL_ROUND] = atomicAdd(&M.scal[SC_ROUND], 1) + 1;
+    w[CTL_NPEND] = npend;
+    w[CTL_NMERGE] = 0;
+    w[CTL_NADD] = 0;
+    w[CTL_NDEF] = 0;
+    w[CTL_NREADY] = 0;
+    w[CTL_NGRPM] = 0;
+  };
+  if (tid == 0) open_bank(ctl, n);
   G.sync();
   int rounds = 0;
-  while (ctl[CTL_NPEND] > 0) {
-    const int np = ctl[CTL_NPEND];  // (the words reset below were last read before the round's final barrier)
+  while (ctl[(rounds & 1) * CTL_W + CTL_NPEND] > 0) {
+    int* const cw = ctl + (rounds & 1) * CTL_W;        // this round's words
+    int* const nw = ctl + ((rounds + 1) & 1) * CTL_W;  // the next round's
+    const int np = cw[CTL_NPEND];
+#ifdef LM_DIAG
+    if (Team::kCluster && tid == 0) g_diag[17 + (rounds < 4 ? rounds : 4)] += np;
+#endif
     if (tm && tid == 0 && rounds > 0) tm[13] += np;  // diagnostics: actions left after round 1
-    if (tid == 0) {
-      ctl[CTL_ROUND] = atomicAdd(&M.scal[SC_ROUND], 1) + 1;
-      ctl[CTL_NMERGE] = 0;
-      ctl[CTL_NADD] = 0;
-      ctl[CTL_NDEF] = 0;
-      ctl[CTL_NREADY] = 0;
-      ctl[CTL_NGRPM] = 0;
-    }
-    G.sync();
-    const unsigned rnd = (unsigned)ctl[CTL_ROUND];
+    const unsigned rnd = (unsigned)cw[CTL_ROUND];
     long long tt = gtime();
+    DIAG_T0
     for (int a = tid; a < n; a += nth) {
       if (!M.s.pend[a]) continue;
       const unsigned long long tag = res_tag(rnd, a);
@@ -1441,39 +1479,64 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
       // the check phase takes tickets with a plain atomicAdd after the barrier
       if (x.kind == LM_ACT_ADD) M.grp_head[x.pid] = (unsigned long long)rnd << 32;
     }
+    DIAG_MAX(0)
     G.sync();
+    DIAG_RESTART
     // check (read-only): stale actions are counted, merges queued for warps, ADDs take a
     // ticket in their point's group (gtick = round << 32 | members)
     for (int a = tid; a < n; a += nth) {
       if (!M.s.pend[a]) continue;
       const unsigned long long tag = res_tag(rnd, a);
       const ActRec x = acts[a];
-      const int ready = for_keys(M, x, [&](int mode, int id) { return holds_key(M, mode, id, tag); });
+      // every key is checked (no early exit): the reservation words load together instead of
+      // one dependent load per key (a merge holds a key per observation of its loser)
+      bool ready = true;
+#ifdef LM_DIAG
+      int blocked = -1;
+      for_keys(M, x, [&](int mode, int id) {
+        const bool h = holds_key(M, mode, id, tag);
+        if (!h && blocked < 0) blocked = mode;
+        ready &= h;
+        return true;
+      });
+      if (Team::kCluster && blocked >= 0) atomicAdd(&g_diag[24 + blocked + 4 * (x.kind == LM_ACT_MERGE)], 1ull);
+#else
+      for_keys(M, x, [&](int mode, int id) {
+        ready &= holds_key(M, mode, id, tag);
+        return true;
+      });
+#endif
       if (!ready) continue;
-      M.s.pend[a] = 0;  // (read by this thread only in this round's loops)
-      atomicAdd(&ctl[CTL_NREADY], 1);
       int partner = -1;
       const int kind = classify(M, x, &partner);
+      M.s.pend[a] = 0;  // (read by this thread only in this round's loops)
+      agg_inc(&cw[CTL_NREADY]);
       if (kind == 0) {
         atomicAdd(&cnt[2], 1);
       } else if (kind == 1) {
-        const int d = atomicAdd(&ctl[CTL_NDEF], 1);
+        const int d = agg_inc(&cw[CTL_NDEF]);
         M.s.def[d] = a;
         M.s.dnxt[d] = atomicAdd(&M.grp_head[x.pid], 1ull) & 0xffffffffull;  // ticket
       } else {
-        const int at = atomicAdd(&ctl[CTL_NMERGE], 1);
+        const int at = agg_inc(&cw[CTL_NMERGE]);
         M.s.merge_a[at] = x.pid;
         M.s.merge_b[at] = partner;
       }
     }
+    DIAG_MAX(1)
     G.sync();
+    DIAG_RESTART
+    if (tid == 0) open_bank(nw, np - cw[CTL_NREADY]);
+#ifdef LM_DIAG
+    if (Team::kCluster && tid == 0 && rounds > 0) diag_fold((rounds + 1) & 1);  // the previous round's maxima are final
+#endif
     if (tm && tid == 0) {
       tm[9] += gtime() - tt;
       tt = gtime();
     }
     // group leaders (ticket 0): a lone low-degree ADD links here (thread), a lone high-degree
     // one goes to a warp; a group of m reserves m entries (base = old length) for its members
-    const int nd = ctl[CTL_NDEF];
+    const int nd = cw[CTL_NDEF];
     for (int d = tid; d < nd; d += nth) {
       if (M.s.dnxt[d] != 0ull) continue;
       const ActRec x = acts[M.s.def[d]];
@@ -1484,7 +1547,7 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
           link(M, p, x.slot, x.j, acc, true);
           atomicAdd(&cnt[1], 1);
         } else {
-          M.s.add_list[atomicAdd(&ctl[CTL_NADD], 1)] = M.s.def[d];
+          M.s.add_list[atomicAdd(&cw[CTL_NADD], 1)] = M.s.def[d];
         }
         continue;
       }
@@ -1504,7 +1567,7 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
         M.ocap[p] = nc;
       }
       M.s.gbase[p] = n0;
-      atomicAdd(&ctl[CTL_NGRPM], m);
+      atomicAdd(&cw[CTL_NGRPM], m);
       M.nobs[p] = n0 + m;
       M.found[p] += m;
       M.ver[p] += 1;
@@ -1512,7 +1575,9 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
       mark_dirty(M, p);
       atomicAdd(&cnt[1], m);
     }
+    DIAG_MAX(2)
     G.sync();
+    DIAG_RESTART
     if (tm && tid == 0) {
       tm[10] += gtime() - tt;
       tt = gtime();
@@ -1533,22 +1598,20 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
       covis_list(M, x.slot, o, base, +1, acc);
     }
     {
-      const int nm = ctl[CTL_NMERGE], na = ctl[CTL_NADD];
+      const int nm = cw[CTL_NMERGE], na = cw[CTL_NADD];
       for (int k = gwarp; k < na; k += nwarps) {
         const ActRec x = acts[M.s.add_list[k]];
-        link_warp(M, x.pid, x.slot, x.j, lane, acc);
-        if (lane == 0) {
-          mark_dirty(M, x.pid);
-          M.found[x.pid] += 1;
-        }
+        link_warp(M, x.pid, x.slot, x.j, lane, acc);  // (found + 1, dirty)
       }
       for (int k = gwarp; k < nm; k += nwarps) merge_pair_warp(M, M.s.merge_a[k], M.s.merge_b[k], lane, acc);
       if (tid == 0) atomicAdd(&cnt[0], nm);
       if (tid == 32) atomicAdd(&cnt[1], na);
     }
+    DIAG_MAX(3)
     G.sync();
+    DIAG_RESTART
     // group members: covisibility with the members of lower ticket (each new pair once)
-    const bool groups = ctl[CTL_NGRPM] > 0;
+    const bool groups = cw[CTL_NGRPM] > 0;
     for (int d = tid; groups && d < nd; d += nth) {
       const ActRec x = acts[M.s.def[d]];
       const int p = x.pid;
@@ -1558,17 +1621,15 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
       const int2* o = M.obs + M.ooff[p];
       covis_list(M, x.slot, o + base, (int)M.s.dnxt[d], +1, acc);
     }
+    DIAG_MAX(4)
     if (groups) G.sync();
-    if (tm && tid == 0) {
-      tm[11] += gtime() - tt;
-      tt = gtime();
-    }
-    G.sync();  // all reads of the control words of this round are done
-    if (tid == 0) ctl[CTL_NPEND] = np - ctl[CTL_NREADY];
-    G.sync();
-    if (tm && tid == 0) tm[12] += gtime() - tt;
+    if (tm && tid == 0) tm[11] += gtime() - tt;
+
     if (++rounds > (1 << 20)) break;
   }
+#ifdef LM_DIAG
+  if (Team::kCluster && tid == 0 && rounds > 0) diag_fold((rounds + 1) & 1);
+#endif
   return rounds;
 }
 
@@ -2785,29 +2846,6 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     };
     // points hitting current keypoint k, whose binding changed, join the touched list (hit
     // list; a keypoint whose list overflowed falls back to scanning the passes of its bitmap)
-    auto hit_list_points = [&](int k) {
-      const int c = M.s.hl_cnt[k];
-      if (c <= HL) {
-        if (lane < c) {
-          const int p = M.s.hl[k * HL + lane];
-          if (M.alive[p] && M.hit[p].y == k && atomicExch(&M.s.rmark[p], tag) != tag)
-            M.s.cands[atomicAdd(&nc_sh, 1)] = p;
-        }
-        return;
-      }
-      for (int w = 0; w < HPW; ++w) {
-        unsigned bits = M.s.hitpass[k * HPW + w];
-        while (bits) {
-          const int tt = 32 * w + __ffs(bits) - 1;
-          bits &= bits - 1;
-          if (tt <= t1 || tt >= T) continue;
-          const int n = M.kp_n[M.s.targets[tt]];
-          const int* pjt = M.s.pj + (size_t)tt * K;
-          for (int kp = lane; kp < n; kp += 32)
-            if (pjt[kp] == k) add_item(tt, kp, tag);
-        }
-      }
-    };
     if (fast_sh) {
       // every action a plain ADD of a distinct point into a distinct unbound keypoint (the
       // pass's item is current, so slot j is free and the point does not see the current

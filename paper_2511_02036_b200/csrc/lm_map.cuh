@@ -377,13 +377,18 @@ __device__ int obs_insert(const DevMap& M, int mp, int slot, int kp) {
   return n;
 }
 
-// does point mp observe keyframe slot? (branch-free scan: independent loads pipeline)
+// does point mp observe keyframe slot? (branch-free scan, 16 independent loads in flight)
 __device__ __forceinline__ bool observes(const DevMap& M, int mp, int slot) {
   const int2* o = M.obs + M.ooff[mp];
   const int n = M.nobs[mp];
   bool f = false;
-#pragma unroll 4
-  for (int k = 0; k < n; ++k) f |= o[k].x == slot;
+  for (int k0 = 0; k0 < n; k0 += 16) {
+    int s[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) s[j] = k0 + j < n ? o[k0 + j].x : -1;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) f |= s[j] == slot;
+  }
   return f;
 }
 
@@ -446,7 +451,8 @@ __device__ void geo_full(const DevMap& M, int mp) {
 // Latency-shaped: the independent loads are issued together before any store.
 // fuse=true: fusion's ADD_OBSERVATION on top (found += 1, representative descriptor marked
 // stale), with the flag/counter loads in the same first round.
-__device__ void link(const DevMap& M, int mp, int slot, int kp, PairAcc* acc = nullptr, bool fuse = false) {
+__device__ void link(const DevMap& M, int mp, int slot, int kp, PairAcc* acc = nullptr, bool fuse = false,
+                     bool covis = true) {
   // every load first: the stores below would otherwise serialise them (aliasing)
   const int n = M.nobs[mp], cap = M.ocap[mp], off = M.ooff[mp];
   const int dirty = M.dirty[mp], gv = M.gval[mp], vr = M.ver[mp];
@@ -464,7 +470,7 @@ __device__ void link(const DevMap& M, int mp, int slot, int kp, PairAcc* acc = n
   const int cv = *cnt;
   const double Sl = M.S[lev];
   const long long kf_last = last >= 0 ? M.kf_id[last] : -1;
-  covis_list(M, slot, o, n, +1, acc);
+  if (covis) covis_list(M, slot, o, n, +1, acc);
   // appended after the newest keyframe of a clean (sorted) list: the cached sums extend exactly
   const bool newest = !dirty && (n == 0 || kf_last < kf_new);
   int at = n;
@@ -506,34 +512,15 @@ __device__ void link(const DevMap& M, int mp, int slot, int kp, PairAcc* acc = n
   }
 }
 
-// link() for high-degree points: lanes share the covisibility bumps, lane 0 the rest
+// fusion's ADD_OBSERVATION (link(fuse=true)) for high-degree points: the lanes share the
+// covisibility bumps, lane 0 the record (loads first, as in link). The caller owns mp's
+// dirty flag in this phase.
 __device__ void link_warp(const DevMap& M, int mp, int slot, int kp, int lane, PairAcc* acc) {
   const int2* o = M.obs + M.ooff[mp];
   const int n = M.nobs[mp];
   for (int k = lane; k < n; k += 32) covis_add(M, slot, o[k].x, +1, acc);
   __syncwarp();
-  if (lane == 0) {
-    const bool newest = !M.dirty[mp] && (n == 0 || M.kf_id[o[n - 1].x] < M.kf_id[slot]);
-    const int at = obs_insert(M, mp, slot, kp);
-    if (at >= 0) {
-      const int g = M.kp_off[slot] + kp;
-      M.kbind[g] = mp;
-      M.counts[(size_t)mp * M.L + M.klev[g]] += 1;
-      M.ver[mp] += 1;
-      double rx, ry, rz, dd, d0;
-      if (M.gval[mp] && newest) {
-        if (geo_term(M, mp, make_int2(slot, kp), rx, ry, rz, dd, d0)) {
-          M.glo[mp] = d0 < M.glo[mp] ? d0 : M.glo[mp];
-          M.ghi[mp] = d0 > M.ghi[mp] ? d0 : M.ghi[mp];
-          M.gacc[3 * mp] = M.gacc[3 * mp] + rx / dd;
-          M.gacc[3 * mp + 1] = M.gacc[3 * mp + 1] + ry / dd;
-          M.gacc[3 * mp + 2] = M.gacc[3 * mp + 2] + rz / dd;
-        }
-      } else {
-        M.gval[mp] = 0;
-      }
-    }
-  }
+  if (lane == 0) link(M, mp, slot, kp, acc, true, false);
   __syncwarp();
 }
 
