@@ -1484,6 +1484,8 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
     DIAG_RESTART
     // check (read-only): stale actions are counted, merges queued for warps, ADDs take a
     // ticket in their point's group (gtick = round << 32 | members)
+    ActRec my_x{0, 0, 0, 0, 0};
+    int my_tick = -1;
     for (int a = tid; a < n; a += nth) {
       if (!M.s.pend[a]) continue;
       const unsigned long long tag = res_tag(rnd, a);
@@ -1514,9 +1516,15 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
       if (kind == 0) {
         atomicAdd(&cnt[2], 1);
       } else if (kind == 1) {
-        const int d = agg_inc(&cw[CTL_NDEF]);
-        M.s.def[d] = a;
-        M.s.dnxt[d] = atomicAdd(&M.grp_head[x.pid], 1ull) & 0xffffffffull;  // ticket
+        const int tick = (int)(atomicAdd(&M.grp_head[x.pid], 1ull) & 0xffffffffull);
+        if (a == tid) {  // the thread's first action stays in registers for the commit phases
+          my_x = x;
+          my_tick = tick;
+        } else {
+          const int d = agg_inc(&cw[CTL_NDEF]);
+          M.s.def[d] = a;
+          M.s.dnxt[d] = tick;
+        }
       } else {
         const int at = agg_inc(&cw[CTL_NMERGE]);
         M.s.merge_a[at] = x.pid;
@@ -1526,7 +1534,7 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
     DIAG_MAX(1)
     G.sync();
     DIAG_RESTART
-    if (tid == 0) open_bank(nw, np - cw[CTL_NREADY]);
+    if (tid == nth - 1) open_bank(nw, np - cw[CTL_NREADY]);  // (the team's last thread: rarely an action)
 #ifdef LM_DIAG
     if (Team::kCluster && tid == 0 && rounds > 0) diag_fold((rounds + 1) & 1);  // the previous round's maxima are final
 #endif
@@ -1537,21 +1545,18 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
     // group leaders (ticket 0): a lone low-degree ADD links here (thread), a lone high-degree
     // one goes to a warp; a group of m reserves m entries (base = old length) for its members
     const int nd = cw[CTL_NDEF];
-    for (int d = tid; d < nd; d += nth) {
-      if (M.s.dnxt[d] != 0ull) continue;
-      const ActRec x = acts[M.s.def[d]];
+    auto head = [&](const ActRec& x, int a_idx) {
       const int p = x.pid;
-      const int m = (int)(M.grp_head[p] & 0xffffffffull);
+      const int m = (int)(M.grp_head[p] & 0xffffffffull), n0 = M.nobs[p];
       if (m == 1) {
-        if (M.nobs[p] <= 24) {
+        if (n0 <= 24) {
           link(M, p, x.slot, x.j, acc, true);
           atomicAdd(&cnt[1], 1);
         } else {
-          M.s.add_list[atomicAdd(&cw[CTL_NADD], 1)] = M.s.def[d];
+          M.s.add_list[atomicAdd(&cw[CTL_NADD], 1)] = a_idx;
         }
-        continue;
+        return;
       }
-      const int n0 = M.nobs[p];
       if (n0 + m > M.ocap[p]) {  // grow by doubling, copy the current entries
         int nc = M.ocap[p] < 4 ? 4 : M.ocap[p];
         while (nc < n0 + m) nc *= 2;
@@ -1559,7 +1564,7 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
         if (off + nc > M.obs_cap) {
           set_err(M, LM_ERR_CAPACITY);
           M.s.gbase[p] = -1;
-          continue;
+          return;
         }
         const int2* src = M.obs + M.ooff[p];
         copy_obs(M.obs + off, src, n0);
@@ -1574,7 +1579,10 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
       M.gval[p] = 0;
       mark_dirty(M, p);
       atomicAdd(&cnt[1], m);
-    }
+    };
+    if (my_tick == 0) head(my_x, tid);
+    for (int d = tid; d < nd; d += nth)
+      if (M.s.dnxt[d] == 0ull) head(acts[M.s.def[d]], M.s.def[d]);
     DIAG_MAX(2)
     G.sync();
     DIAG_RESTART
@@ -1584,19 +1592,20 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
     }
     // group members: own entry, binding, counter, covisibility with the old observers;
     // warps: lone high-degree ADDs and merges (disjoint entities)
-    for (int d = tid; d < nd; d += nth) {
-      const ActRec x = acts[M.s.def[d]];
+    auto member = [&](const ActRec& x, int tick) {
       const int p = x.pid;
       const int m = (int)(M.grp_head[p] & 0xffffffffull);
       const int base = M.s.gbase[p];
-      if (m == 1 || base < 0) continue;
+      if (m == 1 || base < 0) return;
       int2* o = M.obs + M.ooff[p];
-      o[base + (int)M.s.dnxt[d]] = make_int2(x.slot, x.j);
+      o[base + tick] = make_int2(x.slot, x.j);
       const int g = M.kp_off[x.slot] + x.j;
       M.kbind[g] = p;
       atomicAdd(&M.counts[(size_t)p * M.L + M.klev[g]], 1);
       covis_list(M, x.slot, o, base, +1, acc);
-    }
+    };
+    if (my_tick >= 0) member(my_x, my_tick);
+    for (int d = tid; d < nd; d += nth) member(acts[M.s.def[d]], (int)M.s.dnxt[d]);
     {
       const int nm = cw[CTL_NMERGE], na = cw[CTL_NADD];
       for (int k = gwarp; k < na; k += nwarps) {
@@ -1612,15 +1621,16 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
     DIAG_RESTART
     // group members: covisibility with the members of lower ticket (each new pair once)
     const bool groups = cw[CTL_NGRPM] > 0;
-    for (int d = tid; groups && d < nd; d += nth) {
-      const ActRec x = acts[M.s.def[d]];
+    auto member_pairs = [&](const ActRec& x, int tick) {
       const int p = x.pid;
       const int m = (int)(M.grp_head[p] & 0xffffffffull);
       const int base = M.s.gbase[p];
-      if (m == 1 || base < 0) continue;
+      if (m == 1 || base < 0) return;
       const int2* o = M.obs + M.ooff[p];
-      covis_list(M, x.slot, o + base, (int)M.s.dnxt[d], +1, acc);
-    }
+      covis_list(M, x.slot, o + base, tick, +1, acc);
+    };
+    if (groups && my_tick > 0) member_pairs(my_x, my_tick);
+    for (int d = tid; groups && d < nd; d += nth) member_pairs(acts[M.s.def[d]], (int)M.s.dnxt[d]);
     DIAG_MAX(4)
     if (groups) G.sync();
     if (tm && tid == 0) tm[11] += gtime() - tt;
