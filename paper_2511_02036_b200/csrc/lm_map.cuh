@@ -739,28 +739,44 @@ __device__ void kill_point_warp(const DevMap& M, int mp, int lane, PairAcc* acc)
   __syncwarp();
 }
 
-// replace_map_point(loser, winner) (mapmodel.py:245-267), warp-cooperative; returns migrated
-__device__ int replace_point_warp(const DevMap& M, int loser, int winner, int lane, PairAcc* acc) {
-  int2* oL = M.obs + M.ooff[loser];
-  const int2* oW = M.obs + M.ooff[winner];
-  const int nL = M.nobs[loser], nW = M.nobs[winner];
+// fusion._merge (fusion.py) = replace_map_point(loser, winner) (mapmodel.py:245-267) + the
+// winner's found bump, warp-cooperative. Every scalar of both points is loaded in one first
+// round (the stores below would otherwise serialise the loads); the caller owns both points
+// in this phase (exclusive reservations), so the winner's dirty flag is set without an atomic
+// exchange.
+__device__ void merge_pair_warp(const DevMap& M, int a, int b, int lane, PairAcc* acc) {
+  const int na = M.nobs[a], nb = M.nobs[b], fa = M.ooff[a], fb = M.ooff[b], ca = M.ocap[a], cb = M.ocap[b];
+  const int ua = M.found[a], ub = M.found[b], va = M.visible[a], vb = M.visible[b];
+  const int ra = M.ver[a], rb = M.ver[b], da = M.dirty[a], db = M.dirty[b];
+  const int mtag = M.scal[SC_MTAG];
+  const bool la = na == nb ? a > b : na < nb;  // a loses (fewer observations; tie: larger id)
+  const int loser = la ? a : b, winner = la ? b : a;
+  const int nL = la ? na : nb, nW = la ? nb : na, offW = la ? fb : fa, capW = la ? cb : ca;
+  int2* oL = M.obs + (la ? fa : fb);
+  const int2* oW = M.obs + offW;
   // (a) covisibility -1 for every pair of the loser's observers
   covis_pairs_warp(M, oL, nL, -1, lane, acc);
   __syncwarp();
   // (b) migrate the observations of keyframes the winner does not see; compact them in place
   int nM = 0;
   for (int c0 = 0; c0 < nL; c0 += 32) {
-    const int a = c0 + lane;
+    const int k = c0 + lane;
     int2 e = make_int2(0, 0);
     bool mig = false;
-    if (a < nL) {
-      e = oL[a];
+    if (k < nL) {
+      e = oL[k];
       mig = true;
-      for (int w = 0; w < nW; ++w) mig &= oW[w].x != e.x;
+      for (int w0 = 0; w0 < nW; w0 += 8) {  // winner entries 8 at a time (broadcast loads)
+        int sw[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sw[j] = w0 + j < nW ? oW[w0 + j].x : -1;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) mig &= sw[j] != e.x;
+      }
     }
     const unsigned bal = __ballot_sync(0xffffffffu, mig);
     __syncwarp();
-    if (a < nL) {
+    if (k < nL) {
       const int g = M.kp_off[e.x] + e.y;
       M.kbind[g] = mig ? winner : -1;
       if (mig) {
@@ -776,70 +792,48 @@ __device__ int replace_point_warp(const DevMap& M, int loser, int winner, int la
   covis_pairs_warp(M, oL, nM, +1, lane, acc);
   // (d) winner list += migrated observations (appended; the winner is marked dirty, so the
   //     list is re-sorted by keyframe id before any order-dependent read)
+  int nWn = nW, offWn = offW, capWn = capW;
   if (nM > 0) {
-    int off = 0, cap = M.ocap[winner];
-    if (lane == 0) {
-      off = M.ooff[winner];
-      if (nW + nM > cap) {
-        int nc = cap < 4 ? 4 : cap;
-        while (nc < nW + nM) nc *= 2;
-        off = atomicAdd(&M.scal[SC_OBS_HEAD], nc);
-        if (off + nc > M.obs_cap) {
-          set_err(M, LM_ERR_CAPACITY);
-          off = -1;
-        }
-        cap = nc;
+    int off = offW, cap = capW;
+    if (lane == 0 && nW + nM > capW) {
+      int nc = capW < 4 ? 4 : capW;
+      while (nc < nW + nM) nc *= 2;
+      off = atomicAdd(&M.scal[SC_OBS_HEAD], nc);
+      if (off + nc > M.obs_cap) {
+        set_err(M, LM_ERR_CAPACITY);
+        off = -1;
       }
+      cap = nc;
     }
     off = __shfl_sync(0xffffffffu, off, 0);
     cap = __shfl_sync(0xffffffffu, cap, 0);
     if (off >= 0) {
       int2* B = M.obs + off;
-      if (off != M.ooff[winner])
+      if (off != offW)
         for (int i = lane; i < nW; i += 32) B[i] = oW[i];
       for (int j = lane; j < nM; j += 32) B[nW + j] = oL[j];
-      __syncwarp();
-      if (lane == 0) {
-        M.ooff[winner] = off;
-        M.ocap[winner] = cap;
-        M.nobs[winner] = nW + nM;
-      }
+      nWn = nW + nM;
+      offWn = off;
+      capWn = cap;
     }
   }
   __syncwarp();
   for (int l = lane; l < M.L; l += 32) M.counts[(size_t)loser * M.L + l] = 0;
   if (lane == 0) {
+    M.ooff[winner] = offWn;
+    M.ocap[winner] = capWn;
+    M.nobs[winner] = nWn;
     M.nobs[loser] = 0;
-    M.found[winner] += M.found[loser];
-    M.visible[winner] += M.visible[loser];
+    M.found[winner] = ua + ub + 1;  // found(winner) + found(loser), then _merge's own bump
+    M.visible[winner] = va + vb;
     M.alive[loser] = 0;
-    M.mrg[loser] = make_int2(M.scal[SC_MTAG], winner);
+    M.mrg[loser] = make_int2(mtag, winner);
     M.gval[winner] = 0;
     M.gval[loser] = 0;
-    M.ver[winner] += 1;
-    M.ver[loser] += 1;
-    mark_dirty(M, winner);
+    M.ver[winner] = (la ? rb : ra) + 1;
+    M.ver[loser] = (la ? ra : rb) + 1;
+    mark_dirty_owned(M, winner, la ? db : da);
   }
-  __syncwarp();
-  return nM;
-}
-
-// fusion._merge, warp-cooperative
-__device__ void merge_pair_warp(const DevMap& M, int a, int b, int lane, PairAcc* acc) {
-  const int na = M.nobs[a], nb = M.nobs[b];
-  int loser, winner;
-  if (na == nb) {
-    loser = a > b ? a : b;
-    winner = a > b ? b : a;
-  } else if (na < nb) {
-    loser = a;
-    winner = b;
-  } else {
-    loser = b;
-    winner = a;
-  }
-  replace_point_warp(M, loser, winner, lane, acc);
-  if (lane == 0) M.found[winner] += 1;
   __syncwarp();
 }
 
