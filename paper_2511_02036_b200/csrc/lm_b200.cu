@@ -884,7 +884,7 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   A(s.pass_j, d.kpkf_max); A(s.add_list, (size_t)s.act_cap);
   A(s.def, (size_t)s.act_cap); A(s.dnxt, (size_t)s.act_cap); A(s.gbase, MP);
   A(s.pinfo, 3 * TMAX); A(s.hitpass, (size_t)d.kpkf_max * ((TMAX + 31) / 32)); A(s.pj, (size_t)s.act_cap);
-  A(s.pass_of, K); A(s.snap, d.kpkf_max); A(s.chg, d.kpkf_max); A(s.rmark, MP);
+  A(s.pass_of, K); A(s.snap, d.kpkf_max); A(s.chg, d.kpkf_max); A(s.rmark, MP); A(s.die, MP);
   A(s.pmp, (size_t)s.act_cap); A(s.pob, (size_t)s.act_cap); A(s.itag, (size_t)s.act_cap); A(s.ilist, (size_t)s.act_cap);
   A(s.cands, (size_t)s.act_cap); A(s.cneed, (size_t)s.act_cap); A(s.hl_cnt, d.kpkf_max); A(s.hl, (size_t)d.kpkf_max * HL); A(s.hreg, MP); A(s.upts, (size_t)s.act_cap); A(s.sp_list, (size_t)s.act_cap); A(s.sp_obs, (size_t)POST_BLOCKS * 8 * (POST_MAXN + 1));
   A(s.abits, (size_t)TMAX * ((d.kpkf_max + 31) / 32));
@@ -897,6 +897,7 @@ int lm_map_create(lm_ctx* ctx, const lm_map_caps* c, int32_t* map_out) {
   CU(cudaMemsetAsync(d.res_pair, 0xff, sizeof(unsigned long long) * RES_PAIR, ctx->stream));
   CU(cudaMemsetAsync(d.grp_head, 0, sizeof(unsigned long long) * MP, ctx->stream));
   CU(cudaMemsetAsync(d.s.rmark, 0, sizeof(int) * MP, ctx->stream));
+  CU(cudaMemsetAsync(d.s.die, 0, sizeof(int) * MP, ctx->stream));
   CU(cudaMemsetAsync(d.s.itag, 0, sizeof(int) * d.s.act_cap, ctx->stream));
   CU(cudaMemsetAsync(d.mrg, 0, sizeof(int2) * MP, ctx->stream));
   CU(cudaMemsetAsync(d.s.hreg, 0, sizeof(int) * MP, ctx->stream));
@@ -953,6 +954,7 @@ int lm_map_reset(lm_ctx* ctx, int32_t map) {
   CU(cudaMemsetAsync(d.res_pair, 0xff, sizeof(unsigned long long) * RES_PAIR, ctx->stream));
   CU(cudaMemsetAsync(d.grp_head, 0, sizeof(unsigned long long) * MP, ctx->stream));
   CU(cudaMemsetAsync(d.s.rmark, 0, sizeof(int) * MP, ctx->stream));
+  CU(cudaMemsetAsync(d.s.die, 0, sizeof(int) * MP, ctx->stream));
   CU(cudaMemsetAsync(d.s.itag, 0, sizeof(int) * d.s.act_cap, ctx->stream));
   CU(cudaMemsetAsync(d.mrg, 0, sizeof(int2) * MP, ctx->stream));
   CU(cudaMemsetAsync(d.s.hreg, 0, sizeof(int) * MP, ctx->stream));
@@ -2456,6 +2458,7 @@ int lm_map_rewind(lm_ctx* ctx, int32_t map) {
   CU(cudaMemsetAsync(d.res_pair, 0xff, sizeof(unsigned long long) * RES_PAIR, st));
   CU(cudaMemsetAsync(d.grp_head, 0, sizeof(unsigned long long) * MP, st));
   CU(cudaMemsetAsync(d.s.rmark, 0, sizeof(int) * MP, st));
+  CU(cudaMemsetAsync(d.s.die, 0, sizeof(int) * MP, st));
   CU(cudaMemsetAsync(d.s.itag, 0, sizeof(int) * d.s.act_cap, st));
   CU(cudaMemsetAsync(d.mrg, 0, sizeof(int2) * MP, st));
   CU(cudaMemsetAsync(d.s.hreg, 0, sizeof(int) * MP, st));

@@ -1529,12 +1529,13 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
         const int at = agg_inc(&cw[CTL_NMERGE]);
         M.s.merge_a[at] = x.pid;
         M.s.merge_b[at] = partner;
+        const int na = M.nobs[x.pid], nb = M.nobs[partner];  // (merge_pair_warp's loser rule)
+        M.s.die[(na == nb ? x.pid > partner : na < nb) ? x.pid : partner] = (int)rnd;
       }
     }
     DIAG_MAX(1)
     G.sync();
     DIAG_RESTART
-    if (tid == nth - 1) open_bank(nw, np - cw[CTL_NREADY]);  // (the team's last thread: rarely an action)
 #ifdef LM_DIAG
     if (Team::kCluster && tid == 0 && rounds > 0) diag_fold((rounds + 1) & 1);  // the previous round's maxima are final
 #endif
@@ -1583,9 +1584,21 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
     if (my_tick == 0) head(my_x, tid);
     for (int d = tid; d < nd; d += nth)
       if (M.s.dnxt[d] == 0ull) head(acts[M.s.def[d]], M.s.def[d]);
+    // a pending action whose point (or merge partner) loses a merge of this round is stale:
+    // that merge comes first (it holds the point exclusively), and nothing revives a point
+    for (int a = tid; a < n; a += nth) {
+      if (!M.s.pend[a]) continue;
+      const ActRec x = acts[a];
+      if ((x.pid >= 0 && M.s.die[x.pid] == (int)rnd) || (x.kind == LM_ACT_MERGE && x.other >= 0 && M.s.die[x.other] == (int)rnd)) {
+        M.s.pend[a] = 0;
+        agg_inc(&cw[CTL_NREADY]);
+        atomicAdd(&cnt[2], 1);
+      }
+    }
     DIAG_MAX(2)
     G.sync();
     DIAG_RESTART
+    if (tid == nth - 1) open_bank(nw, np - cw[CTL_NREADY]);  // (the team's last thread: rarely an action)
     if (tm && tid == 0) {
       tm[10] += gtime() - tt;
       tt = gtime();

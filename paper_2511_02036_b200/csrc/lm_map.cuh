@@ -123,6 +123,7 @@ struct Scratch {
   int* snap;             // [kpkf_max] current keyframe bindings before an apply
   int* chg;              // [kpkf_max] current keypoints whose binding an apply changed
   int* rmark;            // [mp_cap] dedup tag of the touched-point list
+  int* die;              // [mp_cap] apply round (tag) in which the point loses a merge
   int* pmp;              // [TMAX*kpkf_max] per (pass, keypoint): bound live point at evaluation
   int* pob;              // [TMAX*kpkf_max] per (pass, keypoint): its observation count then
   int* itag;             // [TMAX*kpkf_max] dedup tag of the re-evaluation list
