@@ -2544,6 +2544,8 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   auto add_direct = [&](const ActRec x, int k, int t1, int tag) {
     const int lane = threadIdx.x & 31;
     const int p = x.pid, j = x.j;
+    // first round: every scalar of the point, its speculated post-ADD state (used only when it
+    // matches), the hit list count of j
     const int n = M.nobs[p], off = M.ooff[p], cap = M.ocap[p];
     const int dirty = M.dirty[p], gv = M.gval[p], vr = M.ver[p], found = M.found[p];
     const int lev = TV.lev[j];
@@ -2555,11 +2557,76 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     const int cv = *cntp;
     const double Sl = M.S[lev];
     const int hc = M.s.hl_cnt[j];
+    const uint4 r0 = M.sp_rep[2 * (size_t)p], r1 = M.sp_rep[2 * (size_t)p + 1];
+    const double* sg = M.sp_geo + 5 * (size_t)p;
+    const double g0 = sg[0], g1 = sg[1], g2 = sg[2], g3 = sg[3], g4 = sg[4];
+    const int sh_ = M.sp_hit[p];
+    // second round: the observation entries, the hit list
     const int hp = lane < hc && lane < HL ? M.s.hl[j * HL + lane] : -1;
     const int2* o = M.obs + off;
     const int2 e0 = lane < n ? o[lane] : make_int2(cur, 0), e1 = lane + 32 < n ? o[lane + 32] : make_int2(cur, 0);
     const int o0 = e0.x, o1 = e1.x;
     const int last = n ? o[n - 1].x : -1;
+    const bool spec = stag == mtag && sv0 == vr && sn0 == n && sj == j;
+    // the record first (lane 0; its stores do not feed the item / hit-list walks below: the
+    // point is already listed for this iteration, rmark == tag), so its chain overlaps theirs
+    if (lane == 0) {
+      int2* dst = M.obs + off;
+      if (n == cap) {
+        const int nc = cap < 4 ? 4 : 2 * cap;
+        const int noff = atomicAdd(&M.scal[SC_OBS_HEAD], nc);
+        if (noff + nc > M.obs_cap) {
+          set_err(M, LM_ERR_CAPACITY);  // (the step fails; the record is left as it was)
+          dst = nullptr;
+        } else {
+          copy_obs(M.obs + noff, o, n);
+          M.ooff[p] = noff;
+          M.ocap[p] = nc;
+          dst = M.obs + noff;
+        }
+      }
+      if (dst) {
+        dst[n] = make_int2(cur, j);
+        M.nobs[p] = n + 1;
+        M.kbind[cur_off + j] = p;
+        *cntp = cv + 1;
+        M.ver[p] = vr + 1;
+        M.found[p] = found + 1;
+        if (spec) {
+          M.rep[2 * (size_t)p] = r0;
+          M.rep[2 * (size_t)p + 1] = r1;
+          M.gacc[3 * p] = g0;
+          M.gacc[3 * p + 1] = g1;
+          M.gacc[3 * p + 2] = g2;
+          M.glo[p] = g3;
+          M.ghi[p] = g4;
+          M.gval[p] = 1;
+          M.dirty[p] = 0;
+          M.hit[p] = make_int2(vr + 1, sh_);
+          hit_list_add(M, sh_, p);
+          atomicAdd((unsigned long long*)&M.s.stats->dbg[12], 1ull);
+        } else {
+          mark_dirty_owned(M, p, dirty);
+          const long long kf_last = last >= 0 ? M.kf_id[last] : -1;
+          if (gv && !dirty && (n == 0 || kf_last < kf_cur)) {
+            const double rx = px - cur_pose[12], ry = py - cur_pose[13], rz = pz - cur_pose[14];
+            const double dd = sqrt(rx * rx + ry * ry + rz * rz);
+            if (dd > 0) {  // geo_term
+              const double d0 = dd / Sl;
+              M.glo[p] = d0 < lo ? d0 : lo;
+              M.ghi[p] = d0 > hi ? d0 : hi;
+              M.gacc[3 * p] = ax + rx / dd;
+              M.gacc[3 * p + 1] = ay + ry / dd;
+              M.gacc[3 * p + 2] = az + rz / dd;
+            }
+          } else {
+            M.gval[p] = 0;
+          }
+        }
+        inst_p[k] = spec;
+        if (!spec) atomicAdd(nset_p, 1);
+      }
+    }
     // the point's items in passes after t1 (its observations after the ADD: the old ones and
     // (cur, j)), and the points hitting j (hit list): their hits are unchanged by the apply
     const int tt0 = M.s.pass_of[o0], tt1 = M.s.pass_of[o1], ttc = lane == 0 ? M.s.pass_of[cur] : -1;
@@ -2594,72 +2661,9 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
         }
       }
     }
-    const bool spec = stag == mtag && sv0 == vr && sn0 == n && sj == j;
     covis_add(M, cur, o0, +1, &acc);
     covis_add(M, cur, o1, +1, &acc);
     for (int e = lane + 64; e < n; e += 32) covis_add(M, cur, o[e].x, +1, &acc);
-    int2* dst = nullptr;
-    if (lane == 0) {
-      dst = M.obs + off;
-      if (n == cap) {
-        const int nc = cap < 4 ? 4 : 2 * cap;
-        const int noff = atomicAdd(&M.scal[SC_OBS_HEAD], nc);
-        if (noff + nc > M.obs_cap) {
-          set_err(M, LM_ERR_CAPACITY);  // (the step fails; the record is left as it was)
-          dst = nullptr;
-        } else {
-          copy_obs(M.obs + noff, o, n);
-          M.ooff[p] = noff;
-          M.ocap[p] = nc;
-          dst = M.obs + noff;
-        }
-      }
-    }
-    if (lane == 0 && dst) {
-      dst[n] = make_int2(cur, j);
-      M.nobs[p] = n + 1;
-      M.kbind[cur_off + j] = p;
-      *cntp = cv + 1;
-      M.ver[p] = vr + 1;
-      M.found[p] = found + 1;
-      if (spec) {
-        const uint4 r0 = M.sp_rep[2 * (size_t)p], r1 = M.sp_rep[2 * (size_t)p + 1];
-        const double* sg = M.sp_geo + 5 * (size_t)p;
-        const double g0 = sg[0], g1 = sg[1], g2 = sg[2], g3 = sg[3], g4 = sg[4];
-        const int sh_ = M.sp_hit[p];
-        M.rep[2 * (size_t)p] = r0;
-        M.rep[2 * (size_t)p + 1] = r1;
-        M.gacc[3 * p] = g0;
-        M.gacc[3 * p + 1] = g1;
-        M.gacc[3 * p + 2] = g2;
-        M.glo[p] = g3;
-        M.ghi[p] = g4;
-        M.gval[p] = 1;
-        M.dirty[p] = 0;
-        M.hit[p] = make_int2(vr + 1, sh_);
-        hit_list_add(M, sh_, p);
-        atomicAdd((unsigned long long*)&M.s.stats->dbg[12], 1ull);
-      } else {
-        mark_dirty_owned(M, p, dirty);
-        const long long kf_last = last >= 0 ? M.kf_id[last] : -1;
-        if (gv && !dirty && (n == 0 || kf_last < kf_cur)) {
-          const double rx = px - cur_pose[12], ry = py - cur_pose[13], rz = pz - cur_pose[14];
-          const double dd = sqrt(rx * rx + ry * ry + rz * rz);
-          if (dd > 0) {  // geo_term
-            const double d0 = dd / Sl;
-            M.glo[p] = d0 < lo ? d0 : lo;
-            M.ghi[p] = d0 > hi ? d0 : hi;
-            M.gacc[3 * p] = ax + rx / dd;
-            M.gacc[3 * p + 1] = ay + ry / dd;
-            M.gacc[3 * p + 2] = az + rz / dd;
-          }
-        } else {
-          M.gval[p] = 0;
-        }
-      }
-      inst_p[k] = spec;
-      if (!spec) atomicAdd(nset_p, 1);
-    }
     __syncwarp();
   };
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
