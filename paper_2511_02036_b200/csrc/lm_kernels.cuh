@@ -2410,8 +2410,6 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   constexpr int JBW = 64;    // words of the direct pass's keypoint bitmap
   __shared__ int s_inst[DMAX];  // direct pass: action k's point took its speculated state
   __shared__ unsigned s_jb[JBW];
-  __shared__ int s_wpre[64];         // direct action extraction: prefix counts of the bitmap words
-  __shared__ unsigned s_wbits[64];
   __shared__ int s_nset, tag_base;
   constexpr int ILS = 1024;
   __shared__ int s_il[ILS];     // the iteration's item list (overflow: M.s.ilist)
@@ -2422,7 +2420,6 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   enum { RC_DIRECT = 1, RC_EXIT = 2 };
   // CTA 0's counters and lists, reached by the helper CTAs through distributed shared memory
   int* const ni_p = rank ? cl.map_shared_rank(&ni_sh, 0) : &ni_sh;
-  int* const nc_p = rank ? cl.map_shared_rank(&nc_sh, 0) : &nc_sh;
   int* const nset_p = rank ? cl.map_shared_rank(&s_nset, 0) : &s_nset;
   int* const il_p = rank ? cl.map_shared_rank(s_il, 0) : s_il;
   int* const inst_p = rank ? cl.map_shared_rank(s_inst, 0) : s_inst;
@@ -2521,11 +2518,22 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     if (j < 0) return v;
     atomicOr(&M.s.hitpass[j * HPW + (t >> 5)], 1u << (t & 31));
     const int owner = M.kbind[cur_off + j];
+    // the first 16 list entries load with the owner (used if the keypoint is free: does the
+    // point already observe the current keyframe?), later ones 16 at a time
+    const int2* o = M.obs + off;
+    int sl[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) sl[q] = q < nob ? o[q].x : -1;
     if (owner < 0) {
-      const int2* o = M.obs + off;
       bool f = false;
-#pragma unroll 4
-      for (int k = 0; k < nob; ++k) f |= o[k].x == cur;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) f |= sl[q] == cur;
+      for (int k0 = 16; k0 < nob; k0 += 16) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) sl[q] = k0 + q < nob ? o[k0 + q].x : -1;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) f |= sl[q] == cur;
+      }
       if (!f) {
         v.a = ActRec{cur, mp, j, -1, LM_ACT_ADD};
         v.has = 1;
@@ -2630,7 +2638,12 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     // the point's items in passes after t1 (its observations after the ADD: the old ones and
     // (cur, j)), and the points hitting j (hit list): their hits are unchanged by the apply
     const int tt0 = M.s.pass_of[o0], tt1 = M.s.pass_of[o1], ttc = lane == 0 ? M.s.pass_of[cur] : -1;
-    const bool hq = hp >= 0 && M.alive[hp] && M.hit[hp].y == j;
+    // hit-list point state in one round, its list head included (a point is listed under one
+    // keypoint, its hit, so no other warp of this pass walks it; the action points are marked)
+    const bool hv = hp >= 0;
+    const int hal = hv ? M.alive[hp] : 0, hy = hv ? M.hit[hp].y : -2, hrm = hv ? M.s.rmark[hp] : tag;
+    const int hno = hv ? M.nobs[hp] : 0, hof = hv ? M.ooff[hp] : 0;
+    const bool hq = hv && hal && hy == j && hrm != tag;
     if (lane < n && tt0 > t1) add_item(tt0, e0.y, tag);
     if (lane + 32 < n && tt1 > t1) add_item(tt1, e1.y, tag);
     if (ttc > t1) add_item(ttc, j, tag);
@@ -2639,13 +2652,16 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       const int tt = M.s.pass_of[ob.x];
       if (tt > t1) add_item(tt, ob.y, tag);
     }
-    unsigned hm = __ballot_sync(0xffffffffu, hq && atomicExch(&M.s.rmark[hp], tag) != tag);
+    unsigned hm = __ballot_sync(0xffffffffu, hq);
     while (hm) {  // hit-list points' items (their state is unchanged)
       const int src = __ffs(hm) - 1;
       hm &= hm - 1;
-      const int q = __shfl_sync(0xffffffffu, hp, src);
-      if (lane == 0) M.s.cands[atomicAdd(nc_p, 1)] = q;
-      point_items(q, t1, tag);
+      const int qn = __shfl_sync(0xffffffffu, hno, src), qo = __shfl_sync(0xffffffffu, hof, src);
+      for (int e = lane; e < qn; e += 32) {
+        const int2 ob = M.obs[qo + e];
+        const int tt = M.s.pass_of[ob.x];
+        if (tt > t1) add_item(tt, ob.y, tag);
+      }
     }
     if (hc > HL) {  // overflowed list: scan the passes of the keypoint's bitmap
       for (int w = 0; w < HPW; ++w) {
@@ -2675,7 +2691,13 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       const int cmd = rcmd0[0];
       if (cmd == RC_EXIT) break;
       const int ht1 = rcmd0[1], htag = rcmd0[2], hna = rcmd0[3];
+#ifdef LM_DIAG
+      const long long hd0 = gtime();
+#endif
       for (int k = rank * RW + wid; k < hna; k += nranks * RW) add_direct(M.s.acts[k], k, ht1, htag);
+#ifdef LM_DIAG
+      if (lane == 0) atomicMax(&g_diag[60], (unsigned long long)(gtime() - hd0));
+#endif
       cl.sync();  // (B) this helper's actions are applied
     }
     pair_acc_flush<REV_THREADS>(M, &acc);
@@ -2688,7 +2710,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     //     touched points (action points + current owners of the hit keypoints, deduplicated).
     //     The other warps snapshot the current keyframe's bindings.
     const long long ta = gtime();
-    if (wid == 0) {
+    if (wid == 1) {  // warp 1: the accounting (off warp 0's chain)
       int t1 = T;
       for (int tb = t0; tb < T; tb += 32) {
         const unsigned bal = __ballot_sync(0xffffffffu, tb + lane < T && s_nact[tb + lane] > 0);
@@ -2709,7 +2731,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
         a_p += __shfl_xor_sync(0xffffffffu, a_p, off);
         a_n += __shfl_xor_sync(0xffffffffu, a_n, off);
       }
-      alg += a_b;  // (meaningful on thread 0)
+      alg += a_b;  // (meaningful on thread 32)
       npts += a_p;
       nacts += a_n;
       {  // one record_small_transfer per reverse pass, in pass order (after the forward one)
@@ -2718,17 +2740,43 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
           if (ev0 + t < (unsigned long long)LG_LOG_CAP) M.lg_log[ev0 + t] = (long long)s_live[t] * (long long)mpb;
       }
       ledger_events += te - t0 + 1;
+    }
+    if (wid == 0) {
+      int t1 = T;
+      for (int tb = t0; tb < T; tb += 32) {
+        const unsigned bal = __ballot_sync(0xffffffffu, tb + lane < T && s_nact[tb + lane] > 0);
+        if (bal) {
+          t1 = tb + __ffs(bal) - 1;
+          break;
+        }
+      }
       int na = 0;
       const int tg = tag_base + 1 + iter;
       if (t1 < T) {
         const unsigned* bits = M.s.abits + (size_t)t1 * AW;
         const ActRec* seg = M.s.acts2 + (size_t)t1 * K;
         if (AW <= 64) {
-          // lane per action: both bitmap words per lane loaded at once, word prefix counts in
-          // shared memory, action a = the (a - pre[w])-th set bit of the word w holding it;
-          // all record loads issued before any store
+          // lane per word pair (w = lane, lane + 32): the first two set bits of each word are
+          // extracted in registers and their records loaded at once, while the word prefix
+          // counts are scanned; further bits (rare) in a loop. Keypoint order = word order.
           const unsigned b0 = lane < AW ? bits[lane] : 0u, b1 = lane + 32 < AW ? bits[lane + 32] : 0u;
           const int c0 = __popc(b0), c1 = __popc(b1);
+#ifdef LM_DIAG
+          if (lane == 0) g_diag[48] += gtime() - ta;
+#endif
+          unsigned r0 = b0, r1 = b1;
+          int kq[4];
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            kq[i] = r0 ? 32 * lane + __ffs(r0) - 1 : -1;
+            r0 &= r0 - 1;
+            kq[2 + i] = r1 ? 32 * (lane + 32) + __ffs(r1) - 1 : -1;
+            r1 &= r1 - 1;
+          }
+          ActRec xr[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (kq[i] >= 0) xr[i] = seg[kq[i]];
           int p0 = c0, p1 = c1;
           for (int off = 1; off < 32; off <<= 1) {
             const int y0 = __shfl_up_sync(0xffffffffu, p0, off), y1 = __shfl_up_sync(0xffffffffu, p1, off);
@@ -2739,37 +2787,30 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
           }
           const int tot0 = __shfl_sync(0xffffffffu, p0, 31);
           na = tot0 + __shfl_sync(0xffffffffu, p1, 31);
-          s_wpre[lane] = p0 - c0;
-          s_wpre[32 + lane] = tot0 + p1 - c1;
-          s_wbits[lane] = b0;
-          s_wbits[32 + lane] = b1;
-          __syncwarp();
-          auto kp_of = [&](int a) -> int {  // largest w with pre[w] <= a
-            int lo = 0;
-#pragma unroll
-            for (int step = 32; step; step >>= 1)
-              if (s_wpre[lo + step] <= a && lo + step < 64) lo += step;
-            return 32 * lo + (int)__fns(s_wbits[lo], 0, a - s_wpre[lo] + 1);
-          };
-          ActRec xr[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (lane + 32 * i < na) xr[i] = seg[kp_of(lane + 32 * i)];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int a = lane + 32 * i;
-            if (a < na) {
-              const ActRec y{cur, xr[i].pid, xr[i].j, xr[i].other, xr[i].kind};
-              if (a < DMAX) s_acts[a] = y;
-              M.s.acts[a] = y;
-            }
-          }
-          for (int a = lane + 128; a < na; a += 32) {
-            const ActRec x = seg[kp_of(a)];
+          const int pre0 = p0 - c0, pre1 = tot0 + p1 - c1;
+          auto put = [&](int at, const ActRec& x) {
             const ActRec y{cur, x.pid, x.j, x.other, x.kind};
-            if (a < DMAX) s_acts[a] = y;
-            M.s.acts[a] = y;
+            if (at < DMAX) s_acts[at] = y;
+            M.s.acts[at] = y;
+          };
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            if (kq[i] >= 0) put(pre0 + i, xr[i]);
+            if (kq[2 + i] >= 0) put(pre1 + i, xr[2 + i]);
           }
+          for (int at = pre0 + 2; r0; ++at) {
+            const int kp = 32 * lane + __ffs(r0) - 1;
+            r0 &= r0 - 1;
+            put(at, seg[kp]);
+          }
+          for (int at = pre1 + 2; r1; ++at) {
+            const int kp = 32 * (lane + 32) + __ffs(r1) - 1;
+            r1 &= r1 - 1;
+            put(at, seg[kp]);
+          }
+#ifdef LM_DIAG
+          if (lane == 0) g_diag[49] += gtime() - ta;
+#endif
         } else for (int wb = 0; wb < AW; wb += 32) {
           const int w = wb + lane;
           unsigned bw = w < AW ? bits[w] : 0u;
@@ -2835,8 +2876,14 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
         na_sh = na;
         tag_sh = tg;
       }
+#ifdef LM_DIAG
+      if (lane == 0) g_diag[50] += gtime() - ta;
+#endif
     }
     __syncthreads();
+#ifdef LM_DIAG
+    if (threadIdx.x == 0) g_diag[51] += gtime() - ta;
+#endif
     if (threadIdx.x == 0) tm[1] += gtime() - ta;
     const int t1 = t1_sh;
     if (t1 >= T) break;
@@ -2891,9 +2938,26 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
         }
         cl.sync();  // (A)
       }
+#ifdef LM_DIAG
+      const long long hd0 = gtime();
+#endif
       for (int k = wid; k < na; k += nranks * RW) add_direct(s_acts[k], k, t1, tag);
+#ifdef LM_DIAG
+      if (lane == 0) atomicMax(&g_diag[61], (unsigned long long)(gtime() - hd0));
+      if (threadIdx.x == 0) g_diag[52] += hd0 - ta;  // walk + command
+#endif
       if (nranks > 1) cl.sync();  // (B)
       __syncthreads();
+#ifdef LM_DIAG
+      if (threadIdx.x == 0) {
+        g_diag[53] += gtime() - hd0;  // direct apply wall
+        g_diag[54] += g_diag[60] > g_diag[61] ? g_diag[60] : g_diag[61];  // slowest add_direct
+        g_diag[55] += g_diag[61];
+        g_diag[60] = g_diag[61] = 0;
+        g_diag[56] += 1;
+        g_diag[57] += na;
+      }
+#endif
       if (threadIdx.x == 0) {
         cnt[1] += na;
         ++rounds;
@@ -2982,6 +3046,12 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     const long long t7 = gtime();
     const int ni = ni_sh;
     reeval += ni;
+#ifdef LM_DIAG
+    if (threadIdx.x == 0) {
+      g_diag[58] += ni;
+      g_diag[59] += 1;
+    }
+#endif
     for (int q = threadIdx.x; q < ni; q += REV_THREADS) {
       const int it = q < ILS ? s_il[q] : M.s.ilist[q];
       const int t = it / K, kp = it - t * K;
@@ -3014,7 +3084,18 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     if (threadIdx.x == 0) rcmd[0] = RC_EXIT;
     cl.sync();  // (A) helpers leave their loop
   }
-  pair_acc_flush<REV_THREADS>(M, &acc);
+  __shared__ long long s_acct[4];  // warp 1's accounting, for thread 0's statistics below
+  if (threadIdx.x == 32) {
+    s_acct[0] = alg;
+    s_acct[1] = npts;
+    s_acct[2] = nacts;
+    s_acct[3] = ledger_events;
+  }
+  pair_acc_flush<REV_THREADS>(M, &acc);  // (barriers)
+  alg = s_acct[0];
+  npts = s_acct[1];
+  nacts = s_acct[2];
+  ledger_events = s_acct[3];
   for (int t = threadIdx.x; t < T; t += REV_THREADS) M.s.pass_of[M.s.targets[t]] = -1;
   if (threadIdx.x == 0) {
     M.ledger[LG_NAIVE] += npts * mpb;  // record_small_transfer per pass (devicestore.py:94-101)
