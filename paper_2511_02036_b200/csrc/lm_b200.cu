@@ -74,6 +74,8 @@ struct lm_ctx {
   bool stage_used[kStageRing];
   int stage_pos = 0;
   lm_step_stats* h_stats = nullptr;  // pinned [kMaxBatch]
+  unsigned char* h_io = nullptr;     // pinned scratch of single-call list operations (grown on demand)
+  size_t h_io_bytes = 0;
   std::string err;
   long long launches = 0;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -83,6 +85,9 @@ struct lm_ctx {
   int apply_cluster = 16;               // CTAs per map of the forward-apply cluster (LM_APPLY_CLUSTER)
   int cull_cluster = 8;                 // CTAs per map of the recent-point cull cluster (LM_CULL_CLUSTER)
   int rev_cluster = 8;                  // CTAs per map of the reverse walk (LM_REV_CLUSTER; 1 = CTA 0 alone)
+  int tri_slices = 4;                   // k_tri CTAs per neighbour (LM_TRI_SLICES)
+  int refresh_blocks = 148;             // k_fuse_refresh grid (x) (LM_REFRESH_BLOCKS)
+  int post_blocks = 148;                // k_fuse_post grid (x), <= POST_BLOCKS (LM_POST_BLOCKS)
   // programmatic dependent launch of the step kernels (LM_PDL=0/1 overrides): on for
   // single-session launches; off for batches, whose concurrent stream groups lose SMs to
   // successor CTAs parked in griddepcontrol.wait (C5: 16.2k -> 11.6k KF/s with it)
@@ -740,6 +745,7 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
   CU(cudaFuncSetAttribute(k_fuse_apply, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CU(cudaFuncSetAttribute(k_fuse_rev, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CU(cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, CULL_DYN_SMEM));
+  CU(cudaFuncSetAttribute(k_tri, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
   if (const char* e = getenv("LM_CARVEOUT")) {  // (experiments) shared-memory carve-out hint, percent
     const int pc = atoi(e);
     const void* ks[] = {(const void*)k_insert, (const void*)k_cull, (const void*)k_select, (const void*)k_prep,
@@ -752,6 +758,10 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
   }
   if (const char* e = getenv("LM_PDL")) ctx->pdl = atoi(e) != 0 ? 1 : 0;
   if (const char* e = getenv("LM_REV_CLUSTER")) ctx->rev_cluster = atoi(e) > 0 ? atoi(e) : 1;
+  if (const char* e = getenv("LM_REFRESH_BLOCKS")) ctx->refresh_blocks = atoi(e) > 0 ? atoi(e) : 148;
+  if (const char* e = getenv("LM_POST_BLOCKS"))
+    ctx->post_blocks = atoi(e) > 0 ? (atoi(e) < POST_BLOCKS ? atoi(e) : POST_BLOCKS) : 148;
+  if (const char* e = getenv("LM_TRI_SLICES")) ctx->tri_slices = atoi(e) > 0 ? (atoi(e) < 32 ? atoi(e) : 32) : 1;
   if (const char* e = getenv("LM_CULL_CLUSTER")) {
     const int v = atoi(e);
     ctx->cull_cluster = v < 1 ? 1 : (v > 8 ? 8 : v);
@@ -786,6 +796,7 @@ int lm_ctx_destroy(lm_ctx* ctx) {
   if (ctx->h_args) cudaFreeHost(ctx->h_args);
   if (ctx->d_args) cudaFree(ctx->d_args);
   if (ctx->h_stats) cudaFreeHost(ctx->h_stats);
+  if (ctx->h_io) cudaFreeHost(ctx->h_io);
   for (int i = 0; i < kStageRing; ++i) {
     if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
     if (ctx->d_stage[i]) cudaFree(ctx->d_stage[i]);
@@ -1143,8 +1154,12 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
   StepArgs* h = ctx->h_args + (size_t)e * kMaxBatch;
   StepArgs* dv = ctx->d_args + (size_t)e * kMaxBatch;
   int tiles = 1, slots = 1, kfcap = 2, nbr_dim = 1, kpkf = 1, tfuse = 1;
+  bool any_cull = false, any_create = false, any_fuse = false;
   for (int k = 0; k < n; ++k) {
     HostMap* m = ctx->maps[maps[k]];
+    any_cull |= args[k].do_cull != 0;
+    any_create |= args[k].do_create != 0;
+    any_fuse |= args[k].do_fuse != 0;
     h[k] = args[k];
     h[k].map = maps[k];
     const int want = args[k].explicit_nbr ? 1 : (args[k].n_nbr_req < NMAX ? args[k].n_nbr_req : NMAX);
@@ -1183,29 +1198,53 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
     return LM_OK;
   };
   int rc = LM_OK;
-  ctx->pdl_now = ctx->pdl < 0 ? n == 1 : ctx->pdl == 1;
+  const bool pdl = ctx->pdl < 0 ? n == 1 : ctx->pdl == 1;
+  ctx->pdl_now = pdl;
+  // a stage no entry of the batch runs is not launched (its kernels would only return): the
+  // single-stage calls of the reference-shaped API (cull, create_map_points, run_fusion) pay
+  // for their own stage only. The profiled pass launches everything (fixed event layout).
+  if (ctx->prof) any_cull = any_create = any_fuse = true;
+  int launched = 2;  // k_insert (zeroes the step's statistics) and k_fuse_visible_end (folds them)
   if ((rc = mark())) return rc;
   CU(launch_k(ctx, k_insert, dim3(n), dim3(256), 0, 0, dmaps, dv));
   if ((rc = mark())) return rc;
-  {
+  if (any_cull) {
     // recent-point cull: one cluster per map, as wide as the batch leaves SMs for
     int cl = ctx->cull_cluster / n;
     cl = cl < 1 ? 1 : cl;
     CU(launch_k(ctx, k_cull, dim3(n * cl), dim3(1024), CULL_DYN_SMEM, cl, dmaps, (const StepArgs*)dv));
+    launched += 1;
   }
   if ((rc = mark())) return rc;
+  if (any_create) {
+  // k_select and k_fuse_targets run their first part before waiting for their predecessor,
+  // which is safe only behind the kernel they were written against (k_cull, k_commit_write):
+  // behind any other predecessor they are launched without the PDL attribute (full order)
+  ctx->pdl_now = pdl && any_cull;
   CU(launch_k(ctx, k_select, dim3(n), dim3(256), dyn, 0, dmaps, dv, slots));
+  ctx->pdl_now = pdl;
   if ((rc = mark())) return rc;
   CU(launch_k(ctx, k_prep, dim3(1 + nbr_dim, n), dim3(256), 0, 0, dmaps, dv));
   if ((rc = mark())) return rc;
   CU(launch_k(ctx, k_match, dim3(nbr_dim, tiles, n), dim3(MATCH_WARPS * 32), 0, 0, dmaps, dv));
   if ((rc = mark())) return rc;
-  CU(launch_k(ctx, k_tri, dim3(nbr_dim, n), dim3(256), 0, 0, dmaps, dv));
+  {
+    // triangulation slices per neighbour (LM_TRI_SLICES), each with the compacted survivors
+    // in shared memory; one slice reading them from global memory past 96 KB
+    const size_t tsm = 8 * (size_t)kpkf;
+    const int sl = tsm <= 96 * 1024 ? ctx->tri_slices : 1;
+    CU(launch_k(ctx, k_tri, dim3(nbr_dim, sl, n), dim3(256), sl > 1 ? tsm : 0, 0, dmaps, dv));
+  }
   if ((rc = mark())) return rc;
   CU(launch_k(ctx, k_commit, dim3(n), dim3(1024), 0, 0, dmaps, dv));
   CU(launch_k(ctx, k_commit_write, dim3((kpkf + 127) / 128, NMAX, n), dim3(128), 0, 0, dmaps, dv));
+  launched += 6;
+  }  // any_create
   if ((rc = mark())) return rc;
+  if (any_fuse) {
+  ctx->pdl_now = pdl && any_create;
   CU(launch_k(ctx, k_fuse_targets, dim3(n), dim3(1024), dyn + kfcap + 16, 0, dmaps, dv, slots));
+  ctx->pdl_now = pdl;
   if ((rc = mark())) return rc;
   CU(launch_k(ctx, k_fuse_geo, dim3((kpkf + 7) / 8, n), dim3(256), 0, 0, dmaps, dv));
   if ((rc = mark())) return rc;
@@ -1218,7 +1257,7 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
     CU(launch_k(ctx, k_fuse_apply, dim3(n * cl), dim3(APPLY_THREADS), 0, cl, dmaps, (const StepArgs*)dv));
   }
   if ((rc = mark())) return rc;
-  CU(launch_k(ctx, k_fuse_refresh, dim3(148, n), dim3(256), 0, 0, dmaps, dv));
+  CU(launch_k(ctx, k_fuse_refresh, dim3(ctx->refresh_blocks, n), dim3(256), 0, 0, dmaps, dv));
   if ((rc = mark())) return rc;
   if (n == 1) {
     CU(launch_k(ctx, k_fuse_spec<true>, dim3((kpkf + 255) / 256, tfuse, n), dim3(256), 0, 0, dmaps, dv));
@@ -1226,21 +1265,24 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
     CU(launch_k(ctx, k_fuse_spec_pts, dim3((kpkf + 255) / 256, tfuse, n), dim3(256), 0, 0, dmaps, dv));
     CU(launch_k(ctx, k_fuse_spec_hit, dim3(16, n), dim3(256), 0, 0, dmaps, dv));
     CU(launch_k(ctx, k_fuse_spec<false>, dim3((kpkf + 255) / 256, tfuse, n), dim3(256), 0, 0, dmaps, dv));
-    ctx->launches += 2;
+    launched += 2;
   }
   if ((rc = mark())) return rc;
-  CU(launch_k(ctx, k_fuse_post, dim3(POST_BLOCKS, n), dim3(256), 0, 0, dmaps, dv));
+  CU(launch_k(ctx, k_fuse_post, dim3(ctx->post_blocks, n), dim3(256), 0, 0, dmaps, dv));
   {
     // reverse walk: one cluster per map, CTA 0 walks, the others help with direct passes
     int cl = ctx->rev_cluster / n;
     cl = cl < 1 ? 1 : cl;
     CU(launch_k(ctx, k_fuse_rev, dim3(n * cl), dim3(REV_THREADS), rev_smem, cl, dmaps, dv, (int)rev_smem));
   }
+  launched += 8;
+  }  // any_fuse
   if ((rc = mark())) return rc;
-  CU(launch_k(ctx, k_fuse_visible_end, dim3((kpkf + 255) / 256, tfuse, n), dim3(256), 0, 0, dmaps, dv,
-              ctx->d_totals));
+  // (without fusion one block per map: no pass items, the block folds the statistics)
+  CU(launch_k(ctx, k_fuse_visible_end, any_fuse ? dim3((kpkf + 255) / 256, tfuse, n) : dim3(1, 1, n), dim3(256), 0, 0,
+              dmaps, dv, ctx->d_totals));
   if ((rc = mark())) return rc;
-  ctx->launches += 17;
+  ctx->launches += launched;
   if (ctx->prof) ctx->prof_steps.push_back(evs);
   CHECK_LAUNCH();
   CU(cudaEventRecord(ctx->args_ev[e], ctx->stream));
@@ -1475,35 +1517,96 @@ int lm_cull_recent(lm_ctx* ctx, int32_t map, int32_t processed_index, const lm_c
   return rc;
 }
 
+// pinned host scratch of at least `bytes` (callers synchronise before returning, so the
+// buffer is free at entry)
+static int host_io(lm_ctx* ctx, size_t bytes, unsigned char** out) {
+  if (bytes > ctx->h_io_bytes) {
+    if (ctx->h_io) cudaFreeHost(ctx->h_io);
+    ctx->h_io = nullptr;
+    ctx->h_io_bytes = 0;
+    size_t sz = 1 << 16;
+    while (sz < bytes) sz *= 2;
+    CU(cudaMallocHost(&ctx->h_io, sz));
+    ctx->h_io_bytes = sz;
+  }
+  *out = ctx->h_io;
+  return LM_OK;
+}
+
 int lm_cull_recent_list(lm_ctx* ctx, int32_t map, int32_t processed_index, const lm_cull_cfg* cc, int32_t n,
                         const int64_t* ids, const int32_t* born, int64_t* removed, int32_t* n_removed,
                         int64_t* keep_ids, int32_t* keep_born, int32_t* n_keep) {
   HostMap* m;
   int rc = check_map(ctx, map, &m);
   if (rc) return rc;
+  if (!cc) return LM_ERR_INVALID_ARGUMENT;
   *n_removed = 0;
   *n_keep = 0;
   if (n <= 0) return lm_recent_import(ctx, map, ids, born, 0);
-  int next = 0;
+  if (n > m->d.recent_cap) return fail(ctx, LM_ERR_CAPACITY, "recent list too long");
+  int anchor = -1;  // any live keyframe anchors the cull-only step (the stage does not read it)
+  for (int s = 0; s < m->n_slots && anchor < 0; ++s)
+    if (m->state[s] == KF_LIVE) anchor = s;
+  // two round trips: the point count (validation), then the whole cull -- the list in, both
+  // alive ranges, the kept list and the step's statistics out -- through pinned scratch
+  const size_t N = (size_t)n;
+  unsigned char* hb;
+  if ((rc = host_io(ctx, 64 + 16 * N, &hb))) return rc;  // (grown again below for the ranges)
+  CU(cudaMemcpyAsync(hb, m->d.scal + SC_NEXT_ID, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
-  CU(cudaMemcpy(&next, m->d.scal + SC_NEXT_ID, sizeof(int), cudaMemcpyDeviceToHost));
+  const int next = *(int*)hb;
   long long lo = next, hi = -1;
   for (int k = 0; k < n; ++k) {
     if (ids[k] < 0 || ids[k] >= next) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "unknown map point %lld", (long long)ids[k]);
     lo = ids[k] < lo ? ids[k] : lo;
     hi = ids[k] > hi ? ids[k] : hi;
   }
-  std::vector<unsigned char> before(hi - lo + 1), after(hi - lo + 1);
-  CU(cudaMemcpy(before.data(), m->d.alive + lo, before.size(), cudaMemcpyDeviceToHost));
-  if ((rc = lm_recent_import(ctx, map, ids, born, n))) return rc;
-  int culled = 0;
-  if ((rc = lm_cull_recent(ctx, map, processed_index, cc, &culled))) return rc;
-  CU(cudaMemcpy(after.data(), m->d.alive + lo, after.size(), cudaMemcpyDeviceToHost));
+  const size_t R = (size_t)(hi - lo + 1);
+  const size_t o_id = 0, o_born = o_id + 4 * N, o_n = o_born + 4 * N, o_stats = (o_n + 4 + 7) & ~(size_t)7;
+  const size_t o_kid = o_stats + sizeof(lm_step_stats), o_kborn = o_kid + 4 * N, o_kn = o_kborn + 4 * N;
+  const size_t o_before = o_kn + 4, o_after = o_before + R;
+  if ((rc = host_io(ctx, o_after + R, &hb))) return rc;
+  int* hid = (int*)(hb + o_id);
+  for (int k = 0; k < n; ++k) hid[k] = (int)ids[k];
+  memcpy(hb + o_born, born, 4 * N);
+  *(int*)(hb + o_n) = n;
+  CU(cudaMemcpyAsync(hb + o_before, m->d.alive + lo, R, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(m->d.recent_id, hb + o_id, 4 * N, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(m->d.recent_born, hb + o_born, 4 * N, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(m->d.scal + SC_RECENT_N, hb + o_n, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  if (anchor >= 0) {
+    lm_step_params p;
+    memset(&p, 0, sizeof p);
+    p.do_cull = 1;
+    p.processed_index = processed_index;
+    p.cull = *cc;
+    StepArgs a;
+    if ((rc = fill_args(ctx, m, m->ids[anchor], &p, a, true))) return rc;
+    if ((rc = run_batch(ctx, 1, &map, &a, nullptr))) return rc;  // (no readback: the copies below)
+    CU(cudaMemcpyAsync(hb + o_stats, m->d_stats, sizeof(lm_step_stats), cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CU(cudaMemcpyAsync(hb + o_after, m->d.alive + lo, R, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(hb + o_kn, m->d.scal + SC_RECENT_N, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(hb + o_kid, m->d.recent_id, 4 * N, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(hb + o_kborn, m->d.recent_born, 4 * N, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (anchor >= 0) {
+    const int err = ((const lm_step_stats*)(hb + o_stats))->error;
+    if (err) return step_error(ctx, err, map);
+  }
+  const unsigned char* before = hb + o_before;
+  const unsigned char* after = hb + o_after;
   int r = 0;
   for (int k = 0; k < n; ++k)  // removed = alive before, dead after, in probation order
     if (before[ids[k] - lo] && !after[ids[k] - lo]) removed[r++] = ids[k];
   *n_removed = r;
-  return lm_recent_export(ctx, map, keep_ids, keep_born, n, n_keep);
+  const int kn = *(const int*)(hb + o_kn);
+  if (kn < 0 || kn > n) return fail(ctx, LM_ERR_INVALID_STATE, "probation list grew in a cull (%d > %d)", kn, n);
+  const int* kid = (const int*)(hb + o_kid);
+  for (int k = 0; k < kn; ++k) keep_ids[k] = kid[k];
+  memcpy(keep_born, hb + o_kborn, 4 * (size_t)kn);
+  *n_keep = kn;
+  return LM_OK;
 }
 
 int lm_search(lm_ctx* ctx, int32_t map, int64_t cur_kf, int64_t nbr_kf, const lm_match_cfg* mc,

@@ -60,6 +60,12 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+__device__ __forceinline__ unsigned dyn_smem_bytes() {
+  unsigned v;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(v));
+  return v;
+}
+
 __device__ __forceinline__ long long gtime() {  // ns, device-wide clock
 #ifdef LM_NO_PHASE_TIMERS
   return 0;
@@ -774,14 +780,24 @@ __global__ void __launch_bounds__(MATCH_WARPS * 32, 5) k_match(DevMap* maps, con
 
 // ---------------------------------------------------------------------------------- tri
 
+// grid (neighbour, slice, map): every slice CTA of a neighbour compacts the one-to-one
+// survivors (cheap: two rounds of L2 loads per thread) into its shared memory and takes every
+// gridDim.y-th of them, so the fp64 triangulations (one Jacobi SVD per thread, the kernel's
+// critical path) spread over gridDim.y SMs; slice 0 also writes the compacted list for
+// k_commit. Without shared memory (dynamic size 0: very large keyframes) one slice reads the
+// list back from global memory.
 __global__ void __launch_bounds__(256) k_tri(DevMap* maps, const StepArgs* args) {
   pdl_enter();
-  const StepArgs& A = args[blockIdx.y];
+  const StepArgs& A = args[blockIdx.z];
   const DevMap& M = maps[A.map];
   if (!A.do_create) return;
   const int r = blockIdx.x;
+  const int slice = blockIdx.y, nslice = gridDim.y;
   if (r >= M.s.stats->n_neighbors) return;
   if (M.s.deg[r]) return;  // cand_n[r] = 0 set by k_prep
+  if (slice > 0 && A.search_only) return;
+  extern __shared__ int tri_sm[];  // [kpkf_max] current index, [kpkf_max] neighbour index
+  const bool use_sm = dyn_smem_bytes() >= 8u * (unsigned)M.kpkf_max;
   __shared__ int sh[32];
   const int cur = A.cur;
   const int ncur = M.kp_n[cur];
@@ -806,22 +822,31 @@ __global__ void __launch_bounds__(256) k_tri(DevMap* maps, const StepArgs* args)
 #pragma unroll
     for (int q = 0; q < TQ; ++q)
       if (fl >> q & 1u) {
-        M.s.cand_i[base + count + at] = i0 + q;
-        M.s.cand_j[base + count + at] = (int)(pk[q] & 0xffffffffu);
-        M.s.cand_d[base + count + at] = (int)(pk[q] >> 32);
+        const int k = count + at;
+        if (use_sm) {
+          tri_sm[k] = i0 + q;
+          tri_sm[M.kpkf_max + k] = (int)(pk[q] & 0xffffffffu);
+        }
+        if (slice == 0) {
+          M.s.cand_i[base + k] = i0 + q;
+          M.s.cand_j[base + k] = (int)(pk[q] & 0xffffffffu);
+          M.s.cand_d[base + k] = (int)(pk[q] >> 32);
+        }
         ++at;
       }
     count += tot;
   }
-  // the triangulation loop below reads candidate records other threads just wrote (global
-  // memory: they are visible block-wide only after a barrier)
+  // the triangulation loop below reads candidate records other threads just wrote (shared or
+  // global memory: they are visible block-wide only after a barrier)
   __syncthreads();
-  if (threadIdx.x == 0) M.s.cand_n[r] = count;
+  if (threadIdx.x == 0 && slice == 0) M.s.cand_n[r] = count;
   if (A.search_only) return;
+  if (!use_sm && slice > 0) return;  // (launched with one slice then)
   const int nb = M.s.nbr[r];
   const int offa = M.kp_off[cur], offb = M.kp_off[nb];
-  for (int k = threadIdx.x; k < count; k += 256) {
-    const int i = M.s.cand_i[base + k], j = M.s.cand_j[base + k];
+  for (int k = slice + nslice * threadIdx.x; k < count; k += 256 * nslice) {
+    const int i = use_sm ? tri_sm[k] : M.s.cand_i[base + k];
+    const int j = use_sm ? tri_sm[M.kpkf_max + k] : M.s.cand_j[base + k];
     const int ga = offa + i, gb = offb + j;
     double X[3] = {0, 0, 0};
     int st, border = 0;
@@ -2290,7 +2315,7 @@ __global__ void __launch_bounds__(256) k_fuse_spec(DevMap* maps, const StepArgs*
 // refreshing when the apply did exactly that (one mutation, one observation more, slot j
 // bound to the point: the same observation set).
 constexpr int POST_MAXN = 128;
-constexpr int POST_BLOCKS = 148;  // k_fuse_post grid (x): one warp per speculated point at C2 sizes
+constexpr int POST_BLOCKS = 296;  // k_fuse_post grid (x) upper bound (scratch per warp; LM_POST_BLOCKS)
 __global__ void __launch_bounds__(256) k_fuse_post(DevMap* maps, const StepArgs* args) {
   pdl_enter();
   const StepArgs& A = args[blockIdx.y];

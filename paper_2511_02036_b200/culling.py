@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass
+from operator import attrgetter
 
 import numpy as np
 
@@ -32,14 +33,17 @@ class RecentPoint:
     created_at: int  # processed-keyframe counter at creation time
 
 
+_MP_ID, _BORN = attrgetter("mp_id"), attrgetter("created_at")
+
+
 def cull_recent_map_points(model, recent: list, current_index: int, cfg: CullConfig | None = None):
     cfg = cfg or CullConfig()
     if not recent:
         return [], []
     kind = type(recent[0])  # keep the caller's RecentPoint class (the reference's or this one)
     n = len(recent)
-    ids = np.fromiter((r.mp_id for r in recent), np.int64, n)
-    born = np.fromiter((r.created_at for r in recent), np.int32, n)
+    ids = np.fromiter(map(_MP_ID, recent), np.int64, n)
+    born = np.fromiter(map(_BORN, recent), np.int32, n)
     rem = np.zeros(n, np.int64)
     kid = np.zeros(n, np.int64)
     kborn = np.zeros(n, np.int32)
@@ -48,7 +52,14 @@ def cull_recent_map_points(model, recent: list, current_index: int, cfg: CullCon
     model._call("lm_cull_recent_list", model.map, int(current_index), C.byref(cc), n, ptr(ids, C.c_int64),
                 ptr(born, C.c_int32), ptr(rem, C.c_int64), C.byref(nr), ptr(kid, C.c_int64), ptr(kborn, C.c_int32),
                 C.byref(nk))
-    return rem[:nr.value].tolist(), [kind(k, b) for k, b in zip(kid[:nk.value].tolist(), kborn[:nk.value].tolist())]
+    kid, kborn = kid[:nk.value], kborn[:nk.value]
+    # the kept entries are a subsequence of the list (the device keeps list order): hand back
+    # the caller's own entries, as the reference does (culling.py:58 keep.append(entry)); a
+    # list whose kept ids cannot be located unambiguously (repeated ids) gets new entries
+    at = np.flatnonzero(np.isin(ids, kid))
+    if len(at) == len(kid) and np.array_equal(ids[at], kid) and np.array_equal(born[at], kborn):
+        return rem[:nr.value].tolist(), [recent[i] for i in at.tolist()]
+    return rem[:nr.value].tolist(), [kind(k, b) for k, b in zip(kid.tolist(), kborn.tolist())]
 
 
 _IMPLS = ("baseline", "fast")
