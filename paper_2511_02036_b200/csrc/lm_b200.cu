@@ -67,12 +67,15 @@ struct lm_ctx {
   cudaEvent_t args_ev[kRing];
   bool args_used[kRing];
   int ring_pos = 0;
+  cudaStream_t stage_stream = nullptr;  // keyframe staging (H2D + k_stage), overlapping the steps
+  int last_stage_b = -1;                // ring entry of the latest staging
+  bool stage_unjoined = false;          // a staging the step stream has not waited for yet
   unsigned char* h_stage[kStageRing];
   unsigned char* d_stage[kStageRing];
   size_t stage_bytes = 0;
   cudaEvent_t stage_ev[kStageRing];
   bool stage_used[kStageRing];
-  int stage_pos = 0;
+  long long stage_pos = 0;
   lm_step_stats* h_stats = nullptr;  // pinned [kMaxBatch]
   unsigned char* h_io = nullptr;     // pinned scratch of single-call list operations (grown on demand)
   size_t h_io_bytes = 0;
@@ -125,12 +128,25 @@ static int arena(lm_ctx* ctx, HostMap* m, T** p, size_t count) {
   return LM_OK;
 }
 
-static int check_map(lm_ctx* ctx, int32_t map, HostMap** out) {
+// Keyframes are staged on their own stream (lm_kf_stage), so the upload and scatter of the
+// next keyframe overlap the step already queued. Every other entry point (steps included)
+// first orders the step stream after all staging issued so far (join = true): nothing on the
+// step stream ever sees a keyframe half staged.
+static int join_staging(lm_ctx* ctx) {
+  if (ctx->stage_unjoined) {
+    const cudaError_t e = cudaStreamWaitEvent(ctx->stream, ctx->stage_ev[ctx->last_stage_b], 0);
+    if (e != cudaSuccess) return fail(ctx, LM_ERR_CUDA, "join staging: %s", cudaGetErrorString(e));
+    ctx->stage_unjoined = false;
+  }
+  return LM_OK;
+}
+
+static int check_map(lm_ctx* ctx, int32_t map, HostMap** out, bool join = true) {
   if (!ctx) return LM_ERR_INVALID_ARGUMENT;
   if (map < 0 || map >= (int)ctx->maps.size() || !ctx->maps[map])
     return fail(ctx, LM_ERR_INVALID_ARGUMENT, "unknown map %d", map);
   *out = ctx->maps[map];
-  return LM_OK;
+  return join ? join_staging(ctx) : LM_OK;
 }
 
 static int slot_of(lm_ctx* ctx, HostMap* m, long long kf_id, int* slot, bool need_live) {
@@ -725,6 +741,7 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
   }
   CU(cudaSetDevice(device));
   CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&ctx->stage_stream, cudaStreamNonBlocking));
   CU(cudaMallocHost(&ctx->h_args, sizeof(StepArgs) * kRing * kMaxBatch));
   CU(cudaMalloc(&ctx->d_args, sizeof(StepArgs) * kRing * kMaxBatch));
   CU(cudaMallocHost(&ctx->h_stats, sizeof(lm_step_stats) * kMaxBatch));
@@ -776,6 +793,7 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
 
 int lm_ctx_destroy(lm_ctx* ctx) {
   if (!ctx) return LM_OK;
+  if (ctx->stage_stream) cudaStreamSynchronize(ctx->stage_stream);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (HostMap* m : ctx->maps) {
     if (!m) continue;
@@ -801,6 +819,7 @@ int lm_ctx_destroy(lm_ctx* ctx) {
     if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
     if (ctx->d_stage[i]) cudaFree(ctx->d_stage[i]);
   }
+  if (ctx->stage_stream) cudaStreamDestroy(ctx->stage_stream);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return LM_OK;
@@ -997,7 +1016,7 @@ int lm_kf_stage(lm_ctx* ctx, int32_t map, int64_t kf_id, const double quat[4], c
                 const double cam[6], int32_t n, const double* u, const double* v, const int64_t* level,
                 const uint8_t* desc, const int64_t* bindings) {
   HostMap* m;
-  int rc = check_map(ctx, map, &m);
+  int rc = check_map(ctx, map, &m, false);  // (staging is ordered on its own stream)
   if (rc) return rc;
   DevMap& d = m->d;
   if (m->slot_of.count(kf_id)) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "duplicate keyframe id %lld", (long long)kf_id);
@@ -1011,11 +1030,13 @@ int lm_kf_stage(lm_ctx* ctx, int32_t map, int64_t kf_id, const double quat[4], c
     if (level[i] < 0 || level[i] >= d.L) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "keypoint level outside pyramid");
   // staging buffer (ring)
   const size_t need = sizeof(StageHdr) + (size_t)n * (8 + 8 + 32 + 4 + 1) + 64;
-  const int b = ctx->stage_pos++ % kStageRing;
+  const long long sidx = ctx->stage_pos++;
+  const int b = (int)(sidx % kStageRing);
   if (ctx->stage_used[b]) CU(cudaEventSynchronize(ctx->stage_ev[b]));
   if (ctx->stage_bytes < need) {
     const size_t sz = need < ((size_t)d.kpkf_max * 53 + sizeof(StageHdr) + 64) ? ((size_t)d.kpkf_max * 53 + sizeof(StageHdr) + 64) : need;
     CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stage_stream));
     for (int i = 0; i < kStageRing; ++i) {
       if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
       if (ctx->d_stage[i]) cudaFree(ctx->d_stage[i]);
@@ -1057,12 +1078,14 @@ int lm_kf_stage(lm_ctx* ctx, int32_t map, int64_t kf_id, const double quat[4], c
     pb[i] = bindings ? (int)bindings[i] : -1;
     pl[i] = (unsigned char)level[i];
   }
-  CU(cudaMemcpyAsync(ctx->d_stage[b], hb, need, cudaMemcpyHostToDevice, ctx->stream));
-  k_stage<<<1, 1024, 0, ctx->stream>>>(d, ctx->d_stage[b]);
+  CU(cudaMemcpyAsync(ctx->d_stage[b], hb, need, cudaMemcpyHostToDevice, ctx->stage_stream));
+  k_stage<<<1, 1024, 0, ctx->stage_stream>>>(d, ctx->d_stage[b]);
   CHECK_LAUNCH();
   ctx->launches += 1;
-  CU(cudaEventRecord(ctx->stage_ev[b], ctx->stream));
+  CU(cudaEventRecord(ctx->stage_ev[b], ctx->stage_stream));
   ctx->stage_used[b] = true;
+  ctx->last_stage_b = b;
+  ctx->stage_unjoined = true;
   m->slot_of[kf_id] = slot;
   m->state[slot] = KF_STAGED;
   m->prebound[slot] = bindings != nullptr;
@@ -1425,7 +1448,7 @@ uint64_t lm_kf_record_bytes(int32_t n, uint32_t flags) {
 int lm_kf_stage_record(lm_ctx* ctx, int32_t map, const void* record, uint64_t bytes, int64_t* kf_id_out) {
   if (!ctx || !record) return LM_ERR_INVALID_ARGUMENT;
   HostMap* m;
-  int rc = check_map(ctx, map, &m);
+  int rc = check_map(ctx, map, &m, false);
   if (rc) return rc;
   if (bytes < sizeof(lm_kf_record_hdr)) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "record shorter than its header");
   lm_kf_record_hdr h;

@@ -2315,7 +2315,7 @@ __global__ void __launch_bounds__(256) k_fuse_spec(DevMap* maps, const StepArgs*
 // refreshing when the apply did exactly that (one mutation, one observation more, slot j
 // bound to the point: the same observation set).
 constexpr int POST_MAXN = 128;
-constexpr int POST_BLOCKS = 296;  // k_fuse_post grid (x) upper bound (scratch per warp; LM_POST_BLOCKS)
+constexpr int POST_BLOCKS = 148;  // k_fuse_post grid (x) upper bound: scratch per warp (LM_POST_BLOCKS; 296 measured no faster)
 __global__ void __launch_bounds__(256) k_fuse_post(DevMap* maps, const StepArgs* args) {
   pdl_enter();
   const StepArgs& A = args[blockIdx.y];
