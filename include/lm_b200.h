@@ -240,7 +240,8 @@ int lm_run_fusion(lm_ctx* ctx, int32_t map, int64_t kf_id, const lm_fuse_cfg* fc
 int lm_cull_recent(lm_ctx* ctx, int32_t map, int32_t processed_index, const lm_cull_cfg* cc, int32_t* culled);
 /* cull_recent_map_points(model, recent, current_index, cfg) culling.py:28-59 in one call: the
  * probation list (ids, born) in, (removed ids, kept entries) out, each in list order; removed
- * and keep buffers hold n entries */
+ * and keep buffers hold n entries. An id naming no map point is skipped (neither removed nor
+ * kept), as the reference skips `mp is None`; a point listed twice is LM_ERR_INVALID_ARGUMENT */
 int lm_cull_recent_list(lm_ctx* ctx, int32_t map, int32_t processed_index, const lm_cull_cfg* cc, int32_t n,
                         const int64_t* ids, const int32_t* born, int64_t* removed, int32_t* n_removed,
                         int64_t* keep_ids, int32_t* keep_born, int32_t* n_keep);

@@ -1570,32 +1570,51 @@ int lm_cull_recent_list(lm_ctx* ctx, int32_t map, int32_t processed_index, const
   int anchor = -1;  // any live keyframe anchors the cull-only step (the stage does not read it)
   for (int s = 0; s < m->n_slots && anchor < 0; ++s)
     if (m->state[s] == KF_LIVE) anchor = s;
-  // two round trips: the point count (validation), then the whole cull -- the list in, both
-  // alive ranges, the kept list and the step's statistics out -- through pinned scratch
+  // one round trip: the list in, both alive ranges, the kept list and the step's statistics
+  // out, through pinned scratch. An id that names no map point is skipped, as the reference
+  // skips an entry whose point it cannot find (culling.py:44-46 `mp is None`): ids outside
+  // the point arena are not uploaded; ids not created yet are dead (alive = 0) on the device.
   const size_t N = (size_t)n;
-  unsigned char* hb;
-  if ((rc = host_io(ctx, 64 + 16 * N, &hb))) return rc;  // (grown again below for the ranges)
-  CU(cudaMemcpyAsync(hb, m->d.scal + SC_NEXT_ID, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  CU(cudaStreamSynchronize(ctx->stream));
-  const int next = *(int*)hb;
-  long long lo = next, hi = -1;
+  std::vector<int> kept_in;
+  kept_in.reserve(N);
+  long long lo = m->d.mp_cap, hi = -1, prev = -1;
+  bool increasing = true;
   for (int k = 0; k < n; ++k) {
-    if (ids[k] < 0 || ids[k] >= next) return fail(ctx, LM_ERR_INVALID_ARGUMENT, "unknown map point %lld", (long long)ids[k]);
+    if (ids[k] < 0 || ids[k] >= m->d.mp_cap) continue;
+    kept_in.push_back(k);
     lo = ids[k] < lo ? ids[k] : lo;
     hi = ids[k] > hi ? ids[k] : hi;
+    increasing &= ids[k] > prev;
+    prev = ids[k];
   }
+  const int nv = (int)kept_in.size();
+  if (!increasing) {  // (the pipeline appends ids in creation order; anything else is checked)
+    // a point listed twice would be classified twice in one pass (a double kill), where the
+    // reference's second visit finds it already dead: rejected instead
+    std::vector<long long> sorted;
+    sorted.reserve(nv);
+    for (int q = 0; q < nv; ++q) sorted.push_back(ids[kept_in[q]]);
+    std::sort(sorted.begin(), sorted.end());
+    if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
+      return fail(ctx, LM_ERR_INVALID_ARGUMENT, "map point listed twice in the probation list");
+  }
+  if (nv == 0) return lm_recent_import(ctx, map, ids, born, 0);
+  unsigned char* hb;
   const size_t R = (size_t)(hi - lo + 1);
   const size_t o_id = 0, o_born = o_id + 4 * N, o_n = o_born + 4 * N, o_stats = (o_n + 4 + 7) & ~(size_t)7;
   const size_t o_kid = o_stats + sizeof(lm_step_stats), o_kborn = o_kid + 4 * N, o_kn = o_kborn + 4 * N;
   const size_t o_before = o_kn + 4, o_after = o_before + R;
   if ((rc = host_io(ctx, o_after + R, &hb))) return rc;
   int* hid = (int*)(hb + o_id);
-  for (int k = 0; k < n; ++k) hid[k] = (int)ids[k];
-  memcpy(hb + o_born, born, 4 * N);
-  *(int*)(hb + o_n) = n;
+  int* hborn = (int*)(hb + o_born);
+  for (int q = 0; q < nv; ++q) {
+    hid[q] = (int)ids[kept_in[q]];
+    hborn[q] = born[kept_in[q]];
+  }
+  *(int*)(hb + o_n) = nv;
   CU(cudaMemcpyAsync(hb + o_before, m->d.alive + lo, R, cudaMemcpyDeviceToHost, ctx->stream));
-  CU(cudaMemcpyAsync(m->d.recent_id, hb + o_id, 4 * N, cudaMemcpyHostToDevice, ctx->stream));
-  CU(cudaMemcpyAsync(m->d.recent_born, hb + o_born, 4 * N, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(m->d.recent_id, hb + o_id, 4 * (size_t)nv, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(m->d.recent_born, hb + o_born, 4 * (size_t)nv, cudaMemcpyHostToDevice, ctx->stream));
   CU(cudaMemcpyAsync(m->d.scal + SC_RECENT_N, hb + o_n, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
   if (anchor >= 0) {
     lm_step_params p;
@@ -1610,8 +1629,8 @@ int lm_cull_recent_list(lm_ctx* ctx, int32_t map, int32_t processed_index, const
   }
   CU(cudaMemcpyAsync(hb + o_after, m->d.alive + lo, R, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaMemcpyAsync(hb + o_kn, m->d.scal + SC_RECENT_N, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  CU(cudaMemcpyAsync(hb + o_kid, m->d.recent_id, 4 * N, cudaMemcpyDeviceToHost, ctx->stream));
-  CU(cudaMemcpyAsync(hb + o_kborn, m->d.recent_born, 4 * N, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(hb + o_kid, m->d.recent_id, 4 * (size_t)nv, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(hb + o_kborn, m->d.recent_born, 4 * (size_t)nv, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   if (anchor >= 0) {
     const int err = ((const lm_step_stats*)(hb + o_stats))->error;
@@ -1620,11 +1639,13 @@ int lm_cull_recent_list(lm_ctx* ctx, int32_t map, int32_t processed_index, const
   const unsigned char* before = hb + o_before;
   const unsigned char* after = hb + o_after;
   int r = 0;
-  for (int k = 0; k < n; ++k)  // removed = alive before, dead after, in probation order
-    if (before[ids[k] - lo] && !after[ids[k] - lo]) removed[r++] = ids[k];
+  for (int q = 0; q < nv; ++q) {  // removed = alive before, dead after, in probation order
+    const long long id = ids[kept_in[q]];
+    if (before[id - lo] && !after[id - lo]) removed[r++] = id;
+  }
   *n_removed = r;
   const int kn = *(const int*)(hb + o_kn);
-  if (kn < 0 || kn > n) return fail(ctx, LM_ERR_INVALID_STATE, "probation list grew in a cull (%d > %d)", kn, n);
+  if (kn < 0 || kn > nv) return fail(ctx, LM_ERR_INVALID_STATE, "probation list grew in a cull (%d > %d)", kn, nv);
   const int* kid = (const int*)(hb + o_kid);
   for (int k = 0; k < kn; ++k) keep_ids[k] = kid[k];
   memcpy(keep_born, hb + o_kborn, 4 * (size_t)kn);

@@ -2441,8 +2441,8 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   __shared__ int s_toff[TMAX];  // keypoint offset of each pass's target
   __shared__ ActRec s_acts[DMAX];  // the pass's first DMAX actions
   __shared__ double cur_pose[22];  // R, t, C, cam, cell size of the current keyframe
-  __shared__ int rcmd[4];          // CTA 0 -> helpers: command, t1, tag, action count
-  enum { RC_DIRECT = 1, RC_EXIT = 2 };
+  __shared__ int rcmd[5];          // CTA 0 -> helpers: command, t1, tag, action / point count, ncand
+  enum { RC_DIRECT = 1, RC_EXIT = 2, RC_SETTLE = 3 };
   // CTA 0's counters and lists, reached by the helper CTAs through distributed shared memory
   int* const ni_p = rank ? cl.map_shared_rank(&ni_sh, 0) : &ni_sh;
   int* const nset_p = rank ? cl.map_shared_rank(&s_nset, 0) : &s_nset;
@@ -2708,6 +2708,43 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     __syncwarp();
   };
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // touched point p after the apply, one warp: its post-ADD state when the apply did exactly
+  // the speculated ADD (same observation set as k_fuse_post's; the list is sorted: clean
+  // before, the current keyframe appended last), else refresh (descriptor + geometry) and
+  // a new hit
+  auto settle_point = [&](int p) {
+    if (M.sp_tag[p] == mtag && M.sp_ver0[p] >= 0 && M.ver[p] == M.sp_ver0[p] + 1 &&
+        M.nobs[p] == M.sp_nobs0[p] + 1 && M.kbind[cur_off + M.sp_j[p]] == p) {
+      if (lane == 0) install_post(p);
+      __syncwarp();
+      return;
+    }
+    if (M.dirty[p]) {
+      refresh_rep_warp(M, p, lane);
+      if (lane == 0) M.dirty[p] = 0;
+      __syncwarp();
+    }
+    if (!M.gval[p]) geo_full_warp(M, p, lane);
+    PGeo g;
+    point_geometry(M, p, fc.dist_band_slack, g);  // (every lane: same loads, broadcast)
+    const int j = gather_hit_warp(M, fc, g, cur, TV, lane);
+    if (lane == 0) {
+      M.hit[p] = make_int2(M.ver[p], j);
+      hit_list_add(M, j, p);
+    }
+    __syncwarp();
+  };
+  // settle phase item k of a general pass: touched points (k < ncand) that have items in later
+  // passes settle; the points hitting a re-bound keypoint list their items
+  auto settle_item = [&](int k, int ncand, int t1, int tag) {
+    const int p = M.s.cands[k];
+    if (k < ncand) {
+      if (!M.alive[p] || !M.s.cneed[k]) return;
+      settle_point(p);
+    } else {
+      point_items(p, t1, tag);
+    }
+  };
   const int AW = (K + 31) >> 5;
   constexpr int RW = REV_THREADS / 32;  // warps per CTA
   if (rank > 0) {  // helper CTA: direct-pass actions k = rank*RW + wid (+ nranks*RW) on command
@@ -2715,11 +2752,15 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       cl.sync();  // (A) a command is published
       const int cmd = rcmd0[0];
       if (cmd == RC_EXIT) break;
-      const int ht1 = rcmd0[1], htag = rcmd0[2], hna = rcmd0[3];
+      const int ht1 = rcmd0[1], htag = rcmd0[2], hna = rcmd0[3], hnc = rcmd0[4];
 #ifdef LM_DIAG
       const long long hd0 = gtime();
 #endif
-      for (int k = rank * RW + wid; k < hna; k += nranks * RW) add_direct(M.s.acts[k], k, ht1, htag);
+      if (cmd == RC_SETTLE) {
+        for (int k = rank * RW + wid; k < hna; k += nranks * RW) settle_item(k, hnc, ht1, htag);
+      } else {
+        for (int k = rank * RW + wid; k < hna; k += nranks * RW) add_direct(M.s.acts[k], k, ht1, htag);
+      }
 #ifdef LM_DIAG
       if (lane == 0) atomicMax(&g_diag[60], (unsigned long long)(gtime() - hd0));
 #endif
@@ -2781,27 +2822,16 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
         const unsigned* bits = M.s.abits + (size_t)t1 * AW;
         const ActRec* seg = M.s.acts2 + (size_t)t1 * K;
         if (AW <= 64) {
-          // lane per word pair (w = lane, lane + 32): the first two set bits of each word are
-          // extracted in registers and their records loaded at once, while the word prefix
-          // counts are scanned; further bits (rare) in a loop. Keypoint order = word order.
+          // lane per word pair (w = lane, lane + 32): the word prefix counts give each action
+          // its position (keypoint order = word order); the keypoint indices go to s_il (free
+          // until this iteration's items are listed), then the records load lane-parallel, up
+          // to four per lane in flight (a word with many actions no longer loads them in a
+          // dependent chain on one lane)
           const unsigned b0 = lane < AW ? bits[lane] : 0u, b1 = lane + 32 < AW ? bits[lane + 32] : 0u;
           const int c0 = __popc(b0), c1 = __popc(b1);
 #ifdef LM_DIAG
           if (lane == 0) g_diag[48] += gtime() - ta;
 #endif
-          unsigned r0 = b0, r1 = b1;
-          int kq[4];
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            kq[i] = r0 ? 32 * lane + __ffs(r0) - 1 : -1;
-            r0 &= r0 - 1;
-            kq[2 + i] = r1 ? 32 * (lane + 32) + __ffs(r1) - 1 : -1;
-            r1 &= r1 - 1;
-          }
-          ActRec xr[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (kq[i] >= 0) xr[i] = seg[kq[i]];
           int p0 = c0, p1 = c1;
           for (int off = 1; off < 32; off <<= 1) {
             const int y0 = __shfl_up_sync(0xffffffffu, p0, off), y1 = __shfl_up_sync(0xffffffffu, p1, off);
@@ -2818,20 +2848,30 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
             if (at < DMAX) s_acts[at] = y;
             M.s.acts[at] = y;
           };
+          if (na <= ILS) {
+            int at = pre0;
+            for (unsigned r = b0; r; r &= r - 1) s_il[at++] = 32 * lane + __ffs(r) - 1;
+            at = pre1;
+            for (unsigned r = b1; r; r &= r - 1) s_il[at++] = 32 * (lane + 32) + __ffs(r) - 1;
+            __syncwarp();
+            for (int k0 = 0; k0 < na; k0 += 128) {
+              ActRec xr[4];
 #pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            if (kq[i] >= 0) put(pre0 + i, xr[i]);
-            if (kq[2 + i] >= 0) put(pre1 + i, xr[2 + i]);
-          }
-          for (int at = pre0 + 2; r0; ++at) {
-            const int kp = 32 * lane + __ffs(r0) - 1;
-            r0 &= r0 - 1;
-            put(at, seg[kp]);
-          }
-          for (int at = pre1 + 2; r1; ++at) {
-            const int kp = 32 * (lane + 32) + __ffs(r1) - 1;
-            r1 &= r1 - 1;
-            put(at, seg[kp]);
+              for (int i = 0; i < 4; ++i) {
+                const int k = k0 + 32 * i + lane;
+                if (k < na) xr[i] = seg[s_il[k]];
+              }
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int k = k0 + 32 * i + lane;
+                if (k < na) put(k, xr[i]);
+              }
+            }
+          } else {
+            int at = pre0;
+            for (unsigned r = b0; r; r &= r - 1) put(at++, seg[32 * lane + __ffs(r) - 1]);
+            at = pre1;
+            for (unsigned r = b1; r; r &= r - 1) put(at++, seg[32 * (lane + 32) + __ffs(r) - 1]);
           }
 #ifdef LM_DIAG
           if (lane == 0) g_diag[49] += gtime() - ta;
@@ -2917,32 +2957,6 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     const int na = na_sh, tag = tag_sh, ncand = nc_sh;
     // items of point p (its current observations) in passes after t1; warp-cooperative
     auto add_point_items = [&](int p) -> bool { return point_items(p, t1, tag); };
-    // touched point p after the apply, one warp: its post-ADD state when the apply did exactly
-    // the speculated ADD (same observation set as k_fuse_post's; the list is sorted: clean
-    // before, the current keyframe appended last), else refresh (descriptor + geometry) and
-    // a new hit
-    auto settle_point = [&](int p) {
-      if (M.sp_tag[p] == mtag && M.sp_ver0[p] >= 0 && M.ver[p] == M.sp_ver0[p] + 1 &&
-          M.nobs[p] == M.sp_nobs0[p] + 1 && M.kbind[cur_off + M.sp_j[p]] == p) {
-        if (lane == 0) install_post(p);
-        __syncwarp();
-        return;
-      }
-      if (M.dirty[p]) {
-        refresh_rep_warp(M, p, lane);
-        if (lane == 0) M.dirty[p] = 0;
-        __syncwarp();
-      }
-      if (!M.gval[p]) geo_full_warp(M, p, lane);
-      PGeo g;
-      point_geometry(M, p, fc.dist_band_slack, g);  // (every lane: same loads, broadcast)
-      const int j = gather_hit_warp(M, fc, g, cur, TV, lane);
-      if (lane == 0) {
-        M.hit[p] = make_int2(M.ver[p], j);
-        hit_list_add(M, j, p);
-      }
-      __syncwarp();
-    };
     // points hitting current keypoint k, whose binding changed, join the touched list (hit
     // list; a keypoint whose list overflowed falls back to scanning the passes of its bitmap)
     if (fast_sh) {
@@ -3048,19 +3062,24 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     const long long tv3 = gtime();
     // (3) touched points, warp each: refresh (descriptor + geometry) where stale, then the new
     //     hit (lane 0); the hit-list points' items (their state is unchanged)
+    // (a touched point without items in later passes keeps its dirty flag -- the next step's
+    //  refresh picks it up -- and a stale hit: nothing reads it, the version differs). More
+    //  points than CTA 0 has warps go to the whole cluster (the helper CTAs on command).
     const int nall = nc_sh;
     redo_pts += ncand;
-    for (int k = wid; k < nall; k += REV_THREADS / 32) {
-      const int p = M.s.cands[k];
-      if (k < ncand) {
-        // a touched point without items in later passes keeps its dirty flag (the next
-        // step's refresh picks it up) and a stale hit (nothing reads it: the version differs)
-        if (!M.alive[p] || !M.s.cneed[k]) continue;
-        settle_point(p);
-      } else {
-        add_point_items(p);
+    const bool wide = nranks > 1 && nall > RW;
+    if (wide) {
+      if (threadIdx.x == 0) {
+        rcmd[0] = RC_SETTLE;
+        rcmd[1] = t1;
+        rcmd[2] = tag;
+        rcmd[3] = nall;
+        rcmd[4] = ncand;
       }
+      cl.sync();  // (A)
     }
+    for (int k = wid; k < nall; k += wide ? nranks * RW : RW) settle_item(k, ncand, t1, tag);
+    if (wide) cl.sync();  // (B)
     __syncthreads();
     if (threadIdx.x == 0) {
       tm[0] += gtime() - tv;

@@ -243,6 +243,56 @@ def test_cull_keyframes_matches_oracle_on_a_pipeline_map():
     assert st.ledger.evictions == len(total)
 
 
+def test_cull_recent_skips_unknown_ids_and_rejects_repeats():
+    """cull_recent_map_points (culling.py:28-59) skips an entry whose point the model cannot
+    find (``mp is None``: neither removed nor kept). Two identical device maps, one culled
+    with the pipeline's probation list and one with that list plus entries naming no point
+    (negative, past the arena, not created yet): same removed ids, same kept entries (the
+    caller's own objects), same map afterwards. A point listed twice is rejected."""
+    from helpers import device_kf
+    from paper_2511_02036_b200 import workload as W
+    from paper_2511_02036_b200.culling import RecentPoint, cull_recent_map_points
+    from paper_2511_02036_b200.errors import InvalidArgumentError
+    from paper_2511_02036_b200.fusion import run_fusion
+    from paper_2511_02036_b200.mapmodel import DeviceStore
+    from paper_2511_02036_b200.triangulation import create_map_points
+
+    seq = W.generate_sequence(W.WorldConfig(seed=43, landmark_count=2000, keyframe_count=8, features_per_kf=400,
+                                            pixel_noise_sigma=0.8, descriptor_flip_bits=3, trajectory="line",
+                                            extent=6.0))
+    intr = seq.intrinsics()
+    maps = [MapModel(intr.num_levels, store=store_for(16, 512)) for _ in range(2)]
+    stores = [DeviceStore(), DeviceStore()]
+    recent = [[], []]
+    checked = 0
+    for processed, rec in enumerate(seq.records):
+        out = []
+        for side in range(2):
+            m, st = maps[side], stores[side]
+            kf = device_kf(rec, intr)
+            m.insert_keyframe(kf)
+            st.upload_keyframe(kf)
+            lst = recent[side]
+            if side == 1 and lst:
+                nxt = m._next_id()
+                lst = [RecentPoint(-3, processed)] + lst[: len(lst) // 2] + [RecentPoint(nxt + 50, processed),
+                                                                               RecentPoint(10 ** 9, 0)] + lst[len(lst) // 2:]
+            removed, kept = cull_recent_map_points(m, lst, processed)
+            assert all(any(k is e for e in lst) for k in kept)  # the caller's own entries
+            out.append((removed, [(k.mp_id, k.created_at) for k in kept]))
+            made = create_map_points(m, st, kf.kf_id, 6)
+            recent[side] = kept + [RecentPoint(i, processed) for i in made]
+            run_fusion(m, st, kf.kf_id)
+        assert out[0] == out[1], processed
+        checked += bool(out[0][0]) or bool(out[0][1])
+        assert maps[0]._snapshot().structural_digest() == maps[1]._snapshot().structural_digest(), processed
+    assert checked
+    lst = recent[0]
+    assert lst
+    with pytest.raises(InvalidArgumentError):
+        cull_recent_map_points(maps[0], lst + [lst[0]], len(seq.records))
+
+
 @pytest.mark.parametrize("n_obs", [3, 31, 33, 64, 65, 128, 129, 300, 513, 700])
 def test_representative_descriptor_every_refresh_path(n_obs):
     """_refresh_rep_descriptor (mapmodel.py:165-181) on one point observed n times, through

@@ -47,6 +47,14 @@ def main():
     modes = ["SLOT", "EX", "SH", "PAIR"]
     print("blocked by (first failing key) for ADD:", {m: buf[24 + k] for k, m in enumerate(modes)},
           "MERGE:", {m: buf[28 + k] for k, m in enumerate(modes)})
+    # reverse walk (k_fuse_rev, ns summed over the sequence): select phase, direct passes
+    np_ = max(buf[59], 1)
+    nd = max(buf[56], 1)
+    print(f"rev iterations {buf[59]}  direct passes {buf[56]} ({buf[57]} actions)  items re-evaluated {buf[58]}")
+    print(f"rev select: bits loaded {buf[48] / np_ / 1e3:.2f} us  actions extracted {buf[49] / np_ / 1e3:.2f} us  "
+          f"warp-0 select {buf[50] / np_ / 1e3:.2f} us  to the barrier {buf[51] / np_ / 1e3:.2f} us (per iteration)")
+    print(f"rev direct: walk+command {buf[52] / nd / 1e3:.2f} us  apply wall {buf[53] / nd / 1e3:.2f} us  "
+          f"slowest add_direct {buf[54] / nd / 1e3:.2f} us  (CTA 0's {buf[55] / nd / 1e3:.2f} us) per direct pass")
     fc, dbg = list(tot.fuse_cycles), list(tot.dbg)
     print(f"walls: reserve+check {fc[13] / 1e6:.3f} ms  heads {dbg[8] / 1e6:.3f} ms  members {dbg[9] / 1e6:.3f} ms  "
           f"compaction {fc[15] / 1e6:.3f} ms  fwd apply total {fc[3] / 1e6:.3f} ms")
