@@ -2442,13 +2442,17 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   __shared__ ActRec s_acts[DMAX];  // the pass's first DMAX actions
   __shared__ double cur_pose[22];  // R, t, C, cam, cell size of the current keyframe
   __shared__ int rcmd[5];          // CTA 0 -> helpers: command, t1, tag, action / point count, ncand
-  enum { RC_DIRECT = 1, RC_EXIT = 2, RC_SETTLE = 3 };
+  enum { RC_DIRECT = 1, RC_EXIT = 2, RC_SETTLE = 3, RC_RESCAN = 4 };
   // CTA 0's counters and lists, reached by the helper CTAs through distributed shared memory
   int* const ni_p = rank ? cl.map_shared_rank(&ni_sh, 0) : &ni_sh;
   int* const nset_p = rank ? cl.map_shared_rank(&s_nset, 0) : &s_nset;
   int* const il_p = rank ? cl.map_shared_rank(s_il, 0) : s_il;
   int* const inst_p = rank ? cl.map_shared_rank(s_inst, 0) : s_inst;
   const int* const rcmd0 = cl.map_shared_rank(rcmd, 0);
+  int* const live_p = rank ? cl.map_shared_rank(s_live, 0) : s_live;
+  int* const obs_p = rank ? cl.map_shared_rank(s_obs, 0) : s_obs;
+  int* const nact_p = rank ? cl.map_shared_rank(s_nact, 0) : s_nact;
+  int* const tmin_p = rank ? cl.map_shared_rank(&tmin_sh, 0) : &tmin_sh;
   if (threadIdx.x < 22) {
     const int c = A.cur, k = threadIdx.x;
     cur_pose[k] = k < 9 ? M.R[9 * c + k] : k < 12 ? M.t[3 * c + k - 9] : k < 15 ? M.C[3 * c + k - 12]
@@ -2470,13 +2474,15 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     s_nset = 0;
     tag_base = atomicAdd(&M.scal[SC_ROUND], T + 2);  // one dedupe tag per iteration (<= T + 1)
   }
-  for (int t = threadIdx.x; rank == 0 && t < T; t += REV_THREADS) {
-    s_nact[t] = M.s.pinfo[PI_NACT * TMAX + t];
-    s_live[t] = M.s.pinfo[PI_LIVE * TMAX + t];
-    s_obs[t] = M.s.pinfo[PI_OBS * TMAX + t];
+  for (int t = threadIdx.x; t < T; t += REV_THREADS) {
     const int ts = M.s.targets[t];
-    M.s.pass_of[ts] = t;
-    s_toff[t] = M.kp_off[ts];
+    s_toff[t] = M.kp_off[ts];  // (every CTA: the helpers re-evaluate items too)
+    if (rank == 0) {
+      s_nact[t] = M.s.pinfo[PI_NACT * TMAX + t];
+      s_live[t] = M.s.pinfo[PI_LIVE * TMAX + t];
+      s_obs[t] = M.s.pinfo[PI_OBS * TMAX + t];
+      M.s.pass_of[ts] = t;
+    }
   }
   pair_acc_init<REV_THREADS>(&acc, A.cur);  // (barrier)
   const unsigned long long mpb = M.mp_rec_bytes;
@@ -2747,6 +2753,23 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   };
   const int AW = (K + 31) >> 5;
   constexpr int RW = REV_THREADS / 32;  // warps per CTA
+  // re-evaluation of listed item q: pass totals by deltas (CTA 0's counters), action bitmap
+  // toggled
+  auto rescan_item = [&](int q) {
+    const int it = q < ILS ? il_p[q] : M.s.ilist[q];
+    const int t = it / K, kp = it - t * K;
+    const int oj = M.s.pj[it], ob = M.s.pob[it], oa = M.s.acts2[it].kind != 0;
+    const ItemVal v = eval_rev(t, kp);
+    store_item(M, it, v);
+    const int dl = (v.mp >= 0) - (oj != -3), dob = v.nob - ob, da = v.has - oa;
+    if (dl) atomicAdd(&live_p[t], dl);
+    if (dob) atomicAdd(&obs_p[t], dob);
+    if (da) {
+      atomicAdd(&nact_p[t], da);
+      atomicXor(&M.s.abits[(size_t)t * AW + (kp >> 5)], 1u << (kp & 31));
+    }
+    atomicMin(tmin_p, t);
+  };
   if (rank > 0) {  // helper CTA: direct-pass actions k = rank*RW + wid (+ nranks*RW) on command
     for (;;) {
       cl.sync();  // (A) a command is published
@@ -2758,6 +2781,8 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
 #endif
       if (cmd == RC_SETTLE) {
         for (int k = rank * RW + wid; k < hna; k += nranks * RW) settle_item(k, hnc, ht1, htag);
+      } else if (cmd == RC_RESCAN) {
+        for (int q = rank * REV_THREADS + threadIdx.x; q < hna; q += nranks * REV_THREADS) rescan_item(q);
       } else {
         for (int k = rank * RW + wid; k < hna; k += nranks * RW) add_direct(M.s.acts[k], k, ht1, htag);
       }
@@ -3096,21 +3121,19 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       g_diag[59] += 1;
     }
 #endif
-    for (int q = threadIdx.x; q < ni; q += REV_THREADS) {
-      const int it = q < ILS ? s_il[q] : M.s.ilist[q];
-      const int t = it / K, kp = it - t * K;
-      const int oj = M.s.pj[it], ob = M.s.pob[it], oa = M.s.acts2[it].kind != 0;
-      const ItemVal v = eval_rev(t, kp);
-      store_item(M, it, v);
-      const int dl = (v.mp >= 0) - (oj != -3), dob = v.nob - ob, da = v.has - oa;
-      if (dl) atomicAdd(&s_live[t], dl);
-      if (dob) atomicAdd(&s_obs[t], dob);
-      if (da) {
-        atomicAdd(&s_nact[t], da);
-        atomicXor(&M.s.abits[(size_t)t * AW + (kp >> 5)], 1u << (kp & 31));
+    // more items than CTA 0 has threads go to the whole cluster (the helpers on command)
+    const bool wide_r = nranks > 1 && ni > REV_THREADS;
+    if (wide_r) {
+      if (threadIdx.x == 0) {
+        rcmd[0] = RC_RESCAN;
+        rcmd[1] = t1;
+        rcmd[2] = tag;
+        rcmd[3] = ni;
       }
-      atomicMin(&tmin_sh, t);
+      cl.sync();  // (A)
     }
+    for (int q = threadIdx.x; q < ni; q += wide_r ? nranks * REV_THREADS : REV_THREADS) rescan_item(q);
+    if (wide_r) cl.sync();  // (B)
     __syncthreads();
     if (threadIdx.x == 0) {
       touched_min = tmin_sh;  // (diagnostic, thread 0's only: read here, before the reset below)
