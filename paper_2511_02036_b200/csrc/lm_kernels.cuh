@@ -2442,7 +2442,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   __shared__ ActRec s_acts[DMAX];  // the pass's first DMAX actions
   __shared__ double cur_pose[22];  // R, t, C, cam, cell size of the current keyframe
   __shared__ int rcmd[5];          // CTA 0 -> helpers: command, t1, tag, action / point count, ncand
-  enum { RC_DIRECT = 1, RC_EXIT = 2, RC_SETTLE = 3, RC_RESCAN = 4 };
+  enum { RC_DIRECT = 1, RC_EXIT = 2, RC_SETTLE = 3, RC_RESCAN = 4, RC_PTITEMS = 5 };
   // CTA 0's counters and lists, reached by the helper CTAs through distributed shared memory
   int* const ni_p = rank ? cl.map_shared_rank(&ni_sh, 0) : &ni_sh;
   int* const nset_p = rank ? cl.map_shared_rank(&s_nset, 0) : &s_nset;
@@ -2783,6 +2783,11 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
         for (int k = rank * RW + wid; k < hna; k += nranks * RW) settle_item(k, hnc, ht1, htag);
       } else if (cmd == RC_RESCAN) {
         for (int q = rank * REV_THREADS + threadIdx.x; q < hna; q += nranks * REV_THREADS) rescan_item(q);
+      } else if (cmd == RC_PTITEMS) {
+        for (int k = rank * RW + wid; k < hna; k += nranks * RW) {
+          const bool later = point_items(M.s.cands[k], ht1, htag);
+          if (hnc && lane == 0) M.s.cneed[k] = later;
+        }
       } else {
         for (int k = rank * RW + wid; k < hna; k += nranks * RW) add_direct(M.s.acts[k], k, ht1, htag);
       }
@@ -3038,8 +3043,23 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
         if (threadIdx.x == 0) tm[0] += gtime() - tv;
       }
     } else {
-      for (int k = wid; k < ncand; k += REV_THREADS / 32) add_point_items(M.s.cands[k]);  // before the apply
+      // the touched points' items before the apply (more points than CTA 0 has warps: on the
+      // whole cluster), the current keyframe's bindings before
+      const bool wide_p = nranks > 1 && ncand > RW;
+      auto command_items = [&](int cneed) {
+        if (threadIdx.x == 0) {
+          rcmd[0] = RC_PTITEMS;
+          rcmd[1] = t1;
+          rcmd[2] = tag;
+          rcmd[3] = ncand;
+          rcmd[4] = cneed;
+        }
+        cl.sync();  // (A)
+      };
+      if (wide_p) command_items(0);
+      for (int k = wid; k < ncand; k += wide_p ? nranks * RW : RW) add_point_items(M.s.cands[k]);
       for (int k = threadIdx.x; k < ncur; k += REV_THREADS) M.s.snap[k] = M.kbind[cur_off + k];  // bindings before
+      if (wide_p) cl.sync();  // (B)
       __syncthreads();
       if (threadIdx.x == 0) tm[7] += gtime() - ta;
       rounds += apply_block<REV_THREADS>(M, M.s.acts, na, cnt, sh, &acc, tm);  // (barriers)
@@ -3048,12 +3068,14 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     //     keypoint whose binding changed (hit list; a keypoint whose list overflowed falls
     //     back to scanning the passes of its bitmap) join the touched list
     const long long tv = gtime();
-    for (int k = wid; k < ncand; k += REV_THREADS / 32) {
+    if (wide_p) command_items(1);
+    for (int k = wid; k < ncand; k += wide_p ? nranks * RW : RW) {
       const bool later = add_point_items(M.s.cands[k]);
       if (lane == 0) M.s.cneed[k] = later;  // no later item: its new hit is not needed this step
     }
     for (int k = threadIdx.x; k < ncur; k += REV_THREADS)  // current keypoints whose binding changed
       if (M.kbind[cur_off + k] != M.s.snap[k]) M.s.chg[atomicAdd(&nchg_sh, 1)] = k;
+    if (wide_p) cl.sync();  // (B)
     __syncthreads();
     if (threadIdx.x == 0) tm[4] += gtime() - tv;
     const long long tv2 = gtime();
