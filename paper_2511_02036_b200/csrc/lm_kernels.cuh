@@ -2442,7 +2442,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   __shared__ ActRec s_acts[DMAX];  // the pass's first DMAX actions
   __shared__ double cur_pose[22];  // R, t, C, cam, cell size of the current keyframe
   __shared__ int rcmd[5];          // CTA 0 -> helpers: command, t1, tag, action / point count, ncand
-  enum { RC_DIRECT = 1, RC_EXIT = 2, RC_SETTLE = 3, RC_RESCAN = 4, RC_PTITEMS = 5 };
+  enum { RC_DIRECT = 1, RC_EXIT = 2, RC_SETTLE = 3, RC_RESCAN = 4, RC_PTITEMS = 5, RC_HITLIST = 6 };
   // CTA 0's counters and lists, reached by the helper CTAs through distributed shared memory
   int* const ni_p = rank ? cl.map_shared_rank(&ni_sh, 0) : &ni_sh;
   int* const nset_p = rank ? cl.map_shared_rank(&s_nset, 0) : &s_nset;
@@ -2453,6 +2453,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   int* const obs_p = rank ? cl.map_shared_rank(s_obs, 0) : s_obs;
   int* const nact_p = rank ? cl.map_shared_rank(s_nact, 0) : s_nact;
   int* const tmin_p = rank ? cl.map_shared_rank(&tmin_sh, 0) : &tmin_sh;
+  int* const nc_p = rank ? cl.map_shared_rank(&nc_sh, 0) : &nc_sh;
   if (threadIdx.x < 22) {
     const int c = A.cur, k = threadIdx.x;
     cur_pose[k] = k < 9 ? M.R[9 * c + k] : k < 12 ? M.t[3 * c + k - 9] : k < 15 ? M.C[3 * c + k - 12]
@@ -2518,6 +2519,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       else M.s.ilist[at] = (int)it;
     }
   };
+  auto passof = [&](int slot) -> int { return M.s.pass_of[slot]; };  // (read-only here: L1-resident)
   // items of point p (its current observations) in passes after t1; warp-cooperative; true
   // when p has one
   auto point_items = [&](int p, int t1, int tag) -> bool {
@@ -2527,7 +2529,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     bool any = false;
     for (int e = lane; e < no; e += 32) {
       const int2 ob = o[e];
-      const int tt = M.s.pass_of[ob.x];
+      const int tt = passof(ob.x);
       if (tt > t1) {
         add_item(tt, ob.y, tag);
         any = true;
@@ -2668,7 +2670,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     }
     // the point's items in passes after t1 (its observations after the ADD: the old ones and
     // (cur, j)), and the points hitting j (hit list): their hits are unchanged by the apply
-    const int tt0 = M.s.pass_of[o0], tt1 = M.s.pass_of[o1], ttc = lane == 0 ? M.s.pass_of[cur] : -1;
+    const int tt0 = passof(o0), tt1 = passof(o1), ttc = lane == 0 ? passof(cur) : -1;
     // hit-list point state in one round, its list head included (a point is listed under one
     // keypoint, its hit, so no other warp of this pass walks it; the action points are marked)
     const bool hv = hp >= 0;
@@ -2680,7 +2682,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     if (ttc > t1) add_item(ttc, j, tag);
     for (int e = lane + 64; e < n; e += 32) {
       const int2 ob = o[e];
-      const int tt = M.s.pass_of[ob.x];
+      const int tt = passof(ob.x);
       if (tt > t1) add_item(tt, ob.y, tag);
     }
     unsigned hm = __ballot_sync(0xffffffffu, hq);
@@ -2690,7 +2692,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       const int qn = __shfl_sync(0xffffffffu, hno, src), qo = __shfl_sync(0xffffffffu, hof, src);
       for (int e = lane; e < qn; e += 32) {
         const int2 ob = M.obs[qo + e];
-        const int tt = M.s.pass_of[ob.x];
+        const int tt = passof(ob.x);
         if (tt > t1) add_item(tt, ob.y, tag);
       }
     }
@@ -2740,6 +2742,32 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     }
     __syncwarp();
   };
+  // changed current keypoint q of a general pass: the points hitting it join the touched
+  // list (hit list; a keypoint whose list overflowed scans the passes of its bitmap)
+  auto hitlist_item = [&](int q, int t1, int tag) {
+    const int k = M.s.chg[q];
+    const int c = M.s.hl_cnt[k];
+    if (c <= HL) {
+      if (lane < c) {
+        const int p = M.s.hl[k * HL + lane];
+        if (M.alive[p] && M.hit[p].y == k && atomicExch(&M.s.rmark[p], tag) != tag)
+          M.s.cands[atomicAdd(nc_p, 1)] = p;
+      }
+      return;
+    }
+    for (int w = 0; w < HPW; ++w) {
+      unsigned bits = M.s.hitpass[k * HPW + w];
+      while (bits) {
+        const int tt = 32 * w + __ffs(bits) - 1;
+        bits &= bits - 1;
+        if (tt <= t1 || tt >= T) continue;
+        const int n = M.kp_n[M.s.targets[tt]];
+        const int* pjt = M.s.pj + (size_t)tt * K;
+        for (int kp = lane; kp < n; kp += 32)
+          if (pjt[kp] == k) add_item(tt, kp, tag);
+      }
+    }
+  };
   // settle phase item k of a general pass: touched points (k < ncand) that have items in later
   // passes settle; the points hitting a re-bound keypoint list their items
   auto settle_item = [&](int k, int ncand, int t1, int tag) {
@@ -2783,6 +2811,8 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
         for (int k = rank * RW + wid; k < hna; k += nranks * RW) settle_item(k, hnc, ht1, htag);
       } else if (cmd == RC_RESCAN) {
         for (int q = rank * REV_THREADS + threadIdx.x; q < hna; q += nranks * REV_THREADS) rescan_item(q);
+      } else if (cmd == RC_HITLIST) {
+        for (int q = rank * RW + wid; q < hna; q += nranks * RW) hitlist_item(q, ht1, htag);
       } else if (cmd == RC_PTITEMS) {
         for (int k = rank * RW + wid; k < hna; k += nranks * RW) {
           const bool later = point_items(M.s.cands[k], ht1, htag);
@@ -3080,30 +3110,18 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     if (threadIdx.x == 0) tm[4] += gtime() - tv;
     const long long tv2 = gtime();
     const int nchg = nchg_sh;
-    for (int q = wid; q < nchg; q += REV_THREADS / 32) {
-      const int k = M.s.chg[q];
-      const int c = M.s.hl_cnt[k];
-      if (c <= HL) {
-        if (lane < c) {
-          const int p = M.s.hl[k * HL + lane];
-          if (M.alive[p] && M.hit[p].y == k && atomicExch(&M.s.rmark[p], tag) != tag)
-            M.s.cands[atomicAdd(&nc_sh, 1)] = p;
-        }
-        continue;
+    const bool wide_h = nranks > 1 && nchg > RW;
+    if (wide_h) {
+      if (threadIdx.x == 0) {
+        rcmd[0] = RC_HITLIST;
+        rcmd[1] = t1;
+        rcmd[2] = tag;
+        rcmd[3] = nchg;
       }
-      for (int w = 0; w < HPW; ++w) {
-        unsigned bits = M.s.hitpass[k * HPW + w];
-        while (bits) {
-          const int tt = 32 * w + __ffs(bits) - 1;
-          bits &= bits - 1;
-          if (tt <= t1 || tt >= T) continue;
-          const int n = M.kp_n[M.s.targets[tt]];
-          const int* pjt = M.s.pj + (size_t)tt * K;
-          for (int kp = lane; kp < n; kp += 32)
-            if (pjt[kp] == k) add_item(tt, kp, tag);
-        }
-      }
+      cl.sync();  // (A)
     }
+    for (int q = wid; q < nchg; q += wide_h ? nranks * RW : RW) hitlist_item(q, t1, tag);
+    if (wide_h) cl.sync();  // (B)
     __syncthreads();
     if (threadIdx.x == 0) tm[5] += gtime() - tv2;
     const long long tv3 = gtime();
