@@ -3028,7 +3028,10 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       // items are the points' observations after the apply.
       // (8 lanes per action, four actions per warp, measured 5% slower on C2: more registers
       // spilled and the tile syncs; a warp per action stays)
-      if (nranks > 1) {  // the helper CTAs take their share of the actions
+      // the helper CTAs take their share of the actions when there are more than CTA 0 has
+      // warps (a pass CTA 0 covers alone skips the two cluster barriers)
+      const bool wide_d = nranks > 1 && na > RW;
+      if (wide_d) {
         if (threadIdx.x == 0) {
           rcmd[0] = RC_DIRECT;
           rcmd[1] = t1;
@@ -3040,12 +3043,12 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
 #ifdef LM_DIAG
       const long long hd0 = gtime();
 #endif
-      for (int k = wid; k < na; k += nranks * RW) add_direct(s_acts[k], k, t1, tag);
+      for (int k = wid; k < na; k += wide_d ? nranks * RW : RW) add_direct(s_acts[k], k, t1, tag);
 #ifdef LM_DIAG
       if (lane == 0) atomicMax(&g_diag[61], (unsigned long long)(gtime() - hd0));
       if (threadIdx.x == 0) g_diag[52] += hd0 - ta;  // walk + command
 #endif
-      if (nranks > 1) cl.sync();  // (B)
+      if (wide_d) cl.sync();  // (B)
       __syncthreads();
 #ifdef LM_DIAG
       if (threadIdx.x == 0) {
