@@ -89,6 +89,7 @@ struct lm_ctx {
   int cull_cluster = 8;                 // CTAs per map of the recent-point cull cluster (LM_CULL_CLUSTER)
   int rev_cluster = 8;                  // CTAs per map of the reverse walk (LM_REV_CLUSTER; 1 = CTA 0 alone)
   int tri_slices = 4;                   // k_tri CTAs per neighbour (LM_TRI_SLICES)
+  int rev_wide = 1 | 1 << 8;            // k_fuse_rev cluster-wide thresholds (LM_REV_WIDE="direct,other")
   int refresh_blocks = 148;             // k_fuse_refresh grid (x) (LM_REFRESH_BLOCKS)
   int post_blocks = 148;                // k_fuse_post grid (x), <= POST_BLOCKS (LM_POST_BLOCKS)
   // programmatic dependent launch of the step kernels (LM_PDL=0/1 overrides): on for
@@ -778,6 +779,10 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
   if (const char* e = getenv("LM_REFRESH_BLOCKS")) ctx->refresh_blocks = atoi(e) > 0 ? atoi(e) : 148;
   if (const char* e = getenv("LM_POST_BLOCKS"))
     ctx->post_blocks = atoi(e) > 0 ? (atoi(e) < POST_BLOCKS ? atoi(e) : POST_BLOCKS) : 148;
+  if (const char* e = getenv("LM_REV_WIDE")) {
+    int d = 1, o = 1;
+    if (sscanf(e, "%d,%d", &d, &o) >= 1) ctx->rev_wide = (d < 1 ? 1 : d > 255 ? 255 : d) | (o < 1 ? 1 : o > 255 ? 255 : o) << 8;
+  }
   if (const char* e = getenv("LM_TRI_SLICES")) ctx->tri_slices = atoi(e) > 0 ? (atoi(e) < 32 ? atoi(e) : 32) : 1;
   if (const char* e = getenv("LM_CULL_CLUSTER")) {
     const int v = atoi(e);
@@ -1296,7 +1301,8 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
     // reverse walk: one cluster per map, CTA 0 walks, the others help with direct passes
     int cl = ctx->rev_cluster / n;
     cl = cl < 1 ? 1 : cl;
-    CU(launch_k(ctx, k_fuse_rev, dim3(n * cl), dim3(REV_THREADS), rev_smem, cl, dmaps, dv, (int)rev_smem));
+    CU(launch_k(ctx, k_fuse_rev, dim3(n * cl), dim3(REV_THREADS), rev_smem, cl, dmaps, dv, (int)rev_smem,
+                ctx->rev_wide));
   }
   launched += 8;
   }  // any_fuse

@@ -2388,7 +2388,7 @@ __global__ void __launch_bounds__(256) k_fuse_post(DevMap* maps, const StepArgs*
 }
 
 // reverse passes (fusion.py:337-346), one CTA per map; see the block comment above
-__global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const StepArgs* args, int smem_bytes) {
+__global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const StepArgs* args, int smem_bytes, int wide) {
   pdl_enter();
   // one cluster per map: CTA 0 walks the passes; the other CTAs (if any) only help apply the
   // direct passes' actions, on command (rcmd in CTA 0's shared memory, cluster barriers)
@@ -2781,6 +2781,9 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   };
   const int AW = (K + 31) >> 5;
   constexpr int RW = REV_THREADS / 32;  // warps per CTA
+  // a phase goes to the whole cluster when its work exceeds this many rounds of CTA 0 alone
+  // (byte 0: direct-pass actions; byte 1: the other phases; launch knob LM_REV_WIDE)
+  const int wd = wide & 0xff, wo = (wide >> 8) & 0xff;
   // re-evaluation of listed item q: pass totals by deltas (CTA 0's counters), action bitmap
   // toggled
   auto rescan_item = [&](int q) {
@@ -3030,7 +3033,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       // spilled and the tile syncs; a warp per action stays)
       // the helper CTAs take their share of the actions when there are more than CTA 0 has
       // warps (a pass CTA 0 covers alone skips the two cluster barriers)
-      const bool wide_d = nranks > 1 && na > RW;
+      const bool wide_d = nranks > 1 && na > RW * wd;
       if (wide_d) {
         if (threadIdx.x == 0) {
           rcmd[0] = RC_DIRECT;
@@ -3078,7 +3081,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     } else {
       // the touched points' items before the apply (more points than CTA 0 has warps: on the
       // whole cluster), the current keyframe's bindings before
-      const bool wide_p = nranks > 1 && ncand > RW;
+      const bool wide_p = nranks > 1 && ncand > RW * wo;
       auto command_items = [&](int cneed) {
         if (threadIdx.x == 0) {
           rcmd[0] = RC_PTITEMS;
@@ -3113,7 +3116,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     if (threadIdx.x == 0) tm[4] += gtime() - tv;
     const long long tv2 = gtime();
     const int nchg = nchg_sh;
-    const bool wide_h = nranks > 1 && nchg > RW;
+    const bool wide_h = nranks > 1 && nchg > RW * wo;
     if (wide_h) {
       if (threadIdx.x == 0) {
         rcmd[0] = RC_HITLIST;
@@ -3135,7 +3138,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     //  points than CTA 0 has warps go to the whole cluster (the helper CTAs on command).
     const int nall = nc_sh;
     redo_pts += ncand;
-    const bool wide = nranks > 1 && nall > RW;
+    const bool wide = nranks > 1 && nall > RW * wo;
     if (wide) {
       if (threadIdx.x == 0) {
         rcmd[0] = RC_SETTLE;
@@ -3165,7 +3168,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     }
 #endif
     // more items than CTA 0 has threads go to the whole cluster (the helpers on command)
-    const bool wide_r = nranks > 1 && ni > REV_THREADS;
+    const bool wide_r = nranks > 1 && ni > REV_THREADS * wo;
     if (wide_r) {
       if (threadIdx.x == 0) {
         rcmd[0] = RC_RESCAN;
