@@ -307,6 +307,7 @@ def main():
     # step's kernels on the library stream, for the rooflines and the stage breakdown
     prof_steps = max(1, args.profile_steps)
     lib.lm_profile_enable(ctx.h, 1)
+    one_step(True)  # (warm-up: the timer-carrying kernel instantiations load on their first launch)
     lib.lm_profile_read(ctx.h, (C.c_double * 16)(), (C.c_int64 * 16)())
     prof_acc = {}
     prof_total = 0.0
@@ -317,6 +318,9 @@ def main():
     prof_n = (C.c_int64 * 16)()
     lib.lm_profile_read(ctx.h, prof_ms, prof_n)
     lib.lm_profile_enable(ctx.h, 0)
+    # the in-kernel phase timers run in the profile pass only (globaltimer reads cost ~0.7% of
+    # the step): per-step work counts and phase times come from that pass (same workload)
+    pacc, psteps = prof_acc, prof_steps
     stages = ["insert", "cull", "select", "prep", "match", "tri", "commit", "fuse_targets", "fuse_geo",
               "fuse_gather", "fuse_apply", "fuse_refresh", "fuse_spec", "fuse_rev", "fuse_visible"]
     stage_ms = {s: prof_ms[k] / prof_steps for k, s in enumerate(stages)}
@@ -465,32 +469,32 @@ def main():
             "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
             "roofline_popc": roof_popc, "roofline_fusion_stage": roof_fuse, "stage_ms_per_step": stage_ms,
             "work_per_step": {"keyframes": len(ids), "match_pairs": per_step_pairs, "fuse_bytes": per_step_bytes,
-                              "created": acc["created"] / args.steps, "merged": acc["merged"] / args.steps,
-                              "observations_added": acc["observations_added"] / args.steps,
-                              "apply_rounds": acc["apply_rounds"] / args.steps,
-                              "rev_passes": (acc["fuse_passes"] / args.steps) / 2,
-                              "rev_passes_acting": acc["rev_passes_acting"] / args.steps,
-                              "rev_items_reevaluated": acc["rev_passes_redo"] / args.steps,
-                              "rev_acting_passes_untouched_by_previous_apply": acc["rev_mergeable"] / args.steps,
-                              "rev_points_recomputed": acc["fuse_cycles"][1] / args.steps,
-                              "rev_passes_direct_all_add": acc["dbg"][0] / args.steps,
-                              "cull_phase_ms": {"classify": acc["dbg"][1] / args.steps / 1e6,
-                                                "kills": acc["dbg"][2] / args.steps / 1e6,
-                                                "flush": acc["dbg"][3] / args.steps / 1e6},
-                              "fwd_apply_detail": {"heads_ms": acc["dbg"][8] / args.steps / 1e6,
-                                                   "members_merges_ms": acc["dbg"][9] / args.steps / 1e6,
-                                                   "rounds": acc["dbg"][10] / args.steps,
-                                                   "actions": acc["dbg"][11] / args.steps,
-                                                   "pending_in_later_rounds": acc["dbg"][15] / args.steps},
-                              "rev_touched_points_from_post_add_speculation": acc["dbg"][12] / args.steps,
-                              "culled": acc["culled"] / args.steps,
-                              "cull_probation_entries": acc["dbg"][13] / args.steps,
-                              "cull_kills_over_8_obs": acc["dbg"][14] / args.steps,
-                              "rev_subphase_ms": {"select_actions_preitems": acc["dbg"][7] / args.steps / 1e6,
-                                                  "postitems_changed": acc["dbg"][4] / args.steps / 1e6,
-                                                  "hitlist": acc["dbg"][5] / args.steps / 1e6,
-                                                  "refresh_hits": acc["dbg"][6] / args.steps / 1e6}},
-            "fuse_phase_ms_per_step": {n: acc["fuse_cycles"][k] / args.steps / 1e6
+                              "created": pacc["created"] / psteps, "merged": pacc["merged"] / psteps,
+                              "observations_added": pacc["observations_added"] / psteps,
+                              "apply_rounds": pacc["apply_rounds"] / psteps,
+                              "rev_passes": (pacc["fuse_passes"] / psteps) / 2,
+                              "rev_passes_acting": pacc["rev_passes_acting"] / psteps,
+                              "rev_items_reevaluated": pacc["rev_passes_redo"] / psteps,
+                              "rev_acting_passes_untouched_by_previous_apply": pacc["rev_mergeable"] / psteps,
+                              "rev_points_recomputed": pacc["fuse_cycles"][1] / psteps,
+                              "rev_passes_direct_all_add": pacc["dbg"][0] / psteps,
+                              "cull_phase_ms": {"classify": pacc["dbg"][1] / psteps / 1e6,
+                                                "kills": pacc["dbg"][2] / psteps / 1e6,
+                                                "flush": pacc["dbg"][3] / psteps / 1e6},
+                              "fwd_apply_detail": {"heads_ms": pacc["dbg"][8] / psteps / 1e6,
+                                                   "members_merges_ms": pacc["dbg"][9] / psteps / 1e6,
+                                                   "rounds": pacc["dbg"][10] / psteps,
+                                                   "actions": pacc["dbg"][11] / psteps,
+                                                   "pending_in_later_rounds": pacc["dbg"][15] / psteps},
+                              "rev_touched_points_from_post_add_speculation": pacc["dbg"][12] / psteps,
+                              "culled": pacc["culled"] / psteps,
+                              "cull_probation_entries": pacc["dbg"][13] / psteps,
+                              "cull_kills_over_8_obs": pacc["dbg"][14] / psteps,
+                              "rev_subphase_ms": {"select_actions_preitems": pacc["dbg"][7] / psteps / 1e6,
+                                                  "postitems_changed": pacc["dbg"][4] / psteps / 1e6,
+                                                  "hitlist": pacc["dbg"][5] / psteps / 1e6,
+                                                  "refresh_hits": pacc["dbg"][6] / psteps / 1e6}},
+            "fuse_phase_ms_per_step": {n: pacc["fuse_cycles"][k] / psteps / 1e6
                                        for k, n in enumerate(["targets", "-", "fwd_assemble", "fwd_apply",
                                                               "rev_redo_refresh", "rev_select", "rev_apply",
                                                               "rev_rescan", "rev_prologue", "rev_apply_reserve_check",
@@ -498,7 +502,7 @@ def main():
                                                               "rev_apply_compaction", "fwd_apply_reserve_check",
                                                               "fwd_apply_commit_merges", "fwd_apply_compaction"])
                                        if n != "-"},
-            "rev_recomputed_points_per_step": acc["fuse_cycles"][1] / args.steps}
+            "rev_recomputed_points_per_step": pacc["fuse_cycles"][1] / psteps}
     line["profiled_ms_per_step"] = profiled_step_ms
     line["device_window"] = window
     bl = [x / args.steps for x in acc.get("borderline", [0, 0, 0, 0])]

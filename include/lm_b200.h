@@ -396,7 +396,9 @@ int64_t lm_launch_count(lm_ctx* ctx);
 int lm_totals_fetch(lm_ctx* ctx, int32_t map, lm_step_stats* out);            /* kernels launched by this context so far */
 /* Per-stage CUDA-event timing of the step kernels (stage order: begin+insert, cull, select,
  * prep, match, tri, commit, fuse_targets, fuse_geo, fuse_gather, fuse_apply, fuse_refresh,
- * fuse_rev+end). Enabling adds one event per stage boundary per step. */
+ * fuse_rev+end). Enabling adds one event per stage boundary per step and turns on the
+ * kernels' in-step phase timers (lm_step_stats fuse_cycles / dbg time fields; device-wide),
+ * which read 0 otherwise. */
 int lm_profile_enable(lm_ctx* ctx, int32_t on);
 int lm_profile_read(lm_ctx* ctx, double ms[16], int64_t launches[16]); /* sums, then clears */
 /* Sustained __popc throughput of this device (popc32 results per second). */

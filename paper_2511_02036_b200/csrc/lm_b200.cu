@@ -758,20 +758,25 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
   }
   CU(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
   CU(cudaFuncSetAttribute(k_fuse_targets, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
-  CU(cudaFuncSetAttribute(k_fuse_rev, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  // (k_cull / k_fuse_apply / k_fuse_rev: <false> for every launch, <true> for the profile pass)
+  CU(cudaFuncSetAttribute(k_fuse_rev<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  CU(cudaFuncSetAttribute(k_fuse_rev<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   CU(cudaFuncSetAttribute(k_op, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
-  CU(cudaFuncSetAttribute(k_fuse_apply, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  CU(cudaFuncSetAttribute(k_fuse_rev, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  CU(cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, CULL_DYN_SMEM));
+  CU(cudaFuncSetAttribute(k_fuse_apply<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CU(cudaFuncSetAttribute(k_fuse_apply<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CU(cudaFuncSetAttribute(k_fuse_rev<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CU(cudaFuncSetAttribute(k_fuse_rev<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CU(cudaFuncSetAttribute(k_cull<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, CULL_DYN_SMEM));
+  CU(cudaFuncSetAttribute(k_cull<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CULL_DYN_SMEM));
   CU(cudaFuncSetAttribute(k_tri, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
   if (const char* e = getenv("LM_CARVEOUT")) {  // (experiments) shared-memory carve-out hint, percent
     const int pc = atoi(e);
-    const void* ks[] = {(const void*)k_insert, (const void*)k_cull, (const void*)k_select, (const void*)k_prep,
+    const void* ks[] = {(const void*)k_insert, (const void*)k_cull<false>, (const void*)k_cull<true>, (const void*)k_select, (const void*)k_prep,
                         (const void*)k_match, (const void*)k_tri, (const void*)k_commit, (const void*)k_fuse_targets,
-                        (const void*)k_fuse_geo, (const void*)k_fuse_gather, (const void*)k_fuse_apply,
+                        (const void*)k_fuse_geo, (const void*)k_fuse_gather, (const void*)k_fuse_apply<false>, (const void*)k_fuse_apply<true>,
                         (const void*)k_fuse_refresh, (const void*)k_fuse_spec<true>, (const void*)k_fuse_spec<false>,
                         (const void*)k_fuse_spec_pts, (const void*)k_fuse_spec_hit, (const void*)k_fuse_post,
-                        (const void*)k_fuse_rev, (const void*)k_fuse_visible_end};
+                        (const void*)k_fuse_rev<false>, (const void*)k_fuse_rev<true>, (const void*)k_fuse_visible_end};
     for (const void* k : ks) CU(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pc));
   }
   if (const char* e = getenv("LM_PDL")) ctx->pdl = atoi(e) != 0 ? 1 : 0;
@@ -1240,7 +1245,8 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
     // recent-point cull: one cluster per map, as wide as the batch leaves SMs for
     int cl = ctx->cull_cluster / n;
     cl = cl < 1 ? 1 : cl;
-    CU(launch_k(ctx, k_cull, dim3(n * cl), dim3(1024), CULL_DYN_SMEM, cl, dmaps, (const StepArgs*)dv));
+    CU(launch_k(ctx, ctx->prof ? k_cull<true> : k_cull<false>, dim3(n * cl), dim3(1024), CULL_DYN_SMEM, cl, dmaps,
+                (const StepArgs*)dv));
     launched += 1;
   }
   if ((rc = mark())) return rc;
@@ -1282,7 +1288,8 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
     // forward apply: one cluster per map, as wide as the batch leaves SMs for
     int cl = ctx->apply_cluster / n;
     cl = cl < 1 ? 1 : (cl > ctx->apply_cluster ? ctx->apply_cluster : cl);
-    CU(launch_k(ctx, k_fuse_apply, dim3(n * cl), dim3(APPLY_THREADS), 0, cl, dmaps, (const StepArgs*)dv));
+    CU(launch_k(ctx, ctx->prof ? k_fuse_apply<true> : k_fuse_apply<false>, dim3(n * cl), dim3(APPLY_THREADS), 0, cl,
+                dmaps, (const StepArgs*)dv));
   }
   if ((rc = mark())) return rc;
   CU(launch_k(ctx, k_fuse_refresh, dim3(ctx->refresh_blocks, n), dim3(256), 0, 0, dmaps, dv));
@@ -1301,7 +1308,8 @@ static int launch_steps(lm_ctx* ctx, int n, const int32_t* maps, StepArgs* args)
     // reverse walk: one cluster per map, CTA 0 walks, the others help with direct passes
     int cl = ctx->rev_cluster / n;
     cl = cl < 1 ? 1 : cl;
-    CU(launch_k(ctx, k_fuse_rev, dim3(n * cl), dim3(REV_THREADS), rev_smem, cl, dmaps, dv, (int)rev_smem,
+    CU(launch_k(ctx, ctx->prof ? k_fuse_rev<true> : k_fuse_rev<false>, dim3(n * cl), dim3(REV_THREADS), rev_smem, cl,
+                dmaps, dv, (int)rev_smem,
                 ctx->rev_wide));
   }
   launched += 8;

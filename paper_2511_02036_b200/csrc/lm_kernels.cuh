@@ -76,6 +76,14 @@ __device__ __forceinline__ long long gtime() {  // ns, device-wide clock
 #endif
 }
 
+// phase-timer reads of the kernels instantiated twice: with timers (P, the library's profile
+// pass: lm_profile_enable) and without (every other launch). The timer-free instantiation
+// measured 0.9% faster on C2 than one that reads the timer in every launch.
+template <bool P>
+__device__ __forceinline__ long long gtime_p() {
+  return P ? gtime() : 0;
+}
+
 template <int BLOCK>
 __device__ __forceinline__ int block_excl_scan(int v, int* sh, int& total) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -234,6 +242,7 @@ __global__ void __launch_bounds__(256) k_insert(DevMap* maps, const StepArgs* ar
 constexpr int CULL_CHUNK = 2048;  // probation entries per k_cull iteration (two per thread)
 constexpr int CULL_DYN_SMEM = (3 * CULL_CHUNK + PAIR_W * (CULL_CHUNK / 32)) * 4;  // kill rows + transposed columns
 
+template <bool P>
 __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* args) {
   pdl_enter();
   // one cluster per map: rank 0 classifies and owns the accumulator; every rank takes a share
@@ -259,9 +268,9 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
   int* nbig0 = cl.map_shared_rank(&nbig, 0);
   unsigned* krow0 = cl.map_shared_rank(krow, 0);
   const int* tk0 = cl.map_shared_rank(&tk_sh, 0);
-  const long long c_t0 = gtime();
+  const long long c_t0 = gtime_p<P>();
   pair_acc_init<1024>(&acc, A.cur);
-  const long long c_t1 = gtime();
+  const long long c_t1 = gtime_p<P>();
   long long c_kill = 0;
   const int n = M.scal[SC_RECENT_N];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -310,7 +319,7 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
     }
     }
     cl.sync();  // the chunk's kill list (rank 0) is published
-    const long long c_a = gtime();
+    const long long c_a = gtime_p<P>();
     // independent points, thread each, spread over the cluster: bindings and counters
     // cleared, the observer set as a window bitmask (rows, into rank 0); the covisibility
     // decrements of all of them are the pair counts of the rows' Gram matrix, counted with
@@ -412,12 +421,12 @@ __global__ void __launch_bounds__(1024) k_cull(DevMap* maps, const StepArgs* arg
       }
     }
     __syncthreads();
-    c_kill += gtime() - c_a;
+    c_kill += gtime_p<P>() - c_a;
   }
   if (rank != 0) return;
-  const long long c_t2 = gtime();
+  const long long c_t2 = gtime_p<P>();
   pair_acc_flush<1024>(M, &acc);
-  const long long c_t3 = gtime();
+  const long long c_t3 = gtime_p<P>();
   if (threadIdx.x == 0) {
     M.scal[SC_RECENT_N] = kept;
     M.s.stats->culled = culled;
@@ -1456,7 +1465,7 @@ struct ClusterTeam {
   __device__ void sync() const { cg::this_cluster().sync(); }
 };
 
-template <class Team>
+template <class Team, bool P = true>
 __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh, PairAcc* acc,
                           long long* tm = nullptr) {
   int* const ctl = G.ctl;  // team control words (CTL_*), in the team leader's shared memory
@@ -1490,7 +1499,7 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
 #endif
     if (tm && tid == 0 && rounds > 0) tm[13] += np;  // diagnostics: actions left after round 1
     const unsigned rnd = (unsigned)cw[CTL_ROUND];
-    long long tt = gtime();
+    long long tt = gtime_p<P>();
     DIAG_T0
     for (int a = tid; a < n; a += nth) {
       if (!M.s.pend[a]) continue;
@@ -1565,8 +1574,8 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
     if (Team::kCluster && tid == 0 && rounds > 0) diag_fold((rounds + 1) & 1);  // the previous round's maxima are final
 #endif
     if (tm && tid == 0) {
-      tm[9] += gtime() - tt;
-      tt = gtime();
+      tm[9] += gtime_p<P>() - tt;
+      tt = gtime_p<P>();
     }
     // group leaders (ticket 0): a lone low-degree ADD links here (thread), a lone high-degree
     // one goes to a warp; a group of m reserves m entries (base = old length) for its members
@@ -1625,8 +1634,8 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
     DIAG_RESTART
     if (tid == nth - 1) open_bank(nw, np - cw[CTL_NREADY]);  // (the team's last thread: rarely an action)
     if (tm && tid == 0) {
-      tm[10] += gtime() - tt;
-      tt = gtime();
+      tm[10] += gtime_p<P>() - tt;
+      tt = gtime_p<P>();
     }
     // group members: own entry, binding, counter, covisibility with the old observers;
     // warps: lone high-degree ADDs and merges (disjoint entities)
@@ -1671,7 +1680,7 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
     for (int d = tid; groups && d < nd; d += nth) member_pairs(acts[M.s.def[d]], (int)M.s.dnxt[d]);
     DIAG_MAX(4)
     if (groups) G.sync();
-    if (tm && tid == 0) tm[11] += gtime() - tt;
+    if (tm && tid == 0) tm[11] += gtime_p<P>() - tt;
 
     if (++rounds > (1 << 20)) break;
   }
@@ -1682,12 +1691,12 @@ __device__ int apply_team(const Team& G, const DevMap& M, const ActRec* acts, in
 }
 
 
-template <int BLOCK>
+template <int BLOCK, bool P = true>
 __device__ int apply_block(const DevMap& M, const ActRec* acts, int n, int* cnt, int* sh, PairAcc* acc,
                            long long* tm = nullptr) {
   __shared__ int ctl[CTL_N];
   const BlockTeam<BLOCK> G(ctl);
-  return apply_team(G, M, acts, n, cnt, sh, acc, tm);
+  return apply_team<BlockTeam<BLOCK>, P>(G, M, acts, n, cnt, sh, acc, tm);
 }
 
 // warp per point of pts[0..P) that is dirty (sort + representative descriptor) or whose
@@ -2042,6 +2051,7 @@ constexpr int APPLY_THREADS = 512;  // k_fuse_apply CTA (128 registers: apply_te
 // Forward apply: one thread-block cluster per map (launched with cluster dims; blockIdx.x /
 // cluster size selects the map). The ~4.5k forward actions of a C2 keyframe spread over the
 // cluster's CTAs; the reservation rounds synchronise with barrier.cluster.
+template <bool TP>
 __global__ void __launch_bounds__(APPLY_THREADS, 1) k_fuse_apply(DevMap* maps, const StepArgs* args) {
   pdl_enter();
   cg::cluster_group cl = cg::this_cluster();
@@ -2056,7 +2066,7 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) k_fuse_apply(DevMap* maps, c
   __shared__ int ctl[CTL_N];
   __shared__ PairAcc acc;
   __shared__ long long tmf[16];
-  const long long t0 = gtime();
+  const long long t0 = gtime_p<TP>();
   if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
   if (threadIdx.x < 16) tmf[threadIdx.x] = 0;
   pair_acc_init<APPLY_THREADS>(&acc, A.cur);
@@ -2078,8 +2088,8 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) k_fuse_apply(DevMap* maps, c
     for (int k = threadIdx.x & 31; k < c; k += 32) M.s.acts[o + k] = M.s.acts2[b * 256 + k];
   }
   G.sync();
-  const long long t1 = gtime();
-  const int rr = apply_team(G, M, M.s.acts, nact, cnt, sh, &acc, rank == 0 ? tmf : nullptr);
+  const long long t1 = gtime_p<TP>();
+  const int rr = apply_team<ClusterTeam<APPLY_THREADS>, TP>(G, M, M.s.acts, nact, cnt, sh, &acc, rank == 0 ? tmf : nullptr);
   pair_acc_flush<APPLY_THREADS>(M, &acc);
   lm_step_stats* st = M.s.stats;
   if (threadIdx.x == 0) {
@@ -2092,7 +2102,7 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) k_fuse_apply(DevMap* maps, c
     st->fuse_bytes += 16LL * nact;
     st->apply_rounds += rr;
     st->fuse_cycles[2] += t1 - t0;
-    st->fuse_cycles[3] += gtime() - t1;
+    st->fuse_cycles[3] += gtime_p<TP>() - t1;
     st->fuse_cycles[13] += tmf[9];   // forward: reserve+check
     st->fuse_cycles[14] += tmf[10] + tmf[11];  // forward: commit (plain + merges)
     st->fuse_cycles[15] += tmf[12];  // forward: compaction
@@ -2388,6 +2398,7 @@ __global__ void __launch_bounds__(256) k_fuse_post(DevMap* maps, const StepArgs*
 }
 
 // reverse passes (fusion.py:337-346), one CTA per map; see the block comment above
+template <bool P>
 __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const StepArgs* args, int smem_bytes, int wide) {
   pdl_enter();
   // one cluster per map: CTA 0 walks the passes; the other CTAs (if any) only help apply the
@@ -2399,7 +2410,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
   if (!A.do_fuse) return;  // (uniform over the cluster)
   const int T = M.s.fctl[FC_T];
   if (T == 0) return;
-  const long long t_entry = gtime();
+  const long long t_entry = gtime_p<P>();
   extern __shared__ __align__(16) unsigned char dyn_rev[];
   TgtView TV = tgt_global(M, A.cur);
   {  // stage the current keyframe (target of every reverse pass) in shared memory
@@ -2506,7 +2517,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     atomicAdd((unsigned long long*)&M.s.stats->dbg[12], 1ull);
   };
   const long long kf_cur = M.kf_id[A.cur];
-  if (threadIdx.x == 0) tm[8] = gtime() - t_entry;  // prologue
+  if (threadIdx.x == 0) tm[8] = gtime_p<P>() - t_entry;  // prologue
   long long alg = 0, npts = 0, nacts = 0, ledger_events = 0;
   int iter = 0, rounds = 0, pass_act = 0, reeval = 0, redo_pts = 0, mergeable = 0, touched_min = 0x7fffffff, fast_passes = 0;
   int t0 = 0;
@@ -2808,7 +2819,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       if (cmd == RC_EXIT) break;
       const int ht1 = rcmd0[1], htag = rcmd0[2], hna = rcmd0[3], hnc = rcmd0[4];
 #ifdef LM_DIAG
-      const long long hd0 = gtime();
+      const long long hd0 = gtime_p<P>();
 #endif
       if (cmd == RC_SETTLE) {
         for (int k = rank * RW + wid; k < hna; k += nranks * RW) settle_item(k, hnc, ht1, htag);
@@ -2825,7 +2836,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
         for (int k = rank * RW + wid; k < hna; k += nranks * RW) add_direct(M.s.acts[k], k, ht1, htag);
       }
 #ifdef LM_DIAG
-      if (lane == 0) atomicMax(&g_diag[60], (unsigned long long)(gtime() - hd0));
+      if (lane == 0) atomicMax(&g_diag[60], (unsigned long long)(gtime_p<P>() - hd0));
 #endif
       cl.sync();  // (B) this helper's actions are applied
     }
@@ -2838,7 +2849,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     //     before it, that pass's actions in keypoint order (from its action bitmap), and the
     //     touched points (action points + current owners of the hit keypoints, deduplicated).
     //     The other warps snapshot the current keyframe's bindings.
-    const long long ta = gtime();
+    const long long ta = gtime_p<P>();
     if (wid == 1) {  // warp 1: the accounting (off warp 0's chain)
       int t1 = T;
       for (int tb = t0; tb < T; tb += 32) {
@@ -2893,7 +2904,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
           const unsigned b0 = lane < AW ? bits[lane] : 0u, b1 = lane + 32 < AW ? bits[lane + 32] : 0u;
           const int c0 = __popc(b0), c1 = __popc(b1);
 #ifdef LM_DIAG
-          if (lane == 0) g_diag[48] += gtime() - ta;
+          if (lane == 0) g_diag[48] += gtime_p<P>() - ta;
 #endif
           int p0 = c0, p1 = c1;
           for (int off = 1; off < 32; off <<= 1) {
@@ -2937,7 +2948,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
             for (unsigned r = b1; r; r &= r - 1) put(at++, seg[32 * (lane + 32) + __ffs(r) - 1]);
           }
 #ifdef LM_DIAG
-          if (lane == 0) g_diag[49] += gtime() - ta;
+          if (lane == 0) g_diag[49] += gtime_p<P>() - ta;
 #endif
         } else for (int wb = 0; wb < AW; wb += 32) {
           const int w = wb + lane;
@@ -3005,14 +3016,14 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
         tag_sh = tg;
       }
 #ifdef LM_DIAG
-      if (lane == 0) g_diag[50] += gtime() - ta;
+      if (lane == 0) g_diag[50] += gtime_p<P>() - ta;
 #endif
     }
     __syncthreads();
 #ifdef LM_DIAG
-    if (threadIdx.x == 0) g_diag[51] += gtime() - ta;
+    if (threadIdx.x == 0) g_diag[51] += gtime_p<P>() - ta;
 #endif
-    if (threadIdx.x == 0) tm[1] += gtime() - ta;
+    if (threadIdx.x == 0) tm[1] += gtime_p<P>() - ta;
     const int t1 = t1_sh;
     if (t1 >= T) break;
     if (pass_act > 0) mergeable += touched_min > t1;
@@ -3044,18 +3055,18 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
         cl.sync();  // (A)
       }
 #ifdef LM_DIAG
-      const long long hd0 = gtime();
+      const long long hd0 = gtime_p<P>();
 #endif
       for (int k = wid; k < na; k += wide_d ? nranks * RW : RW) add_direct(s_acts[k], k, t1, tag);
 #ifdef LM_DIAG
-      if (lane == 0) atomicMax(&g_diag[61], (unsigned long long)(gtime() - hd0));
+      if (lane == 0) atomicMax(&g_diag[61], (unsigned long long)(gtime_p<P>() - hd0));
       if (threadIdx.x == 0) g_diag[52] += hd0 - ta;  // walk + command
 #endif
       if (wide_d) cl.sync();  // (B)
       __syncthreads();
 #ifdef LM_DIAG
       if (threadIdx.x == 0) {
-        g_diag[53] += gtime() - hd0;  // direct apply wall
+        g_diag[53] += gtime_p<P>() - hd0;  // direct apply wall
         g_diag[54] += g_diag[60] > g_diag[61] ? g_diag[60] : g_diag[61];  // slowest add_direct
         g_diag[55] += g_diag[61];
         g_diag[60] = g_diag[61] = 0;
@@ -3067,16 +3078,16 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
         cnt[1] += na;
         ++rounds;
         ++fast_passes;
-        tm[7] += gtime() - ta;
-        tm[2] += gtime() - ta;
+        tm[7] += gtime_p<P>() - ta;
+        tm[2] += gtime_p<P>() - ta;
       }
       redo_pts += ncand;
       if (s_nset) {  // points whose speculated state did not apply: refresh + new hit
-        const long long tv = gtime();
+        const long long tv = gtime_p<P>();
         for (int k = wid; k < na; k += REV_THREADS / 32)
           if (!s_inst[k]) settle_point(s_acts[k].pid);
         __syncthreads();
-        if (threadIdx.x == 0) tm[0] += gtime() - tv;
+        if (threadIdx.x == 0) tm[0] += gtime_p<P>() - tv;
       }
     } else {
       // the touched points' items before the apply (more points than CTA 0 has warps: on the
@@ -3097,13 +3108,13 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       for (int k = threadIdx.x; k < ncur; k += REV_THREADS) M.s.snap[k] = M.kbind[cur_off + k];  // bindings before
       if (wide_p) cl.sync();  // (B)
       __syncthreads();
-      if (threadIdx.x == 0) tm[7] += gtime() - ta;
-      rounds += apply_block<REV_THREADS>(M, M.s.acts, na, cnt, sh, &acc, tm);  // (barriers)
-    if (threadIdx.x == 0) tm[2] += gtime() - ta;
+      if (threadIdx.x == 0) tm[7] += gtime_p<P>() - ta;
+      rounds += apply_block<REV_THREADS, P>(M, M.s.acts, na, cnt, sh, &acc, tm);  // (barriers)
+    if (threadIdx.x == 0) tm[2] += gtime_p<P>() - ta;
     // (2) after the apply: the touched points' items, and the points hitting a current
     //     keypoint whose binding changed (hit list; a keypoint whose list overflowed falls
     //     back to scanning the passes of its bitmap) join the touched list
-    const long long tv = gtime();
+    const long long tv = gtime_p<P>();
     if (wide_p) command_items(1);
     for (int k = wid; k < ncand; k += wide_p ? nranks * RW : RW) {
       const bool later = add_point_items(M.s.cands[k]);
@@ -3113,8 +3124,8 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
       if (M.kbind[cur_off + k] != M.s.snap[k]) M.s.chg[atomicAdd(&nchg_sh, 1)] = k;
     if (wide_p) cl.sync();  // (B)
     __syncthreads();
-    if (threadIdx.x == 0) tm[4] += gtime() - tv;
-    const long long tv2 = gtime();
+    if (threadIdx.x == 0) tm[4] += gtime_p<P>() - tv;
+    const long long tv2 = gtime_p<P>();
     const int nchg = nchg_sh;
     const bool wide_h = nranks > 1 && nchg > RW * wo;
     if (wide_h) {
@@ -3129,8 +3140,8 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     for (int q = wid; q < nchg; q += wide_h ? nranks * RW : RW) hitlist_item(q, t1, tag);
     if (wide_h) cl.sync();  // (B)
     __syncthreads();
-    if (threadIdx.x == 0) tm[5] += gtime() - tv2;
-    const long long tv3 = gtime();
+    if (threadIdx.x == 0) tm[5] += gtime_p<P>() - tv2;
+    const long long tv3 = gtime_p<P>();
     // (3) touched points, warp each: refresh (descriptor + geometry) where stale, then the new
     //     hit (lane 0); the hit-list points' items (their state is unchanged)
     // (a touched point without items in later passes keeps its dirty flag -- the next step's
@@ -3153,12 +3164,12 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     if (wide) cl.sync();  // (B)
     __syncthreads();
     if (threadIdx.x == 0) {
-      tm[0] += gtime() - tv;
-      tm[6] += gtime() - tv3;
+      tm[0] += gtime_p<P>() - tv;
+      tm[6] += gtime_p<P>() - tv3;
     }
     }  // general path
     // (5) re-evaluate the listed items; pass totals by deltas, action bitmaps toggled
-    const long long t7 = gtime();
+    const long long t7 = gtime_p<P>();
     const int ni = ni_sh;
     reeval += ni;
 #ifdef LM_DIAG
@@ -3183,7 +3194,7 @@ __global__ void __launch_bounds__(REV_THREADS, 1) k_fuse_rev(DevMap* maps, const
     __syncthreads();
     if (threadIdx.x == 0) {
       touched_min = tmin_sh;  // (diagnostic, thread 0's only: read here, before the reset below)
-      tm[3] += gtime() - t7;
+      tm[3] += gtime_p<P>() - t7;
       nc_sh = 0;  // counters of the next iteration (read above, before this barrier)
       ni_sh = 0;
       nchg_sh = 0;
