@@ -41,13 +41,20 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "u
         "second": 1}
 
 
+def kname(raw: str) -> str:
+    """Kernel name without namespace, arguments or the timer-free instantiation tag
+    (k_fuse_rev<false> is the kernel every step launches; <true> is the profile pass's)."""
+    n = raw.split("(")[0].replace("lm::", "").replace("void ", "")
+    return n.replace("<false>", "").replace("<true>", " (profile pass)")
+
+
 def full_summary(rep: str) -> dict:
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hdr, units = rows[0], rows[1]
     per = collections.defaultdict(list)
     for r in rows[2:]:
-        name = r[hdr.index("Kernel Name")].split("(")[0].replace("lm::", "")
+        name = kname(r[hdr.index("Kernel Name")])
         d = {}
         for m, key in METRICS.items():
             if m in hdr:
@@ -76,7 +83,7 @@ def launch_shares(path: str) -> list[tuple[str, int, float, float]]:
     for r in rows[hi + 1:]:
         if len(r) <= vi:
             continue
-        agg[r[ki].split("(")[0].replace("lm::", "")].append(float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1e-9))
+        agg[kname(r[ki])].append(float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1e-9))
     tot = sum(sum(v) for v in agg.values())
     return sorted(((k, len(v), sum(v) / len(v), sum(v) / tot) for k, v in agg.items()), key=lambda t: -t[3])
 
