@@ -45,7 +45,11 @@ def kname(raw: str) -> str:
     """Kernel name without namespace, arguments or the timer-free instantiation tag
     (k_fuse_rev<false> is the kernel every step launches; <true> is the profile pass's)."""
     n = raw.split("(")[0].replace("lm::", "").replace("void ", "")
-    return n.replace("<false>", "").replace("<true>", " (profile pass)")
+    for k in ("k_fuse_rev", "k_fuse_apply", "k_cull"):  # template <bool P>: phase timers
+        for tag, lab in (("<false>", ""), ("<0>", ""), ("<true>", " (profile pass)"), ("<1>", " (profile pass)")):
+            if n == k + tag:
+                return k + lab
+    return n
 
 
 def full_summary(rep: str) -> dict:
