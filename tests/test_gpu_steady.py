@@ -105,6 +105,28 @@ def test_steady_state_matches_reference_every_keyframe(name):
           f"borderline compares (epi, gates, fusion, rint) {border.tolist()}")
 
 
+def test_streaming_async_c2_matches_reference_final_state():
+    """The streaming path bench.py's e2e times: keyframe k+1 staged (on the staging stream)
+    while step k runs, every step asynchronous, nothing read back until the end. Running
+    counters, the structural digest and the positions after the last keyframe equal the
+    reference's (a half-staged keyframe seen by any step would change them)."""
+    g, pos = load("c2")
+    seq = seq_of(g)
+    intr = seq.intrinsics()
+    dev = mapper_for(g, seq)
+    recs = seq.records[:g["keyframes"]]
+    for rec in recs:
+        dev.stage(device_kf(rec, intr))
+        dev.step(int(rec.kf_id), sync=False)
+    tot = dev.totals()
+    want = g["steps"][len(recs) - 1]
+    assert (tot.created, tot.conflicts, tot.degenerate) == (want["created"], want["conflicts"], want["degenerate"])
+    assert {"merged": tot.merged, "observations_added": tot.observations_added, "stale": tot.stale} == want["fusion"]
+    assert tot.culled == want["culled"]
+    assert dev.snapshot(with_covis=False).structural_digest() == want["digest"]
+    check_positions(dev, pos)
+
+
 def test_c5_sessions_batched_match_reference_every_keyframe():
     names = [n for n in GOLD if n.startswith("c5_")]
     if not names:
