@@ -767,6 +767,8 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
   CU(cudaFuncSetAttribute(k_fuse_rev<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CU(cudaFuncSetAttribute(k_fuse_rev<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CU(cudaFuncSetAttribute(k_cull<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, CULL_DYN_SMEM));
+  CU(cudaFuncSetAttribute(k_cull<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CU(cudaFuncSetAttribute(k_cull<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CU(cudaFuncSetAttribute(k_cull<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CULL_DYN_SMEM));
   CU(cudaFuncSetAttribute(k_tri, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
   if (const char* e = getenv("LM_CARVEOUT")) {  // (experiments) shared-memory carve-out hint, percent
@@ -791,7 +793,7 @@ int lm_ctx_create(int32_t device, lm_ctx** out) {
   if (const char* e = getenv("LM_TRI_SLICES")) ctx->tri_slices = atoi(e) > 0 ? (atoi(e) < 32 ? atoi(e) : 32) : 1;
   if (const char* e = getenv("LM_CULL_CLUSTER")) {
     const int v = atoi(e);
-    ctx->cull_cluster = v < 1 ? 1 : (v > 8 ? 8 : v);
+    ctx->cull_cluster = v < 1 ? 1 : (v > 16 ? 16 : v);
   }
   if (const char* e = getenv("LM_APPLY_CLUSTER")) {
     const int v = atoi(e);
